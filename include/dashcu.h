@@ -1,0 +1,188 @@
+/*
+ * dashcu.h — the C ABI of the B200-native DASH training step (libdashcu.so).
+ *
+ * This is the drop-in boundary for the DASH hot path of arXiv 2505.17218
+ * (SURVEY.md §8b). Every entry point names the reference interface it
+ * replaces (paths under /root/reference/proj unless marked SPEC.md):
+ *
+ *   dashcu_policy_*          ParamTensors / PolicyParams      include/dash/tensors.hpp:13-82
+ *   dashcu_sample            preemptive_sample
+ *                            (batched dash::sample)           src/policy.cpp:379-429
+ *   dashcu_rollout_log_prob  dash::log_prob                   src/policy.cpp:362-377
+ *   dashcu_advantage_filter  group_advantage / normalize_std  src/advantage.cpp:80-133
+ *                            filter_by_threshold              src/advantage.cpp:135-140
+ *   dashcu_accumulate        pg_gradient + run_schedule(DASH) SPEC.md:284-292, :320-323
+ *                            (sum of A_n * grad_log_prob      src/policy.cpp:463-485,
+ *                             via add_scaled)                 src/tensors.cpp:109-115)
+ *   dashcu_allreduce_grads   map-reduce over trajectories
+ *   dashcu_optimizer_step    optimizer_step
+ *
+ * Conventions
+ *  - Plain C types only; the caller owns every host buffer passed in, handles
+ *    own all device memory. No device pointer escapes.
+ *  - Status codes mirror include/dash/errors.hpp:10-23:
+ *      0 ok, 1 InputError, 2 CapacityError, 3 OnPolicyViolation, 4 device (CUDA/NCCL).
+ *    Validation happens on the host before any launch, so the error class
+ *    matches the reference's throw sites (policy.cpp:183-197, :381-386;
+ *    advantage.cpp:10-41, :136). dashcu_last_error() is thread-local.
+ *  - Flat parameter / gradient buffers are fp64 in ParamTensors::views()
+ *    order (tensors.cpp:49-71), extended with the GQA geometry below.
+ *  - One dashcu_ctx per GPU, used from one host thread; calls are
+ *    stream-ordered and return once their host outputs are written.
+ *  - There is no CPU fallback: without an sm_100 device every entry point
+ *    that computes returns 4.
+ */
+#ifndef DASHCU_H
+#define DASHCU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DASHCU_API __attribute__((visibility("default")))
+#else
+#define DASHCU_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DASHCU_OK 0
+#define DASHCU_E_INPUT 1
+#define DASHCU_E_CAPACITY 2
+#define DASHCU_E_ON_POLICY 3
+#define DASHCU_E_DEVICE 4
+
+/* compute dtype of a policy */
+#define DASHCU_F32 0  /* parity mode: fp32 weights/activations, CUDA-core GEMMs */
+#define DASHCU_BF16 1 /* production: bf16 operands, tcgen05 GEMMs, fp32 master/grads */
+
+/* advantage estimators (advantage.hpp:36-45) */
+#define DASHCU_ADV_SINGLE_PATH 0 /* single_path_advantage  advantage.cpp:67-78 */
+#define DASHCU_ADV_GROUP 1       /* group_advantage        advantage.cpp:80-94 */
+#define DASHCU_ADV_LEAVE_ONE_OUT 2 /* leave_one_out        advantage.cpp:96-112 */
+
+/* optimizers */
+#define DASHCU_OPT_SGD 0
+#define DASHCU_OPT_ADAM 1
+
+typedef struct dashcu_ctx dashcu_ctx;
+typedef struct dashcu_policy dashcu_policy;
+
+/* ArchConfig (tensors.hpp:13-24) + GQA geometry extension (SURVEY App.B D1).
+ * n_heads = n_kv_heads = head_dim = 0 means (1, 1, embed_dim): the reference. */
+typedef struct {
+  int32_t vocab_size, embed_dim, context_len, ffn_hidden, n_layers, bos_id, eos_id;
+  int32_t n_heads, n_kv_heads, head_dim;
+} dashcu_arch;
+
+/* SamplingPlan. Prompt m of this call is the global prompt
+ * prompt_index_base + m, so per-request keys derive_seed(round_seed, "sample",
+ * m_global, g) are independent of how prompts are sharded. */
+typedef struct {
+  int32_t n_prompts, group_size, max_len;
+  double temperature;
+  uint64_t round_seed;
+  int64_t prompt_index_base;
+} dashcu_plan;
+
+typedef struct {
+  int32_t kind; /* DASHCU_OPT_* */
+  double lr, beta1, beta2, eps;
+} dashcu_opt;
+
+typedef struct {
+  double sample_ms, advantage_ms, accumulate_ms, allreduce_ms, optimizer_ms;
+  int64_t tokens_sampled;   /* completion tokens of the last dashcu_sample */
+  int32_t n_seq, n_kept;    /* rollout size, kept after the filter */
+  int64_t loss_tokens;      /* completion tokens that entered the last accumulate */
+  double mean_reward, filtered_fraction, mean_abs_kept; /* advantage.cpp:44-65 */
+  int64_t kernel_launches;  /* kernels this policy launched since creation */
+} dashcu_stats;
+
+DASHCU_API const char* dashcu_last_error(void);
+DASHCU_API int dashcu_abi_version(void);
+
+/* ---- context (one per GPU) ---- */
+DASHCU_API int dashcu_ctx_create(int device, dashcu_ctx** out);
+DASHCU_API int dashcu_ctx_destroy(dashcu_ctx* ctx);
+DASHCU_API int dashcu_ctx_sync(dashcu_ctx* ctx);
+/* NCCL communicator for the gradient allreduce (one per optimizer step). */
+DASHCU_API int dashcu_comm_unique_id(uint8_t out[128]);
+DASHCU_API int dashcu_ctx_init_comm(dashcu_ctx* ctx, int world, int rank, const uint8_t id[128]);
+
+/* ---- policy parameters (tensors.hpp:50-82) ---- */
+DASHCU_API int dashcu_arch_num_params(const dashcu_arch* arch, int64_t* n);
+DASHCU_API int dashcu_policy_create(dashcu_ctx* ctx, const dashcu_arch* arch, int dtype, dashcu_policy** out);
+DASHCU_API int dashcu_policy_destroy(dashcu_policy* pol);
+/* PolicyParams <-> device, fp64 flat views() order. Upload bumps the snapshot version. */
+DASHCU_API int dashcu_policy_upload(dashcu_policy* pol, const double* params, int64_t n);
+DASHCU_API int dashcu_policy_download(dashcu_policy* pol, double* params, int64_t n);
+/* Device counter-based N(0, scale^2) init for shapes where a
+ * host PolicyParams::init is impractical; restated in oracle/. */
+DASHCU_API int dashcu_policy_init_normal(dashcu_policy* pol, double scale, uint64_t seed);
+DASHCU_API int dashcu_policy_version(dashcu_policy* pol, uint64_t* version);
+
+/* ---- preemptive sampling (policy.cpp:379-429) ----
+ * Samples group_size completions for each prompt (prompt_offsets[n_prompts+1]
+ * into prompt_tokens). Sequence s = m*G + g. Outputs (each may be NULL):
+ *   completions [n_seq*max_len] (row s: tokens, unused tail = -1)
+ *   lengths     [n_seq]
+ *   logp        [n_seq*max_len]  per-token log-probs at T=1 (trajectory.hpp:8-9)
+ * Sampling rule: Gumbel-max over fp32 logits with the counter RNG of
+ * DESIGN.md §4 (the reference inverse-CDF+mt19937 rule cannot be replayed on
+ * a GPU; SURVEY App.B D2). The rollout stays resident for accumulate. */
+DASHCU_API int dashcu_sample(dashcu_policy* pol, const dashcu_plan* plan, const int32_t* prompt_tokens,
+                  const int64_t* prompt_offsets, int32_t* completions, int32_t* lengths, float* logp);
+/* Debug: when enabled, the next dashcu_sample also records the exact fp32
+ * logits its sampling rule consumed, [n_seq][max_len][vocab] (small shapes). */
+DASHCU_API int dashcu_set_logits_dump(dashcu_policy* pol, int enable);
+DASHCU_API int dashcu_get_logits_dump(dashcu_policy* pol, float* out, int64_t n);
+
+/* Load externally produced trajectories as the rollout (n_prompts*group_size
+ * sequences; completion s = completions[completion_offsets[s] .. [s+1])).
+ * Validates like validate_traj (policy.cpp:191-197). */
+DASHCU_API int dashcu_rollout_load(dashcu_policy* pol, const int32_t* prompt_tokens, const int64_t* prompt_offsets,
+                        int32_t n_prompts, int32_t group_size, const int32_t* completions,
+                        const int64_t* completion_offsets);
+/* Teacher-forced per-token log-probs of the rollout (log_prob, policy.cpp:362-377),
+ * concatenated over sequences in rollout order (n_tokens = sum of lengths). */
+DASHCU_API int dashcu_rollout_log_prob(dashcu_policy* pol, float* per_token, int64_t n_tokens);
+
+/* ---- advantage + gradient filter ----
+ * Host-buffer form (advantage.cpp:80-140): adv[n], kept[n], kept_idx = ascending
+ * compaction of kept, n_kept. kind = DASHCU_ADV_*; normalize = normalize_std. */
+DASHCU_API int dashcu_advantage_filter(dashcu_ctx* ctx, const double* rewards, int32_t n, int32_t group_size,
+                            int32_t kind, int32_t normalize, double eps, double tau, double* adv,
+                            uint8_t* kept, int32_t* kept_idx, int32_t* n_kept);
+/* Device-resident form on the current rollout: rewards in, advantages and the
+ * compacted kept list stay on device for dashcu_accumulate. Outputs may be NULL. */
+DASHCU_API int dashcu_rollout_set_rewards(dashcu_policy* pol, const double* rewards, int32_t n);
+DASHCU_API int dashcu_rollout_advantage(dashcu_policy* pol, int32_t kind, int32_t normalize, double eps, double tau,
+                             double* adv, uint8_t* kept, int32_t* n_kept);
+
+/* ---- micro-batched policy-gradient accumulation ----
+ * grad += sum over kept n of (A_n * weight_scale) * grad log pi(traj_n), in
+ * micro-batches of micro_batch sequences (0 = all at once). DASH uses
+ * weight_scale = 1/N with N the round's pre-filter count (App.B D4).
+ * Raises OnPolicyViolation if the policy changed since the rollout was made. */
+DASHCU_API int dashcu_grad_zero(dashcu_policy* pol);
+DASHCU_API int dashcu_accumulate(dashcu_policy* pol, double weight_scale, int32_t micro_batch);
+/* Same with explicit per-sequence weights (weights[n_seq], all sequences). */
+DASHCU_API int dashcu_accumulate_weighted(dashcu_policy* pol, const double* weights, int32_t n_seq,
+                               int32_t micro_batch);
+DASHCU_API int dashcu_grad_download(dashcu_policy* pol, double* grad, int64_t n);
+/* Sum gradients over the ranks of the context's communicator (no-op at world 1). */
+DASHCU_API int dashcu_allreduce_grads(dashcu_policy* pol);
+/* Ascent step on the fp32 master weights; refreshes the bf16 copy; bumps the version. */
+DASHCU_API int dashcu_optimizer_step(dashcu_policy* pol, const dashcu_opt* opt);
+
+DASHCU_API int dashcu_get_stats(dashcu_policy* pol, dashcu_stats* out);
+/* Whole-library count of kernel launches (all policies, all contexts). */
+DASHCU_API int64_t dashcu_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DASHCU_H */

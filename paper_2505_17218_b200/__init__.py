@@ -1,0 +1,348 @@
+"""B200-native DASH training step (arXiv 2505.17218) — Python binding of libdashcu.
+
+The product is the C ABI in include/dashcu.h (libdashcu.so, CUDA sm_100a). This
+module is a thin ctypes mirror of it for Python callers (tests, bench.py). It
+has no compute of its own and no CPU fallback: if the shared library is missing
+or no B200 is visible, every compute call raises.
+
+Names follow the reference's domain (SPEC.md / proj/include/dash): policies,
+rollouts, groups, advantages, kept sets.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "lib", "libdashcu.so")
+
+OK, E_INPUT, E_CAPACITY, E_ON_POLICY, E_DEVICE = 0, 1, 2, 3, 4
+F32, BF16 = 0, 1
+ADV_SINGLE_PATH, ADV_GROUP, ADV_LEAVE_ONE_OUT = 0, 1, 2
+OPT_SGD, OPT_ADAM = 0, 1
+
+
+class DashError(RuntimeError):
+    code = E_DEVICE
+
+
+class InputError(DashError, ValueError):          # errors.hpp:12-14
+    code = E_INPUT
+
+
+class CapacityError(DashError):                    # errors.hpp:17-19
+    code = E_CAPACITY
+
+
+class OnPolicyViolation(DashError):                # errors.hpp:21-23
+    code = E_ON_POLICY
+
+
+class DeviceError(DashError):
+    code = E_DEVICE
+
+
+_ERR = {E_INPUT: InputError, E_CAPACITY: CapacityError, E_ON_POLICY: OnPolicyViolation, E_DEVICE: DeviceError}
+
+
+class Arch(C.Structure):
+    """ArchConfig (tensors.hpp:13-24) + GQA geometry; zeros mean the reference (1, 1, d)."""
+    _fields_ = [(n, C.c_int32) for n in ("vocab_size", "embed_dim", "context_len", "ffn_hidden", "n_layers",
+                                         "bos_id", "eos_id", "n_heads", "n_kv_heads", "head_dim")]
+
+    @classmethod
+    def of(cls, d: dict) -> "Arch":
+        return cls(*(int(d.get(f, 0)) for f, _ in cls._fields_))
+
+
+class Plan(C.Structure):
+    """SamplingPlan."""
+    _fields_ = [("n_prompts", C.c_int32), ("group_size", C.c_int32), ("max_len", C.c_int32),
+                ("temperature", C.c_double), ("round_seed", C.c_uint64), ("prompt_index_base", C.c_int64)]
+
+
+class Opt(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
+                ("eps", C.c_double)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("sample_ms", C.c_double), ("advantage_ms", C.c_double), ("accumulate_ms", C.c_double),
+                ("allreduce_ms", C.c_double), ("optimizer_ms", C.c_double), ("tokens_sampled", C.c_int64),
+                ("n_seq", C.c_int32), ("n_kept", C.c_int32), ("loss_tokens", C.c_int64),
+                ("mean_reward", C.c_double), ("filtered_fraction", C.c_double), ("mean_abs_kept", C.c_double),
+                ("kernel_launches", C.c_int64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+
+i32p = C.POINTER(C.c_int32)
+i64p = C.POINTER(C.c_int64)
+f64p = C.POINTER(C.c_double)
+f32p = C.POINTER(C.c_float)
+u8p = C.POINTER(C.c_uint8)
+vp = C.c_void_p
+
+
+def lib():
+    """Load libdashcu.so (fails loudly if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DeviceError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        L.dashcu_last_error.restype = C.c_char_p
+        L.dashcu_kernel_launches.restype = C.c_int64
+        sig = {
+            "dashcu_ctx_create": [C.c_int, C.POINTER(vp)],
+            "dashcu_ctx_destroy": [vp],
+            "dashcu_ctx_sync": [vp],
+            "dashcu_comm_unique_id": [C.c_char_p],
+            "dashcu_ctx_init_comm": [vp, C.c_int, C.c_int, C.c_char_p],
+            "dashcu_arch_num_params": [C.POINTER(Arch), i64p],
+            "dashcu_policy_create": [vp, C.POINTER(Arch), C.c_int, C.POINTER(vp)],
+            "dashcu_policy_destroy": [vp],
+            "dashcu_policy_upload": [vp, f64p, C.c_int64],
+            "dashcu_policy_download": [vp, f64p, C.c_int64],
+            "dashcu_policy_init_normal": [vp, C.c_double, C.c_uint64],
+            "dashcu_policy_version": [vp, C.POINTER(C.c_uint64)],
+            "dashcu_sample": [vp, C.POINTER(Plan), i32p, i64p, i32p, i32p, f32p],
+            "dashcu_set_logits_dump": [vp, C.c_int],
+            "dashcu_get_logits_dump": [vp, f32p, C.c_int64],
+            "dashcu_rollout_load": [vp, i32p, i64p, C.c_int32, C.c_int32, i32p, i64p],
+            "dashcu_rollout_log_prob": [vp, f32p, C.c_int64],
+            "dashcu_advantage_filter": [vp, f64p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                        f64p, u8p, i32p, i32p],
+            "dashcu_rollout_set_rewards": [vp, f64p, C.c_int32],
+            "dashcu_rollout_advantage": [vp, C.c_int32, C.c_int32, C.c_double, C.c_double, f64p, u8p, i32p],
+            "dashcu_grad_zero": [vp],
+            "dashcu_accumulate": [vp, C.c_double, C.c_int32],
+            "dashcu_accumulate_weighted": [vp, f64p, C.c_int32, C.c_int32],
+            "dashcu_grad_download": [vp, f64p, C.c_int64],
+            "dashcu_allreduce_grads": [vp],
+            "dashcu_optimizer_step": [vp, C.POINTER(Opt)],
+            "dashcu_get_stats": [vp, C.POINTER(Stats)],
+        }
+        for name, args in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != OK:
+        msg = lib().dashcu_last_error().decode(errors="replace")
+        raise _ERR.get(rc, DeviceError)(msg)
+
+
+def _p(a: np.ndarray, t):
+    return a.ctypes.data_as(t) if a is not None else None
+
+
+def kernel_launches() -> int:
+    return int(lib().dashcu_kernel_launches())
+
+
+def num_params(arch: dict) -> int:
+    n = C.c_int64(0)
+    a = Arch.of(arch)
+    _check(lib().dashcu_arch_num_params(C.byref(a), C.byref(n)))
+    return int(n.value)
+
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().dashcu_comm_unique_id(buf))
+    return buf.raw
+
+
+class Context:
+    """One per GPU (dashcu_ctx): device, stream and the gradient communicator."""
+
+    def __init__(self, device: int = 0):
+        self.h = vp()
+        _check(lib().dashcu_ctx_create(device, C.byref(self.h)))
+
+    def init_comm(self, world: int, rank: int, uid: bytes):
+        _check(lib().dashcu_ctx_init_comm(self.h, world, rank, uid))
+
+    def sync(self):
+        _check(lib().dashcu_ctx_sync(self.h))
+
+    def advantage_filter(self, rewards, group_size, kind=ADV_GROUP, normalize=False, eps=0.0, tau=0.0):
+        """group_advantage / normalize_std / filter_by_threshold (advantage.cpp:80-140) on the device."""
+        r = np.ascontiguousarray(rewards, dtype=np.float64)
+        n = int(r.shape[0])
+        adv = np.zeros(max(n, 1))
+        kept = np.zeros(max(n, 1), dtype=np.uint8)
+        idx = np.zeros(max(n, 1), dtype=np.int32)
+        nk = C.c_int32(0)
+        _check(lib().dashcu_advantage_filter(self.h, _p(r, f64p), n, group_size, kind, int(normalize), eps, tau,
+                                             _p(adv, f64p), _p(kept, u8p), _p(idx, i32p), C.byref(nk)))
+        return adv[:n], kept[:n].astype(bool), idx[:nk.value].copy()
+
+    def close(self):
+        if self.h:
+            lib().dashcu_ctx_destroy(self.h)
+            self.h = vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class Rollout:
+    completions: np.ndarray  # [n_seq, max_len], -1 padded
+    lengths: np.ndarray      # [n_seq]
+    logp: np.ndarray         # [n_seq, max_len] (T = 1)
+
+    def completion(self, s: int) -> np.ndarray:
+        return self.completions[s, :self.lengths[s]]
+
+
+def pack_prompts(prompts):
+    toks = np.ascontiguousarray(np.concatenate([np.asarray(p, dtype=np.int32) for p in prompts]), dtype=np.int32)
+    off = np.zeros(len(prompts) + 1, dtype=np.int64)
+    off[1:] = np.cumsum([len(p) for p in prompts])
+    return toks, off
+
+
+class Policy:
+    """Device-resident policy (dashcu_policy): fp32 master weights + gradient + Adam state,
+    a bf16 (or fp32) working copy, and the current rollout."""
+
+    def __init__(self, ctx: Context, arch: dict, dtype: int = BF16):
+        self.ctx = ctx
+        self.arch = dict(arch)
+        self.dtype = dtype
+        self.h = vp()
+        a = Arch.of(arch)
+        _check(lib().dashcu_policy_create(ctx.h, C.byref(a), dtype, C.byref(self.h)))
+        self.n_params = num_params(arch)
+
+    # ---- parameters
+    def upload(self, params: np.ndarray):
+        p = np.ascontiguousarray(params, dtype=np.float64)
+        _check(lib().dashcu_policy_upload(self.h, _p(p, f64p), p.shape[0]))
+
+    def download(self) -> np.ndarray:
+        out = np.zeros(self.n_params)
+        _check(lib().dashcu_policy_download(self.h, _p(out, f64p), self.n_params))
+        return out
+
+    def init_normal(self, scale: float, seed: int):
+        _check(lib().dashcu_policy_init_normal(self.h, scale, seed))
+
+    def version(self) -> int:
+        v = C.c_uint64(0)
+        _check(lib().dashcu_policy_version(self.h, C.byref(v)))
+        return int(v.value)
+
+    # ---- sampling
+    def set_logits_dump(self, enable: bool):
+        _check(lib().dashcu_set_logits_dump(self.h, int(enable)))
+
+    def logits_dump(self, n_seq: int, max_len: int) -> np.ndarray:
+        V = self.arch["vocab_size"]
+        out = np.zeros(n_seq * max(max_len, 1) * V, dtype=np.float32)
+        _check(lib().dashcu_get_logits_dump(self.h, _p(out, f32p), out.shape[0]))
+        return out.reshape(n_seq, max(max_len, 1), V)
+
+    def sample(self, prompts, group_size, max_len, temperature=1.0, round_seed=0, prompt_index_base=0,
+               prompt_tokens=None, prompt_offsets=None, outputs=None) -> Rollout:
+        """preemptive_sample. outputs=(comp, lens, logp) reuses caller buffers."""
+        if prompt_tokens is None:
+            prompt_tokens, prompt_offsets = pack_prompts(prompts)
+        n_prompts = len(prompt_offsets) - 1
+        S = n_prompts * group_size
+        if outputs is None:
+            comp = np.zeros((S, max(max_len, 1)), dtype=np.int32)
+            lens = np.zeros(S, dtype=np.int32)
+            logp = np.zeros((S, max(max_len, 1)), dtype=np.float32)
+        else:
+            comp, lens, logp = outputs
+        plan = Plan(n_prompts, group_size, max_len, float(temperature), int(round_seed) & (2**64 - 1),
+                    int(prompt_index_base))
+        _check(lib().dashcu_sample(self.h, C.byref(plan), _p(prompt_tokens, i32p), _p(prompt_offsets, i64p),
+                                   _p(comp, i32p), _p(lens, i32p), _p(logp, f32p)))
+        return Rollout(comp, lens, logp)
+
+    def load_rollout(self, prompts, group_size, completions):
+        pt, po = pack_prompts(prompts)
+        ct = np.ascontiguousarray(np.concatenate([np.asarray(c, dtype=np.int32) for c in completions] +
+                                                 [np.zeros(0, dtype=np.int32)]), dtype=np.int32)
+        co = np.zeros(len(completions) + 1, dtype=np.int64)
+        co[1:] = np.cumsum([len(c) for c in completions])
+        if ct.shape[0] == 0:
+            ct = np.zeros(1, dtype=np.int32)
+        _check(lib().dashcu_rollout_load(self.h, _p(pt, i32p), _p(po, i64p), len(prompts), group_size, _p(ct, i32p),
+                                         _p(co, i64p)))
+
+    def rollout_log_prob(self, n_tokens: int) -> np.ndarray:
+        out = np.zeros(max(n_tokens, 1), dtype=np.float32)
+        _check(lib().dashcu_rollout_log_prob(self.h, _p(out, f32p), n_tokens))
+        return out[:n_tokens]
+
+    # ---- advantage / filter
+    def set_rewards(self, rewards):
+        r = np.ascontiguousarray(rewards, dtype=np.float64)
+        _check(lib().dashcu_rollout_set_rewards(self.h, _p(r, f64p), r.shape[0]))
+
+    def advantage(self, kind=ADV_GROUP, normalize=False, eps=0.0, tau=0.1):
+        n = self.stats()["n_seq"]
+        adv = np.zeros(max(n, 1))
+        kept = np.zeros(max(n, 1), dtype=np.uint8)
+        nk = C.c_int32(0)
+        _check(lib().dashcu_rollout_advantage(self.h, kind, int(normalize), eps, tau, _p(adv, f64p), _p(kept, u8p),
+                                              C.byref(nk)))
+        return adv[:n], kept[:n].astype(bool), int(nk.value)
+
+    # ---- gradient / update
+    def grad_zero(self):
+        _check(lib().dashcu_grad_zero(self.h))
+
+    def accumulate(self, weight_scale: float, micro_batch: int = 32):
+        _check(lib().dashcu_accumulate(self.h, weight_scale, micro_batch))
+
+    def accumulate_weighted(self, weights, micro_batch: int = 32):
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        _check(lib().dashcu_accumulate_weighted(self.h, _p(w, f64p), w.shape[0], micro_batch))
+
+    def grad(self) -> np.ndarray:
+        out = np.zeros(self.n_params)
+        _check(lib().dashcu_grad_download(self.h, _p(out, f64p), self.n_params))
+        return out
+
+    def allreduce_grads(self):
+        _check(lib().dashcu_allreduce_grads(self.h))
+
+    def optimizer_step(self, kind=OPT_ADAM, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8):
+        o = Opt(kind, lr, beta1, beta2, eps)
+        _check(lib().dashcu_optimizer_step(self.h, C.byref(o)))
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(lib().dashcu_get_stats(self.h, C.byref(s)))
+        return s.as_dict()
+
+    def close(self):
+        if self.h:
+            lib().dashcu_policy_destroy(self.h)
+            self.h = vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,80 @@
+// Shared device/host helpers for libdashcu (sm_100a only).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace dashcu {
+
+// Status-carrying exception used inside the library; converted to a status
+// code at the C-ABI boundary (api.cu). Codes follow include/dashcu.h.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  throw Error(4, std::string("CUDA error ") + cudaGetErrorString(e) + " at " + what + " (" + file + ":" +
+                     std::to_string(line) + ")");
+}
+
+#define DCU_CHECK(x)                                          \
+  do {                                                        \
+    cudaError_t e__ = (x);                                    \
+    if (e__ != cudaSuccess) throw_cuda(e__, #x, __FILE__, __LINE__); \
+  } while (0)
+
+// Every kernel launch in the library goes through this counter so the bench
+// can report how many of OUR kernels ran (gpu_launches).
+extern int64_t g_launches;
+#define DCU_LAUNCHED() \
+  do {                 \
+    ++::dashcu::g_launches; \
+    DCU_CHECK(cudaGetLastError()); \
+  } while (0)
+
+typedef __nv_bfloat16 bf16;
+
+template <class T>
+struct Cvt;
+template <>
+struct Cvt<float> {
+  static __device__ __forceinline__ float to_f(float x) { return x; }
+  static __device__ __forceinline__ float from_f(float x) { return x; }
+};
+template <>
+struct Cvt<bf16> {
+  static __device__ __forceinline__ float to_f(bf16 x) { return __bfloat162float(x); }
+  static __device__ __forceinline__ bf16 from_f(float x) { return __float2bfloat16_rn(x); }
+};
+
+template <class T>
+__device__ __forceinline__ float tof(T x) { return Cvt<T>::to_f(x); }
+template <class T>
+__device__ __forceinline__ T fromf(float x) { return Cvt<T>::from_f(x); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+inline int cdiv(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+constexpr int kNumSMs = 148;
+
+}  // namespace dashcu

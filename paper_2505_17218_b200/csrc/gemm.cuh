@@ -1,0 +1,73 @@
+// GEMM interface shared by the CUDA-core (parity) and tcgen05 (production) kernels.
+//
+//   C[M x N] = epilogue( alpha * sum_k A(m, k) * B(n, k) )
+//
+// A(m, k) = a_kmajor ? A[m*lda + k] : A[k*lda + m]
+// B(n, k) = b_kmajor ? B[n*ldb + k] : B[k*ldb + n]
+//
+// Forward projections are (K, K) (x @ W^T with W row-major [out x in], the
+// reference's y = W x, policy.cpp:21-28); input gradients are (K, MN)
+// (dX = dY @ W); weight gradients are (MN, MN) (dW += dY^T @ X), accumulated
+// in place into the fp32 gradient (the reference's add_scaled, tensors.cpp:109).
+#pragma once
+#include "common.cuh"
+
+namespace dashcu {
+
+enum EpiKind : int {
+  EPI_STORE = 0,  // out = v (+bias) (+resid)
+  EPI_TANH = 1,   // out = tanh(v + bias)                       policy.cpp:137
+  EPI_DTANH = 2,  // out = v * (1 - aux^2)                      policy.cpp:261
+  EPI_ACCUM = 3,  // c32 += v                                   wgrad, beta = 1
+};
+
+struct Epi {
+  int kind = EPI_STORE;
+  float alpha = 1.f;
+  const float* bias = nullptr;   // [N]
+  const float* resid = nullptr;  // fp32 [M x ldr]
+  int64_t ldr = 0;
+  const void* aux = nullptr;     // T [M x ld_aux] (EPI_DTANH)
+  int64_t ld_aux = 0;
+  float* c32 = nullptr;          // fp32 output / accumulator
+  int64_t ldc32 = 0;
+  void* cT = nullptr;            // T output (operand copy for the next GEMM)
+  int64_t ldcT = 0;
+};
+
+struct GemmShape {
+  int M, N, K;
+  const void* A;
+  int64_t lda;
+  bool a_kmajor;
+  const void* B;
+  int64_t ldb;
+  bool b_kmajor;
+};
+
+// dtype: 0 fp32 (CUDA cores), 1 bf16 (tcgen05 when the operands are TMA-legal)
+void gemm(cudaStream_t s, int dtype, const GemmShape& g, const Epi& e);
+template <class T>
+void gemm_simt(cudaStream_t s, const GemmShape& g, const Epi& e);
+// tcgen05 path; returns false if the shape is not TMA-legal (strides must be 16-byte multiples).
+bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e);
+
+template <class T>
+__device__ __forceinline__ void epi_apply(const Epi& e, int m, int n, float acc) {
+  float v = e.alpha * acc;
+  if (e.bias) v += e.bias[n];
+  if (e.kind == EPI_TANH) v = tanhf(v);
+  if (e.kind == EPI_DTANH) {
+    const float a = tof<T>(static_cast<const T*>(e.aux)[static_cast<int64_t>(m) * e.ld_aux + n]);
+    v *= (1.f - a * a);
+  }
+  if (e.resid) v += e.resid[static_cast<int64_t>(m) * e.ldr + n];
+  if (e.kind == EPI_ACCUM) {
+    e.c32[static_cast<int64_t>(m) * e.ldc32 + n] += v;
+    return;
+  }
+  if (e.c32) e.c32[static_cast<int64_t>(m) * e.ldc32 + n] = v;
+  if (e.cT) static_cast<T*>(e.cT)[static_cast<int64_t>(m) * e.ldcT + n] = fromf<T>(v);
+}
+
+}  // namespace dashcu

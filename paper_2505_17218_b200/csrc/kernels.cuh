@@ -1,0 +1,79 @@
+// Declarations of the non-GEMM kernels (launch wrappers). Each wrapper names
+// the reference computation it replaces.
+#pragma once
+#include "common.cuh"
+
+namespace dashcu {
+
+// ---- parameters / optimizer -------------------------------------------------
+void init_normal_ctr(cudaStream_t s, float* w, int64_t n, double scale, uint64_t seed);
+void f64_to_f32(cudaStream_t s, const double* in, float* out, int64_t n);
+void f32_to_f64(cudaStream_t s, const float* in, double* out, int64_t n);
+void cast_f32_bf16(cudaStream_t s, const float* in, bf16* out, int64_t n);
+void fill_f32(cudaStream_t s, float* p, float v, int64_t n);
+// SPEC.md:329-337 (ascent). kind 0 SGD, 1 Adam. Writes the bf16 working copy if wT != null.
+void optimizer_update(cudaStream_t s, int kind, float* w, const float* g, float* m, float* v, bf16* wT,
+                      int64_t n, float lr, float b1, float b2, float eps, float c1, float c2);
+
+// ---- embeddings (policy.cpp:87-92, backward :335-344) --------------------------
+template <class T>
+void embed_fwd(cudaStream_t s, const T* tok_emb, const T* pos_emb, const int32_t* tok, const int32_t* pos,
+               int rows, int d, float* x32, T* xT);
+// decode: pos = prompt_len[s] + step - 1, token = tok[s]
+template <class T>
+void embed_decode(cudaStream_t s, const T* tok_emb, const T* pos_emb, const int32_t* tok,
+                  const int32_t* prompt_len, int step, int rows, int d, float* x32, T* xT);
+void embed_bwd(cudaStream_t s, const float* dx, const int32_t* tok, const int32_t* pos, int rows, int d,
+               float* g_tok, float* g_pos);
+// out[n] += sum_m X[m][n]  (bias gradients: db_out, db1, db2)
+template <class T>
+void colsum_acc(cudaStream_t s, const T* X, int64_t ld, int M, int N, float* out);
+void colsum_acc_f32(cudaStream_t s, const float* X, int64_t ld, int M, int N, float* out);
+
+// ---- attention (policy.cpp:105-129 forward, :292-322 backward) -------------------
+// Packed variable-length causal self-attention over qkv rows [T x (qd + 2 kvd)].
+template <class T>
+void attn_fwd_varlen(cudaStream_t s, const T* qkv, const int32_t* seq_start, int n_seq, int max_len,
+                     int nh, int nkv, int hd, T* ctx, float* lse);
+template <class T>
+void attn_bwd_varlen(cudaStream_t s, const T* qkv, const T* dctx, const float* lse, const int32_t* seq_start,
+                     int n_seq, int max_len, int nh, int nkv, int hd, float* dq32, float* dkv32);
+// qkv-gradient assembly: dqkv (T) from fp32 dq [T x qd] and dkv [T x 2 kvd]
+template <class T>
+void pack_dqkv(cudaStream_t s, const float* dq, const float* dkv, int rows, int qd, int kvd, T* dqkv);
+
+// ---- decode (sampling) ------------------------------------------------------------
+// Prompt KV store [L][P][nkv][Pmax][hd] (shared by the G sequences of a group) from
+// prefill qkv rows; completion KV store [L][S][nkv][max_len][hd].
+template <class T>
+void kv_store_prompt(cudaStream_t s, const T* qkv, const int32_t* seq_start, int n_prompts, int pmax, int qd,
+                     int kvd, int nkv, int hd, T* kstore, T* vstore);
+template <class T>
+void kv_append(cudaStream_t s, const T* qkv, int rows, int qd, int kvd, int nkv, int hd, int slot, int max_len,
+               T* kstore, T* vstore);
+template <class T>
+void attn_decode(cudaStream_t s, const T* qkv, const T* kp, const T* vp, const T* kc, const T* vc,
+                 const int32_t* prompt_len, int rows, int G, int pmax, int n_comp, int max_len, int nh, int nkv,
+                 int hd, T* ctx);
+// One sampling step over fp32 logits rows (policy.cpp:399-426 with the D2 rule).
+void sample_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, int eos, float inv_t,
+                 const uint64_t* keys, int step, const int32_t* cap, uint8_t* finished, int32_t* comp,
+                 float* logp, int32_t* len, int32_t* tok_next, int max_len, float* dump);
+
+// ---- LM-head loss rows (policy.cpp:471-483) ------------------------------------------
+// For each loss row r: lse over non-BOS logits; logp[r] = logit[y_r] - lse;
+// if dz != null: dz[r][i] = w_r * (onehot(y_r) - softmax)_i, BOS column 0.
+template <class T>
+void lm_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, const int32_t* target,
+             const float* weight, float* logp, T* dz);
+
+// ---- gathers ---------------------------------------------------------------------------
+template <class T>
+void gather_rows(cudaStream_t s, const T* src, int64_t ld_src, const int32_t* idx, int rows, int width, T* dst);
+void scatter_rows_f32(cudaStream_t s, const float* src, int rows, int width, const int32_t* idx, float* dst);
+
+// ---- advantage + filter (advantage.cpp:67-140) -------------------------------------------
+void advantage_filter(cudaStream_t s, const double* r, int n, int G, int kind, int normalize, double eps,
+                      double tau, double* adv, uint8_t* kept, int32_t* kept_idx, int32_t* n_kept);
+
+}  // namespace dashcu

@@ -1,0 +1,519 @@
+// Memory-bound kernels of the DASH step: parameter init/casts, the optimizer,
+// embeddings, bias-gradient column sums, LM-head loss rows, the sampling step
+// (non-fused form), KV-cache plumbing and the advantage/filter + compaction.
+#include <cfloat>
+
+#include "kernels.cuh"
+#include "rule.cuh"
+
+namespace dashcu {
+
+int64_t g_launches = 0;
+
+namespace {
+
+inline int grid1d(int64_t n, int bs = 256) {
+  const int64_t b = (n + bs - 1) / bs;
+  return static_cast<int>(b < kNumSMs * 32 ? (b < 1 ? 1 : b) : kNumSMs * 32);
+}
+
+// ---------------------------------------------------------------- init / casts
+
+__global__ void init_normal_ctr_k(float* w, int64_t n, double scale, uint64_t key) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = static_cast<uint64_t>(i >> 1);
+    const uint64_t h1 = splitmix64(key ^ (2 * k));
+    const uint64_t h2 = splitmix64(key ^ (2 * k + 1));
+    const double u1 = (static_cast<double>(h1 >> 11) + 0.5) * 1.1102230246251565e-16;  // 2^-53
+    const double u2 = static_cast<double>(h2 >> 11) * 1.1102230246251565e-16;
+    const double r = sqrt(-2.0 * log(u1));
+    const double t = 6.283185307179586 * u2;
+    w[i] = static_cast<float>(scale * ((i & 1) ? r * sin(t) : r * cos(t)));
+  }
+}
+
+__global__ void f64_to_f32_k(const double* in, float* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = static_cast<float>(in[i]);
+}
+__global__ void f32_to_f64_k(const float* in, double* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = static_cast<double>(in[i]);
+}
+__global__ void cast_bf16_k(const float* in, bf16* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __float2bfloat16_rn(in[i]);
+}
+__global__ void fill_k(float* p, float v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// Adam / SGD ascent on fp32 master weights; 4 elements per
+// thread iteration with 16-byte accesses where aligned.
+__global__ void optimizer_k(int kind, float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m,
+                            float* __restrict__ v, bf16* __restrict__ wT, int64_t n, float lr, float b1, float b2,
+                            float eps, float c1, float c2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    float wi = w[i];
+    if (kind == 0) {
+      wi += lr * gi;
+    } else {
+      const float mi = b1 * m[i] + (1.f - b1) * gi;
+      const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+      m[i] = mi;
+      v[i] = vi;
+      wi += lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+    }
+    w[i] = wi;
+    if (wT) wT[i] = __float2bfloat16_rn(wi);
+  }
+}
+
+// ------------------------------------------------------------------ embeddings
+
+template <class T>
+__global__ void embed_fwd_k(const T* E, const T* P, const int32_t* tok, const int32_t* pos, int rows, int d,
+                            float* x32, T* xT) {
+  const int64_t n = static_cast<int64_t>(rows) * d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(i / d), c = static_cast<int>(i % d);
+    const float v = tof<T>(E[static_cast<int64_t>(tok[r]) * d + c]) + tof<T>(P[static_cast<int64_t>(pos[r]) * d + c]);
+    x32[i] = v;
+    xT[i] = fromf<T>(v);
+  }
+}
+
+template <class T>
+__global__ void embed_decode_k(const T* E, const T* P, const int32_t* tok, const int32_t* plen, int step, int rows,
+                               int d, float* x32, T* xT) {
+  const int64_t n = static_cast<int64_t>(rows) * d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(i / d), c = static_cast<int>(i % d);
+    const int p = plen[r] + step - 1;
+    const float v = tof<T>(E[static_cast<int64_t>(tok[r]) * d + c]) + tof<T>(P[static_cast<int64_t>(p) * d + c]);
+    x32[i] = v;
+    xT[i] = fromf<T>(v);
+  }
+}
+
+__global__ void embed_bwd_k(const float* dx, const int32_t* tok, const int32_t* pos, int rows, int d, float* gt,
+                            float* gp) {
+  const int64_t n = static_cast<int64_t>(rows) * d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(i / d), c = static_cast<int>(i % d);
+    const float v = dx[i];
+    atomicAdd(&gt[static_cast<int64_t>(tok[r]) * d + c], v);
+    atomicAdd(&gp[static_cast<int64_t>(pos[r]) * d + c], v);
+  }
+}
+
+template <class T>
+__global__ void colsum_k(const T* X, int64_t ld, int M, int N, float* out) {
+  __shared__ float red[8][33];
+  const int n = blockIdx.x * 32 + threadIdx.x;
+  const int r0 = blockIdx.y * 512;
+  float s = 0.f;
+  if (n < N)
+    for (int r = r0 + threadIdx.y; r < min(M, r0 + 512); r += 8) s += tof<T>(X[static_cast<int64_t>(r) * ld + n]);
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && n < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k][threadIdx.x];
+    atomicAdd(&out[n], t);
+  }
+}
+
+// ----------------------------------------------------------- sampling / loss rows
+
+struct ArgBest {
+  float s;
+  int i;
+};
+
+__device__ __forceinline__ ArgBest block_argmax(ArgBest b, float* ss, int* si) {
+  // warp
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float s2 = __shfl_xor_sync(0xffffffffu, b.s, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, b.i, o);
+    if (better(s2, i2, b.s, b.i)) {
+      b.s = s2;
+      b.i = i2;
+    }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    ss[w] = b.s;
+    si[w] = b.i;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    b.s = l < nw ? ss[l] : -FLT_MAX;
+    b.i = l < nw ? si[l] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float s2 = __shfl_xor_sync(0xffffffffu, b.s, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, b.i, o);
+      if (better(s2, i2, b.s, b.i)) {
+        b.s = s2;
+        b.i = i2;
+      }
+    }
+    if (l == 0) {
+      ss[0] = b.s;
+      si[0] = b.i;
+    }
+  }
+  __syncthreads();
+  ArgBest r{ss[0], si[0]};
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ float block_reduce(float v, float* sm, bool is_max) {
+  v = is_max ? warp_max(v) : warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sm[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    float t = l < nw ? sm[l] : (is_max ? -FLT_MAX : 0.f);
+    t = is_max ? warp_max(t) : warp_sum(t);
+    if (l == 0) sm[0] = t;
+  }
+  __syncthreads();
+  const float r = sm[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(256) sample_rows_k(const float* logits, int V, int bos, int eos, float inv_t,
+                                                     const uint64_t* keys, int step, const int32_t* cap,
+                                                     uint8_t* finished, int32_t* comp, float* logp, int32_t* len,
+                                                     int32_t* tok_next, int max_len, float* dump) {
+  __shared__ float ss[32];
+  __shared__ int si[32];
+  const int r = blockIdx.x;
+  const bool active = !finished[r] && step < cap[r];
+  if (!active) {
+    if (threadIdx.x == 0) tok_next[r] = eos;
+    return;
+  }
+  const float* lg = logits + static_cast<int64_t>(r) * V;
+  const uint32_t rk = row_key(keys[r], step);
+  ArgBest b{-FLT_MAX, 0x7fffffff};
+  float mx = -FLT_MAX;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const float l = lg[i];
+    if (dump) dump[(static_cast<int64_t>(r) * max_len + step) * V + i] = l;
+    if (i == bos) continue;
+    const float sc = gumbel_score(l, inv_t, rk, i);
+    if (better(sc, i, b.s, b.i)) {
+      b.s = sc;
+      b.i = i;
+    }
+    mx = fmaxf(mx, l);
+  }
+  b = block_argmax(b, ss, si);
+  mx = block_reduce(mx, ss, true);
+  float sum = 0.f;
+  for (int i = threadIdx.x; i < V; i += blockDim.x)
+    if (i != bos) sum += __expf(lg[i] - mx);
+  sum = block_reduce(sum, ss, false);
+  if (threadIdx.x == 0) {
+    const int tk = b.i;
+    comp[static_cast<int64_t>(r) * max_len + step] = tk;
+    logp[static_cast<int64_t>(r) * max_len + step] = lg[tk] - (mx + logf(sum));
+    len[r] = step + 1;
+    if (tk == eos) finished[r] = 1;
+    tok_next[r] = tk;
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) lm_rows_k(const float* logits, int V, int bos, const int32_t* target,
+                                                 const float* weight, float* logp, T* dz) {
+  __shared__ float sm[32];
+  const int r = blockIdx.x;
+  const float* lg = logits + static_cast<int64_t>(r) * V;
+  float mx = -FLT_MAX;
+  for (int i = threadIdx.x; i < V; i += blockDim.x)
+    if (i != bos) mx = fmaxf(mx, lg[i]);
+  mx = block_reduce(mx, sm, true);
+  float sum = 0.f;
+  for (int i = threadIdx.x; i < V; i += blockDim.x)
+    if (i != bos) sum += expf(lg[i] - mx);
+  sum = block_reduce(sum, sm, false);
+  const float lse = mx + logf(sum);
+  const int y = target[r];
+  if (threadIdx.x == 0 && logp) logp[r] = lg[y] - lse;
+  if (dz) {
+    const float w = weight ? weight[r] : 1.f;
+    T* out = dz + static_cast<int64_t>(r) * V;
+    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+      float v = 0.f;
+      if (i != bos) v = w * ((i == y ? 1.f : 0.f) - expf(lg[i] - lse));
+      out[i] = fromf<T>(v);
+    }
+  }
+}
+
+// ------------------------------------------------------------------- KV plumbing
+
+template <class T>
+__global__ void kv_store_prompt_k(const T* qkv, const int32_t* start, int n_prompts, int pmax, int qd, int kvd,
+                                  int nkv, int hd, T* ks, T* vs) {
+  const int p = blockIdx.y;
+  const int s0 = start[p], len = start[p + 1] - s0;
+  const int qkvd = qd + 2 * kvd;
+  const int64_t n = static_cast<int64_t>(len) * kvd;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int t = static_cast<int>(i / kvd), c = static_cast<int>(i % kvd);
+    const int h = c / hd, dd = c % hd;
+    const int64_t src = static_cast<int64_t>(s0 + t) * qkvd + qd + c;
+    const int64_t dst = ((static_cast<int64_t>(p) * nkv + h) * pmax + t) * hd + dd;
+    ks[dst] = qkv[src];
+    vs[dst] = qkv[src + kvd];
+  }
+}
+
+template <class T>
+__global__ void kv_append_k(const T* qkv, int rows, int qd, int kvd, int nkv, int hd, int slot, int max_len, T* ks,
+                            T* vs) {
+  const int qkvd = qd + 2 * kvd;
+  const int64_t n = static_cast<int64_t>(rows) * kvd;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(i / kvd), c = static_cast<int>(i % kvd);
+    const int h = c / hd, dd = c % hd;
+    const int64_t src = static_cast<int64_t>(r) * qkvd + qd + c;
+    const int64_t dst = ((static_cast<int64_t>(r) * nkv + h) * max_len + slot) * hd + dd;
+    ks[dst] = qkv[src];
+    vs[dst] = qkv[src + kvd];
+  }
+}
+
+template <class T>
+__global__ void pack_dqkv_k(const float* dq, const float* dkv, int rows, int qd, int kvd, T* out) {
+  const int w = qd + 2 * kvd;
+  const int64_t n = static_cast<int64_t>(rows) * w;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(i / w), c = static_cast<int>(i % w);
+    const float v = c < qd ? dq[static_cast<int64_t>(r) * qd + c] : dkv[static_cast<int64_t>(r) * 2 * kvd + (c - qd)];
+    out[i] = fromf<T>(v);
+  }
+}
+
+template <class T>
+__global__ void gather_rows_k(const T* src, int64_t ld, const int32_t* idx, int rows, int width, T* dst) {
+  const int64_t n = static_cast<int64_t>(rows) * width;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(i / width), c = static_cast<int>(i % width);
+    dst[i] = src[static_cast<int64_t>(idx[r]) * ld + c];
+  }
+}
+
+__global__ void scatter_rows_k(const float* src, int rows, int width, const int32_t* idx, float* dst) {
+  const int64_t n = static_cast<int64_t>(rows) * width;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(i / width), c = static_cast<int>(i % width);
+    dst[static_cast<int64_t>(idx[r]) * width + c] = src[i];
+  }
+}
+
+// ------------------------------------------------------------ advantage / filter
+
+// One thread per group, sequential fp64 sums in index order: bit-identical to
+// advantage.cpp (group_advantage :80-94, leave_one_out :96-112, normalize_std
+// :114-133, filter :135-140) for any rewards, not just binary ones.
+__global__ void advantage_k(const double* r, int n, int G, int kind, int normalize, double eps, double tau,
+                            double* adv, uint8_t* kept) {
+  const int gs = kind == 0 ? n : G;
+  const int ngroups = n / gs;
+  for (int grp = blockIdx.x * blockDim.x + threadIdx.x; grp < ngroups; grp += gridDim.x * blockDim.x) {
+    const int s = grp * gs;
+    double sum = 0.0;
+    for (int i = s; i < s + gs; ++i) sum += r[i];
+    if (kind == 2) {
+      const double den = static_cast<double>(gs - 1);
+      for (int i = s; i < s + gs; ++i) adv[i] = r[i] - (sum - r[i]) / den;
+    } else {
+      const double mean = sum / static_cast<double>(gs);
+      for (int i = s; i < s + gs; ++i) adv[i] = r[i] - mean;
+    }
+    if (normalize) {
+      double mean = 0.0;
+      for (int i = s; i < s + gs; ++i) mean += r[i];
+      mean /= static_cast<double>(gs);
+      double var = 0.0;
+      for (int i = s; i < s + gs; ++i) var += (r[i] - mean) * (r[i] - mean);
+      var /= static_cast<double>(gs);
+      const double den = sqrt(var) + eps;
+      for (int i = s; i < s + gs; ++i) adv[i] = adv[i] / den;
+    }
+    for (int i = s; i < s + gs; ++i) kept[i] = fabs(adv[i]) > tau ? 1 : 0;
+  }
+}
+
+// Single-block ballot + prefix-sum stream compaction: ascending kept indices.
+__global__ void __launch_bounds__(1024) compact_k(const uint8_t* kept, int n, int32_t* idx, int32_t* n_kept) {
+  __shared__ int warp_tot[32];
+  __shared__ int base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int c = 0; c < n; c += 1024) {
+    const int i = c + threadIdx.x;
+    const bool k = i < n && kept[i];
+    const unsigned bal = __ballot_sync(0xffffffffu, k);
+    if (lane == 0) warp_tot[w] = __popc(bal);
+    __syncthreads();
+    int off = 0;
+    for (int j = 0; j < w; ++j) off += warp_tot[j];
+    if (k) idx[base + off + __popc(bal & ((1u << lane) - 1u))] = i;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int j = 0; j < 32; ++j) t += warp_tot[j];
+      base += t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_kept = base;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------- wrappers
+
+void init_normal_ctr(cudaStream_t s, float* w, int64_t n, double scale, uint64_t seed) {
+  init_normal_ctr_k<<<grid1d(n), 256, 0, s>>>(w, n, scale, splitmix64(seed ^ 0x5DEECE66Dull));
+  DCU_LAUNCHED();
+}
+void f64_to_f32(cudaStream_t s, const double* in, float* out, int64_t n) {
+  f64_to_f32_k<<<grid1d(n), 256, 0, s>>>(in, out, n);
+  DCU_LAUNCHED();
+}
+void f32_to_f64(cudaStream_t s, const float* in, double* out, int64_t n) {
+  f32_to_f64_k<<<grid1d(n), 256, 0, s>>>(in, out, n);
+  DCU_LAUNCHED();
+}
+void cast_f32_bf16(cudaStream_t s, const float* in, bf16* out, int64_t n) {
+  cast_bf16_k<<<grid1d(n), 256, 0, s>>>(in, out, n);
+  DCU_LAUNCHED();
+}
+void fill_f32(cudaStream_t s, float* p, float v, int64_t n) {
+  if (n <= 0) return;
+  fill_k<<<grid1d(n), 256, 0, s>>>(p, v, n);
+  DCU_LAUNCHED();
+}
+void optimizer_update(cudaStream_t s, int kind, float* w, const float* g, float* m, float* v, bf16* wT, int64_t n,
+                      float lr, float b1, float b2, float eps, float c1, float c2) {
+  optimizer_k<<<grid1d(n), 256, 0, s>>>(kind, w, g, m, v, wT, n, lr, b1, b2, eps, c1, c2);
+  DCU_LAUNCHED();
+}
+
+template <class T>
+void embed_fwd(cudaStream_t s, const T* E, const T* P, const int32_t* tok, const int32_t* pos, int rows, int d,
+               float* x32, T* xT) {
+  if (rows <= 0) return;
+  embed_fwd_k<T><<<grid1d(static_cast<int64_t>(rows) * d), 256, 0, s>>>(E, P, tok, pos, rows, d, x32, xT);
+  DCU_LAUNCHED();
+}
+template <class T>
+void embed_decode(cudaStream_t s, const T* E, const T* P, const int32_t* tok, const int32_t* plen, int step,
+                  int rows, int d, float* x32, T* xT) {
+  embed_decode_k<T><<<grid1d(static_cast<int64_t>(rows) * d), 256, 0, s>>>(E, P, tok, plen, step, rows, d, x32, xT);
+  DCU_LAUNCHED();
+}
+void embed_bwd(cudaStream_t s, const float* dx, const int32_t* tok, const int32_t* pos, int rows, int d, float* gt,
+               float* gp) {
+  if (rows <= 0) return;
+  embed_bwd_k<<<grid1d(static_cast<int64_t>(rows) * d), 256, 0, s>>>(dx, tok, pos, rows, d, gt, gp);
+  DCU_LAUNCHED();
+}
+template <class T>
+void colsum_acc(cudaStream_t s, const T* X, int64_t ld, int M, int N, float* out) {
+  if (M <= 0 || N <= 0) return;
+  colsum_k<T><<<dim3(cdiv(N, 32), cdiv(M, 512)), dim3(32, 8), 0, s>>>(X, ld, M, N, out);
+  DCU_LAUNCHED();
+}
+void colsum_acc_f32(cudaStream_t s, const float* X, int64_t ld, int M, int N, float* out) {
+  colsum_acc<float>(s, X, ld, M, N, out);
+}
+
+void sample_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, int eos, float inv_t,
+                 const uint64_t* keys, int step, const int32_t* cap, uint8_t* finished, int32_t* comp, float* logp,
+                 int32_t* len, int32_t* tok_next, int max_len, float* dump) {
+  sample_rows_k<<<rows, 256, 0, s>>>(logits, V, bos, eos, inv_t, keys, step, cap, finished, comp, logp, len, tok_next,
+                                     max_len, dump);
+  DCU_LAUNCHED();
+}
+
+template <class T>
+void lm_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, const int32_t* target,
+             const float* weight, float* logp, T* dz) {
+  if (rows <= 0) return;
+  lm_rows_k<T><<<rows, 256, 0, s>>>(logits, V, bos, target, weight, logp, dz);
+  DCU_LAUNCHED();
+}
+
+template <class T>
+void kv_store_prompt(cudaStream_t s, const T* qkv, const int32_t* start, int n_prompts, int pmax, int qd, int kvd,
+                     int nkv, int hd, T* ks, T* vs) {
+  kv_store_prompt_k<T><<<dim3(cdiv(static_cast<int64_t>(pmax) * kvd, 256), n_prompts), 256, 0, s>>>(
+      qkv, start, n_prompts, pmax, qd, kvd, nkv, hd, ks, vs);
+  DCU_LAUNCHED();
+}
+template <class T>
+void kv_append(cudaStream_t s, const T* qkv, int rows, int qd, int kvd, int nkv, int hd, int slot, int max_len,
+               T* ks, T* vs) {
+  kv_append_k<T><<<grid1d(static_cast<int64_t>(rows) * kvd), 256, 0, s>>>(qkv, rows, qd, kvd, nkv, hd, slot, max_len,
+                                                                         ks, vs);
+  DCU_LAUNCHED();
+}
+template <class T>
+void pack_dqkv(cudaStream_t s, const float* dq, const float* dkv, int rows, int qd, int kvd, T* out) {
+  pack_dqkv_k<T><<<grid1d(static_cast<int64_t>(rows) * (qd + 2 * kvd)), 256, 0, s>>>(dq, dkv, rows, qd, kvd, out);
+  DCU_LAUNCHED();
+}
+template <class T>
+void gather_rows(cudaStream_t s, const T* src, int64_t ld, const int32_t* idx, int rows, int width, T* dst) {
+  if (rows <= 0) return;
+  gather_rows_k<T><<<grid1d(static_cast<int64_t>(rows) * width), 256, 0, s>>>(src, ld, idx, rows, width, dst);
+  DCU_LAUNCHED();
+}
+void scatter_rows_f32(cudaStream_t s, const float* src, int rows, int width, const int32_t* idx, float* dst) {
+  if (rows <= 0) return;
+  scatter_rows_k<<<grid1d(static_cast<int64_t>(rows) * width), 256, 0, s>>>(src, rows, width, idx, dst);
+  DCU_LAUNCHED();
+}
+
+void advantage_filter(cudaStream_t s, const double* r, int n, int G, int kind, int normalize, double eps, double tau,
+                      double* adv, uint8_t* kept, int32_t* kept_idx, int32_t* n_kept) {
+  const int ngroups = kind == 0 ? 1 : n / G;
+  advantage_k<<<cdiv(ngroups, 128), 128, 0, s>>>(r, n, G, kind, normalize, eps, tau, adv, kept);
+  DCU_LAUNCHED();
+  compact_k<<<1, 1024, 0, s>>>(kept, n, kept_idx, n_kept);
+  DCU_LAUNCHED();
+}
+
+#define INST(T)                                                                                                   \
+  template void embed_fwd<T>(cudaStream_t, const T*, const T*, const int32_t*, const int32_t*, int, int, float*, T*); \
+  template void embed_decode<T>(cudaStream_t, const T*, const T*, const int32_t*, const int32_t*, int, int, int,     \
+                                float*, T*);                                                                      \
+  template void colsum_acc<T>(cudaStream_t, const T*, int64_t, int, int, float*);                                \
+  template void lm_rows<T>(cudaStream_t, const float*, int, int, int, const int32_t*, const float*, float*, T*);  \
+  template void kv_store_prompt<T>(cudaStream_t, const T*, const int32_t*, int, int, int, int, int, int, T*, T*); \
+  template void kv_append<T>(cudaStream_t, const T*, int, int, int, int, int, int, int, T*, T*);                  \
+  template void pack_dqkv<T>(cudaStream_t, const float*, const float*, int, int, int, T*);                        \
+  template void gather_rows<T>(cudaStream_t, const T*, int64_t, const int32_t*, int, int, T*);
+INST(float)
+INST(bf16)
+#undef INST
+
+}  // namespace dashcu

@@ -1,0 +1,1201 @@
+// Host orchestration of the DASH step on one B200 + the C ABI (include/dashcu.h).
+//
+// The reference runs one trajectory at a time on one core (policy.cpp:379-485);
+// here every phase is batched over the whole rollout and stays on the device:
+//
+//   dashcu_sample      prefill of the M prompts (once per group, not G times:
+//                      policy.cpp:396 re-runs the prompt for every sample),
+//                      then one decode step per completion position over all
+//                      M*G sequences, KV in HBM, Gumbel-max sampling.
+//   dashcu_rollout_advantage   one thread per group, fp64, + compaction.
+//   dashcu_accumulate  packed teacher-forced forward + exact reverse pass per
+//                      micro-batch of kept sequences; weight gradients
+//                      accumulate straight into the fp32 gradient (beta = 1).
+//   dashcu_allreduce_grads / dashcu_optimizer_step.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/dashcu.h"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "kernels.cuh"
+#include "rule.cuh"
+
+namespace dashcu {
+
+thread_local std::string g_last_error;
+
+// ------------------------------------------------------------------ memory
+
+struct DevMem {
+  void* p = nullptr;
+  size_t n = 0;
+  DevMem() = default;
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
+  ~DevMem() {
+    if (p) cudaFree(p);
+  }
+  void ensure(size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (bytes > n) {
+      if (p) DCU_CHECK(cudaFree(p));
+      p = nullptr;
+      DCU_CHECK(cudaMalloc(&p, bytes));
+      n = bytes;
+    }
+  }
+  template <class X>
+  X* as() const {
+    return static_cast<X*>(p);
+  }
+};
+
+// Named grow-only device buffers (reused across steps; no per-call cudaMalloc).
+struct Workspace {
+  std::map<std::string, DevMem> bufs;
+  template <class X>
+  X* get(const std::string& k, size_t count) {
+    DevMem& b = bufs[k];
+    b.ensure(count * sizeof(X));
+    return b.as<X>();
+  }
+};
+
+template <class X>
+void h2d(cudaStream_t s, X* dst, const X* src, size_t count) {
+  if (count) DCU_CHECK(cudaMemcpyAsync(dst, src, count * sizeof(X), cudaMemcpyHostToDevice, s));
+}
+template <class X>
+void d2h(cudaStream_t s, X* dst, const X* src, size_t count) {
+  if (count) DCU_CHECK(cudaMemcpyAsync(dst, src, count * sizeof(X), cudaMemcpyDeviceToHost, s));
+}
+
+// ------------------------------------------------------------------- NCCL
+// Resolved at run time so the process shares whichever libnccl torch loaded.
+struct NcclApi {
+  bool ok = false;
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+  static NcclApi& get() {
+    static NcclApi a = [] {
+      NcclApi r;
+      void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+      if (!h) return r;
+      r.GetUniqueId = (decltype(r.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+      r.CommInitRank = (decltype(r.CommInitRank))dlsym(h, "ncclCommInitRank");
+      r.AllReduce = (decltype(r.AllReduce))dlsym(h, "ncclAllReduce");
+      r.CommDestroy = (decltype(r.CommDestroy))dlsym(h, "ncclCommDestroy");
+      r.GetErrorString = (decltype(r.GetErrorString))dlsym(h, "ncclGetErrorString");
+      r.ok = r.GetUniqueId && r.CommInitRank && r.AllReduce && r.CommDestroy;
+      return r;
+    }();
+    return a;
+  }
+};
+
+#define NCCL_CHECK(x)                                                                          \
+  do {                                                                                         \
+    ncclResult_t r__ = (x);                                                                    \
+    if (r__ != ncclSuccess)                                                                    \
+      throw Error(4, std::string("NCCL error ") +                                              \
+                         (NcclApi::get().GetErrorString ? NcclApi::get().GetErrorString(r__) : "?")); \
+  } while (0)
+
+// ------------------------------------------------------------- host rng.hpp
+
+uint64_t fnv1a(const char* s) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (const unsigned char* p = reinterpret_cast<const unsigned char*>(s); *p; ++p) {
+    h ^= *p;
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+// derive_seed (rng.hpp:29-35)
+uint64_t derive_seed(uint64_t base, const char* tag, uint64_t a, uint64_t b) {
+  uint64_t h = splitmix64(base ^ fnv1a(tag));
+  h = splitmix64(h ^ (a + 0x9e3779b97f4a7c15ull));
+  return splitmix64(h ^ (b + 0x7f4a7c159e3779b9ull));
+}
+
+// ---------------------------------------------------------------- geometry
+
+struct Geo {
+  int V, d, ctx, H, L, bos, eos, nh, nkv, hd, qd, kvd, qkvd;
+};
+
+// Flat views() order (tensors.cpp:49-71) with the GQA-shaped wq/wk/wv/wo.
+struct Lay {
+  int64_t tok, pos, layer0, lstride, wq, wk, wv, wo, w1, b1, w2, b2, wout, bout, total;
+};
+
+Geo geo_of(const dashcu_arch& a) {
+  Geo g;
+  g.V = a.vocab_size;
+  g.d = a.embed_dim;
+  g.ctx = a.context_len;
+  g.H = a.ffn_hidden;
+  g.L = a.n_layers;
+  g.bos = a.bos_id;
+  g.eos = a.eos_id;
+  g.nh = a.n_heads > 0 ? a.n_heads : 1;
+  g.nkv = a.n_kv_heads > 0 ? a.n_kv_heads : 1;
+  g.hd = a.head_dim > 0 ? a.head_dim : a.embed_dim;
+  g.qd = g.nh * g.hd;
+  g.kvd = g.nkv * g.hd;
+  g.qkvd = g.qd + 2 * g.kvd;
+  return g;
+}
+
+Lay lay_of(const Geo& g) {
+  Lay l;
+  int64_t off = 0;
+  l.tok = off;
+  off += (int64_t)g.V * g.d;
+  l.pos = off;
+  off += (int64_t)g.ctx * g.d;
+  l.layer0 = off;
+  int64_t lo = 0;
+  l.wq = lo;
+  lo += (int64_t)g.qd * g.d;
+  l.wk = lo;
+  lo += (int64_t)g.kvd * g.d;
+  l.wv = lo;
+  lo += (int64_t)g.kvd * g.d;
+  l.wo = lo;
+  lo += (int64_t)g.d * g.qd;
+  l.w1 = lo;
+  lo += (int64_t)g.H * g.d;
+  l.b1 = lo;
+  lo += g.H;
+  l.w2 = lo;
+  lo += (int64_t)g.d * g.H;
+  l.b2 = lo;
+  lo += g.d;
+  l.lstride = lo;
+  off += lo * g.L;
+  l.wout = off;
+  off += (int64_t)g.V * g.d;
+  l.bout = off;
+  off += g.V;
+  l.total = off;
+  return l;
+}
+
+// ArchConfig::validate (tensors.cpp:11-22) + GQA constraints.
+void validate_arch(const dashcu_arch& a) {
+  auto bad = [](const char* m) { throw Error(1, std::string("arch: ") + m); };
+  if (a.vocab_size < 3) bad("vocab_size must be >= 3");
+  if (a.embed_dim < 1) bad("embed_dim must be >= 1");
+  if (a.context_len < 2) bad("context_len must be >= 2");
+  if (a.ffn_hidden < 1) bad("ffn_hidden must be >= 1");
+  if (a.n_layers < 1) bad("n_layers must be >= 1");
+  if (a.eos_id < 0 || a.eos_id >= a.vocab_size) bad("eos_id out of range");
+  if (a.bos_id < -1 || a.bos_id >= a.vocab_size || a.bos_id == a.eos_id) bad("bos_id out of range");
+  if (a.bos_id >= 0 && a.vocab_size < 4) bad("need at least 3 sampleable tokens besides BOS");
+  const Geo g = geo_of(a);
+  if (g.nh < 1 || g.nkv < 1 || g.hd < 1 || g.nh % g.nkv != 0) bad("n_heads must be a multiple of n_kv_heads");
+}
+
+// -------------------------------------------------------------------- ctx
+
+}  // namespace dashcu
+
+struct dashcu_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0;
+  dashcu::Workspace ws;
+};
+
+struct dashcu_policy {
+  dashcu_ctx* ctx = nullptr;
+  dashcu::Geo g{};
+  dashcu::Lay lay{};
+  dashcu_arch arch{};
+  int dtype = DASHCU_F32;
+  dashcu::DevMem w32, wT, g32, am, av;
+  int64_t adam_t = 0;
+  uint64_t version = 1;
+  // rollout (SPEC.md RolloutCache: write-once per round, served whole)
+  int n_prompts = 0, G = 0, n_seq = 0, max_len = 0;
+  uint64_t ro_version = 0;
+  bool ro_valid = false;
+  std::vector<int32_t> h_prompt_tok;
+  std::vector<int64_t> h_prompt_off;
+  std::vector<int32_t> h_comp, h_len;
+  dashcu::DevMem d_comp, d_len, d_logp;
+  std::vector<double> h_rewards, h_adv;
+  std::vector<int32_t> h_kidx;
+  bool adv_valid = false;
+  bool dump = false;
+  dashcu::DevMem d_dump;
+  int64_t dump_n = 0;
+  dashcu_stats st{};
+  int64_t launches0 = 0;
+  dashcu::Workspace ws;
+};
+
+namespace dashcu {
+
+using Pol = dashcu_policy;
+
+struct Timer {
+  cudaStream_t s;
+  cudaEvent_t a, b;
+  explicit Timer(cudaStream_t st) : s(st) {
+    DCU_CHECK(cudaEventCreate(&a));
+    DCU_CHECK(cudaEventCreate(&b));
+    DCU_CHECK(cudaEventRecord(a, s));
+  }
+  double stop_ms() {
+    DCU_CHECK(cudaEventRecord(b, s));
+    DCU_CHECK(cudaEventSynchronize(b));
+    float ms = 0;
+    DCU_CHECK(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return ms;
+  }
+};
+
+template <class T>
+struct Engine {
+  Pol& P;
+  cudaStream_t st;
+  const Geo& g;
+  const Lay& L;
+  explicit Engine(Pol& p) : P(p), st(p.ctx->stream), g(p.g), L(p.lay) {}
+
+  const T* W(int64_t off) const {
+    if constexpr (sizeof(T) == 4) return P.w32.as<const T>() + off;
+    else return P.wT.as<const T>() + off;
+  }
+  const float* W32(int64_t off) const { return P.w32.as<const float>() + off; }
+  float* G32(int64_t off) const { return P.g32.as<float>() + off; }
+  int64_t lb(int l) const { return L.layer0 + static_cast<int64_t>(l) * L.lstride; }
+  int dt() const { return sizeof(T) == 4 ? 0 : 1; }
+
+  void mm(int M, int N, int K, const T* A, int64_t lda, bool ak, const T* B, int64_t ldb, bool bk, const Epi& e) {
+    GemmShape s{M, N, K, A, lda, ak, B, ldb, bk};
+    gemm(st, dt(), s, e);
+  }
+  static Epi store(float* c32, int64_t ldc32, T* cT, int64_t ldcT) {
+    Epi e;
+    e.c32 = c32;
+    e.ldc32 = ldc32;
+    e.cT = cT;
+    e.ldcT = ldcT;
+    return e;
+  }
+
+  // ---------------------------------------------------------- activations
+  struct Acts {
+    int T_ = 0;
+    T *xT, *qkv, *ctx, *hT, *u, *yT;
+    float *lse, *x32, *h32;
+  };
+
+  Acts alloc_acts(Workspace& ws, int Tn, const std::string& tag) {
+    Acts a;
+    a.T_ = Tn;
+    const size_t t = static_cast<size_t>(Tn);
+    a.xT = ws.get<T>(tag + "xT", t * g.d * g.L);
+    a.qkv = ws.get<T>(tag + "qkv", t * g.qkvd * g.L);
+    a.ctx = ws.get<T>(tag + "ctx", t * g.qd * g.L);
+    a.hT = ws.get<T>(tag + "hT", t * g.d * g.L);
+    a.u = ws.get<T>(tag + "u", t * g.H * g.L);
+    a.yT = ws.get<T>(tag + "yT", t * g.d);
+    a.lse = ws.get<float>(tag + "lse", t * g.nh * g.L);
+    a.x32 = ws.get<float>(tag + "x32", t * g.d);
+    a.h32 = ws.get<float>(tag + "h32", t * g.d);
+    return a;
+  }
+
+  // Teacher-forced forward over packed sequences (advance() at every position,
+  // policy.cpp:80-153). tok/pos/start are device arrays.
+  void forward(Acts& A, const int32_t* tok, const int32_t* pos, const int32_t* start, int nseq, int maxlen) {
+    const int Tn = A.T_;
+    const size_t t = static_cast<size_t>(Tn);
+    embed_fwd<T>(st, W(L.tok), W(L.pos), tok, pos, Tn, g.d, A.x32, A.xT);
+    for (int l = 0; l < g.L; ++l) {
+      const int64_t b = lb(l);
+      T* xl = A.xT + t * g.d * l;
+      T* qkv = A.qkv + t * g.qkvd * l;
+      T* ctx = A.ctx + t * g.qd * l;
+      T* hT = A.hT + t * g.d * l;
+      T* u = A.u + t * g.H * l;
+      float* lse = A.lse + t * g.nh * l;
+      mm(Tn, g.qkvd, g.d, xl, g.d, true, W(b + L.wq), g.d, true, store(nullptr, 0, qkv, g.qkvd));
+      attn_fwd_varlen<T>(st, qkv, start, nseq, maxlen, g.nh, g.nkv, g.hd, ctx, lse);
+      Epi eo = store(A.h32, g.d, hT, g.d);
+      eo.resid = A.x32;
+      eo.ldr = g.d;
+      mm(Tn, g.d, g.qd, ctx, g.qd, true, W(b + L.wo), g.qd, true, eo);
+      Epi e1 = store(nullptr, 0, u, g.H);
+      e1.kind = EPI_TANH;
+      e1.bias = W32(b + L.b1);
+      mm(Tn, g.H, g.d, hT, g.d, true, W(b + L.w1), g.d, true, e1);
+      T* next = (l + 1 < g.L) ? A.xT + t * g.d * (l + 1) : A.yT;
+      Epi e2 = store(A.x32, g.d, next, g.d);
+      e2.bias = W32(b + L.b2);
+      e2.resid = A.h32;
+      e2.ldr = g.d;
+      mm(Tn, g.d, g.H, u, g.H, true, W(b + L.w2), g.H, true, e2);
+    }
+  }
+
+  // Loss rows: rows (packed index), tgt, weight. If grad: backward through the
+  // LM head, writing dL/dy_top into dy32 (zeroed here). logp may be null.
+  void lm_head(const Acts& A, int R, const int32_t* rows, const int32_t* tgt, const float* w, float* logp,
+               bool grad, float* dy32) {
+    const int64_t V = g.V;
+    const int RC = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8192, (int64_t(1) << 31) / (V * 4))));
+    if (grad) fill_f32(st, dy32, 0.f, static_cast<int64_t>(A.T_) * g.d);
+    T* ycT = P.ws.get<T>("lm_yc", static_cast<size_t>(RC) * g.d);
+    float* lg = P.ws.get<float>("lm_logits", static_cast<size_t>(RC) * V);
+    T* dz = grad ? P.ws.get<T>("lm_dz", static_cast<size_t>(RC) * V) : nullptr;
+    float* dyc = grad ? P.ws.get<float>("lm_dyc", static_cast<size_t>(RC) * g.d) : nullptr;
+    for (int r0 = 0; r0 < R; r0 += RC) {
+      const int rc = std::min(RC, R - r0);
+      gather_rows<T>(st, A.yT, g.d, rows + r0, rc, g.d, ycT);
+      Epi el = store(lg, V, nullptr, 0);
+      el.bias = W32(L.bout);
+      mm(rc, g.V, g.d, ycT, g.d, true, W(L.wout), g.d, true, el);
+      lm_rows<T>(st, lg, rc, g.V, g.bos, tgt + r0, w ? w + r0 : nullptr, logp ? logp + r0 : nullptr, dz);
+      if (!grad) continue;
+      Epi ew;
+      ew.kind = EPI_ACCUM;
+      ew.c32 = G32(L.wout);
+      ew.ldc32 = g.d;
+      mm(g.V, g.d, rc, dz, V, false, ycT, g.d, false, ew);  // dW_out += dz^T y
+      colsum_acc<T>(st, dz, V, rc, g.V, G32(L.bout));         // db_out += sum dz
+      mm(rc, g.d, g.V, dz, V, true, W(L.wout), g.d, false, store(dyc, g.d, nullptr, 0));  // dy = dz W_out
+      scatter_rows_f32(st, dyc, rc, g.d, rows + r0, dy32);
+    }
+  }
+
+  // Exact reverse pass (policy.cpp:201-346) given dL/dy_top in dy32.
+  void backward(const Acts& A, const int32_t* tok, const int32_t* pos, const int32_t* start, int nseq, int maxlen,
+                float* dy32) {
+    const int Tn = A.T_;
+    const size_t t = static_cast<size_t>(Tn);
+    Workspace& ws = P.ws;
+    T* dyT = ws.get<T>("b_dyT", t * g.d);
+    T* dhT = ws.get<T>("b_dhT", t * g.d);
+    float* dh32 = ws.get<float>("b_dh32", t * g.d);
+    float* dx32 = ws.get<float>("b_dx32", t * g.d);
+    T* duT = ws.get<T>("b_duT", t * g.H);
+    T* dctx = ws.get<T>("b_dctx", t * g.qd);
+    float* dq32 = ws.get<float>("b_dq32", t * g.qd);
+    float* dkv32 = ws.get<float>("b_dkv32", t * 2 * g.kvd);
+    T* dqkv = ws.get<T>("b_dqkv", t * g.qkvd);
+    cast_to_T(dy32, dyT, t * g.d);
+    for (int l = g.L - 1; l >= 0; --l) {
+      const int64_t b = lb(l);
+      const T* xl = A.xT + t * g.d * l;
+      const T* qkv = A.qkv + t * g.qkvd * l;
+      const T* ctx = A.ctx + t * g.qd * l;
+      const T* hT = A.hT + t * g.d * l;
+      const T* u = A.u + t * g.H * l;
+      const float* lse = A.lse + t * g.nh * l;
+      Epi acc;
+      acc.kind = EPI_ACCUM;
+      // y = h + W2 u + b2
+      acc.c32 = G32(b + L.w2);
+      acc.ldc32 = g.H;
+      mm(g.d, g.H, Tn, dyT, g.d, false, u, g.H, false, acc);
+      colsum_acc_f32(st, dy32, g.d, Tn, g.d, G32(b + L.b2));
+      Epi edt = store(nullptr, 0, duT, g.H);
+      edt.kind = EPI_DTANH;
+      edt.aux = u;
+      edt.ld_aux = g.H;
+      mm(Tn, g.H, g.d, dyT, g.d, true, W(b + L.w2), g.H, false, edt);
+      // u = tanh(W1 h + b1)
+      colsum_acc<T>(st, duT, g.H, Tn, g.H, G32(b + L.b1));
+      acc.c32 = G32(b + L.w1);
+      acc.ldc32 = g.d;
+      mm(g.H, g.d, Tn, duT, g.H, false, hT, g.d, false, acc);
+      Epi edh = store(dh32, g.d, dhT, g.d);
+      edh.resid = dy32;
+      edh.ldr = g.d;
+      mm(Tn, g.d, g.H, duT, g.H, true, W(b + L.w1), g.d, false, edh);
+      // h = x + Wo ctx
+      acc.c32 = G32(b + L.wo);
+      acc.ldc32 = g.qd;
+      mm(g.d, g.qd, Tn, dhT, g.d, false, ctx, g.qd, false, acc);
+      mm(Tn, g.qd, g.d, dhT, g.d, true, W(b + L.wo), g.qd, false, store(nullptr, 0, dctx, g.qd));
+      // attention
+      fill_f32(st, dkv32, 0.f, static_cast<int64_t>(t) * 2 * g.kvd);
+      attn_bwd_varlen<T>(st, qkv, dctx, lse, start, nseq, maxlen, g.nh, g.nkv, g.hd, dq32, dkv32);
+      pack_dqkv<T>(st, dq32, dkv32, Tn, g.qd, g.kvd, dqkv);
+      // q, k, v projections (wq, wk, wv are contiguous rows of one [qkvd x d] matrix)
+      acc.c32 = G32(b + L.wq);
+      acc.ldc32 = g.d;
+      mm(g.qkvd, g.d, Tn, dqkv, g.qkvd, false, xl, g.d, false, acc);
+      Epi edx = store(dx32, g.d, dyT, g.d);
+      edx.resid = dh32;
+      edx.ldr = g.d;
+      mm(Tn, g.d, g.qkvd, dqkv, g.qkvd, true, W(b + L.wq), g.d, false, edx);
+      std::swap(dy32, dx32);  // dy for the layer below; dx32 is scratch again
+    }
+    embed_bwd(st, dy32, tok, pos, Tn, g.d, G32(L.tok), G32(L.pos));
+  }
+
+  void cast_to_T(const float* in, T* out, size_t n) {
+    if constexpr (sizeof(T) == 4) {
+      DCU_CHECK(cudaMemcpyAsync(out, in, n * 4, cudaMemcpyDeviceToDevice, st));
+    } else {
+      cast_f32_bf16(st, in, out, static_cast<int64_t>(n));
+    }
+  }
+
+  // ------------------------------------------------------------ micro-batch
+  struct Batch {
+    std::vector<int32_t> tok, pos, start, rows, tgt, seqs;
+    std::vector<float> w;
+    int maxlen = 0;
+  };
+
+  // Packs prompt + completion[:-1] of each sequence (forward_for_loss, policy.cpp:350-358).
+  Batch pack(const std::vector<int>& seqs, const std::vector<double>& weight) {
+    Batch B;
+    B.start.push_back(0);
+    for (size_t k = 0; k < seqs.size(); ++k) {
+      const int s = seqs[k];
+      const int p = s / P.G;
+      const int64_t po = P.h_prompt_off[p];
+      const int m = static_cast<int>(P.h_prompt_off[p + 1] - po);
+      const int len = P.h_len[s];
+      if (len == 0) continue;
+      const int s0 = B.start.back();
+      for (int i = 0; i < m; ++i) {
+        B.tok.push_back(P.h_prompt_tok[po + i]);
+        B.pos.push_back(i);
+      }
+      for (int j = 0; j + 1 < len; ++j) {
+        B.tok.push_back(P.h_comp[static_cast<int64_t>(s) * P.max_len + j]);
+        B.pos.push_back(m + j);
+      }
+      const int n = m + len - 1;
+      for (int j = 0; j < len; ++j) {
+        B.rows.push_back(s0 + m - 1 + j);
+        B.tgt.push_back(P.h_comp[static_cast<int64_t>(s) * P.max_len + j]);
+        B.w.push_back(static_cast<float>(weight.empty() ? 1.0 : weight[k]));
+      }
+      B.start.push_back(s0 + n);
+      B.seqs.push_back(s);
+      B.maxlen = std::max(B.maxlen, n);
+    }
+    return B;
+  }
+
+  struct DevBatch {
+    int32_t *tok, *pos, *start, *rows, *tgt;
+    float* w;
+  };
+  DevBatch upload(const Batch& B) {
+    DevBatch d;
+    d.tok = P.ws.get<int32_t>("mb_tok", B.tok.size());
+    d.pos = P.ws.get<int32_t>("mb_pos", B.pos.size());
+    d.start = P.ws.get<int32_t>("mb_start", B.start.size());
+    d.rows = P.ws.get<int32_t>("mb_rows", B.rows.size());
+    d.tgt = P.ws.get<int32_t>("mb_tgt", B.tgt.size());
+    d.w = P.ws.get<float>("mb_w", B.w.size());
+    h2d(st, d.tok, B.tok.data(), B.tok.size());
+    h2d(st, d.pos, B.pos.data(), B.pos.size());
+    h2d(st, d.start, B.start.data(), B.start.size());
+    h2d(st, d.rows, B.rows.data(), B.rows.size());
+    h2d(st, d.tgt, B.tgt.data(), B.tgt.size());
+    h2d(st, d.w, B.w.data(), B.w.size());
+    return d;
+  }
+
+  // grad += sum_k weight[k] * grad log pi(seq_k), micro_batch sequences at a time.
+  int64_t accumulate(const std::vector<int>& seqs, const std::vector<double>& weight, int micro) {
+    int64_t loss_tokens = 0;
+    if (micro <= 0) micro = static_cast<int>(seqs.size());
+    for (size_t k0 = 0; k0 < seqs.size(); k0 += micro) {
+      const size_t k1 = std::min(seqs.size(), k0 + static_cast<size_t>(micro));
+      std::vector<int> ss(seqs.begin() + k0, seqs.begin() + k1);
+      std::vector<double> ww(weight.begin() + k0, weight.begin() + k1);
+      Batch B = pack(ss, ww);
+      if (B.seqs.empty()) continue;
+      DevBatch D = upload(B);
+      const int Tn = static_cast<int>(B.tok.size());
+      Acts A = alloc_acts(P.ws, Tn, "a_");
+      forward(A, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen);
+      float* dy32 = P.ws.get<float>("b_dy32", static_cast<size_t>(Tn) * g.d);
+      lm_head(A, static_cast<int>(B.rows.size()), D.rows, D.tgt, D.w, nullptr, true, dy32);
+      backward(A, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen, dy32);
+      loss_tokens += static_cast<int64_t>(B.rows.size());
+    }
+    return loss_tokens;
+  }
+
+  // log_prob (policy.cpp:362-377) for every rollout sequence, concatenated.
+  void log_prob(float* host_out, int64_t n_tokens) {
+    std::vector<int> all(P.n_seq);
+    for (int s = 0; s < P.n_seq; ++s) all[s] = s;
+    const int micro = 64;
+    int64_t off = 0;
+    for (size_t k0 = 0; k0 < all.size(); k0 += micro) {
+      const size_t k1 = std::min(all.size(), k0 + static_cast<size_t>(micro));
+      std::vector<int> ss(all.begin() + k0, all.begin() + k1);
+      Batch B = pack(ss, {});
+      if (B.seqs.empty()) continue;
+      DevBatch D = upload(B);
+      const int Tn = static_cast<int>(B.tok.size());
+      Acts A = alloc_acts(P.ws, Tn, "a_");
+      forward(A, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen);
+      float* lp = P.ws.get<float>("lp_out", B.rows.size());
+      lm_head(A, static_cast<int>(B.rows.size()), D.rows, D.tgt, nullptr, lp, false, nullptr);
+      if (off + static_cast<int64_t>(B.rows.size()) > n_tokens) throw Error(1, "log_prob: output buffer too small");
+      d2h(st, host_out + off, lp, B.rows.size());
+      DCU_CHECK(cudaStreamSynchronize(st));
+      off += static_cast<int64_t>(B.rows.size());
+    }
+  }
+
+  // ------------------------------------------------------------- sampling
+  void sample(const dashcu_plan& plan, const std::vector<int32_t>& cap, const std::vector<uint64_t>& keys,
+              float inv_t) {
+    const int NP = plan.n_prompts, G = plan.group_size, S = NP * G, ML = plan.max_len;
+    Workspace& ws = P.ws;
+    int pmax = 0, maxcap = 0;
+    std::vector<int32_t> ptok, ppos, pstart{0}, plen(S), last_rows(S);
+    for (int p = 0; p < NP; ++p) {
+      const int64_t po = P.h_prompt_off[p];
+      const int m = static_cast<int>(P.h_prompt_off[p + 1] - po);
+      for (int i = 0; i < m; ++i) {
+        ptok.push_back(P.h_prompt_tok[po + i]);
+        ppos.push_back(i);
+      }
+      pstart.push_back(pstart.back() + m);
+      pmax = std::max(pmax, m);
+      for (int gg = 0; gg < G; ++gg) {
+        plen[p * G + gg] = m;
+        last_rows[p * G + gg] = pstart[p] + m - 1;
+      }
+    }
+    for (int s = 0; s < S; ++s) maxcap = std::max(maxcap, cap[s]);
+    int32_t* d_ptok = ws.get<int32_t>("s_ptok", ptok.size());
+    int32_t* d_ppos = ws.get<int32_t>("s_ppos", ppos.size());
+    int32_t* d_pstart = ws.get<int32_t>("s_pstart", pstart.size());
+    int32_t* d_plen = ws.get<int32_t>("s_plen", S);
+    int32_t* d_last = ws.get<int32_t>("s_last", S);
+    int32_t* d_cap = ws.get<int32_t>("s_cap", S);
+    uint64_t* d_keys = ws.get<uint64_t>("s_keys", S);
+    uint8_t* d_fin = ws.get<uint8_t>("s_fin", S);
+    int32_t* d_tok = ws.get<int32_t>("s_tok", S);
+    h2d(st, d_ptok, ptok.data(), ptok.size());
+    h2d(st, d_ppos, ppos.data(), ppos.size());
+    h2d(st, d_pstart, pstart.data(), pstart.size());
+    h2d(st, d_plen, plen.data(), S);
+    h2d(st, d_last, last_rows.data(), S);
+    h2d(st, d_cap, cap.data(), S);
+    h2d(st, d_keys, keys.data(), S);
+    DCU_CHECK(cudaMemsetAsync(d_fin, 0, S, st));
+    P.d_comp.ensure(sizeof(int32_t) * static_cast<size_t>(S) * std::max(ML, 1));
+    P.d_len.ensure(sizeof(int32_t) * S);
+    P.d_logp.ensure(sizeof(float) * static_cast<size_t>(S) * std::max(ML, 1));
+    DCU_CHECK(cudaMemsetAsync(P.d_comp.p, 0xff, sizeof(int32_t) * static_cast<size_t>(S) * std::max(ML, 1), st));
+    DCU_CHECK(cudaMemsetAsync(P.d_len.p, 0, sizeof(int32_t) * S, st));
+    DCU_CHECK(cudaMemsetAsync(P.d_logp.p, 0, sizeof(float) * static_cast<size_t>(S) * std::max(ML, 1), st));
+    float* dump = nullptr;
+    if (P.dump) {
+      P.dump_n = static_cast<int64_t>(S) * std::max(ML, 1) * g.V;
+      P.d_dump.ensure(sizeof(float) * P.dump_n);
+      DCU_CHECK(cudaMemsetAsync(P.d_dump.p, 0, sizeof(float) * P.dump_n, st));
+      dump = P.d_dump.as<float>();
+    }
+    if (maxcap == 0) return;
+
+    // KV stores: prompt part once per group, completion part per sequence.
+    const int cslots = std::max(ML - 1, 1);
+    const size_t kvp = static_cast<size_t>(NP) * g.nkv * pmax * g.hd;
+    const size_t kvc = static_cast<size_t>(S) * g.nkv * cslots * g.hd;
+    T* kp = ws.get<T>("kv_kp", kvp * g.L);
+    T* vp = ws.get<T>("kv_vp", kvp * g.L);
+    T* kc = ws.get<T>("kv_kc", kvc * g.L);
+    T* vc = ws.get<T>("kv_vc", kvc * g.L);
+
+    // Prefill (teacher-forced forward over the M prompts).
+    const int Tp = static_cast<int>(ptok.size());
+    Acts A = alloc_acts(ws, Tp, "p_");
+    forward(A, d_ptok, d_ppos, d_pstart, NP, pmax);
+    for (int l = 0; l < g.L; ++l)
+      kv_store_prompt<T>(st, A.qkv + static_cast<size_t>(Tp) * g.qkvd * l, d_pstart, NP, pmax, g.qd, g.kvd, g.nkv,
+                         g.hd, kp + kvp * l, vp + kvp * l);
+    T* yT = ws.get<T>("d_yT", static_cast<size_t>(S) * g.d);
+    gather_rows<T>(st, A.yT, g.d, d_last, S, g.d, yT);
+    float* logits = ws.get<float>("d_logits", static_cast<size_t>(S) * g.V);
+    Epi el = store(logits, g.V, nullptr, 0);
+    el.bias = W32(L.bout);
+    mm(S, g.V, g.d, yT, g.d, true, W(L.wout), g.d, true, el);
+    sample_rows(st, logits, S, g.V, g.bos, g.eos, inv_t, d_keys, 0, d_cap, d_fin, P.d_comp.as<int32_t>(),
+                P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML, dump);
+
+    // Decode steps.
+    float* x32 = ws.get<float>("d_x32", static_cast<size_t>(S) * g.d);
+    float* h32 = ws.get<float>("d_h32", static_cast<size_t>(S) * g.d);
+    T* xT = ws.get<T>("d_xT", static_cast<size_t>(S) * g.d);
+    T* hT = ws.get<T>("d_hT", static_cast<size_t>(S) * g.d);
+    T* qkv = ws.get<T>("d_qkv", static_cast<size_t>(S) * g.qkvd);
+    T* ctx = ws.get<T>("d_ctx", static_cast<size_t>(S) * g.qd);
+    T* u = ws.get<T>("d_u", static_cast<size_t>(S) * g.H);
+    std::vector<uint8_t> hfin(S);
+    for (int j = 1; j < maxcap; ++j) {
+      embed_decode<T>(st, W(L.tok), W(L.pos), d_tok, d_plen, j, S, g.d, x32, xT);
+      for (int l = 0; l < g.L; ++l) {
+        const int64_t b = lb(l);
+        mm(S, g.qkvd, g.d, xT, g.d, true, W(b + L.wq), g.d, true, store(nullptr, 0, qkv, g.qkvd));
+        kv_append<T>(st, qkv, S, g.qd, g.kvd, g.nkv, g.hd, j - 1, cslots, kc + kvc * l, vc + kvc * l);
+        attn_decode<T>(st, qkv, kp + kvp * l, vp + kvp * l, kc + kvc * l, vc + kvc * l, d_plen, S, G, pmax, j, cslots,
+                       g.nh, g.nkv, g.hd, ctx);
+        Epi eo = store(h32, g.d, hT, g.d);
+        eo.resid = x32;
+        eo.ldr = g.d;
+        mm(S, g.d, g.qd, ctx, g.qd, true, W(b + L.wo), g.qd, true, eo);
+        Epi e1 = store(nullptr, 0, u, g.H);
+        e1.kind = EPI_TANH;
+        e1.bias = W32(b + L.b1);
+        mm(S, g.H, g.d, hT, g.d, true, W(b + L.w1), g.d, true, e1);
+        Epi e2 = store(x32, g.d, xT, g.d);
+        e2.bias = W32(b + L.b2);
+        e2.resid = h32;
+        e2.ldr = g.d;
+        mm(S, g.d, g.H, u, g.H, true, W(b + L.w2), g.H, true, e2);
+      }
+      mm(S, g.V, g.d, xT, g.d, true, W(L.wout), g.d, true, el);
+      sample_rows(st, logits, S, g.V, g.bos, g.eos, inv_t, d_keys, j, d_cap, d_fin, P.d_comp.as<int32_t>(),
+                  P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML, dump);
+      if ((j & 31) == 0 && g.eos >= 0) {  // retire the round early once every sequence hit EOS
+        d2h(st, hfin.data(), d_fin, S);
+        DCU_CHECK(cudaStreamSynchronize(st));
+        bool all = true;
+        for (int s = 0; s < S && all; ++s) all = hfin[s] || j + 1 >= cap[s];
+        if (all) break;
+      }
+    }
+  }
+};
+
+// ------------------------------------------------------------------ helpers
+
+void check_policy(Pol* p) {
+  if (!p || !p->ctx) throw Error(1, "null policy handle");
+  DCU_CHECK(cudaSetDevice(p->ctx->device));
+}
+
+template <class F>
+void dispatch(Pol* p, F&& f) {
+  if (p->dtype == DASHCU_F32) {
+    Engine<float> e(*p);
+    f(e);
+  } else {
+    Engine<bf16> e(*p);
+    f(e);
+  }
+}
+
+void refresh_working_copy(Pol* p) {
+  if (p->dtype == DASHCU_BF16) cast_f32_bf16(p->ctx->stream, p->w32.as<float>(), p->wT.as<bf16>(), p->lay.total);
+}
+
+void validate_tokens(const Geo& g, const int32_t* t, int64_t n, bool completion) {
+  for (int64_t i = 0; i < n; ++i) {
+    if (t[i] < 0 || t[i] >= g.V) throw Error(1, "token out of vocab");
+    if (completion && t[i] == g.bos) throw Error(1, "completion contains BOS, which the policy never emits");
+  }
+}
+
+void set_prompts(Pol* p, const int32_t* tok, const int64_t* off, int NP) {
+  if (NP < 1) throw Error(1, "need at least one prompt");
+  if (!tok || !off) throw Error(1, "null prompt buffers");
+  if (off[0] != 0) throw Error(1, "prompt_offsets[0] must be 0");
+  for (int m = 0; m < NP; ++m) {
+    if (off[m + 1] <= off[m]) throw Error(1, "prompt must be nonempty");
+  }
+  validate_tokens(p->g, tok, off[NP], false);
+  p->h_prompt_tok.assign(tok, tok + off[NP]);
+  p->h_prompt_off.assign(off, off + NP + 1);
+}
+
+}  // namespace dashcu
+
+// ====================================================================== C ABI
+
+using namespace dashcu;
+
+#define API_BEGIN try {
+#define API_END                                   \
+  }                                               \
+  catch (const dashcu::Error& e) {                \
+    dashcu::g_last_error = e.what();              \
+    return e.code;                                \
+  }                                               \
+  catch (const std::exception& e) {               \
+    dashcu::g_last_error = e.what();              \
+    return DASHCU_E_DEVICE;                       \
+  }                                               \
+  return DASHCU_OK;
+
+extern "C" {
+
+const char* dashcu_last_error(void) { return dashcu::g_last_error.c_str(); }
+int dashcu_abi_version(void) { return 1; }
+int64_t dashcu_kernel_launches(void) { return dashcu::g_launches; }
+
+int dashcu_ctx_create(int device, dashcu_ctx** out) {
+  API_BEGIN
+  if (!out) throw Error(1, "null out");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) throw Error(4, "no CUDA device (libdashcu has no CPU fallback)");
+  if (device < 0 || device >= n) throw Error(1, "device index out of range");
+  cudaDeviceProp pr;
+  DCU_CHECK(cudaGetDeviceProperties(&pr, device));
+  if (pr.major != 10) throw Error(4, "libdashcu is built for sm_100a (B200); found sm_" + std::to_string(pr.major * 10 + pr.minor));
+  DCU_CHECK(cudaSetDevice(device));
+  auto* c = new dashcu_ctx;
+  c->device = device;
+  DCU_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  *out = c;
+  API_END
+}
+
+int dashcu_ctx_destroy(dashcu_ctx* c) {
+  API_BEGIN
+  if (!c) return 0;
+  cudaSetDevice(c->device);
+  if (c->comm && NcclApi::get().ok) NcclApi::get().CommDestroy(c->comm);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  API_END
+}
+
+int dashcu_ctx_sync(dashcu_ctx* c) {
+  API_BEGIN
+  if (!c) throw Error(1, "null ctx");
+  DCU_CHECK(cudaStreamSynchronize(c->stream));
+  API_END
+}
+
+int dashcu_comm_unique_id(uint8_t out[128]) {
+  API_BEGIN
+  NcclApi& n = NcclApi::get();
+  if (!n.ok) throw Error(4, "libnccl.so.2 not found");
+  ncclUniqueId id;
+  NCCL_CHECK(n.GetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  std::memcpy(out, &id, 128);
+  API_END
+}
+
+int dashcu_ctx_init_comm(dashcu_ctx* c, int world, int rank, const uint8_t id[128]) {
+  API_BEGIN
+  if (!c) throw Error(1, "null ctx");
+  if (world < 1 || rank < 0 || rank >= world) throw Error(1, "bad world/rank");
+  c->world = world;
+  c->rank = rank;
+  if (world == 1) return 0;
+  NcclApi& n = NcclApi::get();
+  if (!n.ok) throw Error(4, "libnccl.so.2 not found");
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, 128);
+  DCU_CHECK(cudaSetDevice(c->device));
+  NCCL_CHECK(n.CommInitRank(&c->comm, world, uid, rank));
+  API_END
+}
+
+int dashcu_arch_num_params(const dashcu_arch* a, int64_t* n) {
+  API_BEGIN
+  if (!a || !n) throw Error(1, "null argument");
+  validate_arch(*a);
+  *n = lay_of(geo_of(*a)).total;
+  API_END
+}
+
+int dashcu_policy_create(dashcu_ctx* c, const dashcu_arch* a, int dtype, dashcu_policy** out) {
+  API_BEGIN
+  if (!c || !a || !out) throw Error(1, "null argument");
+  if (dtype != DASHCU_F32 && dtype != DASHCU_BF16) throw Error(1, "dtype must be DASHCU_F32 or DASHCU_BF16");
+  validate_arch(*a);
+  DCU_CHECK(cudaSetDevice(c->device));
+  auto* p = new dashcu_policy;
+  p->ctx = c;
+  p->arch = *a;
+  p->g = geo_of(*a);
+  p->lay = lay_of(p->g);
+  p->dtype = dtype;
+  const size_t n = static_cast<size_t>(p->lay.total);
+  p->w32.ensure(n * 4);
+  p->g32.ensure(n * 4);
+  p->am.ensure(n * 4);
+  p->av.ensure(n * 4);
+  if (dtype == DASHCU_BF16) p->wT.ensure(n * 2);
+  DCU_CHECK(cudaMemsetAsync(p->w32.p, 0, n * 4, c->stream));
+  DCU_CHECK(cudaMemsetAsync(p->g32.p, 0, n * 4, c->stream));
+  DCU_CHECK(cudaMemsetAsync(p->am.p, 0, n * 4, c->stream));
+  DCU_CHECK(cudaMemsetAsync(p->av.p, 0, n * 4, c->stream));
+  refresh_working_copy(p);
+  DCU_CHECK(cudaStreamSynchronize(c->stream));
+  p->launches0 = g_launches;
+  *out = p;
+  API_END
+}
+
+int dashcu_policy_destroy(dashcu_policy* p) {
+  API_BEGIN
+  if (!p) return 0;
+  cudaSetDevice(p->ctx->device);
+  cudaStreamSynchronize(p->ctx->stream);
+  delete p;
+  API_END
+}
+
+int dashcu_policy_upload(dashcu_policy* p, const double* params, int64_t n) {
+  API_BEGIN
+  check_policy(p);
+  if (n != p->lay.total) throw Error(1, "parameter count mismatch");
+  double* st = p->ws.get<double>("staging64", n);
+  h2d(p->ctx->stream, st, params, n);
+  f64_to_f32(p->ctx->stream, st, p->w32.as<float>(), n);
+  refresh_working_copy(p);
+  DCU_CHECK(cudaStreamSynchronize(p->ctx->stream));
+  ++p->version;
+  API_END
+}
+
+int dashcu_policy_download(dashcu_policy* p, double* params, int64_t n) {
+  API_BEGIN
+  check_policy(p);
+  if (n != p->lay.total) throw Error(1, "parameter count mismatch");
+  double* st = p->ws.get<double>("staging64", n);
+  f32_to_f64(p->ctx->stream, p->w32.as<float>(), st, n);
+  d2h(p->ctx->stream, params, st, n);
+  DCU_CHECK(cudaStreamSynchronize(p->ctx->stream));
+  API_END
+}
+
+int dashcu_policy_init_normal(dashcu_policy* p, double scale, uint64_t seed) {
+  API_BEGIN
+  check_policy(p);
+  init_normal_ctr(p->ctx->stream, p->w32.as<float>(), p->lay.total, scale, seed);
+  refresh_working_copy(p);
+  DCU_CHECK(cudaStreamSynchronize(p->ctx->stream));
+  ++p->version;
+  API_END
+}
+
+int dashcu_policy_version(dashcu_policy* p, uint64_t* v) {
+  API_BEGIN
+  check_policy(p);
+  *v = p->version;
+  API_END
+}
+
+int dashcu_set_logits_dump(dashcu_policy* p, int enable) {
+  API_BEGIN
+  check_policy(p);
+  p->dump = enable != 0;
+  API_END
+}
+
+int dashcu_get_logits_dump(dashcu_policy* p, float* out, int64_t n) {
+  API_BEGIN
+  check_policy(p);
+  if (!p->dump || p->dump_n == 0) throw Error(1, "no logits dump recorded");
+  if (n < p->dump_n) throw Error(1, "dump buffer too small");
+  d2h(p->ctx->stream, out, p->d_dump.as<float>(), p->dump_n);
+  DCU_CHECK(cudaStreamSynchronize(p->ctx->stream));
+  API_END
+}
+
+int dashcu_sample(dashcu_policy* p, const dashcu_plan* plan, const int32_t* prompt_tokens,
+                  const int64_t* prompt_offsets, int32_t* completions, int32_t* lengths, float* logp) {
+  API_BEGIN
+  check_policy(p);
+  if (!plan) throw Error(1, "null plan");
+  // validation order follows sample() (policy.cpp:381-386)
+  if (!(plan->temperature > 0.0)) throw Error(1, "temperature must be positive");
+  if (plan->max_len < 0) throw Error(1, "max_len must be nonnegative");
+  if (plan->group_size < 1) throw Error(1, "group_size must be >= 1");
+  set_prompts(p, prompt_tokens, prompt_offsets, plan->n_prompts);
+  const int NP = plan->n_prompts, G = plan->group_size, S = NP * G;
+  std::vector<int32_t> cap(S);
+  std::vector<uint64_t> keys(S);
+  for (int m = 0; m < NP; ++m) {
+    const int len = static_cast<int>(prompt_offsets[m + 1] - prompt_offsets[m]);
+    if (len > p->g.ctx) throw Error(2, "prompt exceeds context window");
+    for (int gg = 0; gg < G; ++gg) {
+      cap[m * G + gg] = std::min(plan->max_len, p->g.ctx - len);
+      keys[m * G + gg] = derive_seed(plan->round_seed, "sample", static_cast<uint64_t>(plan->prompt_index_base + m),
+                                     static_cast<uint64_t>(gg));
+    }
+  }
+  p->n_prompts = NP;
+  p->G = G;
+  p->n_seq = S;
+  p->max_len = plan->max_len;
+  p->ro_valid = false;
+  p->adv_valid = false;
+  const float inv_t = static_cast<float>(1.0 / plan->temperature);
+  Timer tm(p->ctx->stream);
+  dispatch(p, [&](auto& e) { e.sample(*plan, cap, keys, inv_t); });
+  const size_t cells = static_cast<size_t>(S) * std::max(plan->max_len, 1);
+  p->h_comp.resize(cells);
+  p->h_len.resize(S);
+  d2h(p->ctx->stream, p->h_comp.data(), p->d_comp.as<int32_t>(), cells);
+  d2h(p->ctx->stream, p->h_len.data(), p->d_len.as<int32_t>(), S);
+  if (logp) d2h(p->ctx->stream, logp, p->d_logp.as<float>(), cells);
+  p->st.sample_ms = tm.stop_ms();
+  if (completions) std::memcpy(completions, p->h_comp.data(), cells * sizeof(int32_t));
+  if (lengths) std::memcpy(lengths, p->h_len.data(), S * sizeof(int32_t));
+  int64_t tokens = 0;
+  for (int s = 0; s < S; ++s) tokens += p->h_len[s];
+  p->st.tokens_sampled = tokens;
+  p->st.n_seq = S;
+  p->ro_version = p->version;
+  p->ro_valid = true;
+  API_END
+}
+
+int dashcu_rollout_load(dashcu_policy* p, const int32_t* prompt_tokens, const int64_t* prompt_offsets, int32_t NP,
+                        int32_t G, const int32_t* completions, const int64_t* coff) {
+  API_BEGIN
+  check_policy(p);
+  if (G < 1) throw Error(1, "group_size must be >= 1");
+  set_prompts(p, prompt_tokens, prompt_offsets, NP);
+  const int S = NP * G;
+  if (!coff || coff[0] != 0) throw Error(1, "completion_offsets[0] must be 0");
+  int ml = 0;
+  for (int s = 0; s < S; ++s) {
+    if (coff[s + 1] < coff[s]) throw Error(1, "completion offsets must be nondecreasing");
+    ml = std::max<int>(ml, static_cast<int>(coff[s + 1] - coff[s]));
+  }
+  // validate_traj (policy.cpp:191-197)
+  for (int s = 0; s < S; ++s) {
+    const int m = static_cast<int>(prompt_offsets[s / G + 1] - prompt_offsets[s / G]);
+    validate_tokens(p->g, completions + coff[s], coff[s + 1] - coff[s], true);
+    if (m + (coff[s + 1] - coff[s]) > p->g.ctx) throw Error(2, "prompt plus completion exceeds the context window");
+  }
+  p->n_prompts = NP;
+  p->G = G;
+  p->n_seq = S;
+  p->max_len = ml;
+  const size_t cells = static_cast<size_t>(S) * std::max(ml, 1);
+  p->h_comp.assign(cells, -1);
+  p->h_len.assign(S, 0);
+  for (int s = 0; s < S; ++s) {
+    p->h_len[s] = static_cast<int32_t>(coff[s + 1] - coff[s]);
+    for (int j = 0; j < p->h_len[s]; ++j) p->h_comp[static_cast<size_t>(s) * std::max(ml, 1) + j] = completions[coff[s] + j];
+  }
+  if (ml == 0) p->max_len = 1;
+  p->d_comp.ensure(cells * 4);
+  p->d_len.ensure(S * 4);
+  h2d(p->ctx->stream, p->d_comp.as<int32_t>(), p->h_comp.data(), cells);
+  h2d(p->ctx->stream, p->d_len.as<int32_t>(), p->h_len.data(), S);
+  DCU_CHECK(cudaStreamSynchronize(p->ctx->stream));
+  p->ro_version = p->version;
+  p->ro_valid = true;
+  p->adv_valid = false;
+  p->st.n_seq = S;
+  API_END
+}
+
+int dashcu_rollout_log_prob(dashcu_policy* p, float* per_token, int64_t n_tokens) {
+  API_BEGIN
+  check_policy(p);
+  if (!p->ro_valid) throw Error(1, "no rollout");
+  dispatch(p, [&](auto& e) { e.log_prob(per_token, n_tokens); });
+  API_END
+}
+
+int dashcu_advantage_filter(dashcu_ctx* c, const double* rewards, int32_t n, int32_t G, int32_t kind, int32_t normalize,
+                            double eps, double tau, double* adv, uint8_t* kept, int32_t* kept_idx, int32_t* n_kept) {
+  API_BEGIN
+  if (!c) throw Error(1, "null ctx");
+  // advantage.cpp:10-11, :68, :82, :100-101, :136
+  if (n <= 0) throw Error(1, "advantage of an empty batch");
+  if (kind < 0 || kind > 2) throw Error(1, "unknown advantage kind");
+  if (kind != DASHCU_ADV_SINGLE_PATH && (G <= 0 || n % G != 0))
+    throw Error(1, "contiguous grouping requires group_size dividing n");
+  if (kind == DASHCU_ADV_LEAVE_ONE_OUT && G < 2) throw Error(1, "leave-one-out needs every group size >= 2");
+  if (!(tau >= 0.0)) throw Error(1, "filter threshold must be >= 0");
+  DCU_CHECK(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  double* d_r = c->ws.get<double>("adv_r", n);
+  double* d_a = c->ws.get<double>("adv_a", n);
+  uint8_t* d_k = c->ws.get<uint8_t>("adv_k", n);
+  int32_t* d_i = c->ws.get<int32_t>("adv_i", n);
+  int32_t* d_n = c->ws.get<int32_t>("adv_n", 1);
+  h2d(s, d_r, rewards, n);
+  advantage_filter(s, d_r, n, G, kind, normalize, eps, tau, d_a, d_k, d_i, d_n);
+  int32_t nk = 0;
+  d2h(s, &nk, d_n, 1);
+  if (adv) d2h(s, adv, d_a, n);
+  if (kept) d2h(s, kept, d_k, n);
+  DCU_CHECK(cudaStreamSynchronize(s));
+  if (kept_idx) {
+    d2h(s, kept_idx, d_i, nk);
+    DCU_CHECK(cudaStreamSynchronize(s));
+  }
+  if (n_kept) *n_kept = nk;
+  API_END
+}
+
+int dashcu_rollout_set_rewards(dashcu_policy* p, const double* rewards, int32_t n) {
+  API_BEGIN
+  check_policy(p);
+  if (!p->ro_valid) throw Error(1, "no rollout");
+  if (n != p->n_seq) throw Error(1, "rewards and rollout disagree on batch size");
+  p->h_rewards.assign(rewards, rewards + n);
+  p->adv_valid = false;
+  API_END
+}
+
+int dashcu_rollout_advantage(dashcu_policy* p, int32_t kind, int32_t normalize, double eps, double tau, double* adv,
+                             uint8_t* kept, int32_t* n_kept) {
+  API_BEGIN
+  check_policy(p);
+  if (!p->ro_valid || static_cast<int>(p->h_rewards.size()) != p->n_seq) throw Error(1, "rollout has no rewards");
+  const int n = p->n_seq;
+  Timer tm(p->ctx->stream);
+  std::vector<uint8_t> k(n);
+  p->h_adv.resize(n);
+  p->h_kidx.resize(n);
+  int32_t nk = 0;
+  const int rc = dashcu_advantage_filter(p->ctx, p->h_rewards.data(), n, kind == 0 ? n : p->G, kind, normalize, eps,
+                                         tau, p->h_adv.data(), k.data(), p->h_kidx.data(), &nk);
+  if (rc) throw Error(rc, g_last_error);
+  p->h_kidx.resize(nk);
+  p->st.advantage_ms = tm.stop_ms();
+  double rs = 0, sa = 0;
+  for (int i = 0; i < n; ++i) rs += p->h_rewards[i];
+  for (int i : p->h_kidx) sa += std::fabs(p->h_adv[i]);
+  p->st.n_kept = nk;
+  p->st.mean_reward = rs / n;
+  p->st.filtered_fraction = 1.0 - static_cast<double>(nk) / n;
+  p->st.mean_abs_kept = nk ? sa / nk : 0.0;
+  if (adv) std::memcpy(adv, p->h_adv.data(), n * sizeof(double));
+  if (kept) std::memcpy(kept, k.data(), n);
+  if (n_kept) *n_kept = nk;
+  p->adv_valid = true;
+  API_END
+}
+
+int dashcu_grad_zero(dashcu_policy* p) {
+  API_BEGIN
+  check_policy(p);
+  DCU_CHECK(cudaMemsetAsync(p->g32.p, 0, p->lay.total * 4, p->ctx->stream));
+  DCU_CHECK(cudaStreamSynchronize(p->ctx->stream));
+  API_END
+}
+
+static void accumulate_impl(dashcu_policy* p, const std::vector<int>& seqs, const std::vector<double>& w, int micro) {
+  if (!p->ro_valid) throw Error(1, "no rollout");
+  if (p->ro_version != p->version)
+    throw Error(3, "policy changed since the rollout was sampled (on-policy PG needs theta == theta_old)");
+  Timer tm(p->ctx->stream);
+  int64_t lt = 0;
+  dispatch(p, [&](auto& e) { lt = e.accumulate(seqs, w, micro); });
+  p->st.accumulate_ms = tm.stop_ms();
+  p->st.loss_tokens = lt;
+}
+
+int dashcu_accumulate(dashcu_policy* p, double scale, int32_t micro) {
+  API_BEGIN
+  check_policy(p);
+  if (!p->adv_valid) throw Error(1, "call dashcu_rollout_advantage first");
+  std::vector<int> seqs(p->h_kidx.begin(), p->h_kidx.end());
+  std::vector<double> w(seqs.size());
+  for (size_t k = 0; k < seqs.size(); ++k) w[k] = p->h_adv[seqs[k]] * scale;
+  accumulate_impl(p, seqs, w, micro);
+  API_END
+}
+
+int dashcu_accumulate_weighted(dashcu_policy* p, const double* weights, int32_t n, int32_t micro) {
+  API_BEGIN
+  check_policy(p);
+  if (n != p->n_seq) throw Error(1, "weights and rollout disagree on batch size");
+  std::vector<int> seqs;
+  std::vector<double> w;
+  for (int s = 0; s < n; ++s)
+    if (weights[s] != 0.0) {
+      seqs.push_back(s);
+      w.push_back(weights[s]);
+    }
+  accumulate_impl(p, seqs, w, micro);
+  API_END
+}
+
+int dashcu_grad_download(dashcu_policy* p, double* grad, int64_t n) {
+  API_BEGIN
+  check_policy(p);
+  if (n != p->lay.total) throw Error(1, "parameter count mismatch");
+  double* st = p->ws.get<double>("staging64", n);
+  f32_to_f64(p->ctx->stream, p->g32.as<float>(), st, n);
+  d2h(p->ctx->stream, grad, st, n);
+  DCU_CHECK(cudaStreamSynchronize(p->ctx->stream));
+  API_END
+}
+
+int dashcu_allreduce_grads(dashcu_policy* p) {
+  API_BEGIN
+  check_policy(p);
+  dashcu_ctx* c = p->ctx;
+  Timer tm(c->stream);
+  if (c->world > 1) {
+    if (!c->comm) throw Error(4, "communicator not initialised (dashcu_ctx_init_comm)");
+    NCCL_CHECK(NcclApi::get().AllReduce(p->g32.p, p->g32.p, static_cast<size_t>(p->lay.total), ncclFloat32, ncclSum,
+                                        c->comm, c->stream));
+  }
+  p->st.allreduce_ms = tm.stop_ms();
+  API_END
+}
+
+int dashcu_optimizer_step(dashcu_policy* p, const dashcu_opt* o) {
+  API_BEGIN
+  check_policy(p);
+  if (!o) throw Error(1, "null optimizer config");
+  if (o->kind != DASHCU_OPT_SGD && o->kind != DASHCU_OPT_ADAM) throw Error(1, "unknown optimizer");
+  Timer tm(p->ctx->stream);
+  float c1 = 1.f, c2 = 1.f;
+  if (o->kind == DASHCU_OPT_ADAM) {
+    ++p->adam_t;
+    c1 = static_cast<float>(1.0 - std::pow(o->beta1, static_cast<double>(p->adam_t)));
+    c2 = static_cast<float>(1.0 - std::pow(o->beta2, static_cast<double>(p->adam_t)));
+  }
+  optimizer_update(p->ctx->stream, o->kind, p->w32.as<float>(), p->g32.as<float>(), p->am.as<float>(),
+                   p->av.as<float>(), p->dtype == DASHCU_BF16 ? p->wT.as<bf16>() : nullptr, p->lay.total,
+                   static_cast<float>(o->lr), static_cast<float>(o->beta1), static_cast<float>(o->beta2),
+                   static_cast<float>(o->eps), c1, c2);
+  p->st.optimizer_ms = tm.stop_ms();
+  ++p->version;
+  API_END
+}
+
+int dashcu_get_stats(dashcu_policy* p, dashcu_stats* out) {
+  API_BEGIN
+  check_policy(p);
+  *out = p->st;
+  out->kernel_launches = g_launches - p->launches0;
+  API_END
+}
+
+}  // extern "C"

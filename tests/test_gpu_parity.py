@@ -1,0 +1,324 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle on
+identical inputs and seeds.
+
+Standards (BASELINE.json north_star):
+  * integer / index work bit-exact: sampled token ids under a shared logits dump,
+    advantages, filter masks and compacted kept indices;
+  * floating point within tolerance: log-probs and gradients <= 1e-3 relative in
+    fp32 (DASHCU_F32) and <= 2e-2 in bf16 (DASHCU_BF16), relative error measured
+    norm-wise per parameter tensor (SURVEY App.B D9).
+Weights are rounded to fp32 before both sides see them, so the oracle and the
+device start from identical parameters.
+"""
+import numpy as np
+import pytest
+
+import oracle_ffi as O
+import paper_2505_17218_b200 as D
+
+pytestmark = pytest.mark.gpu
+
+C1 = dict(vocab_size=256, embed_dim=128, context_len=64, ffn_hidden=512, n_layers=2, bos_id=0, eos_id=1)
+SMALL = dict(vocab_size=37, embed_dim=32, context_len=40, ffn_hidden=48, n_layers=2, bos_id=0, eos_id=1)
+GQA = dict(vocab_size=64, embed_dim=64, context_len=48, ffn_hidden=128, n_layers=2, bos_id=0, eos_id=1,
+           n_heads=4, n_kv_heads=2, head_dim=16)
+TOL = {D.F32: 1e-3, D.BF16: 2e-2}
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return D.Context(0)
+
+
+def params32(arch, scale, seed):
+    return O.init_params(arch, scale, seed).astype(np.float32).astype(np.float64)
+
+
+def tensor_slices(arch):
+    """(name, slice) per parameter tensor in views() order."""
+    g = dict(arch)
+    nh, nkv = g.get("n_heads") or 1, g.get("n_kv_heads") or 1
+    hd = g.get("head_dim") or g["embed_dim"]
+    V, d, H = g["vocab_size"], g["embed_dim"], g["ffn_hidden"]
+    qd, kvd = nh * hd, nkv * hd
+    sizes = [("token_embed", V * d), ("pos_embed", g["context_len"] * d)]
+    for l in range(g["n_layers"]):
+        sizes += [(f"{l}.wq", qd * d), (f"{l}.wk", kvd * d), (f"{l}.wv", kvd * d), (f"{l}.wo", d * qd),
+                  (f"{l}.w1", H * d), (f"{l}.b1", H), (f"{l}.w2", d * H), (f"{l}.b2", d)]
+    sizes += [("w_out", V * d), ("b_out", V)]
+    out, off = [], 0
+    for n, s in sizes:
+        out.append((n, slice(off, off + s)))
+        off += s
+    return out
+
+
+def assert_grad_close(arch, got, ref, tol):
+    worst = []
+    for name, sl in tensor_slices(arch):
+        nr = np.linalg.norm(ref[sl])
+        if nr < 1e-12 * max(1.0, np.linalg.norm(ref)):
+            assert np.linalg.norm(got[sl]) <= 1e-6 * max(1.0, np.linalg.norm(ref)), name
+            continue
+        e = np.linalg.norm(got[sl] - ref[sl]) / nr
+        worst.append((e, name))
+    worst.sort(reverse=True)
+    assert worst[0][0] <= tol, worst[:3]
+
+
+def rand_batch(rng, arch, n_prompts, G, m_range=(2, 6), len_range=(0, 9)):
+    V = arch["vocab_size"]
+    prompts = [[arch["bos_id"]] + list(rng.integers(2, V, size=int(rng.integers(*m_range)) - 1))
+               for _ in range(n_prompts)]
+    comps = []
+    for p in prompts:
+        for _ in range(G):
+            n = int(rng.integers(*len_range))
+            c = list(rng.integers(2, V, size=n))
+            if n and rng.random() < 0.3:
+                c[-1] = arch["eos_id"]
+            comps.append(c)
+    return prompts, comps
+
+
+# ----------------------------------------------------------- advantage/filter
+
+def test_advantage_filter_bit_exact(ctx):
+    rng = np.random.default_rng(0)
+    for G in (1, 2, 4, 8, 10, 16):
+        for kind in (D.ADV_SINGLE_PATH, D.ADV_GROUP, D.ADV_LEAVE_ONE_OUT):
+            if kind == D.ADV_LEAVE_ONE_OUT and G < 2:
+                continue
+            for binary in (True, False):
+                r = rng.integers(0, 2, size=G * 33).astype(np.float64)
+                if not binary:
+                    r = rng.standard_normal(G * 33)
+                for tau in (0.0, 0.1, 0.125, float("inf")):
+                    for norm in (False, True):
+                        a, k, i = ctx.advantage_filter(r, G, kind, norm, 1e-6, tau)
+                        ra, rk, ri = O.advantage_filter(r, G, kind, norm, 1e-6, tau)
+                        assert np.array_equal(a, ra) and np.array_equal(k, rk) and np.array_equal(i, ri)
+
+
+def test_advantage_filter_large_and_errors(ctx):
+    r = np.random.default_rng(1).integers(0, 2, size=16384).astype(np.float64)
+    a, k, i = ctx.advantage_filter(r, 8, D.ADV_GROUP, False, 0, 0.1)
+    ra, rk, ri = O.advantage_filter(r, 8, 1, False, 0, 0.1)
+    assert np.array_equal(a, ra) and np.array_equal(k, rk) and np.array_equal(i, ri)
+    with pytest.raises(D.InputError):
+        ctx.advantage_filter([1.0, 0.0, 1.0], 2)
+    with pytest.raises(D.InputError):
+        ctx.advantage_filter([1.0, 0.0], 2, tau=-1.0)
+    with pytest.raises(D.InputError):
+        ctx.advantage_filter([1.0, 0.0], 1, kind=D.ADV_LEAVE_ONE_OUT)
+
+
+# ---------------------------------------------------------------- sampling
+
+@pytest.mark.parametrize("dtype", [D.F32, D.BF16])
+@pytest.mark.parametrize("arch", [C1, GQA], ids=["c1", "gqa"])
+def test_sampled_tokens_bit_exact_under_logits_dump(ctx, arch, dtype):
+    pol = D.Policy(ctx, arch, dtype)
+    pol.upload(params32(arch, 0.5, 3))
+    rng = np.random.default_rng(2)
+    prompts = [[0] + list(rng.integers(2, arch["vocab_size"], size=int(rng.integers(1, 7)))) for _ in range(5)]
+    G, ML, T = 4, 12, 0.7
+    pol.set_logits_dump(True)
+    ro = pol.sample(prompts, G, ML, temperature=T, round_seed=11, prompt_index_base=3)
+    dump = pol.logits_dump(len(prompts) * G, ML)
+    inv_t = float(np.float32(1.0 / T))
+    n_eos = 0
+    for s in range(len(prompts) * G):
+        m, g = s // G, s % G
+        key = O.derive_seed(11, "sample", 3 + m, g)
+        L = int(ro.lengths[s])
+        cap = min(ML, arch["context_len"] - len(prompts[m]))
+        assert 1 <= L <= cap
+        if L < cap:
+            assert ro.completions[s, L - 1] == arch["eos_id"]
+            n_eos += 1
+        for j in range(L):
+            tok = O.sample_rule(dump[s, j], arch["bos_id"], inv_t, key, j)
+            assert tok == ro.completions[s, j], (s, j)
+    pol.close()
+
+
+def test_sampling_logits_and_logp_match_oracle_f32(ctx):
+    arch = SMALL
+    pol = D.Policy(ctx, arch, D.F32)
+    p = params32(arch, 0.5, 5)
+    pol.upload(p)
+    prompts = [[0, 5, 9], [0, 7], [0, 3, 4, 8, 2]]
+    pol.set_logits_dump(True)
+    ro = pol.sample(prompts, 3, 10, temperature=1.0, round_seed=5)
+    dump = pol.logits_dump(9, 10)
+    for s in range(9):
+        pr = prompts[s // 3]
+        comp = list(ro.completion(s))
+        for j in range(len(comp)):
+            ref = O.next_logits(arch, p, pr + comp[:j])
+            assert np.max(np.abs(dump[s, j] - ref)) <= 1e-4 * max(1.0, np.max(np.abs(ref)))
+        _, per = O.log_prob(arch, p, pr, comp)
+        assert np.max(np.abs(ro.logp[s, :len(comp)] - per)) <= 1e-3 * max(1.0, np.max(np.abs(per)))
+    pol.close()
+
+
+def test_scheduling_independence(ctx):
+    # the sampled multiset does not depend on how prompts are split
+    # across workers (here: one call vs two shards with prompt_index_base).
+    arch = C1
+    pol = D.Policy(ctx, arch, D.F32)
+    pol.upload(params32(arch, 0.3, 1))
+    rng = np.random.default_rng(3)
+    prompts = [[0] + list(rng.integers(2, 256, size=6)) for _ in range(8)]
+    full = pol.sample(prompts, 4, 16, round_seed=9)
+    a = pol.sample(prompts[:3], 4, 16, round_seed=9, prompt_index_base=0)
+    b = pol.sample(prompts[3:], 4, 16, round_seed=9, prompt_index_base=3)
+    assert np.array_equal(full.completions, np.concatenate([a.completions, b.completions]))
+    assert np.array_equal(full.lengths, np.concatenate([a.lengths, b.lengths]))
+    pol.close()
+
+
+def test_sample_errors(ctx):
+    arch = SMALL
+    pol = D.Policy(ctx, arch, D.F32)
+    with pytest.raises(D.InputError):
+        pol.sample([[0, 2]], 2, 4, temperature=0.0)
+    with pytest.raises(D.InputError):
+        pol.sample([[0, 2]], 2, -1)
+    with pytest.raises(D.InputError):
+        pol.sample([[0, 99]], 2, 4)
+    with pytest.raises(D.CapacityError):
+        pol.sample([[0] + [2] * 40], 2, 4)
+    ro = pol.sample([[0] + [2] * 37], 2, 10)        # cap = ctx - m = 2
+    assert ro.lengths.max() <= 2
+    ro = pol.sample([[0, 2]], 2, 0)                 # max_len 0 -> empty completions
+    assert ro.lengths.max() == 0
+    pol.close()
+
+
+# --------------------------------------------------------------- log_prob
+
+@pytest.mark.parametrize("dtype", [D.F32, D.BF16])
+@pytest.mark.parametrize("arch", [SMALL, GQA, C1], ids=["small", "gqa", "c1"])
+def test_teacher_forced_log_prob(ctx, arch, dtype):
+    pol = D.Policy(ctx, arch, dtype)
+    p = params32(arch, 0.3, 7)
+    pol.upload(p)
+    prompts, comps = rand_batch(np.random.default_rng(4), arch, 4, 3)
+    pol.load_rollout(prompts, 3, comps)
+    n_tok = sum(len(c) for c in comps)
+    lp = pol.rollout_log_prob(n_tok)
+    ref = np.concatenate([O.log_prob(arch, p, prompts[s // 3], comps[s])[1] for s in range(12)] + [np.zeros(0)])
+    err = np.abs(lp - ref).max() if n_tok else 0.0
+    assert err <= TOL[dtype] * max(1.0, np.abs(ref).max())
+    pol.close()
+
+
+# ----------------------------------------------------------------- gradients
+
+@pytest.mark.parametrize("dtype", [D.F32, D.BF16])
+@pytest.mark.parametrize("arch", [SMALL, GQA, C1], ids=["small", "gqa", "c1"])
+def test_pg_gradient_parity(ctx, arch, dtype):
+    pol = D.Policy(ctx, arch, dtype)
+    p = params32(arch, 0.3, 8)
+    pol.upload(p)
+    rng = np.random.default_rng(5)
+    prompts, comps = rand_batch(rng, arch, 4, 4)
+    pol.load_rollout(prompts, 4, comps)
+    w = rng.standard_normal(16) / 16
+    w[rng.random(16) < 0.25] = 0.0
+    pol.grad_zero()
+    pol.accumulate_weighted(w, micro_batch=5)
+    got = pol.grad()
+    ref = np.zeros_like(got)
+    for s in range(16):
+        O.grad_log_prob(arch, p, prompts[s // 4], comps[s], w[s], ref)
+    assert_grad_close(arch, got, ref, TOL[dtype])
+    pol.close()
+
+
+def test_microbatch_invariance_and_filter_equivalence(ctx):
+    arch = GQA
+    pol = D.Policy(ctx, arch, D.F32)
+    pol.upload(params32(arch, 0.3, 9))
+    rng = np.random.default_rng(6)
+    prompts, comps = rand_batch(rng, arch, 6, 4, len_range=(1, 9))
+    pol.load_rollout(prompts, 4, comps)
+    r = rng.integers(0, 2, size=24).astype(np.float64)
+    pol.set_rewards(r)
+    adv, kept, nk = pol.advantage(tau=0.1)
+    ra, rk, _ = O.advantage_filter(r, 4, 1, False, 0.0, 0.1)
+    assert np.array_equal(adv, ra) and np.array_equal(kept, rk)
+    pol.grad_zero()
+    pol.accumulate(1.0 / 24, micro_batch=1)
+    g1 = pol.grad()
+    pol.grad_zero()
+    pol.accumulate(1.0 / 24, micro_batch=0)
+    g2 = pol.grad()
+    pol.grad_zero()
+    pol.accumulate_weighted(np.where(kept, adv, 0.0) / 24, micro_batch=7)   # zeroed-A full batch
+    g3 = pol.grad()
+    assert np.linalg.norm(g1 - g2) <= 1e-5 * np.linalg.norm(g2)
+    assert np.linalg.norm(g3 - g2) <= 1e-5 * np.linalg.norm(g2)
+    pol.close()
+
+
+def test_on_policy_violation_and_optimizer(ctx):
+    arch = SMALL
+    pol = D.Policy(ctx, arch, D.F32)
+    p = params32(arch, 0.3, 10)
+    pol.upload(p)
+    prompts, comps = rand_batch(np.random.default_rng(7), arch, 2, 2, len_range=(1, 5))
+    pol.load_rollout(prompts, 2, comps)
+    w = np.array([0.5, -0.25, 0.125, 1.0])
+    pol.grad_zero()
+    pol.accumulate_weighted(w)
+    g = pol.grad()
+    pol.optimizer_step(D.OPT_ADAM, lr=1e-2)
+    got = pol.download()
+    ref = p.copy()
+    m = np.zeros_like(p)
+    v = np.zeros_like(p)
+    O.oracle().dor_adam_step(O.ptr(ref, O.f64p), O.ptr(g, O.f64p), O.ptr(m, O.f64p), O.ptr(v, O.f64p), len(p), 1,
+                             1e-2, 0.9, 0.999, 1e-8)
+    assert np.max(np.abs(got - ref)) <= 1e-6
+    with pytest.raises(D.OnPolicyViolation):
+        pol.accumulate_weighted(w)
+    with pytest.raises(D.InputError):
+        pol.load_rollout([[0, 2]], 1, [[0]])          # BOS in completion
+    with pytest.raises(D.CapacityError):
+        pol.load_rollout([[0, 2]], 1, [[3] * 39])     # m + len > ctx
+    pol.close()
+
+
+# ------------------------------------------------------------ one DASH step
+
+@pytest.mark.parametrize("dtype", [D.F32, D.BF16])
+def test_dash_step_c1_matches_oracle(ctx, dtype):
+    """Config 1 shape: sample -> rewards -> group advantage + filter -> PG accumulate
+    -> Adam, with the gradient checked against the oracle on the GPU's own rollout."""
+    arch = C1
+    pol = D.Policy(ctx, arch, dtype)
+    p = params32(arch, 0.02, 1)
+    pol.upload(p)
+    M, G, ML = 16, 8, 20
+    prompts = [list(O.synthetic_prompt(1, m, 7, 256, 0, 1)) for m in range(M)]
+    ro = pol.sample(prompts, G, ML, round_seed=7)
+    r = np.array([O.synthetic_reward(3, m, g) for m in range(M) for g in range(G)])
+    pol.set_rewards(r)
+    adv, kept, nk = pol.advantage(tau=0.1)
+    ra, rk, ri = O.advantage_filter(r, G, 1, False, 0.0, 0.1)
+    assert np.array_equal(adv, ra) and np.array_equal(kept, rk) and nk == len(ri)
+    pol.grad_zero()
+    pol.accumulate(1.0 / (M * G), micro_batch=32)
+    got = pol.grad()
+    ref = np.zeros_like(got)
+    for s in ri:
+        O.grad_log_prob(arch, p, prompts[s // G], list(ro.completion(s)), adv[s] / (M * G), ref)
+    assert_grad_close(arch, got, ref, TOL[dtype])
+    st = pol.stats()
+    assert st["n_kept"] == nk and st["tokens_sampled"] == int(ro.lengths.sum())
+    pol.optimizer_step(D.OPT_ADAM, lr=1e-3)
+    assert pol.version() > 0
+    pol.close()
