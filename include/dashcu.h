@@ -179,6 +179,15 @@ DASHCU_API int dashcu_allreduce_grads(dashcu_policy* pol);
 DASHCU_API int dashcu_optimizer_step(dashcu_policy* pol, const dashcu_opt* opt);
 
 DASHCU_API int dashcu_get_stats(dashcu_policy* pol, dashcu_stats* out);
+
+/* ---- diagnostics (used by the kernel tests) ----
+ * C[M x N] (fp32, ldc = N) = A(m,k) . B(n,k) on bf16 operands given as raw
+ * bit patterns, through the production GEMM dispatcher (tcgen05 when the
+ * operands are TMA-legal) or, with force_simt, the CUDA-core kernel.
+ * epi: 0 store, 1 tanh(acc + bias), 3 C += acc (C is read first). */
+DASHCU_API int dashcu_selftest_gemm(dashcu_ctx* ctx, int M, int N, int K, const uint16_t* A, int64_t lda,
+                                    int a_kmajor, const uint16_t* B, int64_t ldb, int b_kmajor, const float* bias,
+                                    int epi, int force_simt, float* C);
 /* Whole-library count of kernel launches (all policies, all contexts). */
 DASHCU_API int64_t dashcu_kernel_launches(void);
 

@@ -128,6 +128,8 @@ def lib():
             "dashcu_allreduce_grads": [vp],
             "dashcu_optimizer_step": [vp, C.POINTER(Opt)],
             "dashcu_get_stats": [vp, C.POINTER(Stats)],
+            "dashcu_selftest_gemm": [vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint16), C.c_int64, C.c_int,
+                                     C.POINTER(C.c_uint16), C.c_int64, C.c_int, f32p, C.c_int, C.c_int, f32p],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -188,6 +190,19 @@ class Context:
         _check(lib().dashcu_advantage_filter(self.h, _p(r, f64p), n, group_size, kind, int(normalize), eps, tau,
                                              _p(adv, f64p), _p(kept, u8p), _p(idx, i32p), C.byref(nk)))
         return adv[:n], kept[:n].astype(bool), idx[:nk.value].copy()
+
+    def selftest_gemm(self, A_bits, a_kmajor, B_bits, b_kmajor, M, N, K, bias=None, epi=0, force_simt=False,
+                      C_init=None):
+        """Diagnostics: C = A(m,k).B(n,k) on bf16 bit patterns (uint16) via the production dispatcher."""
+        A = np.ascontiguousarray(A_bits, dtype=np.uint16)
+        B = np.ascontiguousarray(B_bits, dtype=np.uint16)
+        out = np.zeros((M, N), dtype=np.float32) if C_init is None else np.ascontiguousarray(C_init, np.float32).copy()
+        b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float32)
+        u16p = C.POINTER(C.c_uint16)
+        _check(lib().dashcu_selftest_gemm(self.h, M, N, K, A.ctypes.data_as(u16p), A.shape[1], int(a_kmajor),
+                                          B.ctypes.data_as(u16p), B.shape[1], int(b_kmajor),
+                                          None if b is None else _p(b, f32p), epi, int(force_simt), _p(out, f32p)))
+        return out
 
     def close(self):
         if self.h:

@@ -350,7 +350,10 @@ __global__ void advantage_k(const double* r, int n, int G, int kind, int normali
       for (int i = s; i < s + gs; ++i) mean += r[i];
       mean /= static_cast<double>(gs);
       double var = 0.0;
-      for (int i = s; i < s + gs; ++i) var += (r[i] - mean) * (r[i] - mean);
+      for (int i = s; i < s + gs; ++i) {
+        const double dv = __dsub_rn(r[i], mean);
+        var = __dadd_rn(var, __dmul_rn(dv, dv));  // no FMA contraction: bit-equal to the reference
+      }
       var /= static_cast<double>(gs);
       const double den = sqrt(var) + eps;
       for (int i = s; i < s + gs; ++i) adv[i] = adv[i] / den;

@@ -219,6 +219,8 @@ struct dashcu_ctx {
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
   int world = 1, rank = 0;
+  int refs = 0;         // live policies bound to this context
+  bool closed = false;  // dashcu_ctx_destroy called; freed when refs reaches 0
   dashcu::Workspace ws;
 };
 
@@ -778,13 +780,19 @@ int dashcu_ctx_create(int device, dashcu_ctx** out) {
   API_END
 }
 
+static void ctx_free(dashcu_ctx* c) {
+  cudaSetDevice(c->device);
+  if (c->comm && NcclApi::get().ok) NcclApi::get().CommDestroy(c->comm);
+  c->ws.bufs.clear();
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
 int dashcu_ctx_destroy(dashcu_ctx* c) {
   API_BEGIN
   if (!c) return 0;
-  cudaSetDevice(c->device);
-  if (c->comm && NcclApi::get().ok) NcclApi::get().CommDestroy(c->comm);
-  if (c->stream) cudaStreamDestroy(c->stream);
-  delete c;
+  c->closed = true;
+  if (c->refs == 0) ctx_free(c);
   API_END
 }
 
@@ -855,6 +863,7 @@ int dashcu_policy_create(dashcu_ctx* c, const dashcu_arch* a, int dtype, dashcu_
   refresh_working_copy(p);
   DCU_CHECK(cudaStreamSynchronize(c->stream));
   p->launches0 = g_launches;
+  ++c->refs;
   *out = p;
   API_END
 }
@@ -862,9 +871,11 @@ int dashcu_policy_create(dashcu_ctx* c, const dashcu_arch* a, int dtype, dashcu_
 int dashcu_policy_destroy(dashcu_policy* p) {
   API_BEGIN
   if (!p) return 0;
-  cudaSetDevice(p->ctx->device);
-  cudaStreamSynchronize(p->ctx->stream);
+  dashcu_ctx* c = p->ctx;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
   delete p;
+  if (--c->refs == 0 && c->closed) ctx_free(c);
   API_END
 }
 
@@ -1195,6 +1206,36 @@ int dashcu_get_stats(dashcu_policy* p, dashcu_stats* out) {
   check_policy(p);
   *out = p->st;
   out->kernel_launches = g_launches - p->launches0;
+  API_END
+}
+
+int dashcu_selftest_gemm(dashcu_ctx* c, int M, int N, int K, const uint16_t* A, int64_t lda, int a_kmajor,
+                         const uint16_t* B, int64_t ldb, int b_kmajor, const float* bias, int epi, int force_simt,
+                         float* Cout) {
+  API_BEGIN
+  if (!c) throw Error(1, "null ctx");
+  if (M <= 0 || N <= 0 || K < 0) throw Error(1, "bad shape");
+  DCU_CHECK(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  const size_t na = static_cast<size_t>(a_kmajor ? M : K) * lda, nb = static_cast<size_t>(b_kmajor ? N : K) * ldb;
+  uint16_t* dA = c->ws.get<uint16_t>("t_A", na);
+  uint16_t* dB = c->ws.get<uint16_t>("t_B", nb);
+  float* dC = c->ws.get<float>("t_C", static_cast<size_t>(M) * N);
+  float* dbias = c->ws.get<float>("t_bias", N);
+  h2d(s, dA, A, na);
+  h2d(s, dB, B, nb);
+  if (bias) h2d(s, dbias, bias, N);
+  h2d(s, dC, Cout, static_cast<size_t>(M) * N);
+  GemmShape g{M, N, K, dA, lda, a_kmajor != 0, dB, ldb, b_kmajor != 0};
+  Epi e;
+  e.kind = epi;
+  e.c32 = dC;
+  e.ldc32 = N;
+  e.bias = bias ? dbias : nullptr;
+  if (force_simt) gemm_simt<bf16>(s, g, e);
+  else gemm(s, 1, g, e);
+  d2h(s, Cout, dC, static_cast<size_t>(M) * N);
+  DCU_CHECK(cudaStreamSynchronize(s));
   API_END
 }
 

@@ -1,0 +1,74 @@
+"""tcgen05 GEMM kernel against a plain fp32 reference of the same op (bf16 operands
+rounded identically on both sides), for every operand major-ness the DASH step
+uses: (K,K) forward projections, (K,MN) input gradients, (MN,MN) weight gradients."""
+import numpy as np
+import pytest
+
+import paper_2505_17218_b200 as D
+
+pytestmark = pytest.mark.gpu
+
+
+def bf16_bits(x: np.ndarray) -> np.ndarray:
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    return r
+
+
+def bits_to_f32(b: np.ndarray) -> np.ndarray:
+    return (b.astype(np.uint32) << 16).view(np.float32)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return D.Context(0)
+
+
+SHAPES = [(128, 128, 64), (256, 384, 128), (200, 136, 72), (77, 300, 1000), (1024, 896, 896), (36, 1152, 896),
+          (896, 4864, 517)]
+
+
+@pytest.mark.parametrize("ak", [True, False])
+@pytest.mark.parametrize("bk", [True, False])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_tc_gemm_matches_fp32_reference(ctx, ak, bk, shape):
+    M, N, K = shape
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    A = bf16_bits(rng.standard_normal((M, K)).astype(np.float32))
+    B = bf16_bits(rng.standard_normal((N, K)).astype(np.float32))
+    ref = bits_to_f32(A).astype(np.float64) @ bits_to_f32(B).astype(np.float64).T
+    Ast = A if ak else np.ascontiguousarray(A.T)
+    Bst = B if bk else np.ascontiguousarray(B.T)
+    # strides must be 16-byte multiples for TMA; pad the leading dimension when needed
+    def pad(x):
+        cols = x.shape[1]
+        p = (-cols) % 8
+        return np.pad(x, ((0, 0), (0, p))) if p else x
+    Ast, Bst = pad(Ast), pad(Bst)
+    got = ctx.selftest_gemm(Ast, ak, Bst, bk, M, N, K)
+    err = np.abs(got - ref).max() / max(1.0, np.abs(ref).max())
+    assert err < 1e-5, err
+
+
+def test_tc_gemm_epilogues(ctx):
+    M, N, K = 192, 256, 320
+    rng = np.random.default_rng(0)
+    A = bf16_bits(rng.standard_normal((M, K)).astype(np.float32) * 0.1)
+    B = bf16_bits(rng.standard_normal((N, K)).astype(np.float32) * 0.1)
+    bias = rng.standard_normal(N).astype(np.float32)
+    ref = bits_to_f32(A).astype(np.float64) @ bits_to_f32(B).astype(np.float64).T
+    got = ctx.selftest_gemm(A, True, B, True, M, N, K, bias=bias, epi=1)
+    assert np.abs(got - np.tanh(ref + bias)).max() < 1e-5
+    c0 = rng.standard_normal((M, N)).astype(np.float32)
+    got = ctx.selftest_gemm(A, True, B, True, M, N, K, epi=3, C_init=c0)
+    assert np.abs(got - (c0 + ref)).max() < 1e-4
+
+
+def test_tc_matches_simt(ctx):
+    M, N, K = 300, 500, 260
+    rng = np.random.default_rng(1)
+    A = bf16_bits(rng.standard_normal((M, K)).astype(np.float32))
+    B = bf16_bits(rng.standard_normal((K, N)).astype(np.float32))
+    a = ctx.selftest_gemm(A, True, B, False, M, N, K)
+    b = ctx.selftest_gemm(A, True, B, False, M, N, K, force_simt=True)
+    assert np.abs(a - b).max() <= 1e-4 * np.abs(b).max()

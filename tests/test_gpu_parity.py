@@ -31,7 +31,11 @@ def ctx():
 
 
 def params32(arch, scale, seed):
-    return O.init_params(arch, scale, seed).astype(np.float32).astype(np.float64)
+    """Weights rounded to fp32. `scale` is relative: N(0, (scale / sqrt(d))^2) keeps the
+    residual stream O(1) so the attention softmax is not saturated (a saturated softmax
+    makes fp32/bf16-vs-fp64 gradient comparisons meaningless, not wrong)."""
+    sc = scale / np.sqrt(arch["embed_dim"]) if scale > 0.05 else scale
+    return O.init_params(arch, sc, seed).astype(np.float32).astype(np.float64)
 
 
 def tensor_slices(arch):

@@ -380,3 +380,16 @@ def test_synthetic_workload_shapes():
     rs = np.array([O.synthetic_reward(1, m, g) for m in range(400) for g in range(8)]).reshape(400, 8)
     uniform = np.mean([(row.min() == row.max()) for row in rs])
     assert abs(uniform - 2 / 9) < 0.07      # E[p^G + (1-p)^G] = 2/(G+1)
+
+
+def test_workload_restatement_matches_oracle():
+    from paper_2505_17218_b200 import workload as W
+    P = W.synthetic_prompts(5, 10, 14, 128, 151936, 0, 1)
+    for i, m in enumerate(range(10, 14)):
+        assert np.array_equal(P[i], O.synthetic_prompt(5, m, 128, 151936, 0, 1))
+    P = W.synthetic_prompts(9, 0, 3, 9, 40, 5, 2)
+    for m in range(3):
+        assert np.array_equal(P[m], O.synthetic_prompt(9, m, 9, 40, 5, 2))
+    R = W.synthetic_rewards(3, 7, 20, 8)
+    assert np.array_equal(R, [O.synthetic_reward(3, m, g) for m in range(7, 20) for g in range(8)])
+    assert int(W.derive_seed(1, "sample", 2, 3)) == 3124241217676271300
