@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""DASH training-step benchmark (BASELINE.json metric) on 1..8 B200.
+
+One step = the DASH hot path over one synthetic round:
+  preemptive_sample (M prompts x G)  -> synthetic rewards -> group advantage + |A|
+  filter -> micro-batched PG accumulate (fp32 grads) -> NCCL allreduce -> Adam.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Default workload = BASELINE configs[1] (Qwen2.5-0.5B-shaped random-init policy,
+512 prompts x G=8, gen len 1024, one B200), weak-scaled: every rank samples its
+own 512-prompt shard of one global round (keys derive_seed(round, "sample", m, g)),
+one allreduce per optimizer step.
+
+Reported:
+  value     whole-job sampled tokens / s, device-timed (sum of the library's CUDA-
+            event phase timers on its stream), max over ranks
+  e2e       same metric through the C ABI with host buffers: wall clock around the
+            API calls (prompts H2D, completions/logp/advantages D2H), max over ranks
+  roofline  dominant kernel class: algorithmic flops (bytes) / its CUDA-event time
+  cpu_baseline  the reference's own CPU DASH step (oracle/_ref) on a bounded sample
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2505_17218_b200 import workload as W  # noqa: E402
+
+CONFIGS = {
+    "c2": dict(size="0.5b", prompts=512, G=8, prompt_len=128, max_len=1024, micro=32, tau=0.1,
+               workload="BASELINE configs[1]: Qwen2.5-0.5B-shaped random-init policy, 512 prompts x G=8, "
+                        "gen len 1024, per B200"),
+    "c3": dict(size="1.5b", prompts=256, G=8, prompt_len=128, max_len=1024, micro=32, tau=0.1,
+               workload="BASELINE configs[2] shard: Qwen2.5-1.5B-shaped, 2048 prompts x G=8 over 8 B200 "
+                        "(256 prompts per B200), micro-batch 32"),
+    "mini": dict(size="0.5b", prompts=64, G=8, prompt_len=128, max_len=128, micro=32, tau=0.1,
+                 workload="development: Qwen2.5-0.5B-shaped, 64 prompts x G=8, gen len 128"),
+    "c1": dict(size=None, prompts=64, G=8, prompt_len=7, max_len=57, micro=32, tau=0.1,
+               workload="BASELINE configs[0]: SPEC tiny policy (2 layers, d=128, byte vocab), 64 prompts x G=8"),
+}
+C1_ARCH = dict(vocab_size=256, embed_dim=128, context_len=64, ffn_hidden=512, n_layers=2, bos_id=0, eos_id=1)
+# bounded CPU sample of the same workload for the reference arm / cpu_baseline
+REF_SAMPLE = dict(prompts=1, G=8, prompt_len=4, max_len=4)
+
+
+def arch_of(cfg):
+    if cfg["size"] is None:
+        return dict(C1_ARCH)
+    return W.qwen_arch(cfg["size"], cfg["prompt_len"] + cfg["max_len"])
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return dict(hbm=float(d["hbm_gbs"]), tc=float(d["bf16_tflops"]), tc_sus=float(d["bf16_tflops_sustained"]),
+                    src="measured")
+    except Exception:
+        return dict(hbm=6650.0, tc=1590.0, tc_sus=1400.0, src="fallback")
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu: int):
+        self.gpu, self.proc, self.path = gpu, None, f"/tmp/dash_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        load = [s for s in sm if mx and s > 0.3 * mx] or sm
+        return {"sm_mhz": float(np.median(load)) if load else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    return world, rank, local
+
+
+def allreduce(vals, op):
+    """max / sum over ranks of a small list of floats (torch.distributed plumbing)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        return list(vals)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return t.cpu().tolist()
+
+
+def barrier():
+    import torch.distributed as dist
+    if dist.is_initialized():
+        dist.barrier()
+
+
+def pinned(shape, dtype):
+    try:
+        import torch
+        if torch.cuda.is_available():
+            tdt = {np.int32: torch.int32, np.int64: torch.int64, np.float32: torch.float32,
+                   np.float64: torch.float64}[dtype]
+            return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+    except Exception:
+        pass
+    return np.empty(shape, dtype=dtype)
+
+
+# --------------------------------------------------------------- reference arm
+
+def ref_step_runner(cfg, threads):
+    """The reference's own CPU DASH step (oracle/_ref ref_dash_step) on a bounded sample."""
+    import ctypes as C
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_ffi as O
+    arch = arch_of(cfg)
+    for k in ("n_heads", "n_kv_heads", "head_dim"):   # the reference is single-head (policy.cpp:93-129)
+        arch.pop(k, None)
+    rs = REF_SAMPLE if cfg["size"] else dict(prompts=cfg["prompts"], G=cfg["G"], prompt_len=cfg["prompt_len"],
+                                               max_len=cfg["max_len"])
+    arch["context_len"] = max(arch["context_len"], rs["prompt_len"] + rs["max_len"])
+    n = O.num_params(arch)
+    params = (np.random.default_rng(1).standard_normal(n, dtype=np.float32) * 0.02).astype(np.float64)
+    m = np.zeros(n)
+    v = np.zeros(n)
+    t = C.c_int64(0)
+    P = W.synthetic_prompts(1, 0, rs["prompts"], rs["prompt_len"], arch["vocab_size"], arch["bos_id"],
+                            arch["eos_id"])
+    toks = np.ascontiguousarray(P.reshape(-1))
+    off = (np.arange(rs["prompts"] + 1) * rs["prompt_len"]).astype(np.int64)
+    R = O.ref()
+    sample = (f"{rs['prompts']} prompt(s) x G={rs['G']}, prompt {rs['prompt_len']} tok, max_len {rs['max_len']} "
+              f"of the {cfg['size'] or 'tiny'} workload (reference single-head geometry), full DASH step "
+              f"(sample, reward, group adv+filter, sum A/N grad_log_prob, Adam), {threads} threads")
+
+    def run(step):
+        st = O.RefStepStats()
+        rc = R.ref_dash_step(O.arch_ref_vec(arch), O.ptr(params, O.f64p), O.ptr(toks, O.i32p), O.ptr(off, O.i64p),
+                             rs["prompts"], rs["G"], rs["max_len"], 1.0, 1000 + step, 0, 0, 3, None, cfg["tau"], 1,
+                             1e-6, O.ptr(m, O.f64p), O.ptr(v, O.f64p), C.byref(t), threads, C.byref(st))
+        if rc != 0:
+            raise RuntimeError("reference step failed")
+        return st.tokens_sampled, st.total_s
+    return run, sample
+
+
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    run, sample = ref_step_runner(cfg, threads)
+    for i in range(min(args.warmup, 1)):
+        run(i)
+    toks, secs = 0, 0.0
+    for i in range(args.steps):
+        a, b = run(100 + i)
+        toks += a
+        secs += b
+    val = toks / secs
+    line = {"metric": "dash_step_sampled_tokens_per_s", "value": val, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": 1000 * secs / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": cfg["workload"], "parallelism": "host threads"},
+            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- our arm
+
+def run_ours(args, cfg, world, rank, local):
+    import paper_2505_17218_b200 as D
+    arch = arch_of(cfg)
+    M, G, ML = cfg["prompts"], cfg["G"], cfg["max_len"]
+    ctx = D.Context(local)
+    if world > 1:
+        import torch.distributed as dist
+        obj = [D.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.init_comm(world, rank, obj[0])
+    pol = D.Policy(ctx, arch, D.BF16)
+    pol.init_normal(0.02, 1)
+    base = rank * M
+    P = W.synthetic_prompts(1, base, base + M, cfg["prompt_len"], arch["vocab_size"], 0, 1)
+    ptok = pinned(P.size, np.int32)
+    ptok[:] = P.reshape(-1)
+    poff = pinned(M + 1, np.int64)
+    poff[:] = np.arange(M + 1) * cfg["prompt_len"]
+    S = M * G
+    outs = (pinned((S, max(ML, 1)), np.int32), pinned(S, np.int32), pinned((S, max(ML, 1)), np.float32))
+    N_global = M * G * world
+
+    def step(i):
+        t0 = time.perf_counter()
+        ro = pol.sample(None, G, ML, 1.0, round_seed=i, prompt_index_base=base, prompt_tokens=ptok,
+                        prompt_offsets=poff, outputs=outs)
+        r = W.synthetic_rewards(2 + i, base, base + M, G)
+        pol.set_rewards(r)
+        adv, kept, nk = pol.advantage(tau=cfg["tau"])
+        pol.grad_zero()
+        pol.accumulate(1.0 / N_global, cfg["micro"])
+        pol.allreduce_grads()
+        pol.optimizer_step(D.OPT_ADAM, lr=1e-6)
+        st = pol.stats()
+        wall = time.perf_counter() - t0
+        dev = st["sample_ms"] + st["advantage_ms"] + st["accumulate_ms"] + st["allreduce_ms"] + st["optimizer_ms"]
+        return int(ro.lengths.sum()), dev, wall * 1e3, st
+
+    for i in range(args.warmup):
+        step(i)
+    barrier()
+    ctx.sync()
+    clocks = Clocks(local)
+    clocks.start()
+    D.profile_enable()
+    D.profile_read(reset=True)
+    l0 = D.kernel_launches()
+    toks, dev_ms, wall_ms, last = 0, 0.0, 0.0, None
+    for i in range(args.steps):
+        a, b, c, last = step(args.warmup + i)
+        toks += a
+        dev_ms += b
+        wall_ms += c
+    ctx.sync()
+    barrier()
+    launches = D.kernel_launches() - l0
+    prof = D.profile_read(reset=True)
+    D.profile_enable(())
+    clk = clocks.stop()
+    tot_toks = allreduce([toks], "sum")[0]
+    dev_ms, wall_ms = allreduce([dev_ms, wall_ms], "max")
+    ms_step = dev_ms / args.steps
+    value = tot_toks / (dev_ms / 1e3)
+    e2e = tot_toks / (wall_ms / 1e3)
+
+    pk = peaks()
+    top = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    name, pr = top
+    hbm_bound = name in ("attn_decode", "sample", "lm_rows", "optimizer")
+    per_launch_ms = pr["ms"] / max(pr["launches"], 1)
+    if hbm_bound:
+        achieved = pr["bytes"] / (pr["ms"] / 1e3) / 1e9
+        peak, unit = pk["hbm"], "GB/s"
+    else:
+        achieved = pr["flops"] / (pr["ms"] / 1e3) / 1e12
+        peak, unit = pk["tc_sus"], "TFLOP/s"
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(name)
+
+    S_all = S
+    h2d = ptok.nbytes + poff.nbytes + S_all * 8       # prompts + rewards
+    d2h = sum(o.nbytes for o in outs) + S_all * (8 + 1) + 4 * 8   # rollout + advantages/kept + stats
+    line = {
+        "metric": "dash_step_sampled_tokens_per_s", "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "model": f"Qwen2.5-{cfg['size'] or 'tiny'}-shaped (reference math,"
+                   f" GQA {arch.get('n_heads', 1)}/{arch.get('n_kv_heads', 1)})", "prompts_per_gpu": M, "G": G,
+                   "prompt_len": cfg["prompt_len"], "gen_len": ML, "micro_batch": cfg["micro"], "tau": cfg["tau"],
+                   "optimizer": "adam", "global_batch": M * G * world, "seq_len": cfg["prompt_len"] + ML,
+                   "parallelism": f"dp{world}", "l2": "inputs > L2 (KV cache + weights stream every step)"},
+        "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm" if hbm_bound else "tensor", "kernel": name, "achieved": achieved,
+                     "peak": peak, "unit": unit, "frac": achieved / peak, "traffic": traffic,
+                     "per_launch_ms": per_launch_ms, "peak_source": pk["src"] + (" burst" if False else
+                                                                                " sustained" if not hbm_bound else "")},
+        "phases_ms": {k: last[k] for k in ("sample_ms", "advantage_ms", "accumulate_ms", "allreduce_ms",
+                                           "optimizer_ms")},
+        "kernel_classes": {k: {"ms_per_step": v["ms"] / args.steps, "launches": v["launches"]}
+                           for k, v in prof.items() if v["launches"]},
+        "kept": last["n_kept"], "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            run, sample = ref_step_runner(cfg, os.cpu_count() or 1)
+            a, b = run(0)
+            line["cpu_baseline"] = {"value": a / b, "unit": "tokens/s", "cores": os.cpu_count() or 1,
+                                    "kind": "reference", "sample": sample}
+        except Exception as e:  # reference not built on this box
+            line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    pol.close()
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--prompts", type=int, default=None)
+    ap.add_argument("--max-len", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.prompts:
+        cfg["prompts"] = args.prompts
+    if args.max_len:
+        cfg["max_len"] = args.max_len
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+    else:
+        run_ours(args, cfg, world, rank, local)
+    try:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
+    except Exception:
+        pass
+
+
+if __name__ == "__main__":
+    main()

@@ -180,6 +180,19 @@ DASHCU_API int dashcu_optimizer_step(dashcu_policy* pol, const dashcu_opt* opt);
 
 DASHCU_API int dashcu_get_stats(dashcu_policy* pol, dashcu_stats* out);
 
+/* ---- kernel-class profiler (bench.py roofline) ----
+ * Enabled classes (bit i = class i: 0 gemm_tc, 1 gemm_simt, 2 attn_decode,
+ * 3 attn_fwd, 4 attn_bwd, 5 sample, 6 lm_rows, 7 optimizer) have every launch
+ * bracketed by CUDA events on its stream and charged with its algorithmic
+ * flops / bytes. dashcu_profile_read returns one entry per class. */
+typedef struct {
+  char name[32];
+  int64_t launches;
+  double ms, flops, bytes;
+} dashcu_kprof;
+DASHCU_API int dashcu_profile_enable(unsigned class_mask);
+DASHCU_API int dashcu_profile_read(dashcu_kprof* out, int max, int reset);
+
 /* ---- diagnostics (used by the kernel tests) ----
  * C[M x N] (fp32, ldc = N) = A(m,k) . B(n,k) on bf16 operands given as raw
  * bit patterns, through the production GEMM dispatcher (tcgen05 when the

@@ -18,6 +18,8 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <algorithm>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -126,13 +128,17 @@ REF_API int ref_dash_step(const int32_t* arch_i, double* params, const int32_t* 
       if (adv.kept[i]) kept_idx.push_back(i);
     const double t2 = now_s();
 
+    // One accumulator guarded by a mutex: per-thread accumulators would need
+    // threads x num_params doubles (67 GB at the 0.5B shape on 16 threads).
     const int nt = n_threads < 1 ? 1 : n_threads;
-    std::vector<dash::GradientVector> acc(nt, dash::GradientVector::zeros(a));
-    parallel_for(static_cast<int>(kept_idx.size()), nt, [&](int k, int w) {
+    std::vector<dash::GradientVector> acc(1, dash::GradientVector::zeros(a));
+    std::mutex acc_mu;
+    parallel_for(static_cast<int>(kept_idx.size()), nt, [&](int k, int) {
       const int i = kept_idx[k];
-      acc[w].add_scaled(dash::grad_log_prob(p, trajs[i]), adv.advantages[i] / static_cast<double>(n));
+      dash::GradientVector gi = dash::grad_log_prob(p, trajs[i]);
+      std::lock_guard<std::mutex> lk(acc_mu);
+      acc[0].add_scaled(gi, adv.advantages[i] / static_cast<double>(n));
     });
-    for (int w = 1; w < nt; ++w) acc[0].add_scaled(acc[w], 1.0);
     const double t3 = now_s();
 
     if (opt == 0) {
@@ -144,15 +150,24 @@ REF_API int ref_dash_step(const int32_t* arch_i, double* params, const int32_t* 
       const double c2 = 1.0 - std::pow(b2, static_cast<double>(t));
       auto pv = p.views();
       auto gv = acc[0].views();
-      std::size_t off = 0;
-      for (std::size_t ti = 0; ti < pv.size(); ++ti) {
-        for (std::size_t j = 0; j < pv[ti].size; ++j, ++off) {
+      std::vector<std::size_t> base(pv.size(), 0);
+      for (std::size_t ti = 1; ti < pv.size(); ++ti) base[ti] = base[ti - 1] + pv[ti - 1].size;
+      // elementwise, so chunked over threads (the reference has no optimizer code)
+      constexpr std::size_t kChunk = 1 << 20;
+      std::vector<std::pair<std::size_t, std::size_t>> work;  // (tensor, start)
+      for (std::size_t ti = 0; ti < pv.size(); ++ti)
+        for (std::size_t j = 0; j < pv[ti].size; j += kChunk) work.emplace_back(ti, j);
+      parallel_for(static_cast<int>(work.size()), nt, [&](int w, int) {
+        const std::size_t ti = work[w].first, j0 = work[w].second;
+        const std::size_t j1 = std::min(pv[ti].size, j0 + kChunk);
+        for (std::size_t j = j0; j < j1; ++j) {
+          const std::size_t off = base[ti] + j;
           const double g = gv[ti].data[j];
           adam_m[off] = b1 * adam_m[off] + (1.0 - b1) * g;
           adam_v[off] = b2 * adam_v[off] + (1.0 - b2) * g * g;
           pv[ti].data[j] += lr * (adam_m[off] / c1) / (std::sqrt(adam_v[off] / c2) + eps);
         }
-      }
+      });
     }
     {
       std::size_t off = 0;

@@ -135,6 +135,10 @@ def lib():
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = C.c_int
+        L.dashcu_profile_enable.argtypes = [C.c_uint]
+        L.dashcu_profile_enable.restype = C.c_int
+        L.dashcu_profile_read.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.dashcu_profile_read.restype = C.c_int
         _lib = L
     return _lib
 
@@ -151,6 +155,31 @@ def _p(a: np.ndarray, t):
 
 def kernel_launches() -> int:
     return int(lib().dashcu_kernel_launches())
+
+
+class KProf(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("ms", C.c_double), ("flops", C.c_double),
+                ("bytes", C.c_double)]
+
+
+PROF_CLASSES = ("gemm_tc", "gemm_simt", "attn_decode", "attn_fwd", "attn_bwd", "sample", "lm_rows", "optimizer")
+
+
+def profile_enable(classes=PROF_CLASSES):
+    """Bracket every launch of the given kernel classes with CUDA events (algorithmic flops/bytes)."""
+    mask = 0
+    for c in classes:
+        mask |= 1 << PROF_CLASSES.index(c)
+    lib().dashcu_profile_enable(C.c_uint(mask))
+
+
+def profile_read(reset=True) -> dict:
+    arr = (KProf * 16)()
+    n = lib().dashcu_profile_read(arr, 16, int(reset))
+    if n < 0:
+        raise DeviceError("profile read failed")
+    return {arr[i].name.decode(): dict(launches=arr[i].launches, ms=arr[i].ms, flops=arr[i].flops,
+                                       bytes=arr[i].bytes) for i in range(n)}
 
 
 def num_params(arch: dict) -> int:

@@ -181,8 +181,9 @@ void set_smem(const void* fn, size_t bytes) {
 
 template <class T>
 void attn_fwd_varlen(cudaStream_t s, const T* qkv, const int32_t* seq_start, int n_seq, int max_len, int nh, int nkv,
-                     int hd, T* ctx, float* lse) {
+                     int hd, T* ctx, float* lse, double alg_flops) {
   if (n_seq <= 0) return;
+  ProfScope ps(PROF_ATTN_FWD, s, alg_flops, 0);
   const size_t smem = sizeof(float) * kWarps * (max_len + hd);
   set_smem((const void*)attn_fwd_k<T>, smem);
   attn_fwd_k<T><<<dim3(n_seq, nh), 256, smem, s>>>(qkv, seq_start, max_len, nh, nkv, hd, ctx, lse);
@@ -191,8 +192,9 @@ void attn_fwd_varlen(cudaStream_t s, const T* qkv, const int32_t* seq_start, int
 
 template <class T>
 void attn_bwd_varlen(cudaStream_t s, const T* qkv, const T* dctx, const float* lse, const int32_t* seq_start, int n_seq,
-                     int max_len, int nh, int nkv, int hd, float* dq32, float* dkv32) {
+                     int max_len, int nh, int nkv, int hd, float* dq32, float* dkv32, double alg_flops) {
   if (n_seq <= 0) return;
+  ProfScope ps(PROF_ATTN_BWD, s, alg_flops, 0);
   const size_t smem = sizeof(float) * kWarps * (2 * max_len + 2 * hd);
   set_smem((const void*)attn_bwd_k<T>, smem);
   attn_bwd_k<T><<<dim3(n_seq, nh), 256, smem, s>>>(qkv, dctx, lse, seq_start, max_len, nh, nkv, hd, dq32, dkv32);
@@ -202,7 +204,8 @@ void attn_bwd_varlen(cudaStream_t s, const T* qkv, const T* dctx, const float* l
 template <class T>
 void attn_decode(cudaStream_t s, const T* qkv, const T* kp, const T* vp, const T* kc, const T* vc,
                  const int32_t* prompt_len, int rows, int G, int pmax, int n_comp, int max_len, int nh, int nkv, int hd,
-                 T* ctx) {
+                 T* ctx, double alg_bytes) {
+  ProfScope ps(PROF_ATTN_DECODE, s, 0, alg_bytes);
   const size_t smem = sizeof(float) * (pmax + max_len + hd);
   set_smem((const void*)attn_decode_k<T>, smem);
   attn_decode_k<T><<<dim3(rows, nh), 32, smem, s>>>(qkv, kp, vp, kc, vc, prompt_len, G, pmax, n_comp, max_len, nh, nkv,
@@ -211,11 +214,12 @@ void attn_decode(cudaStream_t s, const T* qkv, const T* kp, const T* vp, const T
 }
 
 #define INST(T)                                                                                                     \
-  template void attn_fwd_varlen<T>(cudaStream_t, const T*, const int32_t*, int, int, int, int, int, T*, float*);   \
+  template void attn_fwd_varlen<T>(cudaStream_t, const T*, const int32_t*, int, int, int, int, int, T*, float*,     \
+                                   double);                                                                         \
   template void attn_bwd_varlen<T>(cudaStream_t, const T*, const T*, const float*, const int32_t*, int, int, int, int, \
-                                   int, float*, float*);                                                            \
+                                   int, float*, float*, double);                                                    \
   template void attn_decode<T>(cudaStream_t, const T*, const T*, const T*, const T*, const T*, const int32_t*, int, \
-                               int, int, int, int, int, int, int, T*);
+                               int, int, int, int, int, int, int, T*, double);
 INST(float)
 INST(bf16)
 #undef INST

@@ -37,6 +37,40 @@ extern int64_t g_launches;
     DCU_CHECK(cudaGetLastError()); \
   } while (0)
 
+// Kernel-class profiler: when a class is enabled, its launches are bracketed by
+// CUDA events on the launching stream and charged with their ALGORITHMIC flops
+// and bytes (not measured traffic), so bench.py can report achieved / roofline.
+enum ProfClass : int {
+  PROF_GEMM_TC = 0,
+  PROF_GEMM_SIMT = 1,
+  PROF_ATTN_DECODE = 2,
+  PROF_ATTN_FWD = 3,
+  PROF_ATTN_BWD = 4,
+  PROF_SAMPLE = 5,
+  PROF_LM_ROWS = 6,
+  PROF_OPTIMIZER = 7,
+  PROF_NUM = 8
+};
+extern const char* const kProfNames[PROF_NUM];
+extern unsigned g_prof_mask;
+void prof_begin(int cls, cudaStream_t s, cudaEvent_t* ev);
+void prof_end(int cls, cudaStream_t s, cudaEvent_t ev0, double flops, double bytes);
+
+struct ProfScope {
+  int cls;
+  cudaStream_t s;
+  double flops, bytes;
+  cudaEvent_t ev = nullptr;
+  bool on;
+  ProfScope(int c, cudaStream_t st, double f, double b) : cls(c), s(st), flops(f), bytes(b) {
+    on = (g_prof_mask >> c) & 1u;
+    if (on) prof_begin(c, s, &ev);
+  }
+  ~ProfScope() {
+    if (on) prof_end(cls, s, ev, flops, bytes);
+  }
+};
+
 typedef __nv_bfloat16 bf16;
 
 template <class T>

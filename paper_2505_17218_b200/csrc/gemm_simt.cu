@@ -81,6 +81,7 @@ template <class T>
 void gemm_simt(cudaStream_t s, const GemmShape& g, const Epi& e) {
   if (g.M <= 0 || g.N <= 0) return;
   dim3 grid(cdiv(g.N, BN), cdiv(g.M, BM));
+  ProfScope ps(PROF_GEMM_SIMT, s, 2.0 * g.M * g.N * static_cast<double>(g.K), 0);
   if (g.a_kmajor && g.b_kmajor) gemm_simt_kernel<T, true, true><<<grid, 256, 0, s>>>(g, e);
   else if (g.a_kmajor && !g.b_kmajor) gemm_simt_kernel<T, true, false><<<grid, 256, 0, s>>>(g, e);
   else if (!g.a_kmajor && g.b_kmajor) gemm_simt_kernel<T, false, true><<<grid, 256, 0, s>>>(g, e);

@@ -244,6 +244,7 @@ void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const 
     attr = true;
   }
   dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM);
+  ProfScope ps(PROF_GEMM_TC, s, 2.0 * g.M * g.N * static_cast<double>(g.K), 0);
   k<<<grid, 256, C::SMEM, s>>>(ma, mb, g, e);
   DCU_LAUNCHED();
 }

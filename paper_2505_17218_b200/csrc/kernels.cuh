@@ -34,10 +34,10 @@ void colsum_acc_f32(cudaStream_t s, const float* X, int64_t ld, int M, int N, fl
 // Packed variable-length causal self-attention over qkv rows [T x (qd + 2 kvd)].
 template <class T>
 void attn_fwd_varlen(cudaStream_t s, const T* qkv, const int32_t* seq_start, int n_seq, int max_len,
-                     int nh, int nkv, int hd, T* ctx, float* lse);
+                     int nh, int nkv, int hd, T* ctx, float* lse, double alg_flops = 0);
 template <class T>
 void attn_bwd_varlen(cudaStream_t s, const T* qkv, const T* dctx, const float* lse, const int32_t* seq_start,
-                     int n_seq, int max_len, int nh, int nkv, int hd, float* dq32, float* dkv32);
+                     int n_seq, int max_len, int nh, int nkv, int hd, float* dq32, float* dkv32, double alg_flops = 0);
 // qkv-gradient assembly: dqkv (T) from fp32 dq [T x qd] and dkv [T x 2 kvd]
 template <class T>
 void pack_dqkv(cudaStream_t s, const float* dq, const float* dkv, int rows, int qd, int kvd, T* dqkv);
@@ -54,7 +54,7 @@ void kv_append(cudaStream_t s, const T* qkv, int rows, int qd, int kvd, int nkv,
 template <class T>
 void attn_decode(cudaStream_t s, const T* qkv, const T* kp, const T* vp, const T* kc, const T* vc,
                  const int32_t* prompt_len, int rows, int G, int pmax, int n_comp, int max_len, int nh, int nkv,
-                 int hd, T* ctx);
+                 int hd, T* ctx, double alg_bytes = 0);
 // One sampling step over fp32 logits rows (policy.cpp:399-426 with the D2 rule).
 void sample_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, int eos, float inv_t,
                  const uint64_t* keys, int step, const int32_t* cap, uint8_t* finished, int32_t* comp,

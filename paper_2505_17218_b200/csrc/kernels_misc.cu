@@ -416,6 +416,7 @@ void fill_f32(cudaStream_t s, float* p, float v, int64_t n) {
 }
 void optimizer_update(cudaStream_t s, int kind, float* w, const float* g, float* m, float* v, bf16* wT, int64_t n,
                       float lr, float b1, float b2, float eps, float c1, float c2) {
+  ProfScope ps(PROF_OPTIMIZER, s, 0, 30.0 * static_cast<double>(n));
   optimizer_k<<<grid1d(n), 256, 0, s>>>(kind, w, g, m, v, wT, n, lr, b1, b2, eps, c1, c2);
   DCU_LAUNCHED();
 }
@@ -452,6 +453,7 @@ void colsum_acc_f32(cudaStream_t s, const float* X, int64_t ld, int M, int N, fl
 void sample_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, int eos, float inv_t,
                  const uint64_t* keys, int step, const int32_t* cap, uint8_t* finished, int32_t* comp, float* logp,
                  int32_t* len, int32_t* tok_next, int max_len, float* dump) {
+  ProfScope ps(PROF_SAMPLE, s, 0, 4.0 * rows * static_cast<double>(V));
   sample_rows_k<<<rows, 256, 0, s>>>(logits, V, bos, eos, inv_t, keys, step, cap, finished, comp, logp, len, tok_next,
                                      max_len, dump);
   DCU_LAUNCHED();
@@ -461,6 +463,7 @@ template <class T>
 void lm_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, const int32_t* target,
              const float* weight, float* logp, T* dz) {
   if (rows <= 0) return;
+  ProfScope ps(PROF_LM_ROWS, s, 0, static_cast<double>(rows) * V * (4.0 + (dz ? sizeof(T) : 0)));
   lm_rows_k<T><<<rows, 256, 0, s>>>(logits, V, bos, target, weight, logp, dz);
   DCU_LAUNCHED();
 }

@@ -281,6 +281,7 @@ struct Engine {
   cudaStream_t st;
   const Geo& g;
   const Lay& L;
+  double pairs = 0;  // algorithmic attention work of the current packed batch (profiler)
   explicit Engine(Pol& p) : P(p), st(p.ctx->stream), g(p.g), L(p.lay) {}
 
   const T* W(int64_t off) const {
@@ -343,7 +344,7 @@ struct Engine {
       T* u = A.u + t * g.H * l;
       float* lse = A.lse + t * g.nh * l;
       mm(Tn, g.qkvd, g.d, xl, g.d, true, W(b + L.wq), g.d, true, store(nullptr, 0, qkv, g.qkvd));
-      attn_fwd_varlen<T>(st, qkv, start, nseq, maxlen, g.nh, g.nkv, g.hd, ctx, lse);
+      attn_fwd_varlen<T>(st, qkv, start, nseq, maxlen, g.nh, g.nkv, g.hd, ctx, lse, 4.0 * g.nh * g.hd * pairs);
       Epi eo = store(A.h32, g.d, hT, g.d);
       eo.resid = A.x32;
       eo.ldr = g.d;
@@ -443,7 +444,8 @@ struct Engine {
       mm(Tn, g.qd, g.d, dhT, g.d, true, W(b + L.wo), g.qd, false, store(nullptr, 0, dctx, g.qd));
       // attention
       fill_f32(st, dkv32, 0.f, static_cast<int64_t>(t) * 2 * g.kvd);
-      attn_bwd_varlen<T>(st, qkv, dctx, lse, start, nseq, maxlen, g.nh, g.nkv, g.hd, dq32, dkv32);
+      attn_bwd_varlen<T>(st, qkv, dctx, lse, start, nseq, maxlen, g.nh, g.nkv, g.hd, dq32, dkv32,
+                         10.0 * g.nh * g.hd * pairs);
       pack_dqkv<T>(st, dq32, dkv32, Tn, g.qd, g.kvd, dqkv);
       // q, k, v projections (wq, wk, wv are contiguous rows of one [qkvd x d] matrix)
       acc.c32 = G32(b + L.wq);
@@ -471,6 +473,7 @@ struct Engine {
     std::vector<int32_t> tok, pos, start, rows, tgt, seqs;
     std::vector<float> w;
     int maxlen = 0;
+    double pairs = 0;  // sum over sequences of n(n+1)/2 causal (query, key) pairs
   };
 
   // Packs prompt + completion[:-1] of each sequence (forward_for_loss, policy.cpp:350-358).
@@ -502,6 +505,7 @@ struct Engine {
       B.start.push_back(s0 + n);
       B.seqs.push_back(s);
       B.maxlen = std::max(B.maxlen, n);
+      B.pairs += 0.5 * n * (n + 1.0);
     }
     return B;
   }
@@ -540,6 +544,7 @@ struct Engine {
       DevBatch D = upload(B);
       const int Tn = static_cast<int>(B.tok.size());
       Acts A = alloc_acts(P.ws, Tn, "a_");
+      pairs = B.pairs;
       forward(A, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen);
       float* dy32 = P.ws.get<float>("b_dy32", static_cast<size_t>(Tn) * g.d);
       lm_head(A, static_cast<int>(B.rows.size()), D.rows, D.tgt, D.w, nullptr, true, dy32);
@@ -563,6 +568,7 @@ struct Engine {
       DevBatch D = upload(B);
       const int Tn = static_cast<int>(B.tok.size());
       Acts A = alloc_acts(P.ws, Tn, "a_");
+      pairs = B.pairs;
       forward(A, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen);
       float* lp = P.ws.get<float>("lp_out", B.rows.size());
       lm_head(A, static_cast<int>(B.rows.size()), D.rows, D.tgt, nullptr, lp, false, nullptr);
@@ -639,6 +645,13 @@ struct Engine {
     // Prefill (teacher-forced forward over the M prompts).
     const int Tp = static_cast<int>(ptok.size());
     Acts A = alloc_acts(ws, Tp, "p_");
+    pairs = 0;
+    double sum_m = 0;
+    for (int p = 0; p < NP; ++p) {
+      const double m = static_cast<double>(pstart[p + 1] - pstart[p]);
+      pairs += 0.5 * m * (m + 1);
+      sum_m += m * G;
+    }
     forward(A, d_ptok, d_ppos, d_pstart, NP, pmax);
     for (int l = 0; l < g.L; ++l)
       kv_store_prompt<T>(st, A.qkv + static_cast<size_t>(Tp) * g.qkvd * l, d_pstart, NP, pmax, g.qd, g.kvd, g.nkv,
@@ -667,8 +680,9 @@ struct Engine {
         const int64_t b = lb(l);
         mm(S, g.qkvd, g.d, xT, g.d, true, W(b + L.wq), g.d, true, store(nullptr, 0, qkv, g.qkvd));
         kv_append<T>(st, qkv, S, g.qd, g.kvd, g.nkv, g.hd, j - 1, cslots, kc + kvc * l, vc + kvc * l);
+        // algorithmic bytes: every (sequence, kv head) reads its K and V rows once
         attn_decode<T>(st, qkv, kp + kvp * l, vp + kvp * l, kc + kvc * l, vc + kvc * l, d_plen, S, G, pmax, j, cslots,
-                       g.nh, g.nkv, g.hd, ctx);
+                       g.nh, g.nkv, g.hd, ctx, (sum_m + static_cast<double>(S) * j) * g.kvd * 2.0 * sizeof(T));
         Epi eo = store(h32, g.d, hT, g.d);
         eo.resid = x32;
         eo.ldr = g.d;

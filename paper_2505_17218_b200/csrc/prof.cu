@@ -1,0 +1,112 @@
+// Kernel-class profiler (see common.cuh ProfScope) + its C-ABI readers.
+#include <mutex>
+#include <vector>
+
+#include "../../include/dashcu.h"
+#include "common.cuh"
+
+namespace dashcu {
+
+const char* const kProfNames[PROF_NUM] = {"gemm_tc",   "gemm_simt", "attn_decode", "attn_fwd",
+                                          "attn_bwd",  "sample",    "lm_rows",     "optimizer"};
+unsigned g_prof_mask = 0;
+
+namespace {
+
+struct Pending {
+  int cls;
+  cudaEvent_t a, b;
+  double flops, bytes;
+};
+
+struct Prof {
+  std::mutex mu;
+  std::vector<cudaEvent_t> pool;
+  std::vector<Pending> pending;
+  double ms[PROF_NUM] = {};
+  double flops[PROF_NUM] = {};
+  double bytes[PROF_NUM] = {};
+  int64_t launches[PROF_NUM] = {};
+
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    DCU_CHECK(cudaEventCreate(&e));
+    return e;
+  }
+  void drain() {
+    for (auto& p : pending) {
+      DCU_CHECK(cudaEventSynchronize(p.b));
+      float t = 0.f;
+      DCU_CHECK(cudaEventElapsedTime(&t, p.a, p.b));
+      ms[p.cls] += t;
+      flops[p.cls] += p.flops;
+      bytes[p.cls] += p.bytes;
+      launches[p.cls] += 1;
+      pool.push_back(p.a);
+      pool.push_back(p.b);
+    }
+    pending.clear();
+  }
+};
+
+Prof& prof() {
+  static Prof p;
+  return p;
+}
+
+}  // namespace
+
+void prof_begin(int, cudaStream_t s, cudaEvent_t* ev) {
+  Prof& p = prof();
+  std::lock_guard<std::mutex> lk(p.mu);
+  *ev = p.get();
+  DCU_CHECK(cudaEventRecord(*ev, s));
+}
+
+void prof_end(int cls, cudaStream_t s, cudaEvent_t ev0, double flops, double bytes) {
+  Prof& p = prof();
+  std::lock_guard<std::mutex> lk(p.mu);
+  cudaEvent_t e = p.get();
+  DCU_CHECK(cudaEventRecord(e, s));
+  p.pending.push_back({cls, ev0, e, flops, bytes});
+  if (p.pending.size() > 65536) p.drain();
+}
+
+}  // namespace dashcu
+
+extern "C" {
+
+DASHCU_API int dashcu_profile_enable(unsigned class_mask) {
+  std::lock_guard<std::mutex> lk(dashcu::prof().mu);
+  dashcu::g_prof_mask = class_mask;
+  return 0;
+}
+
+DASHCU_API int dashcu_profile_read(dashcu_kprof* out, int max, int reset) {
+  using namespace dashcu;
+  try {
+    Prof& p = prof();
+    std::lock_guard<std::mutex> lk(p.mu);
+    p.drain();
+    int n = 0;
+    for (int c = 0; c < PROF_NUM && n < max; ++c, ++n) {
+      snprintf(out[n].name, sizeof(out[n].name), "%s", kProfNames[c]);
+      out[n].launches = p.launches[c];
+      out[n].ms = p.ms[c];
+      out[n].flops = p.flops[c];
+      out[n].bytes = p.bytes[c];
+    }
+    if (reset)
+      for (int c = 0; c < PROF_NUM; ++c) p.ms[c] = p.flops[c] = p.bytes[c] = 0, p.launches[c] = 0;
+    return n;
+  } catch (...) {
+    return -1;
+  }
+}
+
+}  // extern "C"
