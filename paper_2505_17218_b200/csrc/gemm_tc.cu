@@ -90,6 +90,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
 template <int BN, int STAGES, bool AK, bool BKM>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
@@ -103,7 +108,7 @@ struct Cfg {
 };
 
 template <int BN, int STAGES, bool AK, bool BKM>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, GemmShape g,
                    Epi e) {
   using C = Cfg<BN, STAGES, AK, BKM>;
@@ -188,13 +193,84 @@ __global__ void __launch_bounds__(256, 1)
     mbar_wait(tfull, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     float v[32];
+    // 16-byte vector path: every pointer / leading dim the epilogue touches is 16-B aligned
+    auto al = [](const void* p, int64_t ld, int esz) {
+      return p == nullptr || (((reinterpret_cast<uintptr_t>(p) | static_cast<uintptr_t>(ld * esz)) & 15) == 0);
+    };
+    const bool vec = al(e.c32, e.ldc32, 4) && al(e.cT, e.ldcT, 2) && al(e.resid, e.ldr, 4) && al(e.aux, e.ld_aux, 2) &&
+                     al(e.bias, 0, 4);
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
-      if (row < g.M) {
+      if (row >= g.M) continue;
+      const int nb = n0 + c;
+      if (vec && nb + 32 <= g.N) {
+        const int64_t r64 = row;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] *= e.alpha;
+        if (e.bias) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 b = *reinterpret_cast<const float4*>(e.bias + nb + i);
+            v[i] += b.x, v[i + 1] += b.y, v[i + 2] += b.z, v[i + 3] += b.w;
+          }
+        }
+        if (e.kind == EPI_TANH) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = tanhf(v[i]);
+        }
+        if (e.kind == EPI_DTANH) {
+          const bf16* ap = static_cast<const bf16*>(e.aux) + r64 * e.ld_aux + nb;
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            const uint4 raw = *reinterpret_cast<const uint4*>(ap + i);
+            const bf16* a8 = reinterpret_cast<const bf16*>(&raw);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const float a = __bfloat162float(a8[k]);
+              v[i + k] *= (1.f - a * a);
+            }
+          }
+        }
+        if (e.resid) {
+          const float* rp = e.resid + r64 * e.ldr + nb;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 x = *reinterpret_cast<const float4*>(rp + i);
+            v[i] += x.x, v[i + 1] += x.y, v[i + 2] += x.z, v[i + 3] += x.w;
+          }
+        }
+        if (e.kind == EPI_ACCUM) {
+          float* cp = e.c32 + r64 * e.ldc32 + nb;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            float4 x = *reinterpret_cast<float4*>(cp + i);
+            x.x += v[i], x.y += v[i + 1], x.z += v[i + 2], x.w += v[i + 3];
+            *reinterpret_cast<float4*>(cp + i) = x;
+          }
+          continue;
+        }
+        if (e.c32) {
+          float* cp = e.c32 + r64 * e.ldc32 + nb;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(cp + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        }
+        if (e.cT) {
+          bf16* cp = static_cast<bf16*>(e.cT) + r64 * e.ldcT + nb;
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint4 o;
+            o.x = pack2(v[i], v[i + 1]);
+            o.y = pack2(v[i + 2], v[i + 3]);
+            o.z = pack2(v[i + 4], v[i + 5]);
+            o.w = pack2(v[i + 6], v[i + 7]);
+            *reinterpret_cast<uint4*>(cp + i) = o;
+          }
+        }
+      } else {
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const int n = n0 + c + i;
+          const int n = nb + i;
           if (n < g.N) epi_apply<bf16>(e, row, n, v[i]);
         }
       }
@@ -260,10 +336,11 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e) {
   bool ok = g.a_kmajor ? make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) : make_map(&ma, g.A, g.K, g.M, g.lda, 64, BK);
   ok = ok && (g.b_kmajor ? make_map(&mb, g.B, g.N, g.K, g.ldb, BK, BN) : make_map(&mb, g.B, g.K, g.N, g.ldb, 64, BK));
   if (!ok) return false;
-  if (g.a_kmajor && g.b_kmajor) launch<BN, 4, true, true>(s, ma, mb, g, e);
-  else if (g.a_kmajor) launch<BN, 4, true, false>(s, ma, mb, g, e);
-  else if (g.b_kmajor) launch<BN, 4, false, true>(s, ma, mb, g, e);
-  else launch<BN, 4, false, false>(s, ma, mb, g, e);
+  // 3 stages x 32 KB: two CTAs per SM, so one CTA's epilogue overlaps the other's mainloop
+  if (g.a_kmajor && g.b_kmajor) launch<BN, 3, true, true>(s, ma, mb, g, e);
+  else if (g.a_kmajor) launch<BN, 3, true, false>(s, ma, mb, g, e);
+  else if (g.b_kmajor) launch<BN, 3, false, true>(s, ma, mb, g, e);
+  else launch<BN, 3, false, false>(s, ma, mb, g, e);
   return true;
 }
 

@@ -38,6 +38,14 @@ void attn_fwd_varlen(cudaStream_t s, const T* qkv, const int32_t* seq_start, int
 template <class T>
 void attn_bwd_varlen(cudaStream_t s, const T* qkv, const T* dctx, const float* lse, const int32_t* seq_start,
                      int n_seq, int max_len, int nh, int nkv, int hd, float* dq32, float* dkv32, double alg_flops = 0);
+// Tensor-core (mma.sync) flash attention for the bf16 path; head_dim 64/128.
+// Return false when the geometry is not covered (caller uses the CUDA-core kernels).
+bool attn_fwd_tc(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int n_seq, int max_len, int nh, int nkv,
+                 int hd, bf16* ctx, float* lse, double alg_flops);
+// dq32 is overwritten (zeroed then accumulated), dkv32 rows are written.
+bool attn_bwd_tc(cudaStream_t s, const bf16* qkv, const bf16* ctx, const bf16* dctx, const float* lse,
+                 const int32_t* seq_start, int n_seq, int max_len, int rows, int nh, int nkv, int hd, float* Dbuf,
+                 float* dq32, float* dkv32, double alg_flops);
 // qkv-gradient assembly: dqkv (T) from fp32 dq [T x qd] and dkv [T x 2 kvd]
 template <class T>
 void pack_dqkv(cudaStream_t s, const float* dq, const float* dkv, int rows, int qd, int kvd, T* dqkv);
@@ -55,6 +63,11 @@ template <class T>
 void attn_decode(cudaStream_t s, const T* qkv, const T* kp, const T* vp, const T* kc, const T* vc,
                  const int32_t* prompt_len, int rows, int G, int pmax, int n_comp, int max_len, int nh, int nkv,
                  int hd, T* ctx, double alg_bytes = 0);
+// Tensor-core decode attention (bf16; head_dim 64/128, <= 16 query heads per KV head).
+// Returns false when the geometry is not covered (caller uses attn_decode).
+bool attn_decode_tc(cudaStream_t s, const bf16* qkv, const bf16* kp, const bf16* vp, const bf16* kc, const bf16* vc,
+                    const int32_t* prompt_len, int rows, int G, int pmax, int n_comp, int cslots, int nh, int nkv,
+                    int hd, bf16* ctx, double alg_bytes);
 // One sampling step over fp32 logits rows (policy.cpp:399-426 with the D2 rule).
 void sample_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, int eos, float inv_t,
                  const uint64_t* keys, int step, const int32_t* cap, uint8_t* finished, int32_t* comp,

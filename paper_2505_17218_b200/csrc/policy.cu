@@ -344,7 +344,11 @@ struct Engine {
       T* u = A.u + t * g.H * l;
       float* lse = A.lse + t * g.nh * l;
       mm(Tn, g.qkvd, g.d, xl, g.d, true, W(b + L.wq), g.d, true, store(nullptr, 0, qkv, g.qkvd));
-      attn_fwd_varlen<T>(st, qkv, start, nseq, maxlen, g.nh, g.nkv, g.hd, ctx, lse, 4.0 * g.nh * g.hd * pairs);
+      bool done = false;
+      if constexpr (sizeof(T) == 2)
+        done = attn_fwd_tc(st, qkv, start, nseq, maxlen, g.nh, g.nkv, g.hd, ctx, lse, 4.0 * g.nh * g.hd * pairs);
+      if (!done)
+        attn_fwd_varlen<T>(st, qkv, start, nseq, maxlen, g.nh, g.nkv, g.hd, ctx, lse, 4.0 * g.nh * g.hd * pairs);
       Epi eo = store(A.h32, g.d, hT, g.d);
       eo.resid = A.x32;
       eo.ldr = g.d;
@@ -444,8 +448,13 @@ struct Engine {
       mm(Tn, g.qd, g.d, dhT, g.d, true, W(b + L.wo), g.qd, false, store(nullptr, 0, dctx, g.qd));
       // attention
       fill_f32(st, dkv32, 0.f, static_cast<int64_t>(t) * 2 * g.kvd);
-      attn_bwd_varlen<T>(st, qkv, dctx, lse, start, nseq, maxlen, g.nh, g.nkv, g.hd, dq32, dkv32,
-                         10.0 * g.nh * g.hd * pairs);
+      bool done = false;
+      if constexpr (sizeof(T) == 2)
+        done = attn_bwd_tc(st, qkv, ctx, dctx, lse, start, nseq, maxlen, Tn, g.nh, g.nkv, g.hd,
+                           ws.get<float>("b_D", t * g.nh), dq32, dkv32, 10.0 * g.nh * g.hd * pairs);
+      if (!done)
+        attn_bwd_varlen<T>(st, qkv, dctx, lse, start, nseq, maxlen, g.nh, g.nkv, g.hd, dq32, dkv32,
+                           10.0 * g.nh * g.hd * pairs);
       pack_dqkv<T>(st, dq32, dkv32, Tn, g.qd, g.kvd, dqkv);
       // q, k, v projections (wq, wk, wv are contiguous rows of one [qkvd x d] matrix)
       acc.c32 = G32(b + L.wq);
@@ -681,8 +690,14 @@ struct Engine {
         mm(S, g.qkvd, g.d, xT, g.d, true, W(b + L.wq), g.d, true, store(nullptr, 0, qkv, g.qkvd));
         kv_append<T>(st, qkv, S, g.qd, g.kvd, g.nkv, g.hd, j - 1, cslots, kc + kvc * l, vc + kvc * l);
         // algorithmic bytes: every (sequence, kv head) reads its K and V rows once
-        attn_decode<T>(st, qkv, kp + kvp * l, vp + kvp * l, kc + kvc * l, vc + kvc * l, d_plen, S, G, pmax, j, cslots,
-                       g.nh, g.nkv, g.hd, ctx, (sum_m + static_cast<double>(S) * j) * g.kvd * 2.0 * sizeof(T));
+        const double kv_bytes = (sum_m + static_cast<double>(S) * j) * g.kvd * 2.0 * sizeof(T);
+        bool done = false;
+        if constexpr (sizeof(T) == 2)
+          done = attn_decode_tc(st, qkv, kp + kvp * l, vp + kvp * l, kc + kvc * l, vc + kvc * l, d_plen, S, G, pmax,
+                                j, cslots, g.nh, g.nkv, g.hd, ctx, kv_bytes);
+        if (!done)
+          attn_decode<T>(st, qkv, kp + kvp * l, vp + kvp * l, kc + kvc * l, vc + kvc * l, d_plen, S, G, pmax, j,
+                         cslots, g.nh, g.nkv, g.hd, ctx, kv_bytes);
         Epi eo = store(h32, g.d, hT, g.d);
         eo.resid = x32;
         eo.ldr = g.d;

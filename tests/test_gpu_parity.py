@@ -22,6 +22,13 @@ C1 = dict(vocab_size=256, embed_dim=128, context_len=64, ffn_hidden=512, n_layer
 SMALL = dict(vocab_size=37, embed_dim=32, context_len=40, ffn_hidden=48, n_layers=2, bos_id=0, eos_id=1)
 GQA = dict(vocab_size=64, embed_dim=64, context_len=48, ffn_hidden=128, n_layers=2, bos_id=0, eos_id=1,
            n_heads=4, n_kv_heads=2, head_dim=16)
+# geometries that exercise the tensor-core attention kernels (head_dim 64 / 128)
+QWENLIKE = dict(vocab_size=300, embed_dim=256, context_len=48, ffn_hidden=256, n_layers=2, bos_id=0, eos_id=1,
+                n_heads=14, n_kv_heads=2, head_dim=64)
+GQA128 = dict(vocab_size=64, embed_dim=128, context_len=48, ffn_hidden=128, n_layers=2, bos_id=0, eos_id=1,
+              n_heads=4, n_kv_heads=2, head_dim=128)
+LONG = dict(vocab_size=64, embed_dim=128, context_len=200, ffn_hidden=128, n_layers=1, bos_id=0, eos_id=1,
+            n_heads=2, n_kv_heads=1, head_dim=64)
 TOL = {D.F32: 1e-3, D.BF16: 2e-2}
 
 
@@ -120,7 +127,7 @@ def test_advantage_filter_large_and_errors(ctx):
 # ---------------------------------------------------------------- sampling
 
 @pytest.mark.parametrize("dtype", [D.F32, D.BF16])
-@pytest.mark.parametrize("arch", [C1, GQA], ids=["c1", "gqa"])
+@pytest.mark.parametrize("arch", [C1, GQA, QWENLIKE, GQA128], ids=["c1", "gqa", "qwenlike", "gqa128"])
 def test_sampled_tokens_bit_exact_under_logits_dump(ctx, arch, dtype):
     pol = D.Policy(ctx, arch, dtype)
     pol.upload(params32(arch, 0.5, 3))
@@ -204,7 +211,8 @@ def test_sample_errors(ctx):
 # --------------------------------------------------------------- log_prob
 
 @pytest.mark.parametrize("dtype", [D.F32, D.BF16])
-@pytest.mark.parametrize("arch", [SMALL, GQA, C1], ids=["small", "gqa", "c1"])
+@pytest.mark.parametrize("arch", [SMALL, GQA, C1, QWENLIKE, GQA128], ids=["small", "gqa", "c1", "qwenlike",
+                                                                          "gqa128"])
 def test_teacher_forced_log_prob(ctx, arch, dtype):
     pol = D.Policy(ctx, arch, dtype)
     p = params32(arch, 0.3, 7)
@@ -222,7 +230,8 @@ def test_teacher_forced_log_prob(ctx, arch, dtype):
 # ----------------------------------------------------------------- gradients
 
 @pytest.mark.parametrize("dtype", [D.F32, D.BF16])
-@pytest.mark.parametrize("arch", [SMALL, GQA, C1], ids=["small", "gqa", "c1"])
+@pytest.mark.parametrize("arch", [SMALL, GQA, C1, QWENLIKE, GQA128], ids=["small", "gqa", "c1", "qwenlike",
+                                                                          "gqa128"])
 def test_pg_gradient_parity(ctx, arch, dtype):
     pol = D.Policy(ctx, arch, dtype)
     p = params32(arch, 0.3, 8)
@@ -325,4 +334,45 @@ def test_dash_step_c1_matches_oracle(ctx, dtype):
     assert st["n_kept"] == nk and st["tokens_sampled"] == int(ro.lengths.sum())
     pol.optimizer_step(D.OPT_ADAM, lr=1e-3)
     assert pol.version() > 0
+    pol.close()
+
+
+@pytest.mark.parametrize("dtype", [D.F32, D.BF16])
+def test_long_sequences_multi_tile(ctx, dtype):
+    """Sequences spanning several 64-key tiles (flash-attention tiling, causal diagonal,
+    ragged tails) through log_prob, the gradient and the decode KV path."""
+    arch = LONG
+    pol = D.Policy(ctx, arch, dtype)
+    p = params32(arch, 0.5, 12)
+    pol.upload(p)
+    rng = np.random.default_rng(13)
+    prompts = [[0] + list(rng.integers(2, 64, size=int(rng.integers(20, 70)))) for _ in range(3)]
+    comps = [list(rng.integers(2, 64, size=int(rng.integers(1, 120)))) for _ in range(6)]
+    pol.load_rollout(prompts, 2, comps)
+    n_tok = sum(len(c) for c in comps)
+    lp = pol.rollout_log_prob(n_tok)
+    ref = np.concatenate([O.log_prob(arch, p, prompts[s // 2], comps[s])[1] for s in range(6)])
+    assert np.abs(lp - ref).max() <= TOL[dtype] * max(1.0, np.abs(ref).max())
+    w = rng.standard_normal(6) / 6
+    pol.grad_zero()
+    pol.accumulate_weighted(w, micro_batch=4)
+    got = pol.grad()
+    g = np.zeros_like(got)
+    for s in range(6):
+        O.grad_log_prob(arch, p, prompts[s // 2], comps[s], w[s], g)
+    assert_grad_close(arch, got, g, TOL[dtype])
+    # decode over long contexts: sampled tokens replay bit-exactly from the logits dump
+    pol.set_logits_dump(True)
+    ro = pol.sample(prompts, 2, 90, round_seed=4)
+    dump = pol.logits_dump(6, 90)
+    for s in range(6):
+        key = O.derive_seed(4, "sample", s // 2, s % 2)
+        for j in range(int(ro.lengths[s])):
+            assert O.sample_rule(dump[s, j], 0, 1.0, key, j) == ro.completions[s, j]
+    # and the dumped logits match the oracle's forward on a few positions
+    for s in (0, 5):
+        comp = list(ro.completion(s))
+        for j in (0, len(comp) // 2, len(comp) - 1):
+            refl = O.next_logits(arch, p, prompts[s // 2] + comp[:j])
+            assert np.abs(dump[s, j] - refl).max() <= (1e-3 if dtype == D.F32 else 5e-2) * max(1, np.abs(refl).max())
     pol.close()
