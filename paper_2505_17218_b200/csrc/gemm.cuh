@@ -45,12 +45,30 @@ struct GemmShape {
   bool b_kmajor;
 };
 
+// LM-head sampling epilogue (policy.cpp:148-151 + :399-424 with the DESIGN.md §4 rule):
+// logits never leave the SM. Per (row, N tile) the epilogue writes 5 floats
+//   {best Gumbel score, best id (bit pattern), logit of best, max logit, sum exp(logit - max)}
+// over non-BOS ids; sample_reduce combines the tiles of a row.
+struct SampleArgs {
+  const uint64_t* keys = nullptr;  // per-row sequence key derive_seed(round, "sample", m, g)
+  int step = 0;
+  float inv_t = 1.f;
+  int bos = -1;
+  float* part = nullptr;  // [rows][ntiles][5]
+  int ntiles = 0;
+  float* dump = nullptr;  // optional: logits row r at dump + r * dump_ld (debug / parity)
+  int64_t dump_ld = 0;
+};
+
 // dtype: 0 fp32 (CUDA cores), 1 bf16 (tcgen05 when the operands are TMA-legal)
 void gemm(cudaStream_t s, int dtype, const GemmShape& g, const Epi& e);
 template <class T>
 void gemm_simt(cudaStream_t s, const GemmShape& g, const Epi& e);
 // tcgen05 path; returns false if the shape is not TMA-legal (strides must be 16-byte multiples).
 bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e);
+// Fused LM head + sampling partials; returns the number of N tiles (0 if not TMA-legal).
+int gemm_tc_sample(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa);
+int gemm_tc_sample_tiles(int N);
 
 template <class T>
 __device__ __forceinline__ void epi_apply(const Epi& e, int m, int n, float acc) {

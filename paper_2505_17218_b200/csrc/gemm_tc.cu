@@ -1,24 +1,30 @@
-// tcgen05 tensor-core GEMM for sm_100a (bf16 x bf16 -> fp32 in TMEM).
+// tcgen05 tensor-core GEMM for sm_100a (bf16 x bf16 -> fp32 in TMEM), persistent.
 //
 //   C[M x N] = epilogue(A(m, k) . B(n, k)),  operands K-major or MN-major.
 //
-// Warp roles per CTA (256 threads, one 128 x BN output tile):
-//   warp 0      TMA producer: 128B-swizzled tiles of A and B into a STAGES-deep
-//               shared-memory ring (cp.async.bulk.tensor + mbarrier complete_tx)
-//   warp 1      MMA issuer: one elected thread issues tcgen05.mma (M=128, N=BN,
-//               K=16) into a TMEM accumulator; tcgen05.commit frees the smem slot
-//   warp 2      TMEM allocator (BN columns)
-//   warps 4..7  epilogue: tcgen05.ld 32 columns at a time -> bias / tanh /
-//               dtanh / residual / fp32 accumulate -> global
+// One CTA per SM loops over 128 x BN output tiles (M fastest, so CTAs running
+// together share the same B (weight) tile through L2). Warp roles:
+//   warp 0      TMA producer: 128B-swizzled A/B k-blocks into a STAGES-deep
+//               shared-memory ring that runs continuously across tiles
+//   warp 1      MMA issuer: one thread issues tcgen05.mma (M=128, N=BN, K=16)
+//               into one of TWO TMEM accumulators, so the epilogue of tile i
+//               overlaps the MMAs of tile i+1; tcgen05.commit frees smem slots
+//               and publishes finished accumulators
+//   warp 2      TMEM allocator (2 x BN columns)
+//   warps 4..   epilogue (EPW warps): tcgen05.ld 32 columns at a time -> bias /
+//               tanh / dtanh / residual / fp32 accumulate (16-byte vector I/O),
+//               or the fused LM-head sampling reduction (Gumbel argmax + LSE)
 // Operand major-ness is encoded in the UMMA instruction descriptor (bits 15/16)
 // and the shared-memory descriptors (K-major: SBO = 1024 B between 8-row groups;
 // MN-major: LBO = one 64-element TMA box, SBO = 1024 B between 8-k groups).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cfloat>
 #include <mutex>
 
 #include "gemm.cuh"
+#include "rule.cuh"
 
 namespace dashcu {
 
@@ -37,6 +43,10 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -95,47 +105,187 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int BN, int STAGES, bool AK, bool BKM>
+template <int BN, int STAGES, bool AK, bool BKM, int EPW>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int THREADS = 128 + EPW * 32;
   // kind::f16 instruction descriptor: D f32, A/B bf16, majors, N>>3, M>>4
   static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((AK ? 0u : 1u) << 15) |
                                     ((BKM ? 0u : 1u) << 16) | (static_cast<uint32_t>(BN >> 3) << 17) |
                                     (static_cast<uint32_t>(BM >> 4) << 24);
 };
 
-template <int BN, int STAGES, bool AK, bool BKM>
-__global__ void __launch_bounds__(256, 2)
+// Generic epilogue on columns [c_lo, c_hi) of one accumulator row.
+__device__ __forceinline__ void epilogue_store(const GemmShape& g, const Epi& e, uint32_t taddr, int row, int n0,
+                                               int c_lo, int c_hi, bool vec) {
+  float v[32];
+#pragma unroll 1
+  for (int c = c_lo; c < c_hi; c += 32) {
+    tmem_ld32(taddr + c, v);
+    if (row >= g.M) continue;
+    const int nb = n0 + c;
+    if (vec && nb + 32 <= g.N) {
+      const int64_t r64 = row;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] *= e.alpha;
+      if (e.bias) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 b = *reinterpret_cast<const float4*>(e.bias + nb + i);
+          v[i] += b.x, v[i + 1] += b.y, v[i + 2] += b.z, v[i + 3] += b.w;
+        }
+      }
+      if (e.kind == EPI_TANH) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = tanhf(v[i]);
+      }
+      if (e.kind == EPI_DTANH) {
+        const bf16* ap = static_cast<const bf16*>(e.aux) + r64 * e.ld_aux + nb;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          const uint4 raw = *reinterpret_cast<const uint4*>(ap + i);
+          const bf16* a8 = reinterpret_cast<const bf16*>(&raw);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float a = __bfloat162float(a8[k]);
+            v[i + k] *= (1.f - a * a);
+          }
+        }
+      }
+      if (e.resid) {
+        const float* rp = e.resid + r64 * e.ldr + nb;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 x = *reinterpret_cast<const float4*>(rp + i);
+          v[i] += x.x, v[i + 1] += x.y, v[i + 2] += x.z, v[i + 3] += x.w;
+        }
+      }
+      if (e.kind == EPI_ACCUM) {
+        float* cp = e.c32 + r64 * e.ldc32 + nb;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          float4 x = *reinterpret_cast<float4*>(cp + i);
+          x.x += v[i], x.y += v[i + 1], x.z += v[i + 2], x.w += v[i + 3];
+          *reinterpret_cast<float4*>(cp + i) = x;
+        }
+        continue;
+      }
+      if (e.c32) {
+        float* cp = e.c32 + r64 * e.ldc32 + nb;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(cp + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      }
+      if (e.cT) {
+        bf16* cp = static_cast<bf16*>(e.cT) + r64 * e.ldcT + nb;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 o;
+          o.x = pack2(v[i], v[i + 1]);
+          o.y = pack2(v[i + 2], v[i + 3]);
+          o.z = pack2(v[i + 4], v[i + 5]);
+          o.w = pack2(v[i + 6], v[i + 7]);
+          *reinterpret_cast<uint4*>(cp + i) = o;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int n = nb + i;
+        if (n < g.N) epi_apply<bf16>(e, row, n, v[i]);
+      }
+    }
+  }
+}
+
+// LM-head sampling epilogue on columns [c_lo, c_hi): Gumbel-max argmax + T=1 LSE,
+// one 5-float partial record per (row, column slice).
+__device__ __forceinline__ void epilogue_sample(const GemmShape& g, const Epi& e, const SampleArgs& sa, uint32_t taddr,
+                                                int row, int n0, int c_lo, int c_hi, int slice) {
+  float v[32];
+  const bool live = row < g.M;
+  const uint32_t rk = live ? row_key(sa.keys[row], sa.step) : 0u;
+  float bs = -FLT_MAX, bl = 0.f, mx = -FLT_MAX, se = 0.f;
+  int bi = 0x7fffffff;
+#pragma unroll 1
+  for (int c = c_lo; c < c_hi; c += 32) {
+    tmem_ld32(taddr + c, v);
+    if (!live) continue;
+    const int nb = n0 + c;
+    float cm = -FLT_MAX;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int n = nb + i;
+      const bool ok = n < g.N && n != sa.bos;
+      const float l = n < g.N ? v[i] + e.bias[n] : 0.f;
+      if (sa.dump && n < g.N) sa.dump[static_cast<int64_t>(row) * sa.dump_ld + n] = l;
+      v[i] = ok ? l : -FLT_MAX;
+      cm = fmaxf(cm, v[i]);
+      if (ok) {
+        const float sc = gumbel_score(l, sa.inv_t, rk, n);
+        if (better(sc, n, bs, bi)) {
+          bs = sc;
+          bi = n;
+          bl = l;
+        }
+      }
+    }
+    if (cm > -FLT_MAX) {
+      const float nm = fmaxf(mx, cm);
+      float acc = se * __expf(mx - nm);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc += v[i] > -FLT_MAX ? __expf(v[i] - nm) : 0.f;
+      se = acc;
+      mx = nm;
+    }
+  }
+  if (live) {
+    float* pp = sa.part + (static_cast<int64_t>(row) * sa.ntiles + slice) * 5;
+    pp[0] = bs;
+    pp[1] = __int_as_float(bi);
+    pp[2] = bl;
+    pp[3] = mx;
+    pp[4] = se;
+  }
+}
+
+template <int BN, int STAGES, bool AK, bool BKM, int EPW, bool SAMPLE>
+__global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, GemmShape g,
-                   Epi e) {
-  using C = Cfg<BN, STAGES, AK, BKM>;
+                   Epi e, SampleArgs sa) {
+  using C = Cfg<BN, STAGES, AK, BKM, EPW>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int nkb = (g.K + BK - 1) / BK;
+  const int tiles_m = (g.M + BM - 1) / BM, tiles_n = (g.N + BN - 1) / BN;
+  const int ntile = tiles_m * tiles_n;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tfull, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], EPW * 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(BN));
+                 "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -145,141 +295,92 @@ __global__ void __launch_bounds__(256, 2)
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* sa = smem + s * C::STAGE_BYTES;
-        uint8_t* sb = sa + C::A_BYTES;
-        mbar_expect_tx(&full[s], C::STAGE_BYTES);
-        const int k0 = kb * BK;
-        if (AK) {
-          tma_load_2d(sa, &mapA, &full[s], k0, m0);
-        } else {
-          tma_load_2d(sa, &mapA, &full[s], m0, k0);
-          tma_load_2d(sa + 64 * BK * 2, &mapA, &full[s], m0 + 64, k0);
-        }
-        if (BKM) {
-          tma_load_2d(sb, &mapB, &full[s], k0, n0);
-        } else {
+      int kb_all = 0;
+      for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+        const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
+        for (int kb = 0; kb < nkb; ++kb, ++kb_all) {
+          const int s = kb_all % STAGES;
+          const uint32_t ph = (kb_all / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* sa_ = smem + s * C::STAGE_BYTES;
+          uint8_t* sb_ = sa_ + C::A_BYTES;
+          mbar_expect_tx(&full[s], C::STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (AK) {
+            tma_load_2d(sa_, &mapA, &full[s], k0, m0);
+          } else {
+            tma_load_2d(sa_, &mapA, &full[s], m0, k0);
+            tma_load_2d(sa_ + 64 * BK * 2, &mapA, &full[s], m0 + 64, k0);
+          }
+          if (BKM) {
+            tma_load_2d(sb_, &mapB, &full[s], k0, n0);
+          } else {
 #pragma unroll
-          for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 64 * BK * 2, &mapB, &full[s], n0 + 64 * j, k0);
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb_ + j * 64 * BK * 2, &mapB, &full[s], n0 + 64 * j, k0);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&full[s], ph);
+      int kb_all = 0, i = 0;
+      for (int t = blockIdx.x; t < ntile; t += gridDim.x, ++i) {
+        const int acc = i & 1;
+        const uint32_t aph = (i >> 1) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t sa = smem_u32(smem + s * C::STAGE_BYTES);
-        const uint32_t sb = sa + C::A_BYTES;
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb, ++kb_all) {
+          const int s = kb_all % STAGES;
+          const uint32_t ph = (kb_all / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa_ = smem_u32(smem + s * C::STAGE_BYTES);
+          const uint32_t sb_ = sa_ + C::A_BYTES;
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          // K-major: advance 32 B inside the swizzle row; MN-major: advance 16 k-rows (2 x 1024 B)
-          const uint64_t da = AK ? smem_desc(sa + k * 32, 16, 1024) : smem_desc(sa + k * 2048, 64 * BK * 2, 1024);
-          const uint64_t db = BKM ? smem_desc(sb + k * 32, 16, 1024) : smem_desc(sb + k * 2048, 64 * BK * 2, 1024);
-          umma_bf16(tmem, da, db, C::IDESC, (kb > 0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: advance 32 B inside the swizzle row; MN-major: advance 16 k-rows (2 x 1024 B)
+            const uint64_t da = AK ? smem_desc(sa_ + k * 32, 16, 1024) : smem_desc(sa_ + k * 2048, 64 * BK * 2, 1024);
+            const uint64_t db = BKM ? smem_desc(sb_ + k * 32, 16, 1024) : smem_desc(sb_ + k * 2048, 64 * BK * 2, 1024);
+            umma_bf16(d, da, db, C::IDESC, (kb > 0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);
         }
-        umma_commit(&empty[s]);
+        umma_commit(&tfull[acc]);
       }
-      umma_commit(tfull);
     }
   } else if (warp >= 4) {
-    const int q = warp - 4;  // TMEM lane quarter
-    const int row = m0 + q * 32 + lane;
-    mbar_wait(tfull, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    float v[32];
-    // 16-byte vector path: every pointer / leading dim the epilogue touches is 16-B aligned
+    const int ew = warp - 4;
+    const int q = ew & 3;                  // TMEM lane quarter (warp % 4 rule)
+    const int slice = ew >> 2;             // column slice handled by this warp
+    constexpr int NSL = EPW / 4;
+    constexpr int CW = BN / NSL;
     auto al = [](const void* p, int64_t ld, int esz) {
       return p == nullptr || (((reinterpret_cast<uintptr_t>(p) | static_cast<uintptr_t>(ld * esz)) & 15) == 0);
     };
-    const bool vec = al(e.c32, e.ldc32, 4) && al(e.cT, e.ldcT, 2) && al(e.resid, e.ldr, 4) && al(e.aux, e.ld_aux, 2) &&
-                     al(e.bias, 0, 4);
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
-      if (row >= g.M) continue;
-      const int nb = n0 + c;
-      if (vec && nb + 32 <= g.N) {
-        const int64_t r64 = row;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] *= e.alpha;
-        if (e.bias) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 b = *reinterpret_cast<const float4*>(e.bias + nb + i);
-            v[i] += b.x, v[i + 1] += b.y, v[i + 2] += b.z, v[i + 3] += b.w;
-          }
-        }
-        if (e.kind == EPI_TANH) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = tanhf(v[i]);
-        }
-        if (e.kind == EPI_DTANH) {
-          const bf16* ap = static_cast<const bf16*>(e.aux) + r64 * e.ld_aux + nb;
-#pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            const uint4 raw = *reinterpret_cast<const uint4*>(ap + i);
-            const bf16* a8 = reinterpret_cast<const bf16*>(&raw);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const float a = __bfloat162float(a8[k]);
-              v[i + k] *= (1.f - a * a);
-            }
-          }
-        }
-        if (e.resid) {
-          const float* rp = e.resid + r64 * e.ldr + nb;
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 x = *reinterpret_cast<const float4*>(rp + i);
-            v[i] += x.x, v[i + 1] += x.y, v[i + 2] += x.z, v[i + 3] += x.w;
-          }
-        }
-        if (e.kind == EPI_ACCUM) {
-          float* cp = e.c32 + r64 * e.ldc32 + nb;
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            float4 x = *reinterpret_cast<float4*>(cp + i);
-            x.x += v[i], x.y += v[i + 1], x.z += v[i + 2], x.w += v[i + 3];
-            *reinterpret_cast<float4*>(cp + i) = x;
-          }
-          continue;
-        }
-        if (e.c32) {
-          float* cp = e.c32 + r64 * e.ldc32 + nb;
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(cp + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-        }
-        if (e.cT) {
-          bf16* cp = static_cast<bf16*>(e.cT) + r64 * e.ldcT + nb;
-#pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            uint4 o;
-            o.x = pack2(v[i], v[i + 1]);
-            o.y = pack2(v[i + 2], v[i + 3]);
-            o.z = pack2(v[i + 4], v[i + 5]);
-            o.w = pack2(v[i + 6], v[i + 7]);
-            *reinterpret_cast<uint4*>(cp + i) = o;
-          }
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int n = nb + i;
-          if (n < g.N) epi_apply<bf16>(e, row, n, v[i]);
-        }
-      }
+    const bool vec = al(e.c32, e.ldc32, 4) && al(e.cT, e.ldcT, 2) && al(e.resid, e.ldr, 4) &&
+                     al(e.aux, e.ld_aux, 2) && al(e.bias, 0, 4);
+    int i = 0;
+    for (int t = blockIdx.x; t < ntile; t += gridDim.x, ++i) {
+      const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
+      const int acc = i & 1;
+      const uint32_t aph = (i >> 1) & 1;
+      mbar_wait(&tfull[acc], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+      const int row = m0 + q * 32 + lane;
+      if constexpr (SAMPLE)
+        epilogue_sample(g, e, sa, taddr, row, n0, slice * CW, (slice + 1) * CW, (t / tiles_m) * NSL + slice);
+      else
+        epilogue_store(g, e, taddr, row, n0, slice * CW, (slice + 1) * CW, vec);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&tempty[acc]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 2) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
   }
 }
 
@@ -310,38 +411,79 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int6
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, int STAGES, bool AK, bool BKM>
-void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& g, const Epi& e) {
-  using C = Cfg<BN, STAGES, AK, BKM>;
-  auto k = gemm_tc_kernel<BN, STAGES, AK, BKM>;
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = kNumSMs;
+  }
+  return n;
+}
+
+template <int BN, int STAGES, bool AK, bool BKM, int EPW, bool SAMPLE>
+void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& g, const Epi& e,
+            const SampleArgs& sa) {
+  using C = Cfg<BN, STAGES, AK, BKM, EPW>;
+  auto k = gemm_tc_kernel<BN, STAGES, AK, BKM, EPW, SAMPLE>;
   static bool attr = false;
   if (!attr) {
     DCU_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
-  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM);
-  ProfScope ps(PROF_GEMM_TC, s, 2.0 * g.M * g.N * static_cast<double>(g.K), 0);
-  k<<<grid, 256, C::SMEM, s>>>(ma, mb, g, e);
+  const int ntile = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+  const int grid = ntile < num_sms() ? ntile : num_sms();
+  ProfScope ps(SAMPLE ? PROF_SAMPLE : PROF_GEMM_TC, s, 2.0 * g.M * g.N * static_cast<double>(g.K), 0);
+  k<<<grid, C::THREADS, C::SMEM, s>>>(ma, mb, g, e, sa);
   DCU_LAUNCHED();
 }
+
+template <int BN, int STAGES>
+void dispatch_majors(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& g, const Epi& e) {
+  const SampleArgs none;
+  if (g.a_kmajor && g.b_kmajor) launch<BN, STAGES, true, true, 4, false>(s, ma, mb, g, e, none);
+  else if (g.a_kmajor) launch<BN, STAGES, true, false, 4, false>(s, ma, mb, g, e, none);
+  else if (g.b_kmajor) launch<BN, STAGES, false, true, 4, false>(s, ma, mb, g, e, none);
+  else launch<BN, STAGES, false, false, 4, false>(s, ma, mb, g, e, none);
+}
+
+bool legal(const GemmShape& g) {
+  if (g.K <= 0 || g.M <= 0 || g.N <= 0) return false;
+  const uintptr_t pa = reinterpret_cast<uintptr_t>(g.A), pb = reinterpret_cast<uintptr_t>(g.B);
+  return !((pa & 15) || (pb & 15) || ((g.lda * 2) & 15) || ((g.ldb * 2) & 15));
+}
+
+constexpr int kSampleBN = 256;
+constexpr int kSampleEPW = 8;  // two column slices per accumulator row: the Gumbel math is ALU-heavy
 
 }  // namespace
 
 bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e) {
-  if (g.K <= 0 || g.M <= 0 || g.N <= 0) return false;
-  const uintptr_t pa = reinterpret_cast<uintptr_t>(g.A), pb = reinterpret_cast<uintptr_t>(g.B);
-  if ((pa & 15) || (pb & 15) || ((g.lda * 2) & 15) || ((g.ldb * 2) & 15)) return false;
-  constexpr int BN = 128;
+  if (!legal(g)) return false;
+  // 128 x 256 tiles unless N is small or a 256-multiple would waste a half tile
+  const bool wide = g.N >= 2048 || (g.N % 256 == 0);
+  const int BN = wide ? 256 : 128;
   CUtensorMap ma, mb;
   bool ok = g.a_kmajor ? make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) : make_map(&ma, g.A, g.K, g.M, g.lda, 64, BK);
   ok = ok && (g.b_kmajor ? make_map(&mb, g.B, g.N, g.K, g.ldb, BK, BN) : make_map(&mb, g.B, g.K, g.N, g.ldb, 64, BK));
   if (!ok) return false;
-  // 3 stages x 32 KB: two CTAs per SM, so one CTA's epilogue overlaps the other's mainloop
-  if (g.a_kmajor && g.b_kmajor) launch<BN, 3, true, true>(s, ma, mb, g, e);
-  else if (g.a_kmajor) launch<BN, 3, true, false>(s, ma, mb, g, e);
-  else if (g.b_kmajor) launch<BN, 3, false, true>(s, ma, mb, g, e);
-  else launch<BN, 3, false, false>(s, ma, mb, g, e);
+  if (wide) dispatch_majors<256, 4>(s, ma, mb, g, e);   // 4 x 48 KB stages
+  else dispatch_majors<128, 6>(s, ma, mb, g, e);        // 6 x 32 KB stages
   return true;
+}
+
+int gemm_tc_sample_tiles(int N) { return ((N + kSampleBN - 1) / kSampleBN) * (kSampleEPW / 4); }
+
+int gemm_tc_sample(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa) {
+  if (!legal(g) || !g.a_kmajor || !g.b_kmajor) return 0;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) || !make_map(&mb, g.B, g.N, g.K, g.ldb, BK, kSampleBN)) return 0;
+  Epi e;
+  e.bias = bias;
+  SampleArgs a = sa;
+  a.ntiles = gemm_tc_sample_tiles(g.N);
+  launch<kSampleBN, 4, true, true, kSampleEPW, true>(s, ma, mb, g, e, a);
+  return a.ntiles;
 }
 
 }  // namespace dashcu

@@ -73,6 +73,11 @@ void sample_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, 
                  const uint64_t* keys, int step, const int32_t* cap, uint8_t* finished, int32_t* comp,
                  float* logp, int32_t* len, int32_t* tok_next, int max_len, float* dump);
 
+// Combine of the fused LM-head sampling partials (gemm_tc_sample) + the same token
+// bookkeeping as sample_rows.
+void sample_reduce(cudaStream_t s, const float* part, int ntiles, int rows, int eos, int step, const int32_t* cap,
+                   uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len);
+
 // ---- LM-head loss rows (policy.cpp:471-483) ------------------------------------------
 // For each loss row r: lse over non-BOS logits; logp[r] = logit[y_r] - lse;
 // if dz != null: dz[r][i] = w_r * (onehot(y_r) - softmax)_i, BOS column 0.

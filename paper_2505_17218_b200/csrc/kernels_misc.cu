@@ -235,6 +235,62 @@ __global__ void __launch_bounds__(256) sample_rows_k(const float* logits, int V,
   }
 }
 
+// Cross-tile combine of the fused LM-head sampling partials (one warp per row):
+// argmax of the Gumbel scores (ties -> lowest id) and the T=1 log-sum-exp.
+__global__ void __launch_bounds__(256) sample_reduce_k(const float* __restrict__ part, int ntiles, int rows, int eos,
+                                                       int step, const int32_t* cap, uint8_t* finished, int32_t* comp,
+                                                       float* logp, int32_t* len, int32_t* tok_next, int max_len) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const bool active = !finished[row] && step < cap[row];
+  if (!active) {
+    if (lane == 0) tok_next[row] = eos;
+    return;
+  }
+  float bs = -FLT_MAX, bl = 0.f, mx = -FLT_MAX, se = 0.f;
+  int bi = 0x7fffffff;
+  for (int t = lane; t < ntiles; t += 32) {
+    const float* p = part + (static_cast<int64_t>(row) * ntiles + t) * 5;
+    const float s = p[0], l = p[2], m2 = p[3], s2 = p[4];
+    const int i = __float_as_int(p[1]);
+    if (better(s, i, bs, bi)) {
+      bs = s;
+      bi = i;
+      bl = l;
+    }
+    if (m2 > -FLT_MAX) {
+      const float nm = fmaxf(mx, m2);
+      se = se * __expf(mx - nm) + s2 * __expf(m2 - nm);
+      mx = nm;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float s = __shfl_xor_sync(0xffffffffu, bs, o);
+    const int i = __shfl_xor_sync(0xffffffffu, bi, o);
+    const float l = __shfl_xor_sync(0xffffffffu, bl, o);
+    if (better(s, i, bs, bi)) {
+      bs = s;
+      bi = i;
+      bl = l;
+    }
+    const float m2 = __shfl_xor_sync(0xffffffffu, mx, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, se, o);
+    const float nm = fmaxf(mx, m2);
+    if (nm > -FLT_MAX) {
+      se = se * __expf(mx - nm) + s2 * __expf(m2 - nm);
+      mx = nm;
+    }
+  }
+  if (lane == 0) {
+    comp[static_cast<int64_t>(row) * max_len + step] = bi;
+    logp[static_cast<int64_t>(row) * max_len + step] = bl - (mx + logf(se));
+    len[row] = step + 1;
+    if (bi == eos) finished[row] = 1;
+    tok_next[row] = bi;
+  }
+}
+
 template <class T>
 __global__ void __launch_bounds__(256) lm_rows_k(const float* logits, int V, int bos, const int32_t* target,
                                                  const float* weight, float* logp, T* dz) {
@@ -456,6 +512,13 @@ void sample_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, 
   ProfScope ps(PROF_SAMPLE, s, 0, 4.0 * rows * static_cast<double>(V));
   sample_rows_k<<<rows, 256, 0, s>>>(logits, V, bos, eos, inv_t, keys, step, cap, finished, comp, logp, len, tok_next,
                                      max_len, dump);
+  DCU_LAUNCHED();
+}
+
+void sample_reduce(cudaStream_t s, const float* part, int ntiles, int rows, int eos, int step, const int32_t* cap,
+                   uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len) {
+  sample_reduce_k<<<cdiv(rows, 8), 256, 0, s>>>(part, ntiles, rows, eos, step, cap, finished, comp, logp, len, tok_next,
+                                                max_len);
   DCU_LAUNCHED();
 }
 

@@ -667,12 +667,36 @@ struct Engine {
                          g.hd, kp + kvp * l, vp + kvp * l);
     T* yT = ws.get<T>("d_yT", static_cast<size_t>(S) * g.d);
     gather_rows<T>(st, A.yT, g.d, d_last, S, g.d, yT);
-    float* logits = ws.get<float>("d_logits", static_cast<size_t>(S) * g.V);
-    Epi el = store(logits, g.V, nullptr, 0);
-    el.bias = W32(L.bout);
-    mm(S, g.V, g.d, yT, g.d, true, W(L.wout), g.d, true, el);
-    sample_rows(st, logits, S, g.V, g.bos, g.eos, inv_t, d_keys, 0, d_cap, d_fin, P.d_comp.as<int32_t>(),
-                P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML, dump);
+    // LM head + sampling step: fused tcgen05 epilogue (bf16) or GEMM + row kernel (fp32 parity path)
+    float* logits = nullptr;
+    float* part = nullptr;
+    if constexpr (sizeof(T) == 2) part = ws.get<float>("d_part", static_cast<size_t>(S) * gemm_tc_sample_tiles(g.V) * 5);
+    auto lm_sample = [&](const T* yrows, int step) {
+      if constexpr (sizeof(T) == 2) {
+        SampleArgs sa;
+        sa.keys = d_keys;
+        sa.step = step;
+        sa.inv_t = inv_t;
+        sa.bos = g.bos;
+        sa.part = part;
+        sa.dump = dump ? dump + static_cast<int64_t>(step) * g.V : nullptr;
+        sa.dump_ld = static_cast<int64_t>(std::max(ML, 1)) * g.V;
+        GemmShape gs{S, g.V, g.d, yrows, g.d, true, W(L.wout), g.d, true};
+        const int nt = gemm_tc_sample(st, gs, W32(L.bout), sa);
+        if (nt > 0) {
+          sample_reduce(st, part, nt, S, g.eos, step, d_cap, d_fin, P.d_comp.as<int32_t>(), P.d_logp.as<float>(),
+                        P.d_len.as<int32_t>(), d_tok, ML);
+          return;
+        }
+      }
+      if (!logits) logits = ws.get<float>("d_logits", static_cast<size_t>(S) * g.V);
+      Epi el = store(logits, g.V, nullptr, 0);
+      el.bias = W32(L.bout);
+      mm(S, g.V, g.d, yrows, g.d, true, W(L.wout), g.d, true, el);
+      sample_rows(st, logits, S, g.V, g.bos, g.eos, inv_t, d_keys, step, d_cap, d_fin, P.d_comp.as<int32_t>(),
+                  P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML, dump);
+    };
+    lm_sample(yT, 0);
 
     // Decode steps.
     float* x32 = ws.get<float>("d_x32", static_cast<size_t>(S) * g.d);
@@ -712,9 +736,7 @@ struct Engine {
         e2.ldr = g.d;
         mm(S, g.d, g.H, u, g.H, true, W(b + L.w2), g.H, true, e2);
       }
-      mm(S, g.V, g.d, xT, g.d, true, W(L.wout), g.d, true, el);
-      sample_rows(st, logits, S, g.V, g.bos, g.eos, inv_t, d_keys, j, d_cap, d_fin, P.d_comp.as<int32_t>(),
-                  P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML, dump);
+      lm_sample(xT, j);
       if ((j & 31) == 0 && g.eos >= 0) {  // retire the round early once every sequence hit EOS
         d2h(st, hfin.data(), d_fin, S);
         DCU_CHECK(cudaStreamSynchronize(st));

@@ -25,7 +25,7 @@ def ctx():
 
 
 SHAPES = [(128, 128, 64), (256, 384, 128), (200, 136, 72), (77, 300, 1000), (1024, 896, 896), (36, 1152, 896),
-          (896, 4864, 517)]
+          (896, 4864, 517), (4096, 4864, 256), (2000, 1152, 300), (3000, 2048, 128)]   # last 3: several tiles/CTA
 
 
 @pytest.mark.parametrize("ak", [True, False])

@@ -29,6 +29,9 @@ GQA128 = dict(vocab_size=64, embed_dim=128, context_len=48, ffn_hidden=128, n_la
               n_heads=4, n_kv_heads=2, head_dim=128)
 LONG = dict(vocab_size=64, embed_dim=128, context_len=200, ffn_hidden=128, n_layers=1, bos_id=0, eos_id=1,
             n_heads=2, n_kv_heads=1, head_dim=64)
+# vocab spanning many fused-sampling tiles (ragged last tile)
+VBIG = dict(vocab_size=5003, embed_dim=64, context_len=32, ffn_hidden=64, n_layers=1, bos_id=0, eos_id=1,
+            n_heads=1, n_kv_heads=1, head_dim=64)
 TOL = {D.F32: 1e-3, D.BF16: 2e-2}
 
 
@@ -127,7 +130,7 @@ def test_advantage_filter_large_and_errors(ctx):
 # ---------------------------------------------------------------- sampling
 
 @pytest.mark.parametrize("dtype", [D.F32, D.BF16])
-@pytest.mark.parametrize("arch", [C1, GQA, QWENLIKE, GQA128], ids=["c1", "gqa", "qwenlike", "gqa128"])
+@pytest.mark.parametrize("arch", [C1, GQA, QWENLIKE, GQA128, VBIG], ids=["c1", "gqa", "qwenlike", "gqa128", "vbig"])
 def test_sampled_tokens_bit_exact_under_logits_dump(ctx, arch, dtype):
     pol = D.Policy(ctx, arch, dtype)
     pol.upload(params32(arch, 0.5, 3))
