@@ -201,6 +201,11 @@ DASHCU_API int dashcu_profile_read(dashcu_kprof* out, int max, int reset);
 DASHCU_API int dashcu_selftest_gemm(dashcu_ctx* ctx, int M, int N, int K, const uint16_t* A, int64_t lda,
                                     int a_kmajor, const uint16_t* B, int64_t ldb, int b_kmajor, const float* bias,
                                     int epi, int force_simt, float* C);
+/* Timing harness: `iters` launches of the production GEMM on device-resident random
+ * bf16 operands, bf16 output (epi 0) or fp32 accumulate (epi 3); mean ms per launch
+ * from CUDA events on the context stream. */
+DASHCU_API int dashcu_selftest_gemm_timed(dashcu_ctx* ctx, int M, int N, int K, int a_kmajor, int b_kmajor, int epi,
+                                          int iters, double* ms);
 /* Whole-library count of kernel launches (all policies, all contexts). */
 DASHCU_API int64_t dashcu_kernel_launches(void);
 

@@ -49,16 +49,28 @@ struct GemmShape {
 // logits never leave the SM. Per (row, N tile) the epilogue writes 5 floats
 //   {best Gumbel score, best id (bit pattern), logit of best, max logit, sum exp(logit - max)}
 // over non-BOS ids; sample_reduce combines the tiles of a row.
+// The same tile machinery also runs the LM-head backward without ever storing
+// fp32 logits (policy.cpp:471-483): pass 1 (LSE mode) writes per (row, slice)
+// {max, sum exp} partials, lse_reduce makes the row LSE; pass 2 (DZ mode)
+// recomputes the logits and writes dz = w_r (onehot(y_r) - softmax) in bf16.
 struct SampleArgs {
   const uint64_t* keys = nullptr;  // per-row sequence key derive_seed(round, "sample", m, g)
   int step = 0;
   float inv_t = 1.f;
   int bos = -1;
-  float* part = nullptr;  // [rows][ntiles][5]
+  float* part = nullptr;  // [rows][ntiles][5] (sample) or [rows][ntiles][2] (lse)
   int ntiles = 0;
   float* dump = nullptr;  // optional: logits row r at dump + r * dump_ld (debug / parity)
   int64_t dump_ld = 0;
+  const float* lse = nullptr;      // DZ: per-row log-sum-exp over non-BOS logits
+  const int32_t* target = nullptr; // DZ: per-row target id
+  const float* weight = nullptr;   // DZ: per-row weight w_r = A_n / N
+  bf16* dz = nullptr;              // DZ: [rows][ld_dz]
+  int64_t ld_dz = 0;
 };
+int gemm_tc_lse(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa);
+bool gemm_tc_dz(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa);
+int gemm_tc_lse_tiles(int N);
 
 // dtype: 0 fp32 (CUDA cores), 1 bf16 (tcgen05 when the operands are TMA-legal)
 void gemm(cudaStream_t s, int dtype, const GemmShape& g, const Epi& e);

@@ -216,20 +216,40 @@ __device__ __forceinline__ void epilogue_sample(const GemmShape& g, const Epi& e
     if (!live) continue;
     const int nb = n0 + c;
     float cm = -FLT_MAX;
+    if (nb + 32 <= g.N && (reinterpret_cast<uintptr_t>(e.bias + nb) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const float4 b = *reinterpret_cast<const float4*>(e.bias + nb + i);
+        v[i] += b.x, v[i + 1] += b.y, v[i + 2] += b.z, v[i + 3] += b.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = nb + i < g.N ? v[i] + e.bias[nb + i] : 0.f;
+    }
+    if (sa.dump) {
+      for (int i = 0; i < 32; ++i)
+        if (nb + i < g.N) sa.dump[static_cast<int64_t>(row) * sa.dump_ld + nb + i] = v[i];
+    }
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       const int n = nb + i;
-      const bool ok = n < g.N && n != sa.bos;
-      const float l = n < g.N ? v[i] + e.bias[n] : 0.f;
-      if (sa.dump && n < g.N) sa.dump[static_cast<int64_t>(row) * sa.dump_ld + n] = l;
-      v[i] = ok ? l : -FLT_MAX;
+      v[i] = (n < g.N && n != sa.bos) ? v[i] : -FLT_MAX;
       cm = fmaxf(cm, v[i]);
-      if (ok) {
-        const float sc = gumbel_score(l, sa.inv_t, rk, n);
+    }
+    // exact Gumbel-max with a conservative filter: only draws that could beat the
+    // running best are pushed through the (expensive) exact score
+    const float kthr = gumbel_draw_threshold(bs, cm, sa.inv_t);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int n = nb + i;
+      if (v[i] == -FLT_MAX) continue;
+      const uint32_t k = gumbel_draw(rk, n);
+      if (static_cast<float>(k) > kthr) {
+        const float sc = __fmaf_rn(v[i], sa.inv_t, gumbel_of_draw(k));
         if (better(sc, n, bs, bi)) {
           bs = sc;
           bi = n;
-          bl = l;
+          bl = v[i];
         }
       }
     }
@@ -252,7 +272,81 @@ __device__ __forceinline__ void epilogue_sample(const GemmShape& g, const Epi& e
   }
 }
 
-template <int BN, int STAGES, bool AK, bool BKM, int EPW, bool SAMPLE>
+// LM-head backward pass 1: per (row, slice) {max, sum exp} of the non-BOS logits.
+__device__ __forceinline__ void epilogue_lse(const GemmShape& g, const Epi& e, const SampleArgs& sa, uint32_t taddr,
+                                             int row, int n0, int c_lo, int c_hi, int slice) {
+  float v[32];
+  const bool live = row < g.M;
+  float mx = -FLT_MAX, se = 0.f;
+#pragma unroll 1
+  for (int c = c_lo; c < c_hi; c += 32) {
+    tmem_ld32(taddr + c, v);
+    if (!live) continue;
+    const int nb = n0 + c;
+    float cm = -FLT_MAX;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int n = nb + i;
+      v[i] = (n < g.N && n != sa.bos) ? v[i] + e.bias[n] : -FLT_MAX;
+      cm = fmaxf(cm, v[i]);
+    }
+    if (cm > -FLT_MAX) {
+      const float nm = fmaxf(mx, cm);
+      float acc = se * __expf(mx - nm);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc += v[i] > -FLT_MAX ? __expf(v[i] - nm) : 0.f;
+      se = acc;
+      mx = nm;
+    }
+  }
+  if (live) {
+    float* pp = sa.part + (static_cast<int64_t>(row) * sa.ntiles + slice) * 2;
+    pp[0] = mx;
+    pp[1] = se;
+  }
+}
+
+// LM-head backward pass 2: dz = w_r (onehot(y_r) - exp(logit - lse_r)), BOS column 0, bf16.
+__device__ __forceinline__ void epilogue_dz(const GemmShape& g, const Epi& e, const SampleArgs& sa, uint32_t taddr,
+                                            int row, int n0, int c_lo, int c_hi) {
+  float v[32];
+  const bool live = row < g.M;
+  const float lse = live ? sa.lse[row] : 0.f;
+  const float w = live ? sa.weight[row] : 0.f;
+  const int y = live ? sa.target[row] : -1;
+  const bool vec = ((reinterpret_cast<uintptr_t>(sa.dz) | static_cast<uintptr_t>(sa.ld_dz * 2)) & 15) == 0;
+#pragma unroll 1
+  for (int c = c_lo; c < c_hi; c += 32) {
+    tmem_ld32(taddr + c, v);
+    if (!live) continue;
+    const int nb = n0 + c;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int n = nb + i;
+      const float l = n < g.N ? v[i] + e.bias[n] : 0.f;
+      v[i] = (n == sa.bos) ? 0.f : w * ((n == y ? 1.f : 0.f) - __expf(l - lse));
+    }
+    bf16* dst = sa.dz + static_cast<int64_t>(row) * sa.ld_dz + nb;
+    if (vec && nb + 32 <= g.N) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 o;
+        o.x = pack2(v[i], v[i + 1]);
+        o.y = pack2(v[i + 2], v[i + 3]);
+        o.z = pack2(v[i + 4], v[i + 5]);
+        o.w = pack2(v[i + 6], v[i + 7]);
+        *reinterpret_cast<uint4*>(dst + i) = o;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (nb + i < g.N) dst[i] = __float2bfloat16_rn(v[i]);
+    }
+  }
+}
+
+// MODE: 0 generic store epilogue, 1 fused sampling, 2 LSE partials, 3 dz
+template <int BN, int STAGES, bool AK, bool BKM, int EPW, int MODE>
 __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, GemmShape g,
                    Epi e, SampleArgs sa) {
@@ -369,8 +463,12 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       const int row = m0 + q * 32 + lane;
-      if constexpr (SAMPLE)
+      if constexpr (MODE == 1)
         epilogue_sample(g, e, sa, taddr, row, n0, slice * CW, (slice + 1) * CW, (t / tiles_m) * NSL + slice);
+      else if constexpr (MODE == 2)
+        epilogue_lse(g, e, sa, taddr, row, n0, slice * CW, (slice + 1) * CW, (t / tiles_m) * NSL + slice);
+      else if constexpr (MODE == 3)
+        epilogue_dz(g, e, sa, taddr, row, n0, slice * CW, (slice + 1) * CW);
       else
         epilogue_store(g, e, taddr, row, n0, slice * CW, (slice + 1) * CW, vec);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -421,11 +519,11 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, bool AK, bool BKM, int EPW, bool SAMPLE>
+template <int BN, int STAGES, bool AK, bool BKM, int EPW, int MODE>
 void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& g, const Epi& e,
             const SampleArgs& sa) {
   using C = Cfg<BN, STAGES, AK, BKM, EPW>;
-  auto k = gemm_tc_kernel<BN, STAGES, AK, BKM, EPW, SAMPLE>;
+  auto k = gemm_tc_kernel<BN, STAGES, AK, BKM, EPW, MODE>;
   static bool attr = false;
   if (!attr) {
     DCU_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -433,7 +531,8 @@ void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const 
   }
   const int ntile = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   const int grid = ntile < num_sms() ? ntile : num_sms();
-  ProfScope ps(SAMPLE ? PROF_SAMPLE : PROF_GEMM_TC, s, 2.0 * g.M * g.N * static_cast<double>(g.K), 0);
+  ProfScope ps(MODE == 1 ? PROF_SAMPLE : MODE >= 2 ? PROF_LM_ROWS : PROF_GEMM_TC, s,
+               2.0 * g.M * g.N * static_cast<double>(g.K), 0);
   k<<<grid, C::THREADS, C::SMEM, s>>>(ma, mb, g, e, sa);
   DCU_LAUNCHED();
 }
@@ -441,10 +540,10 @@ void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const 
 template <int BN, int STAGES>
 void dispatch_majors(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& g, const Epi& e) {
   const SampleArgs none;
-  if (g.a_kmajor && g.b_kmajor) launch<BN, STAGES, true, true, 4, false>(s, ma, mb, g, e, none);
-  else if (g.a_kmajor) launch<BN, STAGES, true, false, 4, false>(s, ma, mb, g, e, none);
-  else if (g.b_kmajor) launch<BN, STAGES, false, true, 4, false>(s, ma, mb, g, e, none);
-  else launch<BN, STAGES, false, false, 4, false>(s, ma, mb, g, e, none);
+  if (g.a_kmajor && g.b_kmajor) launch<BN, STAGES, true, true, 4, 0>(s, ma, mb, g, e, none);
+  else if (g.a_kmajor) launch<BN, STAGES, true, false, 4, 0>(s, ma, mb, g, e, none);
+  else if (g.b_kmajor) launch<BN, STAGES, false, true, 4, 0>(s, ma, mb, g, e, none);
+  else launch<BN, STAGES, false, false, 4, 0>(s, ma, mb, g, e, none);
 }
 
 bool legal(const GemmShape& g) {
@@ -482,8 +581,32 @@ int gemm_tc_sample(cudaStream_t s, const GemmShape& g, const float* bias, const 
   e.bias = bias;
   SampleArgs a = sa;
   a.ntiles = gemm_tc_sample_tiles(g.N);
-  launch<kSampleBN, 4, true, true, kSampleEPW, true>(s, ma, mb, g, e, a);
+  launch<kSampleBN, 4, true, true, kSampleEPW, 1>(s, ma, mb, g, e, a);
   return a.ntiles;
+}
+
+int gemm_tc_lse_tiles(int N) { return (N + 255) / 256; }
+
+int gemm_tc_lse(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa) {
+  if (!legal(g) || !g.a_kmajor || !g.b_kmajor) return 0;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) || !make_map(&mb, g.B, g.N, g.K, g.ldb, BK, 256)) return 0;
+  Epi e;
+  e.bias = bias;
+  SampleArgs a = sa;
+  a.ntiles = gemm_tc_lse_tiles(g.N);
+  launch<256, 4, true, true, 4, 2>(s, ma, mb, g, e, a);
+  return a.ntiles;
+}
+
+bool gemm_tc_dz(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa) {
+  if (!legal(g) || !g.a_kmajor || !g.b_kmajor) return false;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) || !make_map(&mb, g.B, g.N, g.K, g.ldb, BK, 256)) return false;
+  Epi e;
+  e.bias = bias;
+  launch<256, 4, true, true, 4, 3>(s, ma, mb, g, e, sa);
+  return true;
 }
 
 }  // namespace dashcu

@@ -78,6 +78,10 @@ void sample_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, 
 void sample_reduce(cudaStream_t s, const float* part, int ntiles, int rows, int eos, int step, const int32_t* cap,
                    uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len);
 
+// Row LSE from gemm_tc_lse partials; if logp != null also logp = logit[y] - lse.
+void lse_reduce(cudaStream_t s, const float* part, int ntiles, int rows, float* lse, const bf16* Y, int d,
+                const bf16* W, const float* bias, const int32_t* target, float* logp);
+
 // ---- LM-head loss rows (policy.cpp:471-483) ------------------------------------------
 // For each loss row r: lse over non-BOS logits; logp[r] = logit[y_r] - lse;
 // if dz != null: dz[r][i] = w_r * (onehot(y_r) - softmax)_i, BOS column 0.

@@ -291,6 +291,47 @@ __global__ void __launch_bounds__(256) sample_reduce_k(const float* __restrict__
   }
 }
 
+// Row LSE from the LSE-mode GEMM partials; optionally logp = logit[y] - lse with the
+// target logit recomputed as a bf16 dot product in fp32 (one warp per row).
+__global__ void __launch_bounds__(256) lse_reduce_k(const float* __restrict__ part, int ntiles, int rows,
+                                                    float* __restrict__ lse, const bf16* __restrict__ Y, int d,
+                                                    const bf16* __restrict__ W, const float* __restrict__ bias,
+                                                    const int32_t* __restrict__ target, float* __restrict__ logp) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  float mx = -FLT_MAX, se = 0.f;
+  for (int t = lane; t < ntiles; t += 32) {
+    const float m2 = part[(static_cast<int64_t>(row) * ntiles + t) * 2];
+    const float s2 = part[(static_cast<int64_t>(row) * ntiles + t) * 2 + 1];
+    if (m2 > -FLT_MAX) {
+      const float nm = fmaxf(mx, m2);
+      se = se * __expf(mx - nm) + s2 * __expf(m2 - nm);
+      mx = nm;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, mx, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, se, o);
+    const float nm = fmaxf(mx, m2);
+    if (nm > -FLT_MAX) {
+      se = se * __expf(mx - nm) + s2 * __expf(m2 - nm);
+      mx = nm;
+    }
+  }
+  const float L = mx + logf(se);
+  if (lane == 0) lse[row] = L;
+  if (logp) {
+    const int y = target[row];
+    const bf16* yr = Y + static_cast<int64_t>(row) * d;
+    const bf16* wr = W + static_cast<int64_t>(y) * d;
+    float a = 0.f;
+    for (int i = lane; i < d; i += 32) a += __bfloat162float(yr[i]) * __bfloat162float(wr[i]);
+    a = warp_sum(a);
+    if (lane == 0) logp[row] = a + bias[y] - L;
+  }
+}
+
 template <class T>
 __global__ void __launch_bounds__(256) lm_rows_k(const float* logits, int V, int bos, const int32_t* target,
                                                  const float* weight, float* logp, T* dz) {
@@ -512,6 +553,13 @@ void sample_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, 
   ProfScope ps(PROF_SAMPLE, s, 0, 4.0 * rows * static_cast<double>(V));
   sample_rows_k<<<rows, 256, 0, s>>>(logits, V, bos, eos, inv_t, keys, step, cap, finished, comp, logp, len, tok_next,
                                      max_len, dump);
+  DCU_LAUNCHED();
+}
+
+void lse_reduce(cudaStream_t s, const float* part, int ntiles, int rows, float* lse, const bf16* Y, int d,
+                const bf16* W, const float* bias, const int32_t* target, float* logp) {
+  if (rows <= 0) return;
+  lse_reduce_k<<<cdiv(rows, 8), 256, 0, s>>>(part, ntiles, rows, lse, Y, d, W, bias, target, logp);
   DCU_LAUNCHED();
 }
 

@@ -371,19 +371,48 @@ struct Engine {
   void lm_head(const Acts& A, int R, const int32_t* rows, const int32_t* tgt, const float* w, float* logp,
                bool grad, float* dy32) {
     const int64_t V = g.V;
-    const int RC = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8192, (int64_t(1) << 31) / (V * 4))));
+    // bf16: the logits stay in TMEM (LSE pass + dz pass); fp32 parity path: fp32 logits + row kernel
+    constexpr bool fused = sizeof(T) == 2;
+    const int RC = fused ? static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(16384, (int64_t(5) << 30) / (V * 2))))
+                         : static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8192, (int64_t(1) << 31) / (V * 4))));
     if (grad) fill_f32(st, dy32, 0.f, static_cast<int64_t>(A.T_) * g.d);
     T* ycT = P.ws.get<T>("lm_yc", static_cast<size_t>(RC) * g.d);
-    float* lg = P.ws.get<float>("lm_logits", static_cast<size_t>(RC) * V);
+    float* lg = fused ? nullptr : P.ws.get<float>("lm_logits", static_cast<size_t>(RC) * V);
     T* dz = grad ? P.ws.get<T>("lm_dz", static_cast<size_t>(RC) * V) : nullptr;
     float* dyc = grad ? P.ws.get<float>("lm_dyc", static_cast<size_t>(RC) * g.d) : nullptr;
+    float* part = fused ? P.ws.get<float>("lm_part", static_cast<size_t>(RC) * gemm_tc_lse_tiles(g.V) * 2) : nullptr;
+    float* lse = fused ? P.ws.get<float>("lm_lse", RC) : nullptr;
     for (int r0 = 0; r0 < R; r0 += RC) {
       const int rc = std::min(RC, R - r0);
       gather_rows<T>(st, A.yT, g.d, rows + r0, rc, g.d, ycT);
-      Epi el = store(lg, V, nullptr, 0);
-      el.bias = W32(L.bout);
-      mm(rc, g.V, g.d, ycT, g.d, true, W(L.wout), g.d, true, el);
-      lm_rows<T>(st, lg, rc, g.V, g.bos, tgt + r0, w ? w + r0 : nullptr, logp ? logp + r0 : nullptr, dz);
+      bool done = false;
+      if constexpr (fused) {
+        GemmShape gs{rc, g.V, g.d, ycT, g.d, true, W(L.wout), g.d, true};
+        SampleArgs sa;
+        sa.bos = g.bos;
+        sa.part = part;
+        const int nt = gemm_tc_lse(st, gs, W32(L.bout), sa);
+        if (nt > 0) {
+          lse_reduce(st, part, nt, rc, lse, ycT, g.d, W(L.wout), W32(L.bout), tgt + r0, logp ? logp + r0 : nullptr);
+          if (grad) {
+            sa.lse = lse;
+            sa.target = tgt + r0;
+            sa.weight = w + r0;
+            sa.dz = dz;
+            sa.ld_dz = V;
+            done = gemm_tc_dz(st, gs, W32(L.bout), sa);
+          } else {
+            done = true;
+          }
+        }
+      }
+      if (!done) {
+        if (!lg) lg = P.ws.get<float>("lm_logits", static_cast<size_t>(RC) * V);
+        Epi el = store(lg, V, nullptr, 0);
+        el.bias = W32(L.bout);
+        mm(rc, g.V, g.d, ycT, g.d, true, W(L.wout), g.d, true, el);
+        lm_rows<T>(st, lg, rc, g.V, g.bos, tgt + r0, w ? w + r0 : nullptr, logp ? logp + r0 : nullptr, dz);
+      }
       if (!grad) continue;
       Epi ew;
       ew.kind = EPI_ACCUM;
@@ -1287,6 +1316,37 @@ int dashcu_selftest_gemm(dashcu_ctx* c, int M, int N, int K, const uint16_t* A, 
   else gemm(s, 1, g, e);
   d2h(s, Cout, dC, static_cast<size_t>(M) * N);
   DCU_CHECK(cudaStreamSynchronize(s));
+  API_END
+}
+
+int dashcu_selftest_gemm_timed(dashcu_ctx* c, int M, int N, int K, int a_kmajor, int b_kmajor, int epi, int iters,
+                               double* ms) {
+  API_BEGIN
+  if (!c || !ms || M <= 0 || N <= 0 || K <= 0 || iters <= 0) throw Error(1, "bad arguments");
+  DCU_CHECK(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  const size_t na = static_cast<size_t>(M) * K, nb = static_cast<size_t>(N) * K;
+  float* tmp = c->ws.get<float>("tt_f", std::max(na, nb));
+  bf16* dA = c->ws.get<bf16>("tt_A", na);
+  bf16* dB = c->ws.get<bf16>("tt_B", nb);
+  init_normal_ctr(s, tmp, static_cast<int64_t>(na), 1.0, 1);
+  cast_f32_bf16(s, tmp, dA, static_cast<int64_t>(na));
+  init_normal_ctr(s, tmp, static_cast<int64_t>(nb), 1.0, 2);
+  cast_f32_bf16(s, tmp, dB, static_cast<int64_t>(nb));
+  float* c32 = epi == EPI_ACCUM ? c->ws.get<float>("tt_C32", static_cast<size_t>(M) * N) : nullptr;
+  bf16* cT = epi == EPI_ACCUM ? nullptr : c->ws.get<bf16>("tt_CT", static_cast<size_t>(M) * N);
+  if (c32) DCU_CHECK(cudaMemsetAsync(c32, 0, sizeof(float) * static_cast<size_t>(M) * N, s));
+  GemmShape g{M, N, K, dA, a_kmajor ? K : M, a_kmajor != 0, dB, b_kmajor ? K : N, b_kmajor != 0};
+  Epi e;
+  e.kind = epi == EPI_ACCUM ? EPI_ACCUM : EPI_STORE;
+  e.c32 = c32;
+  e.ldc32 = N;
+  e.cT = cT;
+  e.ldcT = N;
+  gemm(s, 1, g, e);  // warm-up (also builds the tensor maps once)
+  Timer tm(s);
+  for (int i = 0; i < iters; ++i) gemm(s, 1, g, e);
+  *ms = tm.stop_ms() / iters;
   API_END
 }
 

@@ -74,6 +74,29 @@ __device__ __forceinline__ float gumbel_score(float logit, float inv_t, uint32_t
   return __fmaf_rn(logit, inv_t, gumbel(rk, token));
 }
 
+// ---- exact filtering (an optimisation that never changes the argmax) -------------
+// gumbel() is increasing in the 23-bit draw K = h >> 9. A token can only beat the
+// running best score b if g > b - logit/T; with logit <= m (chunk max) that needs
+// g > c = b - m/T, i.e. u > exp(-exp(-c)). The threshold below is evaluated with
+// fast intrinsics and then loosened (1e-3 in c, 1e-4 in u), so every token that
+// could win is still scored with the exact rule; the rest are provably losers.
+__device__ __forceinline__ uint32_t gumbel_draw(uint32_t rk, int32_t token) {
+  uint32_t h = fmix32((static_cast<uint32_t>(token) * 0x9e3779b1u) ^ rk);
+  return fmix32(h + 0x7f4a7c15u + rk) >> 9;
+}
+__device__ __forceinline__ float gumbel_of_draw(uint32_t k) {
+  const float u = __fmul_rn(static_cast<float>(k * 2u + 1u), 5.9604644775390625e-08f);  // 2^-24
+  const float e = -soft_logf(u);
+  return -soft_logf(e);
+}
+// draws K > threshold may win; returns -1 (everything passes) when no best exists yet
+__device__ __forceinline__ float gumbel_draw_threshold(float best, float chunk_max_logit, float inv_t) {
+  if (!(best > -3.0e38f)) return -1.f;
+  const float c = best - chunk_max_logit * inv_t - 1e-3f;
+  const float ustar = __expf(-__expf(-c));
+  return (ustar * (1.f - 1e-4f) * 16777216.f - 1.f) * 0.5f;
+}
+
 // (score, index) argmax combine with ties to the lowest index.
 __device__ __forceinline__ bool better(float s1, int i1, float s0, int i0) {
   return s1 > s0 || (s1 == s0 && i1 < i0);

@@ -1,0 +1,37 @@
+"""tcgen05 GEMM throughput on the DASH step's shapes (Qwen2.5-0.5B, config 2).
+Prints one JSON line per shape: ms per launch (CUDA events) and TFLOP/s."""
+import ctypes as C
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2505_17218_b200 as D  # noqa: E402
+
+SHAPES = {
+    # name: (M, N, K, a_kmajor, b_kmajor, epi)
+    "dec_qkv": (4096, 1152, 896, 1, 1, 0), "dec_w1": (4096, 4864, 896, 1, 1, 0),
+    "dec_w2": (4096, 896, 4864, 1, 1, 0), "dec_lm": (4096, 151936, 896, 1, 1, 0),
+    "fwd_w1": (36864, 4864, 896, 1, 1, 0), "fwd_w2": (36864, 896, 4864, 1, 1, 0),
+    "dgrad_w1": (36864, 896, 4864, 1, 0, 0), "wgrad_w1": (4864, 896, 36864, 0, 0, 3),
+    "wgrad_lm": (151936, 896, 16384, 0, 0, 3), "dgrad_lm": (16384, 896, 151936, 1, 0, 0),
+    "big_sq": (8192, 8192, 8192, 1, 1, 0),
+}
+
+
+def main():
+    L = D.lib()
+    L.dashcu_selftest_gemm_timed.argtypes = [C.c_void_p] + [C.c_int] * 7 + [C.POINTER(C.c_double)]
+    ctx = D.Context(0)
+    names = sys.argv[1:] or list(SHAPES)
+    for n in names:
+        M, N, K, ak, bk, epi = SHAPES[n]
+        ms = C.c_double(0)
+        rc = L.dashcu_selftest_gemm_timed(ctx.h, M, N, K, ak, bk, epi, 10, C.byref(ms))
+        assert rc == 0, L.dashcu_last_error()
+        print(json.dumps({"shape": n, "M": M, "N": N, "K": K, "ms": ms.value,
+                          "tflops": 2.0 * M * N * K / (ms.value * 1e-3) / 1e12}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
