@@ -236,29 +236,38 @@ __device__ __forceinline__ void epilogue_sample(const GemmShape& g, const Epi& e
       v[i] = (n < g.N && n != sa.bos) ? v[i] : -FLT_MAX;
       cm = fmaxf(cm, v[i]);
     }
-    // exact Gumbel-max with a conservative filter: only draws that could beat the
-    // running best are pushed through the (expensive) exact score
+    // exact Gumbel-max with a conservative filter: all 32 draws are hashed branch-free
+    // (independent, so the loop has full ILP); only draws that could beat the running
+    // best go through the exact (two soft logs) score, in ascending id order.
     const float kthr = gumbel_draw_threshold(bs, cm, sa.inv_t);
+    uint32_t pass = 0, dk[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      const int n = nb + i;
-      if (v[i] == -FLT_MAX) continue;
-      const uint32_t k = gumbel_draw(rk, n);
-      if (static_cast<float>(k) > kthr) {
-        const float sc = __fmaf_rn(v[i], sa.inv_t, gumbel_of_draw(k));
-        if (better(sc, n, bs, bi)) {
-          bs = sc;
-          bi = n;
-          bl = v[i];
-        }
+      dk[i] = gumbel_draw(rk, nb + i);
+      pass |= (v[i] != -FLT_MAX && static_cast<float>(dk[i]) > kthr) ? (1u << i) : 0u;
+    }
+    while (pass) {
+      const int i = __ffs(pass) - 1;
+      pass &= pass - 1;
+      uint32_t k = 0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) k = j == i ? dk[j] : k;
+      float l = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) l = j == i ? v[j] : l;
+      const float sc = __fmaf_rn(l, sa.inv_t, gumbel_of_draw(k));
+      if (better(sc, nb + i, bs, bi)) {
+        bs = sc;
+        bi = nb + i;
+        bl = l;
       }
     }
     if (cm > -FLT_MAX) {
       const float nm = fmaxf(mx, cm);
-      float acc = se * __expf(mx - nm);
+      float a4[4] = {se * __expf(mx - nm), 0.f, 0.f, 0.f};  // 4 chains: the adds overlap
 #pragma unroll
-      for (int i = 0; i < 32; ++i) acc += v[i] > -FLT_MAX ? __expf(v[i] - nm) : 0.f;
-      se = acc;
+      for (int i = 0; i < 32; ++i) a4[i & 3] += v[i] > -FLT_MAX ? __expf(v[i] - nm) : 0.f;
+      se = (a4[0] + a4[1]) + (a4[2] + a4[3]);
       mx = nm;
     }
   }
@@ -292,10 +301,10 @@ __device__ __forceinline__ void epilogue_lse(const GemmShape& g, const Epi& e, c
     }
     if (cm > -FLT_MAX) {
       const float nm = fmaxf(mx, cm);
-      float acc = se * __expf(mx - nm);
+      float a4[4] = {se * __expf(mx - nm), 0.f, 0.f, 0.f};  // 4 chains: the adds overlap
 #pragma unroll
-      for (int i = 0; i < 32; ++i) acc += v[i] > -FLT_MAX ? __expf(v[i] - nm) : 0.f;
-      se = acc;
+      for (int i = 0; i < 32; ++i) a4[i & 3] += v[i] > -FLT_MAX ? __expf(v[i] - nm) : 0.f;
+      se = (a4[0] + a4[1]) + (a4[2] + a4[3]);
       mx = nm;
     }
   }
@@ -560,7 +569,9 @@ constexpr int kSampleEPW = 8;  // two column slices per accumulator row: the Gum
 bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e) {
   if (!legal(g)) return false;
   // 128 x 256 tiles unless N is small or a 256-multiple would waste a half tile
-  const bool wide = g.N >= 2048 || (g.N % 256 == 0);
+  // (measured: 128x128 tiles are shared-memory-bandwidth bound at ~760 TF/s; 128x256 reaches
+  // ~1100 even with a ragged last tile, so N = 896 also takes the wide tile)
+  const bool wide = g.N >= 768 || (g.N % 256 == 0);
   const int BN = wide ? 256 : 128;
   CUtensorMap ma, mb;
   bool ok = g.a_kmajor ? make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) : make_map(&ma, g.A, g.K, g.M, g.lda, 64, BK);
@@ -585,7 +596,7 @@ int gemm_tc_sample(cudaStream_t s, const GemmShape& g, const float* bias, const 
   return a.ntiles;
 }
 
-int gemm_tc_lse_tiles(int N) { return (N + 255) / 256; }
+int gemm_tc_lse_tiles(int N) { return ((N + 255) / 256) * 2; }  // two column slices per tile (8 epilogue warps)
 
 int gemm_tc_lse(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa) {
   if (!legal(g) || !g.a_kmajor || !g.b_kmajor) return 0;
@@ -595,7 +606,7 @@ int gemm_tc_lse(cudaStream_t s, const GemmShape& g, const float* bias, const Sam
   e.bias = bias;
   SampleArgs a = sa;
   a.ntiles = gemm_tc_lse_tiles(g.N);
-  launch<256, 4, true, true, 4, 2>(s, ma, mb, g, e, a);
+  launch<256, 4, true, true, 8, 2>(s, ma, mb, g, e, a);
   return a.ntiles;
 }
 
@@ -605,7 +616,7 @@ bool gemm_tc_dz(cudaStream_t s, const GemmShape& g, const float* bias, const Sam
   if (!make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) || !make_map(&mb, g.B, g.N, g.K, g.ldb, BK, 256)) return false;
   Epi e;
   e.bias = bias;
-  launch<256, 4, true, true, 4, 3>(s, ma, mb, g, e, sa);
+  launch<256, 4, true, true, 8, 3>(s, ma, mb, g, e, sa);
   return true;
 }
 

@@ -1,0 +1,94 @@
+"""World-size-2 checks of the data-parallel DASH step on CPU (gloo), the multi-GPU
+design of SURVEY §8e: prompts sharded by global index with whole groups per rank,
+per-request keys independent of the split, each rank accumulating its shard's PG
+gradient with the GLOBAL 1/N, one sum-allreduce, then an identical optimizer step.
+The per-rank gradients come from the CPU oracle; the collective is torch.distributed."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle_ffi as O
+from paper_2505_17218_b200 import workload as W
+
+ARCH = dict(vocab_size=13, embed_dim=8, context_len=24, ffn_hidden=12, n_layers=2, bos_id=0, eos_id=1,
+            n_heads=2, n_kv_heads=1, head_dim=4)
+M, G, ML, SEED = 6, 4, 6, 11
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def shard(rank, world):
+    per = M // world
+    return rank * per, (rank + 1) * per
+
+
+def rank_gradient(params, lo, hi):
+    """This rank's contribution: sum over its kept sequences of (A_n / N_global) grad log pi."""
+    g = np.zeros_like(params)
+    prompts = W.synthetic_prompts(3, lo, hi, 4, ARCH["vocab_size"], 0, 1)
+    comps = []
+    for i, m in enumerate(range(lo, hi)):
+        for gg in range(G):
+            c, _ = O.sample(ARCH, params, list(prompts[i]), ML, 1.0, O.derive_seed(SEED, "sample", m, gg))
+            comps.append(list(c))
+    r = W.synthetic_rewards(5, lo, hi, G)
+    adv, kept, idx = O.advantage_filter(r, G, 1, False, 0.0, 0.1)   # groups never straddle ranks
+    for s in idx:
+        O.grad_log_prob(ARCH, params, list(prompts[s // G]), comps[s], adv[s] / (M * G), g)
+    return g, comps
+
+
+def worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    params = O.init_params(ARCH, 0.4, 2)
+    lo, hi = shard(rank, world)
+    g, comps = rank_gradient(params, lo, hi)
+    t = torch.from_numpy(g)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    # replicated Adam step after the allreduce: every rank ends with identical weights
+    p = params.copy()
+    m = np.zeros_like(p)
+    v = np.zeros_like(p)
+    gg = t.numpy().copy()
+    O.oracle().dor_adam_step(O.ptr(p, O.f64p), O.ptr(gg, O.f64p), O.ptr(m, O.f64p), O.ptr(v, O.f64p), len(p), 1,
+                             1e-3, 0.9, 0.999, 1e-8)
+    # bench.py reduction helpers (max of step times, sum of tokens) over the same group
+    import bench
+    mx = bench.allreduce([float(rank + 1)], "max")[0]
+    sm = bench.allreduce([float(rank + 1)], "sum")[0]
+    q.put((rank, gg, p, comps, mx, sm))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sharded_step_equals_single_process():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+    params = O.init_params(ARCH, 0.4, 2)
+    g_all, comps_all = rank_gradient(params, 0, M)
+    # identical token multiset for any worker split
+    assert res[0][3] + res[1][3] == comps_all
+    for r in range(world):
+        assert np.linalg.norm(res[r][1] - g_all) <= 1e-12 * max(1.0, np.linalg.norm(g_all))
+    assert np.array_equal(res[0][2], res[1][2])            # replicated optimizer state stays in sync
+    assert res[0][4] == 2.0 and res[0][5] == 3.0            # max / sum over ranks
