@@ -62,6 +62,8 @@ extern "C" {
 #define DASHCU_ADV_SINGLE_PATH 0 /* single_path_advantage  advantage.cpp:67-78 */
 #define DASHCU_ADV_GROUP 1       /* group_advantage        advantage.cpp:80-94 */
 #define DASHCU_ADV_LEAVE_ONE_OUT 2 /* leave_one_out        advantage.cpp:96-112 */
+#define DASHCU_ADV_GIVEN 3         /* advantages passed in `adv` (in/out): normalize_std
+                                      (advantage.cpp:114-133) and/or filter_by_threshold only */
 
 /* optimizers */
 #define DASHCU_OPT_SGD 0
@@ -135,6 +137,12 @@ DASHCU_API int dashcu_policy_version(dashcu_policy* pol, uint64_t* version);
  * a GPU; SURVEY App.B D2). The rollout stays resident for accumulate. */
 DASHCU_API int dashcu_sample(dashcu_policy* pol, const dashcu_plan* plan, const int32_t* prompt_tokens,
                   const int64_t* prompt_offsets, int32_t* completions, int32_t* lengths, float* logp);
+/* Same with explicit per-sequence keys (seq_keys[n_prompts*group_size]) instead of
+ * derive_seed(round_seed, "sample", m, g): the per-trajectory form of
+ * dash::sample(params, prompt, max_len, T, seed) (policy.cpp:379) with key = seed. */
+DASHCU_API int dashcu_sample_keyed(dashcu_policy* pol, const dashcu_plan* plan, const int32_t* prompt_tokens,
+                                   const int64_t* prompt_offsets, const uint64_t* seq_keys, int32_t* completions,
+                                   int32_t* lengths, float* logp);
 /* Debug: when enabled, the next dashcu_sample also records the exact fp32
  * logits its sampling rule consumed, [n_seq][max_len][vocab] (small shapes). */
 DASHCU_API int dashcu_set_logits_dump(dashcu_policy* pol, int enable);
@@ -173,6 +181,8 @@ DASHCU_API int dashcu_accumulate(dashcu_policy* pol, double weight_scale, int32_
 DASHCU_API int dashcu_accumulate_weighted(dashcu_policy* pol, const double* weights, int32_t n_seq,
                                int32_t micro_batch);
 DASHCU_API int dashcu_grad_download(dashcu_policy* pol, double* grad, int64_t n);
+/* Replace the device gradient (fp64 views() order), e.g. a GradientVector computed elsewhere. */
+DASHCU_API int dashcu_grad_upload(dashcu_policy* pol, const double* grad, int64_t n);
 /* Sum gradients over the ranks of the context's communicator (no-op at world 1). */
 DASHCU_API int dashcu_allreduce_grads(dashcu_policy* pol);
 /* Ascent step on the fp32 master weights; refreshes the bf16 copy; bumps the version. */

@@ -240,26 +240,24 @@ __device__ __forceinline__ void epilogue_sample(const GemmShape& g, const Epi& e
     // (independent, so the loop has full ILP); only draws that could beat the running
     // best go through the exact (two soft logs) score, in ascending id order.
     const float kthr = gumbel_draw_threshold(bs, cm, sa.inv_t);
-    uint32_t pass = 0, dk[32];
+    uint32_t dk[32];
+    bool any = false;
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       dk[i] = gumbel_draw(rk, nb + i);
-      pass |= (v[i] != -FLT_MAX && static_cast<float>(dk[i]) > kthr) ? (1u << i) : 0u;
+      any |= v[i] != -FLT_MAX && static_cast<float>(dk[i]) > kthr;
     }
-    while (pass) {
-      const int i = __ffs(pass) - 1;
-      pass &= pass - 1;
-      uint32_t k = 0;
+    if (any) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) k = j == i ? dk[j] : k;
-      float l = 0.f;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) l = j == i ? v[j] : l;
-      const float sc = __fmaf_rn(l, sa.inv_t, gumbel_of_draw(k));
-      if (better(sc, nb + i, bs, bi)) {
-        bs = sc;
-        bi = nb + i;
-        bl = l;
+      for (int i = 0; i < 32; ++i) {
+        if (v[i] != -FLT_MAX && static_cast<float>(dk[i]) > kthr) {
+          const float sc = __fmaf_rn(v[i], sa.inv_t, gumbel_of_draw(dk[i]));
+          if (better(sc, nb + i, bs, bi)) {
+            bs = sc;
+            bi = nb + i;
+            bl = v[i];
+          }
+        }
       }
     }
     if (cm > -FLT_MAX) {
@@ -562,7 +560,8 @@ bool legal(const GemmShape& g) {
 }
 
 constexpr int kSampleBN = 256;
-constexpr int kSampleEPW = 8;  // two column slices per accumulator row: the Gumbel math is ALU-heavy
+constexpr int kSampleEPW = 16;  // four 64-column slices per accumulator row: the Gumbel math is ALU-heavy,
+                                // 4 epilogue warps per SM sub-partition hide its latency
 
 }  // namespace
 
@@ -571,7 +570,12 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e) {
   // 128 x 256 tiles unless N is small or a 256-multiple would waste a half tile
   // (measured: 128x128 tiles are shared-memory-bandwidth bound at ~760 TF/s; 128x256 reaches
   // ~1100 even with a ragged last tile, so N = 896 also takes the wide tile)
-  const bool wide = g.N >= 768 || (g.N % 256 == 0);
+  // Pick the tile width by the persistent schedule: rounds = ceil(tiles / SMs), and a
+  // 128-wide tile costs ~0.66 of a 256-wide one (measured efficiency 0.76 vs 1.0).
+  const int tm = (g.M + BM - 1) / BM;
+  const double r128 = std::ceil(tm * ((g.N + 127) / 128) / static_cast<double>(num_sms()));
+  const double r256 = std::ceil(tm * ((g.N + 255) / 256) / static_cast<double>(num_sms()));
+  const bool wide = r256 * 256.0 <= r128 * 128.0 / 0.76;
   const int BN = wide ? 256 : 128;
   CUtensorMap ma, mb;
   bool ok = g.a_kmajor ? make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) : make_map(&ma, g.A, g.K, g.M, g.lda, 64, BK);

@@ -435,7 +435,9 @@ __global__ void advantage_k(const double* r, int n, int G, int kind, int normali
     const int s = grp * gs;
     double sum = 0.0;
     for (int i = s; i < s + gs; ++i) sum += r[i];
-    if (kind == 2) {
+    if (kind == 3) {
+      // given advantages (adv holds them already): normalize_std / filter only
+    } else if (kind == 2) {
       const double den = static_cast<double>(gs - 1);
       for (int i = s; i < s + gs; ++i) adv[i] = r[i] - (sum - r[i]) / den;
     } else {

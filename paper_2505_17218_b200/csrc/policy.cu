@@ -1017,8 +1017,28 @@ int dashcu_get_logits_dump(dashcu_policy* p, float* out, int64_t n) {
   API_END
 }
 
+static int sample_impl(dashcu_policy* p, const dashcu_plan* plan, const int32_t* prompt_tokens,
+                       const int64_t* prompt_offsets, const uint64_t* seq_keys, int32_t* completions, int32_t* lengths,
+                       float* logp);
+
 int dashcu_sample(dashcu_policy* p, const dashcu_plan* plan, const int32_t* prompt_tokens,
                   const int64_t* prompt_offsets, int32_t* completions, int32_t* lengths, float* logp) {
+  return sample_impl(p, plan, prompt_tokens, prompt_offsets, nullptr, completions, lengths, logp);
+}
+
+int dashcu_sample_keyed(dashcu_policy* p, const dashcu_plan* plan, const int32_t* prompt_tokens,
+                        const int64_t* prompt_offsets, const uint64_t* seq_keys, int32_t* completions,
+                        int32_t* lengths, float* logp) {
+  if (!seq_keys) {
+    g_last_error = "null seq_keys";
+    return DASHCU_E_INPUT;
+  }
+  return sample_impl(p, plan, prompt_tokens, prompt_offsets, seq_keys, completions, lengths, logp);
+}
+
+static int sample_impl(dashcu_policy* p, const dashcu_plan* plan, const int32_t* prompt_tokens,
+                       const int64_t* prompt_offsets, const uint64_t* seq_keys, int32_t* completions, int32_t* lengths,
+                       float* logp) {
   API_BEGIN
   check_policy(p);
   if (!plan) throw Error(1, "null plan");
@@ -1035,8 +1055,10 @@ int dashcu_sample(dashcu_policy* p, const dashcu_plan* plan, const int32_t* prom
     if (len > p->g.ctx) throw Error(2, "prompt exceeds context window");
     for (int gg = 0; gg < G; ++gg) {
       cap[m * G + gg] = std::min(plan->max_len, p->g.ctx - len);
-      keys[m * G + gg] = derive_seed(plan->round_seed, "sample", static_cast<uint64_t>(plan->prompt_index_base + m),
-                                     static_cast<uint64_t>(gg));
+      keys[m * G + gg] = seq_keys ? seq_keys[m * G + gg]
+                                  : derive_seed(plan->round_seed, "sample",
+                                                static_cast<uint64_t>(plan->prompt_index_base + m),
+                                                static_cast<uint64_t>(gg));
     }
   }
   p->n_prompts = NP;
@@ -1123,11 +1145,13 @@ int dashcu_advantage_filter(dashcu_ctx* c, const double* rewards, int32_t n, int
   if (!c) throw Error(1, "null ctx");
   // advantage.cpp:10-11, :68, :82, :100-101, :136
   if (n <= 0) throw Error(1, "advantage of an empty batch");
-  if (kind < 0 || kind > 2) throw Error(1, "unknown advantage kind");
+  if (kind < 0 || kind > 3) throw Error(1, "unknown advantage kind");
+  if (kind == DASHCU_ADV_GIVEN && !normalize) G = n;  // filter only: grouping irrelevant
   if (kind != DASHCU_ADV_SINGLE_PATH && (G <= 0 || n % G != 0))
     throw Error(1, "contiguous grouping requires group_size dividing n");
   if (kind == DASHCU_ADV_LEAVE_ONE_OUT && G < 2) throw Error(1, "leave-one-out needs every group size >= 2");
   if (!(tau >= 0.0)) throw Error(1, "filter threshold must be >= 0");
+  if (kind == DASHCU_ADV_GIVEN && !adv) throw Error(1, "DASHCU_ADV_GIVEN needs the advantages in adv");
   DCU_CHECK(cudaSetDevice(c->device));
   cudaStream_t s = c->stream;
   double* d_r = c->ws.get<double>("adv_r", n);
@@ -1135,7 +1159,10 @@ int dashcu_advantage_filter(dashcu_ctx* c, const double* rewards, int32_t n, int
   uint8_t* d_k = c->ws.get<uint8_t>("adv_k", n);
   int32_t* d_i = c->ws.get<int32_t>("adv_i", n);
   int32_t* d_n = c->ws.get<int32_t>("adv_n", 1);
-  h2d(s, d_r, rewards, n);
+  if (rewards) h2d(s, d_r, rewards, n);
+  else if (kind != DASHCU_ADV_GIVEN || normalize) throw Error(1, "null rewards");
+  else DCU_CHECK(cudaMemsetAsync(d_r, 0, sizeof(double) * n, s));
+  if (kind == DASHCU_ADV_GIVEN) h2d(s, d_a, adv, n);
   advantage_filter(s, d_r, n, G, kind, normalize, eps, tau, d_a, d_k, d_i, d_n);
   int32_t nk = 0;
   d2h(s, &nk, d_n, 1);
@@ -1242,6 +1269,17 @@ int dashcu_grad_download(dashcu_policy* p, double* grad, int64_t n) {
   double* st = p->ws.get<double>("staging64", n);
   f32_to_f64(p->ctx->stream, p->g32.as<float>(), st, n);
   d2h(p->ctx->stream, grad, st, n);
+  DCU_CHECK(cudaStreamSynchronize(p->ctx->stream));
+  API_END
+}
+
+int dashcu_grad_upload(dashcu_policy* p, const double* grad, int64_t n) {
+  API_BEGIN
+  check_policy(p);
+  if (n != p->lay.total) throw Error(1, "parameter count mismatch");
+  double* st = p->ws.get<double>("staging64", n);
+  h2d(p->ctx->stream, st, grad, n);
+  f64_to_f32(p->ctx->stream, st, p->g32.as<float>(), n);
   DCU_CHECK(cudaStreamSynchronize(p->ctx->stream));
   API_END
 }
