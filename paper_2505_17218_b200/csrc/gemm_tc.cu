@@ -100,6 +100,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// tanh(x) = 1 - 2 / (exp(2x) + 1): ~1e-6 relative, far below the bf16 output rounding;
+// 6 instructions instead of tanhf's ~20 (the W1 epilogue runs it on every element).
+__device__ __forceinline__ float fast_tanh(float x) {
+  const float e = __expf(2.f * fminf(fmaxf(x, -15.f), 15.f));
+  return 1.f - __fdividef(2.f, e + 1.f);
+}
+
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -140,7 +147,7 @@ __device__ __forceinline__ void epilogue_store(const GemmShape& g, const Epi& e,
       }
       if (e.kind == EPI_TANH) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = tanhf(v[i]);
+        for (int i = 0; i < 32; ++i) v[i] = fast_tanh(v[i]);
       }
       if (e.kind == EPI_DTANH) {
         const bf16* ap = static_cast<const bf16*>(e.aux) + r64 * e.ld_aux + nb;
@@ -547,10 +554,11 @@ void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const 
 template <int BN, int STAGES>
 void dispatch_majors(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& g, const Epi& e) {
   const SampleArgs none;
-  if (g.a_kmajor && g.b_kmajor) launch<BN, STAGES, true, true, 4, 0>(s, ma, mb, g, e, none);
-  else if (g.a_kmajor) launch<BN, STAGES, true, false, 4, 0>(s, ma, mb, g, e, none);
-  else if (g.b_kmajor) launch<BN, STAGES, false, true, 4, 0>(s, ma, mb, g, e, none);
-  else launch<BN, STAGES, false, false, 4, 0>(s, ma, mb, g, e, none);
+  // 8 epilogue warps (two per SM sub-partition, each owning half of the tile's columns)
+  if (g.a_kmajor && g.b_kmajor) launch<BN, STAGES, true, true, 8, 0>(s, ma, mb, g, e, none);
+  else if (g.a_kmajor) launch<BN, STAGES, true, false, 8, 0>(s, ma, mb, g, e, none);
+  else if (g.b_kmajor) launch<BN, STAGES, false, true, 8, 0>(s, ma, mb, g, e, none);
+  else launch<BN, STAGES, false, false, 8, 0>(s, ma, mb, g, e, none);
 }
 
 bool legal(const GemmShape& g) {
