@@ -561,8 +561,10 @@ __global__ void __launch_bounds__(128) attn_bwd_tc_k(const bf16* __restrict__ qk
         float* dst = dq32 + static_cast<int64_t>(s0 + q) * qd + h * HD;
 #pragma unroll
         for (int nt2 = 0; nt2 < HD / 8; ++nt2) {
-          atomicAdd(dst + nt2 * 8 + t * 2, dq[nt2][2 * hh2]);
-          atomicAdd(dst + nt2 * 8 + t * 2 + 1, dq[nt2][2 * hh2 + 1]);
+          // one 8-byte vector reduction per column pair (sm_90+ red.v2.f32): half the L2 atomics
+          asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dst + nt2 * 8 + t * 2),
+                       "f"(dq[nt2][2 * hh2]), "f"(dq[nt2][2 * hh2 + 1])
+                       : "memory");
         }
       }
     }

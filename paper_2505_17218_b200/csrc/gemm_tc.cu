@@ -246,25 +246,46 @@ __device__ __forceinline__ void epilogue_sample(const GemmShape& g, const Epi& e
     // exact Gumbel-max with a conservative filter: all 32 draws are hashed branch-free
     // (independent, so the loop has full ILP); only draws that could beat the running
     // best go through the exact (two soft logs) score, in ascending id order.
-    const float kthr = gumbel_draw_threshold(bs, cm, sa.inv_t);
     uint32_t dk[32];
-    bool any = false;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      dk[i] = gumbel_draw(rk, nb + i);
-      any |= v[i] != -FLT_MAX && static_cast<float>(dk[i]) > kthr;
-    }
-    if (any) {
+    for (int i = 0; i < 32; ++i) dk[i] = gumbel_draw(rk, nb + i);
+    if (bs == -FLT_MAX && cm > -FLT_MAX) {
+      // seed the running best with one exact score (the largest draw among valid ids),
+      // so the threshold below already prunes this chunk
+      uint32_t kb = 0;
+      int ib = -1;
+      float lb = 0.f;
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        if (v[i] != -FLT_MAX && static_cast<float>(dk[i]) > kthr) {
-          const float sc = __fmaf_rn(v[i], sa.inv_t, gumbel_of_draw(dk[i]));
-          if (better(sc, nb + i, bs, bi)) {
-            bs = sc;
-            bi = nb + i;
-            bl = v[i];
-          }
-        }
+        const bool take = v[i] != -FLT_MAX && (ib < 0 || dk[i] > kb);
+        kb = take ? dk[i] : kb;
+        lb = take ? v[i] : lb;
+        ib = take ? i : ib;
+      }
+      bs = __fmaf_rn(lb, sa.inv_t, gumbel_of_draw(kb));
+      bi = nb + ib;
+      bl = lb;
+    }
+    const float kthr = gumbel_draw_threshold(bs, cm, sa.inv_t);
+    uint32_t pass = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      pass |= (v[i] != -FLT_MAX && static_cast<float>(dk[i]) > kthr && nb + i != bi) ? (1u << i) : 0u;
+    while (pass) {  // rare: draws that could still beat the running best
+      const int i = __ffs(pass) - 1;
+      pass &= pass - 1;
+      uint32_t k = 0;
+      float l = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        k = j == i ? dk[j] : k;
+        l = j == i ? v[j] : l;
+      }
+      const float sc = __fmaf_rn(l, sa.inv_t, gumbel_of_draw(k));
+      if (better(sc, nb + i, bs, bi)) {
+        bs = sc;
+        bi = nb + i;
+        bl = l;
       }
     }
     if (cm > -FLT_MAX) {
