@@ -580,8 +580,7 @@ uint32_t dor_row_key(uint64_t seq_key, int32_t step) {
 }
 
 float dor_gumbel(uint32_t row_key, int32_t token) {
-  uint32_t h = fmix32(((uint32_t)token * 0x9e3779b1u) ^ row_key);
-  h = fmix32(h + 0x7f4a7c15u + row_key);
+  const uint32_t h = fmix32(((uint32_t)token * 0x9e3779b1u) ^ row_key);
   const float u = (float)((h >> 9) * 2u + 1u) * 0x1.0p-24f;
   const float e = -dor_soft_logf(u);
   return -dor_soft_logf(e);

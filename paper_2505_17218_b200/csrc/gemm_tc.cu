@@ -53,9 +53,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "n"(20000)  // suspend-time hint (ns): waiting warps sleep instead of spinning
       : "memory");
 }
 
@@ -223,7 +223,7 @@ __device__ __forceinline__ void epilogue_sample(const GemmShape& g, const Epi& e
     if (!live) continue;
     const int nb = n0 + c;
     float cm = -FLT_MAX;
-    if (nb + 32 <= g.N && (reinterpret_cast<uintptr_t>(e.bias + nb) & 15) == 0) {
+    if (nb + 32 <= g.N && (reinterpret_cast<uintptr_t>(e.bias + nb) & 15) == 0) {  // bias (fp32 master)
 #pragma unroll
       for (int i = 0; i < 32; i += 4) {
         const float4 b = *reinterpret_cast<const float4*>(e.bias + nb + i);
@@ -237,62 +237,53 @@ __device__ __forceinline__ void epilogue_sample(const GemmShape& g, const Epi& e
       for (int i = 0; i < 32; ++i)
         if (nb + i < g.N) sa.dump[static_cast<int64_t>(row) * sa.dump_ld + nb + i] = v[i];
     }
+    // masking only where a chunk holds BOS or runs past V
+    const bool clean = nb + 32 <= g.N && (sa.bos < nb || sa.bos >= nb + 32);
+    if (!clean) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int n = nb + i;
-      v[i] = (n < g.N && n != sa.bos) ? v[i] : -FLT_MAX;
-      cm = fmaxf(cm, v[i]);
+      for (int i = 0; i < 32; ++i) v[i] = (nb + i < g.N && nb + i != sa.bos) ? v[i] : -FLT_MAX;
     }
-    // exact Gumbel-max with a conservative filter: all 32 draws are hashed branch-free
-    // (independent, so the loop has full ILP); only draws that could beat the running
-    // best go through the exact (two soft logs) score, in ascending id order.
-    uint32_t dk[32];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) dk[i] = gumbel_draw(rk, nb + i);
+    for (int i = 0; i < 32; ++i) cm = fmaxf(cm, v[i]);
+    // exact Gumbel-max with a conservative filter: the 32 draws are hashed branch-free
+    // (independent -> full ILP); only draws that could still beat the running best are
+    // scored exactly (out-of-line soft logs behind a branch), in ascending id order.
+    int dk[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) dk[i] = static_cast<int>(gumbel_draw(rk, nb + i));
     if (bs == -FLT_MAX && cm > -FLT_MAX) {
       // seed the running best with one exact score (the largest draw among valid ids),
       // so the threshold below already prunes this chunk
-      uint32_t kb = 0;
-      int ib = -1;
+      int kb = -1, ib = -1;
       float lb = 0.f;
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        const bool take = v[i] != -FLT_MAX && (ib < 0 || dk[i] > kb);
+        const bool take = v[i] != -FLT_MAX && dk[i] > kb;
         kb = take ? dk[i] : kb;
         lb = take ? v[i] : lb;
         ib = take ? i : ib;
       }
-      bs = __fmaf_rn(lb, sa.inv_t, gumbel_of_draw(kb));
+      bs = __fmaf_rn(lb, sa.inv_t, gumbel_of_draw(static_cast<uint32_t>(kb)));
       bi = nb + ib;
       bl = lb;
     }
-    const float kthr = gumbel_draw_threshold(bs, cm, sa.inv_t);
-    uint32_t pass = 0;
+    const int kthr = gumbel_draw_threshold(bs, cm, sa.inv_t);
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
-      pass |= (v[i] != -FLT_MAX && static_cast<float>(dk[i]) > kthr && nb + i != bi) ? (1u << i) : 0u;
-    while (pass) {  // rare: draws that could still beat the running best
-      const int i = __ffs(pass) - 1;
-      pass &= pass - 1;
-      uint32_t k = 0;
-      float l = 0.f;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        k = j == i ? dk[j] : k;
-        l = j == i ? v[j] : l;
-      }
-      const float sc = __fmaf_rn(l, sa.inv_t, gumbel_of_draw(k));
-      if (better(sc, nb + i, bs, bi)) {
-        bs = sc;
-        bi = nb + i;
-        bl = l;
+    for (int i = 0; i < 32; ++i) {
+      if (dk[i] > kthr && v[i] != -FLT_MAX) {  // rare
+        const float sc = __fmaf_rn(v[i], sa.inv_t, gumbel_of_draw(static_cast<uint32_t>(dk[i])));
+        if (better(sc, nb + i, bs, bi)) {
+          bs = sc;
+          bi = nb + i;
+          bl = v[i];
+        }
       }
     }
     if (cm > -FLT_MAX) {
       const float nm = fmaxf(mx, cm);
       float a4[4] = {se * __expf(mx - nm), 0.f, 0.f, 0.f};  // 4 chains: the adds overlap
 #pragma unroll
-      for (int i = 0; i < 32; ++i) a4[i & 3] += v[i] > -FLT_MAX ? __expf(v[i] - nm) : 0.f;
+      for (int i = 0; i < 32; ++i) a4[i & 3] += __expf(v[i] - nm);  // masked ids: exp(-huge) = 0
       se = (a4[0] + a4[1]) + (a4[2] + a4[3]);
       mx = nm;
     }

@@ -569,17 +569,59 @@ struct Engine {
     return d;
   }
 
+  // All micro-batches of a round packed on the host up front and uploaded with one
+  // copy per array, so the GPU never waits for host packing between micro-batches.
+  std::vector<DevBatch> upload_all(const std::vector<Batch>& bs) {
+    size_t nt = 0, ns = 0, nr = 0;
+    for (const Batch& b : bs) nt += b.tok.size(), ns += b.start.size(), nr += b.rows.size();
+    std::vector<int32_t> tok, pos, start, rows, tgt;
+    std::vector<float> w;
+    tok.reserve(nt), pos.reserve(nt), start.reserve(ns), rows.reserve(nr), tgt.reserve(nr), w.reserve(nr);
+    for (const Batch& b : bs) {
+      tok.insert(tok.end(), b.tok.begin(), b.tok.end());
+      pos.insert(pos.end(), b.pos.begin(), b.pos.end());
+      start.insert(start.end(), b.start.begin(), b.start.end());
+      rows.insert(rows.end(), b.rows.begin(), b.rows.end());
+      tgt.insert(tgt.end(), b.tgt.begin(), b.tgt.end());
+      w.insert(w.end(), b.w.begin(), b.w.end());
+    }
+    int32_t* dtok = P.ws.get<int32_t>("mb_tok", nt);
+    int32_t* dpos = P.ws.get<int32_t>("mb_pos", nt);
+    int32_t* dstart = P.ws.get<int32_t>("mb_start", ns);
+    int32_t* drows = P.ws.get<int32_t>("mb_rows", nr);
+    int32_t* dtgt = P.ws.get<int32_t>("mb_tgt", nr);
+    float* dw = P.ws.get<float>("mb_w", nr);
+    h2d(st, dtok, tok.data(), nt);
+    h2d(st, dpos, pos.data(), nt);
+    h2d(st, dstart, start.data(), ns);
+    h2d(st, drows, rows.data(), nr);
+    h2d(st, dtgt, tgt.data(), nr);
+    h2d(st, dw, w.data(), nr);
+    std::vector<DevBatch> out;
+    size_t ot = 0, os = 0, orr = 0;
+    for (const Batch& b : bs) {
+      out.push_back(DevBatch{dtok + ot, dpos + ot, dstart + os, drows + orr, dtgt + orr, dw + orr});
+      ot += b.tok.size(), os += b.start.size(), orr += b.rows.size();
+    }
+    return out;
+  }
+
   // grad += sum_k weight[k] * grad log pi(seq_k), micro_batch sequences at a time.
   int64_t accumulate(const std::vector<int>& seqs, const std::vector<double>& weight, int micro) {
     int64_t loss_tokens = 0;
     if (micro <= 0) micro = static_cast<int>(seqs.size());
+    std::vector<Batch> batches;
     for (size_t k0 = 0; k0 < seqs.size(); k0 += micro) {
       const size_t k1 = std::min(seqs.size(), k0 + static_cast<size_t>(micro));
       std::vector<int> ss(seqs.begin() + k0, seqs.begin() + k1);
       std::vector<double> ww(weight.begin() + k0, weight.begin() + k1);
       Batch B = pack(ss, ww);
-      if (B.seqs.empty()) continue;
-      DevBatch D = upload(B);
+      if (!B.seqs.empty()) batches.push_back(std::move(B));
+    }
+    const std::vector<DevBatch> dev = upload_all(batches);
+    for (size_t bi = 0; bi < batches.size(); ++bi) {
+      const Batch& B = batches[bi];
+      const DevBatch& D = dev[bi];
       const int Tn = static_cast<int>(B.tok.size());
       Acts A = alloc_acts(P.ws, Tn, "a_");
       pairs = B.pairs;

@@ -63,8 +63,7 @@ __host__ __device__ __forceinline__ uint32_t row_key(uint64_t seq_key, int32_t s
 }
 
 __device__ __forceinline__ float gumbel(uint32_t rk, int32_t token) {
-  uint32_t h = fmix32((static_cast<uint32_t>(token) * 0x9e3779b1u) ^ rk);
-  h = fmix32(h + 0x7f4a7c15u + rk);
+  const uint32_t h = fmix32((static_cast<uint32_t>(token) * 0x9e3779b1u) ^ rk);
   const float u = __fmul_rn(static_cast<float>((h >> 9) * 2u + 1u), 5.9604644775390625e-08f);  // 2^-24
   const float e = -soft_logf(u);
   return -soft_logf(e);
@@ -81,20 +80,23 @@ __device__ __forceinline__ float gumbel_score(float logit, float inv_t, uint32_t
 // fast intrinsics and then loosened (1e-3 in c, 1e-4 in u), so every token that
 // could win is still scored with the exact rule; the rest are provably losers.
 __device__ __forceinline__ uint32_t gumbel_draw(uint32_t rk, int32_t token) {
-  uint32_t h = fmix32((static_cast<uint32_t>(token) * 0x9e3779b1u) ^ rk);
-  return fmix32(h + 0x7f4a7c15u + rk) >> 9;
+  return fmix32((static_cast<uint32_t>(token) * 0x9e3779b1u) ^ rk) >> 9;
 }
-__device__ __forceinline__ float gumbel_of_draw(uint32_t k) {
+// out-of-line on purpose: the (rare) exact score is reached through a branch, so the
+// common "cannot win" path costs a bit test instead of an if-converted soft-log chain
+static __device__ __noinline__ float gumbel_of_draw(uint32_t k) {
   const float u = __fmul_rn(static_cast<float>(k * 2u + 1u), 5.9604644775390625e-08f);  // 2^-24
   const float e = -soft_logf(u);
   return -soft_logf(e);
 }
-// draws K > threshold may win; returns -1 (everything passes) when no best exists yet
-__device__ __forceinline__ float gumbel_draw_threshold(float best, float chunk_max_logit, float inv_t) {
-  if (!(best > -3.0e38f)) return -1.f;
+// draws K > threshold may win (signed integer compare); -1 = everything passes
+__device__ __forceinline__ int gumbel_draw_threshold(float best, float chunk_max_logit, float inv_t) {
+  if (!(best > -3.0e38f)) return -1;
   const float c = best - chunk_max_logit * inv_t - 1e-3f;
   const float ustar = __expf(-__expf(-c));
-  return (ustar * (1.f - 1e-4f) * 16777216.f - 1.f) * 0.5f;
+  const float kf = (ustar * (1.f - 1e-4f) * 16777216.f - 1.f) * 0.5f - 1.f;
+  // every K with u(K) > u* (1 - 1e-4), i.e. K > kf + 1, satisfies K > floor(kf)
+  return kf < 0.f ? -1 : static_cast<int>(kf);
 }
 
 // (score, index) argmax combine with ties to the lowest index.
