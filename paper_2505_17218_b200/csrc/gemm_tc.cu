@@ -53,9 +53,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Epilogue-side wait with a suspend-time hint (ns): many epilogue warps sleep instead of
+// spinning while the MMA of the next tile runs (the producer/MMA waits stay tight).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity), "n"(20000)  // suspend-time hint (ns): waiting warps sleep instead of spinning
+      "r"(parity), "n"(2000)
       : "memory");
 }
 
@@ -485,7 +497,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
       const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
       const int acc = i & 1;
       const uint32_t aph = (i >> 1) & 1;
-      mbar_wait(&tfull[acc], aph);
+      mbar_wait_sleep(&tfull[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       const int row = m0 + q * 32 + lane;

@@ -1,0 +1,42 @@
+"""Training-phase microbenchmark at config-2 shapes (Qwen2.5-0.5B): one micro-batch of
+32 sequences x (128 prompt + 1024 completion) through dashcu_accumulate_weighted;
+prints per-kernel-class CUDA-event times."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import paper_2505_17218_b200 as D  # noqa: E402
+from paper_2505_17218_b200 import workload as W  # noqa: E402
+
+
+def main():
+    n_seq = int(sys.argv[1]) if len(sys.argv) > 1 else 32
+    P, L = 128, 1024
+    arch = W.qwen_arch("0.5b", P + L)
+    ctx = D.Context(0)
+    pol = D.Policy(ctx, arch, D.BF16)
+    pol.init_normal(0.02, 1)
+    rng = np.random.default_rng(0)
+    prompts = [list(p) for p in W.synthetic_prompts(1, 0, n_seq, P, arch["vocab_size"], 0, 1)]
+    comps = [list(rng.integers(2, arch["vocab_size"], size=L)) for _ in range(n_seq)]
+    pol.load_rollout(prompts, 1, comps)
+    w = np.full(n_seq, 1.0 / n_seq)
+    pol.grad_zero()
+    pol.accumulate_weighted(w, micro_batch=n_seq)   # warm-up (allocations)
+    D.profile_enable()
+    D.profile_read(reset=True)
+    pol.accumulate_weighted(w, micro_batch=n_seq)
+    prof = D.profile_read(reset=True)
+    D.profile_enable(())
+    st = pol.stats()
+    out = {k: {"ms": v["ms"], "launches": v["launches"], "tflops": v["flops"] / max(v["ms"], 1e-9) / 1e9}
+           for k, v in prof.items() if v["launches"]}
+    print(json.dumps({"seqs": n_seq, "tokens": n_seq * (P + L - 1), "accumulate_ms": st["accumulate_ms"],
+                      "classes": out}))
+
+
+if __name__ == "__main__":
+    main()
