@@ -395,7 +395,9 @@ struct BwdCfg {
 };
 
 template <int HD>
-__global__ void __launch_bounds__(128) attn_bwd_tc_k(const bf16* __restrict__ qkv, const bf16* __restrict__ dctx,
+// HD 64: <= 168 registers so three CTAs (12 warps) share an SM to hide mma/ldmatrix latency
+__global__ void __launch_bounds__(128, HD == 64 ? 3 : 1)
+    attn_bwd_tc_k(const bf16* __restrict__ qkv, const bf16* __restrict__ dctx,
                                                      const float* __restrict__ lse, const float* __restrict__ Dsum,
                                                      const int32_t* __restrict__ seq_start, int nh, int nkv,
                                                      float* __restrict__ dq32, float* __restrict__ dkv32, float scale,
@@ -445,10 +447,12 @@ __global__ void __launch_bounds__(128) attn_bwd_tc_k(const bf16* __restrict__ qk
     const int h = kvh * grp + it / nq, q0 = (kt + it % nq) * 64;
     load_tile(sQb + buf * Cf::TILE, qkv + h * HD, qkvd, q0);
     load_tile(sOb + buf * Cf::TILE, dctx + h * HD, qd, q0);
-    if (threadIdx.x < 64) {
+    if (threadIdx.x < 64) {  // async 4-byte copies: no thread stalls on global latency here
       const int q = q0 + threadIdx.x;
-      sLb[buf * 64 + threadIdx.x] = q < n ? lse[static_cast<int64_t>(s0 + q) * nh + h] * 1.4426950408889634f : 0.f;
-      sDb[buf * 64 + threadIdx.x] = q < n ? Dsum[static_cast<int64_t>(s0 + q) * nh + h] : 0.f;
+      const bool ok = q < n;
+      const int64_t off = static_cast<int64_t>(s0 + (ok ? q : 0)) * nh + h;
+      cp_async4(smem_addr(sLb + buf * 64 + threadIdx.x), lse + off, ok ? 4 : 0);
+      cp_async4(smem_addr(sDb + buf * 64 + threadIdx.x), Dsum + off, ok ? 4 : 0);
     }
     cp_async_commit();
   };
@@ -499,7 +503,7 @@ __global__ void __launch_bounds__(128) attn_bwd_tc_k(const bf16* __restrict__ qk
           const int q = q0 + qc;
           const int key = kr0 + g + (e >> 1) * 8;
           const bool ok = q < n && key <= q && key < n;
-          const float p = ok ? exp2f(st_[nt][e] * scale_log2 - sL[qc]) : 0.f;
+          const float p = ok ? exp2f(st_[nt][e] * scale_log2 - sL[qc] * 1.4426950408889634f) : 0.f;
           st_[nt][e] = p;
           dp[nt][e] = p * (dp[nt][e] - sD[qc]) * scale;
         }
