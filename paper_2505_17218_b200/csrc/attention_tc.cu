@@ -395,8 +395,8 @@ struct BwdCfg {
 };
 
 template <int HD>
-// HD 64: <= 168 registers so three CTAs (12 warps) share an SM to hide mma/ldmatrix latency
-__global__ void __launch_bounds__(128, HD == 64 ? 3 : 1)
+// (measured: forcing 3 CTAs/SM at HD 64 caps registers at 168 and spills; slower)
+__global__ void __launch_bounds__(128, 1)
     attn_bwd_tc_k(const bf16* __restrict__ qkv, const bf16* __restrict__ dctx,
                                                      const float* __restrict__ lse, const float* __restrict__ Dsum,
                                                      const int32_t* __restrict__ seq_start, int nh, int nkv,

@@ -597,9 +597,266 @@ constexpr int kSampleBN = 256;
 constexpr int kSampleEPW = 16;  // four 64-column slices per accumulator row: the Gumbel math is ALU-heavy,
                                 // 4 epilogue warps per SM sub-partition hide its latency
 
+// ======================================================= CTA-pair (cta_group::2) variant
+// A cluster of two CTAs on one TPC computes a 256 x BN tile: each CTA stages its own 128
+// rows of A and HALF of B (BN/2 rows), and the leader's single thread issues
+// tcgen05.mma.cta_group::2 (M = 256), which reads both CTAs' shared memory. Per SM
+// this halves the B traffic through shared memory (the 1-CTA 128x256 tile needs
+// 192 B/clk of smem read+fill at full MMA rate, the pair 128 B/clk). Each CTA's TMEM
+// holds its own 128 accumulator rows, so the epilogue is unchanged.
+//   full[s]   leader only: expect_tx(both CTAs' bytes); both CTAs' TMA complete on it
+//   empty[s]  both: multicast tcgen05.commit from the leader
+//   tfull[a]  both: multicast commit; tempty[a] leader: arrivals from both epilogues
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {  // same smem offset in CTA rank 0
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                               uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+template <int BN, int STAGES, bool AK, bool BKM, int EPW>
+struct Cfg2 {
+  static constexpr int BNH = BN / 2;  // B rows staged per CTA
+  static constexpr int A_BYTES = 128 * BK * 2;
+  static constexpr int B_BYTES = BNH * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int THREADS = 128 + EPW * 32;
+  static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((AK ? 0u : 1u) << 15) |
+                                    ((BKM ? 0u : 1u) << 16) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                                    (static_cast<uint32_t>(256 >> 4) << 24);
+};
+
+template <int BN, int STAGES, bool AK, bool BKM, int EPW>
+__global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, GemmShape g,
+                    Epi e) {
+  using C = Cfg2<BN, STAGES, AK, BKM, EPW>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int nkb = (g.K + BK - 1) / BK;
+  const int tiles_m = (g.M + 255) / 256, tiles_n = (g.N + BN - 1) / BN;
+  const int ntile = tiles_m * tiles_n;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * EPW * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive / TMA
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int kb_all = 0;
+      for (int t = pair; t < ntile; t += npairs) {
+        const int m0 = (t % tiles_m) * 256 + static_cast<int>(rank) * 128;
+        const int n0 = (t / tiles_m) * BN + static_cast<int>(rank) * C::BNH;
+        for (int kb = 0; kb < nkb; ++kb, ++kb_all) {
+          const int s = kb_all % STAGES;
+          const uint32_t ph = (kb_all / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* sa_ = smem + s * C::STAGE_BYTES;
+          uint8_t* sb_ = sa_ + C::A_BYTES;
+          const uint32_t lb = leader_addr(&full[s]);
+          if (leader) mbar_expect_tx(&full[s], 2 * C::STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (AK) {
+            tma_load_2d_pair(sa_, &mapA, lb, k0, m0);
+          } else {
+            tma_load_2d_pair(sa_, &mapA, lb, m0, k0);
+            tma_load_2d_pair(sa_ + 64 * BK * 2, &mapA, lb, m0 + 64, k0);
+          }
+          if (BKM) {
+            tma_load_2d_pair(sb_, &mapB, lb, k0, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < C::BNH / 64; ++j) tma_load_2d_pair(sb_ + j * 64 * BK * 2, &mapB, lb, n0 + 64 * j, k0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      int kb_all = 0, i = 0;
+      for (int t = pair; t < ntile; t += npairs, ++i) {
+        const int acc = i & 1;
+        const uint32_t aph = (i >> 1) & 1;
+        mbar_wait_cluster(&tempty[acc], aph ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb, ++kb_all) {
+          const int s = kb_all % STAGES;
+          const uint32_t ph = (kb_all / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa_ = smem_u32(smem + s * C::STAGE_BYTES);
+          const uint32_t sb_ = sa_ + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t da = AK ? smem_desc(sa_ + k * 32, 16, 1024) : smem_desc(sa_ + k * 2048, 64 * BK * 2, 1024);
+            const uint64_t db = BKM ? smem_desc(sb_ + k * 32, 16, 1024) : smem_desc(sb_ + k * 2048, 64 * BK * 2, 1024);
+            umma_bf16_pair(d, da, db, C::IDESC, (kb > 0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit_pair(&empty[s]);
+        }
+        umma_commit_pair(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const int q = ew & 3;
+    const int slice = ew >> 2;
+    constexpr int NSL = EPW / 4;
+    constexpr int CW = BN / NSL;
+    auto al = [](const void* p, int64_t ld, int esz) {
+      return p == nullptr || (((reinterpret_cast<uintptr_t>(p) | static_cast<uintptr_t>(ld * esz)) & 15) == 0);
+    };
+    const bool vec = al(e.c32, e.ldc32, 4) && al(e.cT, e.ldcT, 2) && al(e.resid, e.ldr, 4) &&
+                     al(e.aux, e.ld_aux, 2) && al(e.bias, 0, 4);
+    const uint32_t tempty_leader0 = leader_addr(&tempty[0]), tempty_leader1 = leader_addr(&tempty[1]);
+    int i = 0;
+    for (int t = pair; t < ntile; t += npairs, ++i) {
+      const int m0 = (t % tiles_m) * 256 + static_cast<int>(rank) * 128, n0 = (t / tiles_m) * BN;
+      const int acc = i & 1;
+      const uint32_t aph = (i >> 1) & 1;
+      mbar_wait_sleep(&tfull[acc], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+      epilogue_store(g, e, taddr, m0 + q * 32 + lane, n0, slice * CW, (slice + 1) * CW, vec);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(acc ? tempty_leader1
+                                                                                            : tempty_leader0)
+                   : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+  }
+}
+
+template <int BN, int STAGES, bool AK, bool BKM>
+void launch2(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& g, const Epi& e) {
+  using C = Cfg2<BN, STAGES, AK, BKM, 8>;
+  auto k = gemm_tc2_kernel<BN, STAGES, AK, BKM, 8>;
+  static bool attr = false;
+  if (!attr) {
+    DCU_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  const int ntile = ((g.M + 255) / 256) * ((g.N + BN - 1) / BN);
+  const int npairs = ntile < num_sms() / 2 ? ntile : num_sms() / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * npairs);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr_c[1];
+  attr_c[0].id = cudaLaunchAttributeClusterDimension;
+  attr_c[0].val.clusterDim.x = 2;
+  attr_c[0].val.clusterDim.y = 1;
+  attr_c[0].val.clusterDim.z = 1;
+  cfg.attrs = attr_c;
+  cfg.numAttrs = 1;
+  ProfScope ps(PROF_GEMM_TC, s, 2.0 * g.M * g.N * static_cast<double>(g.K), 0);
+  DCU_CHECK(cudaLaunchKernelEx(&cfg, k, ma, mb, g, e));
+  DCU_LAUNCHED();
+}
+
+bool use_pair_default() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("DASHCU_GEMM_PAIR");
+    v = s ? atoi(s) : 0;
+  }
+  return v != 0;
+}
+
 }  // namespace
 
+// cta_group::2 GEMM for 256-row-multiple-friendly shapes. Returns false if not TMA-legal.
+bool gemm_tc_pair(cudaStream_t s, const GemmShape& g, const Epi& e) {
+  if (!legal(g)) return false;
+  CUtensorMap ma, mb;
+  constexpr int BN = 256;
+  bool ok = g.a_kmajor ? make_map(&ma, g.A, g.M, g.K, g.lda, BK, 128) : make_map(&ma, g.A, g.K, g.M, g.lda, 64, BK);
+  ok = ok && (g.b_kmajor ? make_map(&mb, g.B, g.N, g.K, g.ldb, BK, BN / 2) : make_map(&mb, g.B, g.K, g.N, g.ldb, 64, BK));
+  if (!ok) return false;
+  if (g.a_kmajor && g.b_kmajor) launch2<BN, 6, true, true>(s, ma, mb, g, e);
+  else if (g.a_kmajor) launch2<BN, 6, true, false>(s, ma, mb, g, e);
+  else if (g.b_kmajor) launch2<BN, 6, false, true>(s, ma, mb, g, e);
+  else launch2<BN, 6, false, false>(s, ma, mb, g, e);
+  return true;
+}
+
 bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e) {
+  if (use_pair_default() && gemm_tc_pair(s, g, e)) return true;
   if (!legal(g)) return false;
   // 128 x 256 tiles unless N is small or a 256-multiple would waste a half tile
   // (measured: 128x128 tiles are shared-memory-bandwidth bound at ~760 TF/s; 128x256 reaches
