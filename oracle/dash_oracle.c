@@ -13,6 +13,7 @@
  */
 #include "dash_oracle.h"
 
+#include <float.h>
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -586,8 +587,9 @@ float dor_gumbel(uint32_t row_key, int32_t token) {
   return -dor_soft_logf(e);
 }
 
-int32_t dor_sample_rule(const float* logits, int vocab, int bos, float inv_t, uint64_t seq_key,
-                        int32_t step) {
+/* Gumbel-max form (kept as an independent reference distribution in the tests). */
+int32_t dor_sample_rule_gumbel(const float* logits, int vocab, int bos, float inv_t, uint64_t seq_key,
+                               int32_t step) {
   const uint32_t rk = dor_row_key(seq_key, step);
   int32_t best = -1;
   float bs = -INFINITY;
@@ -600,6 +602,119 @@ int32_t dor_sample_rule(const float* logits, int vocab, int bos, float inv_t, ui
     }
   }
   return best;
+}
+
+/* ---- the inverse-CDF contract (device: csrc/rule.cuh, kernels_misc.cu
+ * sample_scan_k, gemm_tc.cu epilogue_sample). The reference scans cum += exp(l/T - max)
+ * in id order and takes the first id with u*den < cum (policy.cpp:402-422); this is the
+ * same scan with the sums organised in 32-id slices and 32 blocks of slices. Every
+ * operation is one IEEE rounding (contraction off), so it matches the GPU bit-for-bit. */
+#define DOR_SLICE 32
+static const float kLOG2E = 1.4426950408889634f;
+
+float dor_sexp2(float x) {
+  x = fmaxf(x, -125.f);
+  const float fl = floorf(x);
+  const float f = x - fl;
+  float p = 1.5252734e-05f;
+  p = fmaf(p, f, 1.5403530e-04f);
+  p = fmaf(p, f, 1.3333558e-03f);
+  p = fmaf(p, f, 9.6181291e-03f);
+  p = fmaf(p, f, 5.5504109e-02f);
+  p = fmaf(p, f, 2.4022651e-01f);
+  p = fmaf(p, f, 6.9314718e-01f);
+  p = fmaf(p, f, 1.0f);
+  int32_t bits;
+  memcpy(&bits, &p, 4);
+  bits += (int32_t)fl * (1 << 23);
+  memcpy(&p, &bits, 4);
+  return p;
+}
+
+int32_t dor_sample_rule(const float* logits, int vocab, int bos, float inv_t, uint64_t seq_key, int32_t step) {
+  const int S = (vocab + DOR_SLICE - 1) / DOR_SLICE;
+  float* ms = malloc(sizeof(float) * (size_t)S);
+  float* Zs = malloc(sizeof(float) * (size_t)S);
+  float M = -FLT_MAX;
+  for (int s = 0; s < S; ++s) {
+    float x[DOR_SLICE], m = -FLT_MAX, a[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int i = 0; i < DOR_SLICE; ++i) {
+      const int id = s * DOR_SLICE + i;
+      x[i] = (id < vocab && id != bos) ? logits[id] * inv_t : -FLT_MAX;
+      m = fmaxf(m, x[i]);
+    }
+    for (int i = 0; i < DOR_SLICE; ++i) a[i & 3] = a[i & 3] + (x[i] == -FLT_MAX ? 0.f : dor_sexp2((x[i] - m) * kLOG2E));
+    ms[s] = m;
+    Zs[s] = (a[0] + a[1]) + (a[2] + a[3]);
+    M = fmaxf(M, m);
+  }
+  const int B = (S + 31) / 32;
+  float T[32];
+  for (int j = 0; j < 32; ++j) {
+    T[j] = 0.f;
+    for (int s = j * B; s < S && s < (j + 1) * B; ++s) T[j] = T[j] + Zs[s] * dor_sexp2((ms[s] - M) * kLOG2E);
+  }
+  float total = 0.f;
+  for (int j = 0; j < 32; ++j) total = total + T[j];
+  const uint32_t rk = dor_row_key(seq_key, step);
+  const float u = (float)((rk >> 9) * 2u + 1u) * 0x1.0p-24f;
+  const float target = u * total;
+  int jb = -1, last_j = -1;
+  float base = 0.f, cum = 0.f, last_base = 0.f;
+  for (int j = 0; j < 32; ++j) {
+    const float prev = cum;
+    cum = cum + T[j];
+    if (T[j] > 0.f) {
+      last_j = j;
+      last_base = prev;
+    }
+    if (jb < 0 && target < cum) {
+      jb = j;
+      base = prev;
+    }
+  }
+  if (jb < 0) {
+    jb = last_j;
+    base = last_base;
+  }
+  int sb = -1, last_s = -1;
+  float sbase = 0.f, last_sbase = 0.f, r = base;
+  for (int s = jb * B; s < S && s < (jb + 1) * B; ++s) {
+    const float Ss = Zs[s] * dor_sexp2((ms[s] - M) * kLOG2E);
+    const float prev = r;
+    r = r + Ss;
+    if (Ss > 0.f) {
+      last_s = s;
+      last_sbase = prev;
+    }
+    if (target < r) {
+      sb = s;
+      sbase = prev;
+      break;
+    }
+  }
+  if (sb < 0) {
+    sb = last_s;
+    sbase = last_sbase;
+  }
+  const float scale = dor_sexp2((ms[sb] - M) * kLOG2E);
+  int tk = -1, last_i = -1;
+  r = sbase;
+  for (int i = 0; i < DOR_SLICE; ++i) {
+    const int id = sb * DOR_SLICE + i;
+    if (id >= vocab || id == bos) continue;
+    const float e = dor_sexp2((logits[id] * inv_t - ms[sb]) * kLOG2E);
+    r = fmaf(e, scale, r);
+    last_i = id;
+    if (target < r) {
+      tk = id;
+      break;
+    }
+  }
+  if (tk < 0) tk = last_i;
+  free(ms);
+  free(Zs);
+  return tk;
 }
 
 int dor_sample(const dor_arch* a, const double* params, const int32_t* prompt, int m, int max_len,

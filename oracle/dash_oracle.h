@@ -62,10 +62,15 @@ void dor_grad_log_prob_acc(const dor_arch* a, const double* params, const int32_
 float dor_soft_logf(float x);
 uint32_t dor_row_key(uint64_t seq_key, int32_t step);
 float dor_gumbel(uint32_t row_key, int32_t token);
-/* Gumbel-max over fp32 logits: argmax_i fmaf(logit_i, inv_t, g_i), BOS excluded,
- * ties to the lowest id. */
+/* The sampling contract: inverse CDF over exp(logit/T - max) (BOS excluded) with the
+ * sums organised in 32-id slices and 32 slice blocks, software exp2 (dor_sexp2) and
+ * u = (2*(row_key >> 9) + 1) * 2^-24. */
 int32_t dor_sample_rule(const float* logits, int vocab, int bos, float inv_t, uint64_t seq_key,
                         int32_t step);
+float dor_sexp2(float x);
+/* Gumbel-max over the same counter RNG (an independent alternative rule, tests only). */
+int32_t dor_sample_rule_gumbel(const float* logits, int vocab, int bos, float inv_t, uint64_t seq_key,
+                               int32_t step);
 /* Full-trajectory sampler: fp64 forward, logits rounded to fp32, then the rule.
  * cap = min(max_len, ctx - m); stops at EOS (policy.cpp:387, :425).
  * logp[j] = log softmax at T=1 (fp64). Returns completion length. */

@@ -58,10 +58,10 @@ struct SampleArgs {
   int step = 0;
   float inv_t = 1.f;
   int bos = -1;
-  float* part = nullptr;  // [rows][ntiles][5] (sample) or [rows][ntiles][2] (lse)
+  float* part = nullptr;  // [rows][ntiles][4] (sample: per 32-id slice) or [rows][ntiles][2] (lse)
   int ntiles = 0;
-  float* dump = nullptr;  // optional: logits row r at dump + r * dump_ld (debug / parity)
-  int64_t dump_ld = 0;
+  float* logits = nullptr;  // sample: fp32 logits row r at logits + r * logits_ld (the scan
+  int64_t logits_ld = 0;    //   reads the chosen slice; also the parity dump)
   const float* lse = nullptr;      // DZ: per-row log-sum-exp over non-BOS logits
   const int32_t* target = nullptr; // DZ: per-row target id
   const float* weight = nullptr;   // DZ: per-row weight w_r = A_n / N

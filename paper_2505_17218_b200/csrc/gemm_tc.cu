@@ -220,95 +220,68 @@ __device__ __forceinline__ void epilogue_store(const GemmShape& g, const Epi& e,
   }
 }
 
-// LM-head sampling epilogue on columns [c_lo, c_hi): Gumbel-max argmax + T=1 LSE,
-// one 5-float partial record per (row, column slice).
+// LM-head sampling epilogue (inverse-CDF contract, rule.cuh): per 32-id slice the
+// epilogue stores the fp32 logits (the scan needs the chosen slice's ids) and one
+// 4-float record {m_s, Z_s, m1_s, Z1_s}: the contract's max / sexp2-sum at 1/T and
+// the T=1 log-sum-exp partials for the recorded log-prob. ~13 instructions per id.
 __device__ __forceinline__ void epilogue_sample(const GemmShape& g, const Epi& e, const SampleArgs& sa, uint32_t taddr,
-                                                int row, int n0, int c_lo, int c_hi, int slice) {
+                                                int row, int n0, int c_lo, int c_hi) {
   float v[32];
   const bool live = row < g.M;
-  const uint32_t rk = live ? row_key(sa.keys[row], sa.step) : 0u;
-  float bs = -FLT_MAX, bl = 0.f, mx = -FLT_MAX, se = 0.f;
-  int bi = 0x7fffffff;
+  const bool t1 = sa.inv_t == 1.f;
 #pragma unroll 1
   for (int c = c_lo; c < c_hi; c += 32) {
     tmem_ld32(taddr + c, v);
     if (!live) continue;
     const int nb = n0 + c;
-    float cm = -FLT_MAX;
-    if (nb + 32 <= g.N && (reinterpret_cast<uintptr_t>(e.bias + nb) & 15) == 0) {  // bias (fp32 master)
+    const bool full = nb + 32 <= g.N;
+    if (full && (reinterpret_cast<uintptr_t>(e.bias + nb) & 15) == 0) {  // bias (fp32 master)
 #pragma unroll
       for (int i = 0; i < 32; i += 4) {
         const float4 b = *reinterpret_cast<const float4*>(e.bias + nb + i);
-        v[i] += b.x, v[i + 1] += b.y, v[i + 2] += b.z, v[i + 3] += b.w;
+        v[i] = __fadd_rn(v[i], b.x), v[i + 1] = __fadd_rn(v[i + 1], b.y);
+        v[i + 2] = __fadd_rn(v[i + 2], b.z), v[i + 3] = __fadd_rn(v[i + 3], b.w);
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = nb + i < g.N ? v[i] + e.bias[nb + i] : 0.f;
+      for (int i = 0; i < 32; ++i) v[i] = nb + i < g.N ? __fadd_rn(v[i], e.bias[nb + i]) : 0.f;
     }
-    if (sa.dump) {
+    float* lrow = sa.logits + static_cast<int64_t>(row) * sa.logits_ld + nb;
+    if (full && (reinterpret_cast<uintptr_t>(lrow) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(lrow + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else {
       for (int i = 0; i < 32; ++i)
-        if (nb + i < g.N) sa.dump[static_cast<int64_t>(row) * sa.dump_ld + nb + i] = v[i];
+        if (nb + i < g.N) lrow[i] = v[i];
     }
-    // masking only where a chunk holds BOS or runs past V
-    const bool clean = nb + 32 <= g.N && (sa.bos < nb || sa.bos >= nb + 32);
-    if (!clean) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = (nb + i < g.N && nb + i != sa.bos) ? v[i] : -FLT_MAX;
-    }
-#pragma unroll
-    for (int i = 0; i < 32; ++i) cm = fmaxf(cm, v[i]);
-    // exact Gumbel-max with a conservative filter: the 32 draws are hashed branch-free
-    // (independent -> full ILP); only draws that could still beat the running best are
-    // scored exactly (out-of-line soft logs behind a branch), in ascending id order.
-    int dk[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) dk[i] = static_cast<int>(gumbel_draw(rk, nb + i));
-    if (bs == -FLT_MAX && cm > -FLT_MAX) {
-      // seed the running best with one exact score (the largest draw among valid ids),
-      // so the threshold below already prunes this chunk
-      int kb = -1, ib = -1;
-      float lb = 0.f;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const bool take = v[i] != -FLT_MAX && dk[i] > kb;
-        kb = take ? dk[i] : kb;
-        lb = take ? v[i] : lb;
-        ib = take ? i : ib;
-      }
-      bs = __fmaf_rn(lb, sa.inv_t, gumbel_of_draw(static_cast<uint32_t>(kb)));
-      bi = nb + ib;
-      bl = lb;
-    }
-    const int kthr = gumbel_draw_threshold(bs, cm, sa.inv_t);
-    // (measured: a per-column branch to the out-of-line exact score beats stashing the chunk
-    // in lane-local memory and walking a survivor list: 3.3 vs 4.4 ms per C2 decode step)
+    const bool clean = full && (sa.bos < nb || sa.bos >= nb + 32);
+    float x[32];
+    float m = -FLT_MAX, m1 = -FLT_MAX;
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      if (dk[i] > kthr && v[i] != -FLT_MAX) {  // rare
-        const float sc = __fmaf_rn(v[i], sa.inv_t, gumbel_of_draw(static_cast<uint32_t>(dk[i])));
-        if (better(sc, nb + i, bs, bi)) {
-          bs = sc;
-          bi = nb + i;
-          bl = v[i];
-        }
-      }
+      const bool ok = clean || (nb + i < g.N && nb + i != sa.bos);
+      x[i] = ok ? __fmul_rn(v[i], sa.inv_t) : -FLT_MAX;
+      m = fmaxf(m, x[i]);
+      m1 = fmaxf(m1, ok ? v[i] : -FLT_MAX);
     }
-    if (cm > -FLT_MAX) {
-      const float nm = fmaxf(mx, cm);
-      float a4[4] = {se * __expf(mx - nm), 0.f, 0.f, 0.f};  // 4 chains: the adds overlap
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int i = 0; i < 32; ++i) a4[i & 3] += __expf(v[i] - nm);  // masked ids: exp(-huge) = 0
-      se = (a4[0] + a4[1]) + (a4[2] + a4[3]);
-      mx = nm;
+    for (int i = 0; i < 32; ++i) {
+      const float ei = x[i] == -FLT_MAX ? 0.f : sexp2(__fmul_rn(__fsub_rn(x[i], m), kLog2e));
+      a[i & 3] = __fadd_rn(a[i & 3], ei);
     }
-  }
-  if (live) {
-    float* pp = sa.part + (static_cast<int64_t>(row) * sa.ntiles + slice) * 5;
-    pp[0] = bs;
-    pp[1] = __int_as_float(bi);
-    pp[2] = bl;
-    pp[3] = mx;
-    pp[4] = se;
+    const float Z = __fadd_rn(__fadd_rn(a[0], a[1]), __fadd_rn(a[2], a[3]));
+    float Z1 = Z;
+    if (!t1) {
+      float b4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int i = 0; i < 32; ++i) b4[i & 3] += x[i] == -FLT_MAX ? 0.f : __expf(v[i] - m1);
+      Z1 = (b4[0] + b4[1]) + (b4[2] + b4[3]);
+    } else {
+      m1 = m;
+    }
+    float4* pp = reinterpret_cast<float4*>(sa.part + (static_cast<int64_t>(row) * sa.ntiles + (nb / kSlice)) * 4);
+    *pp = make_float4(m, Z, m1, Z1);
   }
 }
 
@@ -504,7 +477,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
       const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       const int row = m0 + q * 32 + lane;
       if constexpr (MODE == 1)
-        epilogue_sample(g, e, sa, taddr, row, n0, slice * CW, (slice + 1) * CW, (t / tiles_m) * NSL + slice);
+        epilogue_sample(g, e, sa, taddr, row, n0, slice * CW, (slice + 1) * CW);
       else if constexpr (MODE == 2)
         epilogue_lse(g, e, sa, taddr, row, n0, slice * CW, (slice + 1) * CW, (t / tiles_m) * NSL + slice);
       else if constexpr (MODE == 3)
@@ -594,8 +567,7 @@ bool legal(const GemmShape& g) {
 }
 
 constexpr int kSampleBN = 256;
-constexpr int kSampleEPW = 16;  // four 64-column slices per accumulator row: the Gumbel math is ALU-heavy,
-                                // 4 epilogue warps per SM sub-partition hide its latency
+constexpr int kSampleEPW = 8;  // two 128-column halves per accumulator row
 
 // ======================================================= CTA-pair (cta_group::2) variant
 // A cluster of two CTAs on one TPC computes a 256 x BN tile: each CTA stages its own 128
@@ -877,7 +849,7 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e) {
   return true;
 }
 
-int gemm_tc_sample_tiles(int N) { return ((N + kSampleBN - 1) / kSampleBN) * (kSampleEPW / 4); }
+int gemm_tc_sample_tiles(int N) { return (N + kSlice - 1) / kSlice; }  // one record per 32-id slice
 
 int gemm_tc_sample(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa) {
   if (!legal(g) || !g.a_kmajor || !g.b_kmajor) return 0;

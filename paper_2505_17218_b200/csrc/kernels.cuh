@@ -68,15 +68,18 @@ void attn_decode(cudaStream_t s, const T* qkv, const T* kp, const T* vp, const T
 bool attn_decode_tc(cudaStream_t s, const bf16* qkv, const bf16* kp, const bf16* vp, const bf16* kc, const bf16* vc,
                     const int32_t* prompt_len, int rows, int G, int pmax, int n_comp, int cslots, int nh, int nkv,
                     int hd, bf16* ctx, double alg_bytes);
-// One sampling step over fp32 logits rows (policy.cpp:399-426 with the D2 rule).
+// One sampling step over fp32 logits rows [rows x V] (policy.cpp:399-426 with the
+// inverse-CDF contract of rule.cuh): per-slice partials, then sample_scan.
+// part: scratch of rows * ceil(V/32) * 4 floats.
 void sample_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, int eos, float inv_t,
                  const uint64_t* keys, int step, const int32_t* cap, uint8_t* finished, int32_t* comp,
-                 float* logp, int32_t* len, int32_t* tok_next, int max_len, float* dump);
+                 float* logp, int32_t* len, int32_t* tok_next, int max_len, float* part);
 
-// Combine of the fused LM-head sampling partials (gemm_tc_sample) + the same token
-// bookkeeping as sample_rows.
-void sample_reduce(cudaStream_t s, const float* part, int ntiles, int rows, int eos, int step, const int32_t* cap,
-                   uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len);
+// The contract's walk over per-slice partials {m, Z, m1, Z1} (from sample_rows or the
+// fused LM-head GEMM epilogue) + the token bookkeeping (EOS, cap, logp at T = 1).
+void sample_scan(cudaStream_t s, const float* part, int nslices, const float* logits, int64_t logits_ld, int rows,
+                 int V, int bos, int eos, float inv_t, const uint64_t* keys, int step, const int32_t* cap,
+                 uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len);
 
 // Row LSE from gemm_tc_lse partials; if logp != null also logp = logit[y] - lse.
 void lse_reduce(cudaStream_t s, const float* part, int ntiles, int rows, float* lse, const bf16* Y, int d,

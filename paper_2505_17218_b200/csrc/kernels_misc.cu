@@ -192,54 +192,51 @@ __device__ __forceinline__ float block_reduce(float v, float* sm, bool is_max) {
   return r;
 }
 
-__global__ void __launch_bounds__(256) sample_rows_k(const float* logits, int V, int bos, int eos, float inv_t,
-                                                     const uint64_t* keys, int step, const int32_t* cap,
-                                                     uint8_t* finished, int32_t* comp, float* logp, int32_t* len,
-                                                     int32_t* tok_next, int max_len, float* dump) {
-  __shared__ float ss[32];
-  __shared__ int si[32];
-  const int r = blockIdx.x;
-  const bool active = !finished[r] && step < cap[r];
-  if (!active) {
-    if (threadIdx.x == 0) tok_next[r] = eos;
-    return;
-  }
-  const float* lg = logits + static_cast<int64_t>(r) * V;
-  const uint32_t rk = row_key(keys[r], step);
-  ArgBest b{-FLT_MAX, 0x7fffffff};
-  float mx = -FLT_MAX;
-  for (int i = threadIdx.x; i < V; i += blockDim.x) {
-    const float l = lg[i];
-    if (dump) dump[(static_cast<int64_t>(r) * max_len + step) * V + i] = l;
-    if (i == bos) continue;
-    const float sc = gumbel_score(l, inv_t, rk, i);
-    if (better(sc, i, b.s, b.i)) {
-      b.s = sc;
-      b.i = i;
+// Sampling partials from fp32 logits (the fp32 parity path; the bf16 path computes the
+// same records in the LM-head GEMM epilogue): one thread per (row, 32-id slice),
+// operations in the order of the contract (rule.cuh).
+__global__ void sample_partials_k(const float* __restrict__ logits, int rows, int V, int bos, float inv_t,
+                                  float* __restrict__ part, int nslices) {
+  const int64_t n = static_cast<int64_t>(rows) * nslices;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n; w += (int64_t)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(w / nslices), s = static_cast<int>(w % nslices);
+    const float* l = logits + static_cast<int64_t>(r) * V + s * kSlice;
+    float x[kSlice];
+    float m = -FLT_MAX, m1 = -FLT_MAX;
+#pragma unroll
+    for (int i = 0; i < kSlice; ++i) {
+      const int id = s * kSlice + i;
+      const bool ok = id < V && id != bos;
+      x[i] = ok ? __fmul_rn(l[i], inv_t) : -FLT_MAX;
+      m = fmaxf(m, x[i]);
+      m1 = fmaxf(m1, ok ? l[i] : -FLT_MAX);
     }
-    mx = fmaxf(mx, l);
-  }
-  b = block_argmax(b, ss, si);
-  mx = block_reduce(mx, ss, true);
-  float sum = 0.f;
-  for (int i = threadIdx.x; i < V; i += blockDim.x)
-    if (i != bos) sum += __expf(lg[i] - mx);
-  sum = block_reduce(sum, ss, false);
-  if (threadIdx.x == 0) {
-    const int tk = b.i;
-    comp[static_cast<int64_t>(r) * max_len + step] = tk;
-    logp[static_cast<int64_t>(r) * max_len + step] = lg[tk] - (mx + logf(sum));
-    len[r] = step + 1;
-    if (tk == eos) finished[r] = 1;
-    tok_next[r] = tk;
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < kSlice; ++i)
+      a[i & 3] = __fadd_rn(a[i & 3], x[i] == -FLT_MAX ? 0.f : sexp2(__fmul_rn(__fsub_rn(x[i], m), kLog2e)));
+    const float Z = __fadd_rn(__fadd_rn(a[0], a[1]), __fadd_rn(a[2], a[3]));
+    float Z1 = Z;
+    if (inv_t != 1.f) {
+      Z1 = 0.f;
+      for (int i = 0; i < kSlice; ++i)
+        if (x[i] != -FLT_MAX) Z1 += __expf(l[i] - m1);
+    } else {
+      m1 = m;
+    }
+    reinterpret_cast<float4*>(part)[w] = make_float4(m, Z, m1, Z1);
   }
 }
 
-// Cross-tile combine of the fused LM-head sampling partials (one warp per row):
-// argmax of the Gumbel scores (ties -> lowest id) and the T=1 log-sum-exp.
-__global__ void __launch_bounds__(256) sample_reduce_k(const float* __restrict__ part, int ntiles, int rows, int eos,
-                                                       int step, const int32_t* cap, uint8_t* finished, int32_t* comp,
-                                                       float* logp, int32_t* len, int32_t* tok_next, int max_len) {
+// The inverse-CDF walk of the sampling contract (rule.cuh), one warp per row: lane j
+// owns a block of consecutive slices; block, slice and id sums are accumulated in the
+// contract's order, so the chosen id is a pure function of the fp32 logits, 1/T and the
+// row key. Then the token bookkeeping of policy.cpp:423-426 (EOS stops, cap, logp at T=1).
+__global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ part, int nslices,
+                                                     const float* __restrict__ logits, int64_t logits_ld, int rows,
+                                                     int V, int bos, int eos, float inv_t, const uint64_t* keys,
+                                                     int step, const int32_t* cap, uint8_t* finished, int32_t* comp,
+                                                     float* logp, int32_t* len, int32_t* tok_next, int max_len) {
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= rows) return;
   const bool active = !finished[row] && step < cap[row];
@@ -247,48 +244,98 @@ __global__ void __launch_bounds__(256) sample_reduce_k(const float* __restrict__
     if (lane == 0) tok_next[row] = eos;
     return;
   }
-  float bs = -FLT_MAX, bl = 0.f, mx = -FLT_MAX, se = 0.f;
-  int bi = 0x7fffffff;
-  for (int t = lane; t < ntiles; t += 32) {
-    const float* p = part + (static_cast<int64_t>(row) * ntiles + t) * 5;
-    const float s = p[0], l = p[2], m2 = p[3], s2 = p[4];
-    const int i = __float_as_int(p[1]);
-    if (better(s, i, bs, bi)) {
-      bs = s;
-      bi = i;
-      bl = l;
-    }
-    if (m2 > -FLT_MAX) {
-      const float nm = fmaxf(mx, m2);
-      se = se * __expf(mx - nm) + s2 * __expf(m2 - nm);
-      mx = nm;
-    }
+  const float4* P = reinterpret_cast<const float4*>(part) + static_cast<int64_t>(row) * nslices;
+  const int B = (nslices + 31) / 32;
+  const int s0 = lane * B, s1 = min(nslices, s0 + B);
+  float M = -FLT_MAX, M1 = -FLT_MAX;
+  for (int s = s0; s < s1; ++s) {
+    const float4 p = P[s];
+    M = fmaxf(M, p.x);
+    M1 = fmaxf(M1, p.z);
   }
+  M = warp_max(M);
+  M1 = warp_max(M1);
+  float T = 0.f, L1 = 0.f;
+  for (int s = s0; s < s1; ++s) {
+    const float4 p = P[s];
+    T = __fadd_rn(T, __fmul_rn(p.y, sexp2(__fmul_rn(__fsub_rn(p.x, M), kLog2e))));
+    L1 += p.w * __expf(p.z - M1);
+  }
+  L1 = warp_sum(L1);
+  // lane 0: total and block search in lane order
+  float Tj[32];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float s = __shfl_xor_sync(0xffffffffu, bs, o);
-    const int i = __shfl_xor_sync(0xffffffffu, bi, o);
-    const float l = __shfl_xor_sync(0xffffffffu, bl, o);
-    if (better(s, i, bs, bi)) {
-      bs = s;
-      bi = i;
-      bl = l;
+  for (int j = 0; j < 32; ++j) Tj[j] = __shfl_sync(0xffffffffu, T, j);
+  if (lane != 0) return;
+  float total = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) total = __fadd_rn(total, Tj[j]);
+  const float target = __fmul_rn(row_uniform(keys[row], step), total);
+  int jb = -1;
+  float base = 0.f, cum = 0.f, last_base = 0.f;
+  int last_j = -1;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float prev = cum;
+    cum = __fadd_rn(cum, Tj[j]);
+    if (Tj[j] > 0.f) {
+      last_j = j;
+      last_base = prev;
     }
-    const float m2 = __shfl_xor_sync(0xffffffffu, mx, o);
-    const float s2 = __shfl_xor_sync(0xffffffffu, se, o);
-    const float nm = fmaxf(mx, m2);
-    if (nm > -FLT_MAX) {
-      se = se * __expf(mx - nm) + s2 * __expf(m2 - nm);
-      mx = nm;
+    if (jb < 0 && target < cum) {
+      jb = j;
+      base = prev;
     }
   }
-  if (lane == 0) {
-    comp[static_cast<int64_t>(row) * max_len + step] = bi;
-    logp[static_cast<int64_t>(row) * max_len + step] = bl - (mx + logf(se));
-    len[row] = step + 1;
-    if (bi == eos) finished[row] = 1;
-    tok_next[row] = bi;
+  if (jb < 0) {
+    jb = last_j;
+    base = last_base;
   }
+  // slice search inside block jb
+  int sb = -1, last_s = -1;
+  float sbase = 0.f, last_sbase = 0.f, r = base;
+  for (int s = jb * B; s < min(nslices, (jb + 1) * B); ++s) {
+    const float4 p = P[s];
+    const float Ss = __fmul_rn(p.y, sexp2(__fmul_rn(__fsub_rn(p.x, M), kLog2e)));
+    const float prev = r;
+    r = __fadd_rn(r, Ss);
+    if (Ss > 0.f) {
+      last_s = s;
+      last_sbase = prev;
+    }
+    if (target < r) {
+      sb = s;
+      sbase = prev;
+      break;
+    }
+  }
+  if (sb < 0) {
+    sb = last_s;
+    sbase = last_sbase;
+  }
+  // id search inside slice sb
+  const float4 p = P[sb];
+  const float scale = sexp2(__fmul_rn(__fsub_rn(p.x, M), kLog2e));
+  const float* l = logits + static_cast<int64_t>(row) * logits_ld + sb * kSlice;
+  int tk = -1, last_i = -1;
+  r = sbase;
+  for (int i = 0; i < kSlice; ++i) {
+    const int id = sb * kSlice + i;
+    if (id >= V || id == bos) continue;
+    const float e = sexp2(__fmul_rn(__fsub_rn(__fmul_rn(l[i], inv_t), p.x), kLog2e));
+    r = __fmaf_rn(e, scale, r);
+    last_i = id;
+    if (target < r) {
+      tk = id;
+      break;
+    }
+  }
+  if (tk < 0) tk = last_i;
+  comp[static_cast<int64_t>(row) * max_len + step] = tk;
+  logp[static_cast<int64_t>(row) * max_len + step] = l[tk - sb * kSlice] - (M1 + logf(L1));
+  len[row] = step + 1;
+  if (tk == eos) finished[row] = 1;
+  tok_next[row] = tk;
 }
 
 // Row LSE from the LSE-mode GEMM partials; optionally logp = logit[y] - lse with the
@@ -551,12 +598,17 @@ void colsum_acc_f32(cudaStream_t s, const float* X, int64_t ld, int M, int N, fl
 
 void sample_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, int eos, float inv_t,
                  const uint64_t* keys, int step, const int32_t* cap, uint8_t* finished, int32_t* comp, float* logp,
-                 int32_t* len, int32_t* tok_next, int max_len, float* dump) {
-  ProfScope ps(PROF_SAMPLE, s, 0, 4.0 * rows * static_cast<double>(V));
-  sample_rows_k<<<rows, 256, 0, s>>>(logits, V, bos, eos, inv_t, keys, step, cap, finished, comp, logp, len, tok_next,
-                                     max_len, dump);
-  DCU_LAUNCHED();
+                 int32_t* len, int32_t* tok_next, int max_len, float* part) {
+  const int ns = (V + kSlice - 1) / kSlice;
+  {
+    ProfScope ps(PROF_SAMPLE, s, 0, 4.0 * rows * static_cast<double>(V));
+    sample_partials_k<<<grid1d(static_cast<int64_t>(rows) * ns), 256, 0, s>>>(logits, rows, V, bos, inv_t, part, ns);
+    DCU_LAUNCHED();
+  }
+  sample_scan(s, part, ns, logits, V, rows, V, bos, eos, inv_t, keys, step, cap, finished, comp, logp, len, tok_next,
+              max_len);
 }
+
 
 void lse_reduce(cudaStream_t s, const float* part, int ntiles, int rows, float* lse, const bf16* Y, int d,
                 const bf16* W, const float* bias, const int32_t* target, float* logp) {
@@ -565,10 +617,11 @@ void lse_reduce(cudaStream_t s, const float* part, int ntiles, int rows, float* 
   DCU_LAUNCHED();
 }
 
-void sample_reduce(cudaStream_t s, const float* part, int ntiles, int rows, int eos, int step, const int32_t* cap,
-                   uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len) {
-  sample_reduce_k<<<cdiv(rows, 8), 256, 0, s>>>(part, ntiles, rows, eos, step, cap, finished, comp, logp, len, tok_next,
-                                                max_len);
+void sample_scan(cudaStream_t s, const float* part, int nslices, const float* logits, int64_t logits_ld, int rows,
+                 int V, int bos, int eos, float inv_t, const uint64_t* keys, int step, const int32_t* cap,
+                 uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len) {
+  sample_scan_k<<<cdiv(rows, 8), 256, 0, s>>>(part, nslices, logits, logits_ld, rows, V, bos, eos, inv_t, keys, step,
+                                              cap, finished, comp, logp, len, tok_next, max_len);
   DCU_LAUNCHED();
 }
 

@@ -739,33 +739,39 @@ struct Engine {
     T* yT = ws.get<T>("d_yT", static_cast<size_t>(S) * g.d);
     gather_rows<T>(st, A.yT, g.d, d_last, S, g.d, yT);
     // LM head + sampling step: fused tcgen05 epilogue (bf16) or GEMM + row kernel (fp32 parity path)
-    float* logits = nullptr;
-    float* part = nullptr;
-    if constexpr (sizeof(T) == 2) part = ws.get<float>("d_part", static_cast<size_t>(S) * gemm_tc_sample_tiles(g.V) * 5);
+    const int nslices = (g.V + 31) / 32;
+    float* part = ws.get<float>("d_part", static_cast<size_t>(S) * nslices * 4);
+    float* logits = ws.get<float>("d_logits", static_cast<size_t>(S) * g.V);
     auto lm_sample = [&](const T* yrows, int step) {
       if constexpr (sizeof(T) == 2) {
+        // the epilogue writes the logits straight into the parity dump when one is requested
+        float* lg = dump ? dump + static_cast<int64_t>(step) * g.V : logits;
+        const int64_t ld = dump ? static_cast<int64_t>(std::max(ML, 1)) * g.V : g.V;
         SampleArgs sa;
         sa.keys = d_keys;
         sa.step = step;
         sa.inv_t = inv_t;
         sa.bos = g.bos;
         sa.part = part;
-        sa.dump = dump ? dump + static_cast<int64_t>(step) * g.V : nullptr;
-        sa.dump_ld = static_cast<int64_t>(std::max(ML, 1)) * g.V;
+        sa.logits = lg;
+        sa.logits_ld = ld;
         GemmShape gs{S, g.V, g.d, yrows, g.d, true, W(L.wout), g.d, true};
         const int nt = gemm_tc_sample(st, gs, W32(L.bout), sa);
         if (nt > 0) {
-          sample_reduce(st, part, nt, S, g.eos, step, d_cap, d_fin, P.d_comp.as<int32_t>(), P.d_logp.as<float>(),
-                        P.d_len.as<int32_t>(), d_tok, ML);
+          sample_scan(st, part, nt, lg, ld, S, g.V, g.bos, g.eos, inv_t, d_keys, step, d_cap, d_fin,
+                      P.d_comp.as<int32_t>(), P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML);
           return;
         }
       }
-      if (!logits) logits = ws.get<float>("d_logits", static_cast<size_t>(S) * g.V);
       Epi el = store(logits, g.V, nullptr, 0);
       el.bias = W32(L.bout);
       mm(S, g.V, g.d, yrows, g.d, true, W(L.wout), g.d, true, el);
       sample_rows(st, logits, S, g.V, g.bos, g.eos, inv_t, d_keys, step, d_cap, d_fin, P.d_comp.as<int32_t>(),
-                  P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML, dump);
+                  P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML, part);
+      if (dump)
+        DCU_CHECK(cudaMemcpy2DAsync(dump + static_cast<int64_t>(step) * g.V,
+                                    sizeof(float) * static_cast<size_t>(std::max(ML, 1)) * g.V, logits,
+                                    sizeof(float) * g.V, sizeof(float) * g.V, S, cudaMemcpyDeviceToDevice, st));
     };
     lm_sample(yT, 0);
 
