@@ -234,6 +234,7 @@ __device__ __forceinline__ void epilogue_sample(const GemmShape& g, const Epi& e
     tmem_ld32(taddr + c, v);
     if (!live) continue;
     const int nb = n0 + c;
+    if (nb >= g.N) continue;  // ragged last tile: no slice record past V
     const bool full = nb + 32 <= g.N;
     if (full && (reinterpret_cast<uintptr_t>(e.bias + nb) & 15) == 0) {  // bias (fp32 master)
 #pragma unroll
@@ -801,13 +802,13 @@ void launch2(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const
   DCU_LAUNCHED();
 }
 
-bool use_pair_default() {
-  static int v = -1;
-  if (v < 0) {
+int use_pair_default() {
+  static int v = -2;
+  if (v == -2) {
     const char* s = getenv("DASHCU_GEMM_PAIR");
     v = s ? atoi(s) : 0;
   }
-  return v != 0;
+  return v;
 }
 
 }  // namespace
@@ -828,17 +829,19 @@ bool gemm_tc_pair(cudaStream_t s, const GemmShape& g, const Epi& e) {
 }
 
 bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e) {
-  if (use_pair_default() && gemm_tc_pair(s, g, e)) return true;
   if (!legal(g)) return false;
-  // 128 x 256 tiles unless N is small or a 256-multiple would waste a half tile
-  // (measured: 128x128 tiles are shared-memory-bandwidth bound at ~760 TF/s; 128x256 reaches
-  // ~1100 even with a ragged last tile, so N = 896 also takes the wide tile)
-  // Pick the tile width by the persistent schedule: rounds = ceil(tiles / SMs), and a
-  // 128-wide tile costs ~0.66 of a 256-wide one (measured efficiency 0.76 vs 1.0).
-  const int tm = (g.M + BM - 1) / BM;
-  const double r128 = std::ceil(tm * ((g.N + 127) / 128) / static_cast<double>(num_sms()));
-  const double r256 = std::ceil(tm * ((g.N + 255) / 256) / static_cast<double>(num_sms()));
-  const bool wide = r256 * 256.0 <= r128 * 128.0 / 0.76;
+  // Tile shape by the persistent schedule: time ~ rounds x per-tile cost, rounds =
+  // ceil(tiles / concurrent CTAs). Measured per-SM efficiencies: 128x128 tiles 0.76
+  // (shared-memory bound), 128x256 1.0, CTA-pair 256x256 1.12 (B staged half per SM).
+  const int tm = (g.M + BM - 1) / BM, tm2 = (g.M + 255) / 256;
+  const double sms = static_cast<double>(num_sms());
+  const double r128 = std::ceil(tm * ((g.N + 127) / 128) / sms);
+  const double r256 = std::ceil(tm * ((g.N + 255) / 256) / sms);
+  const double rpair = std::ceil(tm2 * ((g.N + 255) / 256) / std::floor(sms / 2));
+  const double c128 = r128 * 0.5 / 0.76, c256 = r256, cpair = rpair / 1.12;
+  const int forced = use_pair_default();  // DASHCU_GEMM_PAIR: 1 force pair, 0 model, -1 never
+  if (forced != -1 && (forced == 1 || (cpair < c256 && cpair < c128)) && gemm_tc_pair(s, g, e)) return true;
+  const bool wide = c256 <= c128;
   const int BN = wide ? 256 : 128;
   CUtensorMap ma, mb;
   bool ok = g.a_kmajor ? make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) : make_map(&ma, g.A, g.K, g.M, g.lda, 64, BK);
