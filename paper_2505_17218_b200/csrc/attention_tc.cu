@@ -391,13 +391,11 @@ template <int HD>
 struct BwdCfg {
   static constexpr int UNITS = HD / 8;
   static constexpr int TILE = 64 * HD * 2;
-  static constexpr int SMEM = 6 * TILE /*K V, Q dO x 2*/ + 64 * 64 * 2 /*dS^T*/ + 4 * 64 * 4 /*lse, D x 2*/;
+  static constexpr int SMEM = 4 * TILE /*K V Q dO*/ + 64 * 64 * 2 /*dS^T*/ + 2 * 64 * 4 /*lse, D*/;
 };
 
 template <int HD>
-// (measured: forcing 3 CTAs/SM at HD 64 caps registers at 168 and spills; slower)
-__global__ void __launch_bounds__(128, 1)
-    attn_bwd_tc_k(const bf16* __restrict__ qkv, const bf16* __restrict__ dctx,
+__global__ void __launch_bounds__(128) attn_bwd_tc_k(const bf16* __restrict__ qkv, const bf16* __restrict__ dctx,
                                                      const float* __restrict__ lse, const float* __restrict__ Dsum,
                                                      const int32_t* __restrict__ seq_start, int nh, int nkv,
                                                      float* __restrict__ dq32, float* __restrict__ dkv32, float scale,
@@ -412,10 +410,10 @@ __global__ void __launch_bounds__(128, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int grp = nh / nkv;
   const int qd = nh * HD, kvd = nkv * HD, qkvd = qd + 2 * kvd;
-  const uint32_t sK = smem_addr(smem), sV = sK + Cf::TILE, sQb = sV + Cf::TILE, sOb = sQb + 2 * Cf::TILE,
-                 sS = sOb + 2 * Cf::TILE;
-  float* sLb = reinterpret_cast<float*>(smem + 6 * Cf::TILE + 64 * 64 * 2);  // [2][64]
-  float* sDb = sLb + 128;                                                    // [2][64]
+  const uint32_t sK = smem_addr(smem), sV = sK + Cf::TILE, sQ = sV + Cf::TILE, sO = sQ + Cf::TILE,
+                 sS = sO + Cf::TILE;
+  float* sL = reinterpret_cast<float*>(smem + 4 * Cf::TILE + 64 * 64 * 2);
+  float* sD = sL + 64;
 
   auto load_tile = [&](uint32_t dst, const bf16* base, int64_t ld, int row0) {
 #pragma unroll
@@ -440,33 +438,21 @@ __global__ void __launch_bounds__(128, 1)
   const int kr0 = k0 + warp * 16;  // this warp's first key (sequence-relative)
   const int nqt = (n + 63) / 64;
 
-  // (query head, query tile) iterations, double-buffered: the Q / dO tiles (and LSE, D)
-  // of iteration it+1 stream in while iteration it computes.
-  const int nq = nqt - kt, iters = grp * nq;
-  auto issue = [&](int it, int buf) {
-    const int h = kvh * grp + it / nq, q0 = (kt + it % nq) * 64;
-    load_tile(sQb + buf * Cf::TILE, qkv + h * HD, qkvd, q0);
-    load_tile(sOb + buf * Cf::TILE, dctx + h * HD, qd, q0);
-    if (threadIdx.x < 64) {  // async 4-byte copies: no thread stalls on global latency here
-      const int q = q0 + threadIdx.x;
-      const bool ok = q < n;
-      const int64_t off = static_cast<int64_t>(s0 + (ok ? q : 0)) * nh + h;
-      cp_async4(smem_addr(sLb + buf * 64 + threadIdx.x), lse + off, ok ? 4 : 0);
-      cp_async4(smem_addr(sDb + buf * 64 + threadIdx.x), Dsum + off, ok ? 4 : 0);
-    }
-    cp_async_commit();
-  };
-  issue(0, 0);
-  for (int it = 0; it < iters; ++it) {
-      const int buf = it & 1;
-      const int h = kvh * grp + it / nq, q0 = (kt + it % nq) * 64;
-      if (it + 1 < iters) issue(it + 1, buf ^ 1);
-      else cp_async_commit();
-      cp_async_wait<1>();
-      __syncthreads();  // tile `it` landed; every warp is past iteration it-1's reads of this buffer
-      const uint32_t sQ = sQb + buf * Cf::TILE, sO = sOb + buf * Cf::TILE;
-      const float* sL = sLb + buf * 64;
-      const float* sD = sDb + buf * 64;
+  for (int hh = 0; hh < grp; ++hh) {
+    const int h = kvh * grp + hh;
+    for (int qt = kt; qt < nqt; ++qt) {
+      const int q0 = qt * 64;
+      __syncthreads();  // previous iteration done with sQ / sO / sS
+      load_tile(sQ, qkv + h * HD, qkvd, q0);
+      load_tile(sO, dctx + h * HD, qd, q0);
+      cp_async_commit();
+      if (threadIdx.x < 64) {
+        const int q = q0 + threadIdx.x;
+        sL[threadIdx.x] = q < n ? lse[static_cast<int64_t>(s0 + q) * nh + h] * 1.4426950408889634f : 0.f;
+        sD[threadIdx.x] = q < n ? Dsum[static_cast<int64_t>(s0 + q) * nh + h] : 0.f;
+      }
+      cp_async_wait<0>();
+      __syncthreads();
       // S^T [16 keys x 64 q] and dP^T
       float st_[8][4], dp[8][4];
 #pragma unroll
@@ -503,7 +489,7 @@ __global__ void __launch_bounds__(128, 1)
           const int q = q0 + qc;
           const int key = kr0 + g + (e >> 1) * 8;
           const bool ok = q < n && key <= q && key < n;
-          const float p = ok ? exp2f(st_[nt][e] * scale_log2 - sL[qc] * 1.4426950408889634f) : 0.f;
+          const float p = ok ? exp2f(st_[nt][e] * scale_log2 - sL[qc]) : 0.f;
           st_[nt][e] = p;
           dp[nt][e] = p * (dp[nt][e] - sD[qc]) * scale;
         }
@@ -581,8 +567,8 @@ __global__ void __launch_bounds__(128, 1)
                        : "memory");
         }
       }
+    }
   }
-  cp_async_wait<0>();
   // dK, dV of this warp's 16 keys (the tile owns them for the whole KV group)
 #pragma unroll
   for (int hh2 = 0; hh2 < 2; ++hh2) {
