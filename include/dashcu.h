@@ -132,9 +132,9 @@ DASHCU_API int dashcu_policy_version(dashcu_policy* pol, uint64_t* version);
  *   completions [n_seq*max_len] (row s: tokens, unused tail = -1)
  *   lengths     [n_seq]
  *   logp        [n_seq*max_len]  per-token log-probs at T=1 (trajectory.hpp:8-9)
- * Sampling rule: Gumbel-max over fp32 logits with the counter RNG of
- * DESIGN.md §4 (the reference inverse-CDF+mt19937 rule cannot be replayed on
- * a GPU; SURVEY App.B D2). The rollout stays resident for accumulate. */
+ * Sampling rule: inverse CDF over fp32 logits organised in 32-id slices, one
+ * counter-RNG draw per step (the reference's fp64 cumsum +
+ * mt19937 stream cannot be replayed on a GPU, SURVEY App.B D2). The rollout stays resident for accumulate. */
 DASHCU_API int dashcu_sample(dashcu_policy* pol, const dashcu_plan* plan, const int32_t* prompt_tokens,
                   const int64_t* prompt_offsets, int32_t* completions, int32_t* lengths, float* logp);
 /* Same with explicit per-sequence keys (seq_keys[n_prompts*group_size]) instead of

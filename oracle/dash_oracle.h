@@ -5,7 +5,7 @@
  * (SURVEY §8c "CPU restatements required"):
  *   1. PG accumulate          sum_kept (A_n / N) * grad log pi   (App.B D4)
  *   2. Adam / SGD             SPEC:329-337 (ascent)
- *   3. Gumbel-max sampling    counter-RNG contract of DESIGN.md §4 (App.B D2)
+ *   3. Sampling               inverse-CDF counter-RNG contract of DESIGN.md §4 (App.B D2)
  *   4. GQA geometry           (n_heads, n_kv_heads, head_dim); (1, 1, d) is the reference
  * Parity pin: at GQA (1,1,d) the forward is evaluated in the reference's
  * operation order, so log-probs equal oracle/_ref bit-for-bit; gradients are

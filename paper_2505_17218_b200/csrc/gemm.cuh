@@ -46,9 +46,9 @@ struct GemmShape {
 };
 
 // LM-head sampling epilogue (policy.cpp:148-151 + :399-424 with the DESIGN.md §4 rule):
-// logits never leave the SM. Per (row, N tile) the epilogue writes 5 floats
-//   {best Gumbel score, best id (bit pattern), logit of best, max logit, sum exp(logit - max)}
-// over non-BOS ids; sample_reduce combines the tiles of a row.
+// per (row, 32-id slice) the epilogue writes one float4 {m_s, Z_s, m1_s, Z1_s}: the slice
+// max and sexp2 sum at 1/T and at T = 1 over non-BOS ids, plus the fp32 logits;
+// sample_scan walks the slice sums of a row (inverse CDF) and picks the token.
 // The same tile machinery also runs the LM-head backward without ever storing
 // fp32 logits (policy.cpp:471-483): pass 1 (LSE mode) writes per (row, slice)
 // {max, sum exp} partials, lse_reduce makes the row LSE; pass 2 (DZ mode)

@@ -13,7 +13,7 @@
 //   warp 2      TMEM allocator (2 x BN columns)
 //   warps 4..   epilogue (EPW warps): tcgen05.ld 32 columns at a time -> bias /
 //               tanh / dtanh / residual / fp32 accumulate (16-byte vector I/O),
-//               or the fused LM-head sampling reduction (Gumbel argmax + LSE)
+//               or the fused LM-head sampling reduction (inverse-CDF slice sums + LSE)
 // Operand major-ness is encoded in the UMMA instruction descriptor (bits 15/16)
 // and the shared-memory descriptors (K-major: SBO = 1024 B between 8-row groups;
 // MN-major: LBO = one 64-element TMA box, SBO = 1024 B between 8-k groups).

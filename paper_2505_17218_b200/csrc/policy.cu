@@ -6,7 +6,7 @@
 //   dashcu_sample      prefill of the M prompts (once per group, not G times:
 //                      policy.cpp:396 re-runs the prompt for every sample),
 //                      then one decode step per completion position over all
-//                      M*G sequences, KV in HBM, Gumbel-max sampling.
+//                      M*G sequences, KV in HBM, inverse-CDF counter-RNG sampling.
 //   dashcu_rollout_advantage   one thread per group, fp64, + compaction.
 //   dashcu_accumulate  packed teacher-forced forward + exact reverse pass per
 //                      micro-batch of kept sequences; weight gradients
