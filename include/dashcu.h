@@ -202,6 +202,10 @@ typedef struct {
 } dashcu_kprof;
 DASHCU_API int dashcu_profile_enable(unsigned class_mask);
 DASHCU_API int dashcu_profile_read(dashcu_kprof* out, int max, int reset);
+/* With bit 31 of the class mask set, launches are also aggregated per key (kernel
+ * variant + shape). Text, one line per key: "class key\tlaunches\tms\tflops\tbytes".
+ * Returns the full length; copies at most cap-1 bytes + NUL. Reset with profile_read. */
+DASHCU_API int64_t dashcu_profile_keys(char* buf, int64_t cap);
 
 /* ---- diagnostics (used by the kernel tests) ----
  * C[M x N] (fp32, ldc = N) = A(m,k) . B(n,k) on bf16 operands given as raw

@@ -139,6 +139,8 @@ def lib():
         L.dashcu_profile_enable.restype = C.c_int
         L.dashcu_profile_read.argtypes = [C.c_void_p, C.c_int, C.c_int]
         L.dashcu_profile_read.restype = C.c_int
+        L.dashcu_profile_keys.argtypes = [C.c_char_p, C.c_int64]
+        L.dashcu_profile_keys.restype = C.c_int64
         _lib = L
     return _lib
 
@@ -165,12 +167,29 @@ class KProf(C.Structure):
 PROF_CLASSES = ("gemm_tc", "gemm_simt", "attn_decode", "attn_fwd", "attn_bwd", "sample", "lm_rows", "optimizer")
 
 
-def profile_enable(classes=PROF_CLASSES):
-    """Bracket every launch of the given kernel classes with CUDA events (algorithmic flops/bytes)."""
+def profile_enable(classes=PROF_CLASSES, keys=False):
+    """Bracket every launch of the given kernel classes with CUDA events (algorithmic flops/bytes).
+    keys=True also aggregates per kernel variant + shape (profile_keys)."""
     mask = 0
     for c in classes:
         mask |= 1 << PROF_CLASSES.index(c)
+    if keys:
+        mask |= 1 << 31
     lib().dashcu_profile_enable(C.c_uint(mask))
+
+
+def profile_keys() -> list:
+    """Per-key aggregates [(key, launches, ms, flops, bytes)], largest time first."""
+    n = lib().dashcu_profile_keys(None, 0)
+    if n < 0:
+        raise DeviceError("profile read failed")
+    buf = C.create_string_buffer(n + 1)
+    lib().dashcu_profile_keys(buf, n + 1)
+    out = []
+    for line in buf.value.decode().splitlines():
+        k, l, ms, f, b = line.split("\t")
+        out.append((k, int(l), float(ms), float(f), float(b)))
+    return sorted(out, key=lambda r: -r[2])
 
 
 def profile_read(reset=True) -> dict:

@@ -54,7 +54,9 @@ enum ProfClass : int {
 extern const char* const kProfNames[PROF_NUM];
 extern unsigned g_prof_mask;
 void prof_begin(int cls, cudaStream_t s, cudaEvent_t* ev);
-void prof_end(int cls, cudaStream_t s, cudaEvent_t ev0, double flops, double bytes);
+void prof_end(int cls, cudaStream_t s, cudaEvent_t ev0, double flops, double bytes, const char* key);
+// mask bit 31: also aggregate per launch key (kernel variant + shape), see dashcu_profile_keys
+constexpr unsigned kProfKeysBit = 1u << 31;
 
 struct ProfScope {
   int cls;
@@ -62,12 +64,15 @@ struct ProfScope {
   double flops, bytes;
   cudaEvent_t ev = nullptr;
   bool on;
+  char key[96];
   ProfScope(int c, cudaStream_t st, double f, double b) : cls(c), s(st), flops(f), bytes(b) {
     on = (g_prof_mask >> c) & 1u;
+    key[0] = 0;
     if (on) prof_begin(c, s, &ev);
   }
+  bool keyed() const { return on && (g_prof_mask & kProfKeysBit); }
   ~ProfScope() {
-    if (on) prof_end(cls, s, ev, flops, bytes);
+    if (on) prof_end(cls, s, ev, flops, bytes, key[0] ? key : nullptr);
   }
 };
 

@@ -547,6 +547,9 @@ void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const 
   const int grid = ntile < num_sms() ? ntile : num_sms();
   ProfScope ps(MODE == 1 ? PROF_SAMPLE : MODE >= 2 ? PROF_LM_ROWS : PROF_GEMM_TC, s,
                2.0 * g.M * g.N * static_cast<double>(g.K), 0);
+  if (ps.keyed())
+    snprintf(ps.key, sizeof(ps.key), "mode%d 128x%d M%d N%d K%d %c%c epi%d", MODE, BN, g.M, g.N, g.K,
+             AK ? 'k' : 'm', BKM ? 'k' : 'm', e.kind);
   k<<<grid, C::THREADS, C::SMEM, s>>>(ma, mb, g, e, sa);
   DCU_LAUNCHED();
 }
@@ -798,6 +801,9 @@ void launch2(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const
   cfg.attrs = attr_c;
   cfg.numAttrs = 1;
   ProfScope ps(PROF_GEMM_TC, s, 2.0 * g.M * g.N * static_cast<double>(g.K), 0);
+  if (ps.keyed())
+    snprintf(ps.key, sizeof(ps.key), "pair 256x%d M%d N%d K%d %c%c epi%d", BN, g.M, g.N, g.K, AK ? 'k' : 'm',
+             BKM ? 'k' : 'm', e.kind);
   DCU_CHECK(cudaLaunchKernelEx(&cfg, k, ma, mb, g, e));
   DCU_LAUNCHED();
 }

@@ -1,5 +1,9 @@
 // Kernel-class profiler (see common.cuh ProfScope) + its C-ABI readers.
+#include <algorithm>
+#include <cstring>
+#include <map>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "../../include/dashcu.h"
@@ -17,6 +21,12 @@ struct Pending {
   int cls;
   cudaEvent_t a, b;
   double flops, bytes;
+  std::string key;
+};
+
+struct Agg {
+  double ms = 0, flops = 0, bytes = 0;
+  int64_t launches = 0;
 };
 
 struct Prof {
@@ -27,6 +37,7 @@ struct Prof {
   double flops[PROF_NUM] = {};
   double bytes[PROF_NUM] = {};
   int64_t launches[PROF_NUM] = {};
+  std::map<std::string, Agg> keys;
 
   cudaEvent_t get() {
     if (!pool.empty()) {
@@ -47,6 +58,13 @@ struct Prof {
       flops[p.cls] += p.flops;
       bytes[p.cls] += p.bytes;
       launches[p.cls] += 1;
+      if (!p.key.empty()) {
+        Agg& a = keys[p.key];
+        a.ms += t;
+        a.flops += p.flops;
+        a.bytes += p.bytes;
+        a.launches += 1;
+      }
       pool.push_back(p.a);
       pool.push_back(p.b);
     }
@@ -68,12 +86,12 @@ void prof_begin(int, cudaStream_t s, cudaEvent_t* ev) {
   DCU_CHECK(cudaEventRecord(*ev, s));
 }
 
-void prof_end(int cls, cudaStream_t s, cudaEvent_t ev0, double flops, double bytes) {
+void prof_end(int cls, cudaStream_t s, cudaEvent_t ev0, double flops, double bytes, const char* key) {
   Prof& p = prof();
   std::lock_guard<std::mutex> lk(p.mu);
   cudaEvent_t e = p.get();
   DCU_CHECK(cudaEventRecord(e, s));
-  p.pending.push_back({cls, ev0, e, flops, bytes});
+  p.pending.push_back({cls, ev0, e, flops, bytes, key ? std::string(kProfNames[cls]) + " " + key : std::string()});
   if (p.pending.size() > 65536) p.drain();
 }
 
@@ -101,9 +119,37 @@ DASHCU_API int dashcu_profile_read(dashcu_kprof* out, int max, int reset) {
       out[n].flops = p.flops[c];
       out[n].bytes = p.bytes[c];
     }
-    if (reset)
+    if (reset) {
       for (int c = 0; c < PROF_NUM; ++c) p.ms[c] = p.flops[c] = p.bytes[c] = 0, p.launches[c] = 0;
+      p.keys.clear();
+    }
     return n;
+  } catch (...) {
+    return -1;
+  }
+}
+
+// One line per launch key: "<class> <key>\t<launches>\t<ms>\t<flops>\t<bytes>\n".
+// Returns the bytes needed (excluding the NUL); writes at most cap-1 of them.
+DASHCU_API int64_t dashcu_profile_keys(char* buf, int64_t cap) {
+  using namespace dashcu;
+  try {
+    Prof& p = prof();
+    std::lock_guard<std::mutex> lk(p.mu);
+    p.drain();
+    std::string out;
+    char line[256];
+    for (auto& kv : p.keys) {
+      snprintf(line, sizeof(line), "%s\t%lld\t%.6f\t%.6e\t%.6e\n", kv.first.c_str(),
+               static_cast<long long>(kv.second.launches), kv.second.ms, kv.second.flops, kv.second.bytes);
+      out += line;
+    }
+    if (buf && cap > 0) {
+      const int64_t n = std::min<int64_t>(cap - 1, static_cast<int64_t>(out.size()));
+      memcpy(buf, out.data(), n);
+      buf[n] = 0;
+    }
+    return static_cast<int64_t>(out.size());
   } catch (...) {
     return -1;
   }

@@ -21,9 +21,10 @@ def main():
     prompts = W.synthetic_prompts(1, 0, M, P, arch["vocab_size"], 0, 1)
     tok, off = np.ascontiguousarray(prompts.reshape(-1)), (np.arange(M + 1) * P).astype(np.int64)
     pol.sample(None, G, steps, prompt_tokens=tok, prompt_offsets=off)     # warm-up
-    D.profile_enable()
+    D.profile_enable(keys=True)
     D.profile_read(reset=True)
     pol.sample(None, G, steps, prompt_tokens=tok, prompt_offsets=off)
+    keys = D.profile_keys()
     prof = D.profile_read(reset=True)
     D.profile_enable(())
     st = pol.stats()
@@ -31,6 +32,8 @@ def main():
                "tflops": v["flops"] / max(v["ms"], 1e-9) / 1e9, "gbs": v["bytes"] / max(v["ms"], 1e-9) / 1e6}
            for k, v in prof.items() if v["launches"]}
     print(json.dumps({"decode_steps": steps, "sample_ms": st["sample_ms"], "classes": out}))
+    for k, n, ms, f, b in keys:
+        print(f"{ms:9.3f} ms {n:4d}x {f / max(ms, 1e-9) / 1e9:7.1f} TF/s  {k}")
 
 
 if __name__ == "__main__":

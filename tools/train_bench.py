@@ -26,9 +26,10 @@ def main():
     w = np.full(n_seq, 1.0 / n_seq)
     pol.grad_zero()
     pol.accumulate_weighted(w, micro_batch=n_seq)   # warm-up (allocations)
-    D.profile_enable()
+    D.profile_enable(keys=True)
     D.profile_read(reset=True)
     pol.accumulate_weighted(w, micro_batch=n_seq)
+    keys = D.profile_keys()
     prof = D.profile_read(reset=True)
     D.profile_enable(())
     st = pol.stats()
@@ -36,6 +37,8 @@ def main():
            for k, v in prof.items() if v["launches"]}
     print(json.dumps({"seqs": n_seq, "tokens": n_seq * (P + L - 1), "accumulate_ms": st["accumulate_ms"],
                       "classes": out}))
+    for k, n, ms, f, b in keys:
+        print(f"{ms:9.3f} ms {n:4d}x {f / max(ms, 1e-9) / 1e9:7.1f} TF/s  {k}")
 
 
 if __name__ == "__main__":
