@@ -33,6 +33,7 @@ struct Epi {
   int64_t ldc32 = 0;
   void* cT = nullptr;            // T output (operand copy for the next GEMM)
   int64_t ldcT = 0;
+  int tma = 0;                   // set by the tcgen05 launcher: bit 0 c32, bit 1 cT via bulk tensor stores
 };
 
 struct GemmShape {

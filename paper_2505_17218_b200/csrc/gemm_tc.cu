@@ -21,6 +21,8 @@
 #include <cudaTypedefs.h>
 
 #include <cfloat>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "gemm.cuh"
@@ -124,18 +126,107 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// ---- TMA-store epilogue -----------------------------------------------------------
+// A thread owns one accumulator row, so direct 16-byte stores from a warp touch 32
+// different rows per instruction (32 L1 wavefronts each). Instead every epilogue warp
+// stages its 32 rows x 32 columns in a private 4 KB shared-memory buffer (in the TMA
+// swizzle, so the 8 lanes of each store phase hit distinct banks) and one lane issues
+// a bulk tensor store (or an fp32 reduce-add for EPI_ACCUM) of the 32 x 32 box; the
+// tensor map clips rows >= M and columns >= N.
+constexpr int kStageBytes = 4096;
+
+// fp32 row of 32 (128 B, SWIZZLE_128B): 16-B chunk j of row r at r*128 + (j ^ (r & 7))*16
+__device__ __forceinline__ void stage_f32(uint32_t buf, int lane, const float* v) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(buf + lane * 128 + ((j ^ (lane & 7)) << 4)),
+                 "f"(v[4 * j]), "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                 : "memory");
+}
+// bf16 row of 32 (64 B, SWIZZLE_64B): chunk j of row r at r*64 + (j ^ ((r >> 1) & 3))*16
+__device__ __forceinline__ void stage_b16(uint32_t buf, int lane, const float* v) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(buf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)),
+                 "r"(pack2(v[8 * j], v[8 * j + 1])), "r"(pack2(v[8 * j + 2], v[8 * j + 3])),
+                 "r"(pack2(v[8 * j + 4], v[8 * j + 5])), "r"(pack2(v[8 * j + 6], v[8 * j + 7]))
+                 : "memory");
+}
+// Before overwriting the warp's buffer: the previous bulk store has finished reading it.
+__device__ __forceinline__ void stage_acquire(int lane) {
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  __syncwarp();
+}
+// After all lanes staged: make the writes visible to the async proxy, one lane stores.
+__device__ __forceinline__ void stage_release(int lane, const CUtensorMap* map, uint32_t buf, int col, int row,
+                                              bool reduce_add) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    if (reduce_add)
+      asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                       reinterpret_cast<uint64_t>(map)),
+                   "r"(buf), "r"(col), "r"(row)
+                   : "memory");
+    else
+      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                       reinterpret_cast<uint64_t>(map)),
+                   "r"(buf), "r"(col), "r"(row)
+                   : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
+__device__ __forceinline__ void stage_drain(int lane) {
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  __syncwarp();
+}
+
+// Output maps of the TMA-store epilogue (Epi::tma bits 0 / 1).
+struct OutMaps {
+  CUtensorMap f32;  // 32 x 32 fp32 box, SWIZZLE_128B: c32 / logits
+  CUtensorMap b16;  // 32 x 32 bf16 box, SWIZZLE_64B: cT / dz
+};
+
 template <int BN, int STAGES, bool AK, bool BKM, int EPW>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int STG_OFF = STAGES * STAGE_BYTES;  // EPW x 4 KB epilogue staging
+  static constexpr int BAR_OFF = STG_OFF + EPW * kStageBytes;
+  static constexpr int SMEM = BAR_OFF + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int THREADS = 128 + EPW * 32;
   // kind::f16 instruction descriptor: D f32, A/B bf16, majors, N>>3, M>>4
   static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((AK ? 0u : 1u) << 15) |
                                     ((BKM ? 0u : 1u) << 16) | (static_cast<uint32_t>(BN >> 3) << 17) |
                                     (static_cast<uint32_t>(BM >> 4) << 24);
 };
+
+// 32 bias values of columns [nb, nb + 32) (0 past N); issued before the TMEM load so
+// the (broadcast) global loads overlap it.
+__device__ __forceinline__ void load_bias32(const float* bias, int nb, int N, float* b) {
+  if (nb + 32 <= N && (reinterpret_cast<uintptr_t>(bias + nb) & 15) == 0) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(bias + nb + i));
+      b[i] = x.x, b[i + 1] = x.y, b[i + 2] = x.z, b[i + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) b[i] = nb + i < N ? __ldg(bias + nb + i) : 0.f;
+  }
+}
+
+__device__ __forceinline__ float max32(const float* x) {  // tree: max is exact in any order
+  float t[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) t[i] = fmaxf(x[i], x[i + 16]);
+#pragma unroll
+  for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+    for (int i = 0; i < w; ++i) t[i] = fmaxf(t[i], t[i + w]);
+  return t[0];
+}
 
 // Generic epilogue on columns [c_lo, c_hi) of one accumulator row.
 __device__ __forceinline__ void epilogue_store(const GemmShape& g, const Epi& e, uint32_t taddr, int row, int n0,
@@ -148,14 +239,16 @@ __device__ __forceinline__ void epilogue_store(const GemmShape& g, const Epi& e,
     const int nb = n0 + c;
     if (vec && nb + 32 <= g.N) {
       const int64_t r64 = row;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] *= e.alpha;
       if (e.bias) {
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
           const float4 b = *reinterpret_cast<const float4*>(e.bias + nb + i);
-          v[i] += b.x, v[i + 1] += b.y, v[i + 2] += b.z, v[i + 3] += b.w;
+          v[i] = __fmaf_rn(v[i], e.alpha, b.x), v[i + 1] = __fmaf_rn(v[i + 1], e.alpha, b.y);
+          v[i + 2] = __fmaf_rn(v[i + 2], e.alpha, b.z), v[i + 3] = __fmaf_rn(v[i + 3], e.alpha, b.w);
         }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(v[i], e.alpha);
       }
       if (e.kind == EPI_TANH) {
 #pragma unroll
@@ -220,66 +313,149 @@ __device__ __forceinline__ void epilogue_store(const GemmShape& g, const Epi& e,
   }
 }
 
+// Generic epilogue through the TMA-store path (Epi::tma != 0): same math as
+// epilogue_store, outputs staged per warp and written as 32 x 32 boxes.
+__device__ __forceinline__ void epilogue_store_tma(const GemmShape& g, const Epi& e, const OutMaps& om, uint32_t taddr,
+                                                   int row, int r0, int n0, int c_lo, int c_hi, uint32_t stg,
+                                                   int lane) {
+  float v[32], b[32];
+  const bool live = row < g.M;
+  const int64_t r64 = row;
+#pragma unroll 1
+  for (int c = c_lo; c < c_hi; c += 32) {
+    const int nb = n0 + c;
+    if (e.bias && nb < g.N) load_bias32(e.bias, nb, g.N, b);  // broadcast loads, overlap the TMEM load
+    tmem_ld32(taddr + c, v);
+    if (nb >= g.N) continue;  // warp-uniform
+    const bool full = nb + 32 <= g.N;
+    if (e.bias) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __fmaf_rn(v[i], e.alpha, b[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(v[i], e.alpha);
+    }
+    if (e.kind == EPI_TANH) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = fast_tanh(v[i]);
+    }
+    if (e.kind == EPI_DTANH && live) {
+      const bf16* ap = static_cast<const bf16*>(e.aux) + r64 * e.ld_aux + nb;
+      if (full) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          const uint4 raw = *reinterpret_cast<const uint4*>(ap + i);
+          const bf16* a8 = reinterpret_cast<const bf16*>(&raw);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float a = __bfloat162float(a8[k]);
+            v[i + k] *= (1.f - a * a);
+          }
+        }
+      } else {
+        for (int i = 0; i < 32; ++i)
+          if (nb + i < g.N) {
+            const float a = __bfloat162float(ap[i]);
+            v[i] *= (1.f - a * a);
+          }
+      }
+    }
+    if (e.resid && live) {
+      const float* rp = e.resid + r64 * e.ldr + nb;
+      if (full) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 x = *reinterpret_cast<const float4*>(rp + i);
+          v[i] += x.x, v[i + 1] += x.y, v[i + 2] += x.z, v[i + 3] += x.w;
+        }
+      } else {
+        for (int i = 0; i < 32; ++i)
+          if (nb + i < g.N) v[i] += rp[i];
+      }
+    }
+    if (e.tma & 1) {
+      stage_acquire(lane);
+      stage_f32(stg, lane, v);
+      stage_release(lane, &om.f32, stg, nb, r0, e.kind == EPI_ACCUM);
+    }
+    if (e.tma & 2) {
+      stage_acquire(lane);
+      stage_b16(stg, lane, v);
+      stage_release(lane, &om.b16, stg, nb, r0, false);
+    }
+  }
+}
+
 // LM-head sampling epilogue (inverse-CDF contract, rule.cuh): per 32-id slice the
 // epilogue stores the fp32 logits (the scan needs the chosen slice's ids) and one
 // 4-float record {m_s, Z_s, m1_s, Z1_s}: the contract's max / sexp2-sum at 1/T and
-// the T=1 log-sum-exp partials for the recorded log-prob. ~13 instructions per id.
-__device__ __forceinline__ void epilogue_sample(const GemmShape& g, const Epi& e, const SampleArgs& sa, uint32_t taddr,
-                                                int row, int n0, int c_lo, int c_hi) {
-  float v[32];
+// the T=1 log-sum-exp partials for the recorded log-prob. Slices without BOS and
+// inside V (all but two per row) take a branch-free path: tree max, then 32
+// independent sexp2 chains feeding the contract's 4 interleaved partial sums.
+__device__ __forceinline__ void epilogue_sample(const GemmShape& g, const Epi& e, const SampleArgs& sa,
+                                                const OutMaps& om, uint32_t taddr, int row, int r0, int n0, int c_lo,
+                                                int c_hi, uint32_t stg, int lane) {
+  float v[32], b[32];
   const bool live = row < g.M;
   const bool t1 = sa.inv_t == 1.f;
 #pragma unroll 1
   for (int c = c_lo; c < c_hi; c += 32) {
-    tmem_ld32(taddr + c, v);
-    if (!live) continue;
     const int nb = n0 + c;
-    if (nb >= g.N) continue;  // ragged last tile: no slice record past V
+    if (nb < g.N) load_bias32(e.bias, nb, g.N, b);
+    tmem_ld32(taddr + c, v);
+    if (nb >= g.N) continue;  // ragged last tile (warp-uniform): no slice record past V
     const bool full = nb + 32 <= g.N;
-    if (full && (reinterpret_cast<uintptr_t>(e.bias + nb) & 15) == 0) {  // bias (fp32 master)
 #pragma unroll
-      for (int i = 0; i < 32; i += 4) {
-        const float4 b = *reinterpret_cast<const float4*>(e.bias + nb + i);
-        v[i] = __fadd_rn(v[i], b.x), v[i + 1] = __fadd_rn(v[i + 1], b.y);
-        v[i + 2] = __fadd_rn(v[i + 2], b.z), v[i + 3] = __fadd_rn(v[i + 3], b.w);
+    for (int i = 0; i < 32; ++i) v[i] = __fadd_rn(v[i], b[i]);
+    stage_acquire(lane);  // fp32 logits (the scan reads the chosen slice; the parity dump)
+    stage_f32(stg, lane, v);
+    stage_release(lane, &om.f32, stg, nb, r0, false);
+    if (!live) continue;
+    float m, m1, Z, Z1;
+    if (full && (sa.bos < nb || sa.bos >= nb + 32)) {
+      float x[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) x[i] = __fmul_rn(v[i], sa.inv_t);
+      m = max32(x);
+      float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int i = 0; i < 32; ++i) a[i & 3] = __fadd_rn(a[i & 3], sexp2(__fmul_rn(__fsub_rn(x[i], m), kLog2e)));
+      Z = __fadd_rn(__fadd_rn(a[0], a[1]), __fadd_rn(a[2], a[3]));
+      if (t1) {
+        m1 = m, Z1 = Z;
+      } else {
+        m1 = max32(v);
+        float b4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 32; ++i) b4[i & 3] += __expf(v[i] - m1);
+        Z1 = (b4[0] + b4[1]) + (b4[2] + b4[3]);
       }
-    } else {
+    } else {  // the slice holding BOS, or the ragged end of V
+      float x[32];
+      m = -FLT_MAX, m1 = -FLT_MAX;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = nb + i < g.N ? __fadd_rn(v[i], e.bias[nb + i]) : 0.f;
-    }
-    float* lrow = sa.logits + static_cast<int64_t>(row) * sa.logits_ld + nb;
-    if (full && (reinterpret_cast<uintptr_t>(lrow) & 15) == 0) {
+      for (int i = 0; i < 32; ++i) {
+        const bool ok = nb + i < g.N && nb + i != sa.bos;
+        x[i] = ok ? __fmul_rn(v[i], sa.inv_t) : -FLT_MAX;
+        m = fmaxf(m, x[i]);
+        m1 = fmaxf(m1, ok ? v[i] : -FLT_MAX);
+      }
+      float a[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(lrow + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-    } else {
-      for (int i = 0; i < 32; ++i)
-        if (nb + i < g.N) lrow[i] = v[i];
-    }
-    const bool clean = full && (sa.bos < nb || sa.bos >= nb + 32);
-    float x[32];
-    float m = -FLT_MAX, m1 = -FLT_MAX;
+      for (int i = 0; i < 32; ++i) {
+        const float ei = x[i] == -FLT_MAX ? 0.f : sexp2(__fmul_rn(__fsub_rn(x[i], m), kLog2e));
+        a[i & 3] = __fadd_rn(a[i & 3], ei);
+      }
+      Z = __fadd_rn(__fadd_rn(a[0], a[1]), __fadd_rn(a[2], a[3]));
+      Z1 = Z;
+      if (!t1) {
+        float b4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const bool ok = clean || (nb + i < g.N && nb + i != sa.bos);
-      x[i] = ok ? __fmul_rn(v[i], sa.inv_t) : -FLT_MAX;
-      m = fmaxf(m, x[i]);
-      m1 = fmaxf(m1, ok ? v[i] : -FLT_MAX);
-    }
-    float a[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const float ei = x[i] == -FLT_MAX ? 0.f : sexp2(__fmul_rn(__fsub_rn(x[i], m), kLog2e));
-      a[i & 3] = __fadd_rn(a[i & 3], ei);
-    }
-    const float Z = __fadd_rn(__fadd_rn(a[0], a[1]), __fadd_rn(a[2], a[3]));
-    float Z1 = Z;
-    if (!t1) {
-      float b4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int i = 0; i < 32; ++i) b4[i & 3] += x[i] == -FLT_MAX ? 0.f : __expf(v[i] - m1);
-      Z1 = (b4[0] + b4[1]) + (b4[2] + b4[3]);
-    } else {
-      m1 = m;
+        for (int i = 0; i < 32; ++i) b4[i & 3] += x[i] == -FLT_MAX ? 0.f : __expf(v[i] - m1);
+        Z1 = (b4[0] + b4[1]) + (b4[2] + b4[3]);
+      } else {
+        m1 = m;
+      }
     }
     float4* pp = reinterpret_cast<float4*>(sa.part + (static_cast<int64_t>(row) * sa.ntiles + (nb / kSlice)) * 4);
     *pp = make_float4(m, Z, m1, Z1);
@@ -289,21 +465,26 @@ __device__ __forceinline__ void epilogue_sample(const GemmShape& g, const Epi& e
 // LM-head backward pass 1: per (row, slice) {max, sum exp} of the non-BOS logits.
 __device__ __forceinline__ void epilogue_lse(const GemmShape& g, const Epi& e, const SampleArgs& sa, uint32_t taddr,
                                              int row, int n0, int c_lo, int c_hi, int slice) {
-  float v[32];
+  float v[32], b[32];
   const bool live = row < g.M;
   float mx = -FLT_MAX, se = 0.f;
 #pragma unroll 1
   for (int c = c_lo; c < c_hi; c += 32) {
-    tmem_ld32(taddr + c, v);
-    if (!live) continue;
     const int nb = n0 + c;
-    float cm = -FLT_MAX;
+    if (nb < g.N) load_bias32(e.bias, nb, g.N, b);
+    tmem_ld32(taddr + c, v);
+    if (!live || nb >= g.N) continue;
+    if (nb + 32 <= g.N && (sa.bos < nb || sa.bos >= nb + 32)) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int n = nb + i;
-      v[i] = (n < g.N && n != sa.bos) ? v[i] + e.bias[n] : -FLT_MAX;
-      cm = fmaxf(cm, v[i]);
+      for (int i = 0; i < 32; ++i) v[i] += b[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int n = nb + i;
+        v[i] = (n < g.N && n != sa.bos) ? v[i] + b[i] : -FLT_MAX;
+      }
     }
+    const float cm = max32(v);
     if (cm > -FLT_MAX) {
       const float nm = fmaxf(mx, cm);
       float a4[4] = {se * __expf(mx - nm), 0.f, 0.f, 0.f};  // 4 chains: the adds overlap
@@ -321,53 +502,41 @@ __device__ __forceinline__ void epilogue_lse(const GemmShape& g, const Epi& e, c
 }
 
 // LM-head backward pass 2: dz = w_r (onehot(y_r) - exp(logit - lse_r)), BOS column 0, bf16.
-__device__ __forceinline__ void epilogue_dz(const GemmShape& g, const Epi& e, const SampleArgs& sa, uint32_t taddr,
-                                            int row, int n0, int c_lo, int c_hi) {
-  float v[32];
+__device__ __forceinline__ void epilogue_dz(const GemmShape& g, const Epi& e, const SampleArgs& sa, const OutMaps& om,
+                                            uint32_t taddr, int row, int r0, int n0, int c_lo, int c_hi, uint32_t stg,
+                                            int lane) {
+  float v[32], b[32];
   const bool live = row < g.M;
   const float lse = live ? sa.lse[row] : 0.f;
   const float w = live ? sa.weight[row] : 0.f;
   const int y = live ? sa.target[row] : -1;
-  const bool vec = ((reinterpret_cast<uintptr_t>(sa.dz) | static_cast<uintptr_t>(sa.ld_dz * 2)) & 15) == 0;
 #pragma unroll 1
   for (int c = c_lo; c < c_hi; c += 32) {
-    tmem_ld32(taddr + c, v);
-    if (!live) continue;
     const int nb = n0 + c;
+    if (nb < g.N) load_bias32(e.bias, nb, g.N, b);
+    tmem_ld32(taddr + c, v);
+    if (nb >= g.N) continue;  // warp-uniform
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       const int n = nb + i;
-      const float l = n < g.N ? v[i] + e.bias[n] : 0.f;
-      v[i] = (n == sa.bos) ? 0.f : w * ((n == y ? 1.f : 0.f) - __expf(l - lse));
+      const float p = __expf(v[i] + b[i] - lse);
+      v[i] = (n == sa.bos) ? 0.f : w * ((n == y ? 1.f : 0.f) - p);
     }
-    bf16* dst = sa.dz + static_cast<int64_t>(row) * sa.ld_dz + nb;
-    if (vec && nb + 32 <= g.N) {
-#pragma unroll
-      for (int i = 0; i < 32; i += 8) {
-        uint4 o;
-        o.x = pack2(v[i], v[i + 1]);
-        o.y = pack2(v[i + 2], v[i + 3]);
-        o.z = pack2(v[i + 4], v[i + 5]);
-        o.w = pack2(v[i + 6], v[i + 7]);
-        *reinterpret_cast<uint4*>(dst + i) = o;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (nb + i < g.N) dst[i] = __float2bfloat16_rn(v[i]);
-    }
+    stage_acquire(lane);
+    stage_b16(stg, lane, v);
+    stage_release(lane, &om.b16, stg, nb, r0, false);
   }
 }
 
 // MODE: 0 generic store epilogue, 1 fused sampling, 2 LSE partials, 3 dz
 template <int BN, int STAGES, bool AK, bool BKM, int EPW, int MODE>
 __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, GemmShape g,
-                   Epi e, SampleArgs sa) {
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                   const __grid_constant__ OutMaps om, GemmShape g, Epi e, SampleArgs sa) {
   using C = Cfg<BN, STAGES, AK, BKM, EPW>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
@@ -468,6 +637,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
     };
     const bool vec = al(e.c32, e.ldc32, 4) && al(e.cT, e.ldcT, 2) && al(e.resid, e.ldr, 4) &&
                      al(e.aux, e.ld_aux, 2) && al(e.bias, 0, 4);
+    const uint32_t stg = smem_u32(smem + C::STG_OFF + ew * kStageBytes);
     int i = 0;
     for (int t = blockIdx.x; t < ntile; t += gridDim.x, ++i) {
       const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
@@ -476,18 +646,21 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
       mbar_wait_sleep(&tfull[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      const int row = m0 + q * 32 + lane;
+      const int r0 = m0 + q * 32, row = r0 + lane;
       if constexpr (MODE == 1)
-        epilogue_sample(g, e, sa, taddr, row, n0, slice * CW, (slice + 1) * CW);
+        epilogue_sample(g, e, sa, om, taddr, row, r0, n0, slice * CW, (slice + 1) * CW, stg, lane);
       else if constexpr (MODE == 2)
         epilogue_lse(g, e, sa, taddr, row, n0, slice * CW, (slice + 1) * CW, (t / tiles_m) * NSL + slice);
       else if constexpr (MODE == 3)
-        epilogue_dz(g, e, sa, taddr, row, n0, slice * CW, (slice + 1) * CW);
+        epilogue_dz(g, e, sa, om, taddr, row, r0, n0, slice * CW, (slice + 1) * CW, stg, lane);
+      else if (e.tma)
+        epilogue_store_tma(g, e, om, taddr, row, r0, n0, slice * CW, (slice + 1) * CW, stg, lane);
       else
         epilogue_store(g, e, taddr, row, n0, slice * CW, (slice + 1) * CW, vec);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&tempty[acc]);
     }
+    stage_drain(lane);  // bulk stores complete before the CTA's shared memory goes away
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -523,6 +696,38 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int6
   return r == CUDA_SUCCESS;
 }
 
+// 32 x 32 output box for the TMA-store epilogue over a row-major [rows x cols] matrix.
+bool make_out_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, bool f32) {
+  auto fn = encode_fn();
+  const int esz = f32 ? 4 : 2;
+  if (!fn || !base || ((reinterpret_cast<uintptr_t>(base) | static_cast<uintptr_t>(ld * esz)) & 15)) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * esz)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Epilogue outputs through bulk tensor stores when both outputs are TMA-legal
+// (the generic EPI kinds only; returns the Epi::tma bits, 0 = direct stores).
+int out_maps_for(const GemmShape& g, const Epi& e, OutMaps* om) {
+  if (getenv("DASHCU_NO_TMA_STORE")) return 0;
+  int bits = 0;
+  if (e.c32) {
+    if (!make_out_map(&om->f32, e.c32, g.M, g.N, e.ldc32, true)) return 0;
+    bits |= 1;
+  }
+  if (e.cT && e.kind != EPI_ACCUM) {
+    if (!make_out_map(&om->b16, e.cT, g.M, g.N, e.ldcT, false)) return 0;
+    bits |= 2;
+  }
+  return bits;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -534,8 +739,8 @@ int num_sms() {
 }
 
 template <int BN, int STAGES, bool AK, bool BKM, int EPW, int MODE>
-void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& g, const Epi& e,
-            const SampleArgs& sa) {
+void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& om, const GemmShape& g,
+            const Epi& e, const SampleArgs& sa) {
   using C = Cfg<BN, STAGES, AK, BKM, EPW>;
   auto k = gemm_tc_kernel<BN, STAGES, AK, BKM, EPW, MODE>;
   static bool attr = false;
@@ -550,18 +755,19 @@ void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const 
   if (ps.keyed())
     snprintf(ps.key, sizeof(ps.key), "mode%d 128x%d M%d N%d K%d %c%c epi%d", MODE, BN, g.M, g.N, g.K,
              AK ? 'k' : 'm', BKM ? 'k' : 'm', e.kind);
-  k<<<grid, C::THREADS, C::SMEM, s>>>(ma, mb, g, e, sa);
+  k<<<grid, C::THREADS, C::SMEM, s>>>(ma, mb, om, g, e, sa);
   DCU_LAUNCHED();
 }
 
 template <int BN, int STAGES>
-void dispatch_majors(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& g, const Epi& e) {
+void dispatch_majors(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& om,
+                     const GemmShape& g, const Epi& e) {
   const SampleArgs none;
   // 8 epilogue warps (two per SM sub-partition, each owning half of the tile's columns)
-  if (g.a_kmajor && g.b_kmajor) launch<BN, STAGES, true, true, 8, 0>(s, ma, mb, g, e, none);
-  else if (g.a_kmajor) launch<BN, STAGES, true, false, 8, 0>(s, ma, mb, g, e, none);
-  else if (g.b_kmajor) launch<BN, STAGES, false, true, 8, 0>(s, ma, mb, g, e, none);
-  else launch<BN, STAGES, false, false, 8, 0>(s, ma, mb, g, e, none);
+  if (g.a_kmajor && g.b_kmajor) launch<BN, STAGES, true, true, 8, 0>(s, ma, mb, om, g, e, none);
+  else if (g.a_kmajor) launch<BN, STAGES, true, false, 8, 0>(s, ma, mb, om, g, e, none);
+  else if (g.b_kmajor) launch<BN, STAGES, false, true, 8, 0>(s, ma, mb, om, g, e, none);
+  else launch<BN, STAGES, false, false, 8, 0>(s, ma, mb, om, g, e, none);
 }
 
 bool legal(const GemmShape& g) {
@@ -635,7 +841,9 @@ struct Cfg2 {
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = BNH * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int STG_OFF = STAGES * STAGE_BYTES;
+  static constexpr int BAR_OFF = STG_OFF + EPW * kStageBytes;
+  static constexpr int SMEM = BAR_OFF + 1024 + 256;
   static constexpr int THREADS = 128 + EPW * 32;
   static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((AK ? 0u : 1u) << 15) |
                                     ((BKM ? 0u : 1u) << 16) | (static_cast<uint32_t>(BN >> 3) << 17) |
@@ -644,12 +852,12 @@ struct Cfg2 {
 
 template <int BN, int STAGES, bool AK, bool BKM, int EPW>
 __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
-    gemm_tc2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, GemmShape g,
-                    Epi e) {
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                    const __grid_constant__ OutMaps om, GemmShape g, Epi e) {
   using C = Cfg2<BN, STAGES, AK, BKM, EPW>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
@@ -755,6 +963,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
     const bool vec = al(e.c32, e.ldc32, 4) && al(e.cT, e.ldcT, 2) && al(e.resid, e.ldr, 4) &&
                      al(e.aux, e.ld_aux, 2) && al(e.bias, 0, 4);
     const uint32_t tempty_leader0 = leader_addr(&tempty[0]), tempty_leader1 = leader_addr(&tempty[1]);
+    const uint32_t stg = smem_u32(smem + C::STG_OFF + ew * kStageBytes);
     int i = 0;
     for (int t = pair; t < ntile; t += npairs, ++i) {
       const int m0 = (t % tiles_m) * 256 + static_cast<int>(rank) * 128, n0 = (t / tiles_m) * BN;
@@ -763,12 +972,17 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
       mbar_wait_sleep(&tfull[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      epilogue_store(g, e, taddr, m0 + q * 32 + lane, n0, slice * CW, (slice + 1) * CW, vec);
+      if (e.tma)
+        epilogue_store_tma(g, e, om, taddr, m0 + q * 32 + lane, m0 + q * 32, n0, slice * CW, (slice + 1) * CW, stg,
+                           lane);
+      else
+        epilogue_store(g, e, taddr, m0 + q * 32 + lane, n0, slice * CW, (slice + 1) * CW, vec);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(acc ? tempty_leader1
                                                                                             : tempty_leader0)
                    : "memory");
     }
+    stage_drain(lane);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync_all();
@@ -778,7 +992,8 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
 }
 
 template <int BN, int STAGES, bool AK, bool BKM>
-void launch2(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& g, const Epi& e) {
+void launch2(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& om, const GemmShape& g,
+             const Epi& e) {
   using C = Cfg2<BN, STAGES, AK, BKM, 8>;
   auto k = gemm_tc2_kernel<BN, STAGES, AK, BKM, 8>;
   static bool attr = false;
@@ -804,7 +1019,7 @@ void launch2(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const
   if (ps.keyed())
     snprintf(ps.key, sizeof(ps.key), "pair 256x%d M%d N%d K%d %c%c epi%d", BN, g.M, g.N, g.K, AK ? 'k' : 'm',
              BKM ? 'k' : 'm', e.kind);
-  DCU_CHECK(cudaLaunchKernelEx(&cfg, k, ma, mb, g, e));
+  DCU_CHECK(cudaLaunchKernelEx(&cfg, k, ma, mb, om, g, e));
   DCU_LAUNCHED();
 }
 
@@ -827,10 +1042,14 @@ bool gemm_tc_pair(cudaStream_t s, const GemmShape& g, const Epi& e) {
   bool ok = g.a_kmajor ? make_map(&ma, g.A, g.M, g.K, g.lda, BK, 128) : make_map(&ma, g.A, g.K, g.M, g.lda, 64, BK);
   ok = ok && (g.b_kmajor ? make_map(&mb, g.B, g.N, g.K, g.ldb, BK, BN / 2) : make_map(&mb, g.B, g.K, g.N, g.ldb, 64, BK));
   if (!ok) return false;
-  if (g.a_kmajor && g.b_kmajor) launch2<BN, 6, true, true>(s, ma, mb, g, e);
-  else if (g.a_kmajor) launch2<BN, 6, true, false>(s, ma, mb, g, e);
-  else if (g.b_kmajor) launch2<BN, 6, false, true>(s, ma, mb, g, e);
-  else launch2<BN, 6, false, false>(s, ma, mb, g, e);
+  OutMaps om;
+  memset(&om, 0, sizeof(om));
+  Epi et = e;
+  et.tma = out_maps_for(g, e, &om);
+  if (g.a_kmajor && g.b_kmajor) launch2<BN, 6, true, true>(s, ma, mb, om, g, et);
+  else if (g.a_kmajor) launch2<BN, 6, true, false>(s, ma, mb, om, g, et);
+  else if (g.b_kmajor) launch2<BN, 6, false, true>(s, ma, mb, om, g, et);
+  else launch2<BN, 6, false, false>(s, ma, mb, om, g, et);
   return true;
 }
 
@@ -853,8 +1072,12 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e) {
   bool ok = g.a_kmajor ? make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) : make_map(&ma, g.A, g.K, g.M, g.lda, 64, BK);
   ok = ok && (g.b_kmajor ? make_map(&mb, g.B, g.N, g.K, g.ldb, BK, BN) : make_map(&mb, g.B, g.K, g.N, g.ldb, 64, BK));
   if (!ok) return false;
-  if (wide) dispatch_majors<256, 4>(s, ma, mb, g, e);   // 4 x 48 KB stages
-  else dispatch_majors<128, 6>(s, ma, mb, g, e);        // 6 x 32 KB stages
+  OutMaps om;
+  memset(&om, 0, sizeof(om));
+  Epi et = e;
+  et.tma = out_maps_for(g, e, &om);
+  if (wide) dispatch_majors<256, 4>(s, ma, mb, om, g, et);   // 4 x 48 KB stages
+  else dispatch_majors<128, 6>(s, ma, mb, om, g, et);        // 6 x 32 KB stages
   return true;
 }
 
@@ -864,11 +1087,14 @@ int gemm_tc_sample(cudaStream_t s, const GemmShape& g, const float* bias, const 
   if (!legal(g) || !g.a_kmajor || !g.b_kmajor) return 0;
   CUtensorMap ma, mb;
   if (!make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) || !make_map(&mb, g.B, g.N, g.K, g.ldb, BK, kSampleBN)) return 0;
+  OutMaps om;
+  memset(&om, 0, sizeof(om));
+  if (!make_out_map(&om.f32, sa.logits, g.M, g.N, sa.logits_ld, true)) return 0;
   Epi e;
   e.bias = bias;
   SampleArgs a = sa;
   a.ntiles = gemm_tc_sample_tiles(g.N);
-  launch<kSampleBN, 4, true, true, kSampleEPW, 1>(s, ma, mb, g, e, a);
+  launch<kSampleBN, 4, true, true, kSampleEPW, 1>(s, ma, mb, om, g, e, a);
   return a.ntiles;
 }
 
@@ -878,11 +1104,13 @@ int gemm_tc_lse(cudaStream_t s, const GemmShape& g, const float* bias, const Sam
   if (!legal(g) || !g.a_kmajor || !g.b_kmajor) return 0;
   CUtensorMap ma, mb;
   if (!make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) || !make_map(&mb, g.B, g.N, g.K, g.ldb, BK, 256)) return 0;
+  OutMaps om;
+  memset(&om, 0, sizeof(om));
   Epi e;
   e.bias = bias;
   SampleArgs a = sa;
   a.ntiles = gemm_tc_lse_tiles(g.N);
-  launch<256, 4, true, true, 8, 2>(s, ma, mb, g, e, a);
+  launch<256, 4, true, true, 8, 2>(s, ma, mb, om, g, e, a);
   return a.ntiles;
 }
 
@@ -890,9 +1118,12 @@ bool gemm_tc_dz(cudaStream_t s, const GemmShape& g, const float* bias, const Sam
   if (!legal(g) || !g.a_kmajor || !g.b_kmajor) return false;
   CUtensorMap ma, mb;
   if (!make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) || !make_map(&mb, g.B, g.N, g.K, g.ldb, BK, 256)) return false;
+  OutMaps om;
+  memset(&om, 0, sizeof(om));
+  if (!make_out_map(&om.b16, sa.dz, g.M, g.N, sa.ld_dz, false)) return false;
   Epi e;
   e.bias = bias;
-  launch<256, 4, true, true, 8, 3>(s, ma, mb, g, e, sa);
+  launch<256, 4, true, true, 8, 3>(s, ma, mb, om, g, e, sa);
   return true;
 }
 

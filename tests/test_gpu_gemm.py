@@ -72,3 +72,21 @@ def test_tc_matches_simt(ctx):
     a = ctx.selftest_gemm(A, True, B, False, M, N, K)
     b = ctx.selftest_gemm(A, True, B, False, M, N, K, force_simt=True)
     assert np.abs(a - b).max() <= 1e-4 * np.abs(b).max()
+
+
+@pytest.mark.parametrize("shape", [(200, 136, 72), (77, 300, 1000), (3000, 2048, 128)])
+@pytest.mark.parametrize("epi", [0, 1, 3])
+def test_tma_store_epilogue_matches_direct_stores(ctx, monkeypatch, shape, epi):
+    """The bulk-tensor-store epilogue (and its fp32 reduce-add for EPI_ACCUM) writes
+    exactly what the per-thread 16-byte stores write, ragged edges included."""
+    M, N, K = shape
+    rng = np.random.default_rng(5)
+    A = bf16_bits(rng.standard_normal((M, K)).astype(np.float32) * 0.1)
+    B = bf16_bits(rng.standard_normal((N, K)).astype(np.float32) * 0.1)
+    bias = rng.standard_normal(N).astype(np.float32)
+    c0 = rng.standard_normal((M, N)).astype(np.float32)
+    kw = dict(bias=bias if epi != 3 else None, epi=epi, C_init=c0 if epi == 3 else None)
+    got = ctx.selftest_gemm(A, True, B, True, M, N, K, **kw)
+    monkeypatch.setenv("DASHCU_NO_TMA_STORE", "1")
+    ref = ctx.selftest_gemm(A, True, B, True, M, N, K, **kw)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
