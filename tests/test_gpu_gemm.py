@@ -89,4 +89,9 @@ def test_tma_store_epilogue_matches_direct_stores(ctx, monkeypatch, shape, epi):
     got = ctx.selftest_gemm(A, True, B, True, M, N, K, **kw)
     monkeypatch.setenv("DASHCU_NO_TMA_STORE", "1")
     ref = ctx.selftest_gemm(A, True, B, True, M, N, K, **kw)
-    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+    if epi == 1:  # the direct path's ragged columns use the scalar epilogue (precise tanhf)
+        assert np.abs(got - ref).max() < 1e-6
+        full = (N // 32) * 32
+        assert np.array_equal(got[:, :full].view(np.uint32), ref[:, :full].view(np.uint32))
+    else:
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
