@@ -211,7 +211,7 @@ DASHCU_API int64_t dashcu_profile_keys(char* buf, int64_t cap);
  * C[M x N] (fp32, ldc = N) = A(m,k) . B(n,k) on bf16 operands given as raw
  * bit patterns, through the production GEMM dispatcher (tcgen05 when the
  * operands are TMA-legal) or, with force_simt, the CUDA-core kernel.
- * epi: 0 store, 1 tanh(acc + bias), 3 C += acc (C is read first). */
+ * epi: 0 store, 1 tanh(acc + bias), 3 C += acc, 4 C = acc + bias + C (residual). */
 DASHCU_API int dashcu_selftest_gemm(dashcu_ctx* ctx, int M, int N, int K, const uint16_t* A, int64_t lda,
                                     int a_kmajor, const uint16_t* B, int64_t ldb, int b_kmajor, const float* bias,
                                     int epi, int force_simt, float* C);

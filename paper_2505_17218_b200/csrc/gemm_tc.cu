@@ -185,6 +185,8 @@ __device__ __forceinline__ void stage_drain(int lane) {
 struct OutMaps {
   CUtensorMap f32;  // 32 x 32 fp32 box, SWIZZLE_128B: c32 / logits
   CUtensorMap b16;  // 32 x 32 bf16 box, SWIZZLE_64B: cT / dz
+  CUtensorMap rs;   // input: fp32 residual (Epi::tma bit 2)
+  CUtensorMap ax;   // input: bf16 tanh activations of EPI_DTANH (bit 3)
 };
 
 template <int BN, int STAGES, bool AK, bool BKM, int EPW>
@@ -313,20 +315,59 @@ __device__ __forceinline__ void epilogue_store(const GemmShape& g, const Epi& e,
   }
 }
 
-// Generic epilogue through the TMA-store path (Epi::tma != 0): same math as
-// epilogue_store, outputs staged per warp and written as 32 x 32 boxes.
+// Row `lane` of a staged 32 x 32 box (the layouts of stage_f32 / stage_b16).
+__device__ __forceinline__ void unstage_f32(uint32_t buf, int lane, float* x) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(x[4 * j]), "=f"(x[4 * j + 1]), "=f"(x[4 * j + 2]), "=f"(x[4 * j + 3])
+                 : "r"(buf + lane * 128 + ((j ^ (lane & 7)) << 4))
+                 : "memory");
+}
+__device__ __forceinline__ void unstage_b16(uint32_t buf, int lane, float* x) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t r[4];
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(buf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4))
+                 : "memory");
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      x[8 * j + 2 * k] = __uint_as_float(r[k] << 16);
+      x[8 * j + 2 * k + 1] = __uint_as_float(r[k] & 0xffff0000u);
+    }
+  }
+}
+
+// Generic epilogue through the TMA path (Epi::tma != 0): same math as epilogue_store.
+// The fp32 residual (bit 2) or the bf16 tanh activations of EPI_DTANH (bit 3) arrive
+// as a 32 x 32 box in the warp's staging buffer (TMA load, zero-filled past M / N,
+// issued before the TMEM load); outputs leave through the same buffer as bulk stores.
 __device__ __forceinline__ void epilogue_store_tma(const GemmShape& g, const Epi& e, const OutMaps& om, uint32_t taddr,
                                                    int row, int r0, int n0, int c_lo, int c_hi, uint32_t stg,
-                                                   int lane) {
+                                                   int lane, uint64_t* ebar, uint32_t& ephase) {
   float v[32], b[32];
   const bool live = row < g.M;
   const int64_t r64 = row;
+  const bool tres = (e.tma & 4) != 0, taux = (e.tma & 8) != 0;
+  uint8_t* stg_ptr = reinterpret_cast<uint8_t*>(__cvta_shared_to_generic(stg));
 #pragma unroll 1
   for (int c = c_lo; c < c_hi; c += 32) {
     const int nb = n0 + c;
-    if (e.bias && nb < g.N) load_bias32(e.bias, nb, g.N, b);  // broadcast loads, overlap the TMEM load
+    if (nb >= g.N) {  // warp-uniform
+      tmem_ld32(taddr + c, v);
+      continue;
+    }
+    if (tres || taux) {
+      stage_acquire(lane);  // the previous bulk store has finished reading the buffer
+      if (lane == 0) {
+        mbar_expect_tx(ebar, tres ? 4096u : 2048u);
+        tma_load_2d(stg_ptr, tres ? &om.rs : &om.ax, ebar, nb, r0);
+      }
+    }
+    if (e.bias) load_bias32(e.bias, nb, g.N, b);  // broadcast loads, overlap the TMEM load
     tmem_ld32(taddr + c, v);
-    if (nb >= g.N) continue;  // warp-uniform
     const bool full = nb + 32 <= g.N;
     if (e.bias) {
 #pragma unroll
@@ -339,40 +380,36 @@ __device__ __forceinline__ void epilogue_store_tma(const GemmShape& g, const Epi
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = fast_tanh(v[i]);
     }
-    if (e.kind == EPI_DTANH && live) {
-      const bf16* ap = static_cast<const bf16*>(e.aux) + r64 * e.ld_aux + nb;
-      if (full) {
+    if (tres || taux) {
+      mbar_wait(ebar, ephase);
+      ephase ^= 1u;
+    }
+    if (e.kind == EPI_DTANH) {
+      if (taux) {
+        unstage_b16(stg, lane, b);
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          const uint4 raw = *reinterpret_cast<const uint4*>(ap + i);
-          const bf16* a8 = reinterpret_cast<const bf16*>(&raw);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const float a = __bfloat162float(a8[k]);
-            v[i + k] *= (1.f - a * a);
-          }
-        }
-      } else {
+        for (int i = 0; i < 32; ++i) v[i] *= (1.f - b[i] * b[i]);
+      } else if (live) {
+        const bf16* ap = static_cast<const bf16*>(e.aux) + r64 * e.ld_aux + nb;
         for (int i = 0; i < 32; ++i)
-          if (nb + i < g.N) {
+          if (full || nb + i < g.N) {
             const float a = __bfloat162float(ap[i]);
             v[i] *= (1.f - a * a);
           }
       }
     }
-    if (e.resid && live) {
-      const float* rp = e.resid + r64 * e.ldr + nb;
-      if (full) {
+    if (e.resid) {
+      if (tres) {
+        unstage_f32(stg, lane, b);
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 x = *reinterpret_cast<const float4*>(rp + i);
-          v[i] += x.x, v[i + 1] += x.y, v[i + 2] += x.z, v[i + 3] += x.w;
-        }
-      } else {
+        for (int i = 0; i < 32; ++i) v[i] += b[i];
+      } else if (live) {
+        const float* rp = e.resid + r64 * e.ldr + nb;
         for (int i = 0; i < 32; ++i)
-          if (nb + i < g.N) v[i] += rp[i];
+          if (full || nb + i < g.N) v[i] += rp[i];
       }
     }
+    if (tres || taux) __syncwarp();  // every lane has read the box before it is overwritten
     if (e.tma & 1) {
       stage_acquire(lane);
       stage_f32(stg, lane, v);
@@ -540,7 +577,8 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ebar = tempty + 2;       // [EPW] epilogue TMA-load barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + EPW);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkb = (g.K + BK - 1) / BK;
@@ -556,6 +594,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], EPW * 32);
     }
+    for (int w = 0; w < EPW; ++w) mbar_init(&ebar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
@@ -638,6 +677,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
     const bool vec = al(e.c32, e.ldc32, 4) && al(e.cT, e.ldcT, 2) && al(e.resid, e.ldr, 4) &&
                      al(e.aux, e.ld_aux, 2) && al(e.bias, 0, 4);
     const uint32_t stg = smem_u32(smem + C::STG_OFF + ew * kStageBytes);
+    uint32_t ephase = 0;
     int i = 0;
     for (int t = blockIdx.x; t < ntile; t += gridDim.x, ++i) {
       const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
@@ -654,7 +694,8 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
       else if constexpr (MODE == 3)
         epilogue_dz(g, e, sa, om, taddr, row, r0, n0, slice * CW, (slice + 1) * CW, stg, lane);
       else if (e.tma)
-        epilogue_store_tma(g, e, om, taddr, row, r0, n0, slice * CW, (slice + 1) * CW, stg, lane);
+        epilogue_store_tma(g, e, om, taddr, row, r0, n0, slice * CW, (slice + 1) * CW, stg, lane, &ebar[ew],
+                           ephase);
       else
         epilogue_store(g, e, taddr, row, n0, slice * CW, (slice + 1) * CW, vec);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -725,6 +766,10 @@ int out_maps_for(const GemmShape& g, const Epi& e, OutMaps* om) {
     if (!make_out_map(&om->b16, e.cT, g.M, g.N, e.ldcT, false)) return 0;
     bits |= 2;
   }
+  if (!bits) return 0;
+  if (e.resid && make_out_map(&om->rs, e.resid, g.M, g.N, e.ldr, true)) bits |= 4;
+  else if (!e.resid && e.kind == EPI_DTANH && e.aux && make_out_map(&om->ax, e.aux, g.M, g.N, e.ld_aux, false))
+    bits |= 8;
   return bits;
 }
 
@@ -861,7 +906,8 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ebar = tempty + 2;       // [EPW] epilogue TMA-load barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + EPW);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -880,6 +926,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2 * EPW * 32);
     }
+    for (int w = 0; w < EPW; ++w) mbar_init(&ebar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
@@ -964,6 +1011,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
                      al(e.aux, e.ld_aux, 2) && al(e.bias, 0, 4);
     const uint32_t tempty_leader0 = leader_addr(&tempty[0]), tempty_leader1 = leader_addr(&tempty[1]);
     const uint32_t stg = smem_u32(smem + C::STG_OFF + ew * kStageBytes);
+    uint32_t ephase = 0;
     int i = 0;
     for (int t = pair; t < ntile; t += npairs, ++i) {
       const int m0 = (t % tiles_m) * 256 + static_cast<int>(rank) * 128, n0 = (t / tiles_m) * BN;
@@ -974,7 +1022,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
       const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       if (e.tma)
         epilogue_store_tma(g, e, om, taddr, m0 + q * 32 + lane, m0 + q * 32, n0, slice * CW, (slice + 1) * CW, stg,
-                           lane);
+                           lane, &ebar[ew], ephase);
       else
         epilogue_store(g, e, taddr, m0 + q * 32 + lane, n0, slice * CW, (slice + 1) * CW, vec);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

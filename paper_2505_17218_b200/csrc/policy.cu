@@ -1394,9 +1394,13 @@ int dashcu_selftest_gemm(dashcu_ctx* c, int M, int N, int K, const uint16_t* A, 
   h2d(s, dC, Cout, static_cast<size_t>(M) * N);
   GemmShape g{M, N, K, dA, lda, a_kmajor != 0, dB, ldb, b_kmajor != 0};
   Epi e;
-  e.kind = epi;
+  e.kind = epi == 4 ? EPI_STORE : epi;  // 4: store with the residual C_init added in place
   e.c32 = dC;
   e.ldc32 = N;
+  if (epi == 4) {
+    e.resid = dC;
+    e.ldr = N;
+  }
   e.bias = bias ? dbias : nullptr;
   if (force_simt) gemm_simt<bf16>(s, g, e);
   else gemm(s, 1, g, e);

@@ -75,7 +75,7 @@ def test_tc_matches_simt(ctx):
 
 
 @pytest.mark.parametrize("shape", [(200, 136, 72), (77, 300, 1000), (3000, 2048, 128)])
-@pytest.mark.parametrize("epi", [0, 1, 3])
+@pytest.mark.parametrize("epi", [0, 1, 3, 4])
 def test_tma_store_epilogue_matches_direct_stores(ctx, monkeypatch, shape, epi):
     """The bulk-tensor-store epilogue (and its fp32 reduce-add for EPI_ACCUM) writes
     exactly what the per-thread 16-byte stores write, ragged edges included."""
@@ -85,7 +85,7 @@ def test_tma_store_epilogue_matches_direct_stores(ctx, monkeypatch, shape, epi):
     B = bf16_bits(rng.standard_normal((N, K)).astype(np.float32) * 0.1)
     bias = rng.standard_normal(N).astype(np.float32)
     c0 = rng.standard_normal((M, N)).astype(np.float32)
-    kw = dict(bias=bias if epi != 3 else None, epi=epi, C_init=c0 if epi == 3 else None)
+    kw = dict(bias=bias if epi != 3 else None, epi=epi, C_init=c0 if epi in (3, 4) else None)
     got = ctx.selftest_gemm(A, True, B, True, M, N, K, **kw)
     monkeypatch.setenv("DASHCU_NO_TMA_STORE", "1")
     ref = ctx.selftest_gemm(A, True, B, True, M, N, K, **kw)
