@@ -25,10 +25,13 @@ void embed_decode(cudaStream_t s, const T* tok_emb, const T* pos_emb, const int3
                   const int32_t* prompt_len, int step, int rows, int d, float* x32, T* xT);
 void embed_bwd(cudaStream_t s, const float* dx, const int32_t* tok, const int32_t* pos, int rows, int d,
                float* g_tok, float* g_pos);
-// out[n] += sum_m X[m][n]  (bias gradients: db_out, db1, db2)
+// out[n] += sum_m X[m][n]  (bias gradients: db_out, db1, db2); deterministic two-pass,
+// tmp holds colsum_tmp_floats<T>(M, N) floats of row-segment partials
 template <class T>
-void colsum_acc(cudaStream_t s, const T* X, int64_t ld, int M, int N, float* out);
-void colsum_acc_f32(cudaStream_t s, const float* X, int64_t ld, int M, int N, float* out);
+size_t colsum_tmp_floats(int M, int N);
+template <class T>
+void colsum_acc(cudaStream_t s, const T* X, int64_t ld, int M, int N, float* out, float* tmp);
+void colsum_acc_f32(cudaStream_t s, const float* X, int64_t ld, int M, int N, float* out, float* tmp);
 
 // ---- attention (policy.cpp:105-129 forward, :292-322 backward) -------------------
 // Packed variable-length causal self-attention over qkv rows [T x (qd + 2 kvd)].

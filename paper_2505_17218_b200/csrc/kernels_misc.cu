@@ -109,22 +109,45 @@ __global__ void embed_bwd_k(const float* dx, const int32_t* tok, const int32_t* 
   }
 }
 
-template <class T>
-__global__ void colsum_k(const T* X, int64_t ld, int M, int N, float* out) {
-  __shared__ float red[8][33];
-  const int n = blockIdx.x * 32 + threadIdx.x;
-  const int r0 = blockIdx.y * 512;
-  float s = 0.f;
-  if (n < N)
-    for (int r = r0 + threadIdx.y; r < min(M, r0 + 512); r += 8) s += tof<T>(X[static_cast<int64_t>(r) * ld + n]);
-  red[threadIdx.y][threadIdx.x] = s;
-  __syncthreads();
-  if (threadIdx.y == 0 && n < N) {
-    float t = 0.f;
+// Column sums (bias gradients, policy.cpp:250-262 db = sum_rows dY), deterministic and
+// coalesced: pass 1 — thread = VEC consecutive columns (one 16-byte load per row) over
+// one row segment, partial sums to tmp[segment][N]; pass 2 — out[n] += the segments
+// in order. No atomics, so the result does not depend on scheduling.
+template <class T, int VEC>
+__global__ void colsum_part_k(const T* __restrict__ X, int64_t ld, int M, int N, int seg_rows, bool vec,
+                              float* __restrict__ tmp) {
+  const int n0 = (blockIdx.x * blockDim.x + threadIdx.x) * VEC;
+  if (n0 >= N) return;
+  const int r_begin = blockIdx.y * seg_rows, r_end = min(M, r_begin + seg_rows);
+  float acc[VEC];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) t += red[k][threadIdx.x];
-    atomicAdd(&out[n], t);
+  for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+  if (vec && n0 + VEC <= N) {
+#pragma unroll 4
+    for (int r = r_begin; r < r_end; ++r) {
+      const uint4 raw = __ldg(reinterpret_cast<const uint4*>(X + static_cast<int64_t>(r) * ld + n0));
+      const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) acc[i] += tof<T>(e[i]);
+    }
+  } else {
+    for (int r = r_begin; r < r_end; ++r)
+#pragma unroll
+      for (int i = 0; i < VEC; ++i)
+        if (n0 + i < N) acc[i] += tof<T>(X[static_cast<int64_t>(r) * ld + n0 + i]);
   }
+  float* t = tmp + static_cast<int64_t>(blockIdx.y) * N + n0;
+#pragma unroll
+  for (int i = 0; i < VEC; ++i)
+    if (n0 + i < N) t[i] = acc[i];
+}
+
+__global__ void colsum_fin_k(const float* __restrict__ tmp, int nseg, int N, float* __restrict__ out) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  float s = 0.f;
+  for (int y = 0; y < nseg; ++y) s += tmp[static_cast<int64_t>(y) * N + n];
+  out[n] += s;
 }
 
 // ----------------------------------------------------------- sampling / loss rows
@@ -586,14 +609,41 @@ void embed_bwd(cudaStream_t s, const float* dx, const int32_t* tok, const int32_
   embed_bwd_k<<<grid1d(static_cast<int64_t>(rows) * d), 256, 0, s>>>(dx, tok, pos, rows, d, gt, gp);
   DCU_LAUNCHED();
 }
+namespace {
+// nseg <= want, and want is non-decreasing in M (so a buffer sized for M covers any M' <= M)
 template <class T>
-void colsum_acc(cudaStream_t s, const T* X, int64_t ld, int M, int N, float* out) {
+void colsum_geom(int M, int N, int* gx, int* nseg, int* seg_rows, int* want_out = nullptr) {
+  constexpr int VEC = 16 / sizeof(T);
+  *gx = cdiv(cdiv(N, VEC), 256);
+  int want = std::max(1, (kNumSMs * 8) / *gx);  // ~8 blocks per SM
+  want = std::min(want, std::max(1, M / 16));   // at least 16 rows per segment
+  *seg_rows = cdiv(M, want);
+  *nseg = cdiv(M, *seg_rows);
+  if (want_out) *want_out = want;
+}
+}  // namespace
+
+template <class T>
+size_t colsum_tmp_floats(int M, int N) {
+  int gx, nseg, seg_rows, want;
+  colsum_geom<T>(M, N, &gx, &nseg, &seg_rows, &want);
+  return static_cast<size_t>(want) * N;
+}
+
+template <class T>
+void colsum_acc(cudaStream_t s, const T* X, int64_t ld, int M, int N, float* out, float* tmp) {
   if (M <= 0 || N <= 0) return;
-  colsum_k<T><<<dim3(cdiv(N, 32), cdiv(M, 512)), dim3(32, 8), 0, s>>>(X, ld, M, N, out);
+  constexpr int VEC = 16 / sizeof(T);
+  int gx, nseg, seg_rows;
+  colsum_geom<T>(M, N, &gx, &nseg, &seg_rows);
+  const bool vec = ((reinterpret_cast<uintptr_t>(X) | static_cast<uintptr_t>(ld * sizeof(T))) & 15) == 0;
+  colsum_part_k<T, VEC><<<dim3(gx, nseg), 256, 0, s>>>(X, ld, M, N, seg_rows, vec, tmp);
+  DCU_LAUNCHED();
+  colsum_fin_k<<<cdiv(N, 256), 256, 0, s>>>(tmp, nseg, N, out);
   DCU_LAUNCHED();
 }
-void colsum_acc_f32(cudaStream_t s, const float* X, int64_t ld, int M, int N, float* out) {
-  colsum_acc<float>(s, X, ld, M, N, out);
+void colsum_acc_f32(cudaStream_t s, const float* X, int64_t ld, int M, int N, float* out, float* tmp) {
+  colsum_acc<float>(s, X, ld, M, N, out, tmp);
 }
 
 void sample_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, int eos, float inv_t,
@@ -678,7 +728,8 @@ void advantage_filter(cudaStream_t s, const double* r, int n, int G, int kind, i
   template void embed_fwd<T>(cudaStream_t, const T*, const T*, const int32_t*, const int32_t*, int, int, float*, T*); \
   template void embed_decode<T>(cudaStream_t, const T*, const T*, const int32_t*, const int32_t*, int, int, int,     \
                                 float*, T*);                                                                      \
-  template void colsum_acc<T>(cudaStream_t, const T*, int64_t, int, int, float*);                                \
+  template void colsum_acc<T>(cudaStream_t, const T*, int64_t, int, int, float*, float*);                        \
+  template size_t colsum_tmp_floats<T>(int, int);                                                                 \
   template void lm_rows<T>(cudaStream_t, const float*, int, int, int, const int32_t*, const float*, float*, T*);  \
   template void kv_store_prompt<T>(cudaStream_t, const T*, const int32_t*, int, int, int, int, int, int, T*, T*); \
   template void kv_append<T>(cudaStream_t, const T*, int, int, int, int, int, int, int, T*, T*);                  \

@@ -419,7 +419,8 @@ struct Engine {
       ew.c32 = G32(L.wout);
       ew.ldc32 = g.d;
       mm(g.V, g.d, rc, dz, V, false, ycT, g.d, false, ew);  // dW_out += dz^T y
-      colsum_acc<T>(st, dz, V, rc, g.V, G32(L.bout));         // db_out += sum dz
+      colsum_acc<T>(st, dz, V, rc, g.V, G32(L.bout),           // db_out += sum dz
+                    P.ws.get<float>("cs_bout", colsum_tmp_floats<T>(RC, g.V)));
       mm(rc, g.d, g.V, dz, V, true, W(L.wout), g.d, false, store(dyc, g.d, nullptr, 0));  // dy = dz W_out
       scatter_rows_f32(st, dyc, rc, g.d, rows + r0, dy32);
     }
@@ -455,14 +456,14 @@ struct Engine {
       acc.c32 = G32(b + L.w2);
       acc.ldc32 = g.H;
       mm(g.d, g.H, Tn, dyT, g.d, false, u, g.H, false, acc);
-      colsum_acc_f32(st, dy32, g.d, Tn, g.d, G32(b + L.b2));
+      colsum_acc_f32(st, dy32, g.d, Tn, g.d, G32(b + L.b2), ws.get<float>("cs_b2", colsum_tmp_floats<float>(Tn, g.d)));
       Epi edt = store(nullptr, 0, duT, g.H);
       edt.kind = EPI_DTANH;
       edt.aux = u;
       edt.ld_aux = g.H;
       mm(Tn, g.H, g.d, dyT, g.d, true, W(b + L.w2), g.H, false, edt);
       // u = tanh(W1 h + b1)
-      colsum_acc<T>(st, duT, g.H, Tn, g.H, G32(b + L.b1));
+      colsum_acc<T>(st, duT, g.H, Tn, g.H, G32(b + L.b1), ws.get<float>("cs_b1", colsum_tmp_floats<T>(Tn, g.H)));
       acc.c32 = G32(b + L.w1);
       acc.ldc32 = g.d;
       mm(g.H, g.d, Tn, duT, g.H, false, hT, g.d, false, acc);
