@@ -217,7 +217,7 @@ DASHCU_API int dashcu_selftest_gemm(dashcu_ctx* ctx, int M, int N, int K, const 
                                     int epi, int force_simt, float* C);
 /* Timing harness: `iters` launches of the production GEMM on device-resident random
  * bf16 operands, bf16 output (epi 0) or fp32 accumulate (epi 3); mean ms per launch
- * from CUDA events on the context stream. */
+ * from CUDA events on the context stream; epi 4 adds an fp32 residual input and fp32 output. */
 DASHCU_API int dashcu_selftest_gemm_timed(dashcu_ctx* ctx, int M, int N, int K, int a_kmajor, int b_kmajor, int epi,
                                           int iters, double* ms);
 /* Whole-library count of kernel launches (all policies, all contexts). */

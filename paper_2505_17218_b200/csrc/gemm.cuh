@@ -34,6 +34,8 @@ struct Epi {
   void* cT = nullptr;            // T output (operand copy for the next GEMM)
   int64_t ldcT = 0;
   int tma = 0;                   // set by the tcgen05 launcher: bit 0 c32, bit 1 cT via bulk tensor stores
+  int splits = 1;                // set by the tcgen05 launcher: split-K slices (EPI_ACCUM only)
+  uint32_t* split_flags = nullptr;
 };
 
 struct GemmShape {

@@ -181,6 +181,29 @@ __device__ __forceinline__ void stage_drain(int lane) {
   __syncwarp();
 }
 
+// Split-K ordering: the epilogue warp owning (tile, sub-block) for K slice s waits until
+// slices 0..s-1 have reduced into C (flag == s), so the fp32 sums happen in a fixed
+// order (deterministic). Items are dealt round-robin to co-resident persistent CTAs and
+// only ever wait on lower-numbered items, so the chain cannot deadlock.
+__device__ __forceinline__ void split_wait(const uint32_t* flag, uint32_t s, int lane) {
+  if (lane == 0) {
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    } while (v < s);
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // later bulk reduces are ordered after
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ void split_signal(uint32_t* flag, int lane) {
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // this slice's reduces performed
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(flag) : "memory");
+  }
+}
+
 // Output maps of the TMA-store epilogue (Epi::tma bits 0 / 1).
 struct OutMaps {
   CUtensorMap f32;  // 32 x 32 fp32 box, SWIZZLE_128B: c32 / logits
@@ -584,6 +607,10 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
   const int nkb = (g.K + BK - 1) / BK;
   const int tiles_m = (g.M + BM - 1) / BM, tiles_n = (g.N + BN - 1) / BN;
   const int ntile = tiles_m * tiles_n;
+  // split-K (EPI_ACCUM only): work item w = (tile w / S, K slice w % S), slices of kps k-blocks
+  const int S = MODE == 0 ? e.splits : 1;
+  const int kps = (nkb + S - 1) / S;
+  const int nitem = ntile * S;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -612,9 +639,11 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       int kb_all = 0;
-      for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+      for (int w = blockIdx.x; w < nitem; w += gridDim.x) {
+        const int t = w / S, sp = w % S;
         const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
-        for (int kb = 0; kb < nkb; ++kb, ++kb_all) {
+        const int kb_lo = sp * kps, kb_hi = min(nkb, kb_lo + kps);
+        for (int kb = kb_lo; kb < kb_hi; ++kb, ++kb_all) {
           const int s = kb_all % STAGES;
           const uint32_t ph = (kb_all / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
@@ -640,13 +669,14 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       int kb_all = 0, i = 0;
-      for (int t = blockIdx.x; t < ntile; t += gridDim.x, ++i) {
+      for (int w = blockIdx.x; w < nitem; w += gridDim.x, ++i) {
+        const int kb_lo = (w % S) * kps, kb_hi = min(nkb, kb_lo + kps);
         const int acc = i & 1;
         const uint32_t aph = (i >> 1) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < nkb; ++kb, ++kb_all) {
+        for (int kb = kb_lo; kb < kb_hi; ++kb, ++kb_all) {
           const int s = kb_all % STAGES;
           const uint32_t ph = (kb_all / STAGES) & 1;
           mbar_wait(&full[s], ph);
@@ -658,7 +688,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
             // K-major: advance 32 B inside the swizzle row; MN-major: advance 16 k-rows (2 x 1024 B)
             const uint64_t da = AK ? smem_desc(sa_ + k * 32, 16, 1024) : smem_desc(sa_ + k * 2048, 64 * BK * 2, 1024);
             const uint64_t db = BKM ? smem_desc(sb_ + k * 32, 16, 1024) : smem_desc(sb_ + k * 2048, 64 * BK * 2, 1024);
-            umma_bf16(d, da, db, C::IDESC, (kb > 0 || k > 0) ? 1u : 0u);
+            umma_bf16(d, da, db, C::IDESC, (kb > kb_lo || k > 0) ? 1u : 0u);
           }
           umma_commit(&empty[s]);
         }
@@ -679,12 +709,15 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
     const uint32_t stg = smem_u32(smem + C::STG_OFF + ew * kStageBytes);
     uint32_t ephase = 0;
     int i = 0;
-    for (int t = blockIdx.x; t < ntile; t += gridDim.x, ++i) {
+    for (int w = blockIdx.x; w < nitem; w += gridDim.x, ++i) {
+      const int t = w / S, sp = w % S;
       const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
       const int acc = i & 1;
       const uint32_t aph = (i >> 1) & 1;
       mbar_wait_sleep(&tfull[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t* flag = S > 1 ? e.split_flags + t * EPW + ew : nullptr;
+      if (flag && sp > 0) split_wait(flag, sp, lane);  // K slices reduce into C in slice order
       const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       const int r0 = m0 + q * 32, row = r0 + lane;
       if constexpr (MODE == 1)
@@ -700,6 +733,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
         epilogue_store(g, e, taddr, row, n0, slice * CW, (slice + 1) * CW, vec);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&tempty[acc]);
+      if (flag) split_signal(flag, lane);
     }
     stage_drain(lane);  // bulk stores complete before the CTA's shared memory goes away
   }
@@ -773,6 +807,23 @@ int out_maps_for(const GemmShape& g, const Epi& e, OutMaps* om) {
   return bits;
 }
 
+// Per-device split-K flag words (one per tile x epilogue warp), zeroed before each use.
+uint32_t* split_flag_buffer(int n) {
+  static std::mutex mu;
+  static uint32_t* buf[16] = {};
+  static int cap[16] = {};
+  int dev = 0;
+  DCU_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (cap[dev] < n) {
+    if (buf[dev]) DCU_CHECK(cudaFree(buf[dev]));
+    const int c = std::max(n, 1 << 16);
+    DCU_CHECK(cudaMalloc(&buf[dev], sizeof(uint32_t) * c));
+    cap[dev] = c;
+  }
+  return buf[dev];
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -793,13 +844,13 @@ void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const 
     DCU_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
-  const int ntile = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
-  const int grid = ntile < num_sms() ? ntile : num_sms();
+  const int nitem = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) * (MODE == 0 ? e.splits : 1);
+  const int grid = nitem < num_sms() ? nitem : num_sms();  // persistent: all CTAs co-resident
   ProfScope ps(MODE == 1 ? PROF_SAMPLE : MODE >= 2 ? PROF_LM_ROWS : PROF_GEMM_TC, s,
                2.0 * g.M * g.N * static_cast<double>(g.K), 0);
   if (ps.keyed())
-    snprintf(ps.key, sizeof(ps.key), "mode%d 128x%d M%d N%d K%d %c%c epi%d", MODE, BN, g.M, g.N, g.K,
-             AK ? 'k' : 'm', BKM ? 'k' : 'm', e.kind);
+    snprintf(ps.key, sizeof(ps.key), "mode%d 128x%d M%d N%d K%d %c%c epi%d split%d", MODE, BN, g.M, g.N, g.K,
+             AK ? 'k' : 'm', BKM ? 'k' : 'm', e.kind, MODE == 0 ? e.splits : 1);
   k<<<grid, C::THREADS, C::SMEM, s>>>(ma, mb, om, g, e, sa);
   DCU_LAUNCHED();
 }
@@ -1111,7 +1162,25 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e) {
   const double r128 = std::ceil(tm * ((g.N + 127) / 128) / sms);
   const double r256 = std::ceil(tm * ((g.N + 255) / 256) / sms);
   const double rpair = std::ceil(tm2 * ((g.N + 255) / 256) / std::floor(sms / 2));
-  const double c128 = r128 * 0.5 / 0.76, c256 = r256, cpair = rpair / 1.12;
+  double c128 = r128 * 0.5 / 0.76, c256 = r256;
+  const double cpair = rpair / 1.12;
+  // Split-K for accumulating GEMMs with few output tiles (weight gradients over a long
+  // token axis): S K slices per tile fill the machine; each extra slice costs one more
+  // ordered fp32 reduce of the tile (~3%). Slices keep >= 16 k-blocks.
+  int split128 = 1, split256 = 1;
+  const int nkb = (g.K + BK - 1) / BK;
+  if (e.kind == EPI_ACCUM && e.c32 && !getenv("DASHCU_NO_SPLITK")) {
+    auto best = [&](int tiles, double unit, double* cost) {
+      int sb = 1;
+      for (int S = 2; S <= 8 && nkb / S >= 16; ++S) {
+        const double c = std::ceil(tiles * S / sms) / S * unit * (1.0 + 0.03 * (S - 1));
+        if (c < *cost * 0.97) *cost = c, sb = S;
+      }
+      return sb;
+    };
+    split128 = best(tm * ((g.N + 127) / 128), 0.5 / 0.76, &c128);
+    split256 = best(tm * ((g.N + 255) / 256), 1.0, &c256);
+  }
   const int forced = use_pair_default();  // DASHCU_GEMM_PAIR: 1 force pair, 0 model, -1 never
   if (forced != -1 && (forced == 1 || (cpair < c256 && cpair < c128)) && gemm_tc_pair(s, g, e)) return true;
   const bool wide = c256 <= c128;
@@ -1124,6 +1193,13 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e) {
   memset(&om, 0, sizeof(om));
   Epi et = e;
   et.tma = out_maps_for(g, e, &om);
+  const int S = wide ? split256 : split128;
+  if (S > 1 && (et.tma & 1)) {
+    const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+    et.splits = S;
+    et.split_flags = split_flag_buffer(tiles * 8);
+    DCU_CHECK(cudaMemsetAsync(et.split_flags, 0, sizeof(uint32_t) * tiles * 8, s));
+  }
   if (wide) dispatch_majors<256, 4>(s, ma, mb, om, g, et);   // 4 x 48 KB stages
   else dispatch_majors<128, 6>(s, ma, mb, om, g, et);        // 6 x 32 KB stages
   return true;

@@ -142,12 +142,21 @@ __global__ void colsum_part_k(const T* __restrict__ X, int64_t ld, int M, int N,
     if (n0 + i < N) t[i] = acc[i];
 }
 
+// block (32 columns x 32 segment lanes): lane y sums segments y, y+32, ... in order, then
+// a fixed-shape tree over the 32 lanes — deterministic for a given (M, N).
 __global__ void colsum_fin_k(const float* __restrict__ tmp, int nseg, int N, float* __restrict__ out) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
+  __shared__ float red[32][33];
+  const int n = blockIdx.x * 32 + threadIdx.x;
   float s = 0.f;
-  for (int y = 0; y < nseg; ++y) s += tmp[static_cast<int64_t>(y) * N + n];
-  out[n] += s;
+  if (n < N)
+    for (int y = threadIdx.y; y < nseg; y += 32) s += tmp[static_cast<int64_t>(y) * N + n];
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 16; w >= 1; w >>= 1) {
+    if (threadIdx.y < w) red[threadIdx.y][threadIdx.x] += red[threadIdx.y + w][threadIdx.x];
+    __syncthreads();
+  }
+  if (threadIdx.y == 0 && n < N) out[n] += red[0][threadIdx.x];
 }
 
 // ----------------------------------------------------------- sampling / loss rows
@@ -639,7 +648,7 @@ void colsum_acc(cudaStream_t s, const T* X, int64_t ld, int M, int N, float* out
   const bool vec = ((reinterpret_cast<uintptr_t>(X) | static_cast<uintptr_t>(ld * sizeof(T))) & 15) == 0;
   colsum_part_k<T, VEC><<<dim3(gx, nseg), 256, 0, s>>>(X, ld, M, N, seg_rows, vec, tmp);
   DCU_LAUNCHED();
-  colsum_fin_k<<<cdiv(N, 256), 256, 0, s>>>(tmp, nseg, N, out);
+  colsum_fin_k<<<cdiv(N, 32), dim3(32, 32), 0, s>>>(tmp, nseg, N, out);
   DCU_LAUNCHED();
 }
 void colsum_acc_f32(cudaStream_t s, const float* X, int64_t ld, int M, int N, float* out, float* tmp) {

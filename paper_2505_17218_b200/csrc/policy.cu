@@ -1424,9 +1424,12 @@ int dashcu_selftest_gemm_timed(dashcu_ctx* c, int M, int N, int K, int a_kmajor,
   cast_f32_bf16(s, tmp, dA, static_cast<int64_t>(na));
   init_normal_ctr(s, tmp, static_cast<int64_t>(nb), 1.0, 2);
   cast_f32_bf16(s, tmp, dB, static_cast<int64_t>(nb));
-  float* c32 = epi == EPI_ACCUM ? c->ws.get<float>("tt_C32", static_cast<size_t>(M) * N) : nullptr;
+  // epi 4: the residual-stream shape of W_o / W_2 (fp32 out = acc + resid, bf16 copy)
+  float* c32 = epi == EPI_ACCUM || epi == 4 ? c->ws.get<float>("tt_C32", static_cast<size_t>(M) * N) : nullptr;
   bf16* cT = epi == EPI_ACCUM ? nullptr : c->ws.get<bf16>("tt_CT", static_cast<size_t>(M) * N);
+  float* res = epi == 4 ? c->ws.get<float>("tt_R32", static_cast<size_t>(M) * N) : nullptr;
   if (c32) DCU_CHECK(cudaMemsetAsync(c32, 0, sizeof(float) * static_cast<size_t>(M) * N, s));
+  if (res) DCU_CHECK(cudaMemsetAsync(res, 0, sizeof(float) * static_cast<size_t>(M) * N, s));
   GemmShape g{M, N, K, dA, a_kmajor ? K : M, a_kmajor != 0, dB, b_kmajor ? K : N, b_kmajor != 0};
   Epi e;
   e.kind = epi == EPI_ACCUM ? EPI_ACCUM : EPI_STORE;
@@ -1434,6 +1437,8 @@ int dashcu_selftest_gemm_timed(dashcu_ctx* c, int M, int N, int K, int a_kmajor,
   e.ldc32 = N;
   e.cT = cT;
   e.ldcT = N;
+  e.resid = res;
+  e.ldr = N;
   gemm(s, 1, g, e);  // warm-up (also builds the tensor maps once)
   Timer tm(s);
   for (int i = 0; i < iters; ++i) gemm(s, 1, g, e);

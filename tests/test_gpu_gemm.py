@@ -95,3 +95,23 @@ def test_tma_store_epilogue_matches_direct_stores(ctx, monkeypatch, shape, epi):
         assert np.array_equal(got[:, :full].view(np.uint32), ref[:, :full].view(np.uint32))
     else:
         assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("shape", [(128, 128, 8192), (896, 896, 36832 // 8), (300, 200, 5000)])
+def test_split_k_accumulate(ctx, monkeypatch, shape):
+    """Weight-gradient shapes (few output tiles, long K) run as ordered split-K: the
+    slices reduce into C in slice order, so repeated runs are bit-identical and the
+    result matches the unsplit kernel to fp32 rounding."""
+    M, N, K = shape
+    rng = np.random.default_rng(11)
+    A = bf16_bits(rng.standard_normal((K, M)).astype(np.float32))   # MN-major operands, as in dW = dY^T X
+    B = bf16_bits(rng.standard_normal((K, N)).astype(np.float32))
+    c0 = rng.standard_normal((M, N)).astype(np.float32)
+    ref = c0 + bits_to_f32(A).astype(np.float64).T @ bits_to_f32(B).astype(np.float64)
+    a = ctx.selftest_gemm(A, False, B, False, M, N, K, epi=3, C_init=c0)
+    b = ctx.selftest_gemm(A, False, B, False, M, N, K, epi=3, C_init=c0)
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert np.abs(a - ref).max() <= 1e-5 * np.abs(ref).max() + 1e-3
+    monkeypatch.setenv("DASHCU_NO_SPLITK", "1")
+    c = ctx.selftest_gemm(A, False, B, False, M, N, K, epi=3, C_init=c0)
+    assert np.abs(a - c).max() <= 1e-5 * np.abs(ref).max() + 1e-3
