@@ -1,0 +1,292 @@
+// tcgen05 attention backward for head_dim 64 (policy.cpp:292-322, restated for packed
+// causal sequences and GQA; the mma.sync kernel in attention_tc.cu is the fallback).
+//
+// One CTA owns a tile of 128 keys of one (sequence, KV head) and loops over every query
+// head of the KV group x every causal tile of 128 queries. Per iteration, with the key
+// axis as the MMA M dimension and all accumulators in TMEM:
+//   (1) S^T  = K  Q^T      M128 N128 K64   A = K  (K-major)   B = Q  (K-major)
+//   (2) dP^T = V  dO^T     M128 N128 K64   A = V  (K-major)   B = dO (K-major)
+//   softmax warps: P^T = exp(S^T/sqrt(d) - LSE_q), dS^T = P^T (dP^T - D_q)/sqrt(d),
+//   written as bf16 into shared memory in the UMMA 128-byte-swizzle layout
+//   (4) dV  += P^T dO      M128 N64 K128   A = P^T (K-major)  B = dO (MN-major)
+//   (5) dK  += dS^T Q      M128 N64 K128   A = dS^T (K-major) B = Q  (MN-major)
+//   (6) dQ   = dS K        M128 N64 K128   A = dS (MN-major: the dS^T bytes)  B = K (MN-major)
+// dQ is read out of TMEM and reduce-added into the fp32 dQ with bulk tensor reduces
+// (one 32 x 32 box per softmax warp); dK / dV stay in TMEM for the whole group (the GQA
+// sum needs no atomics) and are stored once at the end.
+// Warp roles: 0 TMA producer (K, V once; Q / dO double-buffered), 1 MMA issuer,
+// 2 TMEM allocator, 4..11 softmax (TMEM lane quarter = warp % 4, column half = (warp-4)/4).
+// The MMAs of S(i+1) are issued as soon as the softmax warps have pulled S(i) into
+// registers, so they overlap the softmax of iteration i.
+#include <cfloat>
+#include <cstdlib>
+#include <string>
+
+#include "kernels.cuh"
+#include "tc5.cuh"
+
+namespace dashcu {
+
+namespace {
+
+constexpr int kKeys = 128, kQ = 128, kHD = 64;
+constexpr int kTile = kKeys * kHD * 2;  // 16 KB: [128 rows x 64] bf16, 128-byte swizzle
+
+struct Lay {
+  static constexpr int K = 0, V = kTile, Q = 2 * kTile /*2 stages*/, O = 4 * kTile /*2 stages*/;
+  static constexpr int P = 6 * kTile;   // P^T  [128 keys x 128 q]: two 64-q swizzle atoms
+  static constexpr int S = 8 * kTile;   // dS^T [128 keys x 128 q]
+  static constexpr int DQ = 10 * kTile; // 8 softmax warps x 4 KB dQ staging
+  static constexpr int LD = DQ + 8 * 4096;   // sL[2][128], sD[2][128]
+  static constexpr int BAR = LD + 2048;
+  static constexpr int BYTES = BAR + 256 + 1024;  // + alignment slack
+};
+
+// TMEM columns
+constexpr uint32_t kTS = 0, kTdP = 128, kTdV = 256, kTdK = 320, kTdQ = 384;
+
+constexpr uint32_t idesc(int n, bool a_mn, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// one 128-byte row (64 bf16) of a K-major swizzle atom: chunk j of row r at (j ^ (r & 7))
+__device__ __forceinline__ void st_row64(uint32_t atom, int r, const float* v) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(atom + r * 128 + ((j ^ (r & 7)) << 4)),
+                 "r"(pack2(v[8 * j], v[8 * j + 1])), "r"(pack2(v[8 * j + 2], v[8 * j + 3])),
+                 "r"(pack2(v[8 * j + 4], v[8 * j + 5])), "r"(pack2(v[8 * j + 6], v[8 * j + 7]))
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_tc5_k(const __grid_constant__ CUtensorMap mQKV, const __grid_constant__ CUtensorMap mO,
+                   const __grid_constant__ CUtensorMap mDQ, const int32_t* __restrict__ seq_start,
+                   const float* __restrict__ lse, const float* __restrict__ Dsum, int nh, int nkv,
+                   float* __restrict__ dkv32, float scale, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int kt = blockIdx.x, sq = blockIdx.y, kvh = blockIdx.z;
+  const int s0 = seq_start[sq], n = seq_start[sq + 1] - s0;
+  const int k0 = kt * kKeys;
+  if (k0 >= n) return;  // uniform for the CTA, before any barrier
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = nh / nkv, qd = nh * kHD, kvd = nkv * kHD;
+  const int nq = (n + kQ - 1) / kQ - kt;  // causal query tiles per head: kt .. last
+  const int nit = grp * nq;
+
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR);
+  uint64_t *kvfull = bar, *qfull = bar + 1 /*[2]*/, *qempty = bar + 3 /*[2]*/, *sfull = bar + 5, *sfree = bar + 6,
+           *pready = bar + 7, *pfree = bar + 8, *dqfull = bar + 9, *dqfree = bar + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
+  float* sLD = reinterpret_cast<float*>(smem + Lay::LD);  // [2][sL 128 | sD 128]
+
+  if (threadIdx.x == 0) {
+    mbar_init(kvfull, 1);
+    for (int s = 0; s < 2; ++s) mbar_init(&qfull[s], 1), mbar_init(&qempty[s], 1);
+    mbar_init(sfull, 1);
+    mbar_init(sfree, 256);
+    mbar_init(pready, 256);
+    mbar_init(pfree, 1);
+    mbar_init(dqfull, 1);
+    mbar_init(dqfree, 256);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mQKV)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mO)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sK = smem_u32(smem + Lay::K), sV = smem_u32(smem + Lay::V), sQ = smem_u32(smem + Lay::Q),
+                 sO = smem_u32(smem + Lay::O), sP = smem_u32(smem + Lay::P), sS = smem_u32(smem + Lay::S);
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------------------------------------------------------- TMA
+      mbar_expect_tx(kvfull, 2 * kTile);
+      tma_load_2d(smem + Lay::K, &mQKV, kvfull, qd + kvh * kHD, s0 + k0);
+      tma_load_2d(smem + Lay::V, &mQKV, kvfull, qd + kvd + kvh * kHD, s0 + k0);
+      for (int it = 0; it < nit; ++it) {
+        const int st = it & 1, h = kvh * grp + it / nq, q0 = (kt + it % nq) * kQ;
+        mbar_wait(&qempty[st], ((it >> 1) & 1) ^ 1);
+        mbar_expect_tx(&qfull[st], 2 * kTile);
+        tma_load_2d(smem + Lay::Q + st * kTile, &mQKV, &qfull[st], h * kHD, s0 + q0);
+        tma_load_2d(smem + Lay::O + st * kTile, &mO, &qfull[st], h * kHD, s0 + q0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------------------------------------------------------- MMA
+      constexpr uint32_t I_SS = idesc(128, false, false), I_KM = idesc(64, false, true), I_MM = idesc(64, true, true);
+      mbar_wait(kvfull, 0);
+      auto issue_s = [&](int it) {
+        const int st = it & 1;
+        mbar_wait(&qfull[st], (it >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t q = sQ + st * kTile, o = sO + st * kTile;
+#pragma unroll
+        for (int k = 0; k < kHD / 16; ++k)
+          umma_bf16(tmem + kTS, smem_desc(sK + k * 32, 16, 1024), smem_desc(q + k * 32, 16, 1024), I_SS, k > 0);
+#pragma unroll
+        for (int k = 0; k < kHD / 16; ++k)
+          umma_bf16(tmem + kTdP, smem_desc(sV + k * 32, 16, 1024), smem_desc(o + k * 32, 16, 1024), I_SS, k > 0);
+        umma_commit(sfull);
+      };
+      issue_s(0);
+      for (int it = 0; it < nit; ++it) {
+        const int st = it & 1;
+        if (it + 1 < nit) {  // S(it+1) as soon as the softmax warps hold S(it) in registers
+          mbar_wait(sfree, it & 1);
+          issue_s(it + 1);
+        }
+        mbar_wait(pready, it & 1);
+        if (it > 0) mbar_wait(dqfree, (it - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t q = sQ + st * kTile, o = sO + st * kTile;
+#pragma unroll
+        for (int j = 0; j < kQ / 16; ++j) {  // K = 128 queries: two 64-wide atoms of P^T / dS^T
+          const uint32_t ka = (j >> 2) * kTile + (j & 3) * 32;
+          umma_bf16(tmem + kTdV, smem_desc(sP + ka, 16, 1024), smem_desc(o + j * 2048, kTile, 1024), I_KM,
+                    (it > 0 || j > 0) ? 1u : 0u);
+          umma_bf16(tmem + kTdK, smem_desc(sS + ka, 16, 1024), smem_desc(q + j * 2048, kTile, 1024), I_KM,
+                    (it > 0 || j > 0) ? 1u : 0u);
+        }
+#pragma unroll
+        for (int j = 0; j < kKeys / 16; ++j)  // K = 128 keys; dS read MN-major (q is contiguous)
+          umma_bf16(tmem + kTdQ, smem_desc(sS + j * 2048, kTile, 1024), smem_desc(sK + j * 2048, kTile, 1024), I_MM,
+                    j > 0 ? 1u : 0u);
+        umma_commit(&qempty[st]);
+        umma_commit(pfree);
+        umma_commit(dqfull);
+      }
+    }
+  } else if (warp >= 4) {  // ---------------------------------------------------------- softmax
+    const int ew = warp - 4, qq = ew & 3, hf = ew >> 2;
+    const int tid = threadIdx.x - 128;  // 0..255
+    const int key_l = qq * 32 + lane, key = k0 + key_l;
+    const uint32_t lanes = static_cast<uint32_t>(qq * 32) << 16;
+    const uint32_t stg = smem_u32(smem + Lay::DQ + ew * 4096);
+    for (int it = 0; it < nit; ++it) {
+      const int h = kvh * grp + it / nq, q0 = (kt + it % nq) * kQ;
+      float* L = sLD + (it & 1) * 256;
+      float* D = L + 128;
+      {
+        const int ql = tid & 127, q = q0 + ql;
+        const int64_t idx = static_cast<int64_t>(s0 + q) * nh + h;
+        if (tid < 128) L[ql] = q < n ? lse[idx] * 1.4426950408889634f : 0.f;
+        else D[ql] = q < n ? Dsum[idx] : 0.f;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      mbar_wait(sfull, it & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float sv[64], dp[64];
+      tmem_ld32(tmem + lanes + kTS + hf * 64, sv);
+      tmem_ld32(tmem + lanes + kTS + hf * 64 + 32, sv + 32);
+      tmem_ld32(tmem + lanes + kTdP + hf * 64, dp);
+      tmem_ld32(tmem + lanes + kTdP + hf * 64 + 32, dp + 32);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(sfree);
+#pragma unroll
+      for (int c = 0; c < 64; ++c) {
+        const int ql = hf * 64 + c, q = q0 + ql;
+        const bool ok = q < n && key < n && key <= q;
+        const float p = ok ? ex2(sv[c] * scale_log2 - L[ql]) : 0.f;
+        sv[c] = p;
+        dp[c] = p * (dp[c] - D[ql]) * scale;
+      }
+      if (it > 0) mbar_wait(pfree, (it - 1) & 1);  // MMAs of it-1 done reading P^T / dS^T
+      st_row64(sP + hf * kTile, key_l, sv);
+      st_row64(sS + hf * kTile, key_l, dp);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(pready);
+      // dQ rows q0 + 32 qq + lane, columns hf*32 .. +31 of head h
+      mbar_wait(dqfull, it & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float dq[32];
+      tmem_ld32(tmem + lanes + kTdQ + hf * 32, dq);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(dqfree);
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stg + lane * 128 + ((j ^ (lane & 7)) << 4)),
+                     "f"(dq[4 * j]), "f"(dq[4 * j + 1]), "f"(dq[4 * j + 2]), "f"(dq[4 * j + 3])
+                     : "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile(
+            "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                reinterpret_cast<uint64_t>(&mDQ)),
+            "r"(stg), "r"(h * kHD + hf * 32), "r"(s0 + q0 + qq * 32)
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    // dK, dV of this thread's key row (all MMAs completed: the last dqfull covers them)
+    float dk[32], dv[32];
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    tmem_ld32(tmem + lanes + kTdK + hf * 32, dk);
+    tmem_ld32(tmem + lanes + kTdV + hf * 32, dv);
+    if (key < n) {
+      float* dkr = dkv32 + static_cast<int64_t>(s0 + key) * 2 * kvd + kvh * kHD + hf * 32;
+      float* dvr = dkr + kvd;
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        *reinterpret_cast<float4*>(dkr + i) = make_float4(dk[i], dk[i + 1], dk[i + 2], dk[i + 3]);
+        *reinterpret_cast<float4*>(dvr + i) = make_float4(dv[i], dv[i + 1], dv[i + 2], dv[i + 3]);
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+}  // namespace
+
+bool attn_bwd_tc5(cudaStream_t s, const bf16* qkv, const bf16* dctx, const float* lse, const float* Dbuf,
+                  const int32_t* seq_start, int n_seq, int max_len, int rows, int nh, int nkv, int hd, float* dq32,
+                  float* dkv32) {
+  if (hd != kHD || nh % nkv) return false;
+  const char* force = getenv("DASHCU_ATTN_BWD");
+  if (force && std::string(force) == "mma") return false;
+  const int qd = nh * hd, qkvd = qd + 2 * nkv * hd;
+  CUtensorMap mq, mo, mdq;
+  if (!tma_map_2d(&mq, qkv, rows, qkvd, qkvd, kHD, 128, false, 128, true) ||
+      !tma_map_2d(&mo, dctx, rows, qd, qd, kHD, 128, false, 128, true) ||
+      !tma_map_2d(&mdq, dq32, rows, qd, qd, 32, 32, true, 128, false))
+    return false;
+  static bool attr = false;
+  if (!attr) {
+    DCU_CHECK(cudaFuncSetAttribute(attn_bwd_tc5_k, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::BYTES));
+    attr = true;
+  }
+  const float sc = 1.f / sqrtf(static_cast<float>(hd));
+  dim3 grid((max_len + kKeys - 1) / kKeys, n_seq, nkv);
+  attn_bwd_tc5_k<<<grid, 384, Lay::BYTES, s>>>(mq, mo, mdq, seq_start, lse, Dbuf, nh, nkv, dkv32, sc,
+                                               sc * 1.4426950408889634f);
+  DCU_LAUNCHED();
+  return true;
+}
+
+}  // namespace dashcu

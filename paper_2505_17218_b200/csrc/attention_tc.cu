@@ -621,6 +621,7 @@ bool attn_bwd_tc(cudaStream_t s, const bf16* qkv, const bf16* ctx, const bf16* d
   attn_bwd_dot_k<<<kNumSMs * 8, 256, 0, s>>>(dctx, ctx, rows, nh, hd, Dbuf);
   DCU_LAUNCHED();
   DCU_CHECK(cudaMemsetAsync(dq32, 0, sizeof(float) * static_cast<size_t>(rows) * nh * hd, s));
+  if (attn_bwd_tc5(s, qkv, dctx, lse, Dbuf, seq_start, n_seq, max_len, rows, nh, nkv, hd, dq32, dkv32)) return true;
   const float sc = 1.f / sqrtf(static_cast<float>(hd));
   const float sl2 = kLog2e * sc;
   dim3 grid((max_len + 63) / 64, n_seq, nkv);

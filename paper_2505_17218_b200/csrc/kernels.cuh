@@ -49,6 +49,11 @@ bool attn_fwd_tc(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int 
 bool attn_bwd_tc(cudaStream_t s, const bf16* qkv, const bf16* ctx, const bf16* dctx, const float* lse,
                  const int32_t* seq_start, int n_seq, int max_len, int rows, int nh, int nkv, int hd, float* Dbuf,
                  float* dq32, float* dkv32, double alg_flops);
+// tcgen05 backward (head_dim 64): dq32 must be zero, D (Dbuf) computed; false if not covered
+// (DASHCU_ATTN_BWD=mma forces the mma.sync kernel).
+bool attn_bwd_tc5(cudaStream_t s, const bf16* qkv, const bf16* dctx, const float* lse, const float* Dbuf,
+                  const int32_t* seq_start, int n_seq, int max_len, int rows, int nh, int nkv, int hd, float* dq32,
+                  float* dkv32);
 // qkv-gradient assembly: dqkv (T) from fp32 dq [T x qd] and dkv [T x 2 kvd]
 template <class T>
 void pack_dqkv(cudaStream_t s, const float* dq, const float* dkv, int rows, int qd, int kvd, T* dqkv);

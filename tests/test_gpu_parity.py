@@ -32,6 +32,9 @@ LONG = dict(vocab_size=64, embed_dim=128, context_len=200, ffn_hidden=128, n_lay
 # vocab spanning many fused-sampling tiles (ragged last tile)
 VBIG = dict(vocab_size=5003, embed_dim=64, context_len=32, ffn_hidden=64, n_layers=1, bos_id=0, eos_id=1,
             n_heads=1, n_kv_heads=1, head_dim=64)
+# several 128-key / 128-query tiles per sequence (tcgen05 attention backward, GQA group 2)
+LONGGQA = dict(vocab_size=64, embed_dim=256, context_len=320, ffn_hidden=128, n_layers=1, bos_id=0, eos_id=1,
+               n_heads=4, n_kv_heads=2, head_dim=64)
 TOL = {D.F32: 1e-3, D.BF16: 2e-2}
 
 
@@ -251,6 +254,30 @@ def test_pg_gradient_parity(ctx, arch, dtype):
     for s in range(16):
         O.grad_log_prob(arch, p, prompts[s // 4], comps[s], w[s], ref)
     assert_grad_close(arch, got, ref, TOL[dtype])
+    pol.close()
+
+
+@pytest.mark.parametrize("kernel", ["tc5", "mma"])
+def test_pg_gradient_parity_long_sequences(ctx, monkeypatch, kernel):
+    """Ragged sequences up to 300 tokens: several key and query tiles, the causal
+    diagonal tiles and ragged tile ends, through both attention backward kernels."""
+    if kernel == "mma":
+        monkeypatch.setenv("DASHCU_ATTN_BWD", "mma")
+    arch = LONGGQA
+    pol = D.Policy(ctx, arch, D.BF16)
+    p = params32(arch, 0.3, 10)
+    pol.upload(p)
+    rng = np.random.default_rng(12)
+    prompts, comps = rand_batch(rng, arch, 3, 2, m_range=(2, 20), len_range=(100, 300))
+    pol.load_rollout(prompts, 2, comps)
+    w = rng.standard_normal(6) / 6
+    pol.grad_zero()
+    pol.accumulate_weighted(w, micro_batch=6)
+    got = pol.grad()
+    ref = np.zeros_like(got)
+    for s in range(6):
+        O.grad_log_prob(arch, p, prompts[s // 2], comps[s], w[s], ref)
+    assert_grad_close(arch, got, ref, TOL[D.BF16])
     pol.close()
 
 
