@@ -89,8 +89,8 @@ __global__ void __launch_bounds__(384, 1)
 
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR);
   uint64_t *kvfull = bar, *qfull = bar + 1 /*[2]*/, *qempty = bar + 3 /*[2]*/, *sfull = bar + 5, *sfree = bar + 6,
-           *pready = bar + 7, *pfree = bar + 8, *dqfull = bar + 9, *dqfree = bar + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
+           *pready = bar + 7, *dqfull = bar + 8, *dqfree = bar + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
   float* sLD = reinterpret_cast<float*>(smem + Lay::LD);  // [2][sL 128 | sD 128]
 
   if (threadIdx.x == 0) {
@@ -99,7 +99,6 @@ __global__ void __launch_bounds__(384, 1)
     mbar_init(sfull, 1);
     mbar_init(sfree, 256);
     mbar_init(pready, 256);
-    mbar_init(pfree, 1);
     mbar_init(dqfull, 1);
     mbar_init(dqfree, 256);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -172,7 +171,6 @@ __global__ void __launch_bounds__(384, 1)
           umma_bf16(tmem + kTdQ, smem_desc(sS + j * 2048, kTile, 1024), smem_desc(sK + j * 2048, kTile, 1024), I_MM,
                     j > 0 ? 1u : 0u);
         umma_commit(&qempty[st]);
-        umma_commit(pfree);
         umma_commit(dqfull);
       }
     }
@@ -182,41 +180,17 @@ __global__ void __launch_bounds__(384, 1)
     const int key_l = qq * 32 + lane, key = k0 + key_l;
     const uint32_t lanes = static_cast<uint32_t>(qq * 32) << 16;
     const uint32_t stg = smem_u32(smem + Lay::DQ + ew * 4096);
-    for (int it = 0; it < nit; ++it) {
+    // L (log2-scaled LSE) and D of the next iteration's 128 queries: one value per thread,
+    // loaded a whole iteration ahead so the global latency stays off the critical path
+    auto fetch = [&](int it) -> float {
+      const int h = kvh * grp + it / nq, q = (kt + it % nq) * kQ + (tid & 127);
+      const int64_t idx = static_cast<int64_t>(s0 + q) * nh + h;
+      return q < n ? (tid < 128 ? lse[idx] * 1.4426950408889634f : Dsum[idx]) : 0.f;
+    };
+    // dQ of iteration `it` (rows q0 + 32 qq + lane, head columns hf*32 .. +31): TMEM ->
+    // swizzled staging -> one bulk tensor reduce-add per warp
+    auto dq_out = [&](int it) {  // after mbar_wait(dqfull, it & 1)
       const int h = kvh * grp + it / nq, q0 = (kt + it % nq) * kQ;
-      float* L = sLD + (it & 1) * 256;
-      float* D = L + 128;
-      {
-        const int ql = tid & 127, q = q0 + ql;
-        const int64_t idx = static_cast<int64_t>(s0 + q) * nh + h;
-        if (tid < 128) L[ql] = q < n ? lse[idx] * 1.4426950408889634f : 0.f;
-        else D[ql] = q < n ? Dsum[idx] : 0.f;
-      }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      mbar_wait(sfull, it & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      float sv[64], dp[64];
-      tmem_ld32(tmem + lanes + kTS + hf * 64, sv);
-      tmem_ld32(tmem + lanes + kTS + hf * 64 + 32, sv + 32);
-      tmem_ld32(tmem + lanes + kTdP + hf * 64, dp);
-      tmem_ld32(tmem + lanes + kTdP + hf * 64 + 32, dp + 32);
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(sfree);
-#pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        const int ql = hf * 64 + c, q = q0 + ql;
-        const bool ok = q < n && key < n && key <= q;
-        const float p = ok ? ex2(sv[c] * scale_log2 - L[ql]) : 0.f;
-        sv[c] = p;
-        dp[c] = p * (dp[c] - D[ql]) * scale;
-      }
-      if (it > 0) mbar_wait(pfree, (it - 1) & 1);  // MMAs of it-1 done reading P^T / dS^T
-      st_row64(sP + hf * kTile, key_l, sv);
-      st_row64(sS + hf * kTile, key_l, dp);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(pready);
-      // dQ rows q0 + 32 qq + lane, columns hf*32 .. +31 of head h
-      mbar_wait(dqfull, it & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float dq[32];
       tmem_ld32(tmem + lanes + kTdQ + hf * 32, dq);
@@ -239,7 +213,47 @@ __global__ void __launch_bounds__(384, 1)
             : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
+    };
+    float ldn = fetch(0);
+    for (int it = 0; it < nit; ++it) {
+      const int q0 = (kt + it % nq) * kQ;
+      float* L = sLD + (it & 1) * 256;
+      float* D = L + 128;
+      L[tid] = ldn;  // tid < 128: L[q], else D[q - 128]
+      if (it + 1 < nit) ldn = fetch(it + 1);
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      mbar_wait(sfull, it & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t sr[64], dr[64];
+      tmem_ld32_async(tmem + lanes + kTS + hf * 64, sr);
+      tmem_ld32_async(tmem + lanes + kTS + hf * 64 + 32, sr + 32);
+      tmem_ld32_async(tmem + lanes + kTdP + hf * 64, dr);
+      tmem_ld32_async(tmem + lanes + kTdP + hf * 64 + 32, dr + 32);
+      tmem_wait_ld();
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(sfree);
+      float* sv = reinterpret_cast<float*>(sr);  // P^T and dS^T overwrite S^T / dP^T in place
+      float* dp = reinterpret_cast<float*>(dr);
+#pragma unroll
+      for (int c = 0; c < 64; ++c) {
+        const int ql = hf * 64 + c, q = q0 + ql;
+        const bool ok = q < n && key < n && key <= q;
+        const float p = ok ? ex2(sv[c] * scale_log2 - L[ql]) : 0.f;
+        sv[c] = p;
+        dp[c] = p * (dp[c] - D[ql]) * scale;
+      }
+      // the MMAs of it-1 are complete (dQ ready, P^T / dS^T no longer read): overwrite the
+      // operands, release the next MMAs, then read dQ(it-1) out (TMEM dQ is rewritten only
+      // after dqfree)
+      if (it > 0) mbar_wait(dqfull, (it - 1) & 1);
+      st_row64(sP + hf * kTile, key_l, sv);
+      st_row64(sS + hf * kTile, key_l, dp);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(pready);
+      if (it > 0) dq_out(it - 1);
     }
+    mbar_wait(dqfull, (nit - 1) & 1);
+    dq_out(nit - 1);
     // dK, dV of this thread's key row (all MMAs completed: the last dqfull covers them)
     float dk[32], dv[32];
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
