@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(384, 1)
                    float* __restrict__ dkv32, float scale, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int kt = blockIdx.x, sq = blockIdx.y, kvh = blockIdx.z;
+  // grid (sequence x kv head, key tile): launch order puts every long (early) key tile first
+  const int kt = blockIdx.y, sq = blockIdx.x / nkv, kvh = blockIdx.x % nkv;
   const int s0 = seq_start[sq], n = seq_start[sq + 1] - s0;
   const int k0 = kt * kKeys;
   if (k0 >= n) return;  // uniform for the CTA, before any barrier
@@ -89,8 +90,8 @@ __global__ void __launch_bounds__(384, 1)
 
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR);
   uint64_t *kvfull = bar, *qfull = bar + 1 /*[2]*/, *qempty = bar + 3 /*[2]*/, *sfull = bar + 5, *sfree = bar + 6,
-           *pready = bar + 7, *dqfull = bar + 8, *dqfree = bar + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
+           *pready = bar + 7, *dqfull = bar + 8, *dqfree = bar + 9, *ldfull = bar + 10 /*[2]*/;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
   float* sLD = reinterpret_cast<float*>(smem + Lay::LD);  // [2][sL 128 | sD 128]
 
   if (threadIdx.x == 0) {
@@ -101,6 +102,8 @@ __global__ void __launch_bounds__(384, 1)
     mbar_init(pready, 256);
     mbar_init(dqfull, 1);
     mbar_init(dqfree, 256);
+    mbar_init(&ldfull[0], 32);
+    mbar_init(&ldfull[1], 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mQKV)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mO)) : "memory");
@@ -117,18 +120,33 @@ __global__ void __launch_bounds__(384, 1)
   const uint32_t sK = smem_u32(smem + Lay::K), sV = smem_u32(smem + Lay::V), sQ = smem_u32(smem + Lay::Q),
                  sO = smem_u32(smem + Lay::O), sP = smem_u32(smem + Lay::P), sS = smem_u32(smem + Lay::S);
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------------------------------------------------------- TMA
+  if (warp == 0) {  // ------------------------------------------------------------------ loads
+    if (lane == 0) {
       mbar_expect_tx(kvfull, 2 * kTile);
       tma_load_2d(smem + Lay::K, &mQKV, kvfull, qd + kvh * kHD, s0 + k0);
       tma_load_2d(smem + Lay::V, &mQKV, kvfull, qd + kvd + kvh * kHD, s0 + k0);
-      for (int it = 0; it < nit; ++it) {
-        const int st = it & 1, h = kvh * grp + it / nq, q0 = (kt + it % nq) * kQ;
-        mbar_wait(&qempty[st], ((it >> 1) & 1) ^ 1);
+    }
+    int h = kvh * grp, qt = kt;
+    for (int it = 0; it < nit; ++it) {
+      const int st = it & 1, q0 = qt * kQ;
+      mbar_wait(&qempty[st], ((it >> 1) & 1) ^ 1);
+      if (lane == 0) {
         mbar_expect_tx(&qfull[st], 2 * kTile);
         tma_load_2d(smem + Lay::Q + st * kTile, &mQKV, &qfull[st], h * kHD, s0 + q0);
         tma_load_2d(smem + Lay::O + st * kTile, &mO, &qfull[st], h * kHD, s0 + q0);
       }
+      // log2-scaled LSE and D of the tile's 128 queries (the rows of lse / D are strided
+      // by n_heads, so the warp gathers them rather than TMA)
+      float* L = sLD + st * 256;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int ql = lane + 32 * j, q = q0 + ql;
+        const int64_t idx = static_cast<int64_t>(s0 + q) * nh + h;
+        L[ql] = q < n ? lse[idx] * 1.4426950408889634f : 0.f;
+        L[128 + ql] = q < n ? Dsum[idx] : 0.f;
+      }
+      mbar_arrive(&ldfull[st]);
+      if (++qt * kQ >= n) qt = kt, ++h;
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------------------------------------------------------- MMA
@@ -176,26 +194,20 @@ __global__ void __launch_bounds__(384, 1)
     }
   } else if (warp >= 4) {  // ---------------------------------------------------------- softmax
     const int ew = warp - 4, qq = ew & 3, hf = ew >> 2;
-    const int tid = threadIdx.x - 128;  // 0..255
     const int key_l = qq * 32 + lane, key = k0 + key_l;
     const uint32_t lanes = static_cast<uint32_t>(qq * 32) << 16;
     const uint32_t stg = smem_u32(smem + Lay::DQ + ew * 4096);
-    // L (log2-scaled LSE) and D of the next iteration's 128 queries: one value per thread,
-    // loaded a whole iteration ahead so the global latency stays off the critical path
-    auto fetch = [&](int it) -> float {
-      const int h = kvh * grp + it / nq, q = (kt + it % nq) * kQ + (tid & 127);
-      const int64_t idx = static_cast<int64_t>(s0 + q) * nh + h;
-      return q < n ? (tid < 128 ? lse[idx] * 1.4426950408889634f : Dsum[idx]) : 0.f;
-    };
     // dQ of iteration `it` (rows q0 + 32 qq + lane, head columns hf*32 .. +31): TMEM ->
-    // swizzled staging -> one bulk tensor reduce-add per warp
-    auto dq_out = [&](int it) {  // after mbar_wait(dqfull, it & 1)
-      const int h = kvh * grp + it / nq, q0 = (kt + it % nq) * kQ;
+    // scale -> swizzled staging -> one bulk tensor reduce-add per warp. Call after
+    // mbar_wait(dqfull, it & 1).
+    auto dq_out = [&](int h, int q0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float dq[32];
       tmem_ld32(tmem + lanes + kTdQ + hf * 32, dq);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(dqfree);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) dq[j] *= scale;
       if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       __syncwarp();
 #pragma unroll
@@ -214,14 +226,12 @@ __global__ void __launch_bounds__(384, 1)
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     };
-    float ldn = fetch(0);
+    int h = kvh * grp, qt = kt, ph = 0, pq0 = 0;  // (head, tile) of this and of the previous iteration
     for (int it = 0; it < nit; ++it) {
-      const int q0 = (kt + it % nq) * kQ;
-      float* L = sLD + (it & 1) * 256;
-      float* D = L + 128;
-      L[tid] = ldn;  // tid < 128: L[q], else D[q - 128]
-      if (it + 1 < nit) ldn = fetch(it + 1);
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const int st = it & 1, q0 = qt * kQ;
+      mbar_wait(&ldfull[st], (it >> 1) & 1);
+      const float* L = sLD + st * 256 + hf * 64;
+      const float* D = L + 128;
       mbar_wait(sfull, it & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       uint32_t sr[64], dr[64];
@@ -234,13 +244,23 @@ __global__ void __launch_bounds__(384, 1)
       mbar_arrive(sfree);
       float* sv = reinterpret_cast<float*>(sr);  // P^T and dS^T overwrite S^T / dP^T in place
       float* dp = reinterpret_cast<float*>(dr);
+      // masks only on the causal diagonal and at the sequence end (warp-uniform)
+      const bool edge = qt == kt || q0 + kQ > n || k0 + kKeys > n;
 #pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        const int ql = hf * 64 + c, q = q0 + ql;
-        const bool ok = q < n && key < n && key <= q;
-        const float p = ok ? ex2(sv[c] * scale_log2 - L[ql]) : 0.f;
-        sv[c] = p;
-        dp[c] = p * (dp[c] - D[ql]) * scale;
+      for (int c = 0; c < 64; c += 4) {
+        const float4 l4 = *reinterpret_cast<const float4*>(L + c);
+        const float4 d4 = *reinterpret_cast<const float4*>(D + c);
+        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float p = ex2(__fmaf_rn(sv[c + e], scale_log2, -lv[e]));
+          if (edge) {
+            const int q = q0 + hf * 64 + c + e;
+            p = (q < n && key < n && key <= q) ? p : 0.f;
+          }
+          sv[c + e] = p;
+          dp[c + e] = p * (dp[c + e] - dv4[e]);  // 1/sqrt(d) is applied to dK / dQ at readout
+        }
       }
       // the MMAs of it-1 are complete (dQ ready, P^T / dS^T no longer read): overwrite the
       // operands, release the next MMAs, then read dQ(it-1) out (TMEM dQ is rewritten only
@@ -250,15 +270,19 @@ __global__ void __launch_bounds__(384, 1)
       st_row64(sS + hf * kTile, key_l, dp);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(pready);
-      if (it > 0) dq_out(it - 1);
+      if (it > 0) dq_out(ph, pq0);
+      ph = h, pq0 = q0;
+      if (++qt * kQ >= n) qt = kt, ++h;
     }
     mbar_wait(dqfull, (nit - 1) & 1);
-    dq_out(nit - 1);
+    dq_out(ph, pq0);
     // dK, dV of this thread's key row (all MMAs completed: the last dqfull covers them)
     float dk[32], dv[32];
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     tmem_ld32(tmem + lanes + kTdK + hf * 32, dk);
     tmem_ld32(tmem + lanes + kTdV + hf * 32, dv);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) dk[i] *= scale;
     if (key < n) {
       float* dkr = dkv32 + static_cast<int64_t>(s0 + key) * 2 * kvd + kvh * kHD + hf * 32;
       float* dvr = dkr + kvd;
@@ -296,7 +320,7 @@ bool attn_bwd_tc5(cudaStream_t s, const bf16* qkv, const bf16* dctx, const float
     attr = true;
   }
   const float sc = 1.f / sqrtf(static_cast<float>(hd));
-  dim3 grid((max_len + kKeys - 1) / kKeys, n_seq, nkv);
+  dim3 grid(n_seq * nkv, (max_len + kKeys - 1) / kKeys);
   attn_bwd_tc5_k<<<grid, 384, Lay::BYTES, s>>>(mq, mo, mdq, seq_start, lse, Dbuf, nh, nkv, dkv32, sc,
                                                sc * 1.4426950408889634f);
   DCU_LAUNCHED();
