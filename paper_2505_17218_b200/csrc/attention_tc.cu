@@ -594,11 +594,12 @@ void smem_attr(K k, int bytes) {
 
 }  // namespace
 
-bool attn_fwd_tc(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int n_seq, int max_len, int nh, int nkv,
-                 int hd, bf16* ctx, float* lse, double alg_flops) {
+bool attn_fwd_tc(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int n_seq, int max_len, int rows, int nh,
+                 int nkv, int hd, bf16* ctx, float* lse, double alg_flops) {
   if (hd != 64 && hd != 128) return false;
   if (n_seq <= 0) return true;
   ProfScope ps(PROF_ATTN_FWD, s, alg_flops, 0);
+  if (attn_fwd_tc5(s, qkv, seq_start, n_seq, max_len, rows, nh, nkv, hd, ctx, lse)) return true;
   const float sl2 = kLog2e / sqrtf(static_cast<float>(hd));
   dim3 grid((max_len + 63) / 64, n_seq, nh);
   if (hd == 64) {

@@ -346,7 +346,7 @@ struct Engine {
       mm(Tn, g.qkvd, g.d, xl, g.d, true, W(b + L.wq), g.d, true, store(nullptr, 0, qkv, g.qkvd));
       bool done = false;
       if constexpr (sizeof(T) == 2)
-        done = attn_fwd_tc(st, qkv, start, nseq, maxlen, g.nh, g.nkv, g.hd, ctx, lse, 4.0 * g.nh * g.hd * pairs);
+        done = attn_fwd_tc(st, qkv, start, nseq, maxlen, Tn, g.nh, g.nkv, g.hd, ctx, lse, 4.0 * g.nh * g.hd * pairs);
       if (!done)
         attn_fwd_varlen<T>(st, qkv, start, nseq, maxlen, g.nh, g.nkv, g.hd, ctx, lse, 4.0 * g.nh * g.hd * pairs);
       Epi eo = store(A.h32, g.d, hT, g.d);

@@ -260,9 +260,11 @@ def test_pg_gradient_parity(ctx, arch, dtype):
 @pytest.mark.parametrize("kernel", ["tc5", "mma"])
 def test_pg_gradient_parity_long_sequences(ctx, monkeypatch, kernel):
     """Ragged sequences up to 300 tokens: several key and query tiles, the causal
-    diagonal tiles and ragged tile ends, through both attention backward kernels."""
+    diagonal tiles and ragged tile ends, through the tcgen05 and the mma.sync attention
+    kernels (forward and backward)."""
     if kernel == "mma":
         monkeypatch.setenv("DASHCU_ATTN_BWD", "mma")
+        monkeypatch.setenv("DASHCU_ATTN_FWD", "mma")
     arch = LONGGQA
     pol = D.Policy(ctx, arch, D.BF16)
     p = params32(arch, 0.3, 10)
@@ -270,6 +272,9 @@ def test_pg_gradient_parity_long_sequences(ctx, monkeypatch, kernel):
     rng = np.random.default_rng(12)
     prompts, comps = rand_batch(rng, arch, 3, 2, m_range=(2, 20), len_range=(100, 300))
     pol.load_rollout(prompts, 2, comps)
+    lp = pol.rollout_log_prob(sum(len(c) for c in comps))
+    ref_lp = np.concatenate([O.log_prob(arch, p, prompts[s // 2], comps[s])[1] for s in range(6)])
+    assert np.abs(lp - ref_lp).max() <= TOL[D.BF16] * max(1.0, np.abs(ref_lp).max())
     w = rng.standard_normal(6) / 6
     pol.grad_zero()
     pol.accumulate_weighted(w, micro_batch=6)
