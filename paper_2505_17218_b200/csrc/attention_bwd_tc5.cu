@@ -32,13 +32,15 @@ namespace {
 constexpr int kKeys = 128, kQ = 128, kHD = 64;
 constexpr int kTile = kKeys * kHD * 2;  // 16 KB: [128 rows x 64] bf16, 128-byte swizzle
 
+constexpr int kST = 3;  // Q / dO / (LSE, D) pipeline depth
+
 struct Lay {
-  static constexpr int K = 0, V = kTile, Q = 2 * kTile /*2 stages*/, O = 4 * kTile /*2 stages*/;
-  static constexpr int P = 6 * kTile;   // P^T  [128 keys x 128 q]: two 64-q swizzle atoms
-  static constexpr int S = 8 * kTile;   // dS^T [128 keys x 128 q]
-  static constexpr int DQ = 10 * kTile; // 8 softmax warps x 4 KB dQ staging
-  static constexpr int LD = DQ + 8 * 4096;   // sL[2][128], sD[2][128]
-  static constexpr int BAR = LD + 2048;
+  static constexpr int K = 0, V = kTile, Q = 2 * kTile /*kST stages*/, O = (2 + kST) * kTile /*kST stages*/;
+  static constexpr int P = (2 + 2 * kST) * kTile;  // P^T  [128 keys x 128 q]: two 64-q swizzle atoms
+  static constexpr int S = P + 2 * kTile;           // dS^T [128 keys x 128 q]
+  static constexpr int DQ = S + 2 * kTile;          // 8 softmax warps x 2 KB dQ staging (16 x 32 fp32)
+  static constexpr int LD = DQ + 8 * 2048;          // per stage: sL[128], sD[128]
+  static constexpr int BAR = LD + kST * 1024;
   static constexpr int BYTES = BAR + 256 + 1024;  // + alignment slack
 };
 
@@ -89,21 +91,20 @@ __global__ void __launch_bounds__(384, 1)
   const int nit = grp * nq;
 
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR);
-  uint64_t *kvfull = bar, *qfull = bar + 1 /*[2]*/, *qempty = bar + 3 /*[2]*/, *sfull = bar + 5, *sfree = bar + 6,
-           *pready = bar + 7, *dqfull = bar + 8, *dqfree = bar + 9, *ldfull = bar + 10 /*[2]*/;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t *kvfull = bar, *sfull = bar + 1, *sfree = bar + 2, *pready = bar + 3, *dqfull = bar + 4,
+           *dqfree = bar + 5, *qfull = bar + 6 /*[kST]*/, *qempty = bar + 6 + kST /*[kST]*/,
+           *ldfull = bar + 6 + 2 * kST /*[kST]*/;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 6 + 3 * kST);
   float* sLD = reinterpret_cast<float*>(smem + Lay::LD);  // [2][sL 128 | sD 128]
 
   if (threadIdx.x == 0) {
     mbar_init(kvfull, 1);
-    for (int s = 0; s < 2; ++s) mbar_init(&qfull[s], 1), mbar_init(&qempty[s], 1);
+    for (int s = 0; s < kST; ++s) mbar_init(&qfull[s], 1), mbar_init(&qempty[s], 1), mbar_init(&ldfull[s], 32);
     mbar_init(sfull, 1);
     mbar_init(sfree, 256);
     mbar_init(pready, 256);
     mbar_init(dqfull, 1);
     mbar_init(dqfree, 256);
-    mbar_init(&ldfull[0], 32);
-    mbar_init(&ldfull[1], 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mQKV)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mO)) : "memory");
@@ -128,8 +129,8 @@ __global__ void __launch_bounds__(384, 1)
     }
     int h = kvh * grp, qt = kt;
     for (int it = 0; it < nit; ++it) {
-      const int st = it & 1, q0 = qt * kQ;
-      mbar_wait(&qempty[st], ((it >> 1) & 1) ^ 1);
+      const int st = it % kST, q0 = qt * kQ;
+      mbar_wait(&qempty[st], ((it / kST) & 1) ^ 1);
       if (lane == 0) {
         mbar_expect_tx(&qfull[st], 2 * kTile);
         tma_load_2d(smem + Lay::Q + st * kTile, &mQKV, &qfull[st], h * kHD, s0 + q0);
@@ -153,8 +154,8 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t I_SS = idesc(128, false, false), I_KM = idesc(64, false, true), I_MM = idesc(64, true, true);
       mbar_wait(kvfull, 0);
       auto issue_s = [&](int it) {
-        const int st = it & 1;
-        mbar_wait(&qfull[st], (it >> 1) & 1);
+        const int st = it % kST;
+        mbar_wait(&qfull[st], (it / kST) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t q = sQ + st * kTile, o = sO + st * kTile;
 #pragma unroll
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(384, 1)
       };
       issue_s(0);
       for (int it = 0; it < nit; ++it) {
-        const int st = it & 1;
+        const int st = it % kST;
         if (it + 1 < nit) {  // S(it+1) as soon as the softmax warps hold S(it) in registers
           mbar_wait(sfree, it & 1);
           issue_s(it + 1);
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(384, 1)
     const int ew = warp - 4, qq = ew & 3, hf = ew >> 2;
     const int key_l = qq * 32 + lane, key = k0 + key_l;
     const uint32_t lanes = static_cast<uint32_t>(qq * 32) << 16;
-    const uint32_t stg = smem_u32(smem + Lay::DQ + ew * 4096);
+    const uint32_t stg = smem_u32(smem + Lay::DQ + ew * 2048);
     // dQ of iteration `it` (rows q0 + 32 qq + lane, head columns hf*32 .. +31): TMEM ->
     // scale -> swizzled staging -> one bulk tensor reduce-add per warp. Call after
     // mbar_wait(dqfull, it & 1).
@@ -208,28 +209,34 @@ __global__ void __launch_bounds__(384, 1)
       mbar_arrive(dqfree);
 #pragma unroll
       for (int j = 0; j < 32; ++j) dq[j] *= scale;
-      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      __syncwarp();
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stg + lane * 128 + ((j ^ (lane & 7)) << 4)),
-                     "f"(dq[4 * j]), "f"(dq[4 * j + 1]), "f"(dq[4 * j + 2]), "f"(dq[4 * j + 3])
-                     : "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) {
-        asm volatile(
-            "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                reinterpret_cast<uint64_t>(&mDQ)),
-            "r"(stg), "r"(h * kHD + hf * 32), "r"(s0 + q0 + qq * 32)
-            : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      for (int half = 0; half < 2; ++half) {  // rows 0-15 of the warp, then 16-31 (a 16 x 32 box each)
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        if ((lane >> 4) == half) {
+          const int r = lane & 15;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stg + r * 128 + ((j ^ (r & 7)) << 4)),
+                         "f"(dq[4 * j]), "f"(dq[4 * j + 1]), "f"(dq[4 * j + 2]), "f"(dq[4 * j + 3])
+                         : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile(
+              "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                  reinterpret_cast<uint64_t>(&mDQ)),
+              "r"(stg), "r"(h * kHD + hf * 32), "r"(s0 + q0 + qq * 32 + half * 16)
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
       }
     };
     int h = kvh * grp, qt = kt, ph = 0, pq0 = 0;  // (head, tile) of this and of the previous iteration
     for (int it = 0; it < nit; ++it) {
-      const int st = it & 1, q0 = qt * kQ;
-      mbar_wait(&ldfull[st], (it >> 1) & 1);
+      const int st = it % kST, q0 = qt * kQ;
+      mbar_wait(&ldfull[st], (it / kST) & 1);
       const float* L = sLD + st * 256 + hf * 64;
       const float* D = L + 128;
       mbar_wait(sfull, it & 1);
@@ -312,7 +319,7 @@ bool attn_bwd_tc5(cudaStream_t s, const bf16* qkv, const bf16* dctx, const float
   CUtensorMap mq, mo, mdq;
   if (!tma_map_2d(&mq, qkv, rows, qkvd, qkvd, kHD, 128, false, 128, true) ||
       !tma_map_2d(&mo, dctx, rows, qd, qd, kHD, 128, false, 128, true) ||
-      !tma_map_2d(&mdq, dq32, rows, qd, qd, 32, 32, true, 128, false))
+      !tma_map_2d(&mdq, dq32, rows, qd, qd, 32, 16, true, 128, false))
     return false;
   static bool attr = false;
   if (!attr) {

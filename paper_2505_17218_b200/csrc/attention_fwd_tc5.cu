@@ -8,7 +8,7 @@
 //   O_j = P_j V_j          M128 N64  K128   A = P_j (K-major) B = V_j (MN-major)  -> TMEM O[j&1]
 //   registers: acc = acc * 2^(m_{j-1} - m_j) + O_j,  l likewise; out = acc / l, LSE = m + log l.
 // S and O are double-buffered in TMEM so the MMA of S_{j+1} and of O_j overlap the softmax.
-// Warp roles: 0 TMA producer (Q once, K/V two-stage ring), 1 MMA issuer, 2 TMEM allocator,
+// Warp roles: 0 TMA producer (Q once, K/V kST-stage ring), 1 MMA issuer, 2 TMEM allocator,
 // 4..7 softmax (one thread per query row; TMEM lane quarter = warp % 4).
 #include <cfloat>
 #include <cstdlib>
@@ -24,10 +24,12 @@ namespace {
 constexpr int kQ = 128, kKeys = 128, kHD = 64;
 constexpr int kTile = 128 * kHD * 2;  // 16 KB
 
+constexpr int kST = 4;  // K/V pipeline depth: loads run 3 key tiles ahead of the MMAs
+
 struct FLay {
-  static constexpr int Q = 0, K = kTile /*2 stages*/, V = 3 * kTile /*2 stages*/;
-  static constexpr int P = 5 * kTile;  // P [128 q x 128 keys] bf16: two 64-key swizzle atoms
-  static constexpr int BAR = 7 * kTile;
+  static constexpr int Q = 0, K = kTile /*kST stages*/, V = (1 + kST) * kTile /*kST stages*/;
+  static constexpr int P = (1 + 2 * kST) * kTile;  // P [128 q x 128 keys] bf16: two 64-key swizzle atoms
+  static constexpr int BAR = P + 2 * kTile;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
@@ -64,15 +66,18 @@ __global__ void __launch_bounds__(256, 1)
   const int nkt = qt + 1;  // causal key tiles 0 .. qt
 
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FLay::BAR);
-  uint64_t *qfull = bar, *kvfull = bar + 1 /*[2]*/, *kvempty = bar + 3 /*[2]*/, *sfull = bar + 5 /*[2]*/,
-           *sfree = bar + 7 /*[2]*/, *pready = bar + 9, *ofull = bar + 10 /*[2]*/, *ofree = bar + 12 /*[2]*/;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  uint64_t *qfull = bar, *sfull = bar + 1 /*[2]*/, *sfree = bar + 3 /*[2]*/, *pready = bar + 5,
+           *ofull = bar + 6 /*[2]*/, *ofree = bar + 8 /*[2]*/, *kvfull = bar + 10 /*[kST]*/,
+           *kvempty = bar + 10 + kST /*[kST]*/;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10 + 2 * kST);
 
   if (threadIdx.x == 0) {
     mbar_init(qfull, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kST; ++i) {
       mbar_init(&kvfull[i], 1);
       mbar_init(&kvempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&sfull[i], 1);
       mbar_init(&sfree[i], 128);
       mbar_init(&ofull[i], 1);
@@ -99,8 +104,8 @@ __global__ void __launch_bounds__(256, 1)
       mbar_expect_tx(qfull, kTile);
       tma_load_2d(smem + FLay::Q, &mQKV, qfull, h * kHD, s0 + q0);
       for (int j = 0; j < nkt; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kvempty[st], ((j >> 1) & 1) ^ 1);
+        const int st = j % kST;
+        mbar_wait(&kvempty[st], ((j / kST) & 1) ^ 1);
         mbar_expect_tx(&kvfull[st], 2 * kTile);
         tma_load_2d(smem + FLay::K + st * kTile, &mQKV, &kvfull[st], qd + kvh * kHD, s0 + j * kKeys);
         tma_load_2d(smem + FLay::V + st * kTile, &mQKV, &kvfull[st], qd + kvd + kvh * kHD, s0 + j * kKeys);
@@ -111,31 +116,31 @@ __global__ void __launch_bounds__(256, 1)
       constexpr uint32_t I_S = idesc(128, false, false), I_O = idesc(64, false, true);
       mbar_wait(qfull, 0);
       auto issue_s = [&](int j) {
-        const int st = j & 1;
-        if (j >= 2) mbar_wait(&sfree[st], ((j >> 1) - 1) & 1);  // softmax holds S_{j-2} in registers
-        mbar_wait(&kvfull[st], (j >> 1) & 1);
+        const int sb = j & 1, st = j % kST;
+        if (j >= 2) mbar_wait(&sfree[sb], ((j >> 1) - 1) & 1);  // softmax holds S_{j-2} in registers
+        mbar_wait(&kvfull[st], (j / kST) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t k = sK + st * kTile;
 #pragma unroll
         for (int kk = 0; kk < kHD / 16; ++kk)
-          umma_bf16(tmem + (st ? kTS1 : kTS0), smem_desc(sQ + kk * 32, 16, 1024), smem_desc(k + kk * 32, 16, 1024),
+          umma_bf16(tmem + (sb ? kTS1 : kTS0), smem_desc(sQ + kk * 32, 16, 1024), smem_desc(k + kk * 32, 16, 1024),
                     I_S, kk > 0);
-        umma_commit(&sfull[st]);
+        umma_commit(&sfull[sb]);
       };
       issue_s(0);
       for (int j = 0; j < nkt; ++j) {
-        const int st = j & 1;
+        const int sb = j & 1, st = j % kST;
         if (j + 1 < nkt) issue_s(j + 1);
         mbar_wait(pready, j & 1);
-        if (j >= 2) mbar_wait(&ofree[st], ((j >> 1) - 1) & 1);  // O_{j-2} read out
+        if (j >= 2) mbar_wait(&ofree[sb], ((j >> 1) - 1) & 1);  // O_{j-2} read out
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t v = sV + st * kTile;
 #pragma unroll
         for (int kk = 0; kk < kKeys / 16; ++kk)
-          umma_bf16(tmem + (st ? kTO1 : kTO0), smem_desc(sP + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024),
+          umma_bf16(tmem + (sb ? kTO1 : kTO0), smem_desc(sP + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024),
                     smem_desc(v + kk * 2048, kTile, 1024), I_O, kk > 0);
         umma_commit(&kvempty[st]);
-        umma_commit(&ofull[st]);
+        umma_commit(&ofull[sb]);
       }
     }
   } else if (warp >= 4) {  // ---------------------------------------------------------- softmax
@@ -170,13 +175,10 @@ __global__ void __launch_bounds__(256, 1)
       tmem_wait_ld();
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&sfree[st]);
-      float* sv = reinterpret_cast<float*>(sr);
+      float* sv = reinterpret_cast<float*>(sr);  // raw scores; 1/sqrt(d) * log2(e) goes into the exponent
       if (j == qt) {  // causal diagonal: key j*128 + c > q is masked
 #pragma unroll
-        for (int c = 0; c < kKeys; ++c) sv[c] = (j * kKeys + c <= q) ? sv[c] * scale_log2 : -FLT_MAX;
-      } else {
-#pragma unroll
-        for (int c = 0; c < kKeys; ++c) sv[c] *= scale_log2;
+        for (int c = 0; c < kKeys; ++c) sv[c] = (j * kKeys + c <= q) ? sv[c] : -FLT_MAX;
       }
       float t[16];
 #pragma unroll
@@ -189,12 +191,12 @@ __global__ void __launch_bounds__(256, 1)
       for (int w = 8; w >= 1; w >>= 1)
 #pragma unroll
         for (int i = 0; i < w; ++i) t[i] = fmaxf(t[i], t[i + w]);
-      const float m_new = fmaxf(m, t[0]);
+      const float m_new = fmaxf(m, t[0] * scale_log2);
       float rs[4] = {0.f, 0.f, 0.f, 0.f};
       uint32_t pk[kKeys / 2];
 #pragma unroll
       for (int c = 0; c < kKeys; c += 2) {
-        const float p0 = ex2(sv[c] - m_new), p1 = ex2(sv[c + 1] - m_new);
+        const float p0 = ex2(__fmaf_rn(sv[c], scale_log2, -m_new)), p1 = ex2(__fmaf_rn(sv[c + 1], scale_log2, -m_new));
         rs[(c >> 1) & 3] += p0 + p1;
         pk[c >> 1] = pack2(p0, p1);
       }
