@@ -249,6 +249,9 @@ bool attn_fwd_tc5(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int
   if (hd != kHD || nh % nkv) return false;
   const char* force = getenv("DASHCU_ATTN_FWD");
   if (force && std::string(force) == "mma") return false;
+  // one-tile sequences (the prompt prefill) amortise the per-CTA TMEM / barrier / first-load
+  // latency poorly; the mma.sync kernel (several CTAs per SM) is faster there
+  if (max_len <= 2 * kQ && !(force && std::string(force) == "tc5")) return false;
   const int qkvd = nh * hd + 2 * nkv * hd;
   CUtensorMap mq;
   if (!tma_map_2d(&mq, qkv, rows, qkvd, qkvd, kHD, 128, false, 128, true)) return false;

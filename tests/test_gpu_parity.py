@@ -264,7 +264,7 @@ def test_pg_gradient_parity_long_sequences(ctx, monkeypatch, kernel):
     kernels (forward and backward)."""
     if kernel == "mma":
         monkeypatch.setenv("DASHCU_ATTN_BWD", "mma")
-        monkeypatch.setenv("DASHCU_ATTN_FWD", "mma")
+    monkeypatch.setenv("DASHCU_ATTN_FWD", kernel)  # tc5 also below its 2-tile size threshold
     arch = LONGGQA
     pol = D.Policy(ctx, arch, D.BF16)
     p = params32(arch, 0.3, 10)

@@ -26,11 +26,18 @@ def main():
     w = np.full(n_seq, 1.0 / n_seq)
     pol.grad_zero()
     pol.accumulate_weighted(w, micro_batch=n_seq)   # warm-up (allocations)
-    D.profile_enable(keys=True)
-    D.profile_read(reset=True)
-    pol.accumulate_weighted(w, micro_batch=n_seq)
-    keys = D.profile_keys()
-    prof = D.profile_read(reset=True)
+    reps = int(os.environ.get("REPS", "3"))
+    best = None
+    for _ in range(reps):  # the fastest of a few runs (box-to-box clock variance is large)
+        D.profile_enable(keys=True)
+        D.profile_read(reset=True)
+        pol.accumulate_weighted(w, micro_batch=n_seq)
+        k_ = D.profile_keys()
+        p_ = D.profile_read(reset=True)
+        tot = sum(v["ms"] for v in p_.values())
+        if best is None or tot < best[0]:
+            best = (tot, k_, p_)
+    _, keys, prof = best
     D.profile_enable(())
     st = pol.stats()
     out = {k: {"ms": v["ms"], "launches": v["launches"], "tflops": v["flops"] / max(v["ms"], 1e-9) / 1e9}
