@@ -32,15 +32,16 @@ namespace {
 constexpr int kKeys = 128, kQ = 128, kHD = 64;
 constexpr int kTile = kKeys * kHD * 2;  // 16 KB: [128 rows x 64] bf16, 128-byte swizzle
 
-constexpr int kST = 3;  // Q / dO / (LSE, D) pipeline depth
-
+// ST: Q / dO / (LSE, D) pipeline depth; DQR: rows of the per-warp dQ staging box (32 = one
+// 4 KB bulk reduce per warp and iteration, 16 = two 2 KB reduces, freeing smem for a 3rd stage)
+template <int ST, int DQR>
 struct Lay {
-  static constexpr int K = 0, V = kTile, Q = 2 * kTile /*kST stages*/, O = (2 + kST) * kTile /*kST stages*/;
-  static constexpr int P = (2 + 2 * kST) * kTile;  // P^T  [128 keys x 128 q]: two 64-q swizzle atoms
-  static constexpr int S = P + 2 * kTile;           // dS^T [128 keys x 128 q]
-  static constexpr int DQ = S + 2 * kTile;          // 8 softmax warps x 2 KB dQ staging (16 x 32 fp32)
-  static constexpr int LD = DQ + 8 * 2048;          // per stage: sL[128], sD[128]
-  static constexpr int BAR = LD + kST * 1024;
+  static constexpr int K = 0, V = kTile, Q = 2 * kTile /*ST stages*/, O = (2 + ST) * kTile /*ST stages*/;
+  static constexpr int P = (2 + 2 * ST) * kTile;  // P^T  [128 keys x 128 q]: two 64-q swizzle atoms
+  static constexpr int S = P + 2 * kTile;          // dS^T [128 keys x 128 q]
+  static constexpr int DQ = S + 2 * kTile;         // 8 softmax warps x DQR x 32 fp32 dQ staging
+  static constexpr int LD = DQ + 8 * DQR * 128;    // per stage: sL[128], sD[128]
+  static constexpr int BAR = LD + ST * 1024;
   static constexpr int BYTES = BAR + 256 + 1024;  // + alignment slack
 };
 
@@ -63,16 +64,18 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// one 128-byte row (64 bf16) of a K-major swizzle atom: chunk j of row r at (j ^ (r & 7))
-__device__ __forceinline__ void st_row64(uint32_t atom, int r, const float* v) {
+// half a 128-byte row (32 bf16, chunks c0 .. c0+3) of a K-major swizzle atom: chunk j of
+// row r lives at (j ^ (r & 7))
+__device__ __forceinline__ void st_row32(uint32_t atom, int r, int c0, const float* v) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j)
-    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(atom + r * 128 + ((j ^ (r & 7)) << 4)),
+  for (int j = 0; j < 4; ++j)
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(atom + r * 128 + (((c0 + j) ^ (r & 7)) << 4)),
                  "r"(pack2(v[8 * j], v[8 * j + 1])), "r"(pack2(v[8 * j + 2], v[8 * j + 3])),
                  "r"(pack2(v[8 * j + 4], v[8 * j + 5])), "r"(pack2(v[8 * j + 6], v[8 * j + 7]))
                  : "memory");
 }
 
+template <int ST, int DQR>
 __global__ void __launch_bounds__(384, 1)
     attn_bwd_tc5_k(const __grid_constant__ CUtensorMap mQKV, const __grid_constant__ CUtensorMap mO,
                    const __grid_constant__ CUtensorMap mDQ, const int32_t* __restrict__ seq_start,
@@ -90,6 +93,8 @@ __global__ void __launch_bounds__(384, 1)
   const int nq = (n + kQ - 1) / kQ - kt;  // causal query tiles per head: kt .. last
   const int nit = grp * nq;
 
+  using Lay = dashcu::Lay<ST, DQR>;
+  constexpr int kST = ST;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR);
   uint64_t *kvfull = bar, *sfull = bar + 1, *sfree = bar + 2, *pready = bar + 3, *dqfull = bar + 4,
            *dqfree = bar + 5, *qfull = bar + 6 /*[kST]*/, *qempty = bar + 6 + kST /*[kST]*/,
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(384, 1)
     const int ew = warp - 4, qq = ew & 3, hf = ew >> 2;
     const int key_l = qq * 32 + lane, key = k0 + key_l;
     const uint32_t lanes = static_cast<uint32_t>(qq * 32) << 16;
-    const uint32_t stg = smem_u32(smem + Lay::DQ + ew * 2048);
+    const uint32_t stg = smem_u32(smem + Lay::DQ + ew * DQR * 128);
     // dQ of iteration `it` (rows q0 + 32 qq + lane, head columns hf*32 .. +31): TMEM ->
     // scale -> swizzled staging -> one bulk tensor reduce-add per warp. Call after
     // mbar_wait(dqfull, it & 1).
@@ -210,11 +215,11 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
       for (int j = 0; j < 32; ++j) dq[j] *= scale;
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {  // rows 0-15 of the warp, then 16-31 (a 16 x 32 box each)
+      for (int half = 0; half < 32 / DQR; ++half) {  // DQR-row boxes of the warp's 32 rows
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
-        if ((lane >> 4) == half) {
-          const int r = lane & 15;
+        if (lane / DQR == half) {
+          const int r = lane % DQR;
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stg + r * 128 + ((j ^ (r & 7)) << 4)),
@@ -227,7 +232,7 @@ __global__ void __launch_bounds__(384, 1)
           asm volatile(
               "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                   reinterpret_cast<uint64_t>(&mDQ)),
-              "r"(stg), "r"(h * kHD + hf * 32), "r"(s0 + q0 + qq * 32 + half * 16)
+              "r"(stg), "r"(h * kHD + hf * 32), "r"(s0 + q0 + qq * 32 + half * DQR)
               : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
@@ -241,40 +246,45 @@ __global__ void __launch_bounds__(384, 1)
       const float* D = L + 128;
       mbar_wait(sfull, it & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      uint32_t sr[64], dr[64];
-      tmem_ld32_async(tmem + lanes + kTS + hf * 64, sr);
-      tmem_ld32_async(tmem + lanes + kTS + hf * 64 + 32, sr + 32);
-      tmem_ld32_async(tmem + lanes + kTdP + hf * 64, dr);
-      tmem_ld32_async(tmem + lanes + kTdP + hf * 64 + 32, dr + 32);
-      tmem_wait_ld();
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(sfree);
-      float* sv = reinterpret_cast<float*>(sr);  // P^T and dS^T overwrite S^T / dP^T in place
-      float* dp = reinterpret_cast<float*>(dr);
       // masks only on the causal diagonal and at the sequence end (warp-uniform)
       const bool edge = qt == kt || q0 + kQ > n || k0 + kKeys > n;
+      // two 32-column halves keep 64 registers of scores live; the second half's TMEM loads
+      // release S^T / dP^T for the next iteration's MMAs
 #pragma unroll
-      for (int c = 0; c < 64; c += 4) {
-        const float4 l4 = *reinterpret_cast<const float4*>(L + c);
-        const float4 d4 = *reinterpret_cast<const float4*>(D + c);
-        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float p = ex2(__fmaf_rn(sv[c + e], scale_log2, -lv[e]));
-          if (edge) {
-            const int q = q0 + hf * 64 + c + e;
-            p = (q < n && key < n && key <= q) ? p : 0.f;
-          }
-          sv[c + e] = p;
-          dp[c + e] = p * (dp[c + e] - dv4[e]);  // 1/sqrt(d) is applied to dK / dQ at readout
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t sr[32], dr[32];
+        const uint32_t col = hf * 64 + hh * 32;
+        tmem_ld32_async(tmem + lanes + kTS + col, sr);
+        tmem_ld32_async(tmem + lanes + kTdP + col, dr);
+        tmem_wait_ld();
+        if (hh == 1) {
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          mbar_arrive(sfree);
         }
+        float* sv = reinterpret_cast<float*>(sr);  // P^T and dS^T overwrite S^T / dP^T in place
+        float* dp = reinterpret_cast<float*>(dr);
+#pragma unroll
+        for (int c = 0; c < 32; c += 4) {
+          const float4 l4 = *reinterpret_cast<const float4*>(L + hh * 32 + c);
+          const float4 d4 = *reinterpret_cast<const float4*>(D + hh * 32 + c);
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float p = ex2(__fmaf_rn(sv[c + e], scale_log2, -lv[e]));
+            if (edge) {
+              const int q = q0 + col + c + e;
+              p = (q < n && key < n && key <= q) ? p : 0.f;
+            }
+            sv[c + e] = p;
+            dp[c + e] = p * (dp[c + e] - dv4[e]);  // 1/sqrt(d) is applied to dK / dQ at readout
+          }
+        }
+        // the MMAs of it-1 are complete (dQ ready, P^T / dS^T no longer read) before the
+        // operands are overwritten; TMEM dQ is rewritten only after dqfree
+        if (hh == 0 && it > 0) mbar_wait(dqfull, (it - 1) & 1);
+        st_row32(sP + hf * kTile, key_l, hh * 4, sv);
+        st_row32(sS + hf * kTile, key_l, hh * 4, dp);
       }
-      // the MMAs of it-1 are complete (dQ ready, P^T / dS^T no longer read): overwrite the
-      // operands, release the next MMAs, then read dQ(it-1) out (TMEM dQ is rewritten only
-      // after dqfree)
-      if (it > 0) mbar_wait(dqfull, (it - 1) & 1);
-      st_row64(sP + hf * kTile, key_l, sv);
-      st_row64(sS + hf * kTile, key_l, dp);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(pready);
       if (it > 0) dq_out(ph, pq0);
@@ -309,6 +319,24 @@ __global__ void __launch_bounds__(384, 1)
 
 }  // namespace
 
+namespace {
+template <int ST, int DQR>
+void launch_bwd_tc5(cudaStream_t s, const CUtensorMap& mq, const CUtensorMap& mo, const CUtensorMap& mdq,
+                    const int32_t* seq_start, const float* lse, const float* Dbuf, int n_seq, int max_len, int nh,
+                    int nkv, float* dkv32, float sc) {
+  auto k = attn_bwd_tc5_k<ST, DQR>;
+  static bool attr = false;
+  if (!attr) {
+    DCU_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay<ST, DQR>::BYTES));
+    attr = true;
+  }
+  dim3 grid(n_seq * nkv, (max_len + kKeys - 1) / kKeys);
+  k<<<grid, 384, Lay<ST, DQR>::BYTES, s>>>(mq, mo, mdq, seq_start, lse, Dbuf, nh, nkv, dkv32, sc,
+                                             sc * 1.4426950408889634f);
+  DCU_LAUNCHED();
+}
+}  // namespace
+
 bool attn_bwd_tc5(cudaStream_t s, const bf16* qkv, const bf16* dctx, const float* lse, const float* Dbuf,
                   const int32_t* seq_start, int n_seq, int max_len, int rows, int nh, int nkv, int hd, float* dq32,
                   float* dkv32) {
@@ -316,21 +344,20 @@ bool attn_bwd_tc5(cudaStream_t s, const bf16* qkv, const bf16* dctx, const float
   const char* force = getenv("DASHCU_ATTN_BWD");
   if (force && std::string(force) == "mma") return false;
   const int qd = nh * hd, qkvd = qd + 2 * nkv * hd;
-  CUtensorMap mq, mo, mdq;
+  CUtensorMap mq, mo, mdq, mdq16;
   if (!tma_map_2d(&mq, qkv, rows, qkvd, qkvd, kHD, 128, false, 128, true) ||
       !tma_map_2d(&mo, dctx, rows, qd, qd, kHD, 128, false, 128, true) ||
-      !tma_map_2d(&mdq, dq32, rows, qd, qd, 32, 16, true, 128, false))
+      !tma_map_2d(&mdq, dq32, rows, qd, qd, 32, 32, true, 128, false) ||
+      !tma_map_2d(&mdq16, dq32, rows, qd, qd, 32, 16, true, 128, false))
     return false;
-  static bool attr = false;
-  if (!attr) {
-    DCU_CHECK(cudaFuncSetAttribute(attn_bwd_tc5_k, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::BYTES));
-    attr = true;
-  }
   const float sc = 1.f / sqrtf(static_cast<float>(hd));
-  dim3 grid(n_seq * nkv, (max_len + kKeys - 1) / kKeys);
-  attn_bwd_tc5_k<<<grid, 384, Lay::BYTES, s>>>(mq, mo, mdq, seq_start, lse, Dbuf, nh, nkv, dkv32, sc,
-                                               sc * 1.4426950408889634f);
-  DCU_LAUNCHED();
+  // pipeline variant (DASHCU_ATTN_BWD_CFG): "3x16" = 3 Q/dO stages + 16-row dQ boxes,
+  // default 2 stages + 32-row boxes
+  const char* cfg = getenv("DASHCU_ATTN_BWD_CFG");
+  if (cfg && std::string(cfg) == "3x16")
+    launch_bwd_tc5<3, 16>(s, mq, mo, mdq16, seq_start, lse, Dbuf, n_seq, max_len, nh, nkv, dkv32, sc);
+  else
+    launch_bwd_tc5<2, 32>(s, mq, mo, mdq, seq_start, lse, Dbuf, n_seq, max_len, nh, nkv, dkv32, sc);
   return true;
 }
 
