@@ -1,8 +1,9 @@
 // tcgen05 attention forward for head_dim 64 (teacher-forced causal attention of the
 // training pass, policy.cpp:105-129; the mma.sync kernel in attention_tc.cu is the fallback).
 //
-// One CTA owns 128 queries of one (sequence, query head) and walks the causal key tiles
-// (128 keys each) with an online softmax:
+// One CTA owns 128 queries of one sequence for every query head of a KV group (heads run
+// back to back through one pipeline) and walks the causal key tiles (128 keys each) with an
+// online softmax:
 //   S_j = Q K_j^T          M128 N128 K64    A = Q (K-major)   B = K_j (K-major)   -> TMEM S[j&1]
 //   softmax warps: m_j = max(m_{j-1}, rowmax(S_j)/sqrt(d)), P_j = exp(S_j/sqrt(d) - m_j) (bf16, smem)
 //   O_j = P_j V_j          M128 N64  K128   A = P_j (K-major) B = V_j (MN-major)  -> TMEM O[j&1]
@@ -27,8 +28,8 @@ constexpr int kTile = 128 * kHD * 2;  // 16 KB
 constexpr int kST = 4;  // K/V pipeline depth: loads run 3 key tiles ahead of the MMAs
 
 struct FLay {
-  static constexpr int Q = 0, K = kTile /*kST stages*/, V = (1 + kST) * kTile /*kST stages*/;
-  static constexpr int P = (1 + 2 * kST) * kTile;  // P [128 q x 128 keys] bf16: two 64-key swizzle atoms
+  static constexpr int Q = 0 /*2 stages*/, K = 2 * kTile /*kST stages*/, V = (2 + kST) * kTile /*kST stages*/;
+  static constexpr int P = (2 + 2 * kST) * kTile;  // P [128 q x 128 keys] bf16: two 64-key swizzle atoms
   static constexpr int BAR = P + 2 * kTile;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
@@ -56,28 +57,33 @@ __global__ void __launch_bounds__(256, 1)
                    int nqt_max, bf16* __restrict__ ctx, float* __restrict__ lse, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // grid (sequence x head, query tile), the longest (last) query tiles launched first
-  const int sq = blockIdx.x / nh, h = blockIdx.x % nh, qt = nqt_max - 1 - static_cast<int>(blockIdx.y);
+  // grid (sequence x KV head, query tile), the longest (last) query tiles launched first; the
+  // CTA runs the tile for every query head of the KV group back to back, so the TMEM / barrier
+  // set-up and the pipeline fill are paid once per group and K/V loads of the next head
+  // stream in while the current head finishes
+  const int sq = blockIdx.x / nkv, kvh = blockIdx.x % nkv, qt = nqt_max - 1 - static_cast<int>(blockIdx.y);
   const int s0 = seq_start[sq], n = seq_start[sq + 1] - s0;
   const int q0 = qt * kQ;
   if (q0 >= n) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = nh / nkv, kvh = h / grp, qd = nh * kHD, kvd = nkv * kHD;
-  const int nkt = qt + 1;  // causal key tiles 0 .. qt
+  const int grp = nh / nkv, qd = nh * kHD, kvd = nkv * kHD;
+  const int nkt = qt + 1;         // causal key tiles 0 .. qt per head
+  const int ntiles = grp * nkt;   // global tile counter t = head * nkt + key tile
 
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FLay::BAR);
-  uint64_t *qfull = bar, *sfull = bar + 1 /*[2]*/, *sfree = bar + 3 /*[2]*/, *pready = bar + 5,
-           *ofull = bar + 6 /*[2]*/, *ofree = bar + 8 /*[2]*/, *kvfull = bar + 10 /*[kST]*/,
-           *kvempty = bar + 10 + kST /*[kST]*/;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10 + 2 * kST);
+  uint64_t *qfull = bar /*[2]*/, *qempty = bar + 2 /*[2]*/, *sfull = bar + 4 /*[2]*/, *sfree = bar + 6 /*[2]*/,
+           *pready = bar + 8, *ofull = bar + 9 /*[2]*/, *ofree = bar + 11 /*[2]*/, *kvfull = bar + 13 /*[kST]*/,
+           *kvempty = bar + 13 + kST /*[kST]*/;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13 + 2 * kST);
 
   if (threadIdx.x == 0) {
-    mbar_init(qfull, 1);
     for (int i = 0; i < kST; ++i) {
       mbar_init(&kvfull[i], 1);
       mbar_init(&kvempty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&qfull[i], 1);
+      mbar_init(&qempty[i], 1);
       mbar_init(&sfull[i], 1);
       mbar_init(&sfree[i], 128);
       mbar_init(&ofull[i], 1);
@@ -101,38 +107,43 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------------------------------------------------------- TMA
-      mbar_expect_tx(qfull, kTile);
-      tma_load_2d(smem + FLay::Q, &mQKV, qfull, h * kHD, s0 + q0);
-      for (int j = 0; j < nkt; ++j) {
-        const int st = j % kST;
-        mbar_wait(&kvempty[st], ((j / kST) & 1) ^ 1);
-        mbar_expect_tx(&kvfull[st], 2 * kTile);
-        tma_load_2d(smem + FLay::K + st * kTile, &mQKV, &kvfull[st], qd + kvh * kHD, s0 + j * kKeys);
-        tma_load_2d(smem + FLay::V + st * kTile, &mQKV, &kvfull[st], qd + kvd + kvh * kHD, s0 + j * kKeys);
+      for (int hh = 0, t = 0; hh < grp; ++hh) {
+        const int qs = hh & 1;
+        mbar_wait(&qempty[qs], ((hh >> 1) & 1) ^ 1);
+        mbar_expect_tx(&qfull[qs], kTile);
+        tma_load_2d(smem + FLay::Q + qs * kTile, &mQKV, &qfull[qs], (kvh * grp + hh) * kHD, s0 + q0);
+        for (int j = 0; j < nkt; ++j, ++t) {
+          const int st = t % kST;
+          mbar_wait(&kvempty[st], ((t / kST) & 1) ^ 1);
+          mbar_expect_tx(&kvfull[st], 2 * kTile);
+          tma_load_2d(smem + FLay::K + st * kTile, &mQKV, &kvfull[st], qd + kvh * kHD, s0 + j * kKeys);
+          tma_load_2d(smem + FLay::V + st * kTile, &mQKV, &kvfull[st], qd + kvd + kvh * kHD, s0 + j * kKeys);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------------------------------------------------------- MMA
       constexpr uint32_t I_S = idesc(128, false, false), I_O = idesc(64, false, true);
-      mbar_wait(qfull, 0);
-      auto issue_s = [&](int j) {
-        const int sb = j & 1, st = j % kST;
-        if (j >= 2) mbar_wait(&sfree[sb], ((j >> 1) - 1) & 1);  // softmax holds S_{j-2} in registers
-        mbar_wait(&kvfull[st], (j / kST) & 1);
+      auto issue_s = [&](int t) {
+        const int sb = t & 1, st = t % kST, hh = t / nkt, j = t % nkt, qs = hh & 1;
+        if (t >= 2) mbar_wait(&sfree[sb], ((t >> 1) - 1) & 1);  // softmax holds S_{t-2} in registers
+        if (j == 0) mbar_wait(&qfull[qs], (hh >> 1) & 1);
+        mbar_wait(&kvfull[st], (t / kST) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t k = sK + st * kTile;
+        const uint32_t k = sK + st * kTile, qa = sQ + qs * kTile;
 #pragma unroll
         for (int kk = 0; kk < kHD / 16; ++kk)
-          umma_bf16(tmem + (sb ? kTS1 : kTS0), smem_desc(sQ + kk * 32, 16, 1024), smem_desc(k + kk * 32, 16, 1024),
+          umma_bf16(tmem + (sb ? kTS1 : kTS0), smem_desc(qa + kk * 32, 16, 1024), smem_desc(k + kk * 32, 16, 1024),
                     I_S, kk > 0);
         umma_commit(&sfull[sb]);
+        if (j == nkt - 1) umma_commit(&qempty[qs]);  // the head's last S: its Q tile is free
       };
       issue_s(0);
-      for (int j = 0; j < nkt; ++j) {
-        const int sb = j & 1, st = j % kST;
-        if (j + 1 < nkt) issue_s(j + 1);
-        mbar_wait(pready, j & 1);
-        if (j >= 2) mbar_wait(&ofree[sb], ((j >> 1) - 1) & 1);  // O_{j-2} read out
+      for (int t = 0; t < ntiles; ++t) {
+        const int sb = t & 1, st = t % kST;
+        if (t + 1 < ntiles) issue_s(t + 1);
+        mbar_wait(pready, t & 1);
+        if (t >= 2) mbar_wait(&ofree[sb], ((t >> 1) - 1) & 1);  // O_{t-2} read out
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t v = sV + st * kTile;
 #pragma unroll
@@ -147,94 +158,96 @@ __global__ void __launch_bounds__(256, 1)
     const int qq = warp & 3, r = qq * 32 + lane, q = q0 + r;
     const uint32_t lanes = static_cast<uint32_t>(qq * 32) << 16;
     float acc[kHD];
-#pragma unroll
-    for (int i = 0; i < kHD; ++i) acc[i] = 0.f;
-    float m = -FLT_MAX, m_prev = -FLT_MAX, l = 0.f;
-    // O_j (TMEM) into the register accumulator: acc = acc * 2^(m_old - m_new) + O_j
-    auto take_o = [&](int j, float m_old, float m_new) {
-      const int st = j & 1;
-      mbar_wait(&ofull[st], (j >> 1) & 1);
+    float m, m_prev, l;
+    // O_t (TMEM) into the register accumulator: acc = acc * 2^(m_old - m_new) + O_t
+    auto take_o = [&](int t, float m_old, float m_new) {
+      const int sb = t & 1;
+      mbar_wait(&ofull[sb], (t >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       uint32_t o[kHD];
-      tmem_ld32_async(tmem + lanes + (st ? kTO1 : kTO0), o);
-      tmem_ld32_async(tmem + lanes + (st ? kTO1 : kTO0) + 32, o + 32);
+      tmem_ld32_async(tmem + lanes + (sb ? kTO1 : kTO0), o);
+      tmem_ld32_async(tmem + lanes + (sb ? kTO1 : kTO0) + 32, o + 32);
       tmem_wait_ld();
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(&ofree[st]);
+      mbar_arrive(&ofree[sb]);
       const float c = ex2(m_old - m_new);
 #pragma unroll
       for (int i = 0; i < kHD; ++i) acc[i] = __fmaf_rn(acc[i], c, __uint_as_float(o[i]));
     };
-    for (int j = 0; j < nkt; ++j) {
-      const int st = j & 1;
-      mbar_wait(&sfull[st], (j >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      uint32_t sr[kKeys];
+    for (int hh = 0, t = 0; hh < grp; ++hh) {
+      const int h = kvh * grp + hh;
 #pragma unroll
-      for (int c = 0; c < kKeys; c += 32) tmem_ld32_async(tmem + lanes + (st ? kTS1 : kTS0) + c, sr + c);
-      tmem_wait_ld();
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(&sfree[st]);
-      float* sv = reinterpret_cast<float*>(sr);  // raw scores; 1/sqrt(d) * log2(e) goes into the exponent
-      if (j == qt) {  // causal diagonal: key j*128 + c > q is masked
+      for (int i = 0; i < kHD; ++i) acc[i] = 0.f;
+      m = -FLT_MAX, m_prev = -FLT_MAX, l = 0.f;
+      for (int j = 0; j < nkt; ++j, ++t) {
+        const int sb = t & 1;
+        mbar_wait(&sfull[sb], (t >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        uint32_t sr[kKeys];
 #pragma unroll
-        for (int c = 0; c < kKeys; ++c) sv[c] = (j * kKeys + c <= q) ? sv[c] : -FLT_MAX;
+        for (int c = 0; c < kKeys; c += 32) tmem_ld32_async(tmem + lanes + (sb ? kTS1 : kTS0) + c, sr + c);
+        tmem_wait_ld();
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(&sfree[sb]);
+        float* sv = reinterpret_cast<float*>(sr);  // raw scores; 1/sqrt(d) * log2(e) goes into the exponent
+        if (j == qt) {  // causal diagonal: key j*128 + c > q is masked
+#pragma unroll
+          for (int c = 0; c < kKeys; ++c) sv[c] = (j * kKeys + c <= q) ? sv[c] : -FLT_MAX;
+        }
+        float tm[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          tm[i] = sv[i];
+#pragma unroll
+          for (int k = 1; k < 8; ++k) tm[i] = fmaxf(tm[i], sv[i + 16 * k]);
+        }
+#pragma unroll
+        for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+          for (int i = 0; i < w; ++i) tm[i] = fmaxf(tm[i], tm[i + w]);
+        const float m_new = fmaxf(m, tm[0] * scale_log2);
+        float rs[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[kKeys / 2];
+#pragma unroll
+        for (int c = 0; c < kKeys; c += 2) {
+          const float p0 = ex2(__fmaf_rn(sv[c], scale_log2, -m_new));
+          const float p1 = ex2(__fmaf_rn(sv[c + 1], scale_log2, -m_new));
+          rs[(c >> 1) & 3] += p0 + p1;
+          pk[c >> 1] = pack2(p0, p1);
+        }
+        l = l * ex2(m - m_new) + ((rs[0] + rs[1]) + (rs[2] + rs[3]));
+        // P_t overwrites P_{t-1}: the MMA of O_{t-1} must be complete
+        if (t > 0) mbar_wait(&ofull[(t - 1) & 1], ((t - 1) >> 1) & 1);
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sP + a * kTile + r * 128 +
+                                                                           ((ch ^ (r & 7)) << 4)),
+                         "r"(pk[a * 32 + ch * 4]), "r"(pk[a * 32 + ch * 4 + 1]), "r"(pk[a * 32 + ch * 4 + 2]),
+                         "r"(pk[a * 32 + ch * 4 + 3])
+                         : "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(pready);
+        if (j > 0) take_o(t - 1, m_prev, m);
+        m_prev = m;
+        m = m_new;
       }
-      float t[16];
+      take_o(t - 1, m_prev, m);
+      if (q < n) {
+        const float inv = 1.f / l;
+        bf16* out = ctx + static_cast<int64_t>(s0 + q) * qd + h * kHD;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        t[i] = sv[i];
-#pragma unroll
-        for (int k = 1; k < 8; ++k) t[i] = fmaxf(t[i], sv[i + 16 * k]);
+        for (int i = 0; i < kHD; i += 8) {
+          uint4 v;
+          v.x = pack2(acc[i] * inv, acc[i + 1] * inv);
+          v.y = pack2(acc[i + 2] * inv, acc[i + 3] * inv);
+          v.z = pack2(acc[i + 4] * inv, acc[i + 5] * inv);
+          v.w = pack2(acc[i + 6] * inv, acc[i + 7] * inv);
+          *reinterpret_cast<uint4*>(out + i) = v;
+        }
+        lse[static_cast<int64_t>(s0 + q) * nh + h] = (m + __log2f(l)) * 0.6931471805599453f;
       }
-#pragma unroll
-      for (int w = 8; w >= 1; w >>= 1)
-#pragma unroll
-        for (int i = 0; i < w; ++i) t[i] = fmaxf(t[i], t[i + w]);
-      const float m_new = fmaxf(m, t[0] * scale_log2);
-      float rs[4] = {0.f, 0.f, 0.f, 0.f};
-      uint32_t pk[kKeys / 2];
-#pragma unroll
-      for (int c = 0; c < kKeys; c += 2) {
-        const float p0 = ex2(__fmaf_rn(sv[c], scale_log2, -m_new)), p1 = ex2(__fmaf_rn(sv[c + 1], scale_log2, -m_new));
-        rs[(c >> 1) & 3] += p0 + p1;
-        pk[c >> 1] = pack2(p0, p1);
-      }
-      l = l * ex2(m - m_new) + ((rs[0] + rs[1]) + (rs[2] + rs[3]));
-      // P_j overwrites P_{j-1}: the MMA of O_{j-1} must be complete
-      if (j > 0) {
-        const int sp = (j - 1) & 1;
-        mbar_wait(&ofull[sp], ((j - 1) >> 1) & 1);
-      }
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int ch = 0; ch < 8; ++ch)
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sP + a * kTile + r * 128 +
-                                                                         ((ch ^ (r & 7)) << 4)),
-                       "r"(pk[a * 32 + ch * 4]), "r"(pk[a * 32 + ch * 4 + 1]), "r"(pk[a * 32 + ch * 4 + 2]),
-                       "r"(pk[a * 32 + ch * 4 + 3])
-                       : "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(pready);
-      if (j > 0) take_o(j - 1, m_prev, m);
-      m_prev = m;
-      m = m_new;
-    }
-    take_o(nkt - 1, m_prev, m);
-    if (q < n) {
-      const float inv = 1.f / l;
-      bf16* out = ctx + static_cast<int64_t>(s0 + q) * qd + h * kHD;
-#pragma unroll
-      for (int i = 0; i < kHD; i += 8) {
-        uint4 v;
-        v.x = pack2(acc[i] * inv, acc[i + 1] * inv);
-        v.y = pack2(acc[i + 2] * inv, acc[i + 3] * inv);
-        v.z = pack2(acc[i + 4] * inv, acc[i + 5] * inv);
-        v.w = pack2(acc[i + 6] * inv, acc[i + 7] * inv);
-        *reinterpret_cast<uint4*>(out + i) = v;
-      }
-      lse[static_cast<int64_t>(s0 + q) * nh + h] = (m + __log2f(l)) * 0.6931471805599453f;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -261,7 +274,7 @@ bool attn_fwd_tc5(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int
     attr = true;
   }
   const int nqt = (max_len + kQ - 1) / kQ;
-  dim3 grid(n_seq * nh, nqt);
+  dim3 grid(n_seq * nkv, nqt);
   attn_fwd_tc5_k<<<grid, 256, FLay::BYTES, s>>>(mq, seq_start, nh, nkv, nqt, ctx, lse,
                                                 1.4426950408889634f / sqrtf(static_cast<float>(hd)));
   DCU_LAUNCHED();
