@@ -1012,21 +1012,26 @@ void launch2(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const
 }
 
 int use_pair_default() {
-  static int v = -2;
-  if (v == -2) {
-    const char* s = getenv("DASHCU_GEMM_PAIR");
-    v = s ? atoi(s) : 0;
-  }
-  return v;
+  const char* s = getenv("DASHCU_GEMM_PAIR");
+  return s ? atoi(s) : 0;
 }
 
 }  // namespace
 
 // cta_group::2 GEMM for 256-row-multiple-friendly shapes. Returns false if not TMA-legal.
-bool gemm_tc_pair(cudaStream_t s, const GemmShape& g, const Epi& e) {
+template <int BN, int STAGES>
+void dispatch_pair(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& om, const GemmShape& g,
+                   const Epi& e) {
+  if (g.a_kmajor && g.b_kmajor) launch2<BN, STAGES, true, true>(s, ma, mb, om, g, e);
+  else if (g.a_kmajor) launch2<BN, STAGES, true, false>(s, ma, mb, om, g, e);
+  else if (g.b_kmajor) launch2<BN, STAGES, false, true>(s, ma, mb, om, g, e);
+  else launch2<BN, STAGES, false, false>(s, ma, mb, om, g, e);
+}
+
+// cta_group::2 GEMM with 256 x BN tiles (BN 256 or 128). Returns false if not TMA-legal.
+bool gemm_tc_pair(cudaStream_t s, const GemmShape& g, const Epi& e, int BN) {
   if (!legal(g)) return false;
   CUtensorMap ma, mb;
-  constexpr int BN = 256;
   bool ok = g.a_kmajor ? make_map(&ma, g.A, g.M, g.K, g.lda, BK, 128) : make_map(&ma, g.A, g.K, g.M, g.lda, 64, BK);
   ok = ok && (g.b_kmajor ? make_map(&mb, g.B, g.N, g.K, g.ldb, BK, BN / 2) : make_map(&mb, g.B, g.K, g.N, g.ldb, 64, BK));
   if (!ok) return false;
@@ -1034,10 +1039,8 @@ bool gemm_tc_pair(cudaStream_t s, const GemmShape& g, const Epi& e) {
   memset(&om, 0, sizeof(om));
   Epi et = e;
   et.tma = out_maps_for(g, e, &om);
-  if (g.a_kmajor && g.b_kmajor) launch2<BN, 6, true, true>(s, ma, mb, om, g, et);
-  else if (g.a_kmajor) launch2<BN, 6, true, false>(s, ma, mb, om, g, et);
-  else if (g.b_kmajor) launch2<BN, 6, false, true>(s, ma, mb, om, g, et);
-  else launch2<BN, 6, false, false>(s, ma, mb, om, g, et);
+  if (BN == 256) dispatch_pair<256, 6>(s, ma, mb, om, g, et);  // 6 x 32 KB stages
+  else dispatch_pair<128, 8>(s, ma, mb, om, g, et);            // 8 x 24 KB stages
   return true;
 }
 
@@ -1051,8 +1054,11 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e) {
   const double r128 = std::ceil(tm * ((g.N + 127) / 128) / sms);
   const double r256 = std::ceil(tm * ((g.N + 255) / 256) / sms);
   const double rpair = std::ceil(tm2 * ((g.N + 255) / 256) / std::floor(sms / 2));
+  const double rpair128 = std::ceil(tm2 * ((g.N + 127) / 128) / std::floor(sms / 2));
   double c128 = r128 * 0.5 / 0.76, c256 = r256;
-  const double cpair = rpair / 1.12;
+  // the 256 x 128 pair tile stages as many shared-memory bytes per MMA as the 128 x 256
+  // single-CTA tile (efficiency ~1.0) with half its N granularity
+  const double cpair = rpair / 1.12, cpair128 = rpair128 * 0.5;
   // Split-K for accumulating GEMMs with few output tiles (weight gradients over a long
   // token axis): S K slices per tile fill the machine; each extra slice costs one more
   // ordered fp32 reduce of the tile (~3%). Slices keep >= 16 k-blocks.
@@ -1070,8 +1076,13 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e) {
     split128 = best(tm * ((g.N + 127) / 128), 0.5 / 0.76, &c128);
     split256 = best(tm * ((g.N + 255) / 256), 1.0, &c256);
   }
-  const int forced = use_pair_default();  // DASHCU_GEMM_PAIR: 1 force pair, 0 model, -1 never
-  if (forced != -1 && (forced == 1 || (cpair < c256 && cpair < c128)) && gemm_tc_pair(s, g, e)) return true;
+  // DASHCU_GEMM_PAIR: 1 force the 256x256 pair, 2 force the 256x128 pair, 0 model, -1 never
+  const int forced = use_pair_default();
+  if (forced != -1) {
+    const bool p256 = forced == 1 || (forced == 0 && cpair < c256 && cpair < c128 && cpair <= cpair128);
+    const bool p128 = forced == 2 || (forced == 0 && !p256 && cpair128 < c256 && cpair128 < c128);
+    if ((p256 && gemm_tc_pair(s, g, e, 256)) || (p128 && gemm_tc_pair(s, g, e, 128))) return true;
+  }
   const bool wide = c256 <= c128;
   const int BN = wide ? 256 : 128;
   CUtensorMap ma, mb;

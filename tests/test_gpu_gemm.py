@@ -115,3 +115,20 @@ def test_split_k_accumulate(ctx, monkeypatch, shape):
     monkeypatch.setenv("DASHCU_NO_SPLITK", "1")
     c = ctx.selftest_gemm(A, False, B, False, M, N, K, epi=3, C_init=c0)
     assert np.abs(a - c).max() <= 1e-5 * np.abs(ref).max() + 1e-3
+
+
+@pytest.mark.parametrize("pair", ["1", "2"])
+@pytest.mark.parametrize("ak,bk", [(True, True), (True, False), (False, True), (False, False)])
+@pytest.mark.parametrize("shape", [(256, 128, 64), (300, 200, 136), (4096, 896, 896), (1000, 1152, 320)])
+def test_cta_pair_tiles(ctx, monkeypatch, pair, ak, bk, shape):
+    """The cta_group::2 kernel with 256x256 (pair=1) and 256x128 (pair=2) tiles, forced."""
+    monkeypatch.setenv("DASHCU_GEMM_PAIR", pair)
+    M, N, K = shape
+    rng = np.random.default_rng(M + N + K)
+    A = bf16_bits(rng.standard_normal((M, K)).astype(np.float32))
+    B = bf16_bits(rng.standard_normal((N, K)).astype(np.float32))
+    ref = bits_to_f32(A).astype(np.float64) @ bits_to_f32(B).astype(np.float64).T
+    Ast = A if ak else np.ascontiguousarray(A.T)
+    Bst = B if bk else np.ascontiguousarray(B.T)
+    got = ctx.selftest_gemm(Ast, ak, Bst, bk, M, N, K)
+    assert np.abs(got - ref).max() / max(1.0, np.abs(ref).max()) < 1e-5
