@@ -35,6 +35,8 @@ __global__ void __launch_bounds__(DecCfg<HD>::NW * 32)
                      float scale_log2) {
   using Cf = DecCfg<HD>;
   constexpr int KC = Cf::KC, ST = Cf::ST, UNITS = Cf::UNITS;
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * Cf::NW + warp;
@@ -208,8 +210,8 @@ void launch_decode(cudaStream_t s, const bf16* qkv, const bf16* kp, const bf16* 
   }
   const int items = rows * nkv;
   const float scale_log2 = kLog2e / sqrtf(static_cast<float>(HD));
-  attn_decode_tc_k<HD><<<(items + Cf::NW - 1) / Cf::NW, Cf::NW * 32, Cf::SMEM, s>>>(
-      qkv, kp, vp, kc, vc, plen, rows, G, pmax, n_comp, cslots, nh, nkv, ctx, scale_log2);
+  launch_pdl(attn_decode_tc_k<HD>, dim3((items + Cf::NW - 1) / Cf::NW), dim3(Cf::NW * 32), Cf::SMEM, s, qkv, kp, vp, kc,
+             vc, plen, rows, G, pmax, n_comp, cslots, nh, nkv, ctx, scale_log2);
   DCU_LAUNCHED();
 }
 

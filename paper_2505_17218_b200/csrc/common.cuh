@@ -5,8 +5,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 namespace dashcu {
 
@@ -36,6 +38,36 @@ extern int64_t g_launches;
     ++::dashcu::g_launches; \
     DCU_CHECK(cudaGetLastError()); \
   } while (0)
+
+// Programmatic dependent launch (PDL). Kernels launched with launch_pdl may start (on SMs
+// the previous kernel has left) while it is still finishing: everything before pdl_wait()
+// (barrier init, TMEM allocation, tensor-map prefetch) overlaps the previous kernel's tail;
+// pdl_wait() blocks until the previous grid has completed and its writes are visible, so
+// it must precede every global read of upstream data and every global write. pdl_trigger()
+// lets the next kernel be scheduled early (its CTAs still wait in its own pdl_wait()).
+// DASHCU_NO_PDL=1 launches everything fully serialised.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  const char* s = getenv("DASHCU_NO_PDL");
+  return !(s && s[0] == '1');
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  DCU_CHECK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
 
 // Kernel-class profiler: when a class is enabled, its launches are bracketed by
 // CUDA events on the launching stream and charged with their ALGORITHMIC flops

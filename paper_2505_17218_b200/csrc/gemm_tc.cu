@@ -557,6 +557,8 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();     // set-up above overlapped the previous kernel; its outputs are visible now
+  pdl_trigger();  // the next kernel may take SMs as this grid's CTAs finish
 
   if (warp == 0) {
     if (lane == 0) {
@@ -740,7 +742,7 @@ void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const 
   if (ps.keyed())
     snprintf(ps.key, sizeof(ps.key), "mode%d 128x%d M%d N%d K%d %c%c epi%d split%d", MODE, BN, g.M, g.N, g.K,
              AK ? 'k' : 'm', BKM ? 'k' : 'm', e.kind, MODE == 0 ? e.splits : 1);
-  k<<<grid, C::THREADS, C::SMEM, s>>>(ma, mb, om, g, e, sa);
+  launch_pdl(k, dim3(grid), dim3(C::THREADS), C::SMEM, s, ma, mb, om, g, e, sa);
   DCU_LAUNCHED();
 }
 
@@ -880,6 +882,8 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
   cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive / TMA
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();     // set-up above overlapped the previous kernel; its outputs are visible now
+  pdl_trigger();  // the next kernel may take SMs as this grid's CTAs finish
 
   if (warp == 0) {
     if (lane == 0) {
@@ -996,13 +1000,15 @@ void launch2(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const
   cfg.blockDim = dim3(C::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute attr_c[1];
+  cudaLaunchAttribute attr_c[2];
   attr_c[0].id = cudaLaunchAttributeClusterDimension;
   attr_c[0].val.clusterDim.x = 2;
   attr_c[0].val.clusterDim.y = 1;
   attr_c[0].val.clusterDim.z = 1;
+  attr_c[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr_c[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr_c;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   ProfScope ps(PROF_GEMM_TC, s, 2.0 * g.M * g.N * static_cast<double>(g.K), 0);
   if (ps.keyed())
     snprintf(ps.key, sizeof(ps.key), "pair 256x%d M%d N%d K%d %c%c epi%d", BN, g.M, g.N, g.K, AK ? 'k' : 'm',
@@ -1056,9 +1062,9 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e) {
   const double rpair = std::ceil(tm2 * ((g.N + 255) / 256) / std::floor(sms / 2));
   const double rpair128 = std::ceil(tm2 * ((g.N + 127) / 128) / std::floor(sms / 2));
   double c128 = r128 * 0.5 / 0.76, c256 = r256;
-  // the 256 x 128 pair tile stages as many shared-memory bytes per MMA as the 128 x 256
-  // single-CTA tile (efficiency ~1.0) with half its N granularity
-  const double cpair = rpair / 1.12, cpair128 = rpair128 * 0.5;
+  // the 256 x 128 pair tile: half the N granularity, but measured at ~0.68 of the 128 x 256
+  // per-SM rate (fwd_w2 771 vs 1166 TF/s), so it rarely wins
+  const double cpair = rpair / 1.12, cpair128 = rpair128 * 0.5 / 0.68;
   // Split-K for accumulating GEMMs with few output tiles (weight gradients over a long
   // token axis): S K slices per tile fill the machine; each extra slice costs one more
   // ordered fp32 reduce of the tile (~3%). Slices keep >= 16 k-blocks.

@@ -88,6 +88,8 @@ __global__ void embed_fwd_k(const T* E, const T* P, const int32_t* tok, const in
 template <class T>
 __global__ void embed_decode_k(const T* E, const T* P, const int32_t* tok, const int32_t* plen, int step, int rows,
                                int d, float* x32, T* xT) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t n = static_cast<int64_t>(rows) * d;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int r = static_cast<int>(i / d), c = static_cast<int>(i % d);
@@ -269,6 +271,8 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
                                                      int V, int bos, int eos, float inv_t, const uint64_t* keys,
                                                      int step, const int32_t* cap, uint8_t* finished, int32_t* comp,
                                                      float* logp, int32_t* len, int32_t* tok_next, int max_len) {
+  pdl_wait();
+  pdl_trigger();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= rows) return;
   const bool active = !finished[row] && step < cap[row];
@@ -461,6 +465,8 @@ __global__ void kv_store_prompt_k(const T* qkv, const int32_t* start, int n_prom
 template <class T>
 __global__ void kv_append_k(const T* qkv, int rows, int qd, int kvd, int nkv, int hd, int slot, int max_len, T* ks,
                             T* vs) {
+  pdl_wait();
+  pdl_trigger();
   const int qkvd = qd + 2 * kvd;
   const int64_t n = static_cast<int64_t>(rows) * kvd;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -609,7 +615,8 @@ void embed_fwd(cudaStream_t s, const T* E, const T* P, const int32_t* tok, const
 template <class T>
 void embed_decode(cudaStream_t s, const T* E, const T* P, const int32_t* tok, const int32_t* plen, int step,
                   int rows, int d, float* x32, T* xT) {
-  embed_decode_k<T><<<grid1d(static_cast<int64_t>(rows) * d), 256, 0, s>>>(E, P, tok, plen, step, rows, d, x32, xT);
+  launch_pdl(embed_decode_k<T>, dim3(grid1d(static_cast<int64_t>(rows) * d)), dim3(256), 0, s, E, P, tok, plen, step,
+             rows, d, x32, xT);
   DCU_LAUNCHED();
 }
 void embed_bwd(cudaStream_t s, const float* dx, const int32_t* tok, const int32_t* pos, int rows, int d, float* gt,
@@ -679,8 +686,8 @@ void lse_reduce(cudaStream_t s, const float* part, int ntiles, int rows, float* 
 void sample_scan(cudaStream_t s, const float* part, int nslices, const float* logits, int64_t logits_ld, int rows,
                  int V, int bos, int eos, float inv_t, const uint64_t* keys, int step, const int32_t* cap,
                  uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len) {
-  sample_scan_k<<<cdiv(rows, 8), 256, 0, s>>>(part, nslices, logits, logits_ld, rows, V, bos, eos, inv_t, keys, step,
-                                              cap, finished, comp, logp, len, tok_next, max_len);
+  launch_pdl(sample_scan_k, dim3(cdiv(rows, 8)), dim3(256), 0, s, part, nslices, logits, logits_ld, rows, V, bos, eos,
+             inv_t, keys, step, cap, finished, comp, logp, len, tok_next, max_len);
   DCU_LAUNCHED();
 }
 
@@ -703,8 +710,8 @@ void kv_store_prompt(cudaStream_t s, const T* qkv, const int32_t* start, int n_p
 template <class T>
 void kv_append(cudaStream_t s, const T* qkv, int rows, int qd, int kvd, int nkv, int hd, int slot, int max_len,
                T* ks, T* vs) {
-  kv_append_k<T><<<grid1d(static_cast<int64_t>(rows) * kvd), 256, 0, s>>>(qkv, rows, qd, kvd, nkv, hd, slot, max_len,
-                                                                         ks, vs);
+  launch_pdl(kv_append_k<T>, dim3(grid1d(static_cast<int64_t>(rows) * kvd)), dim3(256), 0, s, qkv, rows, qd, kvd, nkv,
+             hd, slot, max_len, ks, vs);
   DCU_LAUNCHED();
 }
 template <class T>
