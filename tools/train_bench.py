@@ -26,6 +26,10 @@ def main():
     w = np.full(n_seq, 1.0 / n_seq)
     pol.grad_zero()
     pol.accumulate_weighted(w, micro_batch=n_seq)   # warm-up (allocations)
+    plain = []
+    for _ in range(int(os.environ.get("REPS", "3"))):  # unprofiled: per-kernel events serialise launches
+        pol.accumulate_weighted(w, micro_batch=n_seq)
+        plain.append(pol.stats()["accumulate_ms"])
     reps = int(os.environ.get("REPS", "3"))
     best = None
     for _ in range(reps):  # the fastest of a few runs (box-to-box clock variance is large)
@@ -42,7 +46,8 @@ def main():
     st = pol.stats()
     out = {k: {"ms": v["ms"], "launches": v["launches"], "tflops": v["flops"] / max(v["ms"], 1e-9) / 1e9}
            for k, v in prof.items() if v["launches"]}
-    print(json.dumps({"seqs": n_seq, "tokens": n_seq * (P + L - 1), "accumulate_ms": st["accumulate_ms"],
+    print(json.dumps({"seqs": n_seq, "tokens": n_seq * (P + L - 1), "accumulate_ms_unprofiled": min(plain),
+                      "accumulate_ms": st["accumulate_ms"],
                       "classes": out}))
     for k, n, ms, f, b in keys:
         print(f"{ms:9.3f} ms {n:4d}x {f / max(ms, 1e-9) / 1e9:7.1f} TF/s  {k}")
