@@ -45,13 +45,14 @@ extern int64_t g_launches;
 // pdl_wait() blocks until the previous grid has completed and its writes are visible, so
 // it must precede every global read of upstream data and every global write. pdl_trigger()
 // lets the next kernel be scheduled early (its CTAs still wait in its own pdl_wait()).
-// DASHCU_NO_PDL=1 launches everything fully serialised.
+// Opt-in (DASHCU_PDL=1): measured neutral for the training micro-batch and ~6% slower for
+// decode steps with the trigger at kernel start, so launches stay fully serialised by default.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 inline bool pdl_enabled() {
-  const char* s = getenv("DASHCU_NO_PDL");
-  return !(s && s[0] == '1');
+  const char* s = getenv("DASHCU_PDL");
+  return s && s[0] == '1';
 }
 
 template <typename... KArgs, typename... Args>

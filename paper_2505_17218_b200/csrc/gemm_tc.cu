@@ -557,8 +557,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  pdl_wait();     // set-up above overlapped the previous kernel; its outputs are visible now
-  pdl_trigger();  // the next kernel may take SMs as this grid's CTAs finish
+  pdl_wait();  // set-up above overlapped the previous kernel; its outputs are visible now
 
   if (warp == 0) {
     if (lane == 0) {
@@ -661,6 +660,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
     }
     stage_drain(lane);  // bulk stores complete before the CTA's shared memory goes away
   }
+  pdl_trigger();  // this CTA's work is done: the next kernel may be scheduled
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 2) {
@@ -882,8 +882,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
   cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive / TMA
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  pdl_wait();     // set-up above overlapped the previous kernel; its outputs are visible now
-  pdl_trigger();  // the next kernel may take SMs as this grid's CTAs finish
+  pdl_wait();  // set-up above overlapped the previous kernel; its outputs are visible now
 
   if (warp == 0) {
     if (lane == 0) {
@@ -976,6 +975,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
     }
     stage_drain(lane);
   }
+  pdl_trigger();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync_all();
   if (warp == 2) {

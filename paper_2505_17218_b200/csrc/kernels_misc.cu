@@ -89,7 +89,6 @@ template <class T>
 __global__ void embed_decode_k(const T* E, const T* P, const int32_t* tok, const int32_t* plen, int step, int rows,
                                int d, float* x32, T* xT) {
   pdl_wait();
-  pdl_trigger();
   const int64_t n = static_cast<int64_t>(rows) * d;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int r = static_cast<int>(i / d), c = static_cast<int>(i % d);
@@ -272,7 +271,6 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
                                                      int step, const int32_t* cap, uint8_t* finished, int32_t* comp,
                                                      float* logp, int32_t* len, int32_t* tok_next, int max_len) {
   pdl_wait();
-  pdl_trigger();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= rows) return;
   const bool active = !finished[row] && step < cap[row];
@@ -466,7 +464,6 @@ template <class T>
 __global__ void kv_append_k(const T* qkv, int rows, int qd, int kvd, int nkv, int hd, int slot, int max_len, T* ks,
                             T* vs) {
   pdl_wait();
-  pdl_trigger();
   const int qkvd = qd + 2 * kvd;
   const int64_t n = static_cast<int64_t>(rows) * kvd;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
