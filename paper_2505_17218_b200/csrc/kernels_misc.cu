@@ -261,6 +261,8 @@ __global__ void sample_partials_k(const float* __restrict__ logits, int rows, in
   }
 }
 
+constexpr int kScanMaxB = 192;  // slices per lane block staged in shared memory (V <= 196608)
+
 // The inverse-CDF walk of the sampling contract (rule.cuh), one warp per row: lane j
 // owns a block of consecutive slices; block, slice and id sums are accumulated in the
 // contract's order, so the chosen id is a pure function of the fp32 logits, 1/T and the
@@ -300,37 +302,62 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
   float Tj[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) Tj[j] = __shfl_sync(0xffffffffu, T, j);
-  if (lane != 0) return;
+  // slice sums of every block, computed by the whole warp into shared memory (the same
+  // fp32 operations as the sequential definition; only the walk below is sequential)
+  __shared__ float sS[8][kScanMaxB];
+  float* Sw = sS[threadIdx.x >> 5];
+  const bool staged = B <= kScanMaxB;
   float total = 0.f;
 #pragma unroll
   for (int j = 0; j < 32; ++j) total = __fadd_rn(total, Tj[j]);
   const float target = __fmul_rn(row_uniform(keys[row], step), total);
   int jb = -1;
-  float base = 0.f, cum = 0.f, last_base = 0.f;
-  int last_j = -1;
+  float base = 0.f;
+  {
+    float cum = 0.f, last_base = 0.f;
+    int last_j = -1;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const float prev = cum;
-    cum = __fadd_rn(cum, Tj[j]);
-    if (Tj[j] > 0.f) {
-      last_j = j;
-      last_base = prev;
+    for (int j = 0; j < 32; ++j) {
+      const float prev = cum;
+      cum = __fadd_rn(cum, Tj[j]);
+      if (Tj[j] > 0.f) {
+        last_j = j;
+        last_base = prev;
+      }
+      if (jb < 0 && target < cum) {
+        jb = j;
+        base = prev;
+      }
     }
-    if (jb < 0 && target < cum) {
-      jb = j;
-      base = prev;
+    if (jb < 0) {
+      jb = last_j;
+      base = last_base;
     }
   }
-  if (jb < 0) {
-    jb = last_j;
-    base = last_base;
+  if (staged) {
+    for (int k = lane; k < B; k += 32) {
+      const int s = jb * B + k;
+      float v = 0.f;
+      if (s < nslices) {
+        const float4 p = P[s];
+        v = __fmul_rn(p.y, sexp2(__fmul_rn(__fsub_rn(p.x, M), kLog2e)));
+      }
+      Sw[k] = v;
+    }
+    __syncwarp();
   }
+  if (lane != 0) return;
   // slice search inside block jb
   int sb = -1, last_s = -1;
   float sbase = 0.f, last_sbase = 0.f, r = base;
   for (int s = jb * B; s < min(nslices, (jb + 1) * B); ++s) {
-    const float4 p = P[s];
-    const float Ss = __fmul_rn(p.y, sexp2(__fmul_rn(__fsub_rn(p.x, M), kLog2e)));
+    float Ss;
+    if (staged) {
+      Ss = Sw[s - jb * B];
+    } else {
+      const float4 p = P[s];
+      Ss = __fmul_rn(p.y, sexp2(__fmul_rn(__fsub_rn(p.x, M), kLog2e)));
+    }
     const float prev = r;
     r = __fadd_rn(r, Ss);
     if (Ss > 0.f) {
