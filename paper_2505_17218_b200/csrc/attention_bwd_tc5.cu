@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(384, 1)
     int h = kvh * grp, qt = kt;
     for (int it = 0; it < nit; ++it) {
       const int st = it % kST, q0 = qt * kQ;
-      mbar_wait(&qempty[st], ((it / kST) & 1) ^ 1);
+      mbar_wait_sleep(&qempty[st], ((it / kST) & 1) ^ 1);
       if (lane == 0) {
         mbar_expect_tx(&qfull[st], 2 * kTile);
         tma_load_2d(smem + Lay::Q + st * kTile, &mQKV, &qfull[st], h * kHD, s0 + q0);
@@ -157,10 +157,10 @@ __global__ void __launch_bounds__(384, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------------------------------------------------------- MMA
       constexpr uint32_t I_SS = idesc(128, false, false), I_KM = idesc(64, false, true), I_MM = idesc(64, true, true);
-      mbar_wait(kvfull, 0);
+      mbar_wait_sleep(kvfull, 0);
       auto issue_s = [&](int it) {
         const int st = it % kST;
-        mbar_wait(&qfull[st], (it / kST) & 1);
+        mbar_wait_sleep(&qfull[st], (it / kST) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t q = sQ + st * kTile, o = sO + st * kTile;
 #pragma unroll
@@ -175,11 +175,11 @@ __global__ void __launch_bounds__(384, 1)
       for (int it = 0; it < nit; ++it) {
         const int st = it % kST;
         if (it + 1 < nit) {  // S(it+1) as soon as the softmax warps hold S(it) in registers
-          mbar_wait(sfree, it & 1);
+          mbar_wait_sleep(sfree, it & 1);
           issue_s(it + 1);
         }
-        mbar_wait(pready, it & 1);
-        if (it > 0) mbar_wait(dqfree, (it - 1) & 1);
+        mbar_wait_sleep(pready, it & 1);
+        if (it > 0) mbar_wait_sleep(dqfree, (it - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t q = sQ + st * kTile, o = sO + st * kTile;
 #pragma unroll
@@ -241,10 +241,10 @@ __global__ void __launch_bounds__(384, 1)
     int h = kvh * grp, qt = kt, ph = 0, pq0 = 0;  // (head, tile) of this and of the previous iteration
     for (int it = 0; it < nit; ++it) {
       const int st = it % kST, q0 = qt * kQ;
-      mbar_wait(&ldfull[st], (it / kST) & 1);
+      mbar_wait_sleep(&ldfull[st], (it / kST) & 1);
       const float* L = sLD + st * 256 + hf * 64;
       const float* D = L + 128;
-      mbar_wait(sfull, it & 1);
+      mbar_wait_sleep(sfull, it & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       // masks only on the causal diagonal and at the sequence end (warp-uniform)
       const bool edge = qt == kt || q0 + kQ > n || k0 + kKeys > n;
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         // the MMAs of it-1 are complete (dQ ready, P^T / dS^T no longer read) before the
         // operands are overwritten; TMEM dQ is rewritten only after dqfree
-        if (hh == 0 && it > 0) mbar_wait(dqfull, (it - 1) & 1);
+        if (hh == 0 && it > 0) mbar_wait_sleep(dqfull, (it - 1) & 1);
         st_row32(sP + hf * kTile, key_l, hh * 4, sv);
         st_row32(sS + hf * kTile, key_l, hh * 4, dp);
       }
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(384, 1)
       ph = h, pq0 = q0;
       if (++qt * kQ >= n) qt = kt, ++h;
     }
-    mbar_wait(dqfull, (nit - 1) & 1);
+    mbar_wait_sleep(dqfull, (nit - 1) & 1);
     dq_out(ph, pq0);
     // dK, dV of this thread's key row (all MMAs completed: the last dqfull covers them)
     float dk[32], dv[32];

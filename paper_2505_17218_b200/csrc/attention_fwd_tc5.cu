@@ -109,12 +109,12 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {  // ---------------------------------------------------------------- TMA
       for (int hh = 0, t = 0; hh < grp; ++hh) {
         const int qs = hh & 1;
-        mbar_wait(&qempty[qs], ((hh >> 1) & 1) ^ 1);
+        mbar_wait_sleep(&qempty[qs], ((hh >> 1) & 1) ^ 1);
         mbar_expect_tx(&qfull[qs], kTile);
         tma_load_2d(smem + FLay::Q + qs * kTile, &mQKV, &qfull[qs], (kvh * grp + hh) * kHD, s0 + q0);
         for (int j = 0; j < nkt; ++j, ++t) {
           const int st = t % kST;
-          mbar_wait(&kvempty[st], ((t / kST) & 1) ^ 1);
+          mbar_wait_sleep(&kvempty[st], ((t / kST) & 1) ^ 1);
           mbar_expect_tx(&kvfull[st], 2 * kTile);
           tma_load_2d(smem + FLay::K + st * kTile, &mQKV, &kvfull[st], qd + kvh * kHD, s0 + j * kKeys);
           tma_load_2d(smem + FLay::V + st * kTile, &mQKV, &kvfull[st], qd + kvd + kvh * kHD, s0 + j * kKeys);
@@ -126,9 +126,9 @@ __global__ void __launch_bounds__(256, 1)
       constexpr uint32_t I_S = idesc(128, false, false), I_O = idesc(64, false, true);
       auto issue_s = [&](int t) {
         const int sb = t & 1, st = t % kST, hh = t / nkt, j = t % nkt, qs = hh & 1;
-        if (t >= 2) mbar_wait(&sfree[sb], ((t >> 1) - 1) & 1);  // softmax holds S_{t-2} in registers
-        if (j == 0) mbar_wait(&qfull[qs], (hh >> 1) & 1);
-        mbar_wait(&kvfull[st], (t / kST) & 1);
+        if (t >= 2) mbar_wait_sleep(&sfree[sb], ((t >> 1) - 1) & 1);  // softmax holds S_{t-2} in registers
+        if (j == 0) mbar_wait_sleep(&qfull[qs], (hh >> 1) & 1);
+        mbar_wait_sleep(&kvfull[st], (t / kST) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t k = sK + st * kTile, qa = sQ + qs * kTile;
 #pragma unroll
@@ -142,8 +142,8 @@ __global__ void __launch_bounds__(256, 1)
       for (int t = 0; t < ntiles; ++t) {
         const int sb = t & 1, st = t % kST;
         if (t + 1 < ntiles) issue_s(t + 1);
-        mbar_wait(pready, t & 1);
-        if (t >= 2) mbar_wait(&ofree[sb], ((t >> 1) - 1) & 1);  // O_{t-2} read out
+        mbar_wait_sleep(pready, t & 1);
+        if (t >= 2) mbar_wait_sleep(&ofree[sb], ((t >> 1) - 1) & 1);  // O_{t-2} read out
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t v = sV + st * kTile;
 #pragma unroll
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(256, 1)
     // O_t (TMEM) into the register accumulator: acc = acc * 2^(m_old - m_new) + O_t
     auto take_o = [&](int t, float m_old, float m_new) {
       const int sb = t & 1;
-      mbar_wait(&ofull[sb], (t >> 1) & 1);
+      mbar_wait_sleep(&ofull[sb], (t >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       uint32_t o[kHD];
       tmem_ld32_async(tmem + lanes + (sb ? kTO1 : kTO0), o);
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(256, 1)
       m = -FLT_MAX, m_prev = -FLT_MAX, l = 0.f;
       for (int j = 0; j < nkt; ++j, ++t) {
         const int sb = t & 1;
-        mbar_wait(&sfull[sb], (t >> 1) & 1);
+        mbar_wait_sleep(&sfull[sb], (t >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         uint32_t sr[kKeys];
 #pragma unroll
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         l = l * ex2(m - m_new) + ((rs[0] + rs[1]) + (rs[2] + rs[3]));
         // P_t overwrites P_{t-1}: the MMA of O_{t-1} must be complete
-        if (t > 0) mbar_wait(&ofull[(t - 1) & 1], ((t - 1) >> 1) & 1);
+        if (t > 0) mbar_wait_sleep(&ofull[(t - 1) & 1], ((t - 1) >> 1) & 1);
 #pragma unroll
         for (int a = 0; a < 2; ++a)
 #pragma unroll
