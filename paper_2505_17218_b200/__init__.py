@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libdashcu.so")
+LIB_PATH = os.environ.get("DASHCU_LIB_PATH") or os.path.join(PKG, "lib", "libdashcu.so")
 
 OK, E_INPUT, E_CAPACITY, E_ON_POLICY, E_DEVICE = 0, 1, 2, 3, 4
 F32, BF16 = 0, 1

@@ -15,12 +15,15 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "lib")
 OBJ_DIR = os.path.join(OUT_DIR, "obj")
-LIB = os.path.join(OUT_DIR, "libdashcu.so")
+# Experiment builds (A/B of compile-time variants, tools only): DASHCU_NVCC_EXTRA adds nvcc
+# flags (e.g. -D...), DASHCU_LIB_OUT names the output library; load it with DASHCU_LIB_PATH.
+LIB = os.environ.get("DASHCU_LIB_OUT") or os.path.join(OUT_DIR, "libdashcu.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr",
          "-Xptxas", "-v" if os.environ.get("DASHCU_PTXAS_V") else "-O3", f"-I{os.path.join(ROOT, 'include')}"]
+FLAGS += os.environ.get("DASHCU_NVCC_EXTRA", "").split()
 
 
 def sources():

@@ -36,6 +36,17 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle row of bf16
 
+// Producer / MMA-issuer waits on the operand ring. Default: tight try_wait loop; with
+// -DDASHCU_GEMM_SLEEP_WAITS the suspend-hint form (frees issue slots for the epilogue
+// warps sharing the SM sub-partition). A/B with tools builds.
+__device__ __forceinline__ void mbar_wait_pipe(uint64_t* bar, uint32_t parity) {
+#ifdef DASHCU_GEMM_SLEEP_WAITS
+  mbar_wait_sleep(bar, parity);
+#else
+  mbar_wait(bar, parity);
+#endif
+}
+
 // tanh(x) = 1 - 2 / (exp(2x) + 1): ~1e-6 relative, far below the bf16 output rounding;
 // 6 instructions instead of tanhf's ~20 (the W1 epilogue runs it on every element).
 __device__ __forceinline__ float fast_tanh(float x) {
@@ -569,7 +580,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
         for (int kb = kb_lo; kb < kb_hi; ++kb, ++kb_all) {
           const int s = kb_all % STAGES;
           const uint32_t ph = (kb_all / STAGES) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
+          mbar_wait_pipe(&empty[s], ph ^ 1);
           uint8_t* sa_ = smem + s * C::STAGE_BYTES;
           uint8_t* sb_ = sa_ + C::A_BYTES;
           mbar_expect_tx(&full[s], C::STAGE_BYTES);
@@ -596,13 +607,13 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
         const int kb_lo = (w % S) * kps, kb_hi = min(nkb, kb_lo + kps);
         const int acc = i & 1;
         const uint32_t aph = (i >> 1) & 1;
-        mbar_wait(&tempty[acc], aph ^ 1);
+        mbar_wait_pipe(&tempty[acc], aph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * BN;
         for (int kb = kb_lo; kb < kb_hi; ++kb, ++kb_all) {
           const int s = kb_all % STAGES;
           const uint32_t ph = (kb_all / STAGES) & 1;
-          mbar_wait(&full[s], ph);
+          mbar_wait_pipe(&full[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t sa_ = smem_u32(smem + s * C::STAGE_BYTES);
           const uint32_t sb_ = sa_ + C::A_BYTES;
@@ -893,7 +904,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
         for (int kb = 0; kb < nkb; ++kb, ++kb_all) {
           const int s = kb_all % STAGES;
           const uint32_t ph = (kb_all / STAGES) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
+          mbar_wait_pipe(&empty[s], ph ^ 1);
           uint8_t* sa_ = smem + s * C::STAGE_BYTES;
           uint8_t* sb_ = sa_ + C::A_BYTES;
           const uint32_t lb = leader_addr(&full[s]);
@@ -926,7 +937,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
         for (int kb = 0; kb < nkb; ++kb, ++kb_all) {
           const int s = kb_all % STAGES;
           const uint32_t ph = (kb_all / STAGES) & 1;
-          mbar_wait(&full[s], ph);
+          mbar_wait_pipe(&full[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t sa_ = smem_u32(smem + s * C::STAGE_BYTES);
           const uint32_t sb_ = sa_ + C::A_BYTES;
