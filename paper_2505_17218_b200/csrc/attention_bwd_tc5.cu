@@ -38,11 +38,12 @@ template <int ST, int DQR>
 struct Lay {
   static constexpr int K = 0, V = kTile, Q = 2 * kTile /*ST stages*/, O = (2 + ST) * kTile /*ST stages*/;
   static constexpr int P = (2 + 2 * ST) * kTile;  // P^T  [128 keys x 128 q]: two 64-q swizzle atoms
-  static constexpr int S = P + 2 * kTile;          // dS^T [128 keys x 128 q]
-  static constexpr int DQ = S + 2 * kTile;         // 8 softmax warps x DQR x 32 fp32 dQ staging
+  static constexpr int S = P + 2 * kTile;          // dS^T [128 keys x 128 q] x 2 buffers
+  static constexpr int DQ = S + 4 * kTile;         // 8 softmax warps x DQR x 32 fp32 dQ staging
   static constexpr int LD = DQ + 8 * DQR * 128;    // per stage: sL[128], sD[128]
   static constexpr int BAR = LD + ST * 1024;
   static constexpr int BYTES = BAR + 256 + 1024;  // + alignment slack
+  static_assert(BYTES <= 232448, "exceeds the 227 KB of opt-in shared memory per CTA");
 };
 
 // TMEM columns
@@ -97,9 +98,9 @@ __global__ void __launch_bounds__(384, 1)
   constexpr int kST = ST;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR);
   uint64_t *kvfull = bar, *sfull = bar + 1, *sfree = bar + 2, *pready = bar + 3, *dqfull = bar + 4,
-           *dqfree = bar + 5, *qfull = bar + 6 /*[kST]*/, *qempty = bar + 6 + kST /*[kST]*/,
-           *ldfull = bar + 6 + 2 * kST /*[kST]*/;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 6 + 3 * kST);
+           *dqfree = bar + 5, *pfree = bar + 6, *qfull = bar + 7 /*[kST]*/, *qempty = bar + 7 + kST /*[kST]*/,
+           *ldfull = bar + 7 + 2 * kST /*[kST]*/;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 7 + 3 * kST);
   float* sLD = reinterpret_cast<float*>(smem + Lay::LD);  // [2][sL 128 | sD 128]
 
   if (threadIdx.x == 0) {
@@ -110,6 +111,7 @@ __global__ void __launch_bounds__(384, 1)
     mbar_init(pready, 256);
     mbar_init(dqfull, 1);
     mbar_init(dqfree, 256);
+    mbar_init(pfree, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mQKV)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mO)) : "memory");
@@ -181,18 +183,20 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait_sleep(pready, it & 1);
         if (it > 0) mbar_wait_sleep(dqfree, (it - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t q = sQ + st * kTile, o = sO + st * kTile;
+        const uint32_t q = sQ + st * kTile, o = sO + st * kTile, ds = sS + (it & 1) * 2 * kTile;
+        // dV first: its commit releases the single P^T buffer early for the next softmax
 #pragma unroll
-        for (int j = 0; j < kQ / 16; ++j) {  // K = 128 queries: two 64-wide atoms of P^T / dS^T
-          const uint32_t ka = (j >> 2) * kTile + (j & 3) * 32;
-          umma_bf16(tmem + kTdV, smem_desc(sP + ka, 16, 1024), smem_desc(o + j * 2048, kTile, 1024), I_KM,
-                    (it > 0 || j > 0) ? 1u : 0u);
-          umma_bf16(tmem + kTdK, smem_desc(sS + ka, 16, 1024), smem_desc(q + j * 2048, kTile, 1024), I_KM,
-                    (it > 0 || j > 0) ? 1u : 0u);
-        }
+        for (int j = 0; j < kQ / 16; ++j)  // K = 128 queries: two 64-wide atoms of P^T / dS^T
+          umma_bf16(tmem + kTdV, smem_desc(sP + (j >> 2) * kTile + (j & 3) * 32, 16, 1024),
+                    smem_desc(o + j * 2048, kTile, 1024), I_KM, (it > 0 || j > 0) ? 1u : 0u);
+        umma_commit(pfree);
+#pragma unroll
+        for (int j = 0; j < kQ / 16; ++j)
+          umma_bf16(tmem + kTdK, smem_desc(ds + (j >> 2) * kTile + (j & 3) * 32, 16, 1024),
+                    smem_desc(q + j * 2048, kTile, 1024), I_KM, (it > 0 || j > 0) ? 1u : 0u);
 #pragma unroll
         for (int j = 0; j < kKeys / 16; ++j)  // K = 128 keys; dS read MN-major (q is contiguous)
-          umma_bf16(tmem + kTdQ, smem_desc(sS + j * 2048, kTile, 1024), smem_desc(sK + j * 2048, kTile, 1024), I_MM,
+          umma_bf16(tmem + kTdQ, smem_desc(ds + j * 2048, kTile, 1024), smem_desc(sK + j * 2048, kTile, 1024), I_MM,
                     j > 0 ? 1u : 0u);
         umma_commit(&qempty[st]);
         umma_commit(dqfull);
@@ -279,15 +283,20 @@ __global__ void __launch_bounds__(384, 1)
             dp[c + e] = p * (dp[c + e] - dv4[e]);  // 1/sqrt(d) is applied to dK / dQ at readout
           }
         }
-        // the MMAs of it-1 are complete (dQ ready, P^T / dS^T no longer read) before the
-        // operands are overwritten; TMEM dQ is rewritten only after dqfree
-        if (hh == 0 && it > 0) mbar_wait_sleep(dqfull, (it - 1) & 1);
+        // P^T is single-buffered: dV(it-1) must have read it (pfree, committed first);
+        // dS^T alternates between two buffers, the one of it-2 was released with dqfull(it-2)
+        if (hh == 0 && it > 0) mbar_wait_sleep(pfree, (it - 1) & 1);
         st_row32(sP + hf * kTile, key_l, hh * 4, sv);
-        st_row32(sS + hf * kTile, key_l, hh * 4, dp);
+        st_row32(sS + (it & 1) * 2 * kTile + hf * kTile, key_l, hh * 4, dp);
+        // dQ(it-1) is read out between the two halves: its dqfree then reaches the MMA
+        // issuer before pready(it), so the next MMA batch starts as soon as P/dS are written
+        if (hh == 0 && it > 0) {
+          mbar_wait_sleep(dqfull, (it - 1) & 1);
+          dq_out(ph, pq0);
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(pready);
-      if (it > 0) dq_out(ph, pq0);
       ph = h, pq0 = q0;
       if (++qt * kQ >= n) qt = kt, ++h;
     }
@@ -344,20 +353,14 @@ bool attn_bwd_tc5(cudaStream_t s, const bf16* qkv, const bf16* dctx, const float
   const char* force = getenv("DASHCU_ATTN_BWD");
   if (force && std::string(force) == "mma") return false;
   const int qd = nh * hd, qkvd = qd + 2 * nkv * hd;
-  CUtensorMap mq, mo, mdq, mdq16;
+  CUtensorMap mq, mo, mdq16;
   if (!tma_map_2d(&mq, qkv, rows, qkvd, qkvd, kHD, 128, false, 128, true) ||
       !tma_map_2d(&mo, dctx, rows, qd, qd, kHD, 128, false, 128, true) ||
-      !tma_map_2d(&mdq, dq32, rows, qd, qd, 32, 32, true, 128, false) ||
       !tma_map_2d(&mdq16, dq32, rows, qd, qd, 32, 16, true, 128, false))
     return false;
   const float sc = 1.f / sqrtf(static_cast<float>(hd));
-  // pipeline variant (DASHCU_ATTN_BWD_CFG): "3x16" = 3 Q/dO stages + 16-row dQ boxes,
-  // default 2 stages + 32-row boxes
-  const char* cfg = getenv("DASHCU_ATTN_BWD_CFG");
-  if (cfg && std::string(cfg) == "3x16")
-    launch_bwd_tc5<3, 16>(s, mq, mo, mdq16, seq_start, lse, Dbuf, n_seq, max_len, nh, nkv, dkv32, sc);
-  else
-    launch_bwd_tc5<2, 32>(s, mq, mo, mdq, seq_start, lse, Dbuf, n_seq, max_len, nh, nkv, dkv32, sc);
+  // 2 Q/dO stages, two dS^T buffers and 16-row dQ boxes fill the 227 KB of shared memory
+  launch_bwd_tc5<2, 16>(s, mq, mo, mdq16, seq_start, lse, Dbuf, n_seq, max_len, nh, nkv, dkv32, sc);
   return true;
 }
 
