@@ -27,6 +27,20 @@
 
 namespace dashcu {
 
+#ifdef DASHCU_ATTN_TRACE
+// Debug builds only: clock64 timeline of CTA (0, 0), 16 slots per iteration (see TR()).
+__device__ unsigned long long g_attn_trace[64 * 16];
+#define TR(it, k)                                                                             \
+  do {                                                                                        \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && (it) < 64)           \
+      g_attn_trace[(it) * 16 + (k)] = clock64();                                              \
+  } while (0)
+#else
+#define TR(it, k) \
+  do {            \
+  } while (0)
+#endif
+
 namespace {
 
 constexpr int kKeys = 128, kQ = 128, kHD = 64;
@@ -178,10 +192,14 @@ __global__ void __launch_bounds__(384, 1)
         const int st = it % kST;
         if (it + 1 < nit) {  // S(it+1) as soon as the softmax warps hold S(it) in registers
           mbar_wait_sleep(sfree, it & 1);
+          TR(it, 0);
           issue_s(it + 1);
+          TR(it, 1);
         }
         mbar_wait_sleep(pready, it & 1);
+        TR(it, 2);
         if (it > 0) mbar_wait_sleep(dqfree, (it - 1) & 1);
+        TR(it, 3);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t q = sQ + st * kTile, o = sO + st * kTile, ds = sS + (it & 1) * 2 * kTile;
         // dV first: its commit releases the single P^T buffer early for the next softmax
@@ -248,7 +266,9 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait_sleep(&ldfull[st], (it / kST) & 1);
       const float* L = sLD + st * 256 + hf * 64;
       const float* D = L + 128;
+      if (warp == 4) TR(it, 4);
       mbar_wait_sleep(sfull, it & 1);
+      if (warp == 4) TR(it, 5);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       // masks only on the causal diagonal and at the sequence end (warp-uniform)
       const bool edge = qt == kt || q0 + kQ > n || k0 + kKeys > n;
@@ -285,18 +305,23 @@ __global__ void __launch_bounds__(384, 1)
         }
         // P^T is single-buffered: dV(it-1) must have read it (pfree, committed first);
         // dS^T alternates between two buffers, the one of it-2 was released with dqfull(it-2)
+        if (warp == 4) TR(it, 6 + hh * 4);
         if (hh == 0 && it > 0) mbar_wait_sleep(pfree, (it - 1) & 1);
+        if (warp == 4) TR(it, 7 + hh * 4);
         st_row32(sP + hf * kTile, key_l, hh * 4, sv);
         st_row32(sS + (it & 1) * 2 * kTile + hf * kTile, key_l, hh * 4, dp);
         // dQ(it-1) is read out between the two halves: its dqfree then reaches the MMA
         // issuer before pready(it), so the next MMA batch starts as soon as P/dS are written
         if (hh == 0 && it > 0) {
           mbar_wait_sleep(dqfull, (it - 1) & 1);
+          if (warp == 4) TR(it, 8);
           dq_out(ph, pq0);
+          if (warp == 4) TR(it, 9);
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(pready);
+      if (warp == 4) TR(it, 14);
       ph = h, pq0 = q0;
       if (++qt * kQ >= n) qt = kt, ++h;
     }
@@ -327,6 +352,12 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 }  // namespace
+
+#ifdef DASHCU_ATTN_TRACE
+int attn_trace_read(unsigned long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_attn_trace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 namespace {
 template <int ST, int DQR>

@@ -1376,6 +1376,10 @@ int dashcu_get_stats(dashcu_policy* p, dashcu_stats* out) {
   API_END
 }
 
+#ifdef DASHCU_ATTN_TRACE
+DASHCU_API int dashcu_debug_attn_trace(unsigned long long* out, int n) { return dashcu::attn_trace_read(out, n); }
+#endif
+
 int dashcu_selftest_gemm(dashcu_ctx* c, int M, int N, int K, const uint16_t* A, int64_t lda, int a_kmajor,
                          const uint16_t* B, int64_t ldb, int b_kmajor, const float* bias, int epi, int force_simt,
                          float* Cout) {
