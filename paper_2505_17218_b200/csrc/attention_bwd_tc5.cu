@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(384, 1)
     attn_bwd_tc5_k(const __grid_constant__ CUtensorMap mQKV, const __grid_constant__ CUtensorMap mO,
                    const __grid_constant__ CUtensorMap mDQ, const int32_t* __restrict__ seq_start,
                    const float* __restrict__ lse, const float* __restrict__ Dsum, int nh, int nkv,
-                   float* __restrict__ dkv32, float scale, float scale_log2) {
+                   float* __restrict__ dkv32, float* __restrict__ dq32, float scale, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // grid (sequence x kv head, key tile): launch order puts every long (early) key tile first
@@ -236,12 +236,23 @@ __global__ void __launch_bounds__(384, 1)
       mbar_arrive(dqfree);
 #pragma unroll
       for (int j = 0; j < 32; ++j) dq[j] *= scale;
+      if constexpr (DQR == 0) {  // fire-and-forget 16-byte fp32 reductions straight from registers
+        if (q0 + qq * 32 + lane < n) {
+          float* dst = dq32 + static_cast<int64_t>(s0 + q0 + qq * 32 + lane) * qd + h * kHD + hf * 32;
 #pragma unroll
-      for (int half = 0; half < 32 / DQR; ++half) {  // DQR-row boxes of the warp's 32 rows
+          for (int j = 0; j < 8; ++j)
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * j), "f"(dq[4 * j]),
+                         "f"(dq[4 * j + 1]), "f"(dq[4 * j + 2]), "f"(dq[4 * j + 3])
+                         : "memory");
+        }
+        return;
+      }
+#pragma unroll
+      for (int half = 0; half < (DQR ? 32 / DQR : 0); ++half) {  // DQR-row boxes of the warp's 32 rows
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
-        if (lane / DQR == half) {
-          const int r = lane % DQR;
+        if (lane / (DQR ? DQR : 1) == half) {
+          const int r = lane % (DQR ? DQR : 1);
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stg + r * 128 + ((j ^ (r & 7)) << 4)),
@@ -254,7 +265,7 @@ __global__ void __launch_bounds__(384, 1)
           asm volatile(
               "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                   reinterpret_cast<uint64_t>(&mDQ)),
-              "r"(stg), "r"(h * kHD + hf * 32), "r"(s0 + q0 + qq * 32 + half * DQR)
+              "r"(stg), "r"(h * kHD + hf * 32), "r"(s0 + q0 + qq * 32 + half * (DQR ? DQR : 1))
               : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
@@ -363,7 +374,7 @@ namespace {
 template <int ST, int DQR>
 void launch_bwd_tc5(cudaStream_t s, const CUtensorMap& mq, const CUtensorMap& mo, const CUtensorMap& mdq,
                     const int32_t* seq_start, const float* lse, const float* Dbuf, int n_seq, int max_len, int nh,
-                    int nkv, float* dkv32, float sc) {
+                    int nkv, float* dkv32, float* dq32, float sc) {
   auto k = attn_bwd_tc5_k<ST, DQR>;
   static bool attr = false;
   if (!attr) {
@@ -371,7 +382,7 @@ void launch_bwd_tc5(cudaStream_t s, const CUtensorMap& mq, const CUtensorMap& mo
     attr = true;
   }
   dim3 grid(n_seq * nkv, (max_len + kKeys - 1) / kKeys);
-  k<<<grid, 384, Lay<ST, DQR>::BYTES, s>>>(mq, mo, mdq, seq_start, lse, Dbuf, nh, nkv, dkv32, sc,
+  k<<<grid, 384, Lay<ST, DQR>::BYTES, s>>>(mq, mo, mdq, seq_start, lse, Dbuf, nh, nkv, dkv32, dq32, sc,
                                              sc * 1.4426950408889634f);
   DCU_LAUNCHED();
 }
@@ -390,8 +401,13 @@ bool attn_bwd_tc5(cudaStream_t s, const bf16* qkv, const bf16* dctx, const float
       !tma_map_2d(&mdq16, dq32, rows, qd, qd, 32, 16, true, 128, false))
     return false;
   const float sc = 1.f / sqrtf(static_cast<float>(hd));
-  // 2 Q/dO stages, two dS^T buffers and 16-row dQ boxes fill the 227 KB of shared memory
-  launch_bwd_tc5<2, 16>(s, mq, mo, mdq16, seq_start, lse, Dbuf, n_seq, max_len, nh, nkv, dkv32, sc);
+  // dQ: fire-and-forget fp32 reductions from registers (default) or, DASHCU_ATTN_BWD_DQ=tma,
+  // bulk tensor reduce-adds of 16-row boxes staged in shared memory
+  const char* dqm = getenv("DASHCU_ATTN_BWD_DQ");
+  if (dqm && std::string(dqm) == "tma")
+    launch_bwd_tc5<2, 16>(s, mq, mo, mdq16, seq_start, lse, Dbuf, n_seq, max_len, nh, nkv, dkv32, dq32, sc);
+  else
+    launch_bwd_tc5<2, 0>(s, mq, mo, mdq16, seq_start, lse, Dbuf, n_seq, max_len, nh, nkv, dkv32, dq32, sc);
   return true;
 }
 
