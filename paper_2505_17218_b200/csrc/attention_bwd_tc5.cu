@@ -51,8 +51,7 @@ constexpr int kTile = kKeys * kHD * 2;  // 16 KB: [128 rows x 64] bf16, 128-byte
 template <int ST, int DQR>
 struct Lay {
   static constexpr int K = 0, V = kTile, Q = 2 * kTile /*ST stages*/, O = (2 + ST) * kTile /*ST stages*/;
-  static constexpr int P = (2 + 2 * ST) * kTile;  // P^T  [128 keys x 128 q]: two 64-q swizzle atoms
-  static constexpr int S = P + 2 * kTile;          // dS^T [128 keys x 128 q] x 2 buffers
+  static constexpr int S = (2 + 2 * ST) * kTile;  // dS^T [128 keys x 128 q] x 2 buffers (P^T lives in TMEM)
   static constexpr int DQ = S + 4 * kTile;         // 8 softmax warps x DQR x 32 fp32 dQ staging
   static constexpr int LD = DQ + 8 * DQR * 128;    // per stage: sL[128], sD[128]
   static constexpr int BAR = LD + ST * 1024;
@@ -61,7 +60,9 @@ struct Lay {
 };
 
 // TMEM columns
-constexpr uint32_t kTS = 0, kTdP = 128, kTdV = 256, kTdK = 320, kTdQ = 384;
+// TMEM columns: S^T, dP^T (fp32), the dV / dK / dQ accumulators, and P^T as packed bf16
+// pairs (lane = key, column c = queries 2c, 2c+1): the A operand of dV += P^T dO
+constexpr uint32_t kTS = 0, kTdP = 128, kTdV = 256, kTdK = 320, kTdQ = 384, kTP = 448;
 
 constexpr uint32_t idesc(int n, bool a_mn, bool b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
@@ -77,6 +78,26 @@ __device__ __forceinline__ float ex2(float x) {
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// tcgen05.mma with the A operand in TMEM (K-major: lane = row, 8 columns per K=16 step)
+__device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                             uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+
+// 16 consecutive 32-bit TMEM columns of this warp's 32 lanes
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
 }
 
 // half a 128-byte row (32 bf16, chunks c0 .. c0+3) of a K-major swizzle atom: chunk j of
@@ -140,7 +161,7 @@ __global__ void __launch_bounds__(384, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   const uint32_t sK = smem_u32(smem + Lay::K), sV = smem_u32(smem + Lay::V), sQ = smem_u32(smem + Lay::Q),
-                 sO = smem_u32(smem + Lay::O), sP = smem_u32(smem + Lay::P), sS = smem_u32(smem + Lay::S);
+                 sO = smem_u32(smem + Lay::O), sS = smem_u32(smem + Lay::S);
 
   if (warp == 0) {  // ------------------------------------------------------------------ loads
     if (lane == 0) {
@@ -205,8 +226,8 @@ __global__ void __launch_bounds__(384, 1)
         // dV first: its commit releases the single P^T buffer early for the next softmax
 #pragma unroll
         for (int j = 0; j < kQ / 16; ++j)  // K = 128 queries: two 64-wide atoms of P^T / dS^T
-          umma_bf16(tmem + kTdV, smem_desc(sP + (j >> 2) * kTile + (j & 3) * 32, 16, 1024),
-                    smem_desc(o + j * 2048, kTile, 1024), I_KM, (it > 0 || j > 0) ? 1u : 0u);
+          umma_bf16_ts(tmem + kTdV, tmem + kTP + 8 * j, smem_desc(o + j * 2048, kTile, 1024), I_KM,
+                       (it > 0 || j > 0) ? 1u : 0u);
         umma_commit(pfree);
 #pragma unroll
         for (int j = 0; j < kQ / 16; ++j)
@@ -319,7 +340,12 @@ __global__ void __launch_bounds__(384, 1)
         if (warp == 4) TR(it, 6 + hh * 4);
         if (hh == 0 && it > 0) mbar_wait_sleep(pfree, (it - 1) & 1);
         if (warp == 4) TR(it, 7 + hh * 4);
-        st_row32(sP + hf * kTile, key_l, hh * 4, sv);
+        {  // P^T: 32 queries -> 16 packed columns of this lane's TMEM row
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pk[i] = pack2(sv[2 * i], sv[2 * i + 1]);
+          tmem_st16(tmem + lanes + kTP + hf * 32 + hh * 16, pk);
+        }
         st_row32(sS + (it & 1) * 2 * kTile + hf * kTile, key_l, hh * 4, dp);
         // dQ(it-1) is read out between the two halves: its dqfree then reaches the MMA
         // issuer before pready(it), so the next MMA batch starts as soon as P/dS are written
@@ -330,7 +356,9 @@ __global__ void __launch_bounds__(384, 1)
           if (warp == 4) TR(it, 9);
         }
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // P^T stores landed in TMEM
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // dS^T visible to the MMAs
       mbar_arrive(pready);
       if (warp == 4) TR(it, 14);
       ph = h, pq0 = q0;
@@ -395,19 +423,19 @@ bool attn_bwd_tc5(cudaStream_t s, const bf16* qkv, const bf16* dctx, const float
   const char* force = getenv("DASHCU_ATTN_BWD");
   if (force && std::string(force) == "mma") return false;
   const int qd = nh * hd, qkvd = qd + 2 * nkv * hd;
-  CUtensorMap mq, mo, mdq16;
+  CUtensorMap mq, mo, mdq;
   if (!tma_map_2d(&mq, qkv, rows, qkvd, qkvd, kHD, 128, false, 128, true) ||
       !tma_map_2d(&mo, dctx, rows, qd, qd, kHD, 128, false, 128, true) ||
-      !tma_map_2d(&mdq16, dq32, rows, qd, qd, 32, 16, true, 128, false))
+      !tma_map_2d(&mdq, dq32, rows, qd, qd, 32, 32, true, 128, false))
     return false;
   const float sc = 1.f / sqrtf(static_cast<float>(hd));
-  // dQ: fire-and-forget fp32 reductions from registers (default) or, DASHCU_ATTN_BWD_DQ=tma,
-  // bulk tensor reduce-adds of 16-row boxes staged in shared memory
+  // dQ: bulk tensor reduce-adds of 32-row boxes staged in shared memory (default) or,
+  // DASHCU_ATTN_BWD_DQ=red, 16-byte fp32 reductions straight from registers (measured slower)
   const char* dqm = getenv("DASHCU_ATTN_BWD_DQ");
-  if (dqm && std::string(dqm) == "tma")
-    launch_bwd_tc5<2, 16>(s, mq, mo, mdq16, seq_start, lse, Dbuf, n_seq, max_len, nh, nkv, dkv32, dq32, sc);
+  if (dqm && std::string(dqm) == "red")
+    launch_bwd_tc5<2, 0>(s, mq, mo, mdq, seq_start, lse, Dbuf, n_seq, max_len, nh, nkv, dkv32, dq32, sc);
   else
-    launch_bwd_tc5<2, 0>(s, mq, mo, mdq16, seq_start, lse, Dbuf, n_seq, max_len, nh, nkv, dkv32, dq32, sc);
+    launch_bwd_tc5<2, 32>(s, mq, mo, mdq, seq_start, lse, Dbuf, n_seq, max_len, nh, nkv, dkv32, dq32, sc);
   return true;
 }
 
