@@ -219,8 +219,6 @@ __global__ void __launch_bounds__(384, 1)
         }
         mbar_wait_sleep(pready, it & 1);
         TR(it, 2);
-        if (it > 0) mbar_wait_sleep(dqfree, (it - 1) & 1);
-        TR(it, 3);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t q = sQ + st * kTile, o = sO + st * kTile, ds = sS + (it & 1) * 2 * kTile;
         // dV first: its commit releases the single P^T buffer early for the next softmax
@@ -233,6 +231,11 @@ __global__ void __launch_bounds__(384, 1)
         for (int j = 0; j < kQ / 16; ++j)
           umma_bf16(tmem + kTdK, smem_desc(ds + (j >> 2) * kTile + (j & 3) * 32, 16, 1024),
                     smem_desc(q + j * 2048, kTile, 1024), I_KM, (it > 0 || j > 0) ? 1u : 0u);
+        // dQ(it) overwrites the dQ accumulator: dQ(it-1) must have been read out (the
+        // softmax warps do that while dV / dK of this iteration run)
+        if (it > 0) mbar_wait_sleep(dqfree, (it - 1) & 1);
+        TR(it, 3);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
         for (int j = 0; j < kKeys / 16; ++j)  // K = 128 keys; dS read MN-major (q is contiguous)
           umma_bf16(tmem + kTdQ, smem_desc(ds + j * 2048, kTile, 1024), smem_desc(sK + j * 2048, kTile, 1024), I_MM,
@@ -347,20 +350,20 @@ __global__ void __launch_bounds__(384, 1)
           tmem_st16(tmem + lanes + kTP + hf * 32 + hh * 16, pk);
         }
         st_row32(sS + (it & 1) * 2 * kTile + hf * kTile, key_l, hh * 4, dp);
-        // dQ(it-1) is read out between the two halves: its dqfree then reaches the MMA
-        // issuer before pready(it), so the next MMA batch starts as soon as P/dS are written
-        if (hh == 0 && it > 0) {
-          mbar_wait_sleep(dqfull, (it - 1) & 1);
-          if (warp == 4) TR(it, 8);
-          dq_out(ph, pq0);
-          if (warp == 4) TR(it, 9);
-        }
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // P^T stores landed in TMEM
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // dS^T visible to the MMAs
       mbar_arrive(pready);
       if (warp == 4) TR(it, 14);
+      // dQ(it-1) (complete long ago) is read out while dV(it) / dK(it) run; its dqfree
+      // gates only the dQ(it) MMA
+      if (it > 0) {
+        mbar_wait_sleep(dqfull, (it - 1) & 1);
+        if (warp == 4) TR(it, 8);
+        dq_out(ph, pq0);
+        if (warp == 4) TR(it, 9);
+      }
       ph = h, pq0 = q0;
       if (++qt * kQ >= n) qt = kt, ++h;
     }
