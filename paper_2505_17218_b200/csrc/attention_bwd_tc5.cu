@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(384, 1)
         for (int j = 0; j < kQ / 16; ++j)
           umma_bf16(tmem + kTdK, smem_desc(ds + (j >> 2) * kTile + (j & 3) * 32, 16, 1024),
                     smem_desc(q + j * 2048, kTile, 1024), I_KM, (it > 0 || j > 0) ? 1u : 0u);
+        umma_commit(&qempty[st]);  // Q / dO of this stage are no longer read (S, dP, dV, dK issued)
         // dQ(it) overwrites the dQ accumulator: dQ(it-1) must have been read out (the
         // softmax warps do that while dV / dK of this iteration run)
         if (it > 0) mbar_wait_sleep(dqfree, (it - 1) & 1);
@@ -240,7 +241,6 @@ __global__ void __launch_bounds__(384, 1)
         for (int j = 0; j < kKeys / 16; ++j)  // K = 128 keys; dS read MN-major (q is contiguous)
           umma_bf16(tmem + kTdQ, smem_desc(ds + j * 2048, kTile, 1024), smem_desc(sK + j * 2048, kTile, 1024), I_MM,
                     j > 0 ? 1u : 0u);
-        umma_commit(&qempty[st]);
         umma_commit(dqfull);
       }
     }
