@@ -44,6 +44,11 @@ __device__ unsigned long long g_attn_trace[64 * 16];
 namespace {
 
 constexpr int kKeys = 128, kQ = 128, kHD = 64;
+#ifdef DASHCU_NO_SPLIT_EXP
+constexpr bool kSplitExp = false;
+#else
+constexpr bool kSplitExp = true;  // half the softmax exponentials via ex2_poly (tc5.cuh)
+#endif
 constexpr int kTile = kKeys * kHD * 2;  // 16 KB: [128 rows x 64] bf16, 128-byte swizzle
 
 // ST: Q / dO / (LSE, D) pipeline depth; DQR: rows of the per-warp dQ staging box (32 = one
@@ -329,7 +334,9 @@ __global__ void __launch_bounds__(384, 1)
           const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            float p = ex2(__fmaf_rn(sv[c + e], scale_log2, -lv[e]));
+            // odd columns on the FMA pipe, even on MUFU: the exponentials are the bound
+            const float arg = __fmaf_rn(sv[c + e], scale_log2, -lv[e]);
+            float p = (kSplitExp && (e & 1)) ? ex2_poly(arg) : ex2(arg);
             if (edge) {
               const int q = q0 + col + c + e;
               p = (q < n && key < n && key <= q) ? p : 0.f;

@@ -23,6 +23,11 @@ namespace dashcu {
 namespace {
 
 constexpr int kQ = 128, kKeys = 128, kHD = 64;
+#ifdef DASHCU_NO_SPLIT_EXP
+constexpr bool kSplitExp = false;
+#else
+constexpr bool kSplitExp = true;  // half the softmax exponentials via ex2_poly (tc5.cuh)
+#endif
 constexpr int kTile = 128 * kHD * 2;  // 16 KB
 
 constexpr int kST = 4;  // K/V pipeline depth: loads run 3 key tiles ahead of the MMAs
@@ -211,7 +216,8 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int c = 0; c < kKeys; c += 2) {
           const float p0 = ex2(__fmaf_rn(sv[c], scale_log2, -m_new));
-          const float p1 = ex2(__fmaf_rn(sv[c + 1], scale_log2, -m_new));
+          const float a1 = __fmaf_rn(sv[c + 1], scale_log2, -m_new);
+          const float p1 = kSplitExp ? ex2_poly(a1) : ex2(a1);  // half the exponentials on the FMA pipe
           rs[(c >> 1) & 3] += p0 + p1;
           pk[c >> 1] = pack2(p0, p1);
         }

@@ -101,6 +101,21 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 2^x for softmax exponents (x <= 0) on the FMA / integer pipes instead of the MUFU unit
+// (16 ex2 per clock per SM), so attention kernels can split their exponentials between
+// the two: round-to-nearest split x = n + f with |f| <= 1/2 via the 1.5 * 2^23 magic
+// constant, a degree-3 minimax polynomial for 2^f (max relative error 1.02e-4, far below
+// the bf16 rounding of the probabilities it feeds), then n added to the exponent field.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = __fadd_rn(x, 12582912.f);
+  const float f = __fsub_rn(x, __fsub_rn(t, 12582912.f));
+  float p = __fmaf_rn(0.05500831f, f, 0.2422097f);
+  p = __fmaf_rn(p, f, 0.69328284f);
+  p = __fmaf_rn(p, f, 1.f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4b400000) << 23));
+}
+
 }  // namespace
 
 }  // namespace dashcu
