@@ -44,10 +44,12 @@ __device__ unsigned long long g_attn_trace[64 * 16];
 namespace {
 
 constexpr int kKeys = 128, kQ = 128, kHD = 64;
-#ifdef DASHCU_NO_SPLIT_EXP
-constexpr bool kSplitExp = false;
+// -DDASHCU_SPLIT_EXP: half the softmax exponentials via ex2_poly (tc5.cuh). Measured
+// slower for the backward (its softmax warps are issue-bound, not MUFU-bound), neutral forward.
+#ifdef DASHCU_SPLIT_EXP
+constexpr bool kSplitExp = true;
 #else
-constexpr bool kSplitExp = true;  // half the softmax exponentials via ex2_poly (tc5.cuh)
+constexpr bool kSplitExp = false;
 #endif
 constexpr int kTile = kKeys * kHD * 2;  // 16 KB: [128 rows x 64] bf16, 128-byte swizzle
 

@@ -23,10 +23,12 @@ namespace dashcu {
 namespace {
 
 constexpr int kQ = 128, kKeys = 128, kHD = 64;
-#ifdef DASHCU_NO_SPLIT_EXP
-constexpr bool kSplitExp = false;
+// -DDASHCU_SPLIT_EXP: half the softmax exponentials via ex2_poly (tc5.cuh). Measured
+// slower for the backward (its softmax warps are issue-bound, not MUFU-bound), neutral forward.
+#ifdef DASHCU_SPLIT_EXP
+constexpr bool kSplitExp = true;
 #else
-constexpr bool kSplitExp = true;  // half the softmax exponentials via ex2_poly (tc5.cuh)
+constexpr bool kSplitExp = false;
 #endif
 constexpr int kTile = 128 * kHD * 2;  // 16 KB
 
