@@ -126,15 +126,21 @@ __global__ void __launch_bounds__(384, 1)
                    float* __restrict__ dkv32, float* __restrict__ dq32, float scale, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // grid (sequence x kv head, key tile): launch order puts every long (early) key tile first
-  const int kt = blockIdx.y, sq = blockIdx.x / nkv, kvh = blockIdx.x % nkv;
+  // grid (sequence x kv head, key tile x 2): launch order puts every long (early) key tile
+  // first. Key tiles with >= 3 causal query tiles split their query heads over two CTAs
+  // (dK / dV of the halves are then reduce-added: two adds onto zero, order-independent),
+  // which roughly halves the longest CTA and the tail of the last wave.
+  const int kt = blockIdx.y >> 1, part = blockIdx.y & 1, sq = blockIdx.x / nkv, kvh = blockIdx.x % nkv;
   const int s0 = seq_start[sq], n = seq_start[sq + 1] - s0;
   const int k0 = kt * kKeys;
   if (k0 >= n) return;  // uniform for the CTA, before any barrier
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = nh / nkv, qd = nh * kHD, kvd = nkv * kHD;
   const int nq = (n + kQ - 1) / kQ - kt;  // causal query tiles per head: kt .. last
-  const int nit = grp * nq;
+  const bool split = grp > 1 && nq >= 3;
+  if (!split && part) return;
+  const int h_lo = split && part ? (grp + 1) / 2 : 0, h_hi = split && !part ? (grp + 1) / 2 : grp;
+  const int nit = (h_hi - h_lo) * nq;
 
   using Lay = dashcu::Lay<ST, DQR>;
   constexpr int kST = ST;
@@ -176,7 +182,7 @@ __global__ void __launch_bounds__(384, 1)
       tma_load_2d(smem + Lay::K, &mQKV, kvfull, qd + kvh * kHD, s0 + k0);
       tma_load_2d(smem + Lay::V, &mQKV, kvfull, qd + kvd + kvh * kHD, s0 + k0);
     }
-    int h = kvh * grp, qt = kt;
+    int h = kvh * grp + h_lo, qt = kt;
     for (int it = 0; it < nit; ++it) {
       const int st = it % kST, q0 = qt * kQ;
       mbar_wait_sleep(&qempty[st], ((it / kST) & 1) ^ 1);
@@ -302,7 +308,7 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
     };
-    int h = kvh * grp, qt = kt, ph = 0, pq0 = 0;  // (head, tile) of this and of the previous iteration
+    int h = kvh * grp + h_lo, qt = kt, ph = 0, pq0 = 0;  // (head, tile) of this and the previous iteration
     for (int it = 0; it < nit; ++it) {
       const int st = it % kST, q0 = qt * kQ;
       mbar_wait_sleep(&ldfull[st], (it / kST) & 1);
@@ -388,10 +394,22 @@ __global__ void __launch_bounds__(384, 1)
     if (key < n) {
       float* dkr = dkv32 + static_cast<int64_t>(s0 + key) * 2 * kvd + kvh * kHD + hf * 32;
       float* dvr = dkr + kvd;
+      if (split) {  // dkv32 is zero: the two halves' sums are order-independent
 #pragma unroll
-      for (int i = 0; i < 32; i += 4) {
-        *reinterpret_cast<float4*>(dkr + i) = make_float4(dk[i], dk[i + 1], dk[i + 2], dk[i + 3]);
-        *reinterpret_cast<float4*>(dvr + i) = make_float4(dv[i], dv[i + 1], dv[i + 2], dv[i + 3]);
+        for (int i = 0; i < 32; i += 4) {
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dkr + i), "f"(dk[i]), "f"(dk[i + 1]),
+                       "f"(dk[i + 2]), "f"(dk[i + 3])
+                       : "memory");
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dvr + i), "f"(dv[i]), "f"(dv[i + 1]),
+                       "f"(dv[i + 2]), "f"(dv[i + 3])
+                       : "memory");
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          *reinterpret_cast<float4*>(dkr + i) = make_float4(dk[i], dk[i + 1], dk[i + 2], dk[i + 3]);
+          *reinterpret_cast<float4*>(dvr + i) = make_float4(dv[i], dv[i + 1], dv[i + 2], dv[i + 3]);
+        }
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -421,7 +439,7 @@ void launch_bwd_tc5(cudaStream_t s, const CUtensorMap& mq, const CUtensorMap& mo
     DCU_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay<ST, DQR>::BYTES));
     attr = true;
   }
-  dim3 grid(n_seq * nkv, (max_len + kKeys - 1) / kKeys);
+  dim3 grid(n_seq * nkv, 2 * ((max_len + kKeys - 1) / kKeys));
   k<<<grid, 384, Lay<ST, DQR>::BYTES, s>>>(mq, mo, mdq, seq_start, lse, Dbuf, nh, nkv, dkv32, dq32, sc,
                                              sc * 1.4426950408889634f);
   DCU_LAUNCHED();
