@@ -220,6 +220,11 @@ DASHCU_API int dashcu_selftest_gemm(dashcu_ctx* ctx, int M, int N, int K, const 
  * from CUDA events on the context stream; epi 4 adds an fp32 residual input and fp32 output. */
 DASHCU_API int dashcu_selftest_gemm_timed(dashcu_ctx* ctx, int M, int N, int K, int a_kmajor, int b_kmajor, int epi,
                                           int iters, double* ms);
+/* Attention timing harness: packed causal attention over n_seq sequences of seq_len tokens
+ * (random bf16 q/k/v, nh / nkv heads of head_dim hd), forward (which 0) or backward incl.
+ * its D / zeroing prologue (which 1); best of `iters` launches in ms (CUDA events). */
+DASHCU_API int dashcu_selftest_attn_timed(dashcu_ctx* ctx, int n_seq, int seq_len, int nh, int nkv, int hd, int which,
+                                          int iters, double* ms);
 /* Whole-library count of kernel launches (all policies, all contexts). */
 DASHCU_API int64_t dashcu_kernel_launches(void);
 

@@ -68,14 +68,21 @@ __global__ void __launch_bounds__(256, 1)
   // CTA runs the tile for every query head of the KV group back to back, so the TMEM / barrier
   // set-up and the pipeline fill are paid once per group and K/V loads of the next head
   // stream in while the current head finishes
-  const int sq = blockIdx.x / nkv, kvh = blockIdx.x % nkv, qt = nqt_max - 1 - static_cast<int>(blockIdx.y);
+  // Query tiles with >= 3 causal key tiles split the group's heads over two CTAs (y = 2 qt'
+  // + part), which halves the longest CTAs.
+  const int sq = blockIdx.x / nkv, kvh = blockIdx.x % nkv;
+  const int qt = nqt_max - 1 - static_cast<int>(blockIdx.y >> 1), part = blockIdx.y & 1;
   const int s0 = seq_start[sq], n = seq_start[sq + 1] - s0;
   const int q0 = qt * kQ;
   if (q0 >= n) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = nh / nkv, qd = nh * kHD, kvd = nkv * kHD;
-  const int nkt = qt + 1;         // causal key tiles 0 .. qt per head
-  const int ntiles = grp * nkt;   // global tile counter t = head * nkt + key tile
+  const int grp0 = nh / nkv, qd = nh * kHD, kvd = nkv * kHD;
+  const int nkt = qt + 1;  // causal key tiles 0 .. qt per head
+  const bool split = grp0 > 1 && nkt >= 3;
+  if (!split && part) return;
+  const int h_lo = split && part ? (grp0 + 1) / 2 : 0, h_hi = split && !part ? (grp0 + 1) / 2 : grp0;
+  const int grp = h_hi - h_lo;     // heads run by this CTA: kvh * grp0 + h_lo + hh
+  const int ntiles = grp * nkt;    // global tile counter t = head * nkt + key tile
 
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FLay::BAR);
   uint64_t *qfull = bar /*[2]*/, *qempty = bar + 2 /*[2]*/, *sfull = bar + 4 /*[2]*/, *sfree = bar + 6 /*[2]*/,
@@ -118,7 +125,7 @@ __global__ void __launch_bounds__(256, 1)
         const int qs = hh & 1;
         mbar_wait_sleep(&qempty[qs], ((hh >> 1) & 1) ^ 1);
         mbar_expect_tx(&qfull[qs], kTile);
-        tma_load_2d(smem + FLay::Q + qs * kTile, &mQKV, &qfull[qs], (kvh * grp + hh) * kHD, s0 + q0);
+        tma_load_2d(smem + FLay::Q + qs * kTile, &mQKV, &qfull[qs], (kvh * grp0 + h_lo + hh) * kHD, s0 + q0);
         for (int j = 0; j < nkt; ++j, ++t) {
           const int st = t % kST;
           mbar_wait_sleep(&kvempty[st], ((t / kST) & 1) ^ 1);
@@ -182,7 +189,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int i = 0; i < kHD; ++i) acc[i] = __fmaf_rn(acc[i], c, __uint_as_float(o[i]));
     };
     for (int hh = 0, t = 0; hh < grp; ++hh) {
-      const int h = kvh * grp + hh;
+      const int h = kvh * grp0 + h_lo + hh;
 #pragma unroll
       for (int i = 0; i < kHD; ++i) acc[i] = 0.f;
       m = -FLT_MAX, m_prev = -FLT_MAX, l = 0.f;
@@ -282,7 +289,7 @@ bool attn_fwd_tc5(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int
     attr = true;
   }
   const int nqt = (max_len + kQ - 1) / kQ;
-  dim3 grid(n_seq * nkv, nqt);
+  dim3 grid(n_seq * nkv, 2 * nqt);
   attn_fwd_tc5_k<<<grid, 256, FLay::BYTES, s>>>(mq, seq_start, nh, nkv, nqt, ctx, lse,
                                                 1.4426950408889634f / sqrtf(static_cast<float>(hd)));
   DCU_LAUNCHED();

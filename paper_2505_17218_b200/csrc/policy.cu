@@ -1414,6 +1414,53 @@ int dashcu_selftest_gemm(dashcu_ctx* c, int M, int N, int K, const uint16_t* A, 
   API_END
 }
 
+int dashcu_selftest_attn_timed(dashcu_ctx* c, int n_seq, int seq_len, int nh, int nkv, int hd, int which, int iters,
+                               double* ms) {
+  API_BEGIN
+  if (!c || !ms || n_seq <= 0 || seq_len <= 0 || nh <= 0 || nkv <= 0 || nh % nkv || iters <= 0)
+    throw Error(1, "bad arguments");
+  DCU_CHECK(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  const int rows = n_seq * seq_len, qd = nh * hd, kvd = nkv * hd, qkvd = qd + 2 * kvd;
+  const size_t nq = static_cast<size_t>(rows) * qkvd, nc = static_cast<size_t>(rows) * qd;
+  float* tmp = c->ws.get<float>("ta_f", std::max(nq, nc));
+  bf16* qkv = c->ws.get<bf16>("ta_qkv", nq);
+  bf16* ctx = c->ws.get<bf16>("ta_ctx", nc);
+  bf16* dctx = c->ws.get<bf16>("ta_dctx", nc);
+  float* lse = c->ws.get<float>("ta_lse", static_cast<size_t>(rows) * nh);
+  float* D = c->ws.get<float>("ta_D", static_cast<size_t>(rows) * nh);
+  float* dq = c->ws.get<float>("ta_dq", nc);
+  float* dkv = c->ws.get<float>("ta_dkv", static_cast<size_t>(rows) * 2 * kvd);
+  int32_t* start = c->ws.get<int32_t>("ta_start", n_seq + 1);
+  std::vector<int32_t> hs(n_seq + 1);
+  for (int i = 0; i <= n_seq; ++i) hs[i] = i * seq_len;
+  h2d(s, start, hs.data(), n_seq + 1);
+  init_normal_ctr(s, tmp, static_cast<int64_t>(nq), 1.0, 3);
+  cast_f32_bf16(s, tmp, qkv, static_cast<int64_t>(nq));
+  init_normal_ctr(s, tmp, static_cast<int64_t>(nc), 1.0, 4);
+  cast_f32_bf16(s, tmp, dctx, static_cast<int64_t>(nc));
+  const double pairs = static_cast<double>(n_seq) * seq_len * (seq_len + 1) / 2.0;
+  auto fwd = [&] {
+    if (!attn_fwd_tc(s, qkv, start, n_seq, seq_len, rows, nh, nkv, hd, ctx, lse, 4.0 * nh * hd * pairs))
+      throw Error(1, "attention geometry not covered by the tensor-core kernels");
+  };
+  auto bwd = [&] {
+    fill_f32(s, dkv, 0.f, static_cast<int64_t>(rows) * 2 * kvd);
+    attn_bwd_tc(s, qkv, ctx, dctx, lse, start, n_seq, seq_len, rows, nh, nkv, hd, D, dq, dkv,
+                10.0 * nh * hd * pairs);
+  };
+  fwd();
+  if (which) bwd();
+  double best = 1e30;
+  for (int i = 0; i < iters; ++i) {  // best single launch (box clocks vary; the minimum is stable)
+    Timer tm(s);
+    which ? bwd() : fwd();
+    best = std::min(best, tm.stop_ms());
+  }
+  *ms = best;
+  API_END
+}
+
 int dashcu_selftest_gemm_timed(dashcu_ctx* c, int M, int N, int K, int a_kmajor, int b_kmajor, int epi, int iters,
                                double* ms) {
   API_BEGIN
