@@ -323,7 +323,11 @@ __global__ void __launch_bounds__(384, 1)
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
+#ifndef DASHCU_EXP_NO_DQ_STORE  // experiment builds only: time the kernel without the dQ reduce traffic
         if (lane == 0) {
+#else
+        if (false) {
+#endif
           asm volatile(
               "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                   reinterpret_cast<uint64_t>(&mDQ)),
