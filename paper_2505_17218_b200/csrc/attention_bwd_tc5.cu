@@ -21,6 +21,7 @@
 #include <cfloat>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "kernels.cuh"
 #include "tc5.cuh"
@@ -85,31 +86,6 @@ __device__ __forceinline__ float ex2(float x) {
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
-}
-
-// packed fp32x2 helpers (sm_100 FFMA2 / FADD2 / FMUL2 on register pairs)
-__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-}
-__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
 }
 
 // tcgen05.mma with the A operand in TMEM (K-major: lane = row, 8 columns per K=16 step)
@@ -365,32 +341,40 @@ __global__ void __launch_bounds__(384, 1)
         float* sv = reinterpret_cast<float*>(sr);  // P^T and dS^T overwrite S^T / dP^T in place
         float* dp = reinterpret_cast<float*>(dr);
         // element pairs on the packed fp32x2 pipe (FFMA2 / FADD2 / FMUL2): the softmax
-        // warps are issue-bound, this removes a third of their instructions
+        // warps are issue-bound, this removes a third of their instructions. Masks exist
+        // only on edge tiles, in their own loop (predicated-off instructions still issue):
+        // column c of this half is valid iff lo <= c < hi (causal key <= q, q < n, key < n).
         const uint64_t sc2 = f2_pack(scale_log2, scale_log2);
+        const int qb = q0 + col;
+        const int lo = key - qb, hi = key < n ? max(lo, n - qb) : lo;  // empty range when key >= n
+        auto body = [&](auto masked) {
 #pragma unroll
-        for (int c = 0; c < 32; c += 4) {
-          const float4 l4 = *reinterpret_cast<const float4*>(L + hh * 32 + c);  // -L (log2 units)
-          const float4 d4 = *reinterpret_cast<const float4*>(D + hh * 32 + c);
+          for (int c = 0; c < 32; c += 4) {
+            const float4 l4 = *reinterpret_cast<const float4*>(L + hh * 32 + c);  // -L (log2 units)
+            const float4 d4 = *reinterpret_cast<const float4*>(D + hh * 32 + c);
 #pragma unroll
-          for (int e = 0; e < 4; e += 2) {
-            const uint64_t arg = f2_fma(f2_pack(sv[c + e], sv[c + e + 1]), sc2,
-                                        e ? f2_pack(l4.z, l4.w) : f2_pack(l4.x, l4.y));
-            float p0, p1;
-            f2_unpack(arg, p0, p1);
-            p0 = (kSplitExp && false) ? ex2_poly(p0) : ex2(p0);
-            p1 = kSplitExp ? ex2_poly(p1) : ex2(p1);
-            if (edge) {
-              const int q = q0 + col + c + e;
-              p0 = (q < n && key < n && key <= q) ? p0 : 0.f;
-              p1 = (q + 1 < n && key < n && key <= q + 1) ? p1 : 0.f;
+            for (int e = 0; e < 4; e += 2) {
+              const uint64_t arg = f2_fma(f2_pack(sv[c + e], sv[c + e + 1]), sc2,
+                                          e ? f2_pack(l4.z, l4.w) : f2_pack(l4.x, l4.y));
+              float p0, p1;
+              f2_unpack(arg, p0, p1);
+              p0 = ex2(p0);
+              p1 = kSplitExp ? ex2_poly(p1) : ex2(p1);
+              if constexpr (decltype(masked)::value) {
+                const int cc = c + e;
+                p0 = static_cast<unsigned>(cc - lo) < static_cast<unsigned>(hi - lo) ? p0 : 0.f;
+                p1 = static_cast<unsigned>(cc + 1 - lo) < static_cast<unsigned>(hi - lo) ? p1 : 0.f;
+              }
+              sv[c + e] = p0;
+              sv[c + e + 1] = p1;
+              const uint64_t t =
+                  f2_sub(f2_pack(dp[c + e], dp[c + e + 1]), e ? f2_pack(d4.z, d4.w) : f2_pack(d4.x, d4.y));
+              f2_unpack(f2_mul(f2_pack(p0, p1), t), dp[c + e], dp[c + e + 1]);  // 1/sqrt(d) applied at readout
             }
-            sv[c + e] = p0;
-            sv[c + e + 1] = p1;
-            const uint64_t pp = f2_pack(p0, p1);
-            const uint64_t t = f2_sub(f2_pack(dp[c + e], dp[c + e + 1]), e ? f2_pack(d4.z, d4.w) : f2_pack(d4.x, d4.y));
-            f2_unpack(f2_mul(pp, t), dp[c + e], dp[c + e + 1]);  // 1/sqrt(d) applied to dK / dQ at readout
           }
-        }
+        };
+        if (edge) body(std::true_type());
+        else body(std::false_type());
         // P^T is single-buffered: dV(it-1) must have read it (pfree, committed first);
         // dS^T alternates between two buffers, the one of it-2 was released with dqfull(it-2)
         if (warp == 4) TR(it, 6 + hh * 4);

@@ -185,8 +185,11 @@ __global__ void __launch_bounds__(256, 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&ofree[sb]);
       const float c = ex2(m_old - m_new);
+      const uint64_t c2 = f2_pack(c, c);
 #pragma unroll
-      for (int i = 0; i < kHD; ++i) acc[i] = __fmaf_rn(acc[i], c, __uint_as_float(o[i]));
+      for (int i = 0; i < kHD; i += 2)  // packed fp32x2 FMAs
+        f2_unpack(f2_fma(f2_pack(acc[i], acc[i + 1]), c2, f2_pack(__uint_as_float(o[i]), __uint_as_float(o[i + 1]))),
+                  acc[i], acc[i + 1]);
     };
     for (int hh = 0, t = 0; hh < grp; ++hh) {
       const int h = kvh * grp0 + h_lo + hh;
@@ -220,17 +223,22 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int i = 0; i < w; ++i) tm[i] = fmaxf(tm[i], tm[i + w]);
         const float m_new = fmaxf(m, tm[0] * scale_log2);
-        float rs[4] = {0.f, 0.f, 0.f, 0.f};
+        uint64_t rs2[2] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
         uint32_t pk[kKeys / 2];
+        const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nm2 = f2_pack(-m_new, -m_new);
 #pragma unroll
-        for (int c = 0; c < kKeys; c += 2) {
-          const float p0 = ex2(__fmaf_rn(sv[c], scale_log2, -m_new));
-          const float a1 = __fmaf_rn(sv[c + 1], scale_log2, -m_new);
-          const float p1 = kSplitExp ? ex2_poly(a1) : ex2(a1);  // half the exponentials on the FMA pipe
-          rs[(c >> 1) & 3] += p0 + p1;
+        for (int c = 0; c < kKeys; c += 2) {  // exponent arguments and row sums on the fp32x2 pipe
+          float a0, a1;
+          f2_unpack(f2_fma(f2_pack(sv[c], sv[c + 1]), sc2, nm2), a0, a1);
+          const float p0 = ex2(a0);
+          const float p1 = kSplitExp ? ex2_poly(a1) : ex2(a1);  // optionally half on the FMA pipe
+          rs2[(c >> 1) & 1] = f2_add(rs2[(c >> 1) & 1], f2_pack(p0, p1));
           pk[c >> 1] = pack2(p0, p1);
         }
-        l = l * ex2(m - m_new) + ((rs[0] + rs[1]) + (rs[2] + rs[3]));
+        float r0, r1, r2, r3;
+        f2_unpack(rs2[0], r0, r1);
+        f2_unpack(rs2[1], r2, r3);
+        l = l * ex2(m - m_new) + ((r0 + r1) + (r2 + r3));
         // P_t overwrites P_{t-1}: the MMA of O_{t-1} must be complete
         if (t > 0) mbar_wait_sleep(&ofull[(t - 1) & 1], ((t - 1) >> 1) & 1);
 #pragma unroll
