@@ -334,6 +334,7 @@ __global__ void __launch_bounds__(384, 1)
         tmem_ld32_async(tmem + lanes + kTS + col, sr);
         tmem_ld32_async(tmem + lanes + kTdP + col, dr);
         tmem_wait_ld();
+        if (warp == 4) TR(it, 12 + hh);
         if (hh == 1) {
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           mbar_arrive(sfree);

@@ -407,12 +407,26 @@ __device__ __forceinline__ void epilogue_sample(const GemmShape& g, const Epi& e
     float m, m1, Z, Z1;
     if (full && (sa.bos < nb || sa.bos >= nb + 32)) {
       float x[32];
+      if (t1) {  // v * 1.0 == v
 #pragma unroll
-      for (int i = 0; i < 32; ++i) x[i] = __fmul_rn(v[i], sa.inv_t);
+        for (int i = 0; i < 32; ++i) x[i] = v[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = __fmul_rn(v[i], sa.inv_t);
+      }
       m = max32(x);
+      // the contract's e_i = sexp2((x_i - m) * log2e) and the 4 interleaved partial sums,
+      // element pairs on the packed fp32x2 pipe (per lane the same roundings: bit-exact)
       float a[4] = {0.f, 0.f, 0.f, 0.f};
+      const uint64_t m2 = f2_pack(m, m), l2 = f2_pack(kLog2e, kLog2e);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) a[i & 3] = __fadd_rn(a[i & 3], sexp2(__fmul_rn(__fsub_rn(x[i], m), kLog2e)));
+      for (int i = 0; i < 32; i += 2) {
+        float y0, y1, e0, e1;
+        f2_unpack(f2_mul(f2_sub(f2_pack(x[i], x[i + 1]), m2), l2), y0, y1);
+        sexp2_x2(y0, y1, e0, e1);
+        const int j = i & 3;  // 0 or 2: accumulators (a_j, a_j+1) get (e_i, e_i+1)
+        f2_unpack(f2_add(f2_pack(a[j], a[j + 1]), f2_pack(e0, e1)), a[j], a[j + 1]);
+      }
       Z = __fadd_rn(__fadd_rn(a[0], a[1]), __fadd_rn(a[2], a[3]));
       if (t1) {
         m1 = m, Z1 = Z;

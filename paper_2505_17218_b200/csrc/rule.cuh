@@ -64,6 +64,38 @@ __device__ __forceinline__ float sexp2(float x) {  // x <= 0 in all uses
   return __int_as_float(__float_as_int(p) + static_cast<int>(fl) * (1 << 23));  // p * 2^fl, exact
 }
 
+// Two sexp2 evaluations on the packed fp32x2 pipe (FADD2 / FFMA2): per lane exactly the
+// single-rounding operations of sexp2 above (floor via a round-toward-minus-infinity add of
+// 1.5 * 2^23, exact for |x| < 2^22), so results are bit-identical and half the instructions.
+__device__ __forceinline__ void sexp2_x2(float xa, float xb, float& ra, float& rb) {
+  constexpr float kMagic = 12582912.f;
+  xa = fmaxf(xa, -125.f);
+  xb = fmaxf(xb, -125.f);
+  uint64_t x2, mg, t2, fl2, f2, p2, c;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x2) : "f"(xa), "f"(xb));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(mg) : "f"(kMagic));
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(t2) : "l"(x2), "l"(mg));   // floor(x) + magic
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(fl2) : "l"(t2), "l"(mg));  // floor(x)
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(f2) : "l"(x2), "l"(fl2));  // x - floor(x)
+  asm("mov.b64 %0, {%1, %1};" : "=l"(p2) : "f"(1.5252734e-05f));
+#define DCU_SEXP2_STEP(k)                                                  \
+  asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(k));                         \
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p2) : "l"(p2), "l"(f2), "l"(c));
+  DCU_SEXP2_STEP(1.5403530e-04f)
+  DCU_SEXP2_STEP(1.3333558e-03f)
+  DCU_SEXP2_STEP(9.6181291e-03f)
+  DCU_SEXP2_STEP(5.5504109e-02f)
+  DCU_SEXP2_STEP(2.4022651e-01f)
+  DCU_SEXP2_STEP(6.9314718e-01f)
+  DCU_SEXP2_STEP(1.0f)
+#undef DCU_SEXP2_STEP
+  float pa, pb, ta, tb;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(pa), "=f"(pb) : "l"(p2));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(ta), "=f"(tb) : "l"(t2));
+  ra = __int_as_float(__float_as_int(pa) + (__float_as_int(ta) - 0x4b400000) * (1 << 23));
+  rb = __int_as_float(__float_as_int(pb) + (__float_as_int(tb) - 0x4b400000) * (1 << 23));
+}
+
 __device__ __forceinline__ float row_uniform(uint64_t seq_key, int32_t step) {
   const uint32_t h = row_key(seq_key, step);
   return __fmul_rn(static_cast<float>((h >> 9) * 2u + 1u), 5.9604644775390625e-08f);

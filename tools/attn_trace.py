@@ -13,7 +13,7 @@ from paper_2505_17218_b200 import workload as W  # noqa: E402
 
 NAMES = {0: "mma:sfree", 1: "mma:S issued", 2: "mma:pready", 3: "mma:dqfree/456", 4: "sm:wait sfull", 5: "sm:sfull",
          6: "sm:h0 computed", 7: "sm:pfree", 8: "sm:dqfull", 9: "sm:dq_out done", 10: "sm:h1 computed",
-         11: "sm:h1 pfree", 14: "sm:pready"}
+         11: "sm:h1 pfree", 12: "sm:h0 loaded", 13: "sm:h1 loaded", 14: "sm:pready"}
 
 
 def main():
