@@ -1042,6 +1042,14 @@ void launch2(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const
   DCU_LAUNCHED();
 }
 
+// Decode-step shapes: short K (<= 1152 -> <= 18 k-blocks per tile) and at most ~1.5 waves of
+// 128 x 256 tiles, where a tile's mainloop is too short to hide its epilogue.
+bool narrow_tiles(const GemmShape& g, const Epi& e) {
+  if (g.K > 1152 || e.kind == EPI_ACCUM) return false;
+  const long tiles256 = static_cast<long>((g.M + BM - 1) / BM) * ((g.N + 255) / 256);
+  return tiles256 <= 3 * num_sms() / 2;
+}
+
 int use_pair_default() {
   const char* s = getenv("DASHCU_GEMM_PAIR");
   return s ? atoi(s) : 0;
@@ -1109,13 +1117,21 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e) {
   }
   // DASHCU_GEMM_PAIR: 1 force the 256x256 pair, 2 force the 256x128 pair, 0 model, -1 never
   const int forced = use_pair_default();
-  if (forced != -1) {
+  const char* fbn = getenv("DASHCU_GEMM_BN");
+  const char* fnarrow = getenv("DASHCU_GEMM_NARROW");
+  const bool narrow = !fbn && forced == 0 && !(fnarrow && fnarrow[0] == '0') && narrow_tiles(g, e);
+  if (forced != -1 && !narrow) {
     const bool p256 = forced == 1 || (forced == 0 && cpair < c256 && cpair < c128 && cpair <= cpair128);
     const bool p128 = forced == 2 || (forced == 0 && !p256 && cpair128 < c256 && cpair128 < c128);
     if ((p256 && gemm_tc_pair(s, g, e, 256)) || (p128 && gemm_tc_pair(s, g, e, 128))) return true;
   }
   const bool wide = c256 <= c128;
-  const int BN = wide ? 256 : 128;
+  // Narrow 128 x 64 tiles for short-K GEMMs with few tiles (the decode-step projections): the
+  // exposed prologue / last-tile epilogue dominates there, and 4x more, 4x shorter tiles
+  // overlap each tile's epilogue with the next tile's MMAs. DASHCU_GEMM_BN forces 64/128/256.
+  int BN = wide ? 256 : 128;
+  if (fbn) BN = atoi(fbn) == 64 ? 64 : atoi(fbn) == 128 ? 128 : 256;
+  else if (narrow) BN = 64;
   CUtensorMap ma, mb;
   bool ok = g.a_kmajor ? make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) : make_map(&ma, g.A, g.K, g.M, g.lda, 64, BK);
   ok = ok && (g.b_kmajor ? make_map(&mb, g.B, g.N, g.K, g.ldb, BK, BN) : make_map(&mb, g.B, g.K, g.N, g.ldb, 64, BK));
@@ -1124,15 +1140,16 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e) {
   memset(&om, 0, sizeof(om));
   Epi et = e;
   et.tma = out_maps_for(g, e, &om);
-  const int S = wide ? split256 : split128;
+  const int S = BN == 256 ? split256 : BN == 128 ? split128 : 1;
   if (S > 1 && (et.tma & 1)) {
     const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
     et.splits = S;
     et.split_flags = split_flag_buffer(tiles * 8);
     DCU_CHECK(cudaMemsetAsync(et.split_flags, 0, sizeof(uint32_t) * tiles * 8, s));
   }
-  if (wide) dispatch_majors<256, 4>(s, ma, mb, om, g, et);   // 4 x 48 KB stages
-  else dispatch_majors<128, 6>(s, ma, mb, om, g, et);        // 6 x 32 KB stages
+  if (BN == 256) dispatch_majors<256, 4>(s, ma, mb, om, g, et);       // 4 x 48 KB stages
+  else if (BN == 128) dispatch_majors<128, 6>(s, ma, mb, om, g, et);  // 6 x 32 KB stages
+  else dispatch_majors<64, 8>(s, ma, mb, om, g, et);                  // 8 x 24 KB stages
   return true;
 }
 
