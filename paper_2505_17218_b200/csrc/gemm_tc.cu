@@ -1119,16 +1119,17 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e) {
   const int forced = use_pair_default();
   const char* fbn = getenv("DASHCU_GEMM_BN");
   const char* fnarrow = getenv("DASHCU_GEMM_NARROW");
-  const bool narrow = !fbn && forced == 0 && !(fnarrow && fnarrow[0] == '0') && narrow_tiles(g, e);
+  // opt-in (DASHCU_GEMM_NARROW=1): measured slower than the pair / 128-wide tiles on the C2
+  // decode shapes (dec_qkv 22.7 vs 14.8 us, dec_wo 21.8 vs 16.7 us)
+  const bool narrow = !fbn && forced == 0 && fnarrow && fnarrow[0] == '1' && narrow_tiles(g, e);
   if (forced != -1 && !narrow) {
     const bool p256 = forced == 1 || (forced == 0 && cpair < c256 && cpair < c128 && cpair <= cpair128);
     const bool p128 = forced == 2 || (forced == 0 && !p256 && cpair128 < c256 && cpair128 < c128);
     if ((p256 && gemm_tc_pair(s, g, e, 256)) || (p128 && gemm_tc_pair(s, g, e, 128))) return true;
   }
   const bool wide = c256 <= c128;
-  // Narrow 128 x 64 tiles for short-K GEMMs with few tiles (the decode-step projections): the
-  // exposed prologue / last-tile epilogue dominates there, and 4x more, 4x shorter tiles
-  // overlap each tile's epilogue with the next tile's MMAs. DASHCU_GEMM_BN forces 64/128/256.
+  // Optional narrow 128 x 64 tiles for short-K GEMMs with few tiles (see `narrow` above).
+  // DASHCU_GEMM_BN forces 64 / 128 / 256.
   int BN = wide ? 256 : 128;
   if (fbn) BN = atoi(fbn) == 64 ? 64 : atoi(fbn) == 128 ? 128 : 256;
   else if (narrow) BN = 64;
