@@ -196,6 +196,25 @@ def test_scheduling_independence(ctx):
     pol.close()
 
 
+def test_two_stream_half_batch_decode(ctx, monkeypatch):
+    """>= 1024 sequences decode as two half batches on two streams; every sequence's tokens
+    and log-probs equal the single-stream run bit-for-bit (1-CTA GEMM tiles in both, whose
+    per-element accumulation order does not depend on the number of rows)."""
+    monkeypatch.setenv("DASHCU_GEMM_PAIR", "-1")
+    arch = QWENLIKE
+    pol = D.Policy(ctx, arch, D.BF16)
+    pol.upload(params32(arch, 0.3, 21))
+    rng = np.random.default_rng(21)
+    prompts = [[0] + list(rng.integers(2, arch["vocab_size"], size=int(rng.integers(3, 9)))) for _ in range(160)]
+    two = pol.sample(prompts, 8, 20, round_seed=5, temperature=0.7)
+    monkeypatch.setenv("DASHCU_DECODE_HALVES", "0")
+    one = pol.sample(prompts, 8, 20, round_seed=5, temperature=0.7)
+    assert np.array_equal(two.completions, one.completions)
+    assert np.array_equal(two.lengths, one.lengths)
+    assert np.array_equal(two.logp, one.logp)
+    pol.close()
+
+
 def test_sample_errors(ctx):
     arch = SMALL
     pol = D.Policy(ctx, arch, D.F32)
