@@ -72,6 +72,10 @@ struct SampleArgs {
   int64_t ld_dz = 0;
 };
 int gemm_tc_lse(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa);
+// Persistent-grid cap for the tcgen05 GEMMs launched by this thread (0 = every SM): lets a
+// concurrent kernel on another stream keep the remaining SMs.
+int gemm_cta_cap();
+void gemm_set_cta_cap(int n);
 bool gemm_tc_dz(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa);
 int gemm_tc_lse_tiles(int N);
 

@@ -740,6 +740,12 @@ uint32_t* split_flag_buffer(int n) {
   return buf[dev];
 }
 
+namespace {
+thread_local int t_gemm_cta_cap = 0;
+}
+int gemm_cta_cap() { return t_gemm_cta_cap; }
+void gemm_set_cta_cap(int n) { t_gemm_cta_cap = n; }
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -761,7 +767,8 @@ void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const 
     attr = true;
   }
   const int nitem = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) * (MODE == 0 ? e.splits : 1);
-  const int grid = nitem < num_sms() ? nitem : num_sms();  // persistent: all CTAs co-resident
+  const int cap = gemm_cta_cap() > 0 ? std::min(gemm_cta_cap(), num_sms()) : num_sms();
+  const int grid = nitem < cap ? nitem : cap;  // persistent: all CTAs co-resident
   ProfScope ps(MODE == 1 ? PROF_SAMPLE : MODE >= 2 ? PROF_LM_ROWS : PROF_GEMM_TC, s,
                2.0 * g.M * g.N * static_cast<double>(g.K), 0);
   if (ps.keyed())
@@ -1019,7 +1026,8 @@ void launch2(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const
     attr = true;
   }
   const int ntile = ((g.M + 255) / 256) * ((g.N + BN - 1) / BN);
-  const int npairs = ntile < num_sms() / 2 ? ntile : num_sms() / 2;
+  const int pcap = (gemm_cta_cap() > 0 ? std::min(gemm_cta_cap(), num_sms()) : num_sms()) / 2;
+  const int npairs = ntile < pcap ? ntile : pcap;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * npairs);
   cfg.blockDim = dim3(C::THREADS);

@@ -790,14 +790,19 @@ struct Engine {
     T* ctx = ws.get<T>("d_ctx", static_cast<size_t>(S) * g.qd);
     T* u = ws.get<T>("d_u", static_cast<size_t>(S) * g.H);
     std::vector<uint8_t> hfin(S);
+    // opt-in (DASHCU_DECODE_HALVES=1): with full-machine persistent GEMMs the overlap did not
+    // materialise (C2: 11.8 s vs 10.7 s of sampling); DASHCU_DECODE_GEMM_SMS caps the
+    // projections' grid so the other half's attention keeps the remaining SMs
     const char* halves_env = getenv("DASHCU_DECODE_HALVES");
-    const bool halves_on = !(halves_env && halves_env[0] == '0');
+    const bool halves_on = halves_env && halves_env[0] == '1';
+    const char* gsms = getenv("DASHCU_DECODE_GEMM_SMS");
     const int NH = (sizeof(T) == 2 && halves_on && !dump && S >= 1024 && (S / 2) % G == 0) ? 2 : 1;
     const int R = S / NH;  // rows per half
     cudaStream_t main_st = st;
     cudaStream_t streams[2] = {st, st};
     cudaEvent_t ev_main = nullptr, ev_side = nullptr;
     if (NH == 2) {
+      if (gsms) gemm_set_cta_cap(atoi(gsms));
       if (!P.ctx->stream2) DCU_CHECK(cudaStreamCreateWithFlags(&P.ctx->stream2, cudaStreamNonBlocking));
       streams[1] = P.ctx->stream2;
       DCU_CHECK(cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming));
@@ -890,6 +895,7 @@ struct Engine {
     }
     st = main_st;
     join();
+    gemm_set_cta_cap(0);
     if (ev_main) cudaEventDestroy(ev_main);
     if (ev_side) cudaEventDestroy(ev_side);
   }

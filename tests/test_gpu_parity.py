@@ -201,6 +201,8 @@ def test_two_stream_half_batch_decode(ctx, monkeypatch):
     and log-probs equal the single-stream run bit-for-bit (1-CTA GEMM tiles in both, whose
     per-element accumulation order does not depend on the number of rows)."""
     monkeypatch.setenv("DASHCU_GEMM_PAIR", "-1")
+    monkeypatch.setenv("DASHCU_DECODE_HALVES", "1")
+    monkeypatch.setenv("DASHCU_DECODE_GEMM_SMS", "100")
     arch = QWENLIKE
     pol = D.Policy(ctx, arch, D.BF16)
     pol.upload(params32(arch, 0.3, 21))
