@@ -64,7 +64,9 @@ def build(verbose: bool = False) -> str:
                 print(log, file=sys.stderr)
     newest = max(os.path.getmtime(o) for o in objs)
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest or _stale_objs(objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-ldl"]
+        # --no-undefined: a symbol left undefined (e.g. given internal linkage by mistake)
+        # must fail here, not at dlopen time on the GPU box
+        cmd = [NVCC, *ARCH, "-shared", "-Xlinker", "--no-undefined", "-o", LIB, *objs, "-lcudart", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

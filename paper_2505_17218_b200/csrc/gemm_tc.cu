@@ -740,11 +740,8 @@ uint32_t* split_flag_buffer(int n) {
   return buf[dev];
 }
 
-namespace {
 thread_local int t_gemm_cta_cap = 0;
-}
-int gemm_cta_cap() { return t_gemm_cta_cap; }
-void gemm_set_cta_cap(int n) { t_gemm_cta_cap = n; }
+int cta_cap() { return t_gemm_cta_cap; }
 
 int num_sms() {
   static int n = 0;
@@ -767,7 +764,7 @@ void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const 
     attr = true;
   }
   const int nitem = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) * (MODE == 0 ? e.splits : 1);
-  const int cap = gemm_cta_cap() > 0 ? std::min(gemm_cta_cap(), num_sms()) : num_sms();
+  const int cap = cta_cap() > 0 ? std::min(cta_cap(), num_sms()) : num_sms();
   const int grid = nitem < cap ? nitem : cap;  // persistent: all CTAs co-resident
   ProfScope ps(MODE == 1 ? PROF_SAMPLE : MODE >= 2 ? PROF_LM_ROWS : PROF_GEMM_TC, s,
                2.0 * g.M * g.N * static_cast<double>(g.K), 0);
@@ -1026,7 +1023,7 @@ void launch2(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const
     attr = true;
   }
   const int ntile = ((g.M + 255) / 256) * ((g.N + BN - 1) / BN);
-  const int pcap = (gemm_cta_cap() > 0 ? std::min(gemm_cta_cap(), num_sms()) : num_sms()) / 2;
+  const int pcap = (cta_cap() > 0 ? std::min(cta_cap(), num_sms()) : num_sms()) / 2;
   const int npairs = ntile < pcap ? ntile : pcap;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * npairs);
@@ -1242,5 +1239,8 @@ bool tma_map_2d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, in
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
+
+int gemm_cta_cap() { return cta_cap(); }
+void gemm_set_cta_cap(int n) { t_gemm_cta_cap = n; }
 
 }  // namespace dashcu
