@@ -379,6 +379,76 @@ __device__ __forceinline__ void epilogue_store_tma(const GemmShape& g, const Epi
   }
 }
 
+// Residual epilogue with the next chunk's residual box prefetched (CTA-pair kernel, DB
+// variant): per warp two 4 KB residual / fp32-output buffers used alternately and one 2 KB
+// bf16-output buffer. Chunk k adds the residual staged in buf[k & 1], writes the fp32 sum
+// back into the same buffer and bulk-stores it, while the TMA load of chunk k+1's residual
+// is already in flight into buf[(k+1) & 1]. Bulk stores are committed one group each, so
+// "wait_group.read 1" = every store but the newest has finished reading its buffer.
+__device__ __forceinline__ void epilogue_resid_db(const GemmShape& g, const Epi& e, const OutMaps& om, uint32_t taddr,
+                                                  int r0, int n0, int c_lo, int c_hi, uint32_t stg, int lane,
+                                                  uint64_t* ebar2, uint32_t* eph2) {
+  float v[32], b[32];
+  const uint32_t buf[2] = {stg, stg + 4096}, tbuf = stg + 8192;
+  auto load = [&](int k) {  // residual box of chunk k into buf[k & 1]
+    const int nb = n0 + c_lo + 32 * k;
+    if (lane == 0) {
+      mbar_expect_tx(&ebar2[k & 1], 4096u);
+      tma_load_2d(reinterpret_cast<uint8_t*>(__cvta_shared_to_generic(buf[k & 1])), &om.rs, &ebar2[k & 1], nb, r0);
+    }
+  };
+  const int nk = min((c_hi - c_lo) / 32, (g.N - n0 - c_lo + 31) / 32);
+  if (nk <= 0) return;
+  // buf[0]'s last store (previous tile) has been read before the first load reuses it
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  __syncwarp();
+  load(0);
+#pragma unroll 1
+  for (int k = 0; k < nk; ++k) {
+    const int nb = n0 + c_lo + 32 * k;
+    if (k + 1 < nk) {  // buf[(k+1)&1] held chunk k-1's fp32 output: wait until read, then prefetch
+      if (lane == 0) {  // chunk k-1 committed c32 then (optionally) cT: the newest may stay pending
+        if (e.tma & 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+      __syncwarp();
+      load(k + 1);
+    }
+    if (e.bias) load_bias32(e.bias, nb, g.N, b);
+    tmem_ld32(taddr + c_lo + 32 * k, v);
+    if (e.bias) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __fmaf_rn(v[i], e.alpha, b[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(v[i], e.alpha);
+    }
+    if (e.kind == EPI_TANH) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = fast_tanh(v[i]);
+    }
+    mbar_wait(&ebar2[k & 1], eph2[k & 1]);
+    eph2[k & 1] ^= 1u;
+    unstage_f32(buf[k & 1], lane, b);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] += b[i];
+    __syncwarp();  // every lane has read the residual before the buffer is overwritten
+    if (e.tma & 1) {
+      stage_f32(buf[k & 1], lane, v);
+      stage_release(lane, &om.f32, buf[k & 1], nb, r0, false);
+    }
+    if (e.tma & 2) {  // cT(k-1) read; c32(k), committed just now, may stay pending
+      if (lane == 0) {
+        if (e.tma & 1) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+      __syncwarp();
+      stage_b16(tbuf, lane, v);
+      stage_release(lane, &om.b16, tbuf, nb, r0, false);
+    }
+  }
+}
+
 // LM-head sampling epilogue (inverse-CDF contract, rule.cuh): per 32-id slice the
 // epilogue stores the fp32 logits (the scan needs the chosen slice's ids) and one
 // 4-float record {m_s, Z_s, m1_s, Z1_s}: the contract's max / sexp2-sum at 1/T and
@@ -851,34 +921,35 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
-template <int BN, int STAGES, bool AK, bool BKM, int EPW>
+template <int BN, int STAGES, bool AK, bool BKM, int EPW, bool DB = false>
 struct Cfg2 {
   static constexpr int BNH = BN / 2;  // B rows staged per CTA
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = BNH * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STG_OFF = STAGES * STAGE_BYTES;
-  static constexpr int BAR_OFF = STG_OFF + EPW * kStageBytes;
-  static constexpr int SMEM = BAR_OFF + 1024 + 256;
+  static constexpr int STG_WARP = DB ? 10240 : kStageBytes;  // DB: 2 residual/fp32 + 1 bf16 buffer
+  static constexpr int BAR_OFF = STG_OFF + EPW * STG_WARP;
+  static constexpr int SMEM = BAR_OFF + 1024 + 512;
   static constexpr int THREADS = 128 + EPW * 32;
   static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((AK ? 0u : 1u) << 15) |
                                     ((BKM ? 0u : 1u) << 16) | (static_cast<uint32_t>(BN >> 3) << 17) |
                                     (static_cast<uint32_t>(256 >> 4) << 24);
 };
 
-template <int BN, int STAGES, bool AK, bool BKM, int EPW>
-__global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
+template <int BN, int STAGES, bool AK, bool BKM, int EPW, bool DB>
+__global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                     const __grid_constant__ OutMaps om, GemmShape g, Epi e) {
-  using C = Cfg2<BN, STAGES, AK, BKM, EPW>;
+  using C = Cfg2<BN, STAGES, AK, BKM, EPW, DB>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
-  uint64_t* ebar = tempty + 2;       // [EPW] epilogue TMA-load barriers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + EPW);
+  uint64_t* ebar = tempty + 2;       // [2 * EPW] epilogue TMA-load barriers (2 per warp in DB)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 2 * EPW);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -897,7 +968,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2 * EPW * 32);
     }
-    for (int w = 0; w < EPW; ++w) mbar_init(&ebar[w], 1);
+    for (int w = 0; w < 2 * EPW; ++w) mbar_init(&ebar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
@@ -982,8 +1053,8 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
     const bool vec = al(e.c32, e.ldc32, 4) && al(e.cT, e.ldcT, 2) && al(e.resid, e.ldr, 4) &&
                      al(e.aux, e.ld_aux, 2) && al(e.bias, 0, 4);
     const uint32_t tempty_leader0 = leader_addr(&tempty[0]), tempty_leader1 = leader_addr(&tempty[1]);
-    const uint32_t stg = smem_u32(smem + C::STG_OFF + ew * kStageBytes);
-    uint32_t ephase = 0;
+    const uint32_t stg = smem_u32(smem + C::STG_OFF + ew * C::STG_WARP);
+    uint32_t ephase = 0, eph2[2] = {0, 0};
     int i = 0;
     for (int t = pair; t < ntile; t += npairs, ++i) {
       const int m0 = (t % tiles_m) * 256 + static_cast<int>(rank) * 128, n0 = (t / tiles_m) * BN;
@@ -992,9 +1063,12 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
       mbar_wait_sleep(&tfull[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      if (e.tma)
+      if (DB && (e.tma & 4))
+        epilogue_resid_db(g, e, om, taddr, m0 + q * 32, n0, slice * CW, (slice + 1) * CW, stg, lane, &ebar[2 * ew],
+                          eph2);
+      else if (e.tma)
         epilogue_store_tma(g, e, om, taddr, m0 + q * 32 + lane, m0 + q * 32, n0, slice * CW, (slice + 1) * CW, stg,
-                           lane, &ebar[ew], ephase);
+                           lane, &ebar[2 * ew], ephase);
       else
         epilogue_store(g, e, taddr, m0 + q * 32 + lane, n0, slice * CW, (slice + 1) * CW, vec);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1012,11 +1086,11 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
   }
 }
 
-template <int BN, int STAGES, bool AK, bool BKM>
+template <int BN, int STAGES, bool AK, bool BKM, bool DB = false>
 void launch2(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& om, const GemmShape& g,
              const Epi& e) {
-  using C = Cfg2<BN, STAGES, AK, BKM, 8>;
-  auto k = gemm_tc2_kernel<BN, STAGES, AK, BKM, 8>;
+  using C = Cfg2<BN, STAGES, AK, BKM, 8, DB>;
+  auto k = gemm_tc2_kernel<BN, STAGES, AK, BKM, 8, DB>;
   static bool attr = false;
   if (!attr) {
     DCU_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -1063,13 +1137,13 @@ int use_pair_default() {
 }  // namespace
 
 // cta_group::2 GEMM for 256-row-multiple-friendly shapes. Returns false if not TMA-legal.
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool DB = false>
 void dispatch_pair(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& om, const GemmShape& g,
                    const Epi& e) {
-  if (g.a_kmajor && g.b_kmajor) launch2<BN, STAGES, true, true>(s, ma, mb, om, g, e);
-  else if (g.a_kmajor) launch2<BN, STAGES, true, false>(s, ma, mb, om, g, e);
-  else if (g.b_kmajor) launch2<BN, STAGES, false, true>(s, ma, mb, om, g, e);
-  else launch2<BN, STAGES, false, false>(s, ma, mb, om, g, e);
+  if (g.a_kmajor && g.b_kmajor) launch2<BN, STAGES, true, true, DB>(s, ma, mb, om, g, e);
+  else if (g.a_kmajor) launch2<BN, STAGES, true, false, DB>(s, ma, mb, om, g, e);
+  else if (g.b_kmajor) launch2<BN, STAGES, false, true, DB>(s, ma, mb, om, g, e);
+  else launch2<BN, STAGES, false, false, DB>(s, ma, mb, om, g, e);
 }
 
 // cta_group::2 GEMM with 256 x BN tiles (BN 256 or 128). Returns false if not TMA-legal.
@@ -1083,7 +1157,11 @@ bool gemm_tc_pair(cudaStream_t s, const GemmShape& g, const Epi& e, int BN) {
   memset(&om, 0, sizeof(om));
   Epi et = e;
   et.tma = out_maps_for(g, e, &om);
-  if (BN == 256) dispatch_pair<256, 6>(s, ma, mb, om, g, et);  // 6 x 32 KB stages
+  // residual epilogues (fp32 resid in, fp32 + bf16 out): 4 x 32 KB stages and the
+  // double-buffered residual prefetch (DASHCU_GEMM_RESID_DB=0 disables)
+  const char* rdb = getenv("DASHCU_GEMM_RESID_DB");
+  if (BN == 256 && (et.tma & 4) && !(rdb && rdb[0] == '0')) dispatch_pair<256, 4, true>(s, ma, mb, om, g, et);
+  else if (BN == 256) dispatch_pair<256, 6>(s, ma, mb, om, g, et);  // 6 x 32 KB stages
   else dispatch_pair<128, 8>(s, ma, mb, om, g, et);            // 8 x 24 KB stages
   return true;
 }

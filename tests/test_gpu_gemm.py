@@ -132,3 +132,23 @@ def test_cta_pair_tiles(ctx, monkeypatch, pair, ak, bk, shape):
     Bst = B if bk else np.ascontiguousarray(B.T)
     got = ctx.selftest_gemm(Ast, ak, Bst, bk, M, N, K)
     assert np.abs(got - ref).max() / max(1.0, np.abs(ref).max()) < 1e-5
+
+
+@pytest.mark.parametrize("shape", [(300, 200, 136), (4096, 896, 896), (1000, 1152, 320)])
+def test_pair_residual_prefetch_epilogue(ctx, monkeypatch, shape):
+    """The CTA-pair kernel's double-buffered residual epilogue (fp32 resid in, fp32 out)
+    equals the per-thread direct-store epilogue bit-for-bit, ragged edges included."""
+    M, N, K = shape
+    rng = np.random.default_rng(17)
+    A = bf16_bits(rng.standard_normal((M, K)).astype(np.float32) * 0.1)
+    B = bf16_bits(rng.standard_normal((N, K)).astype(np.float32) * 0.1)
+    bias = rng.standard_normal(N).astype(np.float32)
+    c0 = rng.standard_normal((M, N)).astype(np.float32)
+    monkeypatch.setenv("DASHCU_GEMM_PAIR", "1")
+    got = ctx.selftest_gemm(A, True, B, True, M, N, K, bias=bias, epi=4, C_init=c0)
+    monkeypatch.setenv("DASHCU_GEMM_RESID_DB", "0")
+    mid = ctx.selftest_gemm(A, True, B, True, M, N, K, bias=bias, epi=4, C_init=c0)
+    monkeypatch.setenv("DASHCU_NO_TMA_STORE", "1")
+    ref = ctx.selftest_gemm(A, True, B, True, M, N, K, bias=bias, epi=4, C_init=c0)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+    assert np.array_equal(mid.view(np.uint32), ref.view(np.uint32))
