@@ -16,11 +16,17 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 
+#ifndef DASHCU_DEC_ST
+#define DASHCU_DEC_ST 3
+#endif
+#ifndef DASHCU_DEC_NW
+#define DASHCU_DEC_NW 4
+#endif
 template <int HD>
 struct DecCfg {
   static constexpr int KC = 32;             // keys per chunk
-  static constexpr int ST = 3;              // pipeline stages
-  static constexpr int NW = HD == 64 ? 4 : 2;  // warps per CTA
+  static constexpr int ST = DASHCU_DEC_ST;  // pipeline stages (per warp)
+  static constexpr int NW = HD == 64 ? DASHCU_DEC_NW : 2;  // warps per CTA
   static constexpr int UNITS = HD / 8;      // 16-byte units per key row
   static constexpr int CHUNK_BYTES = KC * HD * 2;
   static constexpr int WARP_BYTES = ST * 2 * CHUNK_BYTES;  // K and V
