@@ -72,7 +72,21 @@ def build(verbose: bool = False) -> str:
             raise RuntimeError(f"link failed:\n{r.stderr}")
         with open(LIB + ".objs", "w") as f:
             f.write("\n".join(objs))
+    _prune_objs()
     return LIB
+
+
+def _prune_objs():
+    """Drop object files no library's .objs list references (old header digests)."""
+    keep = set()
+    for f in os.listdir(OUT_DIR):
+        if f.endswith(".objs"):
+            with open(os.path.join(OUT_DIR, f)) as fh:
+                keep.update(os.path.abspath(ln.strip()) for ln in fh if ln.strip())
+    for f in os.listdir(OBJ_DIR):
+        p = os.path.abspath(os.path.join(OBJ_DIR, f))
+        if f.endswith(".o") and p not in keep:
+            os.remove(p)
 
 
 def _stale_objs(objs):
