@@ -17,7 +17,7 @@ namespace {
 constexpr float kLog2e = 1.4426950408889634f;
 
 #ifndef DASHCU_DEC_ST
-#define DASHCU_DEC_ST 3
+#define DASHCU_DEC_ST 2  // 3 CTAs x 4 warps per SM; measured 3.6 % faster than 3 stages at 384 steps
 #endif
 #ifndef DASHCU_DEC_NW
 #define DASHCU_DEC_NW 4
