@@ -51,6 +51,7 @@ CONFIGS = {
 }
 C1_ARCH = dict(vocab_size=256, embed_dim=128, context_len=64, ffn_hidden=512, n_layers=2, bos_id=0, eos_id=1)
 # bounded CPU sample of the same workload for the reference arm / cpu_baseline
+PROF_PERIOD = 17
 REF_SAMPLE = dict(prompts=1, G=8, prompt_len=4, max_len=4)
 
 
@@ -263,6 +264,9 @@ def run_ours(args, cfg, world, rank, local):
     ctx.sync()
     clocks = Clocks(local)
     clocks.start()
+    # per-kernel events on one launch in PROF_PERIOD of each class (a prime, so the sampled
+    # launches cycle through every GEMM shape of a layer), scaled to the class totals
+    D.profile_sampling(PROF_PERIOD)
     D.profile_enable()
     D.profile_read(reset=True)
     l0 = D.kernel_launches()
@@ -316,7 +320,8 @@ def run_ours(args, cfg, world, rank, local):
         "gpu_launches": launches,
         "roofline": {"bound": "hbm" if hbm_bound else "tensor", "kernel": name, "achieved": achieved,
                      "peak": peak, "unit": unit, "frac": achieved / peak, "traffic": traffic,
-                     "per_launch_ms": per_launch_ms, "peak_source": pk["src"] + (" burst" if False else
+                     "per_launch_ms": per_launch_ms, "event_sampling": f"1 in {PROF_PERIOD} launches per class",
+                     "peak_source": pk["src"] + (" burst" if False else
                                                                                 " sustained" if not hbm_bound else "")},
         "phases_ms": {k: last[k] for k in ("sample_ms", "advantage_ms", "accumulate_ms", "allreduce_ms",
                                            "optimizer_ms")},

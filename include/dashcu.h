@@ -201,6 +201,10 @@ typedef struct {
   double ms, flops, bytes;
 } dashcu_kprof;
 DASHCU_API int dashcu_profile_enable(unsigned class_mask);
+/* Bracket only one launch in `period` (>= 1, default 1) of each enabled class with events
+ * (the rest are counted): profile_read then reports the sampled time / flops / bytes
+ * scaled to the class totals, at a fraction of the event overhead. */
+DASHCU_API int dashcu_profile_sampling(int period);
 DASHCU_API int dashcu_profile_read(dashcu_kprof* out, int max, int reset);
 /* With bit 31 of the class mask set, launches are also aggregated per key (kernel
  * variant + shape). Text, one line per key: "class key\tlaunches\tms\tflops\tbytes".

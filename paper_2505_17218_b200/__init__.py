@@ -139,6 +139,8 @@ def lib():
         L.dashcu_profile_enable.restype = C.c_int
         L.dashcu_profile_read.argtypes = [C.c_void_p, C.c_int, C.c_int]
         L.dashcu_profile_read.restype = C.c_int
+        L.dashcu_profile_sampling.argtypes = [C.c_int]
+        L.dashcu_profile_sampling.restype = C.c_int
         L.dashcu_profile_keys.argtypes = [C.c_char_p, C.c_int64]
         L.dashcu_profile_keys.restype = C.c_int64
         _lib = L
@@ -176,6 +178,11 @@ def profile_enable(classes=PROF_CLASSES, keys=False):
     if keys:
         mask |= 1 << 31
     lib().dashcu_profile_enable(C.c_uint(mask))
+
+
+def profile_sampling(period: int = 1):
+    """Event-bracket one launch in `period` per class; profile_read scales to class totals."""
+    lib().dashcu_profile_sampling(int(period))
 
 
 def profile_keys() -> list:

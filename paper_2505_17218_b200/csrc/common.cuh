@@ -86,6 +86,8 @@ enum ProfClass : int {
 };
 extern const char* const kProfNames[PROF_NUM];
 extern unsigned g_prof_mask;
+extern int g_prof_period;              // >= 1: bracket one launch in g_prof_period per class
+extern int64_t g_prof_seen[PROF_NUM];  // launches of each enabled class since the last reset
 void prof_begin(int cls, cudaStream_t s, cudaEvent_t* ev);
 void prof_end(int cls, cudaStream_t s, cudaEvent_t ev0, double flops, double bytes, const char* key);
 // mask bit 31: also aggregate per launch key (kernel variant + shape), see dashcu_profile_keys
@@ -99,7 +101,10 @@ struct ProfScope {
   bool on;
   char key[96];
   ProfScope(int c, cudaStream_t st, double f, double b) : cls(c), s(st), flops(f), bytes(b) {
+    // every launch of an enabled class is counted; one in g_prof_period is bracketed with
+    // events (profile_read scales the sampled time / flops / bytes to the class totals)
     on = (g_prof_mask >> c) & 1u;
+    if (on) on = (g_prof_seen[c]++ % g_prof_period) == 0;
     key[0] = 0;
     if (on) prof_begin(c, s, &ev);
   }

@@ -14,6 +14,8 @@ namespace dashcu {
 const char* const kProfNames[PROF_NUM] = {"gemm_tc",   "gemm_simt", "attn_decode", "attn_fwd",
                                           "attn_bwd",  "sample",    "lm_rows",     "optimizer"};
 unsigned g_prof_mask = 0;
+int g_prof_period = 1;
+int64_t g_prof_seen[PROF_NUM] = {};
 
 namespace {
 
@@ -99,6 +101,12 @@ void prof_end(int cls, cudaStream_t s, cudaEvent_t ev0, double flops, double byt
 
 extern "C" {
 
+DASHCU_API int dashcu_profile_sampling(int period) {
+  std::lock_guard<std::mutex> lk(dashcu::prof().mu);
+  dashcu::g_prof_period = period < 1 ? 1 : period;
+  return 0;
+}
+
 DASHCU_API int dashcu_profile_enable(unsigned class_mask) {
   std::lock_guard<std::mutex> lk(dashcu::prof().mu);
   dashcu::g_prof_mask = class_mask;
@@ -113,14 +121,17 @@ DASHCU_API int dashcu_profile_read(dashcu_kprof* out, int max, int reset) {
     p.drain();
     int n = 0;
     for (int c = 0; c < PROF_NUM && n < max; ++c, ++n) {
+      // sampled launches scaled to the class totals (exact when the sampling period is 1)
+      const int64_t total = std::max<int64_t>(g_prof_seen[c], p.launches[c]);
+      const double f = p.launches[c] ? static_cast<double>(total) / p.launches[c] : 0.0;
       snprintf(out[n].name, sizeof(out[n].name), "%s", kProfNames[c]);
-      out[n].launches = p.launches[c];
-      out[n].ms = p.ms[c];
-      out[n].flops = p.flops[c];
-      out[n].bytes = p.bytes[c];
+      out[n].launches = total;
+      out[n].ms = p.ms[c] * f;
+      out[n].flops = p.flops[c] * f;
+      out[n].bytes = p.bytes[c] * f;
     }
     if (reset) {
-      for (int c = 0; c < PROF_NUM; ++c) p.ms[c] = p.flops[c] = p.bytes[c] = 0, p.launches[c] = 0;
+      for (int c = 0; c < PROF_NUM; ++c) p.ms[c] = p.flops[c] = p.bytes[c] = 0, p.launches[c] = 0, g_prof_seen[c] = 0;
       p.keys.clear();
     }
     return n;
