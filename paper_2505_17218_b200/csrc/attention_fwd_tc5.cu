@@ -10,7 +10,7 @@
 //   registers: acc = acc * 2^(m_{j-1} - m_j) + O_j,  l likewise; out = acc / l, LSE = m + log l.
 // S and O are double-buffered in TMEM so the MMA of S_{j+1} and of O_j overlap the softmax.
 // Warp roles: 0 TMA producer (Q once, K/V kST-stage ring), 1 MMA issuer, 2 TMEM allocator,
-// 4..7 softmax (one thread per query row; TMEM lane quarter = warp % 4).
+// 4..11 softmax (TMEM lane quarter = warp % 4; two warps per quarter split the columns).
 #include <cfloat>
 #include <cstdlib>
 #include <string>
@@ -37,7 +37,8 @@ constexpr int kST = 4;  // K/V pipeline depth: loads run 3 key tiles ahead of th
 struct FLay {
   static constexpr int Q = 0 /*2 stages*/, K = 2 * kTile /*kST stages*/, V = (2 + kST) * kTile /*kST stages*/;
   static constexpr int P = (2 + 2 * kST) * kTile;  // P [128 q x 128 keys] bf16: two 64-key swizzle atoms
-  static constexpr int BAR = P + 2 * kTile;
+  static constexpr int XMAX = P + 2 * kTile;  // row-max exchange [2][2][128] + row sums [2][128]
+  static constexpr int BAR = XMAX + 4096;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
@@ -59,7 +60,7 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_fwd_tc5_k(const __grid_constant__ CUtensorMap mQKV, const int32_t* __restrict__ seq_start, int nh, int nkv,
                    int nqt_max, bf16* __restrict__ ctx, float* __restrict__ lse, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
@@ -99,11 +100,11 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&qfull[i], 1);
       mbar_init(&qempty[i], 1);
       mbar_init(&sfull[i], 1);
-      mbar_init(&sfree[i], 128);
+      mbar_init(&sfree[i], 256);
       mbar_init(&ofull[i], 1);
-      mbar_init(&ofree[i], 128);
+      mbar_init(&ofree[i], 256);
     }
-    mbar_init(pready, 128);
+    mbar_init(pready, 256);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mQKV)) : "memory");
   }
@@ -169,87 +170,88 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {  // ---------------------------------------------------------- softmax
-    const int qq = warp & 3, r = qq * 32 + lane, q = q0 + r;
+    // 8 warps: TMEM lane quarter qq = warp % 4 (query rows 32 qq ..), column half hf: keys
+    // [64 hf, 64 hf + 64) of S and head dims [32 hf, 32 hf + 32) of O. The two warps of a
+    // quarter exchange their row maxima through shared memory once per tile (named barrier
+    // 1 + qq, 64 threads); their row sums stay separate until the end.
+    const int qq = warp & 3, hf = (warp - 4) >> 2, r = qq * 32 + lane, q = q0 + r;
     const uint32_t lanes = static_cast<uint32_t>(qq * 32) << 16;
-    float acc[kHD];
+    float* xmax = reinterpret_cast<float*>(smem + FLay::XMAX);  // [2 parity][2 halves][128 rows]
+    float acc[kHD / 2];
     float m, m_prev, l;
-    // O_t (TMEM) into the register accumulator: acc = acc * 2^(m_old - m_new) + O_t
+    // O_t (TMEM, this warp's 32 head dims) into the registers: acc = acc * 2^(m_old - m_new) + O_t
     auto take_o = [&](int t, float m_old, float m_new) {
       const int sb = t & 1;
       mbar_wait_sleep(&ofull[sb], (t >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      uint32_t o[kHD];
-      tmem_ld32_async(tmem + lanes + (sb ? kTO1 : kTO0), o);
-      tmem_ld32_async(tmem + lanes + (sb ? kTO1 : kTO0) + 32, o + 32);
+      uint32_t o[kHD / 2];
+      tmem_ld32_async(tmem + lanes + (sb ? kTO1 : kTO0) + hf * 32, o);
       tmem_wait_ld();
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&ofree[sb]);
       const float c = ex2(m_old - m_new);
       const uint64_t c2 = f2_pack(c, c);
 #pragma unroll
-      for (int i = 0; i < kHD; i += 2)  // packed fp32x2 FMAs
+      for (int i = 0; i < kHD / 2; i += 2)  // packed fp32x2 FMAs
         f2_unpack(f2_fma(f2_pack(acc[i], acc[i + 1]), c2, f2_pack(__uint_as_float(o[i]), __uint_as_float(o[i + 1]))),
                   acc[i], acc[i + 1]);
     };
     for (int hh = 0, t = 0; hh < grp; ++hh) {
       const int h = kvh * grp0 + h_lo + hh;
 #pragma unroll
-      for (int i = 0; i < kHD; ++i) acc[i] = 0.f;
+      for (int i = 0; i < kHD / 2; ++i) acc[i] = 0.f;
       m = -FLT_MAX, m_prev = -FLT_MAX, l = 0.f;
       for (int j = 0; j < nkt; ++j, ++t) {
         const int sb = t & 1;
         mbar_wait_sleep(&sfull[sb], (t >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        uint32_t sr[kKeys];
-#pragma unroll
-        for (int c = 0; c < kKeys; c += 32) tmem_ld32_async(tmem + lanes + (sb ? kTS1 : kTS0) + c, sr + c);
+        uint32_t sr[64];
+        tmem_ld32_async(tmem + lanes + (sb ? kTS1 : kTS0) + hf * 64, sr);
+        tmem_ld32_async(tmem + lanes + (sb ? kTS1 : kTS0) + hf * 64 + 32, sr + 32);
         tmem_wait_ld();
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         mbar_arrive(&sfree[sb]);
         float* sv = reinterpret_cast<float*>(sr);  // raw scores; 1/sqrt(d) * log2(e) goes into the exponent
-        if (j == qt) {  // causal diagonal: key j*128 + c > q is masked
+        if (j == qt) {  // causal diagonal: key j*128 + 64 hf + c > q is masked
 #pragma unroll
-          for (int c = 0; c < kKeys; ++c) sv[c] = (j * kKeys + c <= q) ? sv[c] : -FLT_MAX;
+          for (int c = 0; c < 64; ++c) sv[c] = (j * kKeys + hf * 64 + c <= q) ? sv[c] : -FLT_MAX;
         }
         float tm[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          tm[i] = sv[i];
-#pragma unroll
-          for (int k = 1; k < 8; ++k) tm[i] = fmaxf(tm[i], sv[i + 16 * k]);
-        }
+        for (int i = 0; i < 16; ++i) tm[i] = fmaxf(fmaxf(sv[i], sv[i + 16]), fmaxf(sv[i + 32], sv[i + 48]));
 #pragma unroll
         for (int w = 8; w >= 1; w >>= 1)
 #pragma unroll
           for (int i = 0; i < w; ++i) tm[i] = fmaxf(tm[i], tm[i + w]);
-        const float m_new = fmaxf(m, tm[0] * scale_log2);
+        // row max over both halves: publish, pair barrier, read the partner's
+        float* xm = xmax + (t & 1) * 256;
+        xm[hf * 128 + r] = tm[0];
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + qq) : "memory");
+        const float m_new = fmaxf(m, fmaxf(tm[0], xm[(hf ^ 1) * 128 + r]) * scale_log2);
         uint64_t rs2[2] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
-        uint32_t pk[kKeys / 2];
+        uint32_t pk[32];
         const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nm2 = f2_pack(-m_new, -m_new);
 #pragma unroll
-        for (int c = 0; c < kKeys; c += 2) {  // exponent arguments and row sums on the fp32x2 pipe
+        for (int c = 0; c < 64; c += 2) {  // exponent arguments and row sums on the fp32x2 pipe
           float a0, a1;
           f2_unpack(f2_fma(f2_pack(sv[c], sv[c + 1]), sc2, nm2), a0, a1);
           const float p0 = ex2(a0);
-          const float p1 = kSplitExp ? ex2_poly(a1) : ex2(a1);  // optionally half on the FMA pipe
+          const float p1 = kSplitExp ? ex2_poly(a1) : ex2(a1);
           rs2[(c >> 1) & 1] = f2_add(rs2[(c >> 1) & 1], f2_pack(p0, p1));
           pk[c >> 1] = pack2(p0, p1);
         }
         float r0, r1, r2, r3;
         f2_unpack(rs2[0], r0, r1);
         f2_unpack(rs2[1], r2, r3);
-        l = l * ex2(m - m_new) + ((r0 + r1) + (r2 + r3));
+        l = l * ex2(m - m_new) + ((r0 + r1) + (r2 + r3));  // this half's share of the row sum
         // P_t overwrites P_{t-1}: the MMA of O_{t-1} must be complete
         if (t > 0) mbar_wait_sleep(&ofull[(t - 1) & 1], ((t - 1) >> 1) & 1);
 #pragma unroll
-        for (int a = 0; a < 2; ++a)
-#pragma unroll
-          for (int ch = 0; ch < 8; ++ch)
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sP + a * kTile + r * 128 +
-                                                                           ((ch ^ (r & 7)) << 4)),
-                         "r"(pk[a * 32 + ch * 4]), "r"(pk[a * 32 + ch * 4 + 1]), "r"(pk[a * 32 + ch * 4 + 2]),
-                         "r"(pk[a * 32 + ch * 4 + 3])
-                         : "memory");
+        for (int ch = 0; ch < 8; ++ch)  // keys [64 hf, 64 hf + 64) = swizzle atom hf of P
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sP + hf * kTile + r * 128 +
+                                                                         ((ch ^ (r & 7)) << 4)),
+                       "r"(pk[ch * 4]), "r"(pk[ch * 4 + 1]), "r"(pk[ch * 4 + 2]), "r"(pk[ch * 4 + 3])
+                       : "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(pready);
         if (j > 0) take_o(t - 1, m_prev, m);
@@ -257,11 +259,17 @@ __global__ void __launch_bounds__(256, 1)
         m = m_new;
       }
       take_o(t - 1, m_prev, m);
+      // full row sum = both halves' shares (same running max in both)
+      float* xl = xmax + 512;
+      xl[hf * 128 + r] = l;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + qq) : "memory");
+      const float lt = l + xl[(hf ^ 1) * 128 + r];
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + qq) : "memory");  // xl reused by the next head
       if (q < n) {
-        const float inv = 1.f / l;
-        bf16* out = ctx + static_cast<int64_t>(s0 + q) * qd + h * kHD;
+        const float inv = 1.f / lt;
+        bf16* out = ctx + static_cast<int64_t>(s0 + q) * qd + h * kHD + hf * 32;
 #pragma unroll
-        for (int i = 0; i < kHD; i += 8) {
+        for (int i = 0; i < kHD / 2; i += 8) {
           uint4 v;
           v.x = pack2(acc[i] * inv, acc[i + 1] * inv);
           v.y = pack2(acc[i + 2] * inv, acc[i + 3] * inv);
@@ -269,7 +277,7 @@ __global__ void __launch_bounds__(256, 1)
           v.w = pack2(acc[i + 6] * inv, acc[i + 7] * inv);
           *reinterpret_cast<uint4*>(out + i) = v;
         }
-        lse[static_cast<int64_t>(s0 + q) * nh + h] = (m + __log2f(l)) * 0.6931471805599453f;
+        if (hf == 0) lse[static_cast<int64_t>(s0 + q) * nh + h] = (m + __log2f(lt)) * 0.6931471805599453f;
       }
     }
   }
@@ -298,7 +306,7 @@ bool attn_fwd_tc5(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int
   }
   const int nqt = (max_len + kQ - 1) / kQ;
   dim3 grid(n_seq * nkv, 2 * nqt);
-  attn_fwd_tc5_k<<<grid, 256, FLay::BYTES, s>>>(mq, seq_start, nh, nkv, nqt, ctx, lse,
+  attn_fwd_tc5_k<<<grid, 384, FLay::BYTES, s>>>(mq, seq_start, nh, nkv, nqt, ctx, lse,
                                                 1.4426950408889634f / sqrtf(static_cast<float>(hd)));
   DCU_LAUNCHED();
   return true;
