@@ -28,7 +28,7 @@
 
 namespace dashcu {
 
-#ifdef DASHCU_ATTN_TRACE
+#if defined(DASHCU_ATTN_TRACE) && DASHCU_ATTN_TRACE != 2
 // Debug builds only: clock64 timeline of CTA (0, 0), 16 slots per iteration (see TR()).
 __device__ unsigned long long g_attn_trace[64 * 16];
 #define TR(it, k)                                                                             \
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(384, 1)
 
 }  // namespace
 
-#ifdef DASHCU_ATTN_TRACE
+#if defined(DASHCU_ATTN_TRACE) && DASHCU_ATTN_TRACE != 2
 int attn_trace_read(unsigned long long* out, int n) {
   return cudaMemcpyFromSymbol(out, g_attn_trace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
 }

@@ -20,6 +20,23 @@
 
 namespace dashcu {
 
+#if defined(DASHCU_ATTN_TRACE) && DASHCU_ATTN_TRACE == 2
+// Debug builds only (-DDASHCU_ATTN_TRACE=2): clock64 timeline of CTA (0, 0), 16 slots per tile.
+__device__ unsigned long long g_attn_trace[64 * 16];
+#define TRF(t, k)                                                                             \
+  do {                                                                                        \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && (t) < 64)           \
+      g_attn_trace[(t) * 16 + (k)] = clock64();                                               \
+  } while (0)
+int attn_trace_read(unsigned long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_attn_trace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
+}
+#else
+#define TRF(t, k) \
+  do {            \
+  } while (0)
+#endif
+
 namespace {
 
 constexpr int kQ = 128, kKeys = 128, kHD = 64;
@@ -157,7 +174,9 @@ __global__ void __launch_bounds__(384, 1)
       for (int t = 0; t < ntiles; ++t) {
         const int sb = t & 1, st = t % kST;
         if (t + 1 < ntiles) issue_s(t + 1);
+        TRF(t, 0);
         mbar_wait_sleep(pready, t & 1);
+        TRF(t, 1);
         if (t >= 2) mbar_wait_sleep(&ofree[sb], ((t >> 1) - 1) & 1);  // O_{t-2} read out
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t v = sV + st * kTile;
@@ -167,6 +186,7 @@ __global__ void __launch_bounds__(384, 1)
                     smem_desc(v + kk * 2048, kTile, 1024), I_O, kk > 0);
         umma_commit(&kvempty[st]);
         umma_commit(&ofull[sb]);
+        TRF(t, 2);
       }
     }
   } else if (warp >= 4) {  // ---------------------------------------------------------- softmax
@@ -203,7 +223,9 @@ __global__ void __launch_bounds__(384, 1)
       m = -FLT_MAX, m_prev = -FLT_MAX, l = 0.f;
       for (int j = 0; j < nkt; ++j, ++t) {
         const int sb = t & 1;
+        if (warp == 4) TRF(t, 4);
         mbar_wait_sleep(&sfull[sb], (t >> 1) & 1);
+        if (warp == 4) TRF(t, 5);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         uint32_t sr[64];
         tmem_ld32_async(tmem + lanes + (sb ? kTS1 : kTS0) + hf * 64, sr);
@@ -226,7 +248,9 @@ __global__ void __launch_bounds__(384, 1)
         // row max over both halves: publish, pair barrier, read the partner's
         float* xm = xmax + (t & 1) * 256;
         xm[hf * 128 + r] = tm[0];
+        if (warp == 4) TRF(t, 6);
         asm volatile("bar.sync %0, 64;" ::"r"(1 + qq) : "memory");
+        if (warp == 4) TRF(t, 7);
         const float m_new = fmaxf(m, fmaxf(tm[0], xm[(hf ^ 1) * 128 + r]) * scale_log2);
         uint64_t rs2[2] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
         uint32_t pk[32];
@@ -245,7 +269,9 @@ __global__ void __launch_bounds__(384, 1)
         f2_unpack(rs2[1], r2, r3);
         l = l * ex2(m - m_new) + ((r0 + r1) + (r2 + r3));  // this half's share of the row sum
         // P_t overwrites P_{t-1}: the MMA of O_{t-1} must be complete
+        if (warp == 4) TRF(t, 8);
         if (t > 0) mbar_wait_sleep(&ofull[(t - 1) & 1], ((t - 1) >> 1) & 1);
+        if (warp == 4) TRF(t, 9);
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch)  // keys [64 hf, 64 hf + 64) = swizzle atom hf of P
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sP + hf * kTile + r * 128 +
@@ -254,7 +280,9 @@ __global__ void __launch_bounds__(384, 1)
                        : "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(pready);
+        if (warp == 4) TRF(t, 10);
         if (j > 0) take_o(t - 1, m_prev, m);
+        if (warp == 4) TRF(t, 11);
         m_prev = m;
         m = m_new;
       }

@@ -16,6 +16,11 @@ NAMES = {0: "mma:sfree", 1: "mma:S issued", 2: "mma:pready", 3: "mma:dqfree/456"
          11: "sm:h1 pfree", 12: "sm:h0 loaded", 13: "sm:h1 loaded", 14: "sm:pready"}
 
 
+FWD_NAMES = {0: "mma:S(t+1) issued", 1: "mma:pready", 2: "mma:PV issued", 4: "sm:wait sfull", 5: "sm:sfull",
+             6: "sm:max done", 7: "sm:pair barrier", 8: "sm:exp done", 9: "sm:ofull(t-1)", 10: "sm:pready",
+             11: "sm:take_o done"}
+
+
 def main():
     n_seq = int(sys.argv[1]) if len(sys.argv) > 1 else 4
     P, L = 128, 1024
@@ -31,6 +36,9 @@ def main():
     pol.grad_zero()
     pol.accumulate_weighted(w, micro_batch=n_seq)
     pol.accumulate_weighted(w, micro_batch=n_seq)
+    global NAMES
+    if os.environ.get("TRACE_FWD"):
+        NAMES = FWD_NAMES
     buf = (C.c_ulonglong * (64 * 16))()
     assert D.lib().dashcu_debug_attn_trace(buf, 64 * 16) == 0
     t = np.array(buf, dtype=np.int64).reshape(64, 16)
