@@ -47,6 +47,10 @@ constexpr bool kSplitExp = true;
 #else
 constexpr bool kSplitExp = false;
 #endif
+#ifndef DASHCU_SPLIT_EVERY
+#define DASHCU_SPLIT_EVERY 2
+#endif
+constexpr int kSplitEvery = DASHCU_SPLIT_EVERY;  // one pair in kSplitEvery uses ex2_poly for its odd element
 constexpr int kTile = 128 * kHD * 2;  // 16 KB
 
 constexpr int kST = 4;  // K/V pipeline depth: loads run 3 key tiles ahead of the MMAs
@@ -260,7 +264,8 @@ __global__ void __launch_bounds__(384, 1)
           float a0, a1;
           f2_unpack(f2_fma(f2_pack(sv[c], sv[c + 1]), sc2, nm2), a0, a1);
           const float p0 = ex2(a0);
-          const float p1 = kSplitExp ? ex2_poly(a1) : ex2(a1);
+          // a fraction of the exponentials on the FMA pipe (the exp loop is MUFU-bound)
+          const float p1 = (kSplitExp && ((c >> 1) % kSplitEvery == 0)) ? ex2_poly(a1) : ex2(a1);
           rs2[(c >> 1) & 1] = f2_add(rs2[(c >> 1) & 1], f2_pack(p0, p1));
           pk[c >> 1] = pack2(p0, p1);
         }
