@@ -40,9 +40,10 @@ int attn_trace_read(unsigned long long* out, int n) {
 namespace {
 
 constexpr int kQ = 128, kKeys = 128, kHD = 64;
-// -DDASHCU_SPLIT_EXP: half the softmax exponentials via ex2_poly (tc5.cuh). Measured
-// slower for the backward (its softmax warps are issue-bound, not MUFU-bound), neutral forward.
-#ifdef DASHCU_SPLIT_EXP
+// A quarter of the forward's exponentials via ex2_poly (tc5.cuh): its exp loop is bound by
+// the MUFU unit (16 ex2 / clock / SM); measured -2.5 % (a half: +1.7 %, issue-bound).
+// -DDASHCU_NO_SPLIT_EXP disables.
+#ifndef DASHCU_NO_SPLIT_EXP
 constexpr bool kSplitExp = true;
 #else
 constexpr bool kSplitExp = false;
