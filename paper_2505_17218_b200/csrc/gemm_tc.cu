@@ -534,8 +534,13 @@ __device__ __forceinline__ void epilogue_sample(const GemmShape& g, const Epi& e
         m1 = m;
       }
     }
-    float4* pp = reinterpret_cast<float4*>(sa.part + (static_cast<int64_t>(row) * sa.ntiles + (nb / kSlice)) * 4);
-    *pp = make_float4(m, Z, m1, Z1);
+    if (t1) {  // m1 = m, Z1 = Z: the compact 8-byte record halves the scan's traffic
+      float2* pp = reinterpret_cast<float2*>(sa.part + (static_cast<int64_t>(row) * sa.ntiles + (nb / kSlice)) * 2);
+      *pp = make_float2(m, Z);
+    } else {
+      float4* pp = reinterpret_cast<float4*>(sa.part + (static_cast<int64_t>(row) * sa.ntiles + (nb / kSlice)) * 4);
+      *pp = make_float4(m, Z, m1, Z1);
+    }
   }
 }
 

@@ -271,7 +271,8 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
                                                      const float* __restrict__ logits, int64_t logits_ld, int rows,
                                                      int V, int bos, int eos, float inv_t, const uint64_t* keys,
                                                      int step, const int32_t* cap, uint8_t* finished, int32_t* comp,
-                                                     float* logp, int32_t* len, int32_t* tok_next, int max_len) {
+                                                     float* logp, int32_t* len, int32_t* tok_next, int max_len,
+                                                     bool compact) {
   pdl_wait();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -280,12 +281,21 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
     if (lane == 0) tok_next[row] = eos;
     return;
   }
-  const float4* P = reinterpret_cast<const float4*>(part) + static_cast<int64_t>(row) * nslices;
+  // records {m, Z, m1, Z1}; at T = 1 the fused epilogue stores only {m, Z} (m1 = m, Z1 = Z)
+  const float4* P4 = reinterpret_cast<const float4*>(part) + static_cast<int64_t>(row) * nslices;
+  const float2* P2 = reinterpret_cast<const float2*>(part) + static_cast<int64_t>(row) * nslices;
+  auto rec = [&](int s) -> float4 {
+    if (compact) {
+      const float2 q = P2[s];
+      return make_float4(q.x, q.y, q.x, q.y);
+    }
+    return P4[s];
+  };
   const int B = (nslices + 31) / 32;
   const int s0 = lane * B, s1 = min(nslices, s0 + B);
   float M = -FLT_MAX, M1 = -FLT_MAX;
   for (int s = s0; s < s1; ++s) {
-    const float4 p = P[s];
+    const float4 p = rec(s);
     M = fmaxf(M, p.x);
     M1 = fmaxf(M1, p.z);
   }
@@ -293,7 +303,7 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
   M1 = warp_max(M1);
   float T = 0.f, L1 = 0.f;
   for (int s = s0; s < s1; ++s) {
-    const float4 p = P[s];
+    const float4 p = rec(s);
     T = __fadd_rn(T, __fmul_rn(p.y, sexp2(__fmul_rn(__fsub_rn(p.x, M), kLog2e))));
     L1 += p.w * __expf(p.z - M1);
   }
@@ -339,7 +349,7 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
       const int s = jb * B + k;
       float v = 0.f;
       if (s < nslices) {
-        const float4 p = P[s];
+        const float4 p = rec(s);
         v = __fmul_rn(p.y, sexp2(__fmul_rn(__fsub_rn(p.x, M), kLog2e)));
       }
       Sw[k] = v;
@@ -355,7 +365,7 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
     if (staged) {
       Ss = Sw[s - jb * B];
     } else {
-      const float4 p = P[s];
+      const float4 p = rec(s);
       Ss = __fmul_rn(p.y, sexp2(__fmul_rn(__fsub_rn(p.x, M), kLog2e)));
     }
     const float prev = r;
@@ -375,7 +385,7 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
     sbase = last_sbase;
   }
   // id search inside slice sb
-  const float4 p = P[sb];
+  const float4 p = rec(sb);
   const float scale = sexp2(__fmul_rn(__fsub_rn(p.x, M), kLog2e));
   const float* l = logits + static_cast<int64_t>(row) * logits_ld + sb * kSlice;
   int tk = -1, last_i = -1;
@@ -731,9 +741,10 @@ void lse_reduce(cudaStream_t s, const float* part, int ntiles, int rows, float* 
 
 void sample_scan(cudaStream_t s, const float* part, int nslices, const float* logits, int64_t logits_ld, int rows,
                  int V, int bos, int eos, float inv_t, const uint64_t* keys, int step, const int32_t* cap,
-                 uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len) {
+                 uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len,
+                 bool compact) {
   launch_pdl(sample_scan_k, dim3(cdiv(rows, 8)), dim3(256), 0, s, part, nslices, logits, logits_ld, rows, V, bos, eos,
-             inv_t, keys, step, cap, finished, comp, logp, len, tok_next, max_len);
+             inv_t, keys, step, cap, finished, comp, logp, len, tok_next, max_len, compact);
   DCU_LAUNCHED();
 }
 

@@ -761,7 +761,7 @@ struct Engine {
         const int nt = gemm_tc_sample(st, gs, W32(L.bout), sa);
         if (nt > 0) {
           sample_scan(st, part, nt, lg, ld, S, g.V, g.bos, g.eos, inv_t, d_keys, step, d_cap, d_fin,
-                      P.d_comp.as<int32_t>(), P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML);
+                      P.d_comp.as<int32_t>(), P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML, inv_t == 1.f);
           return;
         }
       }
@@ -840,7 +840,7 @@ struct Engine {
               sample_scan(st, sa.part, nt, sa.logits, g.V, R, g.V, g.bos, g.eos, inv_t, d_keys + r0, j,
                           d_cap + r0, d_fin + r0, P.d_comp.as<int32_t>() + static_cast<size_t>(r0) * ML,
                           P.d_logp.as<float>() + static_cast<size_t>(r0) * ML, P.d_len.as<int32_t>() + r0,
-                          d_tok + r0, ML);
+                          d_tok + r0, ML, inv_t == 1.f);
             }
             continue;
           }
