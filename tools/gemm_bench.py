@@ -19,6 +19,7 @@ SHAPES = {
     # residual-stream epilogue (fp32 resid in, fp32 + bf16 out)
     "dec_wo_res": (4096, 896, 896, 1, 1, 4), "dec_w2_res": (4096, 896, 4864, 1, 1, 4),
     "fwd_wo_res": (36864, 896, 896, 1, 1, 4), "dgrad_qkv_res": (36864, 896, 1152, 1, 0, 4),
+    "fwd_w2_res": (36864, 896, 4864, 1, 1, 4), "dgrad_w1_res": (36864, 896, 4864, 1, 0, 4),
     # small-output weight gradients (K = tokens of a micro-batch)
     "wgrad_wo": (896, 896, 36864, 0, 0, 3), "wgrad_qkv": (1152, 896, 36864, 0, 0, 3),
 }
