@@ -44,6 +44,12 @@ CONFIGS = {
     "c3": dict(size="1.5b", prompts=256, G=8, prompt_len=128, max_len=1024, micro=32, tau=0.1,
                workload="BASELINE configs[2] shard: Qwen2.5-1.5B-shaped, 2048 prompts x G=8 over 8 B200 "
                         "(256 prompts per B200), micro-batch 32"),
+    "c4": dict(size="3b", prompts=64, G=8, prompt_len=128, max_len=2048, micro=32, tau=0.1,
+               workload="BASELINE configs[3] shard: Qwen2.5-3B-shaped, gen len 2048, |A| filter 0.1, 512 prompts x G=8 "
+                        "over 8 B200 (64 prompts per B200)"),
+    "grpo": dict(size="0.5b", prompts=4, G=8, prompt_len=128, max_len=1024, micro=32, tau=None,
+                 workload="BASELINE configs[4] GRPO-style arm: Qwen2.5-0.5B-shaped, small sampling batch (4 prompts x "
+                          "G=8 per B200), no gradient filter"),
     "mini": dict(size="0.5b", prompts=64, G=8, prompt_len=128, max_len=128, micro=32, tau=0.1,
                  workload="development: Qwen2.5-0.5B-shaped, 64 prompts x G=8, gen len 128"),
     "c1": dict(size=None, prompts=64, G=8, prompt_len=7, max_len=57, micro=32, tau=0.1,
@@ -186,7 +192,8 @@ def ref_step_runner(cfg, threads):
     def run(step):
         st = O.RefStepStats()
         rc = R.ref_dash_step(O.arch_ref_vec(arch), O.ptr(params, O.f64p), O.ptr(toks, O.i32p), O.ptr(off, O.i64p),
-                             rs["prompts"], rs["G"], rs["max_len"], 1.0, 1000 + step, 0, 0, 3, None, cfg["tau"], 1,
+                             rs["prompts"], rs["G"], rs["max_len"], 1.0, 1000 + step, 0, 0, 3, None,
+                             float("-inf") if cfg["tau"] is None else cfg["tau"], 1,
                              1e-6, O.ptr(m, O.f64p), O.ptr(v, O.f64p), C.byref(t), threads, C.byref(st))
         if rc != 0:
             raise RuntimeError("reference step failed")
@@ -251,8 +258,11 @@ def run_ours(args, cfg, world, rank, local):
         adv, kept, nk = pol.advantage(tau=cfg["tau"])
         pol.grad_zero()
         pol.accumulate(1.0 / N_global, cfg["micro"])
-        pol.allreduce_grads()
-        pol.optimizer_step(D.OPT_ADAM, lr=1e-6)
+        if args.sharded:   # ZeRO-1 form: reduce-scatter, update own slice, all-gather
+            pol.sharded_step(D.OPT_ADAM, lr=1e-6)
+        else:
+            pol.allreduce_grads()
+            pol.optimizer_step(D.OPT_ADAM, lr=1e-6)
         st = pol.stats()
         wall = time.perf_counter() - t0
         dev = st["sample_ms"] + st["advantage_ms"] + st["accumulate_ms"] + st["allreduce_ms"] + st["optimizer_ms"]
@@ -313,8 +323,8 @@ def run_ours(args, cfg, world, rank, local):
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": cfg["workload"], "model": f"Qwen2.5-{cfg['size'] or 'tiny'}-shaped (reference math,"
                    f" GQA {arch.get('n_heads', 1)}/{arch.get('n_kv_heads', 1)})", "prompts_per_gpu": M, "G": G,
-                   "prompt_len": cfg["prompt_len"], "gen_len": ML, "micro_batch": cfg["micro"], "tau": cfg["tau"],
-                   "optimizer": "adam", "global_batch": M * G * world, "seq_len": cfg["prompt_len"] + ML,
+                   "prompt_len": cfg["prompt_len"], "gen_len": ML, "micro_batch": cfg["micro"], "tau": cfg["tau"] if cfg["tau"] is not None else "off",
+                   "optimizer": "adam (sharded, ZeRO-1)" if args.sharded else "adam", "global_batch": M * G * world, "seq_len": cfg["prompt_len"] + ML,
                    "parallelism": f"dp{world}", "l2": "inputs > L2 (KV cache + weights stream every step)"},
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
@@ -354,12 +364,16 @@ def main():
     ap.add_argument("--prompts", type=int, default=None)
     ap.add_argument("--max-len", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tau", default=None, help="filter threshold override; 'off' = no filter (GRPO-style)")
+    ap.add_argument("--sharded", action="store_true", help="ZeRO-1 style sharded optimizer step")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.prompts:
         cfg["prompts"] = args.prompts
     if args.max_len:
         cfg["max_len"] = args.max_len
+    if args.tau is not None:
+        cfg["tau"] = None if args.tau == "off" else float(args.tau)
     world, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, cfg, world, rank)

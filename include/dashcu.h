@@ -65,6 +65,11 @@ extern "C" {
 #define DASHCU_ADV_GIVEN 3         /* advantages passed in `adv` (in/out): normalize_std
                                       (advantage.cpp:114-133) and/or filter_by_threshold only */
 
+/* tau value meaning "no filter_by_threshold" (GRPO-style baseline):
+ * every sequence is kept, as group_advantage leaves AdvantageBatch::kept
+ * (advantage.cpp:92). Any other tau < 0 is an InputError (advantage.cpp:136). */
+#define DASHCU_FILTER_OFF (-__builtin_inf())
+
 /* optimizers */
 #define DASHCU_OPT_SGD 0
 #define DASHCU_OPT_ADAM 1
@@ -187,6 +192,16 @@ DASHCU_API int dashcu_grad_upload(dashcu_policy* pol, const double* grad, int64_
 DASHCU_API int dashcu_allreduce_grads(dashcu_policy* pol);
 /* Ascent step on the fp32 master weights; refreshes the bf16 copy; bumps the version. */
 DASHCU_API int dashcu_optimizer_step(dashcu_policy* pol, const dashcu_opt* opt);
+/* ZeRO-1 style alternative to allreduce_grads + optimizer_step (the paper
+ * trains with ZeRO): reduce-scatter the gradient, update only this rank's
+ * slice [off, off+len) of the fp32 master weights with slice-sized Adam moments,
+ * all-gather the master and refresh the bf16 copy. A policy uses one form or the other
+ * for its whole life (InputError otherwise). After it the gradient buffer is valid only
+ * on this rank's slice. */
+DASHCU_API int dashcu_sharded_step(dashcu_policy* pol, const dashcu_opt* opt);
+/* The slice of a `total`-element flat vector rank `rank` of `world` owns in the sharded
+ * step (no device work). */
+DASHCU_API int dashcu_shard_span(int64_t total, int32_t world, int32_t rank, int64_t* off, int64_t* len);
 
 DASHCU_API int dashcu_get_stats(dashcu_policy* pol, dashcu_stats* out);
 

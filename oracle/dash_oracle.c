@@ -751,7 +751,10 @@ int dor_advantage_filter(const double* r, int n, int G, int kind, int normalize,
   if (n <= 0) return 1;                                   /* advantage.cpp:68 */
   if (kind != 0 && (G <= 0 || n % G != 0)) return 1;     /* :10-11 */
   if (kind == 2 && G < 2) return 1;                       /* :100-101 */
-  if (!(tau >= 0.0)) return 1;                            /* :136 */
+  /* tau = -INFINITY: no filter_by_threshold call at all, kept stays all 1 as
+   * group_advantage / single_path_advantage leave it (advantage.cpp:77, :92) */
+  const int no_filter = isinf(tau) && tau < 0;
+  if (!no_filter && !(tau >= 0.0)) return 1;              /* :136 */
   if (kind == 0) {
     double mean = 0.0;
     for (int i = 0; i < n; ++i) mean += r[i];
@@ -785,7 +788,7 @@ int dor_advantage_filter(const double* r, int n, int G, int kind, int normalize,
   }
   int32_t k = 0;
   for (int i = 0; i < n; ++i) {
-    kept[i] = (uint8_t)(fabs(adv[i]) > tau);
+    kept[i] = (uint8_t)(no_filter || fabs(adv[i]) > tau);
     if (kept[i]) kept_idx[k++] = i;
   }
   *n_kept = k;

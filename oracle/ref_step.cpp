@@ -122,7 +122,9 @@ REF_API int ref_dash_step(const int32_t* arch_i, double* params, const int32_t* 
         r[i] = dash::reward(task, inst, trajs[i]).r;
       }
     }
-    auto adv = dash::filter_by_threshold(dash::group_advantage(r, dash::GroupIndex::contiguous(n, G)), tau);
+    // tau = -inf: no filter_by_threshold call (GRPO-style arm), group_advantage keeps all
+    auto adv = dash::group_advantage(r, dash::GroupIndex::contiguous(n, G));
+    if (!(std::isinf(tau) && tau < 0)) adv = dash::filter_by_threshold(adv, tau);
     std::vector<int> kept_idx;
     for (int i = 0; i < n; ++i)
       if (adv.kept[i]) kept_idx.push_back(i);

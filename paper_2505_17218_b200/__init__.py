@@ -22,7 +22,15 @@ LIB_PATH = os.environ.get("DASHCU_LIB_PATH") or os.path.join(PKG, "lib", "libdas
 OK, E_INPUT, E_CAPACITY, E_ON_POLICY, E_DEVICE = 0, 1, 2, 3, 4
 F32, BF16 = 0, 1
 ADV_SINGLE_PATH, ADV_GROUP, ADV_LEAVE_ONE_OUT = 0, 1, 2
+FILTER_OFF = float("-inf")  # DASHCU_FILTER_OFF: no filter_by_threshold, every sequence kept
 OPT_SGD, OPT_ADAM = 0, 1
+
+
+def shard_span(total: int, world: int, rank: int):
+    """(offset, length) of rank's slice in the sharded optimizer step (dashcu_shard_span)."""
+    off, n = C.c_int64(0), C.c_int64(0)
+    _check(lib().dashcu_shard_span(total, world, rank, C.byref(off), C.byref(n)))
+    return off.value, n.value
 
 
 class DashError(RuntimeError):
@@ -125,8 +133,11 @@ def lib():
             "dashcu_accumulate": [vp, C.c_double, C.c_int32],
             "dashcu_accumulate_weighted": [vp, f64p, C.c_int32, C.c_int32],
             "dashcu_grad_download": [vp, f64p, C.c_int64],
+            "dashcu_grad_upload": [vp, f64p, C.c_int64],
             "dashcu_allreduce_grads": [vp],
             "dashcu_optimizer_step": [vp, C.POINTER(Opt)],
+            "dashcu_sharded_step": [vp, C.POINTER(Opt)],
+            "dashcu_shard_span": [C.c_int64, C.c_int32, C.c_int32, i64p, i64p],
             "dashcu_get_stats": [vp, C.POINTER(Stats)],
             "dashcu_selftest_gemm": [vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint16), C.c_int64, C.c_int,
                                      C.POINTER(C.c_uint16), C.c_int64, C.c_int, f32p, C.c_int, C.c_int, f32p],
@@ -237,6 +248,7 @@ class Context:
     def advantage_filter(self, rewards, group_size, kind=ADV_GROUP, normalize=False, eps=0.0, tau=0.0):
         """group_advantage / normalize_std / filter_by_threshold (advantage.cpp:80-140) on the device."""
         r = np.ascontiguousarray(rewards, dtype=np.float64)
+        tau = FILTER_OFF if tau is None else tau
         n = int(r.shape[0])
         adv = np.zeros(max(n, 1))
         kept = np.zeros(max(n, 1), dtype=np.uint8)
@@ -371,6 +383,7 @@ class Policy:
 
     def advantage(self, kind=ADV_GROUP, normalize=False, eps=0.0, tau=0.1):
         n = self.stats()["n_seq"]
+        tau = FILTER_OFF if tau is None else tau   # None: no filter (GRPO-style), every sequence kept
         adv = np.zeros(max(n, 1))
         kept = np.zeros(max(n, 1), dtype=np.uint8)
         nk = C.c_int32(0)
@@ -394,12 +407,21 @@ class Policy:
         _check(lib().dashcu_grad_download(self.h, _p(out, f64p), self.n_params))
         return out
 
+    def grad_upload(self, grad):
+        g = np.ascontiguousarray(grad, dtype=np.float64)
+        _check(lib().dashcu_grad_upload(self.h, _p(g, f64p), g.shape[0]))
+
     def allreduce_grads(self):
         _check(lib().dashcu_allreduce_grads(self.h))
 
     def optimizer_step(self, kind=OPT_ADAM, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8):
         o = Opt(kind, lr, beta1, beta2, eps)
         _check(lib().dashcu_optimizer_step(self.h, C.byref(o)))
+
+    def sharded_step(self, kind=OPT_ADAM, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8):
+        """reduce-scatter + update of this rank's slice + all-gather (dashcu_sharded_step)."""
+        o = Opt(kind, lr, beta1, beta2, eps)
+        _check(lib().dashcu_sharded_step(self.h, C.byref(o)))
 
     def stats(self) -> dict:
         s = Stats()

@@ -86,6 +86,8 @@ struct NcclApi {
   decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
   decltype(&ncclCommInitRank) CommInitRank = nullptr;
   decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclReduceScatter) ReduceScatter = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
   decltype(&ncclCommDestroy) CommDestroy = nullptr;
   decltype(&ncclGetErrorString) GetErrorString = nullptr;
   static NcclApi& get() {
@@ -97,6 +99,8 @@ struct NcclApi {
       r.GetUniqueId = (decltype(r.GetUniqueId))dlsym(h, "ncclGetUniqueId");
       r.CommInitRank = (decltype(r.CommInitRank))dlsym(h, "ncclCommInitRank");
       r.AllReduce = (decltype(r.AllReduce))dlsym(h, "ncclAllReduce");
+      r.ReduceScatter = (decltype(r.ReduceScatter))dlsym(h, "ncclReduceScatter");
+      r.AllGather = (decltype(r.AllGather))dlsym(h, "ncclAllGather");
       r.CommDestroy = (decltype(r.CommDestroy))dlsym(h, "ncclCommDestroy");
       r.GetErrorString = (decltype(r.GetErrorString))dlsym(h, "ncclGetErrorString");
       r.ok = r.GetUniqueId && r.CommInitRank && r.AllReduce && r.CommDestroy;
@@ -210,6 +214,16 @@ void validate_arch(const dashcu_arch& a) {
   if (g.nh < 1 || g.nkv < 1 || g.hd < 1 || g.nh % g.nkv != 0) bad("n_heads must be a multiple of n_kv_heads");
 }
 
+// Slice of the flat parameter vector owned by `rank` in the sharded update: equal slices of
+// ceil(total / world) rounded up to 64 elements (256-byte aligned fp32 chunks for the
+// collectives); the last rank's slice is short (len may be 0 past the end).
+void shard_span(int64_t total, int world, int rank, int64_t* off, int64_t* len, int64_t* slice) {
+  const int64_t s = ((total + world - 1) / world + 63) / 64 * 64;
+  *off = s * rank;
+  *len = std::max<int64_t>(0, std::min<int64_t>(s, total - *off));
+  if (slice) *slice = s;
+}
+
 // -------------------------------------------------------------------- ctx
 
 }  // namespace dashcu
@@ -232,6 +246,11 @@ struct dashcu_policy {
   dashcu_arch arch{};
   int dtype = DASHCU_F32;
   dashcu::DevMem w32, wT, g32, am, av;
+  // Flat buffers are padded to shard_world * shard_len elements (dashcu_shard_span) so the
+  // sharded update can reduce-scatter / all-gather in place; the padding stays zero.
+  int64_t padded = 0;
+  int shard_world = 1;
+  int opt_state = -1;  // -1 none yet, 0 full Adam moments (optimizer_step), 1 this rank's slice (sharded_step)
   int64_t adam_t = 0;
   uint64_t version = 1;
   // rollout (SPEC.md RolloutCache: write-once per round, served whole)
@@ -923,6 +942,25 @@ void refresh_working_copy(Pol* p) {
   if (p->dtype == DASHCU_BF16) cast_f32_bf16(p->ctx->stream, p->w32.as<float>(), p->wT.as<bf16>(), p->lay.total);
 }
 
+// Adam moments: `n` elements, zeroed on first allocation; state 0 = full, 1 = slice.
+void ensure_moments(Pol* p, int64_t n, int state) {
+  if (p->opt_state == state) return;
+  p->am.ensure(static_cast<size_t>(n) * 4);
+  p->av.ensure(static_cast<size_t>(n) * 4);
+  DCU_CHECK(cudaMemsetAsync(p->am.p, 0, static_cast<size_t>(n) * 4, p->ctx->stream));
+  DCU_CHECK(cudaMemsetAsync(p->av.p, 0, static_cast<size_t>(n) * 4, p->ctx->stream));
+  p->opt_state = state;
+}
+
+// Adam bias corrections 1 - beta^t for the step about to run; SGD: 1.
+void bias_corrections(Pol* p, const dashcu_opt* o, float* c1, float* c2) {
+  *c1 = *c2 = 1.f;
+  if (o->kind != DASHCU_OPT_ADAM) return;
+  ++p->adam_t;
+  *c1 = static_cast<float>(1.0 - std::pow(o->beta1, static_cast<double>(p->adam_t)));
+  *c2 = static_cast<float>(1.0 - std::pow(o->beta2, static_cast<double>(p->adam_t)));
+}
+
 void validate_tokens(const Geo& g, const int32_t* t, int64_t n, bool completion) {
   for (int64_t i = 0; i < n; ++i) {
     if (t[i] < 0 || t[i] >= g.V) throw Error(1, "token out of vocab");
@@ -1055,16 +1093,18 @@ int dashcu_policy_create(dashcu_ctx* c, const dashcu_arch* a, int dtype, dashcu_
   p->g = geo_of(*a);
   p->lay = lay_of(p->g);
   p->dtype = dtype;
-  const size_t n = static_cast<size_t>(p->lay.total);
+  int64_t so, sl, slice;
+  shard_span(p->lay.total, c->world, c->rank, &so, &sl, &slice);
+  p->shard_world = c->world;
+  p->padded = slice * c->world;
+  const size_t n = static_cast<size_t>(p->padded);
   p->w32.ensure(n * 4);
   p->g32.ensure(n * 4);
-  p->am.ensure(n * 4);
-  p->av.ensure(n * 4);
   if (dtype == DASHCU_BF16) p->wT.ensure(n * 2);
   DCU_CHECK(cudaMemsetAsync(p->w32.p, 0, n * 4, c->stream));
   DCU_CHECK(cudaMemsetAsync(p->g32.p, 0, n * 4, c->stream));
-  DCU_CHECK(cudaMemsetAsync(p->am.p, 0, n * 4, c->stream));
-  DCU_CHECK(cudaMemsetAsync(p->av.p, 0, n * 4, c->stream));
+  // Adam moments are allocated by the first update: full size (optimizer_step) or only
+  // this rank's slice (sharded_step)
   refresh_working_copy(p);
   DCU_CHECK(cudaStreamSynchronize(c->stream));
   p->launches0 = g_launches;
@@ -1275,7 +1315,8 @@ int dashcu_advantage_filter(dashcu_ctx* c, const double* rewards, int32_t n, int
   if (kind != DASHCU_ADV_SINGLE_PATH && (G <= 0 || n % G != 0))
     throw Error(1, "contiguous grouping requires group_size dividing n");
   if (kind == DASHCU_ADV_LEAVE_ONE_OUT && G < 2) throw Error(1, "leave-one-out needs every group size >= 2");
-  if (!(tau >= 0.0)) throw Error(1, "filter threshold must be >= 0");
+  const bool no_filter = std::isinf(tau) && tau < 0;  // DASHCU_FILTER_OFF: kept stays all 1 (advantage.cpp:77, :92)
+  if (!no_filter && !(tau >= 0.0)) throw Error(1, "filter threshold must be >= 0");
   if (kind == DASHCU_ADV_GIVEN && !adv) throw Error(1, "DASHCU_ADV_GIVEN needs the advantages in adv");
   DCU_CHECK(cudaSetDevice(c->device));
   cudaStream_t s = c->stream;
@@ -1428,18 +1469,73 @@ int dashcu_optimizer_step(dashcu_policy* p, const dashcu_opt* o) {
   check_policy(p);
   if (!o) throw Error(1, "null optimizer config");
   if (o->kind != DASHCU_OPT_SGD && o->kind != DASHCU_OPT_ADAM) throw Error(1, "unknown optimizer");
+  if (p->opt_state == 1) throw Error(1, "optimizer state is sharded: use dashcu_sharded_step");
+  ensure_moments(p, p->lay.total, 0);
   Timer tm(p->ctx->stream);
-  float c1 = 1.f, c2 = 1.f;
-  if (o->kind == DASHCU_OPT_ADAM) {
-    ++p->adam_t;
-    c1 = static_cast<float>(1.0 - std::pow(o->beta1, static_cast<double>(p->adam_t)));
-    c2 = static_cast<float>(1.0 - std::pow(o->beta2, static_cast<double>(p->adam_t)));
-  }
+  float c1, c2;
+  bias_corrections(p, o, &c1, &c2);
   optimizer_update(p->ctx->stream, o->kind, p->w32.as<float>(), p->g32.as<float>(), p->am.as<float>(),
                    p->av.as<float>(), p->dtype == DASHCU_BF16 ? p->wT.as<bf16>() : nullptr, p->lay.total,
                    static_cast<float>(o->lr), static_cast<float>(o->beta1), static_cast<float>(o->beta2),
                    static_cast<float>(o->eps), c1, c2);
   p->st.optimizer_ms = tm.stop_ms();
+  ++p->version;
+  API_END
+}
+
+int dashcu_shard_span(int64_t total, int32_t world, int32_t rank, int64_t* off, int64_t* len) {
+  API_BEGIN
+  if (!off || !len) throw Error(1, "null argument");
+  if (total < 0 || world < 1 || rank < 0 || rank >= world) throw Error(1, "bad total/world/rank");
+  shard_span(total, world, rank, off, len, nullptr);
+  API_END
+}
+
+// ZeRO-1 style update: the summed gradient is reduce-scattered so rank r
+// holds the slice dashcu_shard_span(r); Adam / SGD runs on that slice of the fp32 master
+// weights with slice-sized moments (1/world of the optimizer state and of its HBM
+// traffic per GPU); the updated master slices are all-gathered in place and the bf16
+// working copy is refreshed from the full master. Same arithmetic per element as
+// allreduce_grads + optimizer_step, so the weights agree with the
+// replicated update to the reduction's rounding.
+int dashcu_sharded_step(dashcu_policy* p, const dashcu_opt* o) {
+  API_BEGIN
+  check_policy(p);
+  if (!o) throw Error(1, "null optimizer config");
+  if (o->kind != DASHCU_OPT_SGD && o->kind != DASHCU_OPT_ADAM) throw Error(1, "unknown optimizer");
+  dashcu_ctx* c = p->ctx;
+  if (c->world != p->shard_world) throw Error(1, "communicator changed after the policy was created");
+  if (p->opt_state == 0) throw Error(1, "optimizer state is replicated: use dashcu_optimizer_step");
+  int64_t off, len, slice;
+  shard_span(p->lay.total, c->world, c->rank, &off, &len, &slice);
+  ensure_moments(p, slice, 1);
+  NcclApi& nc = NcclApi::get();
+  if (c->world > 1) {
+    if (!c->comm) throw Error(4, "communicator not initialised (dashcu_ctx_init_comm)");
+    if (!nc.ReduceScatter || !nc.AllGather) throw Error(4, "libnccl lacks ncclReduceScatter / ncclAllGather");
+  }
+  Timer tc(c->stream);
+  float* g = p->g32.as<float>();
+  float* w = p->w32.as<float>();
+  if (c->world > 1)  // in place: rank r's slice of the sum lands at g + r * slice
+    NCCL_CHECK(nc.ReduceScatter(g, g + off, static_cast<size_t>(slice), ncclFloat32, ncclSum, c->comm, c->stream));
+  const double rs_ms = tc.stop_ms();
+  Timer to(c->stream);
+  float c1, c2;
+  bias_corrections(p, o, &c1, &c2);
+  if (len > 0)
+    optimizer_update(c->stream, o->kind, w + off, g + off, p->am.as<float>(), p->av.as<float>(), nullptr, len,
+                     static_cast<float>(o->lr), static_cast<float>(o->beta1), static_cast<float>(o->beta2),
+                     static_cast<float>(o->eps), c1, c2);
+  const double up_ms = to.stop_ms();
+  Timer tg(c->stream);
+  if (c->world > 1)
+    NCCL_CHECK(nc.AllGather(w + off, w, static_cast<size_t>(slice), ncclFloat32, c->comm, c->stream));
+  const double ag_ms = tg.stop_ms();
+  Timer tw(c->stream);
+  refresh_working_copy(p);
+  p->st.allreduce_ms = rs_ms + ag_ms;
+  p->st.optimizer_ms = up_ms + tw.stop_ms();
   ++p->version;
   API_END
 }

@@ -218,6 +218,7 @@ def sample(arch, params, prompt, max_len, temperature, seq_key):
 
 
 def advantage_filter(rewards, group_size, kind=1, normalize=False, eps=0.0, tau=0.0):
+    tau = float("-inf") if tau is None else tau   # no filter (DASHCU_FILTER_OFF)
     r = np.ascontiguousarray(rewards, dtype=np.float64)
     n = r.shape[0]
     adv = np.zeros(max(n, 1))

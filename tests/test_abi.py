@@ -62,3 +62,21 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("a GPU is visible")
     with pytest.raises(D.DeviceError):
         D.Context(0)
+
+
+def test_shard_span_partitions_the_flat_vector():
+    """dashcu_shard_span (the sharded optimizer's slices): disjoint, ordered, covering,
+    64-element aligned, equal slice strides (in-place reduce-scatter / all-gather)."""
+    for total in (1, 63, 64, 65, 468480, 527_000_123):
+        for world in (1, 2, 3, 4, 7, 8):
+            spans = [D.shard_span(total, world, r) for r in range(world)]
+            stride = ((total + world - 1) // world + 63) // 64 * 64
+            pos = 0
+            for r, (off, n) in enumerate(spans):
+                assert off == r * stride and off % 64 == 0 and 0 <= n <= stride
+                if n:
+                    assert off == pos
+                    pos += n
+            assert pos == total
+    with pytest.raises(D.InputError):
+        D.shard_span(10, 2, 2)

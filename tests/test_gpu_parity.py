@@ -110,7 +110,7 @@ def test_advantage_filter_bit_exact(ctx):
                 r = rng.integers(0, 2, size=G * 33).astype(np.float64)
                 if not binary:
                     r = rng.standard_normal(G * 33)
-                for tau in (0.0, 0.1, 0.125, float("inf")):
+                for tau in (0.0, 0.1, 0.125, float("inf"), None):
                     for norm in (False, True):
                         a, k, i = ctx.advantage_filter(r, G, kind, norm, 1e-6, tau)
                         ra, rk, ri = O.advantage_filter(r, G, kind, norm, 1e-6, tau)
@@ -126,6 +126,10 @@ def test_advantage_filter_large_and_errors(ctx):
         ctx.advantage_filter([1.0, 0.0, 1.0], 2)
     with pytest.raises(D.InputError):
         ctx.advantage_filter([1.0, 0.0], 2, tau=-1.0)
+    with pytest.raises(D.InputError):
+        ctx.advantage_filter([1.0, 0.0], 2, tau=float("nan"))
+    a, k, i = ctx.advantage_filter(r, 8, D.ADV_GROUP, False, 0, None)   # filter off: all kept (advantage.cpp:92)
+    assert k.all() and np.array_equal(i, np.arange(len(r))) and np.array_equal(a, ra)
     with pytest.raises(D.InputError):
         ctx.advantage_filter([1.0, 0.0], 1, kind=D.ADV_LEAVE_ONE_OUT)
 
@@ -359,6 +363,35 @@ def test_on_policy_violation_and_optimizer(ctx):
     with pytest.raises(D.CapacityError):
         pol.load_rollout([[0, 2]], 1, [[3] * 39])     # m + len > ctx
     pol.close()
+
+
+@pytest.mark.parametrize("dtype", [D.F32, D.BF16])
+def test_sharded_step_equals_replicated_update(ctx, dtype):
+    """dashcu_sharded_step (ZeRO-1 form) at world 1 == allreduce_grads +
+    optimizer_step bit for bit over several Adam steps (slice-sized moments), the bf16
+    working copy included (identical rollouts); the two forms cannot be mixed."""
+    arch = SMALL
+    p = params32(arch, 0.3, 10)
+    g = np.random.default_rng(3).standard_normal(len(p)).astype(np.float32).astype(np.float64)
+    a, b = D.Policy(ctx, arch, dtype), D.Policy(ctx, arch, dtype)
+    for pol in (a, b):
+        pol.upload(p)
+    for step in range(3):
+        for pol in (a, b):
+            pol.grad_upload(g * (step + 1))
+        a.allreduce_grads()
+        a.optimizer_step(D.OPT_ADAM, lr=1e-2)
+        b.sharded_step(D.OPT_ADAM, lr=1e-2)
+        assert np.array_equal(a.download(), b.download())
+    prompts = [[0, 5, 6], [0, 7]]
+    ra, rb = a.sample(prompts, 4, 9, round_seed=5), b.sample(prompts, 4, 9, round_seed=5)
+    assert np.array_equal(ra.completions, rb.completions) and np.array_equal(ra.lengths, rb.lengths)
+    with pytest.raises(D.InputError):
+        a.sharded_step(D.OPT_ADAM)
+    with pytest.raises(D.InputError):
+        b.optimizer_step(D.OPT_ADAM)
+    a.close()
+    b.close()
 
 
 # ------------------------------------------------------------ one DASH step

@@ -2,7 +2,10 @@
 design of SURVEY §8e: prompts sharded by global index with whole groups per rank,
 per-request keys independent of the split, each rank accumulating its shard's PG
 gradient with the GLOBAL 1/N, one sum-allreduce, then an identical optimizer step.
-The per-rank gradients come from the CPU oracle; the collective is torch.distributed."""
+The per-rank gradients come from the CPU oracle; the collective is torch.distributed.
+The ZeRO-1 form (dashcu_sharded_step) is checked the same way: slices
+from the library's own dashcu_shard_span (no device work), reduce-scatter, Adam on the
+rank's slice with slice-sized moments, all-gather == the replicated update, bit for bit."""
 import os
 import socket
 
@@ -55,6 +58,7 @@ def worker(rank, world, port, q):
     params = O.init_params(ARCH, 0.4, 2)
     lo, hi = shard(rank, world)
     g, comps = rank_gradient(params, lo, hi)
+    g_local = g.copy()
     t = torch.from_numpy(g)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     # replicated Adam step after the allreduce: every rank ends with identical weights
@@ -64,6 +68,27 @@ def worker(rank, world, port, q):
     gg = t.numpy().copy()
     O.oracle().dor_adam_step(O.ptr(p, O.f64p), O.ptr(gg, O.f64p), O.ptr(m, O.f64p), O.ptr(v, O.f64p), len(p), 1,
                              1e-3, 0.9, 0.999, 1e-8)
+    # ZeRO-1: reduce-scatter -> Adam on this rank's slice -> all-gather
+    import paper_2505_17218_b200 as D
+    n = len(params)
+    spans = [D.shard_span(n, world, r) for r in range(world)]
+    sl = spans[0][1]
+    gp = np.zeros(sl * world)
+    gp[:n] = g_local
+    parts = [torch.zeros(sl, dtype=torch.float64) for _ in range(world)]
+    dist.reduce_scatter(parts[rank], list(torch.from_numpy(gp).split(sl)), op=dist.ReduceOp.SUM)
+    off, ln = spans[rank]
+    ws = np.zeros(sl)
+    ws[:ln] = params[off:off + ln]
+    gs = parts[rank].numpy().copy()
+    ms, vs = np.zeros(sl), np.zeros(sl)
+    O.oracle().dor_adam_step(O.ptr(ws, O.f64p), O.ptr(gs, O.f64p), O.ptr(ms, O.f64p), O.ptr(vs, O.f64p), ln, 1,
+                             1e-3, 0.9, 0.999, 1e-8)
+    out = [torch.zeros(sl, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(out, torch.from_numpy(ws))
+    p_sharded = torch.cat(out).numpy()[:n]
+    assert np.array_equal(gs[:ln], gg[off:off + ln]), ("rs", np.abs(gs[:ln] - gg[off:off + ln]).max(), np.abs(gg).max())
+    assert np.array_equal(p_sharded, p), ("upd", np.abs(p_sharded - p).max())
     # bench.py reduction helpers (max of step times, sum of tokens) over the same group
     import bench
     mx = bench.allreduce([float(rank + 1)], "max")[0]

@@ -289,6 +289,11 @@ def test_advantage_matches_reference_random():
                                                  C.byref(kc), C.byref(ff), C.byref(ma)) == 0
                 assert np.array_equal(kept, k.astype(bool))
                 assert list(idx) == list(np.nonzero(k)[0])
+            # no filter (GRPO-style): group_advantage's kept stays all 1 (advantage.cpp:77, :92)
+            adv, kept, idx = O.advantage_filter(r, G, kind=kind, tau=None)
+            assert np.array_equal(adv, out) and kept.all() and list(idx) == list(range(len(r)))
+            with pytest.raises(ValueError):
+                O.advantage_filter(r, G, kind=kind, tau=-0.5)
             norm = np.zeros_like(r)
             assert R.ref_normalize_std(O.ptr(out, O.f64p), O.ptr(r, O.f64p), len(r), G if kind else len(r),
                                        1e-6, O.ptr(norm, O.f64p)) == 0
