@@ -46,6 +46,11 @@ struct GemmShape {
   const void* B;
   int64_t ldb;
   bool b_kmajor;
+  // tile raster of the persistent schedule (set by the dispatcher): false = M tiles vary
+  // fastest (a B panel is shared by the CTAs of a round), true = N tiles vary fastest (an
+  // A panel is shared, so an A larger than L2 streams from HBM once instead of once per
+  // N tile)
+  bool n_fast = false;
 };
 
 // LM-head sampling epilogue (policy.cpp:148-151 + :399-424 with the DESIGN.md §4 rule):

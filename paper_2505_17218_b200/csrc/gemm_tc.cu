@@ -47,6 +47,14 @@ __device__ __forceinline__ void mbar_wait_pipe(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// Persistent-schedule tile t -> (M tile, N tile), raster per GemmShape::n_fast.
+__device__ __forceinline__ int tile_m(const GemmShape& g, int t, int tiles_m, int tiles_n) {
+  return g.n_fast ? t / tiles_n : t % tiles_m;
+}
+__device__ __forceinline__ int tile_n(const GemmShape& g, int t, int tiles_m, int tiles_n) {
+  return g.n_fast ? t % tiles_n : t / tiles_m;
+}
+
 // tanh(x) = 1 - 2 / (exp(2x) + 1): ~1e-6 relative, far below the bf16 output rounding;
 // 6 instructions instead of tanhf's ~20 (the W1 epilogue runs it on every element).
 __device__ __forceinline__ float fast_tanh(float x) {
@@ -664,7 +672,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
       int kb_all = 0;
       for (int w = blockIdx.x; w < nitem; w += gridDim.x) {
         const int t = w / S, sp = w % S;
-        const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
+        const int m0 = tile_m(g, t, tiles_m, tiles_n) * BM, n0 = tile_n(g, t, tiles_m, tiles_n) * BN;
         const int kb_lo = sp * kps, kb_hi = min(nkb, kb_lo + kps);
         for (int kb = kb_lo; kb < kb_hi; ++kb, ++kb_all) {
           const int s = kb_all % STAGES;
@@ -734,7 +742,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
     int i = 0;
     for (int w = blockIdx.x; w < nitem; w += gridDim.x, ++i) {
       const int t = w / S, sp = w % S;
-      const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
+      const int m0 = tile_m(g, t, tiles_m, tiles_n) * BM, n0 = tile_n(g, t, tiles_m, tiles_n) * BN;
       const int acc = i & 1;
       const uint32_t aph = (i >> 1) & 1;
       mbar_wait_sleep(&tfull[acc], aph);
@@ -746,7 +754,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
       if constexpr (MODE == 1)
         epilogue_sample(g, e, sa, om, taddr, row, r0, n0, slice * CW, (slice + 1) * CW, stg, lane);
       else if constexpr (MODE == 2)
-        epilogue_lse(g, e, sa, taddr, row, n0, slice * CW, (slice + 1) * CW, (t / tiles_m) * NSL + slice);
+        epilogue_lse(g, e, sa, taddr, row, n0, slice * CW, (slice + 1) * CW, tile_n(g, t, tiles_m, tiles_n) * NSL + slice);
       else if constexpr (MODE == 3)
         epilogue_dz(g, e, sa, om, taddr, row, r0, n0, slice * CW, (slice + 1) * CW, stg, lane);
       else if (e.tma)
@@ -993,8 +1001,8 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
     if (lane == 0) {
       int kb_all = 0;
       for (int t = pair; t < ntile; t += npairs) {
-        const int m0 = (t % tiles_m) * 256 + static_cast<int>(rank) * 128;
-        const int n0 = (t / tiles_m) * BN + static_cast<int>(rank) * C::BNH;
+        const int m0 = tile_m(g, t, tiles_m, tiles_n) * 256 + static_cast<int>(rank) * 128;
+        const int n0 = tile_n(g, t, tiles_m, tiles_n) * BN + static_cast<int>(rank) * C::BNH;
         for (int kb = 0; kb < nkb; ++kb, ++kb_all) {
           const int s = kb_all % STAGES;
           const uint32_t ph = (kb_all / STAGES) & 1;
@@ -1062,7 +1070,8 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
     uint32_t ephase = 0, eph2[2] = {0, 0};
     int i = 0;
     for (int t = pair; t < ntile; t += npairs, ++i) {
-      const int m0 = (t % tiles_m) * 256 + static_cast<int>(rank) * 128, n0 = (t / tiles_m) * BN;
+      const int m0 = tile_m(g, t, tiles_m, tiles_n) * 256 + static_cast<int>(rank) * 128,
+                n0 = tile_n(g, t, tiles_m, tiles_n) * BN;
       const int acc = i & 1;
       const uint32_t aph = (i >> 1) & 1;
       mbar_wait_sleep(&tfull[acc], aph);
@@ -1171,8 +1180,20 @@ bool gemm_tc_pair(cudaStream_t s, const GemmShape& g, const Epi& e, int BN) {
   return true;
 }
 
-bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e) {
-  if (!legal(g)) return false;
+// Raster of the persistent tile schedule: N tiles fastest when A is the operand that
+// cannot stay in L2 (an A panel is then read from HBM once and shared by the CTAs working
+// on its N tiles), M tiles fastest otherwise. DASHCU_GEMM_RASTER=0/1 forces m / n fast.
+bool raster_n_fast(const GemmShape& g) {
+  const char* r = getenv("DASHCU_GEMM_RASTER");
+  if (r) return r[0] == '1';
+  const double a = 2.0 * g.M * g.K, b = 2.0 * g.N * g.K;
+  return a > 2.0 * b && a > 48e6;
+}
+
+bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
+  if (!legal(g_in)) return false;
+  GemmShape g = g_in;
+  g.n_fast = raster_n_fast(g);
   // Tile shape by the persistent schedule: time ~ rounds x per-tile cost, rounds =
   // ceil(tiles / concurrent CTAs). Measured per-SM efficiencies: 128x128 tiles 0.76
   // (shared-memory bound), 128x256 1.0, CTA-pair 256x256 1.12 (B staged half per SM).

@@ -97,11 +97,13 @@ def test_tma_store_epilogue_matches_direct_stores(ctx, monkeypatch, shape, epi):
         assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
 
 
+@pytest.mark.parametrize("raster", ["0", "1"])
 @pytest.mark.parametrize("shape", [(128, 128, 8192), (896, 896, 36832 // 8), (300, 200, 5000)])
-def test_split_k_accumulate(ctx, monkeypatch, shape):
+def test_split_k_accumulate(ctx, monkeypatch, shape, raster):
     """Weight-gradient shapes (few output tiles, long K) run as ordered split-K: the
     slices reduce into C in slice order, so repeated runs are bit-identical and the
     result matches the unsplit kernel to fp32 rounding."""
+    monkeypatch.setenv("DASHCU_GEMM_RASTER", raster)
     M, N, K = shape
     rng = np.random.default_rng(11)
     A = bf16_bits(rng.standard_normal((K, M)).astype(np.float32))   # MN-major operands, as in dW = dY^T X
@@ -117,12 +119,15 @@ def test_split_k_accumulate(ctx, monkeypatch, shape):
     assert np.abs(a - c).max() <= 1e-5 * np.abs(ref).max() + 1e-3
 
 
-@pytest.mark.parametrize("pair", ["1", "2"])
+@pytest.mark.parametrize("raster", ["0", "1"])
+@pytest.mark.parametrize("pair", ["1", "2", "-1"])
 @pytest.mark.parametrize("ak,bk", [(True, True), (True, False), (False, True), (False, False)])
 @pytest.mark.parametrize("shape", [(256, 128, 64), (300, 200, 136), (4096, 896, 896), (1000, 1152, 320)])
-def test_cta_pair_tiles(ctx, monkeypatch, pair, ak, bk, shape):
-    """The cta_group::2 kernel with 256x256 (pair=1) and 256x128 (pair=2) tiles, forced."""
+def test_cta_pair_tiles(ctx, monkeypatch, pair, ak, bk, shape, raster):
+    """The cta_group::2 kernel with 256x256 (pair=1) and 256x128 (pair=2) tiles, forced, and
+    the single-CTA kernel (pair=-1), under both tile rasters (M or N tiles fastest)."""
     monkeypatch.setenv("DASHCU_GEMM_PAIR", pair)
+    monkeypatch.setenv("DASHCU_GEMM_RASTER", raster)
     M, N, K = shape
     rng = np.random.default_rng(M + N + K)
     A = bf16_bits(rng.standard_normal((M, K)).astype(np.float32))
