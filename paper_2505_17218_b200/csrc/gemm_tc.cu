@@ -1100,11 +1100,11 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
   }
 }
 
-template <int BN, int STAGES, bool AK, bool BKM, bool DB = false>
+template <int BN, int STAGES, bool AK, bool BKM, bool DB = false, int EPW = 8>
 void launch2(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& om, const GemmShape& g,
              const Epi& e) {
-  using C = Cfg2<BN, STAGES, AK, BKM, 8, DB>;
-  auto k = gemm_tc2_kernel<BN, STAGES, AK, BKM, 8, DB>;
+  using C = Cfg2<BN, STAGES, AK, BKM, EPW, DB>;
+  auto k = gemm_tc2_kernel<BN, STAGES, AK, BKM, EPW, DB>;
   static bool attr = false;
   if (!attr) {
     DCU_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -1151,13 +1151,13 @@ int use_pair_default() {
 }  // namespace
 
 // cta_group::2 GEMM for 256-row-multiple-friendly shapes. Returns false if not TMA-legal.
-template <int BN, int STAGES, bool DB = false>
+template <int BN, int STAGES, bool DB = false, int EPW = 8>
 void dispatch_pair(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& om, const GemmShape& g,
                    const Epi& e) {
-  if (g.a_kmajor && g.b_kmajor) launch2<BN, STAGES, true, true, DB>(s, ma, mb, om, g, e);
-  else if (g.a_kmajor) launch2<BN, STAGES, true, false, DB>(s, ma, mb, om, g, e);
-  else if (g.b_kmajor) launch2<BN, STAGES, false, true, DB>(s, ma, mb, om, g, e);
-  else launch2<BN, STAGES, false, false, DB>(s, ma, mb, om, g, e);
+  if (g.a_kmajor && g.b_kmajor) launch2<BN, STAGES, true, true, DB, EPW>(s, ma, mb, om, g, e);
+  else if (g.a_kmajor) launch2<BN, STAGES, true, false, DB, EPW>(s, ma, mb, om, g, e);
+  else if (g.b_kmajor) launch2<BN, STAGES, false, true, DB, EPW>(s, ma, mb, om, g, e);
+  else launch2<BN, STAGES, false, false, DB, EPW>(s, ma, mb, om, g, e);
 }
 
 // cta_group::2 GEMM with 256 x BN tiles (BN 256 or 128). Returns false if not TMA-legal.
@@ -1174,7 +1174,14 @@ bool gemm_tc_pair(cudaStream_t s, const GemmShape& g, const Epi& e, int BN) {
   // residual epilogues (fp32 resid in, fp32 + bf16 out): 4 x 32 KB stages and the
   // double-buffered residual prefetch (DASHCU_GEMM_RESID_DB=0 disables)
   const char* rdb = getenv("DASHCU_GEMM_RESID_DB");
-  if (BN == 256 && (et.tma & 4) && !(rdb && rdb[0] == '0')) dispatch_pair<256, 4, true>(s, ma, mb, om, g, et);
+  // Long-K residual GEMMs (K >= 2048) take 5 stages with 4 epilogue warps: their mainloop
+  // needs the deeper ring more than their epilogue needs 8 warps (measured +6 % at K = 4864,
+  // -10 % at K = 896). DASHCU_GEMM_RESID_DEEP=0/1 forces either.
+  const char* rdeep = getenv("DASHCU_GEMM_RESID_DEEP");
+  const bool deep = rdeep ? rdeep[0] == '1' : g.K >= 2048;
+  if (BN == 256 && (et.tma & 4) && !(rdb && rdb[0] == '0') && deep)
+    dispatch_pair<256, 5, true, 4>(s, ma, mb, om, g, et);
+  else if (BN == 256 && (et.tma & 4) && !(rdb && rdb[0] == '0')) dispatch_pair<256, 4, true>(s, ma, mb, om, g, et);
   else if (BN == 256) dispatch_pair<256, 6>(s, ma, mb, om, g, et);  // 6 x 32 KB stages
   else dispatch_pair<128, 8>(s, ma, mb, om, g, et);            // 8 x 24 KB stages
   return true;

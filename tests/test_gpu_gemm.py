@@ -139,8 +139,9 @@ def test_cta_pair_tiles(ctx, monkeypatch, pair, ak, bk, shape, raster):
     assert np.abs(got - ref).max() / max(1.0, np.abs(ref).max()) < 1e-5
 
 
+@pytest.mark.parametrize("deep", ["0", "1"])
 @pytest.mark.parametrize("shape", [(300, 200, 136), (4096, 896, 896), (1000, 1152, 320)])
-def test_pair_residual_prefetch_epilogue(ctx, monkeypatch, shape):
+def test_pair_residual_prefetch_epilogue(ctx, monkeypatch, shape, deep):
     """The CTA-pair kernel's double-buffered residual epilogue (fp32 resid in, fp32 out)
     equals the per-thread direct-store epilogue bit-for-bit, ragged edges included."""
     M, N, K = shape
@@ -150,6 +151,7 @@ def test_pair_residual_prefetch_epilogue(ctx, monkeypatch, shape):
     bias = rng.standard_normal(N).astype(np.float32)
     c0 = rng.standard_normal((M, N)).astype(np.float32)
     monkeypatch.setenv("DASHCU_GEMM_PAIR", "1")
+    monkeypatch.setenv("DASHCU_GEMM_RESID_DEEP", deep)   # 5 stages x 4 epilogue warps
     got = ctx.selftest_gemm(A, True, B, True, M, N, K, bias=bias, epi=4, C_init=c0)
     monkeypatch.setenv("DASHCU_GEMM_RESID_DB", "0")
     mid = ctx.selftest_gemm(A, True, B, True, M, N, K, bias=bias, epi=4, C_init=c0)
