@@ -94,7 +94,10 @@ void sample_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, 
 void sample_scan(cudaStream_t s, const float* part, int nslices, const float* logits, int64_t logits_ld, int rows,
                  int V, int bos, int eos, float inv_t, const uint64_t* keys, int step, const int32_t* cap,
                  uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len,
-                 bool compact = false);  // compact: {m, Z} records (fused epilogue at T = 1)
+                 bool compact = false,    // compact: {m, Z} records (fused epilogue at T = 1)
+                 float* lse_out = nullptr);  // optional [rows x max_len]: the row's T = 1 log-sum-exp
+// dst[i] = src[idx[i]] (fp32 gather)
+void gather_f32(cudaStream_t s, const float* src, const int32_t* idx, int n, float* dst);
 
 // Row LSE from gemm_tc_lse partials; if logp != null also logp = logit[y] - lse.
 void lse_reduce(cudaStream_t s, const float* part, int ntiles, int rows, float* lse, const bf16* Y, int d,

@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
                                                      int V, int bos, int eos, float inv_t, const uint64_t* keys,
                                                      int step, const int32_t* cap, uint8_t* finished, int32_t* comp,
                                                      float* logp, int32_t* len, int32_t* tok_next, int max_len,
-                                                     bool compact) {
+                                                     bool compact, float* lse_out) {
   pdl_wait();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -403,7 +403,9 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
   }
   if (tk < 0) tk = last_i;
   comp[static_cast<int64_t>(row) * max_len + step] = tk;
-  logp[static_cast<int64_t>(row) * max_len + step] = l[tk - sb * kSlice] - (M1 + logf(L1));
+  const float lse1 = M1 + logf(L1);  // T = 1 log-sum-exp over non-BOS ids (policy.cpp:424)
+  logp[static_cast<int64_t>(row) * max_len + step] = l[tk - sb * kSlice] - lse1;
+  if (lse_out) lse_out[static_cast<int64_t>(row) * max_len + step] = lse1;
   len[row] = step + 1;
   if (tk == eos) finished[row] = 1;
   tok_next[row] = tk;
@@ -742,9 +744,21 @@ void lse_reduce(cudaStream_t s, const float* part, int ntiles, int rows, float* 
 void sample_scan(cudaStream_t s, const float* part, int nslices, const float* logits, int64_t logits_ld, int rows,
                  int V, int bos, int eos, float inv_t, const uint64_t* keys, int step, const int32_t* cap,
                  uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len,
-                 bool compact) {
+                 bool compact, float* lse_out) {
   launch_pdl(sample_scan_k, dim3(cdiv(rows, 8)), dim3(256), 0, s, part, nslices, logits, logits_ld, rows, V, bos, eos,
-             inv_t, keys, step, cap, finished, comp, logp, len, tok_next, max_len, compact);
+             inv_t, keys, step, cap, finished, comp, logp, len, tok_next, max_len, compact, lse_out);
+  DCU_LAUNCHED();
+}
+
+__global__ void gather_f32_k(const float* __restrict__ src, const int32_t* __restrict__ idx, int n,
+                             float* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+
+void gather_f32(cudaStream_t s, const float* src, const int32_t* idx, int n, float* dst) {
+  if (n <= 0) return;
+  gather_f32_k<<<cdiv(n, 256), 256, 0, s>>>(src, idx, n, dst);
   DCU_LAUNCHED();
 }
 

@@ -261,6 +261,10 @@ struct dashcu_policy {
   std::vector<int64_t> h_prompt_off;
   std::vector<int32_t> h_comp, h_len;
   dashcu::DevMem d_comp, d_len, d_logp;
+  // T = 1 log-sum-exp of every sampled position [n_seq x max_len], written by the fused
+  // sampling epilogue (bf16 path); reused by the teacher-forced LM-head backward
+  dashcu::DevMem d_lse;
+  bool lse_valid = false;
   std::vector<double> h_rewards, h_adv;
   std::vector<int32_t> h_kidx;
   bool adv_valid = false;
@@ -389,7 +393,7 @@ struct Engine {
   // Loss rows: rows (packed index), tgt, weight. If grad: backward through the
   // LM head, writing dL/dy_top into dy32 (zeroed here). logp may be null.
   void lm_head(const Acts& A, int R, const int32_t* rows, const int32_t* tgt, const float* w, float* logp,
-               bool grad, float* dy32) {
+               bool grad, float* dy32, const int32_t* lsei = nullptr) {
     const int64_t V = g.V;
     // bf16: the logits stay in TMEM (LSE pass + dz pass); fp32 parity path: fp32 logits + row kernel
     constexpr bool fused = sizeof(T) == 2;
@@ -411,9 +415,12 @@ struct Engine {
         SampleArgs sa;
         sa.bos = g.bos;
         sa.part = part;
-        const int nt = gemm_tc_lse(st, gs, W32(L.bout), sa);
+        const bool have_lse = lsei && grad && !logp;
+        const int nt = have_lse ? 1 : gemm_tc_lse(st, gs, W32(L.bout), sa);
         if (nt > 0) {
-          lse_reduce(st, part, nt, rc, lse, ycT, g.d, W(L.wout), W32(L.bout), tgt + r0, logp ? logp + r0 : nullptr);
+          if (have_lse) gather_f32(st, P.d_lse.as<float>(), lsei + r0, rc, lse);  // the sampler's row LSE
+          else
+            lse_reduce(st, part, nt, rc, lse, ycT, g.d, W(L.wout), W32(L.bout), tgt + r0, logp ? logp + r0 : nullptr);
           if (grad) {
             sa.lse = lse;
             sa.target = tgt + r0;
@@ -529,7 +536,7 @@ struct Engine {
 
   // ------------------------------------------------------------ micro-batch
   struct Batch {
-    std::vector<int32_t> tok, pos, start, rows, tgt, seqs;
+    std::vector<int32_t> tok, pos, start, rows, tgt, seqs, lsei;  // lsei: row -> d_lse cell
     std::vector<float> w;
     int maxlen = 0;
     double pairs = 0;  // sum over sequences of n(n+1)/2 causal (query, key) pairs
@@ -559,6 +566,7 @@ struct Engine {
       for (int j = 0; j < len; ++j) {
         B.rows.push_back(s0 + m - 1 + j);
         B.tgt.push_back(P.h_comp[static_cast<int64_t>(s) * P.max_len + j]);
+        B.lsei.push_back(static_cast<int32_t>(static_cast<int64_t>(s) * P.max_len + j));
         B.w.push_back(static_cast<float>(weight.empty() ? 1.0 : weight[k]));
       }
       B.start.push_back(s0 + n);
@@ -572,6 +580,7 @@ struct Engine {
   struct DevBatch {
     int32_t *tok, *pos, *start, *rows, *tgt;
     float* w;
+    int32_t* lsei;
   };
   DevBatch upload(const Batch& B) {
     DevBatch d;
@@ -587,6 +596,7 @@ struct Engine {
     h2d(st, d.rows, B.rows.data(), B.rows.size());
     h2d(st, d.tgt, B.tgt.data(), B.tgt.size());
     h2d(st, d.w, B.w.data(), B.w.size());
+    d.lsei = nullptr;
     return d;
   }
 
@@ -595,9 +605,10 @@ struct Engine {
   std::vector<DevBatch> upload_all(const std::vector<Batch>& bs) {
     size_t nt = 0, ns = 0, nr = 0;
     for (const Batch& b : bs) nt += b.tok.size(), ns += b.start.size(), nr += b.rows.size();
-    std::vector<int32_t> tok, pos, start, rows, tgt;
+    std::vector<int32_t> tok, pos, start, rows, tgt, lsei;
     std::vector<float> w;
     tok.reserve(nt), pos.reserve(nt), start.reserve(ns), rows.reserve(nr), tgt.reserve(nr), w.reserve(nr);
+    lsei.reserve(nr);
     for (const Batch& b : bs) {
       tok.insert(tok.end(), b.tok.begin(), b.tok.end());
       pos.insert(pos.end(), b.pos.begin(), b.pos.end());
@@ -605,6 +616,7 @@ struct Engine {
       rows.insert(rows.end(), b.rows.begin(), b.rows.end());
       tgt.insert(tgt.end(), b.tgt.begin(), b.tgt.end());
       w.insert(w.end(), b.w.begin(), b.w.end());
+      lsei.insert(lsei.end(), b.lsei.begin(), b.lsei.end());
     }
     int32_t* dtok = P.ws.get<int32_t>("mb_tok", nt);
     int32_t* dpos = P.ws.get<int32_t>("mb_pos", nt);
@@ -612,6 +624,8 @@ struct Engine {
     int32_t* drows = P.ws.get<int32_t>("mb_rows", nr);
     int32_t* dtgt = P.ws.get<int32_t>("mb_tgt", nr);
     float* dw = P.ws.get<float>("mb_w", nr);
+    int32_t* dlsei = P.ws.get<int32_t>("mb_lsei", nr);
+    h2d(st, dlsei, lsei.data(), nr);
     h2d(st, dtok, tok.data(), nt);
     h2d(st, dpos, pos.data(), nt);
     h2d(st, dstart, start.data(), ns);
@@ -621,7 +635,7 @@ struct Engine {
     std::vector<DevBatch> out;
     size_t ot = 0, os = 0, orr = 0;
     for (const Batch& b : bs) {
-      out.push_back(DevBatch{dtok + ot, dpos + ot, dstart + os, drows + orr, dtgt + orr, dw + orr});
+      out.push_back(DevBatch{dtok + ot, dpos + ot, dstart + os, drows + orr, dtgt + orr, dw + orr, dlsei + orr});
       ot += b.tok.size(), os += b.start.size(), orr += b.rows.size();
     }
     return out;
@@ -640,6 +654,11 @@ struct Engine {
       if (!B.seqs.empty()) batches.push_back(std::move(B));
     }
     const std::vector<DevBatch> dev = upload_all(batches);
+    // The sampler already computed the T = 1 log-sum-exp of every completion position
+    // under the same weights (on-policy: the version check above), so the backward skips
+    // the LM-head LSE pass and reads it (DASHCU_LSE_RECOMPUTE=1 recomputes instead)
+    const char* rec = getenv("DASHCU_LSE_RECOMPUTE");
+    const bool reuse_lse = sizeof(T) == 2 && P.lse_valid && !(rec && rec[0] == '1');
     for (size_t bi = 0; bi < batches.size(); ++bi) {
       const Batch& B = batches[bi];
       const DevBatch& D = dev[bi];
@@ -648,7 +667,7 @@ struct Engine {
       pairs = B.pairs;
       forward(A, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen);
       float* dy32 = P.ws.get<float>("b_dy32", static_cast<size_t>(Tn) * g.d);
-      lm_head(A, static_cast<int>(B.rows.size()), D.rows, D.tgt, D.w, nullptr, true, dy32);
+      lm_head(A, static_cast<int>(B.rows.size()), D.rows, D.tgt, D.w, nullptr, true, dy32, reuse_lse ? D.lsei : nullptr);
       backward(A, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen, dy32);
       loss_tokens += static_cast<int64_t>(B.rows.size());
     }
@@ -722,6 +741,10 @@ struct Engine {
     P.d_comp.ensure(sizeof(int32_t) * static_cast<size_t>(S) * std::max(ML, 1));
     P.d_len.ensure(sizeof(int32_t) * S);
     P.d_logp.ensure(sizeof(float) * static_cast<size_t>(S) * std::max(ML, 1));
+    P.d_lse.ensure(sizeof(float) * static_cast<size_t>(S) * std::max(ML, 1));
+    float* lse_out = sizeof(T) == 2 ? P.d_lse.as<float>() : nullptr;
+    bool lse_all = sizeof(T) == 2;  // every step went through the fused epilogue + scan
+    P.lse_valid = false;
     DCU_CHECK(cudaMemsetAsync(P.d_comp.p, 0xff, sizeof(int32_t) * static_cast<size_t>(S) * std::max(ML, 1), st));
     DCU_CHECK(cudaMemsetAsync(P.d_len.p, 0, sizeof(int32_t) * S, st));
     DCU_CHECK(cudaMemsetAsync(P.d_logp.p, 0, sizeof(float) * static_cast<size_t>(S) * std::max(ML, 1), st));
@@ -780,10 +803,12 @@ struct Engine {
         const int nt = gemm_tc_sample(st, gs, W32(L.bout), sa);
         if (nt > 0) {
           sample_scan(st, part, nt, lg, ld, S, g.V, g.bos, g.eos, inv_t, d_keys, step, d_cap, d_fin,
-                      P.d_comp.as<int32_t>(), P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML, inv_t == 1.f);
+                      P.d_comp.as<int32_t>(), P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML, inv_t == 1.f,
+                      lse_out);
           return;
         }
       }
+      lse_all = false;
       Epi el = store(logits, g.V, nullptr, 0);
       el.bias = W32(L.bout);
       mm(S, g.V, g.d, yrows, g.d, true, W(L.wout), g.d, true, el);
@@ -859,7 +884,7 @@ struct Engine {
               sample_scan(st, sa.part, nt, sa.logits, g.V, R, g.V, g.bos, g.eos, inv_t, d_keys + r0, j,
                           d_cap + r0, d_fin + r0, P.d_comp.as<int32_t>() + static_cast<size_t>(r0) * ML,
                           P.d_logp.as<float>() + static_cast<size_t>(r0) * ML, P.d_len.as<int32_t>() + r0,
-                          d_tok + r0, ML, inv_t == 1.f);
+                          d_tok + r0, ML, inv_t == 1.f, lse_out + static_cast<size_t>(r0) * ML);
             }
             continue;
           }
@@ -915,6 +940,7 @@ struct Engine {
     st = main_st;
     join();
     gemm_set_cta_cap(0);
+    P.lse_valid = lse_all;
     if (ev_main) cudaEventDestroy(ev_main);
     if (ev_side) cudaEventDestroy(ev_side);
   }
@@ -1291,6 +1317,7 @@ int dashcu_rollout_load(dashcu_policy* p, const int32_t* prompt_tokens, const in
   DCU_CHECK(cudaStreamSynchronize(p->ctx->stream));
   p->ro_version = p->version;
   p->ro_valid = true;
+  p->lse_valid = false;  // external trajectories: the backward runs its own LSE pass
   p->adv_valid = false;
   p->st.n_seq = S;
   API_END

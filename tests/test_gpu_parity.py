@@ -426,6 +426,37 @@ def test_dash_step_c1_matches_oracle(ctx, dtype):
     pol.close()
 
 
+@pytest.mark.parametrize("arch", [QWENLIKE, VBIG, LONGGQA], ids=["qwenlike", "vbig", "longgqa"])
+@pytest.mark.parametrize("temperature", [1.0, 0.7])
+def test_backward_reuses_sampler_lse(ctx, monkeypatch, arch, temperature):
+    """The bf16 backward of a sampled rollout takes each position's T = 1 log-sum-exp
+    from the sampling epilogue instead of an LM-head LSE pass (same weights: on-policy).
+    Gradient vs the oracle within the bf16 tolerance, and vs the recomputing path."""
+    pol = D.Policy(ctx, arch, D.BF16)
+    p = params32(arch, 0.5, 21)
+    pol.upload(p)
+    rng = np.random.default_rng(5)
+    V = arch["vocab_size"]
+    prompts = [[0] + list(rng.integers(2, V, size=int(rng.integers(3, 9)))) for _ in range(4)]
+    G, ML = 4, min(24, arch["context_len"] - 10)
+    ro = pol.sample(prompts, G, ML, temperature=temperature, round_seed=9)
+    w = rng.standard_normal(len(prompts) * G) / 16
+    pol.grad_zero()
+    pol.accumulate_weighted(w, micro_batch=8)
+    reuse = pol.grad()
+    monkeypatch.setenv("DASHCU_LSE_RECOMPUTE", "1")
+    pol.grad_zero()
+    pol.accumulate_weighted(w, micro_batch=8)
+    recompute = pol.grad()
+    ref = np.zeros_like(reuse)
+    for s in range(len(w)):
+        O.grad_log_prob(arch, p, prompts[s // G], list(ro.completion(s)), w[s], ref)
+    assert_grad_close(arch, reuse, ref, TOL[D.BF16])
+    assert_grad_close(arch, recompute, ref, TOL[D.BF16])
+    assert np.linalg.norm(reuse - recompute) <= 1e-2 * np.linalg.norm(recompute)
+    pol.close()
+
+
 @pytest.mark.parametrize("dtype", [D.F32, D.BF16])
 def test_long_sequences_multi_tile(ctx, dtype):
     """Sequences spanning several 64-key tiles (flash-attention tiling, causal diagonal,
