@@ -55,11 +55,19 @@ __device__ __forceinline__ int tile_n(const GemmShape& g, int t, int tiles_m, in
   return g.n_fast ? t % tiles_n : t / tiles_m;
 }
 
-// tanh(x) = 1 - 2 / (exp(2x) + 1): ~1e-6 relative, far below the bf16 output rounding;
-// 6 instructions instead of tanhf's ~20 (the W1 epilogue runs it on every element).
+// The W1 epilogue runs tanh on every element and its output is stored as bf16 (relative
+// rounding 2^-9): the one-instruction MUFU tanh.approx (max relative error ~2^-11) is below
+// that rounding and halves the epilogue's MUFU work against 1 - 2 / (exp(2x) + 1)
+// (ex2 + rcp, ~1e-6 relative; -DDASHCU_TANH_ACCURATE selects it).
 __device__ __forceinline__ float fast_tanh(float x) {
+#ifdef DASHCU_TANH_ACCURATE
   const float e = __expf(2.f * fminf(fmaxf(x, -15.f), 15.f));
   return 1.f - __fdividef(2.f, e + 1.f);
+#else
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+#endif
 }
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
@@ -937,8 +945,14 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
 template <int BN, int STAGES, bool AK, bool BKM, int EPW, bool DB = false>
 struct Cfg2 {
   static constexpr int BNH = BN / 2;  // B rows staged per CTA
+  // BN = 224 (N = 896 = 4 x 224 without the half-empty fourth 256 tile): the B stage keeps
+  // the 128-row footprint (K-major loads 112 rows; MN-major loads two 64-column swizzle
+  // atoms, the MMA reads 112 of their columns), TMEM buffers sit 224 columns apart
+  static constexpr int BNS = BN == 224 ? 128 : BNH;  // staged B footprint (rows / columns)
+  static constexpr int TMEM_COLS = BN == 224 ? 512 : 2 * BN;  // alloc: power of two
   static constexpr int A_BYTES = 128 * BK * 2;
-  static constexpr int B_BYTES = BNH * BK * 2;
+  static constexpr int B_BYTES = BNS * BK * 2;
+  static constexpr int B_LOAD = (BKM ? BNH : BNS) * BK * 2;  // bytes the B loads of a stage deliver
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STG_OFF = STAGES * STAGE_BYTES;
   static constexpr int STG_WARP = DB ? 10240 : kStageBytes;  // DB: 2 residual/fp32 + 1 bf16 buffer
@@ -988,7 +1002,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * BN));
+                 "r"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1010,7 +1024,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
           uint8_t* sa_ = smem + s * C::STAGE_BYTES;
           uint8_t* sb_ = sa_ + C::A_BYTES;
           const uint32_t lb = leader_addr(&full[s]);
-          if (leader) mbar_expect_tx(&full[s], 2 * C::STAGE_BYTES);
+          if (leader) mbar_expect_tx(&full[s], 2 * (C::A_BYTES + C::B_LOAD));
           const int k0 = kb * BK;
           if (AK) {
             tma_load_2d_pair(sa_, &mapA, lb, k0, m0);
@@ -1022,7 +1036,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
             tma_load_2d_pair(sb_, &mapB, lb, k0, n0);
           } else {
 #pragma unroll
-            for (int j = 0; j < C::BNH / 64; ++j) tma_load_2d_pair(sb_ + j * 64 * BK * 2, &mapB, lb, n0 + 64 * j, k0);
+            for (int j = 0; j < C::BNS / 64; ++j) tma_load_2d_pair(sb_ + j * 64 * BK * 2, &mapB, lb, n0 + 64 * j, k0);
           }
         }
       }
@@ -1059,7 +1073,8 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
     const int q = ew & 3;
     const int slice = ew >> 2;
     constexpr int NSL = EPW / 4;
-    constexpr int CW = BN / NSL;
+    constexpr int CW = (BN / 32 + NSL - 1) / NSL * 32;  // 32-column chunks per slice (224: 128 + 96)
+    const int c_lo = min(BN, slice * CW), c_hi = min(BN, (slice + 1) * CW);
     auto al = [](const void* p, int64_t ld, int esz) {
       return p == nullptr || (((reinterpret_cast<uintptr_t>(p) | static_cast<uintptr_t>(ld * esz)) & 15) == 0);
     };
@@ -1078,13 +1093,12 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       if (DB && (e.tma & 4))
-        epilogue_resid_db(g, e, om, taddr, m0 + q * 32, n0, slice * CW, (slice + 1) * CW, stg, lane, &ebar[2 * ew],
-                          eph2);
+        epilogue_resid_db(g, e, om, taddr, m0 + q * 32, n0, c_lo, c_hi, stg, lane, &ebar[2 * ew], eph2);
       else if (e.tma)
-        epilogue_store_tma(g, e, om, taddr, m0 + q * 32 + lane, m0 + q * 32, n0, slice * CW, (slice + 1) * CW, stg,
-                           lane, &ebar[2 * ew], ephase);
+        epilogue_store_tma(g, e, om, taddr, m0 + q * 32 + lane, m0 + q * 32, n0, c_lo, c_hi, stg, lane,
+                           &ebar[2 * ew], ephase);
       else
-        epilogue_store(g, e, taddr, m0 + q * 32 + lane, n0, slice * CW, (slice + 1) * CW, vec);
+        epilogue_store(g, e, taddr, m0 + q * 32 + lane, n0, c_lo, c_hi, vec);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(acc ? tempty_leader1
                                                                                             : tempty_leader0)
@@ -1096,7 +1110,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync_all();
   if (warp == 2) {
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
   }
 }
 
@@ -1179,9 +1193,14 @@ bool gemm_tc_pair(cudaStream_t s, const GemmShape& g, const Epi& e, int BN) {
   // -10 % at K = 896). DASHCU_GEMM_RESID_DEEP=0/1 forces either.
   const char* rdeep = getenv("DASHCU_GEMM_RESID_DEEP");
   const bool deep = rdeep ? rdeep[0] == '1' : g.K >= 2048;
-  if (BN == 256 && (et.tma & 4) && !(rdb && rdb[0] == '0') && deep)
+  const bool rdbl = (et.tma & 4) && !(rdb && rdb[0] == '0');
+  if (BN == 224) {  // N = 4 x 224 (e.g. d = 896) without the half-empty 256 tile
+    if (rdbl && deep) dispatch_pair<224, 5, true, 4>(s, ma, mb, om, g, et);
+    else if (rdbl) dispatch_pair<224, 4, true>(s, ma, mb, om, g, et);
+    else dispatch_pair<224, 6>(s, ma, mb, om, g, et);
+  } else if (BN == 256 && rdbl && deep)
     dispatch_pair<256, 5, true, 4>(s, ma, mb, om, g, et);
-  else if (BN == 256 && (et.tma & 4) && !(rdb && rdb[0] == '0')) dispatch_pair<256, 4, true>(s, ma, mb, om, g, et);
+  else if (BN == 256 && rdbl) dispatch_pair<256, 4, true>(s, ma, mb, om, g, et);
   else if (BN == 256) dispatch_pair<256, 6>(s, ma, mb, om, g, et);  // 6 x 32 KB stages
   else dispatch_pair<128, 8>(s, ma, mb, om, g, et);            // 8 x 24 KB stages
   return true;
@@ -1214,6 +1233,11 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
   // the 256 x 128 pair tile: half the N granularity, but measured at ~0.68 of the 128 x 256
   // per-SM rate (fwd_w2 771 vs 1166 TF/s), so it rarely wins
   const double cpair = rpair / 1.12, cpair128 = rpair128 * 0.5 / 0.68;
+  // 256 x 224 pair tiles: same tile count as 256 x 256 when N is a multiple of 224 but not
+  // of 256 (N = 896: 4 full tiles instead of 3.5), 7/8 of the MMA work per tile
+  const int tn224 = (g.N + 223) / 224;
+  const char* n224 = getenv("DASHCU_GEMM_N224");
+  const bool use224 = !(n224 && n224[0] == '0') && g.N % 224 == 0 && tn224 == (g.N + 255) / 256;
   // Split-K for accumulating GEMMs with few output tiles (weight gradients over a long
   // token axis): S K slices per tile fill the machine; each extra slice costs one more
   // ordered fp32 reduce of the tile (~3%). Slices keep >= 16 k-blocks.
@@ -1231,7 +1255,8 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
     split128 = best(tm * ((g.N + 127) / 128), 0.5 / 0.76, &c128);
     split256 = best(tm * ((g.N + 255) / 256), 1.0, &c256);
   }
-  // DASHCU_GEMM_PAIR: 1 force the 256x256 pair, 2 force the 256x128 pair, 0 model, -1 never
+  // DASHCU_GEMM_PAIR: 1 force the 256x256 pair, 2 force the 256x128 pair, 3 force the
+  // 256x224 pair, 0 model, -1 never
   const int forced = use_pair_default();
   const char* fbn = getenv("DASHCU_GEMM_BN");
   const char* fnarrow = getenv("DASHCU_GEMM_NARROW");
@@ -1239,9 +1264,11 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
   // decode shapes (dec_qkv 22.7 vs 14.8 us, dec_wo 21.8 vs 16.7 us)
   const bool narrow = !fbn && forced == 0 && fnarrow && fnarrow[0] == '1' && narrow_tiles(g, e);
   if (forced != -1 && !narrow) {
-    const bool p256 = forced == 1 || (forced == 0 && cpair < c256 && cpair < c128 && cpair <= cpair128);
+    const double cp = use224 ? cpair * 0.875 : cpair;
+    const bool p256 = forced == 1 || forced == 3 || (forced == 0 && cp < c256 && cp < c128 && cp <= cpair128);
     const bool p128 = forced == 2 || (forced == 0 && !p256 && cpair128 < c256 && cpair128 < c128);
-    if ((p256 && gemm_tc_pair(s, g, e, 256)) || (p128 && gemm_tc_pair(s, g, e, 128))) return true;
+    const int bn = forced == 3 || (forced != 1 && use224) ? 224 : 256;
+    if ((p256 && gemm_tc_pair(s, g, e, bn)) || (p128 && gemm_tc_pair(s, g, e, 128))) return true;
   }
   const bool wide = c256 <= c128;
   // Optional narrow 128 x 64 tiles for short-K GEMMs with few tiles (see `narrow` above).

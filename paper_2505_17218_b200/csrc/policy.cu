@@ -1682,7 +1682,13 @@ int dashcu_selftest_gemm_timed(dashcu_ctx* c, int M, int N, int K, int a_kmajor,
   if (res) DCU_CHECK(cudaMemsetAsync(res, 0, sizeof(float) * static_cast<size_t>(M) * N, s));
   GemmShape g{M, N, K, dA, a_kmajor ? K : M, a_kmajor != 0, dB, b_kmajor ? K : N, b_kmajor != 0};
   Epi e;
-  e.kind = epi == EPI_ACCUM ? EPI_ACCUM : EPI_STORE;
+  // epi 1: the W1 shape (bias + tanh, bf16 out)
+  e.kind = epi == EPI_ACCUM ? EPI_ACCUM : epi == EPI_TANH ? EPI_TANH : EPI_STORE;
+  if (epi == EPI_TANH) {
+    float* bias = c->ws.get<float>("tt_bias", N);
+    DCU_CHECK(cudaMemsetAsync(bias, 0, sizeof(float) * N, s));
+    e.bias = bias;
+  }
   e.c32 = c32;
   e.ldc32 = N;
   e.cT = cT;

@@ -58,7 +58,7 @@ def test_tc_gemm_epilogues(ctx):
     bias = rng.standard_normal(N).astype(np.float32)
     ref = bits_to_f32(A).astype(np.float64) @ bits_to_f32(B).astype(np.float64).T
     got = ctx.selftest_gemm(A, True, B, True, M, N, K, bias=bias, epi=1)
-    assert np.abs(got - np.tanh(ref + bias)).max() < 1e-5
+    assert np.abs(got - np.tanh(ref + bias)).max() < 1e-3   # tanh.approx: 2^-10.99 relative
     c0 = rng.standard_normal((M, N)).astype(np.float32)
     got = ctx.selftest_gemm(A, True, B, True, M, N, K, epi=3, C_init=c0)
     assert np.abs(got - (c0 + ref)).max() < 1e-4
@@ -89,8 +89,9 @@ def test_tma_store_epilogue_matches_direct_stores(ctx, monkeypatch, shape, epi):
     got = ctx.selftest_gemm(A, True, B, True, M, N, K, **kw)
     monkeypatch.setenv("DASHCU_NO_TMA_STORE", "1")
     ref = ctx.selftest_gemm(A, True, B, True, M, N, K, **kw)
-    if epi == 1:  # the direct path's ragged columns use the scalar epilogue (precise tanhf)
-        assert np.abs(got - ref).max() < 1e-6
+    if epi == 1:  # the direct path's ragged columns use the scalar epilogue (precise tanhf);
+        # the vector paths use MUFU tanh.approx (max relative error 2^-10.99, below bf16 rounding)
+        assert np.abs(got - ref).max() < 1e-3
         full = (N // 32) * 32
         assert np.array_equal(got[:, :full].view(np.uint32), ref[:, :full].view(np.uint32))
     else:
@@ -120,12 +121,13 @@ def test_split_k_accumulate(ctx, monkeypatch, shape, raster):
 
 
 @pytest.mark.parametrize("raster", ["0", "1"])
-@pytest.mark.parametrize("pair", ["1", "2", "-1"])
+@pytest.mark.parametrize("pair", ["1", "2", "3", "-1"])
 @pytest.mark.parametrize("ak,bk", [(True, True), (True, False), (False, True), (False, False)])
-@pytest.mark.parametrize("shape", [(256, 128, 64), (300, 200, 136), (4096, 896, 896), (1000, 1152, 320)])
+@pytest.mark.parametrize("shape", [(256, 128, 64), (300, 200, 136), (4096, 896, 896), (1000, 1152, 320),
+                                   (520, 448, 200)])
 def test_cta_pair_tiles(ctx, monkeypatch, pair, ak, bk, shape, raster):
-    """The cta_group::2 kernel with 256x256 (pair=1) and 256x128 (pair=2) tiles, forced, and
-    the single-CTA kernel (pair=-1), under both tile rasters (M or N tiles fastest)."""
+    """The cta_group::2 kernel with 256x256 (pair=1), 256x128 (pair=2) and 256x224 (pair=3)
+    tiles, forced, and the single-CTA kernel (pair=-1), under both tile rasters."""
     monkeypatch.setenv("DASHCU_GEMM_PAIR", pair)
     monkeypatch.setenv("DASHCU_GEMM_RASTER", raster)
     M, N, K = shape
@@ -139,9 +141,10 @@ def test_cta_pair_tiles(ctx, monkeypatch, pair, ak, bk, shape, raster):
     assert np.abs(got - ref).max() / max(1.0, np.abs(ref).max()) < 1e-5
 
 
+@pytest.mark.parametrize("pair", ["1", "3"])
 @pytest.mark.parametrize("deep", ["0", "1"])
 @pytest.mark.parametrize("shape", [(300, 200, 136), (4096, 896, 896), (1000, 1152, 320)])
-def test_pair_residual_prefetch_epilogue(ctx, monkeypatch, shape, deep):
+def test_pair_residual_prefetch_epilogue(ctx, monkeypatch, shape, deep, pair):
     """The CTA-pair kernel's double-buffered residual epilogue (fp32 resid in, fp32 out)
     equals the per-thread direct-store epilogue bit-for-bit, ragged edges included."""
     M, N, K = shape
@@ -150,7 +153,7 @@ def test_pair_residual_prefetch_epilogue(ctx, monkeypatch, shape, deep):
     B = bf16_bits(rng.standard_normal((N, K)).astype(np.float32) * 0.1)
     bias = rng.standard_normal(N).astype(np.float32)
     c0 = rng.standard_normal((M, N)).astype(np.float32)
-    monkeypatch.setenv("DASHCU_GEMM_PAIR", "1")
+    monkeypatch.setenv("DASHCU_GEMM_PAIR", pair)
     monkeypatch.setenv("DASHCU_GEMM_RESID_DEEP", deep)   # 5 stages x 4 epilogue warps
     got = ctx.selftest_gemm(A, True, B, True, M, N, K, bias=bias, epi=4, C_init=c0)
     monkeypatch.setenv("DASHCU_GEMM_RESID_DB", "0")

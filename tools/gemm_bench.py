@@ -21,6 +21,8 @@ SHAPES = {
     "fwd_wo_res": (36864, 896, 896, 1, 1, 4), "dgrad_qkv_res": (36864, 896, 1152, 1, 0, 4),
     "fwd_w2_res": (36864, 896, 4864, 1, 1, 4), "dgrad_w1_res": (36864, 896, 4864, 1, 0, 4),
     # small-output weight gradients (K = tokens of a micro-batch)
+    # tanh epilogue (W1 forward, decode and training)
+    "dec_w1_tanh": (4096, 4864, 896, 1, 1, 1), "fwd_w1_tanh": (36864, 4864, 896, 1, 1, 1),
     "wgrad_wo": (896, 896, 36864, 0, 0, 3), "wgrad_qkv": (1152, 896, 36864, 0, 0, 3),
 }
 
