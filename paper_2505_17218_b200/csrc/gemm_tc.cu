@@ -164,7 +164,12 @@ struct OutMaps {
 template <int BN, int STAGES, bool AK, bool BKM, int EPW>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  // BN = 224 (N = 4 x 224): the B stage keeps the 256-row footprint (K-major loads 224 rows,
+  // MN-major four 64-column atoms of which the MMA reads 224 columns)
+  static constexpr int BNS = BN == 224 ? 256 : BN;
+  static constexpr int B_BYTES = BNS * BK * 2;
+  static constexpr int B_LOAD = (BKM ? BN : BNS) * BK * 2;  // bytes the B loads of a stage deliver
+  static constexpr int TMEM_COLS = BN == 224 ? 512 : 2 * BN;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STG_OFF = STAGES * STAGE_BYTES;  // EPW x 4 KB epilogue staging
   static constexpr int BAR_OFF = STG_OFF + EPW * kStageBytes;
@@ -666,7 +671,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * BN));
+                 "r"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -688,7 +693,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
           mbar_wait_pipe(&empty[s], ph ^ 1);
           uint8_t* sa_ = smem + s * C::STAGE_BYTES;
           uint8_t* sb_ = sa_ + C::A_BYTES;
-          mbar_expect_tx(&full[s], C::STAGE_BYTES);
+          mbar_expect_tx(&full[s], C::A_BYTES + C::B_LOAD);
           const int k0 = kb * BK;
           if (AK) {
             tma_load_2d(sa_, &mapA, &full[s], k0, m0);
@@ -700,7 +705,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
             tma_load_2d(sb_, &mapB, &full[s], k0, n0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb_ + j * 64 * BK * 2, &mapB, &full[s], n0 + 64 * j, k0);
+            for (int j = 0; j < C::BNS / 64; ++j) tma_load_2d(sb_ + j * 64 * BK * 2, &mapB, &full[s], n0 + 64 * j, k0);
           }
         }
       }
@@ -739,7 +744,8 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
     const int q = ew & 3;                  // TMEM lane quarter (warp % 4 rule)
     const int slice = ew >> 2;             // column slice handled by this warp
     constexpr int NSL = EPW / 4;
-    constexpr int CW = BN / NSL;
+    constexpr int CW = (BN / 32 + NSL - 1) / NSL * 32;  // 32-column chunks per slice (224: 128 + 96)
+    const int c_lo = min(BN, slice * CW), c_hi = min(BN, (slice + 1) * CW);
     auto al = [](const void* p, int64_t ld, int esz) {
       return p == nullptr || (((reinterpret_cast<uintptr_t>(p) | static_cast<uintptr_t>(ld * esz)) & 15) == 0);
     };
@@ -760,16 +766,15 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
       const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       const int r0 = m0 + q * 32, row = r0 + lane;
       if constexpr (MODE == 1)
-        epilogue_sample(g, e, sa, om, taddr, row, r0, n0, slice * CW, (slice + 1) * CW, stg, lane);
+        epilogue_sample(g, e, sa, om, taddr, row, r0, n0, c_lo, c_hi, stg, lane);
       else if constexpr (MODE == 2)
-        epilogue_lse(g, e, sa, taddr, row, n0, slice * CW, (slice + 1) * CW, tile_n(g, t, tiles_m, tiles_n) * NSL + slice);
+        epilogue_lse(g, e, sa, taddr, row, n0, c_lo, c_hi, tile_n(g, t, tiles_m, tiles_n) * NSL + slice);
       else if constexpr (MODE == 3)
-        epilogue_dz(g, e, sa, om, taddr, row, r0, n0, slice * CW, (slice + 1) * CW, stg, lane);
+        epilogue_dz(g, e, sa, om, taddr, row, r0, n0, c_lo, c_hi, stg, lane);
       else if (e.tma)
-        epilogue_store_tma(g, e, om, taddr, row, r0, n0, slice * CW, (slice + 1) * CW, stg, lane, &ebar[ew],
-                           ephase);
+        epilogue_store_tma(g, e, om, taddr, row, r0, n0, c_lo, c_hi, stg, lane, &ebar[ew], ephase);
       else
-        epilogue_store(g, e, taddr, row, n0, slice * CW, (slice + 1) * CW, vec);
+        epilogue_store(g, e, taddr, row, n0, c_lo, c_hi, vec);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&tempty[acc]);
       if (flag) split_signal(flag, lane);
@@ -780,7 +785,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 2) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
   }
 }
 
@@ -1273,8 +1278,10 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
   const bool wide = c256 <= c128;
   // Optional narrow 128 x 64 tiles for short-K GEMMs with few tiles (see `narrow` above).
   // DASHCU_GEMM_BN forces 64 / 128 / 256.
+  // 128 x 224 single-CTA tiles exist (DASHCU_GEMM_BN=224) but measured no faster on the
+  // split-K weight-gradient shapes that take this path (wgrad_w1 -4 %, wgrad_wo +3 %)
   int BN = wide ? 256 : 128;
-  if (fbn) BN = atoi(fbn) == 64 ? 64 : atoi(fbn) == 128 ? 128 : 256;
+  if (fbn) BN = atoi(fbn) == 64 ? 64 : atoi(fbn) == 128 ? 128 : atoi(fbn) == 224 ? 224 : 256;
   else if (narrow) BN = 64;
   CUtensorMap ma, mb;
   bool ok = g.a_kmajor ? make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) : make_map(&ma, g.A, g.K, g.M, g.lda, 64, BK);
@@ -1284,7 +1291,7 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
   memset(&om, 0, sizeof(om));
   Epi et = e;
   et.tma = out_maps_for(g, e, &om);
-  const int S = BN == 256 ? split256 : BN == 128 ? split128 : 1;
+  const int S = BN == 256 || BN == 224 ? split256 : BN == 128 ? split128 : 1;
   if (S > 1 && (et.tma & 1)) {
     const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
     et.splits = S;
@@ -1292,6 +1299,7 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
     DCU_CHECK(cudaMemsetAsync(et.split_flags, 0, sizeof(uint32_t) * tiles * 8, s));
   }
   if (BN == 256) dispatch_majors<256, 4>(s, ma, mb, om, g, et);       // 4 x 48 KB stages
+  else if (BN == 224) dispatch_majors<224, 4>(s, ma, mb, om, g, et);  // 4 x 48 KB stages (B: 256-row footprint)
   else if (BN == 128) dispatch_majors<128, 6>(s, ma, mb, om, g, et);  // 6 x 32 KB stages
   else dispatch_majors<64, 8>(s, ma, mb, om, g, et);                  // 8 x 24 KB stages
   return true;

@@ -125,11 +125,16 @@ def test_split_k_accumulate(ctx, monkeypatch, shape, raster):
 @pytest.mark.parametrize("ak,bk", [(True, True), (True, False), (False, True), (False, False)])
 @pytest.mark.parametrize("shape", [(256, 128, 64), (300, 200, 136), (4096, 896, 896), (1000, 1152, 320),
                                    (520, 448, 200)])
-def test_cta_pair_tiles(ctx, monkeypatch, pair, ak, bk, shape, raster):
+@pytest.mark.parametrize("bn", ["", "224"])
+def test_cta_pair_tiles(ctx, monkeypatch, pair, ak, bk, shape, raster, bn):
     """The cta_group::2 kernel with 256x256 (pair=1), 256x128 (pair=2) and 256x224 (pair=3)
     tiles, forced, and the single-CTA kernel (pair=-1), under both tile rasters."""
+    if bn and pair != "-1":
+        pytest.skip("DASHCU_GEMM_BN selects the single-CTA tile width")
     monkeypatch.setenv("DASHCU_GEMM_PAIR", pair)
     monkeypatch.setenv("DASHCU_GEMM_RASTER", raster)
+    if bn:
+        monkeypatch.setenv("DASHCU_GEMM_BN", bn)   # 128 x 224 single-CTA tiles, forced
     M, N, K = shape
     rng = np.random.default_rng(M + N + K)
     A = bf16_bits(rng.standard_normal((M, K)).astype(np.float32))
