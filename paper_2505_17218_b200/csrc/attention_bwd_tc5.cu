@@ -124,14 +124,25 @@ __global__ void __launch_bounds__(384, 1)
     attn_bwd_tc5_k(const __grid_constant__ CUtensorMap mQKV, const __grid_constant__ CUtensorMap mO,
                    const __grid_constant__ CUtensorMap mDQ, const int32_t* __restrict__ seq_start,
                    const float* __restrict__ lse, const float* __restrict__ Dsum, int nh, int nkv,
-                   float* __restrict__ dkv32, float* __restrict__ dq32, float scale, float scale_log2) {
+                   float* __restrict__ dkv32, float* __restrict__ dq32, float scale, float scale_log2,
+                   int n_seq, int nkt2, int chunk) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // grid (sequence x kv head, key tile x 2): launch order puts every long (early) key tile
   // first. Key tiles with >= 3 causal query tiles split their query heads over two CTAs
   // (dK / dV of the halves are then reduce-added: two adds onto zero, order-independent),
   // which roughly halves the longest CTA and the tail of the last wave.
-  const int kt = blockIdx.y >> 1, part = blockIdx.y & 1, sq = blockIdx.x / nkv, kvh = blockIdx.x % nkv;
+  // chunk > 0 (1-D grid): CTAs in chunks of `chunk` sequences, each chunk ordered longest key
+  // tile first; the chunk's Q / dO / dQ rows stay in L2 while its CTAs run (the 2-D order
+  // walks every sequence's tile 0 first, a working set of the whole micro-batch)
+  int bx = blockIdx.x, by = blockIdx.y;
+  if (chunk > 0) {
+    const int per = chunk * nkv * nkt2, ch = bx / per, r = bx % per;
+    const int cs = min(chunk, n_seq - ch * chunk) * nkv;  // (sequence, kv head) pairs in this chunk
+    by = r / cs;
+    bx = ch * chunk * nkv + r % cs;
+  }
+  const int kt = by >> 1, part = by & 1, sq = bx / nkv, kvh = bx % nkv;
   const int s0 = seq_start[sq], n = seq_start[sq + 1] - s0;
   const int k0 = kt * kKeys;
   if (k0 >= n) return;  // uniform for the CTA, before any barrier
@@ -462,9 +473,14 @@ void launch_bwd_tc5(cudaStream_t s, const CUtensorMap& mq, const CUtensorMap& mo
     DCU_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay<ST, DQR>::BYTES));
     attr = true;
   }
-  dim3 grid(n_seq * nkv, 2 * ((max_len + kKeys - 1) / kKeys));
+  const int nkt2 = 2 * ((max_len + kKeys - 1) / kKeys);
+  const char* ce = getenv("DASHCU_ATTN_BWD_CHUNK");
+  // measured (C2 micro-batch, same box): 2-D order 0.508 ms, chunks of 2 / 4 / 8 sequences
+  // 0.429 / 0.413 / 0.415 ms (DRAM reads of Q / dO / dQ fall once a chunk fits in L2)
+  const int chunk = ce ? atoi(ce) : 4;
+  dim3 grid = chunk > 0 ? dim3(n_seq * nkv * nkt2, 1) : dim3(n_seq * nkv, nkt2);
   k<<<grid, 384, Lay<ST, DQR>::BYTES, s>>>(mq, mo, mdq, seq_start, lse, Dbuf, nh, nkv, dkv32, dq32, sc,
-                                             sc * 1.4426950408889634f);
+                                             sc * 1.4426950408889634f, n_seq, nkt2, chunk);
   DCU_LAUNCHED();
 }
 }  // namespace

@@ -953,8 +953,8 @@ struct Cfg2 {
   // BN = 224 (N = 896 = 4 x 224 without the half-empty fourth 256 tile): the B stage keeps
   // the 128-row footprint (K-major loads 112 rows; MN-major loads two 64-column swizzle
   // atoms, the MMA reads 112 of their columns), TMEM buffers sit 224 columns apart
-  static constexpr int BNS = BN == 224 ? 128 : BNH;  // staged B footprint (rows / columns)
-  static constexpr int TMEM_COLS = BN == 224 ? 512 : 2 * BN;  // alloc: power of two
+  static constexpr int BNS = BN == 224 || BN == 192 ? 128 : BNH;  // staged B footprint (rows / columns)
+  static constexpr int TMEM_COLS = BN == 224 || BN == 192 ? 512 : 2 * BN;  // alloc: power of two
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = BNS * BK * 2;
   static constexpr int B_LOAD = (BKM ? BNH : BNS) * BK * 2;  // bytes the B loads of a stage deliver
@@ -1203,6 +1203,10 @@ bool gemm_tc_pair(cudaStream_t s, const GemmShape& g, const Epi& e, int BN) {
     if (rdbl && deep) dispatch_pair<224, 5, true, 4>(s, ma, mb, om, g, et);
     else if (rdbl) dispatch_pair<224, 4, true>(s, ma, mb, om, g, et);
     else dispatch_pair<224, 6>(s, ma, mb, om, g, et);
+  } else if (BN == 192) {  // N = 6 x 192 (e.g. the QKV width 1152)
+    if (rdbl && deep) dispatch_pair<192, 5, true, 4>(s, ma, mb, om, g, et);
+    else if (rdbl) dispatch_pair<192, 4, true>(s, ma, mb, om, g, et);
+    else dispatch_pair<192, 6>(s, ma, mb, om, g, et);
   } else if (BN == 256 && rdbl && deep)
     dispatch_pair<256, 5, true, 4>(s, ma, mb, om, g, et);
   else if (BN == 256 && rdbl) dispatch_pair<256, 4, true>(s, ma, mb, om, g, et);
@@ -1240,9 +1244,19 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
   const double cpair = rpair / 1.12, cpair128 = rpair128 * 0.5 / 0.68;
   // 256 x 224 pair tiles: same tile count as 256 x 256 when N is a multiple of 224 but not
   // of 256 (N = 896: 4 full tiles instead of 3.5), 7/8 of the MMA work per tile
-  const int tn224 = (g.N + 223) / 224;
+  // Narrower pair tiles when N is not a multiple of 256: cost = rounds x BN / 256 over
+  // BN in {256, 224, 192} (N = 896: 4 x 224 instead of 3.5 x 256; N = 1152: 6 x 192 instead of
+  // 4.5 x 256). DASHCU_GEMM_N224=0 keeps 256.
   const char* n224 = getenv("DASHCU_GEMM_N224");
-  const bool use224 = !(n224 && n224[0] == '0') && g.N % 224 == 0 && tn224 == (g.N + 255) / 256;
+  int pbn = 256;
+  double pscale = 1.0;
+  if (!(n224 && n224[0] == '0')) {
+    for (int bn : {224, 192}) {
+      const double c = std::ceil(tm2 * ((g.N + bn - 1) / bn) / std::floor(sms / 2)) * bn / 256.0;
+      if (c < rpair * pscale * 0.98) pbn = bn, pscale = c / rpair;
+    }
+  }
+  const bool use224 = pbn != 256;
   // Split-K for accumulating GEMMs with few output tiles (weight gradients over a long
   // token axis): S K slices per tile fill the machine; each extra slice costs one more
   // ordered fp32 reduce of the tile (~3%). Slices keep >= 16 k-blocks.
@@ -1260,8 +1274,8 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
     split128 = best(tm * ((g.N + 127) / 128), 0.5 / 0.76, &c128);
     split256 = best(tm * ((g.N + 255) / 256), 1.0, &c256);
   }
-  // DASHCU_GEMM_PAIR: 1 force the 256x256 pair, 2 force the 256x128 pair, 3 force the
-  // 256x224 pair, 0 model, -1 never
+  // DASHCU_GEMM_PAIR: 1 force the 256x256 pair, 2 force the 256x128 pair, 3 / 4 force the
+  // 256x224 / 256x192 pair, 0 model, -1 never
   const int forced = use_pair_default();
   const char* fbn = getenv("DASHCU_GEMM_BN");
   const char* fnarrow = getenv("DASHCU_GEMM_NARROW");
@@ -1269,10 +1283,10 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
   // decode shapes (dec_qkv 22.7 vs 14.8 us, dec_wo 21.8 vs 16.7 us)
   const bool narrow = !fbn && forced == 0 && fnarrow && fnarrow[0] == '1' && narrow_tiles(g, e);
   if (forced != -1 && !narrow) {
-    const double cp = use224 ? cpair * 0.875 : cpair;
-    const bool p256 = forced == 1 || forced == 3 || (forced == 0 && cp < c256 && cp < c128 && cp <= cpair128);
+    const double cp = cpair * pscale;
+    const bool p256 = forced == 1 || forced == 3 || forced == 4 || (forced == 0 && cp < c256 && cp < c128 && cp <= cpair128);
     const bool p128 = forced == 2 || (forced == 0 && !p256 && cpair128 < c256 && cpair128 < c128);
-    const int bn = forced == 3 || (forced != 1 && use224) ? 224 : 256;
+    const int bn = forced == 3 ? 224 : forced == 4 ? 192 : (forced != 1 && use224) ? pbn : 256;
     if ((p256 && gemm_tc_pair(s, g, e, bn)) || (p128 && gemm_tc_pair(s, g, e, 128))) return true;
   }
   const bool wide = c256 <= c128;

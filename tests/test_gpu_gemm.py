@@ -121,7 +121,7 @@ def test_split_k_accumulate(ctx, monkeypatch, shape, raster):
 
 
 @pytest.mark.parametrize("raster", ["0", "1"])
-@pytest.mark.parametrize("pair", ["1", "2", "3", "-1"])
+@pytest.mark.parametrize("pair", ["1", "2", "3", "4", "-1"])
 @pytest.mark.parametrize("ak,bk", [(True, True), (True, False), (False, True), (False, False)])
 @pytest.mark.parametrize("shape", [(256, 128, 64), (300, 200, 136), (4096, 896, 896), (1000, 1152, 320),
                                    (520, 448, 200)])
@@ -146,7 +146,7 @@ def test_cta_pair_tiles(ctx, monkeypatch, pair, ak, bk, shape, raster, bn):
     assert np.abs(got - ref).max() / max(1.0, np.abs(ref).max()) < 1e-5
 
 
-@pytest.mark.parametrize("pair", ["1", "3"])
+@pytest.mark.parametrize("pair", ["1", "3", "4"])
 @pytest.mark.parametrize("deep", ["0", "1"])
 @pytest.mark.parametrize("shape", [(300, 200, 136), (4096, 896, 896), (1000, 1152, 320)])
 def test_pair_residual_prefetch_epilogue(ctx, monkeypatch, shape, deep, pair):

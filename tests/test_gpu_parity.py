@@ -282,13 +282,19 @@ def test_pg_gradient_parity(ctx, arch, dtype):
     pol.close()
 
 
-@pytest.mark.parametrize("kernel", ["tc5", "mma"])
+@pytest.mark.parametrize("kernel", ["tc5", "mma", "tc5:box:0", "tc5:box:3", "tc5:red:2"])
 def test_pg_gradient_parity_long_sequences(ctx, monkeypatch, kernel):
     """Ragged sequences up to 300 tokens: several key and query tiles, the causal
     diagonal tiles and ragged tile ends, through the tcgen05 and the mma.sync attention
-    kernels (forward and backward)."""
+    kernels (forward and backward); tc5:<dQ mode>:<chunk> are the backward's pipeline /
+    dQ-reduce variants and its chunked CTA order."""
     if kernel == "mma":
         monkeypatch.setenv("DASHCU_ATTN_BWD", "mma")
+    if kernel.startswith("tc5:"):
+        _, dq, chunk = kernel.split(":")
+        monkeypatch.setenv("DASHCU_ATTN_BWD_DQ", dq)
+        monkeypatch.setenv("DASHCU_ATTN_BWD_CHUNK", chunk)
+        kernel = "tc5"
     monkeypatch.setenv("DASHCU_ATTN_FWD", kernel)  # tc5 also below its 2-tile size threshold
     arch = LONGGQA
     pol = D.Policy(ctx, arch, D.BF16)

@@ -1,6 +1,7 @@
 """Training-phase microbenchmark at config-2 shapes (Qwen2.5-0.5B): one micro-batch of
 32 sequences x (128 prompt + 1024 completion) through dashcu_accumulate_weighted;
-prints per-kernel-class CUDA-event times."""
+prints per-kernel-class CUDA-event times. The rollout is sampled (4 prompts x G = 8, as in
+the DASH step); LOADED=1 loads random trajectories instead (LSE pass included)."""
 import json
 import os
 import sys
@@ -20,9 +21,15 @@ def main():
     pol = D.Policy(ctx, arch, D.BF16)
     pol.init_normal(0.02, 1)
     rng = np.random.default_rng(0)
-    prompts = [list(p) for p in W.synthetic_prompts(1, 0, n_seq, P, arch["vocab_size"], 0, 1)]
-    comps = [list(rng.integers(2, arch["vocab_size"], size=L)) for _ in range(n_seq)]
-    pol.load_rollout(prompts, 1, comps)
+    if os.environ.get("LOADED"):  # external trajectories: the backward runs its own LSE pass
+        prompts = [list(p) for p in W.synthetic_prompts(1, 0, n_seq, P, arch["vocab_size"], 0, 1)]
+        comps = [list(rng.integers(2, arch["vocab_size"], size=L)) for _ in range(n_seq)]
+        pol.load_rollout(prompts, 1, comps)
+    else:  # a sampled rollout (as in the DASH step): the backward reuses the sampler's LSE
+        G = 8
+        pr = W.synthetic_prompts(1, 0, n_seq // G, P, arch["vocab_size"], 0, 1)
+        pol.sample(None, G, L, prompt_tokens=pr.reshape(-1).copy(),
+                   prompt_offsets=(np.arange(n_seq // G + 1) * P).astype(np.int64))
     w = np.full(n_seq, 1.0 / n_seq)
     pol.grad_zero()
     pol.accumulate_weighted(w, micro_batch=n_seq)   # warm-up (allocations)
