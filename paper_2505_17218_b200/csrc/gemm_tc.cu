@@ -1245,13 +1245,14 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
   // 256 x 224 pair tiles: same tile count as 256 x 256 when N is a multiple of 224 but not
   // of 256 (N = 896: 4 full tiles instead of 3.5), 7/8 of the MMA work per tile
   // Narrower pair tiles when N is not a multiple of 256: cost = rounds x BN / 256 over
-  // BN in {256, 224, 192} (N = 896: 4 x 224 instead of 3.5 x 256; N = 1152: 6 x 192 instead of
-  // 4.5 x 256). DASHCU_GEMM_N224=0 keeps 256.
+  // BN in {256, 224} (N = 896: 4 x 224 instead of 3.5 x 256). DASHCU_GEMM_N224=0 keeps 256.
   const char* n224 = getenv("DASHCU_GEMM_N224");
   int pbn = 256;
   double pscale = 1.0;
   if (!(n224 && n224[0] == '0')) {
-    for (int bn : {224, 192}) {
+    // 192 (N = 1152 = 6 x 192) is modelled 10 % cheaper but measured 10 % slower on the
+    // training QKV shape (M 36832, K 896) and +3 % on the decode one: forced only (PAIR=4)
+    for (int bn : {224}) {
       const double c = std::ceil(tm2 * ((g.N + bn - 1) / bn) / std::floor(sms / 2)) * bn / 256.0;
       if (c < rpair * pscale * 0.98) pbn = bn, pscale = c / rpair;
     }
