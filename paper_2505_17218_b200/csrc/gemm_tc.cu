@@ -990,6 +990,11 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
   const int nkb = (g.K + BK - 1) / BK;
   const int tiles_m = (g.M + 255) / 256, tiles_n = (g.N + BN - 1) / BN;
   const int ntile = tiles_m * tiles_n;
+  // split-K (EPI_ACCUM only), as in the single-CTA kernel: item w = (tile w / S, K slice
+  // w % S); each CTA's epilogue warps reduce their 128-row half in slice order
+  const int S = e.splits > 1 ? e.splits : 1;
+  const int kps = (nkb + S - 1) / S;
+  const int nitem = ntile * S;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -1019,10 +1024,11 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
   if (warp == 0) {
     if (lane == 0) {
       int kb_all = 0;
-      for (int t = pair; t < ntile; t += npairs) {
+      for (int w = pair; w < nitem; w += npairs) {
+        const int t = w / S, kb_lo = (w % S) * kps, kb_hi = min(nkb, kb_lo + kps);
         const int m0 = tile_m(g, t, tiles_m, tiles_n) * 256 + static_cast<int>(rank) * 128;
         const int n0 = tile_n(g, t, tiles_m, tiles_n) * BN + static_cast<int>(rank) * C::BNH;
-        for (int kb = 0; kb < nkb; ++kb, ++kb_all) {
+        for (int kb = kb_lo; kb < kb_hi; ++kb, ++kb_all) {
           const int s = kb_all % STAGES;
           const uint32_t ph = (kb_all / STAGES) & 1;
           mbar_wait_pipe(&empty[s], ph ^ 1);
@@ -1049,13 +1055,14 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
   } else if (warp == 1) {
     if (leader && lane == 0) {
       int kb_all = 0, i = 0;
-      for (int t = pair; t < ntile; t += npairs, ++i) {
+      for (int w = pair; w < nitem; w += npairs, ++i) {
+        const int kb_lo = (w % S) * kps, kb_hi = min(nkb, kb_lo + kps);
         const int acc = i & 1;
         const uint32_t aph = (i >> 1) & 1;
         mbar_wait_cluster(&tempty[acc], aph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < nkb; ++kb, ++kb_all) {
+        for (int kb = kb_lo; kb < kb_hi; ++kb, ++kb_all) {
           const int s = kb_all % STAGES;
           const uint32_t ph = (kb_all / STAGES) & 1;
           mbar_wait_pipe(&full[s], ph);
@@ -1066,7 +1073,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t da = AK ? smem_desc(sa_ + k * 32, 16, 1024) : smem_desc(sa_ + k * 2048, 64 * BK * 2, 1024);
             const uint64_t db = BKM ? smem_desc(sb_ + k * 32, 16, 1024) : smem_desc(sb_ + k * 2048, 64 * BK * 2, 1024);
-            umma_bf16_pair(d, da, db, C::IDESC, (kb > 0 || k > 0) ? 1u : 0u);
+            umma_bf16_pair(d, da, db, C::IDESC, (kb > kb_lo || k > 0) ? 1u : 0u);
           }
           umma_commit_pair(&empty[s]);
         }
@@ -1089,13 +1096,16 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
     const uint32_t stg = smem_u32(smem + C::STG_OFF + ew * C::STG_WARP);
     uint32_t ephase = 0, eph2[2] = {0, 0};
     int i = 0;
-    for (int t = pair; t < ntile; t += npairs, ++i) {
+    for (int w = pair; w < nitem; w += npairs, ++i) {
+      const int t = w / S, sp = w % S;
       const int m0 = tile_m(g, t, tiles_m, tiles_n) * 256 + static_cast<int>(rank) * 128,
                 n0 = tile_n(g, t, tiles_m, tiles_n) * BN;
       const int acc = i & 1;
       const uint32_t aph = (i >> 1) & 1;
       mbar_wait_sleep(&tfull[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t* flag = S > 1 ? e.split_flags + (t * 2 + static_cast<int>(rank)) * EPW + ew : nullptr;
+      if (flag && sp > 0) split_wait(flag, sp, lane);  // K slices reduce into C in slice order
       const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       if (DB && (e.tma & 4))
         epilogue_resid_db(g, e, om, taddr, m0 + q * 32, n0, c_lo, c_hi, stg, lane, &ebar[2 * ew], eph2);
@@ -1108,6 +1118,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
       asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(acc ? tempty_leader1
                                                                                             : tempty_leader0)
                    : "memory");
+      if (flag) split_signal(flag, lane);
     }
     stage_drain(lane);
   }
@@ -1129,7 +1140,7 @@ void launch2(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const
     DCU_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
-  const int ntile = ((g.M + 255) / 256) * ((g.N + BN - 1) / BN);
+  const int ntile = ((g.M + 255) / 256) * ((g.N + BN - 1) / BN) * (e.splits > 1 ? e.splits : 1);
   const int pcap = (cta_cap() > 0 ? std::min(cta_cap(), num_sms()) : num_sms()) / 2;
   const int npairs = ntile < pcap ? ntile : pcap;
   cudaLaunchConfig_t cfg = {};
@@ -1180,7 +1191,7 @@ void dispatch_pair(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb,
 }
 
 // cta_group::2 GEMM with 256 x BN tiles (BN 256 or 128). Returns false if not TMA-legal.
-bool gemm_tc_pair(cudaStream_t s, const GemmShape& g, const Epi& e, int BN) {
+bool gemm_tc_pair(cudaStream_t s, const GemmShape& g, const Epi& e, int BN, int splits = 1) {
   if (!legal(g)) return false;
   CUtensorMap ma, mb;
   bool ok = g.a_kmajor ? make_map(&ma, g.A, g.M, g.K, g.lda, BK, 128) : make_map(&ma, g.A, g.K, g.M, g.lda, 64, BK);
@@ -1190,6 +1201,14 @@ bool gemm_tc_pair(cudaStream_t s, const GemmShape& g, const Epi& e, int BN) {
   memset(&om, 0, sizeof(om));
   Epi et = e;
   et.tma = out_maps_for(g, e, &om);
+  if (splits > 1 && e.kind == EPI_ACCUM && (et.tma & 1)) {  // ordered split-K (weight gradients)
+    const int tiles = ((g.M + 255) / 256) * ((g.N + BN - 1) / BN);
+    et.splits = splits;
+    et.split_flags = split_flag_buffer(tiles * 16);  // (tile, CTA of the pair, epilogue warp)
+    DCU_CHECK(cudaMemsetAsync(et.split_flags, 0, sizeof(uint32_t) * tiles * 16, s));
+  } else {
+    et.splits = 1;
+  }
   // residual epilogues (fp32 resid in, fp32 + bf16 out): 4 x 32 KB stages and the
   // double-buffered residual prefetch (DASHCU_GEMM_RESID_DB=0 disables)
   const char* rdb = getenv("DASHCU_GEMM_RESID_DB");
@@ -1258,6 +1277,18 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
     }
   }
   const bool use224 = pbn != 256;
+  // ordered split-K for accumulating pair GEMMs with few tiles (the weight gradients, e.g.
+  // dW1 = 19 x 4 pair tiles for 74 pairs: 2 rounds of which one is 3 % full), same cost
+  // model as the single-CTA split below
+  int splitp = 1;
+  double cpair_s = rpair * pscale;
+  if (e.kind == EPI_ACCUM && e.c32 && !getenv("DASHCU_NO_SPLITK") && !getenv("DASHCU_NO_PAIR_SPLITK")) {
+    const int tp = tm2 * ((g.N + pbn - 1) / pbn), nkb_ = (g.K + BK - 1) / BK;
+    for (int S = 2; S <= 8 && nkb_ / S >= 16; ++S) {
+      const double c = std::ceil(tp * S / std::floor(sms / 2)) / S * (pbn / 256.0) * (1.0 + 0.03 * (S - 1));
+      if (c < cpair_s * 0.97) cpair_s = c, splitp = S;
+    }
+  }
   // Split-K for accumulating GEMMs with few output tiles (weight gradients over a long
   // token axis): S K slices per tile fill the machine; each extra slice costs one more
   // ordered fp32 reduce of the tile (~3%). Slices keep >= 16 k-blocks.
@@ -1284,11 +1315,12 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
   // decode shapes (dec_qkv 22.7 vs 14.8 us, dec_wo 21.8 vs 16.7 us)
   const bool narrow = !fbn && forced == 0 && fnarrow && fnarrow[0] == '1' && narrow_tiles(g, e);
   if (forced != -1 && !narrow) {
-    const double cp = cpair * pscale;
+    const double cp = cpair_s / 1.12;
     const bool p256 = forced == 1 || forced == 3 || forced == 4 || (forced == 0 && cp < c256 && cp < c128 && cp <= cpair128);
     const bool p128 = forced == 2 || (forced == 0 && !p256 && cpair128 < c256 && cpair128 < c128);
     const int bn = forced == 3 ? 224 : forced == 4 ? 192 : (forced != 1 && use224) ? pbn : 256;
-    if ((p256 && gemm_tc_pair(s, g, e, bn)) || (p128 && gemm_tc_pair(s, g, e, 128))) return true;
+    if ((p256 && gemm_tc_pair(s, g, e, bn, bn == pbn ? splitp : 1)) || (p128 && gemm_tc_pair(s, g, e, 128)))
+      return true;
   }
   const bool wide = c256 <= c128;
   // Optional narrow 128 x 64 tiles for short-K GEMMs with few tiles (see `narrow` above).

@@ -98,13 +98,15 @@ def test_tma_store_epilogue_matches_direct_stores(ctx, monkeypatch, shape, epi):
         assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
 
 
+@pytest.mark.parametrize("pair", ["-1", "0", "3"])
 @pytest.mark.parametrize("raster", ["0", "1"])
-@pytest.mark.parametrize("shape", [(128, 128, 8192), (896, 896, 36832 // 8), (300, 200, 5000)])
-def test_split_k_accumulate(ctx, monkeypatch, shape, raster):
-    """Weight-gradient shapes (few output tiles, long K) run as ordered split-K: the
-    slices reduce into C in slice order, so repeated runs are bit-identical and the
-    result matches the unsplit kernel to fp32 rounding."""
+@pytest.mark.parametrize("shape", [(128, 128, 8192), (896, 896, 36832 // 8), (300, 200, 5000), (4864, 896, 4096)])
+def test_split_k_accumulate(ctx, monkeypatch, shape, raster, pair):
+    """Weight-gradient shapes (few output tiles, long K) run as ordered split-K (single-CTA
+    and CTA-pair kernels): the slices reduce into C in slice order, so repeated runs are
+    bit-identical and the result matches the unsplit kernel to fp32 rounding."""
     monkeypatch.setenv("DASHCU_GEMM_RASTER", raster)
+    monkeypatch.setenv("DASHCU_GEMM_PAIR", pair)   # -1 single-CTA split-K, 3: 256x224 pair split-K
     M, N, K = shape
     rng = np.random.default_rng(11)
     A = bf16_bits(rng.standard_normal((K, M)).astype(np.float32))   # MN-major operands, as in dW = dY^T X

@@ -1,8 +1,11 @@
 #!/bin/bash
 # Same-box A/B of a GEMM environment switch: tools/ab_gemm.sh VAR "v0 v1" shape...
-# (box-to-box variance is 10-30 %, so both arms run back to back in one call)
+# (box-to-box variance is 10-30 %, so both arms run back to back in one call); value "-" = unset
 VAR=$1; VALS=$2; shift 2
-for v in $VALS; do env $VAR=$v timeout 120 python tools/gemm_bench.py "$@" > gpurun_out/ab_$v.log; done
+for v in $VALS; do
+  if [ "$v" = "-" ]; then env -u $VAR timeout 120 python tools/gemm_bench.py "$@" > gpurun_out/ab_$v.log
+  else env $VAR=$v timeout 120 python tools/gemm_bench.py "$@" > gpurun_out/ab_$v.log; fi
+done
 python - "$VALS" <<'PY'
 import json, sys
 vals = sys.argv[1].split()
