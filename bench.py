@@ -41,10 +41,14 @@ CONFIGS = {
     "c2": dict(size="0.5b", prompts=512, G=8, prompt_len=128, max_len=1024, micro=32, tau=0.1,
                workload="BASELINE configs[1]: Qwen2.5-0.5B-shaped random-init policy, 512 prompts x G=8, "
                         "gen len 1024, per B200"),
-    "c3": dict(size="1.5b", prompts=256, G=8, prompt_len=128, max_len=1024, micro=32, tau=0.1,
+    # init std 0.01 at 1.5B / 3B: the reference math has no normalisation, and at std 0.02 the
+    # 28-layer residual stream grows until the fp32 gradient of a gen-1024 rollout overflows
+    # (|g| -> inf, measured with tools/len_probe.py; the update then NaNs the policy and later
+    # rollouts end after ~30 tokens). At 0.01: |g| 25 (1.5B) / 237 (3B), near-uniform policy.
+    "c3": dict(size="1.5b", prompts=256, G=8, prompt_len=128, max_len=1024, micro=32, tau=0.1, init=0.01,
                workload="BASELINE configs[2] shard: Qwen2.5-1.5B-shaped, 2048 prompts x G=8 over 8 B200 "
                         "(256 prompts per B200), micro-batch 32"),
-    "c4": dict(size="3b", prompts=64, G=8, prompt_len=128, max_len=2048, micro=32, tau=0.1,
+    "c4": dict(size="3b", prompts=64, G=8, prompt_len=128, max_len=2048, micro=32, tau=0.1, init=0.01,
                workload="BASELINE configs[3] shard: Qwen2.5-3B-shaped, gen len 2048, |A| filter 0.1, 512 prompts x G=8 "
                         "over 8 B200 (64 prompts per B200)"),
     "grpo": dict(size="0.5b", prompts=4, G=8, prompt_len=128, max_len=1024, micro=32, tau=None,
@@ -238,7 +242,7 @@ def run_ours(args, cfg, world, rank, local):
         dist.broadcast_object_list(obj, src=0)
         ctx.init_comm(world, rank, obj[0])
     pol = D.Policy(ctx, arch, D.BF16)
-    pol.init_normal(0.02, 1)
+    pol.init_normal(cfg.get("init", 0.02), 1)
     base = rank * M
     P = W.synthetic_prompts(1, base, base + M, cfg["prompt_len"], arch["vocab_size"], 0, 1)
     ptok = pinned(P.size, np.int32)
@@ -325,7 +329,8 @@ def run_ours(args, cfg, world, rank, local):
                    f" GQA {arch.get('n_heads', 1)}/{arch.get('n_kv_heads', 1)})", "prompts_per_gpu": M, "G": G,
                    "prompt_len": cfg["prompt_len"], "gen_len": ML, "micro_batch": cfg["micro"], "tau": cfg["tau"] if cfg["tau"] is not None else "off",
                    "optimizer": "adam (sharded, ZeRO-1)" if args.sharded else "adam", "global_batch": M * G * world, "seq_len": cfg["prompt_len"] + ML,
-                   "parallelism": f"dp{world}", "l2": "inputs > L2 (KV cache + weights stream every step)"},
+                   "parallelism": f"dp{world}", "init_std": cfg.get("init", 0.02),
+                   "mean_completion_len": tot_toks / (args.steps * M * G * world), "l2": "inputs > L2 (KV cache + weights stream every step)"},
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm" if hbm_bound else "tensor", "kernel": name, "achieved": achieved,

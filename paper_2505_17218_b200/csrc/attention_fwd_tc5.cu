@@ -1,14 +1,16 @@
-// tcgen05 attention forward for head_dim 64 (teacher-forced causal attention of the
+// tcgen05 attention forward for head_dim 64 and 128 (teacher-forced causal attention of the
 // training pass, policy.cpp:105-129; the mma.sync kernel in attention_tc.cu is the fallback).
 //
 // One CTA owns 128 queries of one sequence for every query head of a KV group (heads run
 // back to back through one pipeline) and walks the causal key tiles (128 keys each) with an
 // online softmax:
-//   S_j = Q K_j^T          M128 N128 K64    A = Q (K-major)   B = K_j (K-major)   -> TMEM S[j&1]
+//   S_j = Q K_j^T          M128 N128 K=hd   A = Q (K-major)   B = K_j (K-major)   -> TMEM S[j&1]
 //   softmax warps: m_j = max(m_{j-1}, rowmax(S_j)/sqrt(d)), P_j = exp(S_j/sqrt(d) - m_j) (bf16, smem)
-//   O_j = P_j V_j          M128 N64  K128   A = P_j (K-major) B = V_j (MN-major)  -> TMEM O[j&1]
+//   O_j = P_j V_j          M128 N=hd K128   A = P_j (K-major) B = V_j (MN-major)  -> TMEM O[j&1]
 //   registers: acc = acc * 2^(m_{j-1} - m_j) + O_j,  l likewise; out = acc / l, LSE = m + log l.
 // S and O are double-buffered in TMEM so the MMA of S_{j+1} and of O_j overlap the softmax.
+// Tiles of hd 128 are two 64-column swizzle atoms side by side (two TMA boxes); with 32 KB
+// tiles the shared-memory budget allows one Q stage and a 2-deep K/V ring.
 // Warp roles: 0 TMA producer (Q once, K/V kST-stage ring), 1 MMA issuer, 2 TMEM allocator,
 // 4..11 softmax (TMEM lane quarter = warp % 4; two warps per quarter split the columns).
 #include <cfloat>
@@ -39,7 +41,7 @@ int attn_trace_read(unsigned long long* out, int n) {
 
 namespace {
 
-constexpr int kQ = 128, kKeys = 128, kHD = 64;
+constexpr int kQ = 128, kKeys = 128;
 // A quarter of the forward's exponentials via ex2_poly (tc5.cuh): its exp loop is bound by
 // the MUFU unit (16 ex2 / clock / SM); measured -2.5 % (a half: +1.7 %, issue-bound).
 // -DDASHCU_NO_SPLIT_EXP disables.
@@ -52,19 +54,22 @@ constexpr bool kSplitExp = false;
 #define DASHCU_SPLIT_EVERY 2
 #endif
 constexpr int kSplitEvery = DASHCU_SPLIT_EVERY;  // one pair in kSplitEvery uses ex2_poly for its odd element
-constexpr int kTile = 128 * kHD * 2;  // 16 KB
+constexpr int kAtom = 128 * 64 * 2;  // 16 KB: 128 rows x one 64-column (128-byte) swizzle atom
 
-constexpr int kST = 4;  // K/V pipeline depth: loads run 3 key tiles ahead of the MMAs
-
+template <int HD>
 struct FLay {
-  static constexpr int Q = 0 /*2 stages*/, K = 2 * kTile /*kST stages*/, V = (2 + kST) * kTile /*kST stages*/;
-  static constexpr int P = (2 + 2 * kST) * kTile;  // P [128 q x 128 keys] bf16: two 64-key swizzle atoms
-  static constexpr int XMAX = P + 2 * kTile;  // row-max exchange [2][2][128] + row sums [2][128]
+  static constexpr int kTile = 128 * HD * 2;  // 16 / 32 KB: HD / 64 atoms
+  static constexpr int kQS = HD == 64 ? 2 : 1;  // Q stages
+  static constexpr int kST = HD == 64 ? 4 : 2;  // K/V pipeline depth (loads run kST - 1 key tiles ahead)
+  static constexpr int Q = 0, K = kQS * kTile, V = K + kST * kTile;
+  static constexpr int P = V + kST * kTile;  // P [128 q x 128 keys] bf16: two 64-key swizzle atoms
+  static constexpr int XMAX = P + 2 * kAtom;  // row-max exchange [2][2][128] + row sums [2][128]
   static constexpr int BAR = XMAX + 4096;
   static constexpr int BYTES = BAR + 256 + 1024;
+  static_assert(BYTES <= 232448, "exceeds the 227 KB of opt-in shared memory per CTA");
+  // TMEM columns: S double buffer, then the O double buffer (HD columns each)
+  static constexpr uint32_t TS0 = 0, TS1 = 128, TO0 = 256, TO1 = 256 + HD;
 };
-
-constexpr uint32_t kTS0 = 0, kTS1 = 128, kTO0 = 256, kTO1 = 320;
 
 constexpr uint32_t idesc(int n, bool a_mn, bool b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
@@ -82,9 +87,13 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+template <int HD>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_tc5_k(const __grid_constant__ CUtensorMap mQKV, const int32_t* __restrict__ seq_start, int nh, int nkv,
                    int nqt_max, bf16* __restrict__ ctx, float* __restrict__ lse, float scale_log2) {
+  using FLay = dashcu::FLay<HD>;
+  constexpr int kHD = HD, kTile = FLay::kTile, kST = FLay::kST, kQS = FLay::kQS;
+  constexpr uint32_t kTS0 = FLay::TS0, kTS1 = FLay::TS1, kTO0 = FLay::TO0, kTO1 = FLay::TO1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // grid (sequence x KV head, query tile), the longest (last) query tiles launched first; the
@@ -145,33 +154,42 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 0) {
     if (lane == 0) {  // ---------------------------------------------------------------- TMA
       for (int hh = 0, t = 0; hh < grp; ++hh) {
-        const int qs = hh & 1;
-        mbar_wait_sleep(&qempty[qs], ((hh >> 1) & 1) ^ 1);
+        const int qs = hh % kQS;
+        mbar_wait_sleep(&qempty[qs], ((hh / kQS) & 1) ^ 1);
         mbar_expect_tx(&qfull[qs], kTile);
-        tma_load_2d(smem + FLay::Q + qs * kTile, &mQKV, &qfull[qs], (kvh * grp0 + h_lo + hh) * kHD, s0 + q0);
+#pragma unroll
+        for (int a = 0; a < kHD / 64; ++a)
+          tma_load_2d(smem + FLay::Q + qs * kTile + a * kAtom, &mQKV, &qfull[qs],
+                      (kvh * grp0 + h_lo + hh) * kHD + a * 64, s0 + q0);
         for (int j = 0; j < nkt; ++j, ++t) {
           const int st = t % kST;
           mbar_wait_sleep(&kvempty[st], ((t / kST) & 1) ^ 1);
           mbar_expect_tx(&kvfull[st], 2 * kTile);
-          tma_load_2d(smem + FLay::K + st * kTile, &mQKV, &kvfull[st], qd + kvh * kHD, s0 + j * kKeys);
-          tma_load_2d(smem + FLay::V + st * kTile, &mQKV, &kvfull[st], qd + kvd + kvh * kHD, s0 + j * kKeys);
+#pragma unroll
+          for (int a = 0; a < kHD / 64; ++a) {
+            tma_load_2d(smem + FLay::K + st * kTile + a * kAtom, &mQKV, &kvfull[st], qd + kvh * kHD + a * 64,
+                        s0 + j * kKeys);
+            tma_load_2d(smem + FLay::V + st * kTile + a * kAtom, &mQKV, &kvfull[st], qd + kvd + kvh * kHD + a * 64,
+                        s0 + j * kKeys);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------------------------------------------------------- MMA
-      constexpr uint32_t I_S = idesc(128, false, false), I_O = idesc(64, false, true);
+      constexpr uint32_t I_S = idesc(128, false, false), I_O = idesc(kHD, false, true);
       auto issue_s = [&](int t) {
-        const int sb = t & 1, st = t % kST, hh = t / nkt, j = t % nkt, qs = hh & 1;
+        const int sb = t & 1, st = t % kST, hh = t / nkt, j = t % nkt, qs = hh % kQS;
         if (t >= 2) mbar_wait_sleep(&sfree[sb], ((t >> 1) - 1) & 1);  // softmax holds S_{t-2} in registers
-        if (j == 0) mbar_wait_sleep(&qfull[qs], (hh >> 1) & 1);
+        if (j == 0) mbar_wait_sleep(&qfull[qs], (hh / kQS) & 1);
         mbar_wait_sleep(&kvfull[st], (t / kST) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t k = sK + st * kTile, qa = sQ + qs * kTile;
 #pragma unroll
-        for (int kk = 0; kk < kHD / 16; ++kk)
-          umma_bf16(tmem + (sb ? kTS1 : kTS0), smem_desc(qa + kk * 32, 16, 1024), smem_desc(k + kk * 32, 16, 1024),
-                    I_S, kk > 0);
+        for (int kk = 0; kk < kHD / 16; ++kk) {  // 16-dim K step kk: atom kk / 4, 32-byte chunk kk % 4
+          const uint32_t o = (kk >> 2) * kAtom + (kk & 3) * 32;
+          umma_bf16(tmem + (sb ? kTS1 : kTS0), smem_desc(qa + o, 16, 1024), smem_desc(k + o, 16, 1024), I_S, kk > 0);
+        }
         umma_commit(&sfull[sb]);
         if (j == nkt - 1) umma_commit(&qempty[qs]);  // the head's last S: its Q tile is free
       };
@@ -187,8 +205,8 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t v = sV + st * kTile;
 #pragma unroll
         for (int kk = 0; kk < kKeys / 16; ++kk)
-          umma_bf16(tmem + (sb ? kTO1 : kTO0), smem_desc(sP + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024),
-                    smem_desc(v + kk * 2048, kTile, 1024), I_O, kk > 0);
+          umma_bf16(tmem + (sb ? kTO1 : kTO0), smem_desc(sP + (kk >> 2) * kAtom + (kk & 3) * 32, 16, 1024),
+                    smem_desc(v + kk * 2048, kAtom, 1024), I_O, kk > 0);  // V atoms kAtom apart along hd
         umma_commit(&kvempty[st]);
         umma_commit(&ofull[sb]);
         TRF(t, 2);
@@ -196,7 +214,7 @@ __global__ void __launch_bounds__(384, 1)
     }
   } else if (warp >= 4) {  // ---------------------------------------------------------- softmax
     // 8 warps: TMEM lane quarter qq = warp % 4 (query rows 32 qq ..), column half hf: keys
-    // [64 hf, 64 hf + 64) of S and head dims [32 hf, 32 hf + 32) of O. The two warps of a
+    // [64 hf, 64 hf + 64) of S and head dims [hd/2 hf, hd/2 hf + hd/2) of O. The two warps of a
     // quarter exchange their row maxima through shared memory once per tile (named barrier
     // 1 + qq, 64 threads); their row sums stay separate until the end.
     const int qq = warp & 3, hf = (warp - 4) >> 2, r = qq * 32 + lane, q = q0 + r;
@@ -209,17 +227,23 @@ __global__ void __launch_bounds__(384, 1)
       const int sb = t & 1;
       mbar_wait_sleep(&ofull[sb], (t >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      uint32_t o[kHD / 2];
-      tmem_ld32_async(tmem + lanes + (sb ? kTO1 : kTO0) + hf * 32, o);
-      tmem_wait_ld();
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(&ofree[sb]);
       const float c = ex2(m_old - m_new);
       const uint64_t c2 = f2_pack(c, c);
 #pragma unroll
-      for (int i = 0; i < kHD / 2; i += 2)  // packed fp32x2 FMAs
-        f2_unpack(f2_fma(f2_pack(acc[i], acc[i + 1]), c2, f2_pack(__uint_as_float(o[i]), __uint_as_float(o[i + 1]))),
-                  acc[i], acc[i + 1]);
+      for (int ch = 0; ch < kHD / 64; ++ch) {  // 32-column chunks (registers at hd 128)
+        uint32_t o[32];
+        tmem_ld32_async(tmem + lanes + (sb ? kTO1 : kTO0) + hf * (kHD / 2) + ch * 32, o);
+        tmem_wait_ld();
+        if (ch == kHD / 64 - 1) {
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          mbar_arrive(&ofree[sb]);
+        }
+#pragma unroll
+        for (int i = 0; i < 32; i += 2)  // packed fp32x2 FMAs
+          f2_unpack(f2_fma(f2_pack(acc[ch * 32 + i], acc[ch * 32 + i + 1]), c2,
+                           f2_pack(__uint_as_float(o[i]), __uint_as_float(o[i + 1]))),
+                    acc[ch * 32 + i], acc[ch * 32 + i + 1]);
+      }
     };
     for (int hh = 0, t = 0; hh < grp; ++hh) {
       const int h = kvh * grp0 + h_lo + hh;
@@ -280,7 +304,7 @@ __global__ void __launch_bounds__(384, 1)
         if (warp == 4) TRF(t, 9);
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch)  // keys [64 hf, 64 hf + 64) = swizzle atom hf of P
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sP + hf * kTile + r * 128 +
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sP + hf * kAtom + r * 128 +
                                                                          ((ch ^ (r & 7)) << 4)),
                        "r"(pk[ch * 4]), "r"(pk[ch * 4 + 1]), "r"(pk[ch * 4 + 2]), "r"(pk[ch * 4 + 3])
                        : "memory");
@@ -301,7 +325,7 @@ __global__ void __launch_bounds__(384, 1)
       asm volatile("bar.sync %0, 64;" ::"r"(1 + qq) : "memory");  // xl reused by the next head
       if (q < n) {
         const float inv = 1.f / lt;
-        bf16* out = ctx + static_cast<int64_t>(s0 + q) * qd + h * kHD + hf * 32;
+        bf16* out = ctx + static_cast<int64_t>(s0 + q) * qd + h * kHD + hf * (kHD / 2);
 #pragma unroll
         for (int i = 0; i < kHD / 2; i += 8) {
           uint4 v;
@@ -322,9 +346,25 @@ __global__ void __launch_bounds__(384, 1)
 
 }  // namespace
 
+namespace {
+template <int HD>
+void launch_fwd_tc5(cudaStream_t s, const CUtensorMap& mq, const int32_t* seq_start, int n_seq, int nqt, int nh,
+                    int nkv, bf16* ctx, float* lse) {
+  static bool attr = false;
+  if (!attr) {
+    DCU_CHECK(cudaFuncSetAttribute(attn_fwd_tc5_k<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, FLay<HD>::BYTES));
+    attr = true;
+  }
+  dim3 grid(n_seq * nkv, 2 * nqt);
+  attn_fwd_tc5_k<HD><<<grid, 384, FLay<HD>::BYTES, s>>>(mq, seq_start, nh, nkv, nqt, ctx, lse,
+                                                        1.4426950408889634f / sqrtf(static_cast<float>(HD)));
+  DCU_LAUNCHED();
+}
+}  // namespace
+
 bool attn_fwd_tc5(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int n_seq, int max_len, int rows, int nh,
                   int nkv, int hd, bf16* ctx, float* lse) {
-  if (hd != kHD || nh % nkv) return false;
+  if ((hd != 64 && hd != 128) || nh % nkv) return false;
   const char* force = getenv("DASHCU_ATTN_FWD");
   if (force && std::string(force) == "mma") return false;
   // one-tile sequences (the prompt prefill) amortise the per-CTA TMEM / barrier / first-load
@@ -332,17 +372,12 @@ bool attn_fwd_tc5(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int
   if (max_len <= 2 * kQ && !(force && std::string(force) == "tc5")) return false;
   const int qkvd = nh * hd + 2 * nkv * hd;
   CUtensorMap mq;
-  if (!tma_map_2d(&mq, qkv, rows, qkvd, qkvd, kHD, 128, false, 128, true)) return false;
-  static bool attr = false;
-  if (!attr) {
-    DCU_CHECK(cudaFuncSetAttribute(attn_fwd_tc5_k, cudaFuncAttributeMaxDynamicSharedMemorySize, FLay::BYTES));
-    attr = true;
-  }
+  if (!tma_map_2d(&mq, qkv, rows, qkvd, qkvd, 64, 128, false, 128, true)) return false;  // one swizzle atom per box
   const int nqt = (max_len + kQ - 1) / kQ;
-  dim3 grid(n_seq * nkv, 2 * nqt);
-  attn_fwd_tc5_k<<<grid, 384, FLay::BYTES, s>>>(mq, seq_start, nh, nkv, nqt, ctx, lse,
-                                                1.4426950408889634f / sqrtf(static_cast<float>(hd)));
-  DCU_LAUNCHED();
+  if (hd == 64)
+    launch_fwd_tc5<64>(s, mq, seq_start, n_seq, nqt, nh, nkv, ctx, lse);
+  else
+    launch_fwd_tc5<128>(s, mq, seq_start, n_seq, nqt, nh, nkv, ctx, lse);
   return true;
 }
 

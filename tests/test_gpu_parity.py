@@ -35,6 +35,9 @@ VBIG = dict(vocab_size=5003, embed_dim=64, context_len=32, ffn_hidden=64, n_laye
 # several 128-key / 128-query tiles per sequence (tcgen05 attention backward, GQA group 2)
 LONGGQA = dict(vocab_size=64, embed_dim=256, context_len=320, ffn_hidden=128, n_layers=1, bos_id=0, eos_id=1,
                n_heads=4, n_kv_heads=2, head_dim=64)
+# head_dim 128 (the 1.5B / 3B geometry) over several 128-key tiles
+LONGGQA128 = dict(vocab_size=64, embed_dim=256, context_len=320, ffn_hidden=128, n_layers=1, bos_id=0, eos_id=1,
+                  n_heads=4, n_kv_heads=2, head_dim=128)
 TOL = {D.F32: 1e-3, D.BF16: 2e-2}
 
 
@@ -301,6 +304,33 @@ def test_pg_gradient_parity_long_sequences(ctx, monkeypatch, kernel):
     p = params32(arch, 0.3, 10)
     pol.upload(p)
     rng = np.random.default_rng(12)
+    prompts, comps = rand_batch(rng, arch, 3, 2, m_range=(2, 20), len_range=(100, 300))
+    pol.load_rollout(prompts, 2, comps)
+    lp = pol.rollout_log_prob(sum(len(c) for c in comps))
+    ref_lp = np.concatenate([O.log_prob(arch, p, prompts[s // 2], comps[s])[1] for s in range(6)])
+    assert np.abs(lp - ref_lp).max() <= TOL[D.BF16] * max(1.0, np.abs(ref_lp).max())
+    w = rng.standard_normal(6) / 6
+    pol.grad_zero()
+    pol.accumulate_weighted(w, micro_batch=6)
+    got = pol.grad()
+    ref = np.zeros_like(got)
+    for s in range(6):
+        O.grad_log_prob(arch, p, prompts[s // 2], comps[s], w[s], ref)
+    assert_grad_close(arch, got, ref, TOL[D.BF16])
+    pol.close()
+
+
+@pytest.mark.parametrize("fwd,bwd", [("tc5", "tc5"), ("mma", "mma"), ("tc5", "mma")])
+def test_pg_gradient_parity_long_sequences_hd128(ctx, monkeypatch, fwd, bwd):
+    """head_dim 128 (two swizzle atoms per tile) over ragged sequences up to 300 tokens:
+    the tcgen05 forward / backward against the oracle, and the mma.sync kernels."""
+    monkeypatch.setenv("DASHCU_ATTN_FWD", fwd)
+    monkeypatch.setenv("DASHCU_ATTN_BWD", bwd)
+    arch = LONGGQA128
+    pol = D.Policy(ctx, arch, D.BF16)
+    p = params32(arch, 0.3, 10)
+    pol.upload(p)
+    rng = np.random.default_rng(14)
     prompts, comps = rand_batch(rng, arch, 3, 2, m_range=(2, 20), len_range=(100, 300))
     pol.load_rollout(prompts, 2, comps)
     lp = pol.rollout_log_prob(sum(len(c) for c in comps))
