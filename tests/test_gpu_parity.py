@@ -320,18 +320,21 @@ def test_pg_gradient_parity_long_sequences(ctx, monkeypatch, kernel):
     pol.close()
 
 
-@pytest.mark.parametrize("fwd,bwd", [("tc5", "tc5"), ("mma", "mma"), ("tc5", "mma")])
-def test_pg_gradient_parity_long_sequences_hd128(ctx, monkeypatch, fwd, bwd):
-    """head_dim 128 (two swizzle atoms per tile) over ragged sequences up to 300 tokens:
-    the tcgen05 forward / backward against the oracle, and the mma.sync kernels."""
+@pytest.mark.parametrize("fwd,bwd,ctxlen", [("tc5", "tc5", 320), ("mma", "mma", 320), ("tc5", "mma", 320),
+                                            ("tc5", "tc5", 600)])
+def test_pg_gradient_parity_long_sequences_hd128(ctx, monkeypatch, fwd, bwd, ctxlen):
+    """head_dim 128 (two swizzle atoms per tile) over ragged sequences up to 300 / 580
+    tokens: the tcgen05 forward / backward (64-query tiles, transposed dQ; at 600 the key
+    tiles with >= 6 query tiles split their heads over two CTAs) against the oracle, and
+    the mma.sync kernels."""
     monkeypatch.setenv("DASHCU_ATTN_FWD", fwd)
     monkeypatch.setenv("DASHCU_ATTN_BWD", bwd)
-    arch = LONGGQA128
+    arch = dict(LONGGQA128, context_len=ctxlen)
     pol = D.Policy(ctx, arch, D.BF16)
     p = params32(arch, 0.3, 10)
     pol.upload(p)
     rng = np.random.default_rng(14)
-    prompts, comps = rand_batch(rng, arch, 3, 2, m_range=(2, 20), len_range=(100, 300))
+    prompts, comps = rand_batch(rng, arch, 3, 2, m_range=(2, 20), len_range=(100, ctxlen - 20 - 1))
     pol.load_rollout(prompts, 2, comps)
     lp = pol.rollout_log_prob(sum(len(c) for c in comps))
     ref_lp = np.concatenate([O.log_prob(arch, p, prompts[s // 2], comps[s])[1] for s in range(6)])
