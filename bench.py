@@ -48,7 +48,9 @@ CONFIGS = {
     "c3": dict(size="1.5b", prompts=256, G=8, prompt_len=128, max_len=1024, micro=32, tau=0.1, init=0.01,
                workload="BASELINE configs[2] shard: Qwen2.5-1.5B-shaped, 2048 prompts x G=8 over 8 B200 "
                         "(256 prompts per B200), micro-batch 32"),
-    "c4": dict(size="3b", prompts=64, G=8, prompt_len=128, max_len=2048, micro=32, tau=0.1, init=0.01,
+    # micro-batch 16 at 3B: 32 x 2175 tokens of saved activations (~3.3 GB per layer x 36) do
+    # not fit beside the weights, Adam state and the 41 GB KV cache
+    "c4": dict(size="3b", prompts=64, G=8, prompt_len=128, max_len=2048, micro=16, tau=0.1, init=0.01,
                workload="BASELINE configs[3] shard: Qwen2.5-3B-shaped, gen len 2048, |A| filter 0.1, 512 prompts x G=8 "
                         "over 8 B200 (64 prompts per B200)"),
     "grpo": dict(size="0.5b", prompts=4, G=8, prompt_len=128, max_len=1024, micro=32, tau=None,

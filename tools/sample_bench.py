@@ -13,11 +13,11 @@ from paper_2505_17218_b200 import workload as W  # noqa: E402
 
 def main():
     steps = int(sys.argv[1]) if len(sys.argv) > 1 else 8
-    M, G, P = 512, 8, 128
-    arch = W.qwen_arch("0.5b", P + 1024)
+    M, G, P = int(os.environ.get("PROMPTS", "512")), 8, 128
+    arch = W.qwen_arch(os.environ.get("SIZE", "0.5b"), P + 1024)
     ctx = D.Context(0)
     pol = D.Policy(ctx, arch, D.BF16)
-    pol.init_normal(0.02, 1)
+    pol.init_normal(0.02 if os.environ.get("SIZE", "0.5b") == "0.5b" else 0.01, 1)  # as bench.py
     prompts = W.synthetic_prompts(1, 0, M, P, arch["vocab_size"], 0, 1)
     tok, off = np.ascontiguousarray(prompts.reshape(-1)), (np.arange(M + 1) * P).astype(np.int64)
     pol.sample(None, G, steps, prompt_tokens=tok, prompt_offsets=off)     # warm-up

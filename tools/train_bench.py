@@ -16,10 +16,10 @@ from paper_2505_17218_b200 import workload as W  # noqa: E402
 def main():
     n_seq = int(sys.argv[1]) if len(sys.argv) > 1 else 32
     P, L = 128, 1024
-    arch = W.qwen_arch("0.5b", P + L)
+    arch = W.qwen_arch(os.environ.get("SIZE", "0.5b"), P + L)
     ctx = D.Context(0)
     pol = D.Policy(ctx, arch, D.BF16)
-    pol.init_normal(0.02, 1)
+    pol.init_normal(0.02 if os.environ.get("SIZE", "0.5b") == "0.5b" else 0.01, 1)  # as bench.py
     rng = np.random.default_rng(0)
     if os.environ.get("LOADED"):  # external trajectories: the backward runs its own LSE pass
         prompts = [list(p) for p in W.synthetic_prompts(1, 0, n_seq, P, arch["vocab_size"], 0, 1)]
