@@ -321,9 +321,11 @@ __device__ __forceinline__ void unstage_b16(uint32_t buf, int lane, float* x) {
 // The fp32 residual (bit 2) or the bf16 tanh activations of EPI_DTANH (bit 3) arrive
 // as a 32 x 32 box in the warp's staging buffer (TMA load, zero-filled past M / N,
 // issued before the TMEM load); outputs leave through the same buffer as bulk stores.
+// `bias` is e.bias, or null for K slices after the first of a split-K accumulate (the
+// bias is added once per output element).
 __device__ __forceinline__ void epilogue_store_tma(const GemmShape& g, const Epi& e, const OutMaps& om, uint32_t taddr,
                                                    int row, int r0, int n0, int c_lo, int c_hi, uint32_t stg,
-                                                   int lane, uint64_t* ebar, uint32_t& ephase) {
+                                                   int lane, uint64_t* ebar, uint32_t& ephase, const float* bias) {
   float v[32], b[32];
   const bool live = row < g.M;
   const int64_t r64 = row;
@@ -343,10 +345,10 @@ __device__ __forceinline__ void epilogue_store_tma(const GemmShape& g, const Epi
         tma_load_2d(stg_ptr, tres ? &om.rs : &om.ax, ebar, nb, r0);
       }
     }
-    if (e.bias) load_bias32(e.bias, nb, g.N, b);  // broadcast loads, overlap the TMEM load
+    if (bias) load_bias32(bias, nb, g.N, b);  // broadcast loads, overlap the TMEM load
     tmem_ld32(taddr + c, v);
     const bool full = nb + 32 <= g.N;
-    if (e.bias) {
+    if (bias) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = __fmaf_rn(v[i], e.alpha, b[i]);
     } else {
@@ -772,7 +774,8 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
       else if constexpr (MODE == 3)
         epilogue_dz(g, e, sa, om, taddr, row, r0, n0, c_lo, c_hi, stg, lane);
       else if (e.tma)
-        epilogue_store_tma(g, e, om, taddr, row, r0, n0, c_lo, c_hi, stg, lane, &ebar[ew], ephase);
+        epilogue_store_tma(g, e, om, taddr, row, r0, n0, c_lo, c_hi, stg, lane, &ebar[ew], ephase,
+                           sp > 0 ? nullptr : e.bias);
       else
         epilogue_store(g, e, taddr, row, n0, c_lo, c_hi, vec);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1111,7 +1114,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
         epilogue_resid_db(g, e, om, taddr, m0 + q * 32, n0, c_lo, c_hi, stg, lane, &ebar[2 * ew], eph2);
       else if (e.tma)
         epilogue_store_tma(g, e, om, taddr, m0 + q * 32 + lane, m0 + q * 32, n0, c_lo, c_hi, stg, lane,
-                           &ebar[2 * ew], ephase);
+                           &ebar[2 * ew], ephase, sp > 0 ? nullptr : e.bias);
       else
         epilogue_store(g, e, taddr, m0 + q * 32 + lane, n0, c_lo, c_hi, vec);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1244,6 +1247,37 @@ bool raster_n_fast(const GemmShape& g) {
   return a > 2.0 * b && a > 48e6;
 }
 
+// K slices for an fp32-accumulate (EPI_ACCUM) CTA-pair GEMM of this shape such that every
+// slice of every tile runs in ONE round of the persistent grid (1 = no split); the caller
+// requests them through Epi::splits. The
+// decode uses it to pick the accumulate form of its long-K residual projections whose few
+// output tiles leave most SMs idle (C4 W2: M 512 x N 2048 = 20 pair tiles of 256 x 224 for
+// 74 pairs, K 11008: 3 slices, 61 -> 45 us). With more than one round the in-order slice reduces serialise the epilogues
+// (measured: C3 W2, 56 tiles x 5 slices, 77 -> 108 us).
+int gemm_tc_accum_splits(int M, int N, int K) {
+  if (getenv("DASHCU_NO_SPLITK") || getenv("DASHCU_NO_PAIR_SPLITK") || getenv("DASHCU_NO_DECODE_SPLITK")) return 1;
+  // K >= 4096 only: the accumulate form costs a bf16 copy kernel, which shorter K slices do
+  // not repay (measured: C4 Wo, K 2048, 2 slices: slower than the store form)
+  if (K < 4096) return 1;
+  const int tm2 = (M + 255) / 256, nkb = (K + BK - 1) / BK;
+  const double pairs = std::floor(num_sms() / 2.0);
+  const double rpair = std::ceil(tm2 * ((N + 255) / 256) / pairs);
+  int pbn = 256;
+  double cost = rpair;
+  const char* n224 = getenv("DASHCU_GEMM_N224");
+  if (!(n224 && n224[0] == '0')) {
+    const double c = std::ceil(tm2 * ((N + 223) / 224) / pairs) * 224 / 256.0;
+    if (c < rpair * 0.98) pbn = 224, cost = c;
+  }
+  const int tp = tm2 * ((N + pbn - 1) / pbn);
+  int split = 1;
+  for (int S = 2; S <= 8 && nkb / S >= 16 && tp * S <= pairs; ++S) {
+    const double c = 1.0 / S * (pbn / 256.0) * (1.0 + 0.03 * (S - 1));
+    if (c < cost * 0.97) cost = c, split = S;
+  }
+  return split;
+}
+
 bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
   if (!legal(g_in)) return false;
   GemmShape g = g_in;
@@ -1277,6 +1311,8 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
     }
   }
   const bool use224 = pbn != 256;
+  // caller-requested K slices (gemm_tc_accum_splits: the decode's residual projections)
+  if (e.kind == EPI_ACCUM && e.c32 && e.splits > 1 && gemm_tc_pair(s, g, e, pbn, e.splits)) return true;
   // ordered split-K for accumulating pair GEMMs with few tiles (the weight gradients, e.g.
   // dW1 = 19 x 4 pair tiles for 74 pairs: 2 rounds of which one is 3 % full), same cost
   // model as the single-CTA split below
@@ -1338,6 +1374,7 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
   memset(&om, 0, sizeof(om));
   Epi et = e;
   et.tma = out_maps_for(g, e, &om);
+  et.splits = 1;  // a caller's request applies to the pair path only
   const int S = BN == 256 || BN == 224 ? split256 : BN == 128 ? split128 : 1;
   if (S > 1 && (et.tma & 1)) {
     const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);

@@ -321,6 +321,15 @@ struct Engine {
     GemmShape s{M, N, K, A, lda, ak, B, ldb, bk};
     gemm(st, dt(), s, e);
   }
+  static Epi accum(float* c32, int64_t ldc32, const float* bias, int splits = 1) {  // c32 += v (+ bias)
+    Epi e;
+    e.splits = splits;  // > 1: K slices requested from the tcgen05 pair GEMM
+    e.kind = EPI_ACCUM;
+    e.c32 = c32;
+    e.ldc32 = ldc32;
+    e.bias = bias;
+    return e;
+  }
   static Epi store(float* c32, int64_t ldc32, T* cT, int64_t ldcT) {
     Epi e;
     e.c32 = c32;
@@ -842,6 +851,10 @@ struct Engine {
     const char* gsms = getenv("DASHCU_DECODE_GEMM_SMS");
     const int NH = (sizeof(T) == 2 && halves_on && !dump && S >= 1024 && (S / 2) % G == 0) ? 2 : 1;
     const int R = S / NH;  // rows per half
+    // accumulate form of the residual projections (see the layer loop); DASHCU_NO_DECODE_SPLITK=1 disables
+    const int spl_wo = sizeof(T) == 2 ? gemm_tc_accum_splits(R, g.d, g.qd) : 1;
+    const int spl_w2 = sizeof(T) == 2 ? gemm_tc_accum_splits(R, g.d, g.H) : 1;
+    const bool acc_wo = spl_wo > 1, acc_w2 = spl_w2 > 1;
     cudaStream_t main_st = st;
     cudaStream_t streams[2] = {st, st};
     cudaEvent_t ev_main = nullptr, ev_side = nullptr;
@@ -908,19 +921,37 @@ struct Engine {
           if (!done)
             attn_decode<T>(st, qkv_h, kp_h, vp_h, kc_h, vc_h, d_plen + r0, R, G, pmax, j, cslots, g.nh, g.nkv, g.hd,
                            ctx_h, kv_bytes);
-          Epi eo = store(h32 + rd, g.d, hT + rd, g.d);
-          eo.resid = x32 + rd;
-          eo.ldr = g.d;
-          mm(R, g.d, g.qd, ctx_h, g.qd, true, W(b + L.wo), g.qd, true, eo);
+          // residual projections h = x + Wo ctx, x' = h + W2 u + b2: the store form (fp32 + bf16
+          // outputs in the epilogue) or, where the planner splits K with every slice in one
+          // round (few output tiles over a long K: C4's W2 / Wo), the accumulate form in place
+          // on x32 (ordered split-K, bias on the first slice) followed by the bf16 copy the
+          // next GEMM reads
+          if (acc_wo) {
+            mm(R, g.d, g.qd, ctx_h, g.qd, true, W(b + L.wo), g.qd, true, accum(x32 + rd, g.d, nullptr, spl_wo));
+            if constexpr (sizeof(T) == 2)
+              cast_f32_bf16(st, x32 + rd, reinterpret_cast<bf16*>(hT + rd), static_cast<int64_t>(R) * g.d);
+          } else {
+            Epi eo = store(acc_w2 ? x32 + rd : h32 + rd, g.d, hT + rd, g.d);  // acc_w2: h in place in x32
+            eo.resid = x32 + rd;
+            eo.ldr = g.d;
+            mm(R, g.d, g.qd, ctx_h, g.qd, true, W(b + L.wo), g.qd, true, eo);
+          }
           Epi e1 = store(nullptr, 0, u + static_cast<size_t>(r0) * g.H, g.H);
           e1.kind = EPI_TANH;
           e1.bias = W32(b + L.b1);
           mm(R, g.H, g.d, hT + rd, g.d, true, W(b + L.w1), g.d, true, e1);
-          Epi e2 = store(x32 + rd, g.d, xT + rd, g.d);
-          e2.bias = W32(b + L.b2);
-          e2.resid = h32 + rd;
-          e2.ldr = g.d;
-          mm(R, g.d, g.H, u + static_cast<size_t>(r0) * g.H, g.H, true, W(b + L.w2), g.H, true, e2);
+          if (acc_w2) {
+            mm(R, g.d, g.H, u + static_cast<size_t>(r0) * g.H, g.H, true, W(b + L.w2), g.H, true,
+               accum(x32 + rd, g.d, W32(b + L.b2), spl_w2));
+            if constexpr (sizeof(T) == 2)
+              cast_f32_bf16(st, x32 + rd, reinterpret_cast<bf16*>(xT + rd), static_cast<int64_t>(R) * g.d);
+          } else {
+            Epi e2 = store(x32 + rd, g.d, xT + rd, g.d);
+            e2.bias = W32(b + L.b2);
+            e2.resid = (acc_wo ? x32 : h32) + rd;  // acc_wo: h in place in x32
+            e2.ldr = g.d;
+            mm(R, g.d, g.H, u + static_cast<size_t>(r0) * g.H, g.H, true, W(b + L.w2), g.H, true, e2);
+          }
         }
       }
       st = main_st;

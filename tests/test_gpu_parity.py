@@ -38,6 +38,10 @@ LONGGQA = dict(vocab_size=64, embed_dim=256, context_len=320, ffn_hidden=128, n_
 # head_dim 128 (the 1.5B / 3B geometry) over several 128-key tiles
 LONGGQA128 = dict(vocab_size=64, embed_dim=256, context_len=320, ffn_hidden=128, n_layers=1, bos_id=0, eos_id=1,
                   n_heads=4, n_kv_heads=2, head_dim=128)
+# ffn_hidden 4096: the decode's W2 GEMM (K = 4096, one output tile) takes the ordered
+# split-K accumulate form (x32 += W2 u + b2 in place, then the bf16 copy)
+WIDEFFN = dict(vocab_size=64, embed_dim=128, context_len=48, ffn_hidden=4096, n_layers=2, bos_id=0, eos_id=1,
+               n_heads=2, n_kv_heads=1, head_dim=64)
 TOL = {D.F32: 1e-3, D.BF16: 2e-2}
 
 
@@ -534,4 +538,33 @@ def test_long_sequences_multi_tile(ctx, dtype):
         for j in (0, len(comp) // 2, len(comp) - 1):
             refl = O.next_logits(arch, p, prompts[s // 2] + comp[:j])
             assert np.abs(dump[s, j] - refl).max() <= (1e-3 if dtype == D.F32 else 5e-2) * max(1, np.abs(refl).max())
+    pol.close()
+
+
+@pytest.mark.parametrize("splitk", ["1", "0"])
+def test_decode_split_k_residual_projection(ctx, monkeypatch, splitk):
+    """Decode with a long-K W2 (ffn_hidden 4096): the split-K accumulate form of the
+    residual projection (default) and the store form (DASHCU_NO_DECODE_SPLITK=1) both
+    replay their tokens bit-exactly from the logits dump, and the dumped logits match the
+    oracle's forward."""
+    if splitk == "0":
+        monkeypatch.setenv("DASHCU_NO_DECODE_SPLITK", "1")
+    arch = WIDEFFN
+    pol = D.Policy(ctx, arch, D.BF16)
+    p = params32(arch, 0.5, 21)
+    pol.upload(p)
+    rng = np.random.default_rng(22)
+    prompts = [[0] + list(rng.integers(2, 64, size=int(rng.integers(3, 12)))) for _ in range(3)]
+    pol.set_logits_dump(True)
+    ro = pol.sample(prompts, 4, 30, round_seed=5)
+    dump = pol.logits_dump(12, 30)
+    for s in range(12):
+        key = O.derive_seed(5, "sample", s // 4, s % 4)
+        for j in range(int(ro.lengths[s])):
+            assert O.sample_rule(dump[s, j], 0, 1.0, key, j) == ro.completions[s, j]
+    for s in (0, 7, 11):
+        comp = list(ro.completion(s))
+        for j in (0, len(comp) // 2, max(len(comp) - 1, 0)):
+            refl = O.next_logits(arch, p, prompts[s // 4] + comp[:j])
+            assert np.abs(dump[s, j] - refl).max() <= 5e-2 * max(1, np.abs(refl).max())
     pol.close()
