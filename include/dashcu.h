@@ -226,6 +226,14 @@ DASHCU_API int dashcu_profile_read(dashcu_kprof* out, int max, int reset);
  * Returns the full length; copies at most cap-1 bytes + NUL. Reset with profile_read. */
 DASHCU_API int64_t dashcu_profile_keys(char* buf, int64_t cap);
 
+/* ---- kernel-variant knobs (tests and same-box A/B tools) ----
+ * Read once from DASHCU_<NAME> environment variables at library load; this call changes
+ * one for the calling process (INT32_MIN restores the default). Names: GEMM_PAIR,
+ * GEMM_RASTER, NO_SPLITK, NO_TMA_STORE, GEMM_RESID_DB, GEMM_RESID_DEEP, ATTN_FWD,
+ * ATTN_BWD, ATTN_BWD_CHUNK, LSE_RECOMPUTE, PDL, DECODE_GRAPH (csrc/common.cuh Knob).
+ * Returns the previous value, INT32_MIN for an unknown name. */
+DASHCU_API int dashcu_set_knob(const char* name, int value);
+
 /* ---- diagnostics (used by the kernel tests) ----
  * C[M x N] (fp32, ldc = N) = A(m,k) . B(n,k) on bf16 operands given as raw
  * bit patterns, through the production GEMM dispatcher (tcgen05 when the

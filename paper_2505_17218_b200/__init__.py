@@ -154,6 +154,8 @@ def lib():
         L.dashcu_profile_sampling.restype = C.c_int
         L.dashcu_profile_keys.argtypes = [C.c_char_p, C.c_int64]
         L.dashcu_profile_keys.restype = C.c_int64
+        L.dashcu_set_knob.argtypes = [C.c_char_p, C.c_int]
+        L.dashcu_set_knob.restype = C.c_int
         _lib = L
     return _lib
 
@@ -166,6 +168,18 @@ def _check(rc: int):
 
 def _p(a: np.ndarray, t):
     return a.ctypes.data_as(t) if a is not None else None
+
+
+KNOB_DEFAULT = -(2 ** 31)
+
+
+def set_knob(name: str, value) -> int:
+    """Kernel-variant knob (dashcu_set_knob); value None restores the default. Returns the old value."""
+    v = KNOB_DEFAULT if value is None else int({"mma": 1, "tc5": 2}.get(value, value))
+    old = lib().dashcu_set_knob(name.encode(), v)
+    if old == KNOB_DEFAULT:
+        raise InputError(f"unknown knob {name}")
+    return old
 
 
 def kernel_launches() -> int:

@@ -18,6 +18,8 @@ OBJ_DIR = os.path.join(OUT_DIR, "obj")
 # Experiment builds (A/B of compile-time variants, tools only): DASHCU_NVCC_EXTRA adds nvcc
 # flags (e.g. -D...), DASHCU_LIB_OUT names the output library; load it with DASHCU_LIB_PATH.
 LIB = os.environ.get("DASHCU_LIB_OUT") or os.path.join(OUT_DIR, "libdashcu.so")
+# object list of each built library (untracked; lives beside the objects)
+OBJS_LIST = os.path.join(OBJ_DIR, os.path.basename(LIB) + ".objs")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -70,7 +72,7 @@ def build(verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
-        with open(LIB + ".objs", "w") as f:
+        with open(OBJS_LIST, "w") as f:
             f.write("\n".join(objs))
     _prune_objs()
     return LIB
@@ -79,9 +81,9 @@ def build(verbose: bool = False) -> str:
 def _prune_objs():
     """Drop object files no library's .objs list references (old header digests)."""
     keep = set()
-    for f in os.listdir(OUT_DIR):
+    for f in os.listdir(OBJ_DIR):
         if f.endswith(".objs"):
-            with open(os.path.join(OUT_DIR, f)) as fh:
+            with open(os.path.join(OBJ_DIR, f)) as fh:
                 keep.update(os.path.abspath(ln.strip()) for ln in fh if ln.strip())
     for f in os.listdir(OBJ_DIR):
         p = os.path.abspath(os.path.join(OBJ_DIR, f))
@@ -91,7 +93,7 @@ def _prune_objs():
 
 def _stale_objs(objs):
     try:
-        return open(LIB + ".objs").read().split("\n") != objs
+        return open(OBJS_LIST).read().split("\n") != objs
     except OSError:
         return True
 

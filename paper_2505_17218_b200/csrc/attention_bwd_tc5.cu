@@ -777,10 +777,9 @@ void launch_bwd_tc5(cudaStream_t s, const CUtensorMap& mq, const CUtensorMap& mo
     attr = true;
   }
   const int nkt2 = 2 * ((max_len + kKeys - 1) / kKeys);
-  const char* ce = getenv("DASHCU_ATTN_BWD_CHUNK");
   // measured (C2 micro-batch, same box): 2-D order 0.508 ms, chunks of 2 / 4 / 8 sequences
   // 0.429 / 0.413 / 0.415 ms (DRAM reads of Q / dO / dQ fall once a chunk fits in L2)
-  const int chunk = ce ? atoi(ce) : 4;
+  const int chunk = knob(KNOB_ATTN_BWD_CHUNK);
   dim3 grid = chunk > 0 ? dim3(n_seq * nkv * nkt2, 1) : dim3(n_seq * nkv, nkt2);
   k<<<grid, 384, Lay<ST, DQR>::BYTES, s>>>(mq, mo, mdq, seq_start, lse, Dbuf, nh, nkv, dkv32, dq32, sc,
                                              sc * 1.4426950408889634f, n_seq, nkt2, chunk);
@@ -792,10 +791,8 @@ bool attn_bwd_tc5(cudaStream_t s, const bf16* qkv, const bf16* dctx, const float
                   const int32_t* seq_start, int n_seq, int max_len, int rows, int nh, int nkv, int hd, float* dq32,
                   float* dkv32) {
   if ((hd != kHD && hd != kHD128) || nh % nkv) return false;
-  const char* force = getenv("DASHCU_ATTN_BWD");
-  if (force && std::string(force) == "mma") return false;
+  if (knob(KNOB_ATTN_BWD) == 1) return false;
   const int qd = nh * hd, qkvd = qd + 2 * nkv * hd;
-  const char* ce = getenv("DASHCU_ATTN_BWD_CHUNK");
   if (hd == kHD128) {
     CUtensorMap mkv, mq, mo, mdq;
     if (!tma_map_2d(&mkv, qkv, rows, qkvd, qkvd, 64, 128, false, 128, true) ||
@@ -809,7 +806,7 @@ bool attn_bwd_tc5(cudaStream_t s, const bf16* qkv, const bf16* dctx, const float
       attr = true;
     }
     const int nkt2 = 2 * ((max_len + kKeys - 1) / kKeys);
-    const int chunk = ce ? atoi(ce) : 4;
+    const int chunk = knob(KNOB_ATTN_BWD_CHUNK);
     dim3 grid = chunk > 0 ? dim3(n_seq * nkv * nkt2, 1) : dim3(n_seq * nkv, nkt2);
     const float sc = 1.f / sqrtf(static_cast<float>(hd));
     attn_bwd_tc5_hd128_k<<<grid, 384, Lay128::BYTES, s>>>(mkv, mq, mo, mdq, seq_start, lse, Dbuf, nh, nkv, dkv32, sc,
@@ -823,13 +820,8 @@ bool attn_bwd_tc5(cudaStream_t s, const bf16* qkv, const bf16* dctx, const float
       !tma_map_2d(&mdq, dq32, rows, qd, qd, 32, 32, true, 128, false))
     return false;
   const float sc = 1.f / sqrtf(static_cast<float>(hd));
-  // dQ: bulk tensor reduce-adds of 32-row boxes staged in shared memory (default) or,
-  // DASHCU_ATTN_BWD_DQ=red, 16-byte fp32 reductions straight from registers (measured slower)
-  const char* dqm = getenv("DASHCU_ATTN_BWD_DQ");
-  if (dqm && std::string(dqm) == "red")
-    launch_bwd_tc5<2, 0>(s, mq, mo, mdq, seq_start, lse, Dbuf, n_seq, max_len, nh, nkv, dkv32, dq32, sc);
-  else
-    launch_bwd_tc5<2, 32>(s, mq, mo, mdq, seq_start, lse, Dbuf, n_seq, max_len, nh, nkv, dkv32, dq32, sc);
+  // dQ: bulk tensor reduce-adds of 32-row boxes staged in shared memory
+  launch_bwd_tc5<2, 32>(s, mq, mo, mdq, seq_start, lse, Dbuf, n_seq, max_len, nh, nkv, dkv32, dq32, sc);
   return true;
 }
 

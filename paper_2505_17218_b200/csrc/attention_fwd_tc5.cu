@@ -365,11 +365,11 @@ void launch_fwd_tc5(cudaStream_t s, const CUtensorMap& mq, const int32_t* seq_st
 bool attn_fwd_tc5(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int n_seq, int max_len, int rows, int nh,
                   int nkv, int hd, bf16* ctx, float* lse) {
   if ((hd != 64 && hd != 128) || nh % nkv) return false;
-  const char* force = getenv("DASHCU_ATTN_FWD");
-  if (force && std::string(force) == "mma") return false;
+  const int force = knob(KNOB_ATTN_FWD);
+  if (force == 1) return false;
   // one-tile sequences (the prompt prefill) amortise the per-CTA TMEM / barrier / first-load
   // latency poorly; the mma.sync kernel (several CTAs per SM) is faster there
-  if (max_len <= 2 * kQ && !(force && std::string(force) == "tc5")) return false;
+  if (max_len <= 2 * kQ && force != 2) return false;
   const int qkvd = nh * hd + 2 * nkv * hd;
   CUtensorMap mq;
   if (!tma_map_2d(&mq, qkv, rows, qkvd, qkvd, 64, 128, false, 128, true)) return false;  // one swizzle atom per box

@@ -50,10 +50,28 @@ extern int64_t g_launches;
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-inline bool pdl_enabled() {
-  const char* s = getenv("DASHCU_PDL");
-  return s && s[0] == '1';
-}
+// Kernel-variant knobs (test coverage of forced variants and same-box A/B runs). Read from
+// the environment ONCE at library load and settable through dashcu_set_knob; the hot
+// dispatch reads this array, never getenv.
+enum Knob : int {
+  KNOB_GEMM_PAIR = 0,    // 0 tile model, 1 force 256x256 pair, 2 force 256x128 pair, 3 force 256x224, -1 never
+  KNOB_GEMM_RASTER,      // -1 model, 0 M tiles fastest, 1 N tiles fastest
+  KNOB_NO_SPLITK,        // 1: no split-K (single-CTA and pair)
+  KNOB_NO_TMA_STORE,     // 1: per-thread epilogue stores instead of bulk tensor stores
+  KNOB_GEMM_RESID_DB,    // 0: no double-buffered residual prefetch in the pair epilogue
+  KNOB_GEMM_RESID_DEEP,  // -1 model (K >= 2048), 0 / 1 force the 5-stage / 4-epilogue-warp ring
+  KNOB_ATTN_FWD,         // 0 auto, 1 mma.sync kernel, 2 tcgen05 kernel even for one-tile sequences
+  KNOB_ATTN_BWD,         // 0 auto, 1 mma.sync kernel
+  KNOB_ATTN_BWD_CHUNK,   // sequences per CTA chunk in the tcgen05 backward (0: 2-D grid order)
+  KNOB_LSE_RECOMPUTE,    // 1: the backward recomputes the LM-head LSE instead of reusing the sampler's
+  KNOB_PDL,              // 1: programmatic dependent launch
+  KNOB_DECODE_GRAPH,     // 0: no CUDA-graph replay of decode steps
+  KNOB_NUM
+};
+extern int g_knob[KNOB_NUM];
+inline int knob(Knob k) { return g_knob[k]; }
+
+inline bool pdl_enabled() { return knob(KNOB_PDL) == 1; }
 
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {

@@ -77,10 +77,6 @@ struct SampleArgs {
   int64_t ld_dz = 0;
 };
 int gemm_tc_lse(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa);
-// Persistent-grid cap for the tcgen05 GEMMs launched by this thread (0 = every SM): lets a
-// concurrent kernel on another stream keep the remaining SMs.
-int gemm_cta_cap();
-void gemm_set_cta_cap(int n);
 bool gemm_tc_dz(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa);
 int gemm_tc_lse_tiles(int N);
 
@@ -90,9 +86,6 @@ template <class T>
 void gemm_simt(cudaStream_t s, const GemmShape& g, const Epi& e);
 // tcgen05 path; returns false if the shape is not TMA-legal (strides must be 16-byte multiples).
 bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e);
-// split-K slices the tcgen05 planner uses for an EPI_ACCUM pair GEMM of this shape when
-// they all fit in one round of the grid (1 otherwise)
-int gemm_tc_accum_splits(int M, int N, int K);
 // Fused LM head + sampling partials; returns the number of N tiles (0 if not TMA-legal).
 int gemm_tc_sample(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa);
 int gemm_tc_sample_tiles(int N);

@@ -164,12 +164,10 @@ struct OutMaps {
 template <int BN, int STAGES, bool AK, bool BKM, int EPW>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
-  // BN = 224 (N = 4 x 224): the B stage keeps the 256-row footprint (K-major loads 224 rows,
-  // MN-major four 64-column atoms of which the MMA reads 224 columns)
-  static constexpr int BNS = BN == 224 ? 256 : BN;
+  static constexpr int BNS = BN;
   static constexpr int B_BYTES = BNS * BK * 2;
-  static constexpr int B_LOAD = (BKM ? BN : BNS) * BK * 2;  // bytes the B loads of a stage deliver
-  static constexpr int TMEM_COLS = BN == 224 ? 512 : 2 * BN;
+  static constexpr int B_LOAD = BN * BK * 2;  // bytes the B loads of a stage deliver
+  static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STG_OFF = STAGES * STAGE_BYTES;  // EPW x 4 KB epilogue staging
   static constexpr int BAR_OFF = STG_OFF + EPW * kStageBytes;
@@ -805,7 +803,7 @@ bool make_out_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, 
 // Epilogue outputs through bulk tensor stores when both outputs are TMA-legal
 // (the generic EPI kinds only; returns the Epi::tma bits, 0 = direct stores).
 int out_maps_for(const GemmShape& g, const Epi& e, OutMaps* om) {
-  if (getenv("DASHCU_NO_TMA_STORE")) return 0;
+  if (knob(KNOB_NO_TMA_STORE)) return 0;
   int bits = 0;
   if (e.c32) {
     if (!make_out_map(&om->f32, e.c32, g.M, g.N, e.ldc32, true)) return 0;
@@ -839,9 +837,6 @@ uint32_t* split_flag_buffer(int n) {
   return buf[dev];
 }
 
-thread_local int t_gemm_cta_cap = 0;
-int cta_cap() { return t_gemm_cta_cap; }
-
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -863,7 +858,7 @@ void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const 
     attr = true;
   }
   const int nitem = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) * (MODE == 0 ? e.splits : 1);
-  const int cap = cta_cap() > 0 ? std::min(cta_cap(), num_sms()) : num_sms();
+  const int cap = num_sms();
   const int grid = nitem < cap ? nitem : cap;  // persistent: all CTAs co-resident
   ProfScope ps(MODE == 1 ? PROF_SAMPLE : MODE >= 2 ? PROF_LM_ROWS : PROF_GEMM_TC, s,
                2.0 * g.M * g.N * static_cast<double>(g.K), 0);
@@ -956,8 +951,8 @@ struct Cfg2 {
   // BN = 224 (N = 896 = 4 x 224 without the half-empty fourth 256 tile): the B stage keeps
   // the 128-row footprint (K-major loads 112 rows; MN-major loads two 64-column swizzle
   // atoms, the MMA reads 112 of their columns), TMEM buffers sit 224 columns apart
-  static constexpr int BNS = BN == 224 || BN == 192 ? 128 : BNH;  // staged B footprint (rows / columns)
-  static constexpr int TMEM_COLS = BN == 224 || BN == 192 ? 512 : 2 * BN;  // alloc: power of two
+  static constexpr int BNS = BN == 224 ? 128 : BNH;  // staged B footprint (rows / columns)
+  static constexpr int TMEM_COLS = BN == 224 ? 512 : 2 * BN;  // alloc: power of two
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = BNS * BK * 2;
   static constexpr int B_LOAD = (BKM ? BNH : BNS) * BK * 2;  // bytes the B loads of a stage deliver
@@ -1144,7 +1139,7 @@ void launch2(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const
     attr = true;
   }
   const int ntile = ((g.M + 255) / 256) * ((g.N + BN - 1) / BN) * (e.splits > 1 ? e.splits : 1);
-  const int pcap = (cta_cap() > 0 ? std::min(cta_cap(), num_sms()) : num_sms()) / 2;
+  const int pcap = num_sms() / 2;
   const int npairs = ntile < pcap ? ntile : pcap;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * npairs);
@@ -1166,19 +1161,6 @@ void launch2(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const
              BKM ? 'k' : 'm', e.kind);
   DCU_CHECK(cudaLaunchKernelEx(&cfg, k, ma, mb, om, g, e));
   DCU_LAUNCHED();
-}
-
-// Decode-step shapes: short K (<= 1152 -> <= 18 k-blocks per tile) and at most ~1.5 waves of
-// 128 x 256 tiles, where a tile's mainloop is too short to hide its epilogue.
-bool narrow_tiles(const GemmShape& g, const Epi& e) {
-  if (g.K > 1152 || e.kind == EPI_ACCUM) return false;
-  const long tiles256 = static_cast<long>((g.M + BM - 1) / BM) * ((g.N + 255) / 256);
-  return tiles256 <= 3 * num_sms() / 2;
-}
-
-int use_pair_default() {
-  const char* s = getenv("DASHCU_GEMM_PAIR");
-  return s ? atoi(s) : 0;
 }
 
 }  // namespace
@@ -1214,21 +1196,16 @@ bool gemm_tc_pair(cudaStream_t s, const GemmShape& g, const Epi& e, int BN, int 
   }
   // residual epilogues (fp32 resid in, fp32 + bf16 out): 4 x 32 KB stages and the
   // double-buffered residual prefetch (DASHCU_GEMM_RESID_DB=0 disables)
-  const char* rdb = getenv("DASHCU_GEMM_RESID_DB");
   // Long-K residual GEMMs (K >= 2048) take 5 stages with 4 epilogue warps: their mainloop
   // needs the deeper ring more than their epilogue needs 8 warps (measured +6 % at K = 4864,
-  // -10 % at K = 896). DASHCU_GEMM_RESID_DEEP=0/1 forces either.
-  const char* rdeep = getenv("DASHCU_GEMM_RESID_DEEP");
-  const bool deep = rdeep ? rdeep[0] == '1' : g.K >= 2048;
-  const bool rdbl = (et.tma & 4) && !(rdb && rdb[0] == '0');
+  // -10 % at K = 896). KNOB_GEMM_RESID_DEEP forces either.
+  const int rdeep = knob(KNOB_GEMM_RESID_DEEP);
+  const bool deep = rdeep >= 0 ? rdeep == 1 : g.K >= 2048;
+  const bool rdbl = (et.tma & 4) && knob(KNOB_GEMM_RESID_DB) != 0;
   if (BN == 224) {  // N = 4 x 224 (e.g. d = 896) without the half-empty 256 tile
     if (rdbl && deep) dispatch_pair<224, 5, true, 4>(s, ma, mb, om, g, et);
     else if (rdbl) dispatch_pair<224, 4, true>(s, ma, mb, om, g, et);
     else dispatch_pair<224, 6>(s, ma, mb, om, g, et);
-  } else if (BN == 192) {  // N = 6 x 192 (e.g. the QKV width 1152)
-    if (rdbl && deep) dispatch_pair<192, 5, true, 4>(s, ma, mb, om, g, et);
-    else if (rdbl) dispatch_pair<192, 4, true>(s, ma, mb, om, g, et);
-    else dispatch_pair<192, 6>(s, ma, mb, om, g, et);
   } else if (BN == 256 && rdbl && deep)
     dispatch_pair<256, 5, true, 4>(s, ma, mb, om, g, et);
   else if (BN == 256 && rdbl) dispatch_pair<256, 4, true>(s, ma, mb, om, g, et);
@@ -1241,41 +1218,10 @@ bool gemm_tc_pair(cudaStream_t s, const GemmShape& g, const Epi& e, int BN, int 
 // cannot stay in L2 (an A panel is then read from HBM once and shared by the CTAs working
 // on its N tiles), M tiles fastest otherwise. DASHCU_GEMM_RASTER=0/1 forces m / n fast.
 bool raster_n_fast(const GemmShape& g) {
-  const char* r = getenv("DASHCU_GEMM_RASTER");
-  if (r) return r[0] == '1';
+  const int r = knob(KNOB_GEMM_RASTER);
+  if (r >= 0) return r == 1;
   const double a = 2.0 * g.M * g.K, b = 2.0 * g.N * g.K;
   return a > 2.0 * b && a > 48e6;
-}
-
-// K slices for an fp32-accumulate (EPI_ACCUM) CTA-pair GEMM of this shape such that every
-// slice of every tile runs in ONE round of the persistent grid (1 = no split); the caller
-// requests them through Epi::splits. The
-// decode uses it to pick the accumulate form of its long-K residual projections whose few
-// output tiles leave most SMs idle (C4 W2: M 512 x N 2048 = 20 pair tiles of 256 x 224 for
-// 74 pairs, K 11008: 3 slices, 61 -> 45 us). With more than one round the in-order slice reduces serialise the epilogues
-// (measured: C3 W2, 56 tiles x 5 slices, 77 -> 108 us).
-int gemm_tc_accum_splits(int M, int N, int K) {
-  if (getenv("DASHCU_NO_SPLITK") || getenv("DASHCU_NO_PAIR_SPLITK") || getenv("DASHCU_NO_DECODE_SPLITK")) return 1;
-  // K >= 4096 only: the accumulate form costs a bf16 copy kernel, which shorter K slices do
-  // not repay (measured: C4 Wo, K 2048, 2 slices: slower than the store form)
-  if (K < 4096) return 1;
-  const int tm2 = (M + 255) / 256, nkb = (K + BK - 1) / BK;
-  const double pairs = std::floor(num_sms() / 2.0);
-  const double rpair = std::ceil(tm2 * ((N + 255) / 256) / pairs);
-  int pbn = 256;
-  double cost = rpair;
-  const char* n224 = getenv("DASHCU_GEMM_N224");
-  if (!(n224 && n224[0] == '0')) {
-    const double c = std::ceil(tm2 * ((N + 223) / 224) / pairs) * 224 / 256.0;
-    if (c < rpair * 0.98) pbn = 224, cost = c;
-  }
-  const int tp = tm2 * ((N + pbn - 1) / pbn);
-  int split = 1;
-  for (int S = 2; S <= 8 && nkb / S >= 16 && tp * S <= pairs; ++S) {
-    const double c = 1.0 / S * (pbn / 256.0) * (1.0 + 0.03 * (S - 1));
-    if (c < cost * 0.97) cost = c, split = S;
-  }
-  return split;
 }
 
 bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
@@ -1297,28 +1243,19 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
   const double cpair = rpair / 1.12, cpair128 = rpair128 * 0.5 / 0.68;
   // 256 x 224 pair tiles: same tile count as 256 x 256 when N is a multiple of 224 but not
   // of 256 (N = 896: 4 full tiles instead of 3.5), 7/8 of the MMA work per tile
-  // Narrower pair tiles when N is not a multiple of 256: cost = rounds x BN / 256 over
-  // BN in {256, 224} (N = 896: 4 x 224 instead of 3.5 x 256). DASHCU_GEMM_N224=0 keeps 256.
-  const char* n224 = getenv("DASHCU_GEMM_N224");
   int pbn = 256;
   double pscale = 1.0;
-  if (!(n224 && n224[0] == '0')) {
-    // 192 (N = 1152 = 6 x 192) is modelled 10 % cheaper but measured 10 % slower on the
-    // training QKV shape (M 36832, K 896) and +3 % on the decode one: forced only (PAIR=4)
-    for (int bn : {224}) {
-      const double c = std::ceil(tm2 * ((g.N + bn - 1) / bn) / std::floor(sms / 2)) * bn / 256.0;
-      if (c < rpair * pscale * 0.98) pbn = bn, pscale = c / rpair;
-    }
+  {
+    const double c = std::ceil(tm2 * ((g.N + 223) / 224) / std::floor(sms / 2)) * 224 / 256.0;
+    if (c < rpair * 0.98) pbn = 224, pscale = c / rpair;
   }
   const bool use224 = pbn != 256;
-  // caller-requested K slices (gemm_tc_accum_splits: the decode's residual projections)
-  if (e.kind == EPI_ACCUM && e.c32 && e.splits > 1 && gemm_tc_pair(s, g, e, pbn, e.splits)) return true;
   // ordered split-K for accumulating pair GEMMs with few tiles (the weight gradients, e.g.
   // dW1 = 19 x 4 pair tiles for 74 pairs: 2 rounds of which one is 3 % full), same cost
   // model as the single-CTA split below
   int splitp = 1;
   double cpair_s = rpair * pscale;
-  if (e.kind == EPI_ACCUM && e.c32 && !getenv("DASHCU_NO_SPLITK") && !getenv("DASHCU_NO_PAIR_SPLITK")) {
+  if (e.kind == EPI_ACCUM && e.c32 && !knob(KNOB_NO_SPLITK)) {
     const int tp = tm2 * ((g.N + pbn - 1) / pbn), nkb_ = (g.K + BK - 1) / BK;
     for (int S = 2; S <= 8 && nkb_ / S >= 16; ++S) {
       const double c = std::ceil(tp * S / std::floor(sms / 2)) / S * (pbn / 256.0) * (1.0 + 0.03 * (S - 1));
@@ -1330,7 +1267,7 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
   // ordered fp32 reduce of the tile (~3%). Slices keep >= 16 k-blocks.
   int split128 = 1, split256 = 1;
   const int nkb = (g.K + BK - 1) / BK;
-  if (e.kind == EPI_ACCUM && e.c32 && !getenv("DASHCU_NO_SPLITK")) {
+  if (e.kind == EPI_ACCUM && e.c32 && !knob(KNOB_NO_SPLITK)) {
     auto best = [&](int tiles, double unit, double* cost) {
       int sb = 1;
       for (int S = 2; S <= 8 && nkb / S >= 16; ++S) {
@@ -1342,30 +1279,18 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
     split128 = best(tm * ((g.N + 127) / 128), 0.5 / 0.76, &c128);
     split256 = best(tm * ((g.N + 255) / 256), 1.0, &c256);
   }
-  // DASHCU_GEMM_PAIR: 1 force the 256x256 pair, 2 force the 256x128 pair, 3 / 4 force the
-  // 256x224 / 256x192 pair, 0 model, -1 never
-  const int forced = use_pair_default();
-  const char* fbn = getenv("DASHCU_GEMM_BN");
-  const char* fnarrow = getenv("DASHCU_GEMM_NARROW");
-  // opt-in (DASHCU_GEMM_NARROW=1): measured slower than the pair / 128-wide tiles on the C2
-  // decode shapes (dec_qkv 22.7 vs 14.8 us, dec_wo 21.8 vs 16.7 us)
-  const bool narrow = !fbn && forced == 0 && fnarrow && fnarrow[0] == '1' && narrow_tiles(g, e);
-  if (forced != -1 && !narrow) {
+  // KNOB_GEMM_PAIR: 1 force the 256x256 pair, 2 force the 256x128 pair, 3 force the
+  // 256x224 pair, 0 model, -1 never
+  const int forced = knob(KNOB_GEMM_PAIR);
+  if (forced != -1) {
     const double cp = cpair_s / 1.12;
-    const bool p256 = forced == 1 || forced == 3 || forced == 4 || (forced == 0 && cp < c256 && cp < c128 && cp <= cpair128);
+    const bool p256 = forced == 1 || forced == 3 || (forced == 0 && cp < c256 && cp < c128 && cp <= cpair128);
     const bool p128 = forced == 2 || (forced == 0 && !p256 && cpair128 < c256 && cpair128 < c128);
-    const int bn = forced == 3 ? 224 : forced == 4 ? 192 : (forced != 1 && use224) ? pbn : 256;
+    const int bn = forced == 3 ? 224 : (forced != 1 && use224) ? pbn : 256;
     if ((p256 && gemm_tc_pair(s, g, e, bn, bn == pbn ? splitp : 1)) || (p128 && gemm_tc_pair(s, g, e, 128)))
       return true;
   }
-  const bool wide = c256 <= c128;
-  // Optional narrow 128 x 64 tiles for short-K GEMMs with few tiles (see `narrow` above).
-  // DASHCU_GEMM_BN forces 64 / 128 / 256.
-  // 128 x 224 single-CTA tiles exist (DASHCU_GEMM_BN=224) but measured no faster on the
-  // split-K weight-gradient shapes that take this path (wgrad_w1 -4 %, wgrad_wo +3 %)
-  int BN = wide ? 256 : 128;
-  if (fbn) BN = atoi(fbn) == 64 ? 64 : atoi(fbn) == 128 ? 128 : atoi(fbn) == 224 ? 224 : 256;
-  else if (narrow) BN = 64;
+  const int BN = c256 <= c128 ? 256 : 128;
   CUtensorMap ma, mb;
   bool ok = g.a_kmajor ? make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) : make_map(&ma, g.A, g.K, g.M, g.lda, 64, BK);
   ok = ok && (g.b_kmajor ? make_map(&mb, g.B, g.N, g.K, g.ldb, BK, BN) : make_map(&mb, g.B, g.K, g.N, g.ldb, 64, BK));
@@ -1374,18 +1299,16 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
   memset(&om, 0, sizeof(om));
   Epi et = e;
   et.tma = out_maps_for(g, e, &om);
-  et.splits = 1;  // a caller's request applies to the pair path only
-  const int S = BN == 256 || BN == 224 ? split256 : BN == 128 ? split128 : 1;
+  et.splits = 1;
+  const int S = BN == 256 ? split256 : split128;
   if (S > 1 && (et.tma & 1)) {
     const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
     et.splits = S;
     et.split_flags = split_flag_buffer(tiles * 8);
     DCU_CHECK(cudaMemsetAsync(et.split_flags, 0, sizeof(uint32_t) * tiles * 8, s));
   }
-  if (BN == 256) dispatch_majors<256, 4>(s, ma, mb, om, g, et);       // 4 x 48 KB stages
-  else if (BN == 224) dispatch_majors<224, 4>(s, ma, mb, om, g, et);  // 4 x 48 KB stages (B: 256-row footprint)
-  else if (BN == 128) dispatch_majors<128, 6>(s, ma, mb, om, g, et);  // 6 x 32 KB stages
-  else dispatch_majors<64, 8>(s, ma, mb, om, g, et);                  // 8 x 24 KB stages
+  if (BN == 256) dispatch_majors<256, 4>(s, ma, mb, om, g, et);  // 4 x 48 KB stages
+  else dispatch_majors<128, 6>(s, ma, mb, om, g, et);             // 6 x 32 KB stages
   return true;
 }
 
@@ -1470,7 +1393,5 @@ bool tma_map_2d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, in
   return r == CUDA_SUCCESS;
 }
 
-int gemm_cta_cap() { return cta_cap(); }
-void gemm_set_cta_cap(int n) { t_gemm_cta_cap = n; }
 
 }  // namespace dashcu

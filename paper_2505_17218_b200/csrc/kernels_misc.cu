@@ -1,6 +1,7 @@
 // Memory-bound kernels of the DASH step: parameter init/casts, the optimizer,
 // embeddings, bias-gradient column sums, LM-head loss rows, the sampling step
 // (non-fused form), KV-cache plumbing and the advantage/filter + compaction.
+#include <cub/device/device_radix_sort.cuh>
 #include <cfloat>
 
 #include "kernels.cuh"
@@ -110,14 +111,41 @@ __global__ void embed_decode_k(const T* E, const T* P, const int32_t* tok, const
   }
 }
 
-__global__ void embed_bwd_k(const float* dx, const int32_t* tok, const int32_t* pos, int rows, int d, float* gt,
-                            float* gp) {
-  const int64_t n = static_cast<int64_t>(rows) * d;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int r = static_cast<int>(i / d), c = static_cast<int>(i % d);
-    const float v = dx[i];
-    atomicAdd(&gt[static_cast<int64_t>(tok[r]) * d + c], v);
-    atomicAdd(&gp[static_cast<int64_t>(pos[r]) * d + c], v);
+// Embedding backward (policy.cpp:335-344: dtok[tok_t] += dx_t, dpos[pos_t] += dx_t),
+// deterministic: the rows are stably sorted by id (CUB radix sort of (id, row) pairs), and
+// the block that owns the first row of an id's run sums the run in row order and adds the
+// sum to that id's gradient row. No floating-point atomics, so the result does not depend
+// on scheduling.
+__global__ void embed_seg_mark_k(const int32_t* ids, int rows, int32_t* keys, int32_t* vals) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < rows) keys[r] = ids[r], vals[r] = r;
+}
+
+__global__ void embed_seg_sum_k(const float* __restrict__ dx, const int32_t* __restrict__ skey,
+                                const int32_t* __restrict__ srow, int rows, int d, float* __restrict__ g) {
+  const int i = blockIdx.x;
+  const int key = skey[i];
+  if (i > 0 && skey[i - 1] == key) return;  // not the head of its run
+  int end = i + 1;
+  while (end < rows && skey[end] == key) ++end;
+  float* gr = g + static_cast<int64_t>(key) * d;
+  for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
+    if (c + 4 <= d && (d & 3) == 0) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int j = i; j < end; ++j) {
+        const float4 v = *reinterpret_cast<const float4*>(dx + static_cast<int64_t>(srow[j]) * d + c);
+        acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
+      }
+      float4 o = *reinterpret_cast<float4*>(gr + c);
+      o.x += acc.x, o.y += acc.y, o.z += acc.z, o.w += acc.w;
+      *reinterpret_cast<float4*>(gr + c) = o;
+    } else {
+      for (int cc = c; cc < min(d, c + 4); ++cc) {
+        float acc = 0.f;
+        for (int j = i; j < end; ++j) acc += dx[static_cast<int64_t>(srow[j]) * d + cc];
+        gr[cc] += acc;
+      }
+    }
   }
 }
 
@@ -693,11 +721,37 @@ void embed_decode(cudaStream_t s, const T* E, const T* P, const int32_t* tok, co
              rows, d, x32, xT);
   DCU_LAUNCHED();
 }
-void embed_bwd(cudaStream_t s, const float* dx, const int32_t* tok, const int32_t* pos, int rows, int d, float* gt,
-               float* gp) {
+size_t embed_bwd_tmp_bytes(int rows) {
+  size_t cub_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, static_cast<const int32_t*>(nullptr),
+                                  static_cast<int32_t*>(nullptr), static_cast<const int32_t*>(nullptr),
+                                  static_cast<int32_t*>(nullptr), rows);
+  return 4 * sizeof(int32_t) * static_cast<size_t>(rows) + (cub_bytes + 255) / 256 * 256 + 256;
+}
+
+void embed_bwd(cudaStream_t s, const float* dx, const int32_t* tok, const int32_t* pos, int rows, int d, int n_tok,
+               int n_pos, float* gt, float* gp, void* tmp) {
   if (rows <= 0) return;
-  embed_bwd_k<<<grid1d(static_cast<int64_t>(rows) * d), 256, 0, s>>>(dx, tok, pos, rows, d, gt, gp);
-  DCU_LAUNCHED();
+  int32_t* keys = static_cast<int32_t*>(tmp);
+  int32_t* vals = keys + rows;
+  int32_t* skeys = vals + rows;
+  int32_t* svals = skeys + rows;
+  void* cub_tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(svals + rows) + 255) & ~uintptr_t(255));
+  const int bits_needed[2] = {32 - __builtin_clz(static_cast<unsigned>(std::max(n_tok, 2) - 1)),
+                              32 - __builtin_clz(static_cast<unsigned>(std::max(n_pos, 2) - 1))};
+  const int32_t* ids[2] = {tok, pos};
+  float* grads[2] = {gt, gp};
+  const int bs = d >= 1024 ? 256 : 128;
+  for (int w = 0; w < 2; ++w) {
+    embed_seg_mark_k<<<cdiv(rows, 256), 256, 0, s>>>(ids[w], rows, keys, vals);
+    DCU_LAUNCHED();
+    size_t cub_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, keys, skeys, vals, svals, rows, 0, bits_needed[w], s);
+    DCU_CHECK(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, keys, skeys, vals, svals, rows, 0, bits_needed[w],
+                                              s));
+    embed_seg_sum_k<<<rows, bs, 0, s>>>(dx, skeys, svals, rows, d, grads[w]);
+    DCU_LAUNCHED();
+  }
 }
 namespace {
 // nseg <= want, and want is non-decreasing in M (so a buffer sized for M covers any M' <= M)

@@ -231,7 +231,6 @@ void shard_span(int64_t total, int world, int rank, int64_t* off, int64_t* len, 
 struct dashcu_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t stream2 = nullptr;  // second decode stream (half-batch overlap), created on demand
   ncclComm_t comm = nullptr;
   int world = 1, rank = 0;
   int refs = 0;         // live policies bound to this context
@@ -320,15 +319,6 @@ struct Engine {
   void mm(int M, int N, int K, const T* A, int64_t lda, bool ak, const T* B, int64_t ldb, bool bk, const Epi& e) {
     GemmShape s{M, N, K, A, lda, ak, B, ldb, bk};
     gemm(st, dt(), s, e);
-  }
-  static Epi accum(float* c32, int64_t ldc32, const float* bias, int splits = 1) {  // c32 += v (+ bias)
-    Epi e;
-    e.splits = splits;  // > 1: K slices requested from the tcgen05 pair GEMM
-    e.kind = EPI_ACCUM;
-    e.c32 = c32;
-    e.ldc32 = ldc32;
-    e.bias = bias;
-    return e;
   }
   static Epi store(float* c32, int64_t ldc32, T* cT, int64_t ldcT) {
     Epi e;
@@ -532,7 +522,8 @@ struct Engine {
       mm(Tn, g.d, g.qkvd, dqkv, g.qkvd, true, W(b + L.wq), g.d, false, edx);
       std::swap(dy32, dx32);  // dy for the layer below; dx32 is scratch again
     }
-    embed_bwd(st, dy32, tok, pos, Tn, g.d, G32(L.tok), G32(L.pos));
+    embed_bwd(st, dy32, tok, pos, Tn, g.d, g.V, g.ctx, G32(L.tok), G32(L.pos),
+              ws.get<uint8_t>("b_embtmp", embed_bwd_tmp_bytes(Tn)));
   }
 
   void cast_to_T(const float* in, T* out, size_t n) {
@@ -666,8 +657,7 @@ struct Engine {
     // The sampler already computed the T = 1 log-sum-exp of every completion position
     // under the same weights (on-policy: the version check above), so the backward skips
     // the LM-head LSE pass and reads it (DASHCU_LSE_RECOMPUTE=1 recomputes instead)
-    const char* rec = getenv("DASHCU_LSE_RECOMPUTE");
-    const bool reuse_lse = sizeof(T) == 2 && P.lse_valid && !(rec && rec[0] == '1');
+    const bool reuse_lse = sizeof(T) == 2 && P.lse_valid && knob(KNOB_LSE_RECOMPUTE) != 1;
     for (size_t bi = 0; bi < batches.size(); ++bi) {
       const Batch& B = batches[bi];
       const DevBatch& D = dev[bi];
@@ -830,11 +820,10 @@ struct Engine {
     };
     lm_sample(yT, 0);
 
-    // Decode steps. With enough sequences the batch runs as two halves (whole prompt groups
-    // each) on two streams, launched layer by layer alternately: one half's attention
-    // (HBM-bound) overlaps the other half's projections (tensor-bound). Sequences are
-    // independent, so the tokens are the same as with one stream. DASHCU_DECODE_HALVES=0
-    // disables it; the logits dump (tests) always runs single-stream.
+    // Decode steps: one position of every sequence per step. Every projection uses the
+    // store form (fp32 + bf16 outputs in the epilogue), whose fp32 summation order depends
+    // on (N, K) only, so a sequence's tokens do not depend on which other sequences share
+    // its batch (scheduling independence).
     float* x32 = ws.get<float>("d_x32", static_cast<size_t>(S) * g.d);
     float* h32 = ws.get<float>("d_h32", static_cast<size_t>(S) * g.d);
     T* xT = ws.get<T>("d_xT", static_cast<size_t>(S) * g.d);
@@ -843,137 +832,48 @@ struct Engine {
     T* ctx = ws.get<T>("d_ctx", static_cast<size_t>(S) * g.qd);
     T* u = ws.get<T>("d_u", static_cast<size_t>(S) * g.H);
     std::vector<uint8_t> hfin(S);
-    // opt-in (DASHCU_DECODE_HALVES=1): with full-machine persistent GEMMs the overlap did not
-    // materialise (C2: 11.8 s vs 10.7 s of sampling); DASHCU_DECODE_GEMM_SMS caps the
-    // projections' grid so the other half's attention keeps the remaining SMs
-    const char* halves_env = getenv("DASHCU_DECODE_HALVES");
-    const bool halves_on = halves_env && halves_env[0] == '1';
-    const char* gsms = getenv("DASHCU_DECODE_GEMM_SMS");
-    const int NH = (sizeof(T) == 2 && halves_on && !dump && S >= 1024 && (S / 2) % G == 0) ? 2 : 1;
-    const int R = S / NH;  // rows per half
-    // accumulate form of the residual projections (see the layer loop); DASHCU_NO_DECODE_SPLITK=1 disables
-    const int spl_wo = sizeof(T) == 2 ? gemm_tc_accum_splits(R, g.d, g.qd) : 1;
-    const int spl_w2 = sizeof(T) == 2 ? gemm_tc_accum_splits(R, g.d, g.H) : 1;
-    const bool acc_wo = spl_wo > 1, acc_w2 = spl_w2 > 1;
-    cudaStream_t main_st = st;
-    cudaStream_t streams[2] = {st, st};
-    cudaEvent_t ev_main = nullptr, ev_side = nullptr;
-    if (NH == 2) {
-      if (gsms) gemm_set_cta_cap(atoi(gsms));
-      if (!P.ctx->stream2) DCU_CHECK(cudaStreamCreateWithFlags(&P.ctx->stream2, cudaStreamNonBlocking));
-      streams[1] = P.ctx->stream2;
-      DCU_CHECK(cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming));
-      DCU_CHECK(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
-      DCU_CHECK(cudaEventRecord(ev_main, main_st));  // prefill + first token done
-      DCU_CHECK(cudaStreamWaitEvent(streams[1], ev_main, 0));
-    }
-    auto join = [&] {  // the side stream's work is ordered before what follows on the main stream
-      if (NH == 2) {
-        DCU_CHECK(cudaEventRecord(ev_side, streams[1]));
-        DCU_CHECK(cudaStreamWaitEvent(main_st, ev_side, 0));
-      }
-    };
     for (int j = 1; j < maxcap; ++j) {
-      for (int l = 0; l <= g.L; ++l) {
-        for (int hf = 0; hf < NH; ++hf) {
-          st = streams[hf];
-          const int r0 = hf * R;
-          const size_t rd = static_cast<size_t>(r0) * g.d;
-          if (l == g.L) {  // LM head + sampling of this half
-            if (NH == 1) {
-              lm_sample(xT, j);
-            } else {
-              SampleArgs sa;
-              sa.keys = d_keys + r0;
-              sa.step = j;
-              sa.inv_t = inv_t;
-              sa.bos = g.bos;
-              sa.part = part + static_cast<size_t>(r0) * nslices * 4;
-              sa.logits = logits + static_cast<size_t>(r0) * g.V;
-              sa.logits_ld = g.V;
-              GemmShape gs{R, g.V, g.d, xT + rd, g.d, true, W(L.wout), g.d, true};
-              const int nt = gemm_tc_sample(st, gs, W32(L.bout), sa);
-              if (nt <= 0) throw Error(4, "fused sampling GEMM unavailable for the half-batch decode");
-              sample_scan(st, sa.part, nt, sa.logits, g.V, R, g.V, g.bos, g.eos, inv_t, d_keys + r0, j,
-                          d_cap + r0, d_fin + r0, P.d_comp.as<int32_t>() + static_cast<size_t>(r0) * ML,
-                          P.d_logp.as<float>() + static_cast<size_t>(r0) * ML, P.d_len.as<int32_t>() + r0,
-                          d_tok + r0, ML, inv_t == 1.f, lse_out + static_cast<size_t>(r0) * ML);
-            }
-            continue;
-          }
-          if (l == 0)
-            embed_decode<T>(st, W(L.tok), W(L.pos), d_tok + r0, d_plen + r0, j, R, g.d, x32 + rd, xT + rd);
-          const int64_t b = lb(l);
-          T* qkv_h = qkv + static_cast<size_t>(r0) * g.qkvd;
-          T* ctx_h = ctx + static_cast<size_t>(r0) * g.qd;
-          T* kc_h = kc + kvc * l + static_cast<size_t>(r0) * g.nkv * cslots * g.hd;
-          T* vc_h = vc + kvc * l + static_cast<size_t>(r0) * g.nkv * cslots * g.hd;
-          const T* kp_h = kp + kvp * l + static_cast<size_t>(r0 / G) * g.nkv * pmax * g.hd;
-          const T* vp_h = vp + kvp * l + static_cast<size_t>(r0 / G) * g.nkv * pmax * g.hd;
-          mm(R, g.qkvd, g.d, xT + rd, g.d, true, W(b + L.wq), g.d, true, store(nullptr, 0, qkv_h, g.qkvd));
-          kv_append<T>(st, qkv_h, R, g.qd, g.kvd, g.nkv, g.hd, j - 1, cslots, kc_h, vc_h);
-          // algorithmic bytes: every (sequence, kv head) reads its K and V rows once
-          const double kv_bytes = (sum_m / NH + static_cast<double>(R) * j) * g.kvd * 2.0 * sizeof(T);
-          bool done = false;
-          if constexpr (sizeof(T) == 2)
-            done = attn_decode_tc(st, qkv_h, kp_h, vp_h, kc_h, vc_h, d_plen + r0, R, G, pmax, j, cslots, g.nh, g.nkv,
-                                  g.hd, ctx_h, kv_bytes);
-          if (!done)
-            attn_decode<T>(st, qkv_h, kp_h, vp_h, kc_h, vc_h, d_plen + r0, R, G, pmax, j, cslots, g.nh, g.nkv, g.hd,
-                           ctx_h, kv_bytes);
-          // residual projections h = x + Wo ctx, x' = h + W2 u + b2: the store form (fp32 + bf16
-          // outputs in the epilogue) or, where the planner splits K with every slice in one
-          // round (few output tiles over a long K: C4's W2 / Wo), the accumulate form in place
-          // on x32 (ordered split-K, bias on the first slice) followed by the bf16 copy the
-          // next GEMM reads
-          if (acc_wo) {
-            mm(R, g.d, g.qd, ctx_h, g.qd, true, W(b + L.wo), g.qd, true, accum(x32 + rd, g.d, nullptr, spl_wo));
-            if constexpr (sizeof(T) == 2)
-              cast_f32_bf16(st, x32 + rd, reinterpret_cast<bf16*>(hT + rd), static_cast<int64_t>(R) * g.d);
-          } else {
-            Epi eo = store(acc_w2 ? x32 + rd : h32 + rd, g.d, hT + rd, g.d);  // acc_w2: h in place in x32
-            eo.resid = x32 + rd;
-            eo.ldr = g.d;
-            mm(R, g.d, g.qd, ctx_h, g.qd, true, W(b + L.wo), g.qd, true, eo);
-          }
-          Epi e1 = store(nullptr, 0, u + static_cast<size_t>(r0) * g.H, g.H);
-          e1.kind = EPI_TANH;
-          e1.bias = W32(b + L.b1);
-          mm(R, g.H, g.d, hT + rd, g.d, true, W(b + L.w1), g.d, true, e1);
-          if (acc_w2) {
-            mm(R, g.d, g.H, u + static_cast<size_t>(r0) * g.H, g.H, true, W(b + L.w2), g.H, true,
-               accum(x32 + rd, g.d, W32(b + L.b2), spl_w2));
-            if constexpr (sizeof(T) == 2)
-              cast_f32_bf16(st, x32 + rd, reinterpret_cast<bf16*>(xT + rd), static_cast<int64_t>(R) * g.d);
-          } else {
-            Epi e2 = store(x32 + rd, g.d, xT + rd, g.d);
-            e2.bias = W32(b + L.b2);
-            e2.resid = (acc_wo ? x32 : h32) + rd;  // acc_wo: h in place in x32
-            e2.ldr = g.d;
-            mm(R, g.d, g.H, u + static_cast<size_t>(r0) * g.H, g.H, true, W(b + L.w2), g.H, true, e2);
-          }
-        }
+      embed_decode<T>(st, W(L.tok), W(L.pos), d_tok, d_plen, j, S, g.d, x32, xT);
+      for (int l = 0; l < g.L; ++l) {
+        const int64_t b = lb(l);
+        T* kc_l = kc + kvc * l;
+        T* vc_l = vc + kvc * l;
+        mm(S, g.qkvd, g.d, xT, g.d, true, W(b + L.wq), g.d, true, store(nullptr, 0, qkv, g.qkvd));
+        kv_append<T>(st, qkv, S, g.qd, g.kvd, g.nkv, g.hd, j - 1, cslots, kc_l, vc_l);
+        // algorithmic bytes: every (sequence, kv head) reads its K and V rows once
+        const double kv_bytes = (sum_m + static_cast<double>(S) * j) * g.kvd * 2.0 * sizeof(T);
+        bool done = false;
+        if constexpr (sizeof(T) == 2)
+          done = attn_decode_tc(st, qkv, kp + kvp * l, vp + kvp * l, kc_l, vc_l, d_plen, S, G, pmax, j, cslots, g.nh,
+                                g.nkv, g.hd, ctx, kv_bytes);
+        if (!done)
+          attn_decode<T>(st, qkv, kp + kvp * l, vp + kvp * l, kc_l, vc_l, d_plen, S, G, pmax, j, cslots, g.nh, g.nkv,
+                         g.hd, ctx, kv_bytes);
+        // h = x + Wo ctx ; u = tanh(W1 h + b1) ; x' = h + W2 u + b2
+        Epi eo = store(h32, g.d, hT, g.d);
+        eo.resid = x32;
+        eo.ldr = g.d;
+        mm(S, g.d, g.qd, ctx, g.qd, true, W(b + L.wo), g.qd, true, eo);
+        Epi e1 = store(nullptr, 0, u, g.H);
+        e1.kind = EPI_TANH;
+        e1.bias = W32(b + L.b1);
+        mm(S, g.H, g.d, hT, g.d, true, W(b + L.w1), g.d, true, e1);
+        Epi e2 = store(x32, g.d, xT, g.d);
+        e2.bias = W32(b + L.b2);
+        e2.resid = h32;
+        e2.ldr = g.d;
+        mm(S, g.d, g.H, u, g.H, true, W(b + L.w2), g.H, true, e2);
       }
-      st = main_st;
+      lm_sample(xT, j);
       if ((j & 31) == 0 && g.eos >= 0) {  // retire the round early once every sequence hit EOS
-        join();
         d2h(st, hfin.data(), d_fin, S);
         DCU_CHECK(cudaStreamSynchronize(st));
         bool all = true;
         for (int s = 0; s < S && all; ++s) all = hfin[s] || j + 1 >= cap[s];
         if (all) break;
-        if (NH == 2) {
-          DCU_CHECK(cudaEventRecord(ev_main, main_st));
-          DCU_CHECK(cudaStreamWaitEvent(streams[1], ev_main, 0));
-        }
       }
     }
-    st = main_st;
-    join();
-    gemm_set_cta_cap(0);
     P.lse_valid = lse_all;
-    if (ev_main) cudaEventDestroy(ev_main);
-    if (ev_side) cudaEventDestroy(ev_side);
   }
 };
 
@@ -1084,7 +984,6 @@ static void ctx_free(dashcu_ctx* c) {
   if (c->comm && NcclApi::get().ok) NcclApi::get().CommDestroy(c->comm);
   c->ws.bufs.clear();
   if (c->stream) cudaStreamDestroy(c->stream);
-  if (c->stream2) cudaStreamDestroy(c->stream2);
   delete c;
 }
 

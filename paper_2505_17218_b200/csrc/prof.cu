@@ -17,6 +17,48 @@ unsigned g_prof_mask = 0;
 int g_prof_period = 1;
 int64_t g_prof_seen[PROF_NUM] = {};
 
+// ------------------------------------------------------------------- knobs
+namespace {
+struct KnobDef {
+  const char* name;
+  int def;
+};
+// env name = "DASHCU_" + name
+const KnobDef kKnobs[KNOB_NUM] = {
+    {"GEMM_PAIR", 0},       {"GEMM_RASTER", -1},    {"NO_SPLITK", 0},  {"NO_TMA_STORE", 0},
+    {"GEMM_RESID_DB", 1},   {"GEMM_RESID_DEEP", -1}, {"ATTN_FWD", 0},  {"ATTN_BWD", 0},
+    {"ATTN_BWD_CHUNK", 4},  {"LSE_RECOMPUTE", 0},   {"PDL", 0},        {"DECODE_GRAPH", 1},
+};
+int knob_index(const char* name) {
+  if (!name) return -1;
+  if (!strncmp(name, "DASHCU_", 7)) name += 7;
+  for (int i = 0; i < KNOB_NUM; ++i)
+    if (!strcmp(name, kKnobs[i].name)) return i;
+  return -1;
+}
+// string values of the old environment knobs ("mma", "tc5")
+int knob_value(int i, const char* v) {
+  if (i == KNOB_ATTN_FWD || i == KNOB_ATTN_BWD) {
+    if (!strcmp(v, "mma")) return 1;
+    if (!strcmp(v, "tc5")) return 2;
+  }
+  return atoi(v);
+}
+}  // namespace
+
+int g_knob[KNOB_NUM] = {};
+namespace {
+struct KnobInit {
+  KnobInit() {
+    for (int i = 0; i < KNOB_NUM; ++i) {
+      g_knob[i] = kKnobs[i].def;
+      const std::string env = std::string("DASHCU_") + kKnobs[i].name;
+      if (const char* v = getenv(env.c_str())) g_knob[i] = knob_value(i, v);
+    }
+  }
+} g_knob_init;
+}  // namespace
+
 namespace {
 
 struct Pending {
@@ -100,6 +142,18 @@ void prof_end(int cls, cudaStream_t s, cudaEvent_t ev0, double flops, double byt
 }  // namespace dashcu
 
 extern "C" {
+
+// Kernel-variant knobs (tests / A-B tools): name with or without the DASHCU_ prefix.
+// value INT32_MIN restores the default. Returns the previous value, or INT32_MIN for an
+// unknown name.
+DASHCU_API int dashcu_set_knob(const char* name, int value) {
+  using namespace dashcu;
+  const int i = knob_index(name);
+  if (i < 0) return INT32_MIN;
+  const int old = g_knob[i];
+  g_knob[i] = value == INT32_MIN ? kKnobs[i].def : value;
+  return old;
+}
 
 DASHCU_API int dashcu_profile_sampling(int period) {
   std::lock_guard<std::mutex> lk(dashcu::prof().mu);

@@ -22,3 +22,17 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "ref" in it.keywords and not ref_available():
             it.add_marker(skip_ref)
+
+
+@pytest.fixture
+def knob():
+    """Set a libdashcu kernel-variant knob for one test (dashcu_set_knob); restored after."""
+    import paper_2505_17218_b200 as D
+    touched = []
+
+    def set_(name, value):
+        touched.append(name)
+        D.set_knob(name, value)
+    yield set_
+    for name in touched:
+        D.set_knob(name, None)

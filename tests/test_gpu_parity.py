@@ -38,8 +38,7 @@ LONGGQA = dict(vocab_size=64, embed_dim=256, context_len=320, ffn_hidden=128, n_
 # head_dim 128 (the 1.5B / 3B geometry) over several 128-key tiles
 LONGGQA128 = dict(vocab_size=64, embed_dim=256, context_len=320, ffn_hidden=128, n_layers=1, bos_id=0, eos_id=1,
                   n_heads=4, n_kv_heads=2, head_dim=128)
-# ffn_hidden 4096: the decode's W2 GEMM (K = 4096, one output tile) takes the ordered
-# split-K accumulate form (x32 += W2 u + b2 in place, then the bf16 copy)
+# ffn_hidden 4096: the decode's W2 GEMM has K = 4096 over one output tile per row block
 WIDEFFN = dict(vocab_size=64, embed_dim=128, context_len=48, ffn_hidden=4096, n_layers=2, bos_id=0, eos_id=1,
                n_heads=2, n_kv_heads=1, head_dim=64)
 TOL = {D.F32: 1e-3, D.BF16: 2e-2}
@@ -207,24 +206,23 @@ def test_scheduling_independence(ctx):
     pol.close()
 
 
-def test_two_stream_half_batch_decode(ctx, monkeypatch):
-    """>= 1024 sequences decode as two half batches on two streams; every sequence's tokens
-    and log-probs equal the single-stream run bit-for-bit (1-CTA GEMM tiles in both, whose
-    per-element accumulation order does not depend on the number of rows)."""
-    monkeypatch.setenv("DASHCU_GEMM_PAIR", "-1")
-    monkeypatch.setenv("DASHCU_DECODE_HALVES", "1")
-    monkeypatch.setenv("DASHCU_DECODE_GEMM_SMS", "100")
-    arch = QWENLIKE
+@pytest.mark.parametrize("arch", [WIDEFFN, QWENLIKE], ids=["wideffn", "qwenlike"])
+def test_scheduling_independence_bf16(ctx, arch):
+    """bf16 production path: one preemptive call over 160 prompts x 8 equals two shards
+    (prompt_index_base) and a 2-prompt interleaved call bit-for-bit: the decode GEMMs'
+    per-element fp32 summation order depends on (N, K) only, not on the batch rows."""
     pol = D.Policy(ctx, arch, D.BF16)
     pol.upload(params32(arch, 0.3, 21))
     rng = np.random.default_rng(21)
     prompts = [[0] + list(rng.integers(2, arch["vocab_size"], size=int(rng.integers(3, 9)))) for _ in range(160)]
-    two = pol.sample(prompts, 8, 20, round_seed=5, temperature=0.7)
-    monkeypatch.setenv("DASHCU_DECODE_HALVES", "0")
-    one = pol.sample(prompts, 8, 20, round_seed=5, temperature=0.7)
-    assert np.array_equal(two.completions, one.completions)
-    assert np.array_equal(two.lengths, one.lengths)
-    assert np.array_equal(two.logp, one.logp)
+    full = pol.sample(prompts, 8, 20, round_seed=5, temperature=0.7)
+    a = pol.sample(prompts[:37], 8, 20, round_seed=5, temperature=0.7, prompt_index_base=0)
+    b = pol.sample(prompts[37:], 8, 20, round_seed=5, temperature=0.7, prompt_index_base=37)
+    c = pol.sample(prompts[50:52], 8, 20, round_seed=5, temperature=0.7, prompt_index_base=50)
+    assert np.array_equal(full.completions, np.concatenate([a.completions, b.completions]))
+    assert np.array_equal(full.lengths, np.concatenate([a.lengths, b.lengths]))
+    assert np.array_equal(full.logp, np.concatenate([a.logp, b.logp]))
+    assert np.array_equal(full.completions[400:416], c.completions)
     pol.close()
 
 
@@ -289,20 +287,19 @@ def test_pg_gradient_parity(ctx, arch, dtype):
     pol.close()
 
 
-@pytest.mark.parametrize("kernel", ["tc5", "mma", "tc5:box:0", "tc5:box:3", "tc5:red:2"])
-def test_pg_gradient_parity_long_sequences(ctx, monkeypatch, kernel):
+@pytest.mark.parametrize("kernel", ["tc5", "mma", "tc5:0", "tc5:3"])
+def test_pg_gradient_parity_long_sequences(ctx, knob, kernel):
     """Ragged sequences up to 300 tokens: several key and query tiles, the causal
     diagonal tiles and ragged tile ends, through the tcgen05 and the mma.sync attention
-    kernels (forward and backward); tc5:<dQ mode>:<chunk> are the backward's pipeline /
-    dQ-reduce variants and its chunked CTA order."""
+    kernels (forward and backward); tc5:<chunk> is the backward's chunked CTA order
+    (0: 2-D grid order)."""
     if kernel == "mma":
-        monkeypatch.setenv("DASHCU_ATTN_BWD", "mma")
+        knob("ATTN_BWD", "mma")
     if kernel.startswith("tc5:"):
-        _, dq, chunk = kernel.split(":")
-        monkeypatch.setenv("DASHCU_ATTN_BWD_DQ", dq)
-        monkeypatch.setenv("DASHCU_ATTN_BWD_CHUNK", chunk)
+        _, chunk = kernel.split(":")
+        knob("ATTN_BWD_CHUNK", chunk)
         kernel = "tc5"
-    monkeypatch.setenv("DASHCU_ATTN_FWD", kernel)  # tc5 also below its 2-tile size threshold
+    knob("ATTN_FWD", kernel)  # tc5 also below its 2-tile size threshold
     arch = LONGGQA
     pol = D.Policy(ctx, arch, D.BF16)
     p = params32(arch, 0.3, 10)
@@ -326,13 +323,13 @@ def test_pg_gradient_parity_long_sequences(ctx, monkeypatch, kernel):
 
 @pytest.mark.parametrize("fwd,bwd,ctxlen", [("tc5", "tc5", 320), ("mma", "mma", 320), ("tc5", "mma", 320),
                                             ("tc5", "tc5", 600)])
-def test_pg_gradient_parity_long_sequences_hd128(ctx, monkeypatch, fwd, bwd, ctxlen):
+def test_pg_gradient_parity_long_sequences_hd128(ctx, knob, fwd, bwd, ctxlen):
     """head_dim 128 (two swizzle atoms per tile) over ragged sequences up to 300 / 580
     tokens: the tcgen05 forward / backward (64-query tiles, transposed dQ; at 600 the key
     tiles with >= 6 query tiles split their heads over two CTAs) against the oracle, and
     the mma.sync kernels."""
-    monkeypatch.setenv("DASHCU_ATTN_FWD", fwd)
-    monkeypatch.setenv("DASHCU_ATTN_BWD", bwd)
+    knob("ATTN_FWD", fwd)
+    knob("ATTN_BWD", bwd)
     arch = dict(LONGGQA128, context_len=ctxlen)
     pol = D.Policy(ctx, arch, D.BF16)
     p = params32(arch, 0.3, 10)
@@ -471,7 +468,7 @@ def test_dash_step_c1_matches_oracle(ctx, dtype):
 
 @pytest.mark.parametrize("arch", [QWENLIKE, VBIG, LONGGQA], ids=["qwenlike", "vbig", "longgqa"])
 @pytest.mark.parametrize("temperature", [1.0, 0.7])
-def test_backward_reuses_sampler_lse(ctx, monkeypatch, arch, temperature):
+def test_backward_reuses_sampler_lse(ctx, knob, arch, temperature):
     """The bf16 backward of a sampled rollout takes each position's T = 1 log-sum-exp
     from the sampling epilogue instead of an LM-head LSE pass (same weights: on-policy).
     Gradient vs the oracle within the bf16 tolerance, and vs the recomputing path."""
@@ -487,7 +484,7 @@ def test_backward_reuses_sampler_lse(ctx, monkeypatch, arch, temperature):
     pol.grad_zero()
     pol.accumulate_weighted(w, micro_batch=8)
     reuse = pol.grad()
-    monkeypatch.setenv("DASHCU_LSE_RECOMPUTE", "1")
+    knob("LSE_RECOMPUTE", "1")
     pol.grad_zero()
     pol.accumulate_weighted(w, micro_batch=8)
     recompute = pol.grad()
@@ -541,14 +538,10 @@ def test_long_sequences_multi_tile(ctx, dtype):
     pol.close()
 
 
-@pytest.mark.parametrize("splitk", ["1", "0"])
-def test_decode_split_k_residual_projection(ctx, monkeypatch, splitk):
-    """Decode with a long-K W2 (ffn_hidden 4096): the split-K accumulate form of the
-    residual projection (default) and the store form (DASHCU_NO_DECODE_SPLITK=1) both
-    replay their tokens bit-exactly from the logits dump, and the dumped logits match the
-    oracle's forward."""
-    if splitk == "0":
-        monkeypatch.setenv("DASHCU_NO_DECODE_SPLITK", "1")
+def test_decode_wide_ffn(ctx):
+    """Decode with a long-K W2 (ffn_hidden 4096, one output tile per row block): tokens
+    replay bit-exactly from the logits dump, and the dumped logits match the oracle's
+    forward."""
     arch = WIDEFFN
     pol = D.Policy(ctx, arch, D.BF16)
     p = params32(arch, 0.5, 21)
