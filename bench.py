@@ -129,6 +129,8 @@ def dist_setup():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # NCCL init lines: nranks, NVLink / NVLS paths
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch
         import torch.distributed as dist
         backend = "nccl" if torch.cuda.is_available() else "gloo"
@@ -136,6 +138,22 @@ def dist_setup():
             torch.cuda.set_device(local)
         dist.init_process_group(backend)
     return world, rank, local
+
+
+def self_launch(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: re-exec as N ranks (one per GPU) under
+    torch.distributed.run on 127.0.0.1, exactly as the driver launches it."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # NCCL's init lines (nranks, NVLS / NVLink paths)
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
 
 
 def allreduce(vals, op):
@@ -381,7 +399,11 @@ def main():
         cfg["max_len"] = args.max_len
     if args.tau is not None:
         cfg["tau"] = None if args.tau == "off" else float(args.tau)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus))
     world, rank, local = dist_setup()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
     if args.impl == "reference":
         run_reference(args, cfg, world, rank)
     else:

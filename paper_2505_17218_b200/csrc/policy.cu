@@ -21,6 +21,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/dashcu.h"
@@ -90,6 +91,13 @@ struct NcclApi {
   decltype(&ncclAllGather) AllGather = nullptr;
   decltype(&ncclCommDestroy) CommDestroy = nullptr;
   decltype(&ncclGetErrorString) GetErrorString = nullptr;
+  decltype(&ncclCommGetAsyncError) CommGetAsyncError = nullptr;
+  decltype(&ncclCommAbort) CommAbort = nullptr;
+  decltype(&ncclCommCount) CommCount = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
   static NcclApi& get() {
     static NcclApi a = [] {
       NcclApi r;
@@ -103,6 +111,13 @@ struct NcclApi {
       r.AllGather = (decltype(r.AllGather))dlsym(h, "ncclAllGather");
       r.CommDestroy = (decltype(r.CommDestroy))dlsym(h, "ncclCommDestroy");
       r.GetErrorString = (decltype(r.GetErrorString))dlsym(h, "ncclGetErrorString");
+      r.CommGetAsyncError = (decltype(r.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+      r.CommAbort = (decltype(r.CommAbort))dlsym(h, "ncclCommAbort");
+      r.CommCount = (decltype(r.CommCount))dlsym(h, "ncclCommCount");
+      r.GroupStart = (decltype(r.GroupStart))dlsym(h, "ncclGroupStart");
+      r.GroupEnd = (decltype(r.GroupEnd))dlsym(h, "ncclGroupEnd");
+      r.Send = (decltype(r.Send))dlsym(h, "ncclSend");
+      r.Recv = (decltype(r.Recv))dlsym(h, "ncclRecv");
       r.ok = r.GetUniqueId && r.CommInitRank && r.AllReduce && r.CommDestroy;
       return r;
     }();
@@ -117,6 +132,29 @@ struct NcclApi {
       throw Error(4, std::string("NCCL error ") +                                              \
                          (NcclApi::get().GetErrorString ? NcclApi::get().GetErrorString(r__) : "?")); \
   } while (0)
+
+// Wait for the stream while polling the communicator's asynchronous error state (a peer that
+// died or a network fault otherwise leaves the collective spinning forever): on an error
+// the communicator is aborted and the call fails with status 4.
+void nccl_wait(ncclComm_t comm, cudaStream_t s) {
+  NcclApi& n = NcclApi::get();
+  if (!comm || !n.CommGetAsyncError) {
+    DCU_CHECK(cudaStreamSynchronize(s));
+    return;
+  }
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) DCU_CHECK(q);
+    ncclResult_t ae = ncclSuccess;
+    NCCL_CHECK(n.CommGetAsyncError(comm, &ae));
+    if (ae != ncclSuccess && ae != ncclInProgress) {
+      if (n.CommAbort) n.CommAbort(comm);
+      throw Error(4, std::string("NCCL asynchronous error: ") + (n.GetErrorString ? n.GetErrorString(ae) : "?"));
+    }
+    std::this_thread::yield();
+  }
+}
 
 // ------------------------------------------------------------- host rng.hpp
 
@@ -1026,6 +1064,12 @@ int dashcu_ctx_init_comm(dashcu_ctx* c, int world, int rank, const uint8_t id[12
   std::memcpy(&uid, id, 128);
   DCU_CHECK(cudaSetDevice(c->device));
   NCCL_CHECK(n.CommInitRank(&c->comm, world, uid, rank));
+  if (n.CommCount) {
+    int cnt = 0;
+    NCCL_CHECK(n.CommCount(c->comm, &cnt));
+    if (cnt != world) throw Error(4, "NCCL communicator has " + std::to_string(cnt) + " ranks, expected " +
+                                         std::to_string(world));
+  }
   API_END
 }
 
@@ -1416,6 +1460,7 @@ int dashcu_allreduce_grads(dashcu_policy* p) {
     if (!c->comm) throw Error(4, "communicator not initialised (dashcu_ctx_init_comm)");
     NCCL_CHECK(NcclApi::get().AllReduce(p->g32.p, p->g32.p, static_cast<size_t>(p->lay.total), ncclFloat32, ncclSum,
                                         c->comm, c->stream));
+    nccl_wait(c->comm, c->stream);
   }
   p->st.allreduce_ms = tm.stop_ms();
   API_END
@@ -1475,7 +1520,10 @@ int dashcu_sharded_step(dashcu_policy* p, const dashcu_opt* o) {
   float* g = p->g32.as<float>();
   float* w = p->w32.as<float>();
   if (c->world > 1)  // in place: rank r's slice of the sum lands at g + r * slice
+  {
     NCCL_CHECK(nc.ReduceScatter(g, g + off, static_cast<size_t>(slice), ncclFloat32, ncclSum, c->comm, c->stream));
+    nccl_wait(c->comm, c->stream);
+  }
   const double rs_ms = tc.stop_ms();
   Timer to(c->stream);
   float c1, c2;
@@ -1487,7 +1535,10 @@ int dashcu_sharded_step(dashcu_policy* p, const dashcu_opt* o) {
   const double up_ms = to.stop_ms();
   Timer tg(c->stream);
   if (c->world > 1)
+  {
     NCCL_CHECK(nc.AllGather(w + off, w, static_cast<size_t>(slice), ncclFloat32, c->comm, c->stream));
+    nccl_wait(c->comm, c->stream);
+  }
   const double ag_ms = tg.stop_ms();
   Timer tw(c->stream);
   refresh_working_copy(p);
