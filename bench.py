@@ -67,6 +67,31 @@ PROF_PERIOD = 17
 REF_SAMPLE = dict(prompts=1, G=8, prompt_len=4, max_len=4)
 
 
+def prompts_of(cfg, arch, m_lo, m_hi, reference=False):
+    """[m_hi - m_lo, prompt_len] prompts of global prompt ids m_lo..m_hi-1: the ADD task's
+    generate_instance (difficulty 2, byte vocabulary; tasks.cpp:105-112) for configs[0],
+    uniform random ids after BOS for the Qwen-shaped configs."""
+    if cfg["size"] is None:
+        seeds = [int(W.derive_seed(1, "prompt", m, 0)) for m in range(m_lo, m_hi)]
+        if reference:   # the reference arm: the reference's own generate_instance (oracle/_ref)
+            import ctypes as C
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            import oracle_ffi as O
+            out = np.zeros((m_hi - m_lo, 16), dtype=np.int32)
+            for i, sd in enumerate(seeds):
+                m, ans = C.c_int32(0), C.create_string_buffer(16)
+                row = np.zeros(16, dtype=np.int32)
+                if O.ref().ref_add_instance(2, C.c_uint64(sd), O.ptr(row, O.i32p), C.byref(m), ans, 16):
+                    raise RuntimeError("reference generate_instance failed")
+                out[i] = row
+            return out[:, :cfg["prompt_len"]]
+        import paper_2505_17218_b200 as D
+        toks, off, _ = D.task_instances(D.TASK_ADD, 2, seeds, D.VOCAB_BYTE)
+        assert np.all(np.diff(off) == cfg["prompt_len"])
+        return toks.reshape(m_hi - m_lo, cfg["prompt_len"])
+    return W.synthetic_prompts(1, m_lo, m_hi, cfg["prompt_len"], arch["vocab_size"], arch["bos_id"], arch["eos_id"])
+
+
 def arch_of(cfg):
     if cfg["size"] is None:
         return dict(C1_ARCH)
@@ -204,8 +229,7 @@ def ref_step_runner(cfg, threads):
     m = np.zeros(n)
     v = np.zeros(n)
     t = C.c_int64(0)
-    P = W.synthetic_prompts(1, 0, rs["prompts"], rs["prompt_len"], arch["vocab_size"], arch["bos_id"],
-                            arch["eos_id"])
+    P = prompts_of(dict(cfg, prompt_len=rs["prompt_len"]), arch, 0, rs["prompts"], reference=True)
     toks = np.ascontiguousarray(P.reshape(-1))
     off = (np.arange(rs["prompts"] + 1) * rs["prompt_len"]).astype(np.int64)
     R = O.ref()
@@ -264,7 +288,7 @@ def run_ours(args, cfg, world, rank, local):
     pol = D.Policy(ctx, arch, D.BF16)
     pol.init_normal(cfg.get("init", 0.02), 1)
     base = rank * M
-    P = W.synthetic_prompts(1, base, base + M, cfg["prompt_len"], arch["vocab_size"], 0, 1)
+    P = prompts_of(cfg, arch, base, base + M)
     ptok = pinned(P.size, np.int32)
     ptok[:] = P.reshape(-1)
     poff = pinned(M + 1, np.int64)

@@ -226,6 +226,37 @@ DASHCU_API int dashcu_profile_read(dashcu_kprof* out, int max, int reset);
  * Returns the full length; copies at most cap-1 bytes + NUL. Reset with profile_read. */
 DASHCU_API int64_t dashcu_profile_keys(char* buf, int64_t cap);
 
+/* ---- synthetic verifiable tasks (host only; tasks.cpp:105-175) ----
+ * generate_instance / reward of the reference's task module: the prompt feeder and the
+ * trajectory reward of a DASH round. kind: DASHCU_TASK_*; vocab:
+ * DASHCU_VOCAB_TASK (the task's own vocabulary, build_vocab tasks.cpp:23-53) or
+ * DASHCU_VOCAB_BYTE (BASELINE configs[0]: 0 "<s>", 1 "</s>", ids 2..255 the bytes).
+ * Errors: InputError for difficulty < 1 (TaskSpec::make), CapacityError for a short buffer. */
+#define DASHCU_TASK_ADD 0
+#define DASHCU_TASK_MOD 1
+#define DASHCU_TASK_REVERSE 2
+#define DASHCU_TASK_PARITY 3
+#define DASHCU_TASK_MICRO 4
+#define DASHCU_VOCAB_TASK 0
+#define DASHCU_VOCAB_BYTE 1
+DASHCU_API int dashcu_task_vocab_size(int32_t kind, int32_t vocab, int32_t* size);
+/* n instances, seeds[i] = the instance seed (generate_instance(task, seed)); prompts
+ * concatenated (BOS first) into prompt_tokens[prompt_cap] with prompt_offsets[n+1]
+ * (prompt_tokens may be null to size the buffer); answers (optional) NUL-terminated,
+ * answer_stride bytes apart. */
+DASHCU_API int dashcu_task_instances(int32_t kind, int32_t difficulty, int32_t vocab, const uint64_t* seeds,
+                                     int32_t n, int32_t* prompt_tokens, int64_t prompt_cap, int64_t* prompt_offsets,
+                                     char* answers, int32_t answer_stride);
+/* reward (tasks.cpp:155-175) of sequence s = m * group_size + g, whose completion is
+ * completions[s * stride .. + lengths[s]), against instance seeds[m]. */
+DASHCU_API int dashcu_task_rewards(int32_t kind, int32_t difficulty, int32_t vocab, const uint64_t* seeds,
+                                   int32_t n_prompts, int32_t group_size, const int32_t* completions, int32_t stride,
+                                   const int32_t* lengths, double* rewards);
+/* Rewards of the policy's current rollout ("rewards on arrival") from the
+ * task: same as dashcu_task_rewards + dashcu_rollout_set_rewards. */
+DASHCU_API int dashcu_rollout_task_rewards(dashcu_policy* pol, int32_t kind, int32_t difficulty, int32_t vocab,
+                                           const uint64_t* seeds);
+
 /* ---- kernel-variant knobs (tests and same-box A/B tools) ----
  * Read once from DASHCU_<NAME> environment variables at library load; this call changes
  * one for the calling process (INT32_MIN restores the default). Names: GEMM_PAIR,

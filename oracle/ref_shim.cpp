@@ -88,6 +88,18 @@ dash::TaskSpec byte_add_task(int difficulty) {
   return dash::TaskSpec{dash::TaskKind::Add, difficulty, std::move(v)};
 }
 
+// TaskSpec of kind k (0 add, 1 mod, 2 reverse, 3 parity, 4 micro) over the task's own
+// vocabulary (TaskSpec::make) or, vocab == 1, the byte vocabulary above.
+dash::TaskSpec task_of(int kind, int difficulty, int vocab) {
+  static const dash::TaskKind kinds[5] = {dash::TaskKind::Add, dash::TaskKind::Mod, dash::TaskKind::Reverse,
+                                          dash::TaskKind::Parity, dash::TaskKind::Micro};
+  if (kind < 0 || kind > 4) throw dash::InputError("unknown task kind");
+  if (vocab == 0) return dash::TaskSpec::make(kinds[kind], difficulty);
+  dash::TaskSpec t = byte_add_task(difficulty);
+  t.kind = kinds[kind];
+  return t;
+}
+
 }  // namespace
 
 REF_API const char* ref_last_error() { return g_err.c_str(); }
@@ -253,5 +265,43 @@ REF_API int ref_add_reward(int difficulty, uint64_t seed, const int32_t* complet
     t.prompt = inst.prompt;
     t.completion = ivec(completion, len);
     *r = dash::reward(task, inst, t).r;
+  });
+}
+
+// generate_instance (tasks.cpp:105-153) for any task kind and either vocabulary.
+REF_API int ref_task_instance(int kind, int difficulty, int vocab, uint64_t seed, int32_t* prompt, int32_t* m,
+                              char* answer, int answer_cap) {
+  return guarded([&] {
+    auto task = task_of(kind, difficulty, vocab);
+    auto inst = dash::generate_instance(task, seed);
+    *m = static_cast<int32_t>(inst.prompt.size());
+    for (std::size_t i = 0; i < inst.prompt.size(); ++i) prompt[i] = inst.prompt[i];
+    std::snprintf(answer, answer_cap, "%s", inst.answer.c_str());
+  });
+}
+
+// reward (tasks.cpp:155-175) for any task kind and either vocabulary.
+REF_API int ref_task_reward(int kind, int difficulty, int vocab, uint64_t seed, const int32_t* completion, int len,
+                            double* r) {
+  return guarded([&] {
+    auto task = task_of(kind, difficulty, vocab);
+    auto inst = dash::generate_instance(task, seed);
+    dash::Trajectory t;
+    t.prompt = inst.prompt;
+    t.completion = ivec(completion, len);
+    *r = dash::reward(task, inst, t).r;
+  });
+}
+
+// expert_trajectory (tasks.cpp:177-...) completion: always rewarded 1.
+REF_API int ref_task_expert(int kind, int difficulty, int vocab, uint64_t seed, int stepwise, int32_t* completion,
+                            int cap, int32_t* len) {
+  return guarded([&] {
+    auto task = task_of(kind, difficulty, vocab);
+    auto inst = dash::generate_instance(task, seed);
+    auto tr = dash::expert_trajectory(task, inst, stepwise ? dash::Verbosity::Stepwise : dash::Verbosity::Terse);
+    if (static_cast<int>(tr.completion.size()) > cap) throw dash::CapacityError("completion buffer too small");
+    *len = static_cast<int32_t>(tr.completion.size());
+    for (std::size_t i = 0; i < tr.completion.size(); ++i) completion[i] = tr.completion[i];
   });
 }

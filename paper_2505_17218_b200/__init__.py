@@ -24,6 +24,8 @@ F32, BF16 = 0, 1
 ADV_SINGLE_PATH, ADV_GROUP, ADV_LEAVE_ONE_OUT = 0, 1, 2
 FILTER_OFF = float("-inf")  # DASHCU_FILTER_OFF: no filter_by_threshold, every sequence kept
 OPT_SGD, OPT_ADAM = 0, 1
+TASK_ADD, TASK_MOD, TASK_REVERSE, TASK_PARITY, TASK_MICRO = 0, 1, 2, 3, 4
+VOCAB_TASK, VOCAB_BYTE = 0, 1
 
 
 def shard_span(total: int, world: int, rank: int):
@@ -139,6 +141,12 @@ def lib():
             "dashcu_sharded_step": [vp, C.POINTER(Opt)],
             "dashcu_shard_span": [C.c_int64, C.c_int32, C.c_int32, i64p, i64p],
             "dashcu_get_stats": [vp, C.POINTER(Stats)],
+            "dashcu_task_vocab_size": [C.c_int32, C.c_int32, i32p],
+            "dashcu_task_instances": [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_uint64), C.c_int32, i32p,
+                                      C.c_int64, i64p, C.c_char_p, C.c_int32],
+            "dashcu_task_rewards": [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_uint64), C.c_int32, C.c_int32,
+                                    i32p, C.c_int32, i32p, f64p],
+            "dashcu_rollout_task_rewards": [vp, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_uint64)],
             "dashcu_selftest_gemm": [vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint16), C.c_int64, C.c_int,
                                      C.POINTER(C.c_uint16), C.c_int64, C.c_int, f32p, C.c_int, C.c_int, f32p],
         }
@@ -231,6 +239,46 @@ def profile_read(reset=True) -> dict:
         raise DeviceError("profile read failed")
     return {arr[i].name.decode(): dict(launches=arr[i].launches, ms=arr[i].ms, flops=arr[i].flops,
                                        bytes=arr[i].bytes) for i in range(n)}
+
+
+def _seeds(seeds):
+    return np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+
+
+def task_vocab_size(kind: int, vocab: int = VOCAB_TASK) -> int:
+    n = C.c_int32(0)
+    _check(lib().dashcu_task_vocab_size(kind, vocab, C.byref(n)))
+    return int(n.value)
+
+
+def task_instances(kind: int, difficulty: int, seeds, vocab: int = VOCAB_TASK):
+    """generate_instance (tasks.cpp:105-153) per seed: (prompt_tokens, prompt_offsets, answers)."""
+    sd = _seeds(seeds)
+    n = sd.shape[0]
+    off = np.zeros(n + 1, dtype=np.int64)
+    u64 = C.POINTER(C.c_uint64)
+    _check(lib().dashcu_task_instances(kind, difficulty, vocab, sd.ctypes.data_as(u64), n, None, 0, _p(off, i64p),
+                                       None, 0))
+    toks = np.zeros(max(int(off[-1]), 1), dtype=np.int32)
+    stride = 64
+    ans = C.create_string_buffer(max(n, 1) * stride)
+    _check(lib().dashcu_task_instances(kind, difficulty, vocab, sd.ctypes.data_as(u64), n, _p(toks, i32p),
+                                       toks.shape[0], _p(off, i64p), ans, stride))
+    answers = [ans.raw[i * stride:(i + 1) * stride].split(b"\0", 1)[0].decode() for i in range(n)]
+    return toks[:int(off[-1])], off, answers
+
+
+def task_rewards(kind: int, difficulty: int, seeds, group_size: int, completions, lengths,
+                 vocab: int = VOCAB_TASK) -> np.ndarray:
+    """reward (tasks.cpp:155-175) of completions [n_prompts * G, stride] against seeds[m]."""
+    sd = _seeds(seeds)
+    comp = np.ascontiguousarray(completions, dtype=np.int32)
+    lens = np.ascontiguousarray(lengths, dtype=np.int32)
+    out = np.zeros(max(lens.shape[0], 1))
+    _check(lib().dashcu_task_rewards(kind, difficulty, vocab, sd.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                     sd.shape[0], group_size, _p(comp, i32p), comp.shape[1], _p(lens, i32p),
+                                     _p(out, f64p)))
+    return out[:lens.shape[0]]
 
 
 def num_params(arch: dict) -> int:
@@ -391,6 +439,12 @@ class Policy:
         return out[:n_tokens]
 
     # ---- advantage / filter
+    def task_rewards(self, kind: int, difficulty: int, seeds, vocab: int = VOCAB_TASK):
+        """Rewards of the current rollout from the task (dashcu_rollout_task_rewards)."""
+        sd = _seeds(seeds)
+        _check(lib().dashcu_rollout_task_rewards(self.h, kind, difficulty, vocab,
+                                                 sd.ctypes.data_as(C.POINTER(C.c_uint64))))
+
     def set_rewards(self, rewards):
         r = np.ascontiguousarray(rewards, dtype=np.float64)
         _check(lib().dashcu_rollout_set_rewards(self.h, _p(r, f64p), r.shape[0]))

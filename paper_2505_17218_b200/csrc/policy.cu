@@ -1354,6 +1354,20 @@ int dashcu_rollout_set_rewards(dashcu_policy* p, const double* rewards, int32_t 
   API_END
 }
 
+int dashcu_rollout_task_rewards(dashcu_policy* p, int32_t kind, int32_t difficulty, int32_t vocab,
+                                const uint64_t* seeds) {
+  API_BEGIN
+  check_policy(p);
+  if (!p->ro_valid) throw Error(1, "no rollout");
+  std::vector<double> r(p->n_seq);
+  const int rc = dashcu_task_rewards(kind, difficulty, vocab, seeds, p->n_prompts, p->G, p->h_comp.data(),
+                                     std::max(p->max_len, 1), p->h_len.data(), r.data());
+  if (rc) throw Error(rc, g_last_error);
+  p->h_rewards = std::move(r);
+  p->adv_valid = false;
+  API_END
+}
+
 int dashcu_rollout_advantage(dashcu_policy* p, int32_t kind, int32_t normalize, double eps, double tau, double* adv,
                              uint8_t* kept, int32_t* n_kept) {
   API_BEGIN

@@ -466,6 +466,37 @@ def test_dash_step_c1_matches_oracle(ctx, dtype):
     pol.close()
 
 
+@pytest.mark.ref
+def test_dash_step_c1_add_task_rewards(ctx):
+    """BASELINE configs[0] as specified: ADD prompts from the product's
+    generate_instance (byte vocabulary, difficulty 2), 64 prompts x G=8, max_len 57,
+    sampled on the GPU, rewarded by the product's task reward == the reference's
+    tasks::reward on the same completions, then group advantage + filter."""
+    import ctypes as C
+    arch = C1
+    pol = D.Policy(ctx, arch, D.BF16)
+    pol.upload(params32(arch, 0.02, 1))
+    M, G, ML = 64, 8, 57
+    seeds = [int(O.derive_seed(1, "prompt", m, 0)) for m in range(M)]
+    toks, off, answers = D.task_instances(D.TASK_ADD, 2, seeds, D.VOCAB_BYTE)
+    assert np.all(np.diff(off) == 7)
+    ro = pol.sample(None, G, ML, round_seed=5, prompt_tokens=toks, prompt_offsets=off)
+    pol.task_rewards(D.TASK_ADD, 2, seeds, D.VOCAB_BYTE)
+    adv, kept, nk = pol.advantage(tau=0.1)
+    R = O.ref()
+    R.ref_task_reward.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, O.i32p, C.c_int, O.f64p]
+    ref_r = np.zeros(M * G)
+    for s in range(M * G):
+        r = C.c_double(0)
+        comp = np.ascontiguousarray(ro.completions[s, :ro.lengths[s]])
+        assert R.ref_task_reward(0, 2, 1, seeds[s // G], O.ptr(comp, O.i32p), int(ro.lengths[s]), C.byref(r)) == 0
+        ref_r[s] = r.value
+    ra, rk, ri = O.advantage_filter(ref_r, G, 1, False, 0.0, 0.1)
+    assert np.array_equal(adv, ra) and np.array_equal(kept, rk) and nk == len(ri)
+    assert pol.stats()["mean_reward"] == ref_r.mean()
+    pol.close()
+
+
 @pytest.mark.parametrize("arch", [QWENLIKE, VBIG, LONGGQA], ids=["qwenlike", "vbig", "longgqa"])
 @pytest.mark.parametrize("temperature", [1.0, 0.7])
 def test_backward_reuses_sampler_lse(ctx, knob, arch, temperature):
