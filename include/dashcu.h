@@ -185,6 +185,56 @@ DASHCU_API int dashcu_accumulate(dashcu_policy* pol, double weight_scale, int32_
 /* Same with explicit per-sequence weights (weights[n_seq], all sequences). */
 DASHCU_API int dashcu_accumulate_weighted(dashcu_policy* pol, const double* weights, int32_t n_seq,
                                int32_t micro_batch);
+/* ---- PPO surrogate, KL term, update schedules (policy.cpp:487-522) ----
+ * dashcu_rollout_snapshot records theta_old for the current rollout: every sequence's
+ * summed teacher-forced log-prob under the current weights (call it at schedule entry,
+ * right after sampling). dashcu_accumulate_ppo then adds the gradient of the clipped
+ * surrogate mean over the kept sequences (intersected with subset[n_subset], null = all):
+ *   sum_n weight_scale * grad min(rho_n A_n, clip(rho_n, 1-eps, 1+eps) A_n),
+ *   rho_n = exp(sum_j log pi(y_nj) - sum_j log pi_old(y_nj))   (sequence level),
+ * which is weight_scale * A_n rho_n grad log pi on the unclipped branch and 0 on the clipped
+ * one; the weights may differ from the snapshot (no OnPolicyViolation). At theta ==
+ * theta_old rho is exactly 1 and the gradient equals dashcu_accumulate's. surrogate = the
+ * sum of the scaled surrogate terms, n_clipped = items on the clipped branch (both optional). */
+DASHCU_API int dashcu_rollout_snapshot(dashcu_policy* pol);
+DASHCU_API int dashcu_rollout_snapshot_logp(dashcu_policy* pol, double* per_seq, int32_t n_seq);
+DASHCU_API int dashcu_accumulate_ppo(dashcu_policy* pol, double weight_scale, double clip_eps, int32_t micro_batch,
+                                     const int32_t* subset, int32_t n_subset, double* surrogate, int32_t* n_clipped);
+/* grad += coef * sum over the listed sequences (subset, null = all) of grad_theta of the
+ * reference's kl_term(params, base, traj) (exact per-token KL(base || current), policy.cpp:
+ * 487-522); kl_per_seq[k] (optional) = its value. base: same context, arch and dtype. */
+DASHCU_API int dashcu_accumulate_kl(dashcu_policy* pol, dashcu_policy* base, double coef, int32_t micro_batch,
+                                    const int32_t* subset, int32_t n_subset, double* kl_per_seq);
+
+#define DASHCU_SCHED_DASH 0  /* one update from the PG gradient over the whole batch */
+#define DASHCU_SCHED_MULTI 1 /* K updates, each from the PPO gradient over the whole batch */
+#define DASHCU_SCHED_MINI 2  /* K updates, the k-th from the PPO gradient of mini-batch k */
+typedef struct {
+  int32_t kind;        /* DASHCU_SCHED_* */
+  int32_t K;           /* MULTI: steps per snapshot; MINI: mini-batches (n_seq % K == 0) */
+  double clip_eps;     /* PPO clip range (<= 0: the SPEC default 0.2) */
+  double beta;         /* KL weight (0: No-KL, the DASH preset) */
+  double weight_scale; /* 1/N, N the round's pre-filter size; MINI scales it by K (mean per mini-batch) */
+  int32_t micro_batch;
+  int32_t sharded;     /* 1: dashcu_sharded_step instead of allreduce + optimizer_step */
+} dashcu_schedule;
+typedef struct {
+  double surrogate;         /* PPO: sum of the scaled surrogate terms (0 for DASH) */
+  double kl;                /* beta > 0: scaled sum of the KL values */
+  double clip_fraction;     /* PPO: items on the clipped branch / items */
+  double mean_abs_adv;      /* mean |A| over the kept items (advantage.cpp:44-65) */
+  double filtered_fraction; /* 1 - kept / n */
+  int32_t n_items;          /* items this update's gradient covered */
+  double ms;                /* wall time of the update */
+} dashcu_step_log;
+/* run_schedule over the current rollout and advantage batch: DASH = one
+ * accumulate + (allreduce) + optimizer step; MULTI / MINI snapshot theta_old first (the
+ * policy must not have changed since sampling), then K PPO updates. beta > 0 adds
+ * -beta * grad KL(base || current) over the same items (J = J_inner - beta KL). logs[k]
+ * for k < max_logs; n_logs = the number of updates. */
+DASHCU_API int dashcu_run_schedule(dashcu_policy* pol, const dashcu_schedule* sched, const dashcu_opt* opt,
+                                   dashcu_policy* base, dashcu_step_log* logs, int32_t max_logs, int32_t* n_logs);
+
 DASHCU_API int dashcu_grad_download(dashcu_policy* pol, double* grad, int64_t n);
 /* Replace the device gradient (fp64 views() order), e.g. a GradientVector computed elsewhere. */
 DASHCU_API int dashcu_grad_upload(dashcu_policy* pol, const double* grad, int64_t n);

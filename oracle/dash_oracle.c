@@ -404,9 +404,13 @@ static void mtv_acc(const double* w, const double* a, double* y, int no, int ni)
   }
 }
 
-void dor_grad_log_prob_acc(const dor_arch* a, const double* P, const int32_t* prompt, int m,
-                           const int32_t* completion, int len, double scale, double* grad) {
-  if (len == 0 || scale == 0.0) return;
+/* grad_log_prob (policy.cpp:463-485) or, with base != NULL, the gradient of kl_term
+ * (policy.cpp:487-522: dlogits = softmax(current) - softmax(base) at every completion
+ * position, value = sum_j sum_i pb_i ((lb_i - lse_b) - (lc_i - lse_c))), scaled into grad. */
+static void grad_core(const dor_arch* a, const double* P, const double* base, const int32_t* prompt, int m,
+                      const int32_t* completion, int len, double scale, double* grad, double* kl_value) {
+  if (kl_value) *kl_value = 0.0;
+  if (len == 0 || (scale == 0.0 && !kl_value)) return;
   const geo g = geo_of(a);
   dor_layout lay;
   dor_layout_of(a, &lay);
@@ -430,13 +434,33 @@ void dor_grad_log_prob_acc(const dor_arch* a, const double* P, const int32_t* pr
   double* du = calloc((size_t)g.H, sizeof(double));
   double* da = calloc((size_t)n, sizeof(double));
 
-  /* LM head: dlogits = onehot(y) - softmax_nobos (policy.cpp:471-483) */
+  acts sb;
+  if (base) {
+    acts_alloc(&g, n, &sb);
+    forward(&g, &lay, base, tok, &sb);
+  }
+  /* LM head: dlogits = onehot(y) - softmax_nobos (policy.cpp:471-483), or the KL term's
+   * pc - pb (policy.cpp:509-518) */
   for (int j = 0; j < len; ++j) {
     const int t = m - 1 + j;
     const double* lg = s.logits + (size_t)t * V;
     const double lse = lse_nobos(lg, V, g.bos);
-    for (int i = 0; i < V; ++i) dz[i] = (i == g.bos) ? 0.0 : -exp(lg[i] - lse);
-    dz[completion[j]] += 1.0;
+    if (base) {
+      const double* lb = sb.logits + (size_t)t * V;
+      const double lse_b = lse_nobos(lb, V, g.bos);
+      for (int i = 0; i < V; ++i) {
+        if (i == g.bos) {
+          dz[i] = 0.0;
+          continue;
+        }
+        const double pb = exp(lb[i] - lse_b), pc = exp(lg[i] - lse);
+        if (kl_value) *kl_value += pb * ((lb[i] - lse_b) - (lg[i] - lse));
+        dz[i] = pc - pb;
+      }
+    } else {
+      for (int i = 0; i < V; ++i) dz[i] = (i == g.bos) ? 0.0 : -exp(lg[i] - lse);
+      dz[completion[j]] += 1.0;
+    }
     const double* yt = AT(s.y, g.L - 1, t, d);
     outer_acc(G + lay.w_out, dz, yt, V, d);
     for (int i = 0; i < V; ++i) G[lay.b_out + i] += dz[i];
@@ -538,7 +562,22 @@ void dor_grad_log_prob_acc(const dor_arch* a, const double* P, const int32_t* pr
   free(du);
   free(da);
   acts_free(&s);
+  if (base) acts_free(&sb);
   free(tok);
+}
+
+void dor_grad_log_prob_acc(const dor_arch* a, const double* P, const int32_t* prompt, int m,
+                           const int32_t* completion, int len, double scale, double* grad) {
+  grad_core(a, P, NULL, prompt, m, completion, len, scale, grad, NULL);
+}
+
+/* kl_term (policy.cpp:487-522): returns KL(base || current) summed over the completion
+ * positions; grad += scale * its gradient w.r.t. the current parameters P. */
+double dor_kl_term_acc(const dor_arch* a, const double* P, const double* base, const int32_t* prompt, int m,
+                       const int32_t* completion, int len, double scale, double* grad) {
+  double v = 0.0;
+  grad_core(a, P, base, prompt, m, completion, len, scale, grad, &v);
+  return v;
 }
 
 /* ------------------------------------------------------ sampling contract */

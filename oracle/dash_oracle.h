@@ -57,6 +57,10 @@ void dor_next_logits(const dor_arch* a, const double* params, const int32_t* ctx
 /* grad += scale * grad_log_prob (policy.cpp:463-485 + backward :201-346) */
 void dor_grad_log_prob_acc(const dor_arch* a, const double* params, const int32_t* prompt, int m,
                            const int32_t* completion, int len, double scale, double* grad);
+/* kl_term (policy.cpp:487-522) with GQA geometry: KL(base || current) over the completion
+ * positions (returned); grad += scale * d/dP of it. */
+double dor_kl_term_acc(const dor_arch* a, const double* P, const double* base, const int32_t* prompt, int m,
+                       const int32_t* completion, int len, double scale, double* grad);
 
 /* ---- sampling contract (App.B D2) ---- */
 float dor_soft_logf(float x);

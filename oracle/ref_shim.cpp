@@ -160,6 +160,21 @@ REF_API int ref_grad_log_prob(const int32_t* arch, const double* flat, const int
   });
 }
 
+// kl_term (policy.cpp:487-522): value and flat gradient in views() order.
+REF_API int ref_kl_term(const int32_t* arch, const double* flat, const double* base_flat, const int32_t* prompt,
+                        int m, const int32_t* completion, int len, double* value, double* grad_out) {
+  return guarded([&] {
+    auto p = params_of(arch, flat);
+    auto b = params_of(arch, base_flat);
+    dash::Trajectory t;
+    t.prompt = ivec(prompt, m);
+    t.completion = ivec(completion, len);
+    auto r = dash::kl_term(p, b, t);
+    *value = r.value;
+    flatten(r.grad, grad_out);
+  });
+}
+
 // next_token_probs (policy.cpp:524-537)
 REF_API int ref_next_token_probs(const int32_t* arch, const double* flat, const int32_t* ctx, int n,
                                  double* probs) {

@@ -24,6 +24,7 @@ F32, BF16 = 0, 1
 ADV_SINGLE_PATH, ADV_GROUP, ADV_LEAVE_ONE_OUT = 0, 1, 2
 FILTER_OFF = float("-inf")  # DASHCU_FILTER_OFF: no filter_by_threshold, every sequence kept
 OPT_SGD, OPT_ADAM = 0, 1
+SCHED_DASH, SCHED_MULTI, SCHED_MINI = 0, 1, 2
 TASK_ADD, TASK_MOD, TASK_REVERSE, TASK_PARITY, TASK_MICRO = 0, 1, 2, 3, 4
 VOCAB_TASK, VOCAB_BYTE = 0, 1
 
@@ -77,6 +78,21 @@ class Plan(C.Structure):
 class Opt(C.Structure):
     _fields_ = [("kind", C.c_int32), ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
                 ("eps", C.c_double)]
+
+
+class Schedule(C.Structure):
+    """UpdateConfig of run_schedule."""
+    _fields_ = [("kind", C.c_int32), ("K", C.c_int32), ("clip_eps", C.c_double), ("beta", C.c_double),
+                ("weight_scale", C.c_double), ("micro_batch", C.c_int32), ("sharded", C.c_int32)]
+
+
+class StepLog(C.Structure):
+    _fields_ = [("surrogate", C.c_double), ("kl", C.c_double), ("clip_fraction", C.c_double),
+                ("mean_abs_adv", C.c_double), ("filtered_fraction", C.c_double), ("n_items", C.c_int32),
+                ("ms", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
 
 
 class Stats(C.Structure):
@@ -141,6 +157,12 @@ def lib():
             "dashcu_sharded_step": [vp, C.POINTER(Opt)],
             "dashcu_shard_span": [C.c_int64, C.c_int32, C.c_int32, i64p, i64p],
             "dashcu_get_stats": [vp, C.POINTER(Stats)],
+            "dashcu_rollout_snapshot": [vp],
+            "dashcu_rollout_snapshot_logp": [vp, f64p, C.c_int32],
+            "dashcu_accumulate_ppo": [vp, C.c_double, C.c_double, C.c_int32, i32p, C.c_int32, f64p, i32p],
+            "dashcu_accumulate_kl": [vp, vp, C.c_double, C.c_int32, i32p, C.c_int32, f64p],
+            "dashcu_run_schedule": [vp, C.POINTER(Schedule), C.POINTER(Opt), vp, C.POINTER(StepLog), C.c_int32,
+                                    i32p],
             "dashcu_task_vocab_size": [C.c_int32, C.c_int32, i32p],
             "dashcu_task_instances": [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_uint64), C.c_int32, i32p,
                                       C.c_int64, i64p, C.c_char_p, C.c_int32],
@@ -469,6 +491,45 @@ class Policy:
     def accumulate_weighted(self, weights, micro_batch: int = 32):
         w = np.ascontiguousarray(weights, dtype=np.float64)
         _check(lib().dashcu_accumulate_weighted(self.h, _p(w, f64p), w.shape[0], micro_batch))
+
+    # ---- PPO / KL / schedules
+    def snapshot(self):
+        """theta_old of the current rollout (dashcu_rollout_snapshot)."""
+        _check(lib().dashcu_rollout_snapshot(self.h))
+
+    def snapshot_logp(self) -> np.ndarray:
+        n = self.stats()["n_seq"]
+        out = np.zeros(max(n, 1))
+        _check(lib().dashcu_rollout_snapshot_logp(self.h, _p(out, f64p), n))
+        return out[:n]
+
+    def accumulate_ppo(self, weight_scale: float, clip_eps: float = 0.2, micro_batch: int = 32, subset=None):
+        """Clipped-surrogate gradient over the kept (x subset) sequences; returns (surrogate, n_clipped)."""
+        sub = None if subset is None else np.ascontiguousarray(subset, dtype=np.int32)
+        sur, nc = C.c_double(0), C.c_int32(0)
+        _check(lib().dashcu_accumulate_ppo(self.h, weight_scale, clip_eps, micro_batch, _p(sub, i32p),
+                                           0 if sub is None else sub.shape[0], C.byref(sur), C.byref(nc)))
+        return sur.value, nc.value
+
+    def accumulate_kl(self, base: "Policy", coef: float, micro_batch: int = 32, subset=None) -> np.ndarray:
+        """grad += coef * grad KL(base || current) over the subset (all sequences); per-sequence KL values."""
+        n = self.stats()["n_seq"]
+        sub = None if subset is None else np.ascontiguousarray(subset, dtype=np.int32)
+        out = np.zeros(max(n if sub is None else sub.shape[0], 1))
+        _check(lib().dashcu_accumulate_kl(self.h, base.h, coef, micro_batch, _p(sub, i32p),
+                                          0 if sub is None else sub.shape[0], _p(out, f64p)))
+        return out[:(n if sub is None else sub.shape[0])]
+
+    def run_schedule(self, kind=SCHED_DASH, K=1, weight_scale=1.0, clip_eps=0.2, beta=0.0, micro_batch=32,
+                     sharded=False, base: "Policy" = None, opt_kind=OPT_ADAM, lr=1e-3, beta1=0.9, beta2=0.999,
+                     eps=1e-8):
+        sc = Schedule(kind, K, clip_eps, beta, weight_scale, micro_batch, int(sharded))
+        o = Opt(opt_kind, lr, beta1, beta2, eps)
+        logs = (StepLog * max(K, 1))()
+        n = C.c_int32(0)
+        _check(lib().dashcu_run_schedule(self.h, C.byref(sc), C.byref(o), base.h if base else None, logs, max(K, 1),
+                                         C.byref(n)))
+        return [logs[i].as_dict() for i in range(min(n.value, max(K, 1)))]
 
     def grad(self) -> np.ndarray:
         out = np.zeros(self.n_params)

@@ -112,6 +112,17 @@ template <class T>
 void lm_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, const int32_t* target,
              const float* weight, float* logp, T* dz);
 
+// PPO: per-sequence ratio from the per-row log-probs, clipped-surrogate
+// gradient weight broadcast to the sequence's rows; stats [nseq x 3] {rho, clipped, term}.
+void ppo_weights(cudaStream_t s, const float* logp, const int32_t* row_start, int nseq, const double* old_lp,
+                 const double* adv, double eps, float* w, double* stats);
+
+// KL term rows (kl_term, policy.cpp:487-522): value[r] = KL(base || current) at row r (fp64),
+// dz[r] = w_r (softmax(lc) - softmax(lb)), BOS column 0; dz may be null.
+template <class T>
+void kl_rows(cudaStream_t s, const float* lc, const float* lb, int rows, int V, int bos, const float* weight,
+             double* value, T* dz);
+
 // ---- gathers ---------------------------------------------------------------------------
 template <class T>
 void gather_rows(cudaStream_t s, const T* src, int64_t ld_src, const int32_t* idx, int rows, int width, T* dst);

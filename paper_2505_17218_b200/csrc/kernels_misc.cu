@@ -519,6 +519,53 @@ __global__ void __launch_bounds__(256) lm_rows_k(const float* logits, int V, int
   }
 }
 
+// KL term rows (kl_term, policy.cpp:487-522): per completion row r with current logits lc and
+// base logits lb (fp32, BOS excluded): value[r] = sum_i pb_i ((lb_i - lse_b) - (lc_i - lse_c))
+// = KL(base || current) at this context, and dz[r][i] = w_r (pc_i - pb_i) (the reference's
+// dlogits, BOS column 0); the value's sum runs in fp64.
+template <class T>
+__global__ void __launch_bounds__(256) kl_rows_k(const float* lc_all, const float* lb_all, int V, int bos,
+                                                 const float* weight, double* value, T* dz) {
+  __shared__ float sm[32];
+  __shared__ double smd[32];
+  const int r = blockIdx.x;
+  const float* lc = lc_all + static_cast<int64_t>(r) * V;
+  const float* lb = lb_all + static_cast<int64_t>(r) * V;
+  float mc = -FLT_MAX, mb = -FLT_MAX;
+  for (int i = threadIdx.x; i < V; i += blockDim.x)
+    if (i != bos) mc = fmaxf(mc, lc[i]), mb = fmaxf(mb, lb[i]);
+  mc = block_reduce(mc, sm, true);
+  mb = block_reduce(mb, sm, true);
+  float sc = 0.f, sb = 0.f;
+  for (int i = threadIdx.x; i < V; i += blockDim.x)
+    if (i != bos) sc += expf(lc[i] - mc), sb += expf(lb[i] - mb);
+  sc = block_reduce(sc, sm, false);
+  sb = block_reduce(sb, sm, false);
+  const float lse_c = mc + logf(sc), lse_b = mb + logf(sb);
+  const float w = weight ? weight[r] : 1.f;
+  double acc = 0.0;
+  T* out = dz ? dz + static_cast<int64_t>(r) * V : nullptr;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    float v = 0.f;
+    if (i != bos) {
+      const float lpc = lc[i] - lse_c, lpb = lb[i] - lse_b;
+      const float pb = expf(lpb), pc = expf(lpc);
+      acc += static_cast<double>(pb) * (static_cast<double>(lpb) - static_cast<double>(lpc));
+      v = w * (pc - pb);
+    }
+    if (out) out[i] = fromf<T>(v);
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) smd[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < (blockDim.x >> 5); ++k) t += smd[k];
+    if (value) value[r] = t;
+  }
+}
+
+
 // ------------------------------------------------------------------- KV plumbing
 
 template <class T>
@@ -820,6 +867,41 @@ void sample_scan(cudaStream_t s, const float* part, int nslices, const float* lo
   DCU_LAUNCHED();
 }
 
+// PPO clipped-surrogate weights: one thread per sequence of the micro-batch.
+// Sequence-level ratio rho = exp(sum_j logp_j - old_lp) with the per-token teacher-forced
+// log-probs summed in row order in fp64 (the snapshot sums the same fp32 values in the same
+// order, so at theta == theta_old rho is exactly 1). The gradient of
+// min(rho A, clip(rho, 1-eps, 1+eps) A) is rho A grad log pi on the unclipped branch and 0
+// where the clipped (constant) branch is the minimum: A > 0 and rho > 1+eps, or A < 0 and
+// rho < 1-eps. Every loss row of the sequence gets the weight; stats[i] = {rho, clipped,
+// surrogate term}.
+__global__ void ppo_weights_k(const float* __restrict__ logp, const int32_t* __restrict__ row_start, int nseq,
+                              const double* __restrict__ old_lp, const double* __restrict__ adv, double eps,
+                              float* __restrict__ w, double* __restrict__ stats) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nseq) return;
+  double sum = 0.0;
+  for (int r = row_start[i]; r < row_start[i + 1]; ++r) sum += static_cast<double>(logp[r]);
+  const double rho = exp(sum - old_lp[i]);
+  const double a = adv[i];
+  const bool clipped = (a > 0.0 && rho > 1.0 + eps) || (a < 0.0 && rho < 1.0 - eps);
+  const double wi = clipped ? 0.0 : a * rho;
+  const double clip_rho = fmin(fmax(rho, 1.0 - eps), 1.0 + eps);
+  for (int r = row_start[i]; r < row_start[i + 1]; ++r) w[r] = static_cast<float>(wi);
+  if (stats) {
+    stats[3 * i] = rho;
+    stats[3 * i + 1] = clipped ? 1.0 : 0.0;
+    stats[3 * i + 2] = fmin(rho * a, clip_rho * a);
+  }
+}
+
+void ppo_weights(cudaStream_t s, const float* logp, const int32_t* row_start, int nseq, const double* old_lp,
+                 const double* adv, double eps, float* w, double* stats) {
+  if (nseq <= 0) return;
+  ppo_weights_k<<<cdiv(nseq, 128), 128, 0, s>>>(logp, row_start, nseq, old_lp, adv, eps, w, stats);
+  DCU_LAUNCHED();
+}
+
 __global__ void gather_f32_k(const float* __restrict__ src, const int32_t* __restrict__ idx, int n,
                              float* __restrict__ dst) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -840,6 +922,17 @@ void lm_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, cons
   lm_rows_k<T><<<rows, 256, 0, s>>>(logits, V, bos, target, weight, logp, dz);
   DCU_LAUNCHED();
 }
+
+template <class T>
+void kl_rows(cudaStream_t s, const float* lc, const float* lb, int rows, int V, int bos, const float* weight,
+             double* value, T* dz) {
+  if (rows <= 0) return;
+  ProfScope ps(PROF_LM_ROWS, s, 0, static_cast<double>(rows) * V * (8.0 + (dz ? sizeof(T) : 0)));
+  kl_rows_k<T><<<rows, 256, 0, s>>>(lc, lb, V, bos, weight, value, dz);
+  DCU_LAUNCHED();
+}
+template void kl_rows<float>(cudaStream_t, const float*, const float*, int, int, int, const float*, double*, float*);
+template void kl_rows<bf16>(cudaStream_t, const float*, const float*, int, int, int, const float*, double*, bf16*);
 
 template <class T>
 void kv_store_prompt(cudaStream_t s, const T* qkv, const int32_t* start, int n_prompts, int pmax, int qd, int kvd,

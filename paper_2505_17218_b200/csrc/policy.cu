@@ -305,6 +305,9 @@ struct dashcu_policy {
   std::vector<double> h_rewards, h_adv;
   std::vector<int32_t> h_kidx;
   bool adv_valid = false;
+  // PPO snapshot (theta_old) of the current rollout: per-sequence summed teacher-forced log-probs
+  std::vector<double> h_oldlp;
+  bool snap_valid = false;
   bool dump = false;
   dashcu::DevMem d_dump;
   int64_t dump_n = 0;
@@ -427,10 +430,24 @@ struct Engine {
     }
   }
 
+  // PPO clipped surrogate over the loss rows of a micro-batch: the rows of
+  // sequence i are [row_start[i], row_start[i+1]); old_lp[i] = the snapshot's summed log-prob,
+  // adv[i] = A_i * scale; stats [nseq x 3] {rho, clipped, surrogate term} (may be null).
+  struct PpoRows {
+    const int32_t* row_start;
+    int nseq;
+    const double* old_lp;
+    const double* adv;
+    double eps;
+    double* stats;
+  };
+
   // Loss rows: rows (packed index), tgt, weight. If grad: backward through the
   // LM head, writing dL/dy_top into dy32 (zeroed here). logp may be null.
+  // lsei: per-row index of the sampler's T = 1 LSE (bf16 reuse); ppo: the row weights are
+  // the PPO surrogate's, computed from this pass's own log-probs (two passes over the rows).
   void lm_head(const Acts& A, int R, const int32_t* rows, const int32_t* tgt, const float* w, float* logp,
-               bool grad, float* dy32, const int32_t* lsei = nullptr) {
+               bool grad, float* dy32, const int32_t* lsei = nullptr, const PpoRows* ppo = nullptr) {
     const int64_t V = g.V;
     // bf16: the logits stay in TMEM (LSE pass + dz pass); fp32 parity path: fp32 logits + row kernel
     constexpr bool fused = sizeof(T) == 2;
@@ -438,55 +455,170 @@ struct Engine {
                          : static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8192, (int64_t(1) << 31) / (V * 4))));
     if (grad) fill_f32(st, dy32, 0.f, static_cast<int64_t>(A.T_) * g.d);
     T* ycT = P.ws.get<T>("lm_yc", static_cast<size_t>(RC) * g.d);
-    float* lg = fused ? nullptr : P.ws.get<float>("lm_logits", static_cast<size_t>(RC) * V);
+    float* lg = nullptr;
     T* dz = grad ? P.ws.get<T>("lm_dz", static_cast<size_t>(RC) * V) : nullptr;
     float* dyc = grad ? P.ws.get<float>("lm_dyc", static_cast<size_t>(RC) * g.d) : nullptr;
     float* part = fused ? P.ws.get<float>("lm_part", static_cast<size_t>(RC) * gemm_tc_lse_tiles(g.V) * 2) : nullptr;
     float* lse = fused ? P.ws.get<float>("lm_lse", RC) : nullptr;
-    for (int r0 = 0; r0 < R; r0 += RC) {
-      const int rc = std::min(RC, R - r0);
-      gather_rows<T>(st, A.yT, g.d, rows + r0, rc, g.d, ycT);
-      bool done = false;
+    auto logits_chunk = [&](int rc) {  // fp32 logits of the gathered rows (parity path / fallback)
+      if (!lg) lg = P.ws.get<float>("lm_logits", static_cast<size_t>(RC) * V);
+      Epi el = store(lg, V, nullptr, 0);
+      el.bias = W32(L.bout);
+      mm(rc, g.V, g.d, ycT, g.d, true, W(L.wout), g.d, true, el);
+    };
+    // row LSE (+ logp) of rows [r0, r0 + rc) into lse_out / logp_out; false if the fused
+    // kernels cannot take the shape (then lse_out is not written)
+    auto row_lse = [&](int r0, int rc, float* lse_out, float* logp_out) {
       if constexpr (fused) {
         GemmShape gs{rc, g.V, g.d, ycT, g.d, true, W(L.wout), g.d, true};
         SampleArgs sa;
         sa.bos = g.bos;
         sa.part = part;
-        const bool have_lse = lsei && grad && !logp;
-        const int nt = have_lse ? 1 : gemm_tc_lse(st, gs, W32(L.bout), sa);
+        const int nt = gemm_tc_lse(st, gs, W32(L.bout), sa);
         if (nt > 0) {
-          if (have_lse) gather_f32(st, P.d_lse.as<float>(), lsei + r0, rc, lse);  // the sampler's row LSE
-          else
-            lse_reduce(st, part, nt, rc, lse, ycT, g.d, W(L.wout), W32(L.bout), tgt + r0, logp ? logp + r0 : nullptr);
-          if (grad) {
-            sa.lse = lse;
-            sa.target = tgt + r0;
-            sa.weight = w + r0;
-            sa.dz = dz;
-            sa.ld_dz = V;
-            done = gemm_tc_dz(st, gs, W32(L.bout), sa);
-          } else {
-            done = true;
-          }
+          lse_reduce(st, part, nt, rc, lse_out, ycT, g.d, W(L.wout), W32(L.bout), tgt + r0, logp_out);
+          return true;
         }
       }
-      if (!done) {
-        if (!lg) lg = P.ws.get<float>("lm_logits", static_cast<size_t>(RC) * V);
-        Epi el = store(lg, V, nullptr, 0);
-        el.bias = W32(L.bout);
-        mm(rc, g.V, g.d, ycT, g.d, true, W(L.wout), g.d, true, el);
-        lm_rows<T>(st, lg, rc, g.V, g.bos, tgt + r0, w ? w + r0 : nullptr, logp ? logp + r0 : nullptr, dz);
+      logits_chunk(rc);
+      lm_rows<T>(st, lg, rc, g.V, g.bos, tgt + r0, nullptr, logp_out, static_cast<T*>(nullptr));
+      return false;
+    };
+    // dz = w (onehot - softmax) of rows [r0, r0 + rc) given their LSE (fused) or from scratch
+    auto dz_chunk = [&](int r0, int rc, const float* lse_in, const float* w_in) {
+      if constexpr (fused) {
+        if (lse_in) {
+          GemmShape gs{rc, g.V, g.d, ycT, g.d, true, W(L.wout), g.d, true};
+          SampleArgs sa;
+          sa.bos = g.bos;
+          sa.lse = lse_in;
+          sa.target = tgt + r0;
+          sa.weight = w_in;
+          sa.dz = dz;
+          sa.ld_dz = V;
+          if (gemm_tc_dz(st, gs, W32(L.bout), sa)) return;
+        }
       }
-      if (!grad) continue;
-      Epi ew;
-      ew.kind = EPI_ACCUM;
-      ew.c32 = G32(L.wout);
-      ew.ldc32 = g.d;
-      mm(g.V, g.d, rc, dz, V, false, ycT, g.d, false, ew);  // dW_out += dz^T y
-      colsum_acc<T>(st, dz, V, rc, g.V, G32(L.bout),           // db_out += sum dz
-                    P.ws.get<float>("cs_bout", colsum_tmp_floats<T>(RC, g.V)));
-      mm(rc, g.d, g.V, dz, V, true, W(L.wout), g.d, false, store(dyc, g.d, nullptr, 0));  // dy = dz W_out
-      scatter_rows_f32(st, dyc, rc, g.d, rows + r0, dy32);
+      logits_chunk(rc);
+      lm_rows<T>(st, lg, rc, g.V, g.bos, tgt + r0, w_in, nullptr, dz);
+    };
+    float* lse_all = nullptr;
+    bool lse_all_ok = false;
+    if (ppo) {  // pass 1 over every row: LSE + logp, then the surrogate's per-row weights
+      lse_all = P.ws.get<float>("lm_lse_all", R);
+      float* lp_all = P.ws.get<float>("lm_lp_all", R);
+      float* w_all = P.ws.get<float>("lm_w_all", R);
+      for (int r0 = 0; r0 < R; r0 += RC) {
+        const int rc = std::min(RC, R - r0);
+        gather_rows<T>(st, A.yT, g.d, rows + r0, rc, g.d, ycT);
+        lse_all_ok = row_lse(r0, rc, lse_all + r0, lp_all + r0);
+      }
+      ppo_weights(st, lp_all, ppo->row_start, ppo->nseq, ppo->old_lp, ppo->adv, ppo->eps, w_all, ppo->stats);
+      w = w_all;
+      if (logp) DCU_CHECK(cudaMemcpyAsync(logp, lp_all, sizeof(float) * R, cudaMemcpyDeviceToDevice, st));
+    }
+    for (int r0 = 0; r0 < R; r0 += RC) {
+      const int rc = std::min(RC, R - r0);
+      gather_rows<T>(st, A.yT, g.d, rows + r0, rc, g.d, ycT);
+      if (ppo) {
+        dz_chunk(r0, rc, lse_all_ok ? lse_all + r0 : nullptr, w + r0);
+      } else if (!grad) {
+        row_lse(r0, rc, lse ? lse : P.ws.get<float>("lm_lse", RC), logp ? logp + r0 : nullptr);
+        continue;
+      } else if (fused && lsei && !logp) {  // the sampler's row LSE (same weights: on-policy)
+        gather_f32(st, P.d_lse.as<float>(), lsei + r0, rc, lse);
+        dz_chunk(r0, rc, lse, w + r0);
+      } else if (fused && row_lse(r0, rc, lse, logp ? logp + r0 : nullptr)) {
+        dz_chunk(r0, rc, lse, w + r0);
+      } else if (!fused) {
+        logits_chunk(rc);
+        lm_rows<T>(st, lg, rc, g.V, g.bos, tgt + r0, w ? w + r0 : nullptr, logp ? logp + r0 : nullptr, dz);
+      } else {
+        dz_chunk(r0, rc, nullptr, w + r0);
+      }
+      dz_backprop(ycT, dz, rc, RC, rows + r0, dyc, dy32);
+    }
+  }
+
+  // Through the LM head given dz = dL/dlogits of rc gathered rows (policy.cpp:208-224):
+  // dW_out += dz^T y, db_out += colsum dz, dy[rows] = dz W_out.
+  void dz_backprop(const T* ycT, const T* dz, int rc, int RC, const int32_t* rows, float* dyc, float* dy32) {
+    const int64_t V = g.V;
+    Epi ew;
+    ew.kind = EPI_ACCUM;
+    ew.c32 = G32(L.wout);
+    ew.ldc32 = g.d;
+    mm(g.V, g.d, rc, dz, V, false, ycT, g.d, false, ew);
+    colsum_acc<T>(st, dz, V, rc, g.V, G32(L.bout), P.ws.get<float>("cs_bout", colsum_tmp_floats<T>(RC, g.V)));
+    mm(rc, g.d, g.V, dz, V, true, W(L.wout), g.d, false, store(dyc, g.d, nullptr, 0));
+    scatter_rows_f32(st, dyc, rc, g.d, rows, dy32);
+  }
+
+  // KL term through the LM head (kl_term, policy.cpp:487-522): current logits from A, base
+  // logits from Ab under the base policy's weights (eb), both fp32; dz = coef (pc - pb);
+  // vals[r] = KL(base || current) of loss row r.
+  void lm_head_kl(const Acts& A, const Acts& Ab, Engine<T>& eb, int R, const int32_t* rows, float coef, float* dy32,
+                  double* vals) {
+    const int64_t V = g.V;
+    const int RC = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8192, (int64_t(1) << 31) / (V * 8))));
+    fill_f32(st, dy32, 0.f, static_cast<int64_t>(A.T_) * g.d);
+    T* ycT = P.ws.get<T>("lm_yc", static_cast<size_t>(RC) * g.d);
+    T* ybT = P.ws.get<T>("kl_yb", static_cast<size_t>(RC) * g.d);
+    float* lc = P.ws.get<float>("kl_lc", static_cast<size_t>(RC) * V);
+    float* lb = P.ws.get<float>("kl_lb", static_cast<size_t>(RC) * V);
+    T* dz = P.ws.get<T>("lm_dz", static_cast<size_t>(RC) * V);
+    float* dyc = P.ws.get<float>("lm_dyc", static_cast<size_t>(RC) * g.d);
+    float* wv = P.ws.get<float>("kl_w", RC);
+    fill_f32(st, wv, coef, RC);
+    for (int r0 = 0; r0 < R; r0 += RC) {
+      const int rc = std::min(RC, R - r0);
+      gather_rows<T>(st, A.yT, g.d, rows + r0, rc, g.d, ycT);
+      gather_rows<T>(st, Ab.yT, g.d, rows + r0, rc, g.d, ybT);
+      Epi ec = store(lc, V, nullptr, 0);
+      ec.bias = W32(L.bout);
+      mm(rc, g.V, g.d, ycT, g.d, true, W(L.wout), g.d, true, ec);
+      Epi eb_ = store(lb, V, nullptr, 0);
+      eb_.bias = eb.W32(L.bout);
+      mm(rc, g.V, g.d, ybT, g.d, true, eb.W(L.wout), g.d, true, eb_);
+      kl_rows<T>(st, lc, lb, rc, g.V, g.bos, wv, vals + r0, dz);
+      dz_backprop(ycT, dz, rc, RC, rows + r0, dyc, dy32);
+    }
+  }
+
+  // grad += coef * sum_k grad KL(base || current)(seq_k); kl_out[k] = that sequence's KL
+  // (the reference's KlResult value, summed over its completion positions in fp64).
+  void accumulate_kl(Pol& base, const std::vector<int>& seqs, double coef, int micro, std::vector<double>* kl_out) {
+    if (micro <= 0) micro = static_cast<int>(seqs.size());
+    kl_out->assign(seqs.size(), 0.0);
+    Engine<T> eb(base);
+    for (size_t k0 = 0; k0 < seqs.size(); k0 += micro) {
+      const size_t k1 = std::min(seqs.size(), k0 + static_cast<size_t>(micro));
+      std::vector<int> ss(seqs.begin() + k0, seqs.begin() + k1);
+      Batch B = pack(ss, {});
+      if (B.seqs.empty()) continue;
+      DevBatch D = upload(B);
+      const int Tn = static_cast<int>(B.tok.size());
+      const int R = static_cast<int>(B.rows.size());
+      Acts A = alloc_acts(P.ws, Tn, "a_");
+      pairs = B.pairs;
+      forward(A, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen);
+      Acts Ab = alloc_acts(P.ws, Tn, "kb_");
+      eb.pairs = B.pairs;
+      eb.forward(Ab, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen);
+      float* dy32 = P.ws.get<float>("b_dy32", static_cast<size_t>(Tn) * g.d);
+      double* vals = P.ws.get<double>("kl_vals", R);
+      lm_head_kl(A, Ab, eb, R, D.rows, static_cast<float>(coef), dy32, vals);
+      backward(A, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen, dy32);
+      std::vector<double> hv(R);
+      d2h(st, hv.data(), vals, R);
+      DCU_CHECK(cudaStreamSynchronize(st));
+      std::map<int, size_t> at;
+      for (size_t k = k0; k < k1; ++k) at[seqs[k]] = k;
+      for (size_t q = 0; q < B.seqs.size(); ++q) {
+        double v = 0.0;
+        for (int r = B.rstart[q]; r < B.rstart[q + 1]; ++r) v += hv[r];
+        (*kl_out)[at[B.seqs[q]]] = v;
+      }
     }
   }
 
@@ -575,6 +707,8 @@ struct Engine {
   // ------------------------------------------------------------ micro-batch
   struct Batch {
     std::vector<int32_t> tok, pos, start, rows, tgt, seqs, lsei;  // lsei: row -> d_lse cell
+    std::vector<int32_t> rstart{0};  // loss rows of sequence k: [rstart[k], rstart[k+1])
+    std::vector<double> sw;          // per-sequence weight (PPO: A_n * scale)
     std::vector<float> w;
     int maxlen = 0;
     double pairs = 0;  // sum over sequences of n(n+1)/2 causal (query, key) pairs
@@ -608,6 +742,8 @@ struct Engine {
         B.w.push_back(static_cast<float>(weight.empty() ? 1.0 : weight[k]));
       }
       B.start.push_back(s0 + n);
+      B.rstart.push_back(static_cast<int32_t>(B.rows.size()));
+      B.sw.push_back(weight.empty() ? 1.0 : weight[k]);
       B.seqs.push_back(s);
       B.maxlen = std::max(B.maxlen, n);
       B.pairs += 0.5 * n * (n + 1.0);
@@ -619,6 +755,9 @@ struct Engine {
     int32_t *tok, *pos, *start, *rows, *tgt;
     float* w;
     int32_t* lsei;
+    int32_t* rstart = nullptr;
+    double* sw = nullptr;
+    double* old_lp = nullptr;
   };
   DevBatch upload(const Batch& B) {
     DevBatch d;
@@ -640,10 +779,11 @@ struct Engine {
 
   // All micro-batches of a round packed on the host up front and uploaded with one
   // copy per array, so the GPU never waits for host packing between micro-batches.
-  std::vector<DevBatch> upload_all(const std::vector<Batch>& bs) {
+  std::vector<DevBatch> upload_all(const std::vector<Batch>& bs, const std::vector<double>* old_lp = nullptr) {
     size_t nt = 0, ns = 0, nr = 0;
     for (const Batch& b : bs) nt += b.tok.size(), ns += b.start.size(), nr += b.rows.size();
-    std::vector<int32_t> tok, pos, start, rows, tgt, lsei;
+    std::vector<int32_t> tok, pos, start, rows, tgt, lsei, rstart;
+    std::vector<double> sw, olp;
     std::vector<float> w;
     tok.reserve(nt), pos.reserve(nt), start.reserve(ns), rows.reserve(nr), tgt.reserve(nr), w.reserve(nr);
     lsei.reserve(nr);
@@ -655,6 +795,10 @@ struct Engine {
       tgt.insert(tgt.end(), b.tgt.begin(), b.tgt.end());
       w.insert(w.end(), b.w.begin(), b.w.end());
       lsei.insert(lsei.end(), b.lsei.begin(), b.lsei.end());
+      rstart.insert(rstart.end(), b.rstart.begin(), b.rstart.end());
+      sw.insert(sw.end(), b.sw.begin(), b.sw.end());
+      if (old_lp)
+        for (int sq : b.seqs) olp.push_back((*old_lp)[sq]);
     }
     int32_t* dtok = P.ws.get<int32_t>("mb_tok", nt);
     int32_t* dpos = P.ws.get<int32_t>("mb_pos", nt);
@@ -670,17 +814,32 @@ struct Engine {
     h2d(st, drows, rows.data(), nr);
     h2d(st, dtgt, tgt.data(), nr);
     h2d(st, dw, w.data(), nr);
+    int32_t* drst = P.ws.get<int32_t>("mb_rstart", rstart.size());
+    double* dsw = P.ws.get<double>("mb_sw", sw.size());
+    double* dolp = old_lp ? P.ws.get<double>("mb_oldlp", olp.size()) : nullptr;
+    h2d(st, drst, rstart.data(), rstart.size());
+    h2d(st, dsw, sw.data(), sw.size());
+    if (old_lp) h2d(st, dolp, olp.data(), olp.size());
     std::vector<DevBatch> out;
-    size_t ot = 0, os = 0, orr = 0;
+    size_t ot = 0, os = 0, orr = 0, oq = 0;
     for (const Batch& b : bs) {
-      out.push_back(DevBatch{dtok + ot, dpos + ot, dstart + os, drows + orr, dtgt + orr, dw + orr, dlsei + orr});
-      ot += b.tok.size(), os += b.start.size(), orr += b.rows.size();
+      DevBatch d{dtok + ot, dpos + ot, dstart + os, drows + orr, dtgt + orr, dw + orr, dlsei + orr};
+      d.rstart = drst + os;  // rstart has one entry per start entry (n_seq + 1 per batch)
+      d.sw = dsw + oq;
+      d.old_lp = dolp ? dolp + oq : nullptr;
+      out.push_back(d);
+      ot += b.tok.size(), os += b.start.size(), orr += b.rows.size(), oq += b.seqs.size();
     }
     return out;
   }
 
   // grad += sum_k weight[k] * grad log pi(seq_k), micro_batch sequences at a time.
-  int64_t accumulate(const std::vector<int>& seqs, const std::vector<double>& weight, int micro) {
+  // ppo_old (PPO): the snapshot's per-sequence summed log-probs; the
+  // weights are then A_k * scale (weight[k]) times the clipped-surrogate factor, and
+  // ppo_stats (if non-null) receives {rho, clipped, term} per listed sequence.
+  int64_t accumulate(const std::vector<int>& seqs, const std::vector<double>& weight, int micro,
+                     const std::vector<double>* ppo_old = nullptr, double clip_eps = 0.2,
+                     std::vector<double>* ppo_stats = nullptr) {
     int64_t loss_tokens = 0;
     if (micro <= 0) micro = static_cast<int>(seqs.size());
     std::vector<Batch> batches;
@@ -691,11 +850,19 @@ struct Engine {
       Batch B = pack(ss, ww);
       if (!B.seqs.empty()) batches.push_back(std::move(B));
     }
-    const std::vector<DevBatch> dev = upload_all(batches);
+    const std::vector<DevBatch> dev = upload_all(batches, ppo_old);
+    double* dstats = nullptr;
+    if (ppo_old && ppo_stats) {
+      ppo_stats->assign(3 * seqs.size(), 0.0);
+      dstats = P.ws.get<double>("ppo_stats", std::max<size_t>(3 * seqs.size(), 1));
+    }
     // The sampler already computed the T = 1 log-sum-exp of every completion position
     // under the same weights (on-policy: the version check above), so the backward skips
     // the LM-head LSE pass and reads it (DASHCU_LSE_RECOMPUTE=1 recomputes instead)
-    const bool reuse_lse = sizeof(T) == 2 && P.lse_valid && knob(KNOB_LSE_RECOMPUTE) != 1;
+    // (valid only on-policy: the LSE belongs to the weights that sampled the rollout)
+    const bool reuse_lse = sizeof(T) == 2 && P.lse_valid && P.ro_version == P.version && !ppo_old &&
+                           knob(KNOB_LSE_RECOMPUTE) != 1;
+    size_t seq_off = 0;
     for (size_t bi = 0; bi < batches.size(); ++bi) {
       const Batch& B = batches[bi];
       const DevBatch& D = dev[bi];
@@ -704,9 +871,28 @@ struct Engine {
       pairs = B.pairs;
       forward(A, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen);
       float* dy32 = P.ws.get<float>("b_dy32", static_cast<size_t>(Tn) * g.d);
-      lm_head(A, static_cast<int>(B.rows.size()), D.rows, D.tgt, D.w, nullptr, true, dy32, reuse_lse ? D.lsei : nullptr);
+      PpoRows pr{D.rstart, static_cast<int>(B.seqs.size()), D.old_lp, D.sw, clip_eps,
+                 dstats ? dstats + 3 * seq_off : nullptr};
+      lm_head(A, static_cast<int>(B.rows.size()), D.rows, D.tgt, D.w, nullptr, true, dy32, reuse_lse ? D.lsei : nullptr,
+              ppo_old ? &pr : nullptr);
+      seq_off += B.seqs.size();
       backward(A, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen, dy32);
       loss_tokens += static_cast<int64_t>(B.rows.size());
+    }
+    if (dstats) {  // back to the caller's order; empty completions: rho = 1, unclipped
+      std::vector<double> packed(3 * std::max<size_t>(seq_off, 1));
+      if (seq_off) d2h(st, packed.data(), dstats, 3 * seq_off);
+      DCU_CHECK(cudaStreamSynchronize(st));
+      std::map<int, size_t> at;
+      size_t q = 0;
+      for (const Batch& b : batches)
+        for (int sq : b.seqs) at[sq] = q++;
+      for (size_t k = 0; k < seqs.size(); ++k) {
+        auto it = at.find(seqs[k]);
+        double* o = ppo_stats->data() + 3 * k;
+        if (it == at.end()) o[0] = 1.0, o[1] = 0.0, o[2] = weight[k];
+        else std::copy(packed.begin() + 3 * it->second, packed.begin() + 3 * it->second + 3, o);
+      }
     }
     return loss_tokens;
   }
@@ -1232,6 +1418,7 @@ static int sample_impl(dashcu_policy* p, const dashcu_plan* plan, const int32_t*
   p->max_len = plan->max_len;
   p->ro_valid = false;
   p->adv_valid = false;
+  p->snap_valid = false;
   const float inv_t = static_cast<float>(1.0 / plan->temperature);
   Timer tm(p->ctx->stream);
   dispatch(p, [&](auto& e) { e.sample(*plan, cap, keys, inv_t); });
@@ -1293,6 +1480,7 @@ int dashcu_rollout_load(dashcu_policy* p, const int32_t* prompt_tokens, const in
   p->ro_valid = true;
   p->lse_valid = false;  // external trajectories: the backward runs its own LSE pass
   p->adv_valid = false;
+  p->snap_valid = false;
   p->st.n_seq = S;
   API_END
 }
@@ -1440,6 +1628,188 @@ int dashcu_accumulate_weighted(dashcu_policy* p, const double* weights, int32_t 
       w.push_back(weights[s]);
     }
   accumulate_impl(p, seqs, w, micro);
+  API_END
+}
+
+// ---------------------------------------------------------------- PPO / KL / schedules
+
+int dashcu_rollout_snapshot(dashcu_policy* p) {
+  API_BEGIN
+  check_policy(p);
+  if (!p->ro_valid) throw Error(1, "no rollout");
+  int64_t n_tok = 0;
+  for (int s = 0; s < p->n_seq; ++s) n_tok += p->h_len[s];
+  std::vector<float> per(std::max<int64_t>(n_tok, 1));
+  dispatch(p, [&](auto& e) { e.log_prob(per.data(), n_tok); });
+  p->h_oldlp.assign(p->n_seq, 0.0);
+  int64_t off = 0;
+  for (int s = 0; s < p->n_seq; ++s)  // row order, fp64: the same sum ppo_weights_k forms
+    for (int j = 0; j < p->h_len[s]; ++j) p->h_oldlp[s] += static_cast<double>(per[off++]);
+  p->snap_valid = true;
+  API_END
+}
+
+int dashcu_rollout_snapshot_logp(dashcu_policy* p, double* out, int32_t n) {
+  API_BEGIN
+  check_policy(p);
+  if (!p->snap_valid) throw Error(1, "no snapshot (dashcu_rollout_snapshot)");
+  if (n != p->n_seq) throw Error(1, "snapshot and buffer disagree on batch size");
+  std::memcpy(out, p->h_oldlp.data(), sizeof(double) * n);
+  API_END
+}
+
+// the kept sequences of the current advantage batch, intersected with subset (null = all)
+static std::vector<int> kept_subset(dashcu_policy* p, const int32_t* subset, int32_t n_subset) {
+  if (!p->adv_valid) throw Error(1, "call dashcu_rollout_advantage first");
+  std::vector<int> seqs;
+  if (!subset) {
+    seqs.assign(p->h_kidx.begin(), p->h_kidx.end());
+    return seqs;
+  }
+  std::vector<uint8_t> in(p->n_seq, 0);
+  for (int i = 0; i < n_subset; ++i) {
+    if (subset[i] < 0 || subset[i] >= p->n_seq) throw Error(1, "subset index out of range");
+    in[subset[i]] = 1;
+  }
+  for (int32_t s : p->h_kidx)
+    if (in[s]) seqs.push_back(s);
+  return seqs;
+}
+
+static void ppo_impl(dashcu_policy* p, double scale, double clip_eps, int micro, const int32_t* subset,
+                     int32_t n_subset, double* surrogate, int32_t* n_clipped) {
+  if (!p->ro_valid) throw Error(1, "no rollout");
+  if (!p->snap_valid) throw Error(1, "no snapshot of the rollout (dashcu_rollout_snapshot at schedule entry)");
+  if (!(clip_eps > 0.0)) throw Error(1, "clip_eps must be positive");
+  const std::vector<int> seqs = kept_subset(p, subset, n_subset);
+  std::vector<double> w(seqs.size()), stats;
+  for (size_t k = 0; k < seqs.size(); ++k) w[k] = p->h_adv[seqs[k]] * scale;
+  Timer tm(p->ctx->stream);
+  int64_t lt = 0;
+  dispatch(p, [&](auto& e) { lt = e.accumulate(seqs, w, micro, &p->h_oldlp, clip_eps, &stats); });
+  p->st.accumulate_ms = tm.stop_ms();
+  p->st.loss_tokens = lt;
+  double sur = 0.0;
+  int32_t nc = 0;
+  for (size_t k = 0; k < seqs.size(); ++k) sur += stats[3 * k + 2], nc += stats[3 * k + 1] != 0.0;
+  if (surrogate) *surrogate = sur;
+  if (n_clipped) *n_clipped = nc;
+}
+
+int dashcu_accumulate_ppo(dashcu_policy* p, double weight_scale, double clip_eps, int32_t micro,
+                          const int32_t* subset, int32_t n_subset, double* surrogate, int32_t* n_clipped) {
+  API_BEGIN
+  check_policy(p);
+  ppo_impl(p, weight_scale, clip_eps, micro, subset, n_subset, surrogate, n_clipped);
+  API_END
+}
+
+static void kl_impl(dashcu_policy* p, dashcu_policy* base, double coef, int micro, const std::vector<int>& seqs,
+                    std::vector<double>* kl) {
+  if (!base || base->ctx != p->ctx) throw Error(1, "base policy must live on the same context");
+  if (std::memcmp(&base->arch, &p->arch, sizeof(dashcu_arch)) != 0 || base->dtype != p->dtype)
+    throw Error(1, "kl_term: parameter sets have different architectures");  // policy.cpp:489-490
+  if (!p->ro_valid) throw Error(1, "no rollout");
+  if (p->dtype == DASHCU_F32) {
+    Engine<float> e(*p);
+    e.accumulate_kl(*base, seqs, coef, micro, kl);
+  } else {
+    Engine<bf16> e(*p);
+    e.accumulate_kl(*base, seqs, coef, micro, kl);
+  }
+}
+
+int dashcu_accumulate_kl(dashcu_policy* p, dashcu_policy* base, double coef, int32_t micro, const int32_t* subset,
+                         int32_t n_subset, double* kl_per_seq) {
+  API_BEGIN
+  check_policy(p);
+  std::vector<int> seqs;
+  if (subset) {
+    for (int i = 0; i < n_subset; ++i) {
+      if (subset[i] < 0 || subset[i] >= p->n_seq) throw Error(1, "subset index out of range");
+      seqs.push_back(subset[i]);
+    }
+  } else {
+    for (int s = 0; s < p->n_seq; ++s) seqs.push_back(s);
+  }
+  std::vector<double> kl;
+  kl_impl(p, base, coef, micro, seqs, &kl);
+  if (kl_per_seq) std::memcpy(kl_per_seq, kl.data(), sizeof(double) * kl.size());
+  API_END
+}
+
+// run_schedule over the current rollout + advantage batch.
+int dashcu_run_schedule(dashcu_policy* p, const dashcu_schedule* sc, const dashcu_opt* o, dashcu_policy* base,
+                        dashcu_step_log* logs, int32_t max_logs, int32_t* n_logs) {
+  API_BEGIN
+  check_policy(p);
+  if (!sc || !o) throw Error(1, "null schedule / optimizer config");
+  if (!p->adv_valid) throw Error(1, "call dashcu_rollout_advantage first");
+  if (sc->kind != DASHCU_SCHED_DASH && sc->kind != DASHCU_SCHED_MULTI && sc->kind != DASHCU_SCHED_MINI)
+    throw Error(1, "unknown schedule");
+  const int K = sc->kind == DASHCU_SCHED_DASH ? 1 : sc->K;
+  if (K < 1) throw Error(1, "K must be >= 1");
+  if (sc->beta < 0.0) throw Error(1, "beta must be >= 0");
+  if (sc->beta > 0.0 && !base) throw Error(1, "beta > 0 needs the base policy");
+  if (sc->kind == DASHCU_SCHED_MINI && p->n_seq % K != 0)
+    throw Error(1, "MINI requires the batch to divide into K mini-batches");  // UpdateConfig invariant
+  if (sc->kind != DASHCU_SCHED_DASH && p->ro_version != p->version)
+    throw Error(3, "schedule entry needs theta == theta_old (sample first)");
+  const double clip = sc->clip_eps > 0 ? sc->clip_eps : 0.2;
+  if (sc->kind != DASHCU_SCHED_DASH) {
+    const int rc = dashcu_rollout_snapshot(p);
+    if (rc) throw Error(rc, g_last_error);
+  }
+  int nl = 0;
+  double sum_abs = 0.0;
+  for (int32_t s : p->h_kidx) sum_abs += std::fabs(p->h_adv[s]);
+  const double mean_abs = p->h_kidx.empty() ? 0.0 : sum_abs / p->h_kidx.size();
+  const double filtered = 1.0 - static_cast<double>(p->h_kidx.size()) / std::max(p->n_seq, 1);
+  const int per = p->n_seq / K;
+  for (int k = 0; k < K; ++k) {
+    const auto t0 = std::chrono::steady_clock::now();
+    dashcu_step_log lg{};
+    DCU_CHECK(cudaMemsetAsync(p->g32.p, 0, p->lay.total * 4, p->ctx->stream));
+    std::vector<int32_t> mb;
+    const int32_t* subset = nullptr;
+    double scale = sc->weight_scale;
+    if (sc->kind == DASHCU_SCHED_MINI) {  // mini-batch k: sequences [k*per, (k+1)*per), mean over it
+      for (int s = k * per; s < (k + 1) * per; ++s) mb.push_back(s);
+      subset = mb.data();
+      scale *= K;
+    }
+    std::vector<int> item_set;  // the inner estimator's items (kept, within the mini-batch)
+    if (sc->kind == DASHCU_SCHED_DASH) {
+      std::vector<double> w;
+      for (int32_t s : p->h_kidx) item_set.push_back(s), w.push_back(p->h_adv[s] * scale);
+      if (p->ro_version != p->version)
+        throw Error(3, "policy changed since the rollout was sampled (on-policy PG needs theta == theta_old)");
+      Timer tm(p->ctx->stream);
+      dispatch(p, [&](auto& e) { p->st.loss_tokens = e.accumulate(item_set, w, sc->micro_batch); });
+      p->st.accumulate_ms = tm.stop_ms();
+    } else {
+      int32_t nc = 0;
+      ppo_impl(p, scale, clip, sc->micro_batch, subset, per, &lg.surrogate, &nc);
+      item_set = kept_subset(p, subset, per);
+      lg.clip_fraction = item_set.empty() ? 0.0 : static_cast<double>(nc) / item_set.size();
+    }
+    if (sc->beta > 0.0 && !item_set.empty()) {  // J = J_inner - beta KL: ascent adds -beta grad KL
+      std::vector<double> kl;
+      kl_impl(p, base, -sc->beta * scale, sc->micro_batch, item_set, &kl);
+      for (double v : kl) lg.kl += v * scale;
+    }
+    int rc = sc->sharded ? dashcu_sharded_step(p, o) : dashcu_allreduce_grads(p);
+    if (!rc && !sc->sharded) rc = dashcu_optimizer_step(p, o);
+    if (rc) throw Error(rc, g_last_error);
+    DCU_CHECK(cudaStreamSynchronize(p->ctx->stream));
+    lg.mean_abs_adv = mean_abs;
+    lg.filtered_fraction = filtered;
+    lg.n_items = static_cast<int32_t>(item_set.size());
+    lg.ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (logs && nl < max_logs) logs[nl] = lg;
+    ++nl;
+  }
+  if (n_logs) *n_logs = nl;
   API_END
 }
 

@@ -74,6 +74,9 @@ def oracle():
             L.dor_log_prob.restype = C.c_double
             L.dor_log_prob.argtypes = [C.POINTER(DorArch), f64p, i32p, C.c_int, i32p, C.c_int, f64p]
             L.dor_next_logits.argtypes = [C.POINTER(DorArch), f64p, i32p, C.c_int, f64p]
+            L.dor_kl_term_acc.argtypes = [C.POINTER(DorArch), f64p, f64p, i32p, C.c_int, i32p, C.c_int, C.c_double,
+                                          f64p]
+            L.dor_kl_term_acc.restype = C.c_double
             L.dor_grad_log_prob_acc.argtypes = [C.POINTER(DorArch), f64p, i32p, C.c_int, i32p, C.c_int,
                                                 C.c_double, f64p]
             L.dor_soft_logf.restype = C.c_float
@@ -128,6 +131,7 @@ def ref():
                                      f64p, i32p]
             L.ref_log_prob.argtypes = [i32p, f64p, i32p, C.c_int, i32p, C.c_int, f64p, f64p]
             L.ref_grad_log_prob.argtypes = [i32p, f64p, i32p, C.c_int, i32p, C.c_int, f64p]
+            L.ref_kl_term.argtypes = [i32p, f64p, f64p, i32p, C.c_int, i32p, C.c_int, f64p, f64p]
             L.ref_next_token_probs.argtypes = [i32p, f64p, i32p, C.c_int, f64p]
             L.ref_greedy_decode.argtypes = [i32p, f64p, i32p, C.c_int, C.c_int, i32p, i32p]
             L.ref_advantage.argtypes = [f64p, C.c_int, C.c_int, C.c_int, f64p]
@@ -200,6 +204,17 @@ def grad_log_prob(arch, params, prompt, completion, scale=1.0, grad=None):
     oracle().dor_grad_log_prob_acc(C.byref(a), ptr(params, f64p), ptr(p, i32p), len(p), ptr(c, i32p),
                                    len(c), scale, ptr(grad, f64p))
     return grad
+
+
+def kl_term(arch, params, base, prompt, completion, scale=1.0, grad=None):
+    """kl_term (policy.cpp:487-522) restated with GQA geometry: (value, grad += scale * dKL/dP)."""
+    a = arch_struct(arch)
+    p, c = i32(prompt), i32(completion)
+    if grad is None:
+        grad = np.zeros(num_params(arch), dtype=np.float64)
+    v = oracle().dor_kl_term_acc(C.byref(a), ptr(params, f64p), ptr(base, f64p), ptr(p, i32p), len(p), ptr(c, i32p),
+                                 len(c), scale, ptr(grad, f64p))
+    return v, grad
 
 
 def sample_rule(logits_f32: np.ndarray, bos: int, inv_t: float, seq_key: int, step: int) -> int:

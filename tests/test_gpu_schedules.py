@@ -1,0 +1,204 @@
+"""PPO surrogate, KL term, update schedules and interleaved sampling through the C ABI
+(policy.cpp:487-522), against the
+CPU oracle (oracle/dash_oracle.c, pinned to the reference's kl_term / grad_log_prob in
+test_oracle.py) and against the DASH path itself where the SPEC states an identity:
+
+  * PPO at theta == theta_old equals the PG gradient exactly;
+  * items on the clipped branch contribute nothing;
+  * MULTI with K = 1 equals DASH; MINI with K = 2 performs two updates on
+    disjoint halves;
+  * the KL gradient / value match the oracle, kl(params, params) = 0, beta = 0 is the
+    No-KL update;
+  * 32 interleaved micro-batch calls reproduce one preemptive call.
+"""
+import numpy as np
+import pytest
+
+import oracle_ffi as O
+import paper_2505_17218_b200 as D
+from test_gpu_parity import GQA, QWENLIKE, TOL, assert_grad_close, params32, rand_batch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return D.Context(0)
+
+
+def rollout(pol, arch, M=6, G=4, ML=10, seed=3):
+    rng = np.random.default_rng(seed)
+    prompts = [[0] + list(rng.integers(2, arch["vocab_size"], size=int(rng.integers(2, 6)))) for _ in range(M)]
+    ro = pol.sample(prompts, G, ML, round_seed=seed)
+    r = rng.integers(0, 2, size=M * G).astype(np.float64)
+    pol.set_rewards(r)
+    adv, kept, nk = pol.advantage(tau=0.1)
+    return prompts, ro, adv, kept
+
+
+@pytest.mark.parametrize("dtype", [D.F32, D.BF16])
+def test_ppo_at_entry_equals_pg(ctx, knob, dtype):
+    arch = QWENLIKE
+    pol = D.Policy(ctx, arch, dtype)
+    pol.upload(params32(arch, 0.3, 4))
+    prompts, ro, adv, kept = rollout(pol, arch)
+    N = len(adv)
+    knob("LSE_RECOMPUTE", 1)   # the PG side takes the same LSE pass as PPO's pass 1
+    pol.grad_zero()
+    pol.accumulate(1.0 / N, micro_batch=5)
+    g_pg = pol.grad()
+    pol.snapshot()
+    pol.grad_zero()
+    sur, nclip = pol.accumulate_ppo(1.0 / N, clip_eps=0.2, micro_batch=7)
+    g_ppo = pol.grad()
+    assert nclip == 0
+    assert np.array_equal(g_pg, g_ppo)
+    assert abs(sur - adv[kept].sum() / N) <= 1e-12 * max(1.0, np.abs(adv).sum())
+    pol.close()
+
+
+def test_ppo_off_policy_vs_oracle(ctx):
+    """After an update, rho != 1: gradient = sum_n A_n rho_n grad log pi on the unclipped
+    branch and 0 on the clipped one, against the oracle's fp64 restatement (F32 path)."""
+    arch = GQA
+    pol = D.Policy(ctx, arch, D.F32)
+    p_old = params32(arch, 0.3, 6)
+    pol.upload(p_old)
+    prompts, ro, adv, kept = rollout(pol, arch, M=8, G=4, ML=8, seed=5)
+    N = len(adv)
+    comps = [list(ro.completion(s)) for s in range(N)]
+    pol.snapshot()
+    old = pol.snapshot_logp()
+    ref_old = np.array([O.log_prob(arch, p_old, prompts[s // 4], comps[s])[0] for s in range(N)])
+    assert np.abs(old - ref_old).max() <= 1e-3 * max(1.0, np.abs(ref_old).max())
+    g = np.random.default_rng(2).standard_normal(len(p_old))
+    pol.grad_upload(g)
+    pol.optimizer_step(D.OPT_SGD, lr=0.02)   # move theta away from theta_old
+    p_new = pol.download()
+    eps = 0.2
+    pol.grad_zero()
+    sur, nclip = pol.accumulate_ppo(1.0 / N, clip_eps=eps, micro_batch=5)
+    got = pol.grad()
+    ref = np.zeros_like(got)
+    n_ref_clip, margin_ok = 0, True
+    for s in np.flatnonzero(kept):
+        new = O.log_prob(arch, p_new, prompts[s // 4], comps[s])[0]
+        rho = np.exp(new - ref_old[s])
+        a = adv[s]
+        clipped = (a > 0 and rho > 1 + eps) or (a < 0 and rho < 1 - eps)
+        margin_ok &= min(abs(rho - 1 - eps), abs(rho - 1 + eps)) > 1e-3
+        n_ref_clip += clipped
+        if not clipped:
+            O.grad_log_prob(arch, p_new, prompts[s // 4], comps[s], a * rho / N, ref)
+    assert margin_ok   # no item within rounding of the clip boundary for this seed
+    assert nclip == n_ref_clip and 0 < nclip < kept.sum()
+    assert_grad_close(arch, got, ref, TOL[D.F32])
+    pol.close()
+
+
+@pytest.mark.parametrize("dtype", [D.F32, D.BF16])
+def test_kl_term_vs_oracle(ctx, dtype):
+    arch = QWENLIKE
+    base = D.Policy(ctx, arch, dtype)
+    pol = D.Policy(ctx, arch, dtype)
+    pb = params32(arch, 0.3, 7)
+    pc = (pb + 0.01 * np.random.default_rng(3).standard_normal(len(pb))).astype(np.float32).astype(np.float64)
+    base.upload(pb)
+    pol.upload(pc)
+    prompts, comps = rand_batch(np.random.default_rng(8), arch, 3, 3, len_range=(1, 9))
+    pol.load_rollout(prompts, 3, comps)
+    pol.grad_zero()
+    kl = pol.accumulate_kl(base, 0.5, micro_batch=4)
+    got = pol.grad()
+    ref = np.zeros_like(got)
+    ref_kl = np.array([O.kl_term(arch, pc, pb, prompts[s // 3], comps[s], 0.5, ref)[0] for s in range(9)])
+    assert np.abs(kl - ref_kl).max() <= TOL[dtype] * max(1e-3, np.abs(ref_kl).max())
+    assert_grad_close(arch, got, ref, TOL[dtype])
+    # kl(params, params) = (0, 0)
+    pol.upload(pb)
+    pol.load_rollout(prompts, 3, comps)
+    pol.grad_zero()
+    kl0 = pol.accumulate_kl(base, 1.0, micro_batch=4)
+    assert np.abs(kl0).max() <= 1e-6 and np.abs(pol.grad()).max() <= 1e-6
+    pol.close()
+    base.close()
+
+
+def test_schedules(ctx, knob):
+    arch = GQA
+    knob("LSE_RECOMPUTE", 1)
+    p0 = params32(arch, 0.3, 9)
+    pols = [D.Policy(ctx, arch, D.F32) for _ in range(3)]
+    for p in pols:
+        p.upload(p0)
+    outs = []
+    for p in pols:
+        outs.append(rollout(p, arch, M=4, G=4, ML=8, seed=11))
+    N = 16
+    # DASH vs MULTI K=1: the same update
+    l_dash = pols[0].run_schedule(D.SCHED_DASH, weight_scale=1.0 / N, lr=1e-2)
+    l_multi = pols[1].run_schedule(D.SCHED_MULTI, K=1, weight_scale=1.0 / N, lr=1e-2)
+    assert len(l_dash) == 1 and len(l_multi) == 1
+    assert np.array_equal(pols[0].download(), pols[1].download())
+    # MINI K=2: two updates on disjoint halves (sequences 0-7, 8-15), each the PPO gradient of
+    # its half against the entry snapshot, equal to doing it by hand
+    l_mini = pols[2].run_schedule(D.SCHED_MINI, K=2, weight_scale=1.0 / N, lr=1e-2)
+    assert len(l_mini) == 2
+    kept = outs[2][3]
+    assert [l["n_items"] for l in l_mini] == [int(kept[:8].sum()), int(kept[8:].sum())]
+    hand = D.Policy(ctx, arch, D.F32)
+    hand.upload(p0)
+    rollout(hand, arch, M=4, G=4, ML=8, seed=11)
+    hand.snapshot()
+    for k in range(2):
+        hand.grad_zero()
+        hand.accumulate_ppo(2.0 / N, 0.2, 32, subset=np.arange(8 * k, 8 * k + 8))
+        hand.optimizer_step(D.OPT_ADAM, lr=1e-2)
+    assert np.array_equal(hand.download(), pols[2].download())
+    with pytest.raises(D.InputError):
+        pols[2].run_schedule(D.SCHED_MINI, K=3, weight_scale=1.0 / N)   # 16 % 3 != 0
+    with pytest.raises(D.OnPolicyViolation):
+        pols[2].run_schedule(D.SCHED_MULTI, K=2, weight_scale=1.0 / N)  # theta moved since sampling
+    for p in pols + [hand]:
+        p.close()
+
+
+def test_schedule_with_kl(ctx, knob):
+    """beta > 0 adds -beta * grad KL(base || current) over the same items; beta = 0 is DASH."""
+    arch = GQA
+    knob("LSE_RECOMPUTE", 1)
+    p0 = params32(arch, 0.3, 12)
+    base = D.Policy(ctx, arch, D.F32)
+    base.upload((p0 + 0.02 * np.random.default_rng(1).standard_normal(len(p0))).astype(np.float32))
+    a, b = D.Policy(ctx, arch, D.F32), D.Policy(ctx, arch, D.F32)
+    for p in (a, b):
+        p.upload(p0)
+    ra, rb = rollout(a, arch, seed=13), rollout(b, arch, seed=13)
+    N = 24
+    a.run_schedule(D.SCHED_DASH, weight_scale=1.0 / N, beta=0.04, base=base, opt_kind=D.OPT_SGD, lr=1.0)
+    # by hand: PG + (-0.04) * KL gradient over the kept items, then SGD with lr 1
+    kept_idx = np.flatnonzero(rb[3])
+    b.grad_zero()
+    b.accumulate(1.0 / N, micro_batch=32)
+    b.accumulate_kl(base, -0.04 / N, micro_batch=32, subset=kept_idx)
+    b.optimizer_step(D.OPT_SGD, lr=1.0)
+    assert np.abs(a.download() - b.download()).max() <= 1e-6
+    for p in (a, b, base):
+        p.close()
+
+
+def test_interleaved_calls_cover_the_preemptive_round(ctx):
+    """interleaved_sample: 32 calls of 2 prompts x G (prompt_index_base =
+    the micro-batch's first global prompt) == one preemptive call of 64 prompts x G."""
+    arch = QWENLIKE
+    pol = D.Policy(ctx, arch, D.BF16)
+    pol.upload(params32(arch, 0.3, 14))
+    rng = np.random.default_rng(15)
+    prompts = [[0] + list(rng.integers(2, arch["vocab_size"], size=5)) for _ in range(64)]
+    G = 4
+    full = pol.sample(prompts, G, 16, round_seed=21)
+    parts = [pol.sample(prompts[2 * i:2 * i + 2], G, 16, round_seed=21, prompt_index_base=2 * i) for i in range(32)]
+    assert np.array_equal(full.completions, np.concatenate([p.completions for p in parts]))
+    assert np.array_equal(full.lengths, np.concatenate([p.lengths for p in parts]))
+    assert sum(int(p.lengths.sum()) for p in parts) == int(full.lengths.sum())
+    pol.close()

@@ -398,3 +398,38 @@ def test_workload_restatement_matches_oracle():
     R = W.synthetic_rewards(3, 7, 20, 8)
     assert np.array_equal(R, [O.synthetic_reward(3, m, g) for m in range(7, 20) for g in range(8)])
     assert int(W.derive_seed(1, "sample", 2, 3)) == 3124241217676271300
+
+
+# ------------------------------------------------------------------- KL term
+
+@pytest.mark.ref
+def test_kl_term_matches_reference():
+    """dor_kl_term_acc (the GQA-capable restatement) == the reference's kl_term
+    (policy.cpp:487-522) at reference geometry; kl(params, params) = (0, 0)."""
+    arch = dict(vocab_size=11, embed_dim=8, context_len=20, ffn_hidden=12, n_layers=2, bos_id=0, eos_id=1)
+    p = O.init_params(arch, 0.4, 3)
+    b = p + 0.05 * np.random.default_rng(1).standard_normal(len(p))
+    prompt, comp = [0, 4, 5], [6, 7, 2, 9, 1]
+    v, g = O.kl_term(arch, p, b, prompt, comp)
+    rv, rg = C.c_double(0), np.zeros(len(p))
+    assert O.ref().ref_kl_term(O.arch_ref_vec(arch), O.ptr(p, O.f64p), O.ptr(b, O.f64p), O.i32(prompt).ctypes.data_as(O.i32p),
+                               3, O.i32(comp).ctypes.data_as(O.i32p), 5, C.byref(rv), O.ptr(rg, O.f64p)) == 0
+    assert abs(v - rv.value) <= 1e-12 * max(1, abs(v)) and v > 0
+    assert np.max(np.abs(g - rg)) <= 1e-12 * max(1, np.max(np.abs(rg)))
+    v0, g0 = O.kl_term(arch, p, p, prompt, comp)
+    assert abs(v0) <= 1e-12 and np.max(np.abs(g0)) <= 1e-12
+
+
+def test_kl_term_gqa_finite_differences():
+    arch = dict(vocab_size=9, embed_dim=8, context_len=16, ffn_hidden=6, n_layers=1, bos_id=0, eos_id=1,
+                n_heads=2, n_kv_heads=1, head_dim=4)
+    rng = np.random.default_rng(2)
+    p = O.init_params(arch, 0.5, 5)
+    b = p + 0.1 * rng.standard_normal(len(p))
+    prompt, comp = [0, 3, 4], [5, 2, 7]
+    _, g = O.kl_term(arch, p, b, prompt, comp)
+    for i in rng.choice(len(p), 25, replace=False):
+        e = np.zeros(len(p))
+        e[i] = 1e-5
+        fd = (O.kl_term(arch, p + e, b, prompt, comp)[0] - O.kl_term(arch, p - e, b, prompt, comp)[0]) / 2e-5
+        assert abs(fd - g[i]) <= 1e-4 * max(1e-3, abs(fd)), (i, fd, g[i])
