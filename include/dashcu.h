@@ -253,6 +253,18 @@ DASHCU_API int dashcu_sharded_step(dashcu_policy* pol, const dashcu_opt* opt);
  * step (no device work). */
 DASHCU_API int dashcu_shard_span(int64_t total, int32_t world, int32_t rank, int64_t* off, int64_t* len);
 
+/* ---- checkpoint container ----
+ * Flat named-tensor file: "DASHCKPT", version 1, the dashcu_arch descriptor, tensor count,
+ * flags (bit 0: Adam state), Adam step count, the reference's content_hash
+ * (tensors.cpp:95-107), then per tensor {name, shape, row-major f64 data} in the views()
+ * order and names of tensors.cpp:49-71, optionally followed by "adam.m" / "adam.v". Save
+ * writes the fp32 master weights exactly (as f64); load checks the architecture, names,
+ * shapes and hash (InputError otherwise), restores the master + bf16 copy (and, with
+ * with_optimizer, the Adam moments and step count) and bumps the policy version. */
+DASHCU_API int dashcu_policy_save(dashcu_policy* pol, const char* path, int32_t with_optimizer);
+DASHCU_API int dashcu_policy_load(dashcu_policy* pol, const char* path, int32_t with_optimizer);
+DASHCU_API int dashcu_checkpoint_arch(const char* path, dashcu_arch* out);
+
 DASHCU_API int dashcu_get_stats(dashcu_policy* pol, dashcu_stats* out);
 
 /* ---- kernel-class profiler (bench.py roofline) ----

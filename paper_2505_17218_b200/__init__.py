@@ -158,6 +158,9 @@ def lib():
             "dashcu_shard_span": [C.c_int64, C.c_int32, C.c_int32, i64p, i64p],
             "dashcu_get_stats": [vp, C.POINTER(Stats)],
             "dashcu_rollout_snapshot": [vp],
+            "dashcu_policy_save": [vp, C.c_char_p, C.c_int32],
+            "dashcu_policy_load": [vp, C.c_char_p, C.c_int32],
+            "dashcu_checkpoint_arch": [C.c_char_p, C.POINTER(Arch)],
             "dashcu_rollout_snapshot_logp": [vp, f64p, C.c_int32],
             "dashcu_accumulate_ppo": [vp, C.c_double, C.c_double, C.c_int32, i32p, C.c_int32, f64p, i32p],
             "dashcu_accumulate_kl": [vp, vp, C.c_double, C.c_int32, i32p, C.c_int32, f64p],
@@ -303,6 +306,13 @@ def task_rewards(kind: int, difficulty: int, seeds, group_size: int, completions
     return out[:lens.shape[0]]
 
 
+def checkpoint_arch(path: str) -> dict:
+    """The architecture descriptor in a DASHCKPT file's header (no device work)."""
+    a = Arch()
+    _check(lib().dashcu_checkpoint_arch(os.fsencode(path), C.byref(a)))
+    return {f: getattr(a, f) for f, _ in Arch._fields_}
+
+
 def num_params(arch: dict) -> int:
     n = C.c_int64(0)
     a = Arch.of(arch)
@@ -406,6 +416,13 @@ class Policy:
         out = np.zeros(self.n_params)
         _check(lib().dashcu_policy_download(self.h, _p(out, f64p), self.n_params))
         return out
+
+    def save(self, path: str, with_optimizer: bool = True):
+        """Checkpoint container (dashcu_policy_save)."""
+        _check(lib().dashcu_policy_save(self.h, os.fsencode(path), int(with_optimizer)))
+
+    def load(self, path: str, with_optimizer: bool = True):
+        _check(lib().dashcu_policy_load(self.h, os.fsencode(path), int(with_optimizer)))
 
     def init_normal(self, scale: float, seed: int):
         _check(lib().dashcu_policy_init_normal(self.h, scale, seed))

@@ -1932,6 +1932,219 @@ int dashcu_sharded_step(dashcu_policy* p, const dashcu_opt* o) {
   API_END
 }
 
+// ------------------------------------------------------------------ checkpoint container
+// SPEC.md:100 "flat named-tensor container (name -> shape -> row-major 64-bit floats), with
+// the architecture descriptor in a header". Layout (little endian):
+//   "DASHCKPT" | u32 version=1 | i32 arch[10] (dashcu_arch) | u32 n_tensors | u32 flags
+//   (bit 0: Adam state follows) | i64 adam_t | u64 content_hash
+//   n_tensors x { u16 name_len | name | u8 ndim | u64 dims[ndim] | f64 data[prod dims] }
+// Tensors are the views() order and names of tensors.cpp:49-71 ("token_embed",
+// "pos_embed", "layers.<l>.wq" .. "layers.<l>.b2", "w_out", "b_out"); with flag bit 0 the
+// Adam moments follow as two flat tensors "adam.m" / "adam.v". content_hash is the
+// reference's ParamTensors::content_hash (tensors.cpp:95-107: FNV-1a over the 7-int
+// ArchConfig then every parameter's f64 bytes in views() order); a GQA geometry hashes
+// all 10 arch ints.
+namespace dashcu {
+namespace {
+struct TensorSpec {
+  std::string name;
+  std::vector<int64_t> dims;
+  int64_t off;
+};
+std::vector<TensorSpec> tensor_specs(const Geo& g, const Lay& l) {
+  std::vector<TensorSpec> t;
+  t.push_back({"token_embed", {g.V, g.d}, l.tok});
+  t.push_back({"pos_embed", {g.ctx, g.d}, l.pos});
+  for (int i = 0; i < g.L; ++i) {
+    const std::string pre = "layers." + std::to_string(i) + ".";
+    const int64_t b = l.layer0 + static_cast<int64_t>(i) * l.lstride;
+    t.push_back({pre + "wq", {g.qd, g.d}, b + l.wq});
+    t.push_back({pre + "wk", {g.kvd, g.d}, b + l.wk});
+    t.push_back({pre + "wv", {g.kvd, g.d}, b + l.wv});
+    t.push_back({pre + "wo", {g.d, g.qd}, b + l.wo});
+    t.push_back({pre + "w1", {g.H, g.d}, b + l.w1});
+    t.push_back({pre + "b1", {g.H}, b + l.b1});
+    t.push_back({pre + "w2", {g.d, g.H}, b + l.w2});
+    t.push_back({pre + "b2", {g.d}, b + l.b2});
+  }
+  t.push_back({"w_out", {g.V, g.d}, l.wout});
+  t.push_back({"b_out", {g.V}, l.bout});
+  return t;
+}
+bool reference_geometry(const dashcu_arch& a) {
+  const Geo g = geo_of(a);
+  return g.nh == 1 && g.nkv == 1 && g.hd == g.d;
+}
+uint64_t fnv_mix(uint64_t h, const void* bytes, size_t n) {
+  const unsigned char* q = static_cast<const unsigned char*>(bytes);
+  for (size_t i = 0; i < n; ++i) {
+    h ^= q[i];
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+uint64_t content_hash(const dashcu_arch& a, const std::vector<double>& flat) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  h = fnv_mix(h, &a, reference_geometry(a) ? 7 * sizeof(int32_t) : sizeof(dashcu_arch));
+  return fnv_mix(h, flat.data(), flat.size() * sizeof(double));
+}
+constexpr char kMagic[8] = {'D', 'A', 'S', 'H', 'C', 'K', 'P', 'T'};
+struct File {
+  FILE* f;
+  explicit File(const char* path, const char* mode) : f(path ? fopen(path, mode) : nullptr) {
+    if (!f) throw Error(1, std::string("cannot open checkpoint ") + (path ? path : "(null)"));
+  }
+  ~File() {
+    if (f) fclose(f);
+  }
+  void put(const void* p, size_t n) {
+    if (fwrite(p, 1, n, f) != n) throw Error(4, "checkpoint write failed");
+  }
+  void get(void* p, size_t n) {
+    if (fread(p, 1, n, f) != n) throw Error(1, "checkpoint truncated");
+  }
+};
+void read_header(File& F, dashcu_arch* a, uint32_t* nt, uint32_t* flags, int64_t* t, uint64_t* hash) {
+  char m[8];
+  uint32_t ver = 0;
+  F.get(m, 8);
+  if (std::memcmp(m, kMagic, 8) != 0) throw Error(1, "not a DASHCKPT checkpoint");
+  F.get(&ver, 4);
+  if (ver != 1) throw Error(1, "unsupported checkpoint version " + std::to_string(ver));
+  F.get(a, sizeof(dashcu_arch));
+  F.get(nt, 4);
+  F.get(flags, 4);
+  F.get(t, 8);
+  F.get(hash, 8);
+}
+}  // namespace
+}  // namespace dashcu
+
+int dashcu_checkpoint_arch(const char* path, dashcu_arch* out) {
+  API_BEGIN
+  if (!out) throw Error(1, "null argument");
+  File F(path, "rb");
+  uint32_t nt, flags;
+  int64_t t;
+  uint64_t h;
+  read_header(F, out, &nt, &flags, &t, &h);
+  API_END
+}
+
+int dashcu_policy_save(dashcu_policy* p, const char* path, int32_t with_optimizer) {
+  API_BEGIN
+  check_policy(p);
+  const int64_t n = p->lay.total;
+  std::vector<double> flat(n);
+  {
+    double* stg = p->ws.get<double>("staging64", n);
+    f32_to_f64(p->ctx->stream, p->w32.as<float>(), stg, n);
+    d2h(p->ctx->stream, flat.data(), stg, n);
+    DCU_CHECK(cudaStreamSynchronize(p->ctx->stream));
+  }
+  const bool opt = with_optimizer && p->opt_state == 0;
+  if (with_optimizer && p->opt_state == 1)
+    throw Error(1, "optimizer state is sharded across ranks: save without it");
+  File F(path, "wb");
+  F.put(kMagic, 8);
+  const uint32_t ver = 1;
+  F.put(&ver, 4);
+  F.put(&p->arch, sizeof(dashcu_arch));
+  const std::vector<TensorSpec> specs = tensor_specs(p->g, p->lay);
+  const uint32_t nt = static_cast<uint32_t>(specs.size() + (opt ? 2 : 0)), flags = opt ? 1u : 0u;
+  F.put(&nt, 4);
+  F.put(&flags, 4);
+  F.put(&p->adam_t, 8);
+  const uint64_t h = content_hash(p->arch, flat);
+  F.put(&h, 8);
+  auto put_tensor = [&](const std::string& name, const std::vector<int64_t>& dims, const double* data) {
+    const uint16_t nl = static_cast<uint16_t>(name.size());
+    const uint8_t nd = static_cast<uint8_t>(dims.size());
+    F.put(&nl, 2);
+    F.put(name.data(), nl);
+    F.put(&nd, 1);
+    int64_t cnt = 1;
+    for (int64_t dd : dims) {
+      const uint64_t u = static_cast<uint64_t>(dd);
+      F.put(&u, 8);
+      cnt *= dd;
+    }
+    F.put(data, sizeof(double) * cnt);
+  };
+  for (const TensorSpec& t : specs) put_tensor(t.name, t.dims, flat.data() + t.off);
+  if (opt) {
+    for (int which = 0; which < 2; ++which) {
+      double* stg = p->ws.get<double>("staging64", n);
+      f32_to_f64(p->ctx->stream, (which ? p->av : p->am).as<float>(), stg, n);
+      d2h(p->ctx->stream, flat.data(), stg, n);
+      DCU_CHECK(cudaStreamSynchronize(p->ctx->stream));
+      put_tensor(which ? "adam.v" : "adam.m", {n}, flat.data());
+    }
+  }
+  API_END
+}
+
+int dashcu_policy_load(dashcu_policy* p, const char* path, int32_t with_optimizer) {
+  API_BEGIN
+  check_policy(p);
+  File F(path, "rb");
+  dashcu_arch a;
+  uint32_t nt, flags;
+  int64_t adam_t;
+  uint64_t hash;
+  read_header(F, &a, &nt, &flags, &adam_t, &hash);
+  if (std::memcmp(&a, &p->arch, sizeof(dashcu_arch)) != 0)
+    throw Error(1, "checkpoint architecture differs from the policy's");
+  const std::vector<TensorSpec> specs = tensor_specs(p->g, p->lay);
+  const bool opt = flags & 1u;
+  if (nt != specs.size() + (opt ? 2 : 0)) throw Error(1, "checkpoint tensor count mismatch");
+  const int64_t n = p->lay.total;
+  std::vector<double> flat(n), m, v;
+  auto get_tensor = [&](const std::string& name, const std::vector<int64_t>& dims, double* data) {
+    uint16_t nl = 0;
+    uint8_t nd = 0;
+    F.get(&nl, 2);
+    std::string got(nl, '\0');
+    F.get(&got[0], nl);
+    if (got != name) throw Error(1, "checkpoint tensor " + got + " where " + name + " was expected");
+    F.get(&nd, 1);
+    if (nd != dims.size()) throw Error(1, "checkpoint tensor " + name + " has the wrong rank");
+    int64_t cnt = 1;
+    for (int64_t dd : dims) {
+      uint64_t u = 0;
+      F.get(&u, 8);
+      if (static_cast<int64_t>(u) != dd) throw Error(1, "checkpoint tensor " + name + " has the wrong shape");
+      cnt *= dd;
+    }
+    F.get(data, sizeof(double) * cnt);
+  };
+  for (const TensorSpec& t : specs) get_tensor(t.name, t.dims, flat.data() + t.off);
+  if (content_hash(a, flat) != hash) throw Error(1, "checkpoint content hash mismatch (corrupted file)");
+  if (opt && with_optimizer) {
+    m.resize(n);
+    v.resize(n);
+    get_tensor("adam.m", {n}, m.data());
+    get_tensor("adam.v", {n}, v.data());
+  }
+  cudaStream_t s = p->ctx->stream;
+  double* stg = p->ws.get<double>("staging64", n);
+  h2d(s, stg, flat.data(), n);
+  f64_to_f32(s, stg, p->w32.as<float>(), n);
+  refresh_working_copy(p);
+  if (opt && with_optimizer) {
+    ensure_moments(p, n, 0);
+    h2d(s, stg, m.data(), n);
+    f64_to_f32(s, stg, p->am.as<float>(), n);
+    DCU_CHECK(cudaStreamSynchronize(s));
+    h2d(s, stg, v.data(), n);
+    f64_to_f32(s, stg, p->av.as<float>(), n);
+    p->adam_t = adam_t;
+  }
+  DCU_CHECK(cudaStreamSynchronize(s));
+  ++p->version;
+  API_END
+}
+
 int dashcu_get_stats(dashcu_policy* p, dashcu_stats* out) {
   API_BEGIN
   check_policy(p);
