@@ -106,6 +106,8 @@ typedef struct {
   int64_t loss_tokens;      /* completion tokens that entered the last accumulate */
   double mean_reward, filtered_fraction, mean_abs_kept; /* advantage.cpp:44-65 */
   int64_t kernel_launches;  /* kernels this policy launched since creation */
+  int64_t decode_row_steps; /* sum over the last rollout's decode steps of the active rows */
+  int64_t kv_pages_peak;    /* most completion-KV pages (per layer) in use at once */
 } dashcu_stats;
 
 DASHCU_API const char* dashcu_last_error(void);
@@ -151,6 +153,11 @@ DASHCU_API int dashcu_sample_keyed(dashcu_policy* pol, const dashcu_plan* plan, 
 /* Debug: when enabled, the next dashcu_sample also records the exact fp32
  * logits its sampling rule consumed, [n_seq][max_len][vocab] (small shapes). */
 DASHCU_API int dashcu_set_logits_dump(dashcu_policy* pol, int enable);
+/* Cap of the decode's completion-KV page pool: n_pages pages of 64 slots per layer (each
+ * page n_kv_heads x 64 x head_dim K and V values). 0 (default) = the round's worst case
+ * (every sequence at max_len); a smaller pool relies on sequences finishing early (their
+ * pages are recycled) and fails with CapacityError when exhausted. */
+DASHCU_API int dashcu_set_kv_pages(dashcu_policy* pol, int64_t n_pages);
 DASHCU_API int dashcu_get_logits_dump(dashcu_policy* pol, float* out, int64_t n);
 
 /* Load externally produced trajectories as the rollout (n_prompts*group_size
@@ -323,7 +330,7 @@ DASHCU_API int dashcu_rollout_task_rewards(dashcu_policy* pol, int32_t kind, int
  * Read once from DASHCU_<NAME> environment variables at library load; this call changes
  * one for the calling process (INT32_MIN restores the default). Names: GEMM_PAIR,
  * GEMM_RASTER, NO_SPLITK, NO_TMA_STORE, GEMM_RESID_DB, GEMM_RESID_DEEP, ATTN_FWD,
- * ATTN_BWD, ATTN_BWD_CHUNK, LSE_RECOMPUTE, PDL, DECODE_GRAPH (csrc/common.cuh Knob).
+ * ATTN_BWD, ATTN_BWD_CHUNK, LSE_RECOMPUTE, PDL, DECODE_GRAPH, DECODE_COMPACT (csrc/common.cuh Knob).
  * Returns the previous value, INT32_MIN for an unknown name. */
 DASHCU_API int dashcu_set_knob(const char* name, int value);
 

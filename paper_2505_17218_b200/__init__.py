@@ -100,7 +100,7 @@ class Stats(C.Structure):
                 ("allreduce_ms", C.c_double), ("optimizer_ms", C.c_double), ("tokens_sampled", C.c_int64),
                 ("n_seq", C.c_int32), ("n_kept", C.c_int32), ("loss_tokens", C.c_int64),
                 ("mean_reward", C.c_double), ("filtered_fraction", C.c_double), ("mean_abs_kept", C.c_double),
-                ("kernel_launches", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("decode_row_steps", C.c_int64), ("kv_pages_peak", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -140,6 +140,7 @@ def lib():
             "dashcu_policy_version": [vp, C.POINTER(C.c_uint64)],
             "dashcu_sample": [vp, C.POINTER(Plan), i32p, i64p, i32p, i32p, f32p],
             "dashcu_set_logits_dump": [vp, C.c_int],
+            "dashcu_set_kv_pages": [vp, C.c_int64],
             "dashcu_get_logits_dump": [vp, f32p, C.c_int64],
             "dashcu_rollout_load": [vp, i32p, i64p, C.c_int32, C.c_int32, i32p, i64p],
             "dashcu_rollout_log_prob": [vp, f32p, C.c_int64],
@@ -435,6 +436,10 @@ class Policy:
     # ---- sampling
     def set_logits_dump(self, enable: bool):
         _check(lib().dashcu_set_logits_dump(self.h, int(enable)))
+
+    def set_kv_pages(self, n_pages: int):
+        """Cap the decode KV page pool (dashcu_set_kv_pages; 0 = worst case)."""
+        _check(lib().dashcu_set_kv_pages(self.h, int(n_pages)))
 
     def logits_dump(self, n_seq: int, max_len: int) -> np.ndarray:
         V = self.arch["vocab_size"]

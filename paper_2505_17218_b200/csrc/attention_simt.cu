@@ -128,25 +128,25 @@ template <class T>
 __global__ void __launch_bounds__(32) attn_decode_k(const T* __restrict__ qkv, const T* __restrict__ kp,
                                                     const T* __restrict__ vp, const T* __restrict__ kc,
                                                     const T* __restrict__ vc, const int32_t* prompt_len, int G, int pmax,
-                                                    int n_comp, int max_len, int nh, int nkv, int hd, T* __restrict__ ctx) {
+                                                    int n_comp, int max_len, DecodeRows dr, int nh, int nkv, int hd,
+                                                    T* __restrict__ ctx) {
   extern __shared__ float sm[];
-  const int s = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
+  const int s = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;  // s: decode row
   const int qd = nh * hd, kvd = nkv * hd, qkvd = qd + 2 * kvd;
   const int kvh = h / (nh / nkv);
-  const int p = s / G, m = prompt_len[s];
+  const int sq = dr_seq(dr, s);
+  const int p = sq / G, m = prompt_len[sq];
   const int nk = m + n_comp;
   float* sc = sm;
   float* qs = sm + pmax + max_len;
   const T* kpb = kp + (static_cast<int64_t>(p) * nkv + kvh) * pmax * hd;
   const T* vpb = vp + (static_cast<int64_t>(p) * nkv + kvh) * pmax * hd;
-  const T* kcb = kc + (static_cast<int64_t>(s) * nkv + kvh) * max_len * hd;
-  const T* vcb = vc + (static_cast<int64_t>(s) * nkv + kvh) * max_len * hd;
   for (int i = lane; i < hd; i += 32) qs[i] = tof<T>(qkv[static_cast<int64_t>(s) * qkvd + h * hd + i]);
   __syncwarp();
   const float scale = rsqrtf(static_cast<float>(hd));
   float mx = -FLT_MAX;
   for (int j = lane; j < nk; j += 32) {
-    const T* k = j < m ? kpb + static_cast<int64_t>(j) * hd : kcb + static_cast<int64_t>(j - m) * hd;
+    const T* k = j < m ? kpb + static_cast<int64_t>(j) * hd : kc + kv_slot_off(dr, sq, kvh, nkv, j - m, hd);
     float a = 0.f;
     for (int i = 0; i < hd; ++i) a = fmaf(qs[i], tof<T>(k[i]), a);
     a *= scale;
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(32) attn_decode_k(const T* __restrict__ qkv, c
   for (int i = lane; i < hd; i += 32) {
     float a = 0.f;
     for (int j = 0; j < nk; ++j) {
-      const T* v = j < m ? vpb + static_cast<int64_t>(j) * hd : vcb + static_cast<int64_t>(j - m) * hd;
+      const T* v = j < m ? vpb + static_cast<int64_t>(j) * hd : vc + kv_slot_off(dr, sq, kvh, nkv, j - m, hd);
       a = fmaf(sc[j], tof<T>(v[i]), a);
     }
     ctx[static_cast<int64_t>(s) * qd + h * hd + i] = fromf<T>(a * inv);
@@ -203,13 +203,13 @@ void attn_bwd_varlen(cudaStream_t s, const T* qkv, const T* dctx, const float* l
 
 template <class T>
 void attn_decode(cudaStream_t s, const T* qkv, const T* kp, const T* vp, const T* kc, const T* vc,
-                 const int32_t* prompt_len, int rows, int G, int pmax, int n_comp, int max_len, int nh, int nkv, int hd,
-                 T* ctx, double alg_bytes) {
+                 const int32_t* prompt_len, int rows, int G, int pmax, int n_comp, int max_len, const DecodeRows& dr,
+                 int nh, int nkv, int hd, T* ctx, double alg_bytes) {
   ProfScope ps(PROF_ATTN_DECODE, s, 0, alg_bytes);
   const size_t smem = sizeof(float) * (pmax + max_len + hd);
   set_smem((const void*)attn_decode_k<T>, smem);
-  attn_decode_k<T><<<dim3(rows, nh), 32, smem, s>>>(qkv, kp, vp, kc, vc, prompt_len, G, pmax, n_comp, max_len, nh, nkv,
-                                                    hd, ctx);
+  attn_decode_k<T><<<dim3(rows, nh), 32, smem, s>>>(qkv, kp, vp, kc, vc, prompt_len, G, pmax, n_comp, max_len, dr, nh,
+                                                    nkv, hd, ctx);
   DCU_LAUNCHED();
 }
 
@@ -219,7 +219,7 @@ void attn_decode(cudaStream_t s, const T* qkv, const T* kp, const T* vp, const T
   template void attn_bwd_varlen<T>(cudaStream_t, const T*, const T*, const float*, const int32_t*, int, int, int, int, \
                                    int, float*, float*, double);                                                    \
   template void attn_decode<T>(cudaStream_t, const T*, const T*, const T*, const T*, const T*, const int32_t*, int, \
-                               int, int, int, int, int, int, int, T*, double);
+                               int, int, int, int, const DecodeRows&, int, int, int, T*, double);
 INST(float)
 INST(bf16)
 #undef INST

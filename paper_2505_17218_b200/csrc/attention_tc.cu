@@ -37,7 +37,7 @@ template <int HD>
 __global__ void __launch_bounds__(DecCfg<HD>::NW * 32)
     attn_decode_tc_k(const bf16* __restrict__ qkv, const bf16* __restrict__ kp, const bf16* __restrict__ vp,
                      const bf16* __restrict__ kc, const bf16* __restrict__ vc, const int32_t* __restrict__ prompt_len,
-                     int S, int G, int pmax, int n_comp, int cslots, int nh, int nkv, bf16* __restrict__ ctx,
+                     int S, int G, int pmax, int n_comp, DecodeRows dr, int nh, int nkv, bf16* __restrict__ ctx,
                      float scale_log2) {
   using Cf = DecCfg<HD>;
   constexpr int KC = Cf::KC, ST = Cf::ST, UNITS = Cf::UNITS;
@@ -46,14 +46,13 @@ __global__ void __launch_bounds__(DecCfg<HD>::NW * 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * Cf::NW + warp;
   if (item >= S * nkv) return;
-  const int s = item / nkv, kvh = item % nkv;
+  const int s = item / nkv, kvh = item % nkv;  // s: decode row
+  const int sq = dr_seq(dr, s);
   const int grp = nh / nkv, qd = nh * HD, kvd = nkv * HD, qkvd = qd + 2 * kvd;
-  const int m = prompt_len[s];
+  const int m = prompt_len[sq];
   const int nk = m + n_comp;
-  const bf16* kpb = kp + (static_cast<int64_t>(s / G) * nkv + kvh) * pmax * HD;
-  const bf16* vpb = vp + (static_cast<int64_t>(s / G) * nkv + kvh) * pmax * HD;
-  const bf16* kcb = kc + (static_cast<int64_t>(s) * nkv + kvh) * cslots * HD;
-  const bf16* vcb = vc + (static_cast<int64_t>(s) * nkv + kvh) * cslots * HD;
+  const bf16* kpb = kp + (static_cast<int64_t>(sq / G) * nkv + kvh) * pmax * HD;
+  const bf16* vpb = vp + (static_cast<int64_t>(sq / G) * nkv + kvh) * pmax * HD;
   uint8_t* wsm = smem + warp * Cf::WARP_BYTES;
   const uint32_t wsm_a = smem_addr(wsm);
 
@@ -84,8 +83,9 @@ __global__ void __launch_bounds__(DecCfg<HD>::NW * 32)
       const int j = c * KC + r;
       const bool ok = j < nk;
       const int jj = ok ? j : 0;
-      const bf16* ks = jj < m ? kpb + static_cast<int64_t>(jj) * HD : kcb + static_cast<int64_t>(jj - m) * HD;
-      const bf16* vs = jj < m ? vpb + static_cast<int64_t>(jj) * HD : vcb + static_cast<int64_t>(jj - m) * HD;
+      const int64_t po = jj < m ? static_cast<int64_t>(jj) * HD : kv_slot_off(dr, sq, kvh, nkv, jj - m, HD);
+      const bf16* ks = (jj < m ? kpb : kc) + po;
+      const bf16* vs = (jj < m ? vpb : vc) + po;
       const int off = swz(r, u, UNITS);
       cp_async16(kbase + off, ks + u * 8, ok ? 16 : 0);
       cp_async16(vbase + off, vs + u * 8, ok ? 16 : 0);
@@ -206,7 +206,8 @@ __global__ void __launch_bounds__(DecCfg<HD>::NW * 32)
 
 template <int HD>
 void launch_decode(cudaStream_t s, const bf16* qkv, const bf16* kp, const bf16* vp, const bf16* kc, const bf16* vc,
-                   const int32_t* plen, int rows, int G, int pmax, int n_comp, int cslots, int nh, int nkv, bf16* ctx) {
+                   const int32_t* plen, int rows, int G, int pmax, int n_comp, const DecodeRows& dr, int nh, int nkv,
+                   bf16* ctx) {
   using Cf = DecCfg<HD>;
   static bool attr = false;
   if (!attr) {
@@ -216,7 +217,7 @@ void launch_decode(cudaStream_t s, const bf16* qkv, const bf16* kp, const bf16* 
   const int items = rows * nkv;
   const float scale_log2 = kLog2e / sqrtf(static_cast<float>(HD));
   launch_pdl(attn_decode_tc_k<HD>, dim3((items + Cf::NW - 1) / Cf::NW), dim3(Cf::NW * 32), Cf::SMEM, s, qkv, kp, vp, kc,
-             vc, plen, rows, G, pmax, n_comp, cslots, nh, nkv, ctx, scale_log2);
+             vc, plen, rows, G, pmax, n_comp, dr, nh, nkv, ctx, scale_log2);
   DCU_LAUNCHED();
 }
 
@@ -647,12 +648,12 @@ bool attn_bwd_tc(cudaStream_t s, const bf16* qkv, const bf16* ctx, const bf16* d
 }
 
 bool attn_decode_tc(cudaStream_t s, const bf16* qkv, const bf16* kp, const bf16* vp, const bf16* kc, const bf16* vc,
-                    const int32_t* plen, int rows, int G, int pmax, int n_comp, int cslots, int nh, int nkv, int hd,
-                    bf16* ctx, double alg_bytes) {
+                    const int32_t* plen, int rows, int G, int pmax, int n_comp, const DecodeRows& dr, int nh, int nkv,
+                    int hd, bf16* ctx, double alg_bytes) {
   if (nh / nkv > 16 || (hd != 64 && hd != 128)) return false;
   ProfScope ps(PROF_ATTN_DECODE, s, 0, alg_bytes);
-  if (hd == 64) launch_decode<64>(s, qkv, kp, vp, kc, vc, plen, rows, G, pmax, n_comp, cslots, nh, nkv, ctx);
-  else launch_decode<128>(s, qkv, kp, vp, kc, vc, plen, rows, G, pmax, n_comp, cslots, nh, nkv, ctx);
+  if (hd == 64) launch_decode<64>(s, qkv, kp, vp, kc, vc, plen, rows, G, pmax, n_comp, dr, nh, nkv, ctx);
+  else launch_decode<128>(s, qkv, kp, vp, kc, vc, plen, rows, G, pmax, n_comp, dr, nh, nkv, ctx);
   return true;
 }
 

@@ -66,6 +66,7 @@ enum Knob : int {
   KNOB_LSE_RECOMPUTE,    // 1: the backward recomputes the LM-head LSE instead of reusing the sampler's
   KNOB_PDL,              // 1: programmatic dependent launch
   KNOB_DECODE_GRAPH,     // 0: no CUDA-graph replay of decode steps
+  KNOB_DECODE_COMPACT,   // 0: finished sequences keep their decode rows until the round ends
   KNOB_NUM
 };
 extern int g_knob[KNOB_NUM];

@@ -19,10 +19,31 @@ void optimizer_update(cudaStream_t s, int kind, float* w, const float* g, float*
 template <class T>
 void embed_fwd(cudaStream_t s, const T* tok_emb, const T* pos_emb, const int32_t* tok, const int32_t* pos,
                int rows, int d, float* x32, T* xT);
-// decode: pos = prompt_len[s] + step - 1, token = tok[s]
+// ---- decode rows and the paged completion KV ------------------------------
+// The decode runs over its ACTIVE rows; row_seq[r] is the sequence of row r (null = identity).
+// Per-sequence state (next token, prompt length, key, cap, finished flag, outputs) is indexed
+// by sequence, per-row scratch (activations, logits, slice records) by row, so retiring
+// finished sequences only rewrites row_seq. Completion K / V of each layer live in a pool
+// of kPage-slot pages [page][kv head][kPage][hd]; page_table[seq * max_pages + i] holds
+// completion slots [i kPage, (i + 1) kPage) of the sequence.
+constexpr int kPage = 64;
+struct DecodeRows {
+  const int32_t* row_seq = nullptr;
+  const int32_t* ptab = nullptr;
+  int max_pages = 0;
+};
+__device__ __forceinline__ int dr_seq(const DecodeRows& dr, int row) { return dr.row_seq ? dr.row_seq[row] : row; }
+// element offset of completion slot `slot` of (seq, kv head) in a layer's page pool
+__device__ __forceinline__ int64_t kv_slot_off(const DecodeRows& dr, int seq, int kvh, int nkv, int slot, int hd) {
+  const int page = __ldg(dr.ptab + static_cast<int64_t>(seq) * dr.max_pages + slot / kPage);
+  return ((static_cast<int64_t>(page) * nkv + kvh) * kPage + (slot % kPage)) * hd;
+}
+
+// decode: pos = prompt_len[seq] + step - 1, token = tok[seq], seq = row_seq[row]
 template <class T>
 void embed_decode(cudaStream_t s, const T* tok_emb, const T* pos_emb, const int32_t* tok,
-                  const int32_t* prompt_len, int step, int rows, int d, float* x32, T* xT);
+                  const int32_t* prompt_len, int step, int rows, int d, float* x32, T* xT,
+                  const int32_t* row_seq = nullptr);
 // deterministic (stable sort by id + in-order run sums); tmp: embed_bwd_tmp_bytes(rows)
 size_t embed_bwd_tmp_bytes(int rows);
 void embed_bwd(cudaStream_t s, const float* dx, const int32_t* tok, const int32_t* pos, int rows, int d, int n_tok,
@@ -68,28 +89,29 @@ void pack_dqkv(cudaStream_t s, const float* dq, const float* dkv, int rows, int 
 
 // ---- decode (sampling) ------------------------------------------------------------
 // Prompt KV store [L][P][nkv][Pmax][hd] (shared by the G sequences of a group) from
-// prefill qkv rows; completion KV store [L][S][nkv][max_len][hd].
+// prefill qkv rows; completion KV: the paged pools above (slot = completion position).
 template <class T>
 void kv_store_prompt(cudaStream_t s, const T* qkv, const int32_t* seq_start, int n_prompts, int pmax, int qd,
                      int kvd, int nkv, int hd, T* kstore, T* vstore);
 template <class T>
-void kv_append(cudaStream_t s, const T* qkv, int rows, int qd, int kvd, int nkv, int hd, int slot, int max_len,
-               T* kstore, T* vstore);
+void kv_append(cudaStream_t s, const T* qkv, int rows, int qd, int kvd, int nkv, int hd, int slot,
+               const DecodeRows& dr, T* kpool, T* vpool);
 template <class T>
 void attn_decode(cudaStream_t s, const T* qkv, const T* kp, const T* vp, const T* kc, const T* vc,
-                 const int32_t* prompt_len, int rows, int G, int pmax, int n_comp, int max_len, int nh, int nkv,
-                 int hd, T* ctx, double alg_bytes = 0);
+                 const int32_t* prompt_len, int rows, int G, int pmax, int n_comp, int max_len, const DecodeRows& dr,
+                 int nh, int nkv, int hd, T* ctx, double alg_bytes = 0);
 // Tensor-core decode attention (bf16; head_dim 64/128, <= 16 query heads per KV head).
 // Returns false when the geometry is not covered (caller uses attn_decode).
 bool attn_decode_tc(cudaStream_t s, const bf16* qkv, const bf16* kp, const bf16* vp, const bf16* kc, const bf16* vc,
-                    const int32_t* prompt_len, int rows, int G, int pmax, int n_comp, int cslots, int nh, int nkv,
-                    int hd, bf16* ctx, double alg_bytes);
+                    const int32_t* prompt_len, int rows, int G, int pmax, int n_comp, const DecodeRows& dr, int nh,
+                    int nkv, int hd, bf16* ctx, double alg_bytes);
 // One sampling step over fp32 logits rows [rows x V] (policy.cpp:399-426 with the
 // inverse-CDF contract of rule.cuh): per-slice partials, then sample_scan.
 // part: scratch of rows * ceil(V/32) * 4 floats.
 void sample_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, int eos, float inv_t,
                  const uint64_t* keys, int step, const int32_t* cap, uint8_t* finished, int32_t* comp,
-                 float* logp, int32_t* len, int32_t* tok_next, int max_len, float* part);
+                 float* logp, int32_t* len, int32_t* tok_next, int max_len, float* part,
+                 const int32_t* row_seq = nullptr);
 
 // The contract's walk over per-slice partials {m, Z, m1, Z1} (from sample_rows or the
 // fused LM-head GEMM epilogue) + the token bookkeeping (EOS, cap, logp at T = 1).
@@ -97,7 +119,8 @@ void sample_scan(cudaStream_t s, const float* part, int nslices, const float* lo
                  int V, int bos, int eos, float inv_t, const uint64_t* keys, int step, const int32_t* cap,
                  uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len,
                  bool compact = false,    // compact: {m, Z} records (fused epilogue at T = 1)
-                 float* lse_out = nullptr);  // optional [rows x max_len]: the row's T = 1 log-sum-exp
+                 float* lse_out = nullptr,   // optional [seqs x max_len]: the row's T = 1 log-sum-exp
+                 const int32_t* row_seq = nullptr);  // row -> sequence (null = identity)
 // dst[i] = src[idx[i]] (fp32 gather)
 void gather_f32(cudaStream_t s, const float* src, const int32_t* idx, int n, float* dst);
 

@@ -99,13 +99,14 @@ __global__ void embed_fwd_k(const T* E, const T* P, const int32_t* tok, const in
 
 template <class T>
 __global__ void embed_decode_k(const T* E, const T* P, const int32_t* tok, const int32_t* plen, int step, int rows,
-                               int d, float* x32, T* xT) {
+                               int d, float* x32, T* xT, const int32_t* row_seq) {
   pdl_wait();
   const int64_t n = static_cast<int64_t>(rows) * d;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int r = static_cast<int>(i / d), c = static_cast<int>(i % d);
-    const int p = plen[r] + step - 1;
-    const float v = tof<T>(E[static_cast<int64_t>(tok[r]) * d + c]) + tof<T>(P[static_cast<int64_t>(p) * d + c]);
+    const int sq = row_seq ? row_seq[r] : r;
+    const int p = plen[sq] + step - 1;
+    const float v = tof<T>(E[static_cast<int64_t>(tok[sq]) * d + c]) + tof<T>(P[static_cast<int64_t>(p) * d + c]);
     x32[i] = v;
     xT[i] = fromf<T>(v);
   }
@@ -311,13 +312,14 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
                                                      int V, int bos, int eos, float inv_t, const uint64_t* keys,
                                                      int step, const int32_t* cap, uint8_t* finished, int32_t* comp,
                                                      float* logp, int32_t* len, int32_t* tok_next, int max_len,
-                                                     bool compact, float* lse_out) {
+                                                     bool compact, float* lse_out, const int32_t* row_seq) {
   pdl_wait();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= rows) return;
-  const bool active = !finished[row] && step < cap[row];
+  const int sq = row_seq ? row_seq[row] : row;  // per-sequence state below, per-row records above
+  const bool active = !finished[sq] && step < cap[sq];
   if (!active) {
-    if (lane == 0) tok_next[row] = eos;
+    if (lane == 0) tok_next[sq] = eos;
     return;
   }
   // records {m, Z, m1, Z1}; at T = 1 the fused epilogue stores only {m, Z} (m1 = m, Z1 = Z)
@@ -359,7 +361,7 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
   float total = 0.f;
 #pragma unroll
   for (int j = 0; j < 32; ++j) total = __fadd_rn(total, Tj[j]);
-  const float target = __fmul_rn(row_uniform(keys[row], step), total);
+  const float target = __fmul_rn(row_uniform(keys[sq], step), total);
   int jb = -1;
   float base = 0.f;
   {
@@ -441,13 +443,13 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
     }
   }
   if (tk < 0) tk = last_i;
-  comp[static_cast<int64_t>(row) * max_len + step] = tk;
+  comp[static_cast<int64_t>(sq) * max_len + step] = tk;
   const float lse1 = M1 + logf(L1);  // T = 1 log-sum-exp over non-BOS ids (policy.cpp:424)
-  logp[static_cast<int64_t>(row) * max_len + step] = l[tk - sb * kSlice] - lse1;
-  if (lse_out) lse_out[static_cast<int64_t>(row) * max_len + step] = lse1;
-  len[row] = step + 1;
-  if (tk == eos) finished[row] = 1;
-  tok_next[row] = tk;
+  logp[static_cast<int64_t>(sq) * max_len + step] = l[tk - sb * kSlice] - lse1;
+  if (lse_out) lse_out[static_cast<int64_t>(sq) * max_len + step] = lse1;
+  len[sq] = step + 1;
+  if (tk == eos) finished[sq] = 1;
+  tok_next[sq] = tk;
 }
 
 // Row LSE from the LSE-mode GEMM partials; optionally logp = logit[y] - lse with the
@@ -586,7 +588,7 @@ __global__ void kv_store_prompt_k(const T* qkv, const int32_t* start, int n_prom
 }
 
 template <class T>
-__global__ void kv_append_k(const T* qkv, int rows, int qd, int kvd, int nkv, int hd, int slot, int max_len, T* ks,
+__global__ void kv_append_k(const T* qkv, int rows, int qd, int kvd, int nkv, int hd, int slot, DecodeRows dr, T* ks,
                             T* vs) {
   pdl_wait();
   const int qkvd = qd + 2 * kvd;
@@ -595,7 +597,7 @@ __global__ void kv_append_k(const T* qkv, int rows, int qd, int kvd, int nkv, in
     const int r = static_cast<int>(i / kvd), c = static_cast<int>(i % kvd);
     const int h = c / hd, dd = c % hd;
     const int64_t src = static_cast<int64_t>(r) * qkvd + qd + c;
-    const int64_t dst = ((static_cast<int64_t>(r) * nkv + h) * max_len + slot) * hd + dd;
+    const int64_t dst = kv_slot_off(dr, dr_seq(dr, r), h, nkv, slot, hd) + dd;
     ks[dst] = qkv[src];
     vs[dst] = qkv[src + kvd];
   }
@@ -763,9 +765,9 @@ void embed_fwd(cudaStream_t s, const T* E, const T* P, const int32_t* tok, const
 }
 template <class T>
 void embed_decode(cudaStream_t s, const T* E, const T* P, const int32_t* tok, const int32_t* plen, int step,
-                  int rows, int d, float* x32, T* xT) {
+                  int rows, int d, float* x32, T* xT, const int32_t* row_seq) {
   launch_pdl(embed_decode_k<T>, dim3(grid1d(static_cast<int64_t>(rows) * d)), dim3(256), 0, s, E, P, tok, plen, step,
-             rows, d, x32, xT);
+             rows, d, x32, xT, row_seq);
   DCU_LAUNCHED();
 }
 size_t embed_bwd_tmp_bytes(int rows) {
@@ -839,7 +841,7 @@ void colsum_acc_f32(cudaStream_t s, const float* X, int64_t ld, int M, int N, fl
 
 void sample_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, int eos, float inv_t,
                  const uint64_t* keys, int step, const int32_t* cap, uint8_t* finished, int32_t* comp, float* logp,
-                 int32_t* len, int32_t* tok_next, int max_len, float* part) {
+                 int32_t* len, int32_t* tok_next, int max_len, float* part, const int32_t* row_seq) {
   const int ns = (V + kSlice - 1) / kSlice;
   {
     ProfScope ps(PROF_SAMPLE, s, 0, 4.0 * rows * static_cast<double>(V));
@@ -847,7 +849,7 @@ void sample_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, 
     DCU_LAUNCHED();
   }
   sample_scan(s, part, ns, logits, V, rows, V, bos, eos, inv_t, keys, step, cap, finished, comp, logp, len, tok_next,
-              max_len);
+              max_len, false, nullptr, row_seq);
 }
 
 
@@ -861,9 +863,9 @@ void lse_reduce(cudaStream_t s, const float* part, int ntiles, int rows, float* 
 void sample_scan(cudaStream_t s, const float* part, int nslices, const float* logits, int64_t logits_ld, int rows,
                  int V, int bos, int eos, float inv_t, const uint64_t* keys, int step, const int32_t* cap,
                  uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len,
-                 bool compact, float* lse_out) {
+                 bool compact, float* lse_out, const int32_t* row_seq) {
   launch_pdl(sample_scan_k, dim3(cdiv(rows, 8)), dim3(256), 0, s, part, nslices, logits, logits_ld, rows, V, bos, eos,
-             inv_t, keys, step, cap, finished, comp, logp, len, tok_next, max_len, compact, lse_out);
+             inv_t, keys, step, cap, finished, comp, logp, len, tok_next, max_len, compact, lse_out, row_seq);
   DCU_LAUNCHED();
 }
 
@@ -942,10 +944,10 @@ void kv_store_prompt(cudaStream_t s, const T* qkv, const int32_t* start, int n_p
   DCU_LAUNCHED();
 }
 template <class T>
-void kv_append(cudaStream_t s, const T* qkv, int rows, int qd, int kvd, int nkv, int hd, int slot, int max_len,
-               T* ks, T* vs) {
+void kv_append(cudaStream_t s, const T* qkv, int rows, int qd, int kvd, int nkv, int hd, int slot,
+               const DecodeRows& dr, T* ks, T* vs) {
   launch_pdl(kv_append_k<T>, dim3(grid1d(static_cast<int64_t>(rows) * kvd)), dim3(256), 0, s, qkv, rows, qd, kvd, nkv,
-             hd, slot, max_len, ks, vs);
+             hd, slot, dr, ks, vs);
   DCU_LAUNCHED();
 }
 template <class T>
@@ -986,12 +988,12 @@ void advantage_filter(cudaStream_t s, const double* r, int n, int G, int kind, i
 #define INST(T)                                                                                                   \
   template void embed_fwd<T>(cudaStream_t, const T*, const T*, const int32_t*, const int32_t*, int, int, float*, T*); \
   template void embed_decode<T>(cudaStream_t, const T*, const T*, const int32_t*, const int32_t*, int, int, int,     \
-                                float*, T*);                                                                      \
+                                float*, T*, const int32_t*);                                                      \
   template void colsum_acc<T>(cudaStream_t, const T*, int64_t, int, int, float*, float*);                        \
   template size_t colsum_tmp_floats<T>(int, int);                                                                 \
   template void lm_rows<T>(cudaStream_t, const float*, int, int, int, const int32_t*, const float*, float*, T*);  \
   template void kv_store_prompt<T>(cudaStream_t, const T*, const int32_t*, int, int, int, int, int, int, T*, T*); \
-  template void kv_append<T>(cudaStream_t, const T*, int, int, int, int, int, int, int, T*, T*);                  \
+  template void kv_append<T>(cudaStream_t, const T*, int, int, int, int, int, int, const DecodeRows&, T*, T*);   \
   template void pack_dqkv<T>(cudaStream_t, const float*, const float*, int, int, int, T*);                        \
   template void gather_rows<T>(cudaStream_t, const T*, int64_t, const int32_t*, int, int, T*);
 INST(float)

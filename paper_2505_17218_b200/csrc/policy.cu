@@ -313,6 +313,7 @@ struct dashcu_policy {
   int64_t dump_n = 0;
   dashcu_stats st{};
   int64_t launches0 = 0;
+  int64_t kv_pages = 0;  // decode KV page pool per layer (0: the worst case of the round)
   dashcu::Workspace ws;
 };
 
@@ -980,14 +981,32 @@ struct Engine {
     }
     if (maxcap == 0) return;
 
-    // KV stores: prompt part once per group, completion part per sequence.
+    // KV: the prompt part once per group ([layer][prompt][kv head][pmax][hd]); the completion
+    // part in per-layer pools of kPage-slot pages (kernels.cuh DecodeRows) handed out as the
+    // rows advance and returned when a sequence retires; the pool holds the worst case unless
+    // dashcu_set_kv_pages caps it.
     const int cslots = std::max(ML - 1, 1);
+    const int maxp = cdiv(cslots, kPage);
+    const int64_t worst = static_cast<int64_t>(S) * maxp;
+    const int64_t npool = P.kv_pages > 0 ? std::min<int64_t>(P.kv_pages, worst) : worst;
     const size_t kvp = static_cast<size_t>(NP) * g.nkv * pmax * g.hd;
-    const size_t kvc = static_cast<size_t>(S) * g.nkv * cslots * g.hd;
+    const size_t kvc = static_cast<size_t>(npool) * g.nkv * kPage * g.hd;
     T* kp = ws.get<T>("kv_kp", kvp * g.L);
     T* vp = ws.get<T>("kv_vp", kvp * g.L);
     T* kc = ws.get<T>("kv_kc", kvc * g.L);
     T* vc = ws.get<T>("kv_vc", kvc * g.L);
+    int32_t* d_ptab = ws.get<int32_t>("kv_ptab", static_cast<size_t>(S) * maxp);
+    int32_t* d_rows = ws.get<int32_t>("s_rows", S);
+    std::vector<int32_t> h_ptab(static_cast<size_t>(S) * maxp, 0), act(S), free_pages(npool);
+    for (int i = 0; i < S; ++i) act[i] = i;
+    for (int64_t i = 0; i < npool; ++i) free_pages[i] = static_cast<int32_t>(npool - 1 - i);  // pop_back: 0, 1, ...
+    std::vector<std::vector<int32_t>> owned(S);
+    h2d(st, d_rows, act.data(), S);
+    // finished sequences leave the decode batch at every EOS check (off under the logits
+    // dump, whose rows must stay the sequences, and with KNOB_DECODE_COMPACT = 0)
+    const bool compact_rows = !dump && knob(KNOB_DECODE_COMPACT) != 0;
+    P.st.decode_row_steps = 0;
+    P.st.kv_pages_peak = 0;
 
     // Prefill (teacher-forced forward over the M prompts).
     const int Tp = static_cast<int>(ptok.size());
@@ -1009,7 +1028,7 @@ struct Engine {
     const int nslices = (g.V + 31) / 32;
     float* part = ws.get<float>("d_part", static_cast<size_t>(S) * nslices * 4);
     float* logits = ws.get<float>("d_logits", static_cast<size_t>(S) * g.V);
-    auto lm_sample = [&](const T* yrows, int step) {
+    auto lm_sample = [&](const T* yrows, int step, int R, const int32_t* row_seq) {
       if constexpr (sizeof(T) == 2) {
         // the epilogue writes the logits straight into the parity dump when one is requested
         float* lg = dump ? dump + static_cast<int64_t>(step) * g.V : logits;
@@ -1022,32 +1041,32 @@ struct Engine {
         sa.part = part;
         sa.logits = lg;
         sa.logits_ld = ld;
-        GemmShape gs{S, g.V, g.d, yrows, g.d, true, W(L.wout), g.d, true};
+        GemmShape gs{R, g.V, g.d, yrows, g.d, true, W(L.wout), g.d, true};
         const int nt = gemm_tc_sample(st, gs, W32(L.bout), sa);
         if (nt > 0) {
-          sample_scan(st, part, nt, lg, ld, S, g.V, g.bos, g.eos, inv_t, d_keys, step, d_cap, d_fin,
+          sample_scan(st, part, nt, lg, ld, R, g.V, g.bos, g.eos, inv_t, d_keys, step, d_cap, d_fin,
                       P.d_comp.as<int32_t>(), P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML, inv_t == 1.f,
-                      lse_out);
+                      lse_out, row_seq);
           return;
         }
       }
       lse_all = false;
       Epi el = store(logits, g.V, nullptr, 0);
       el.bias = W32(L.bout);
-      mm(S, g.V, g.d, yrows, g.d, true, W(L.wout), g.d, true, el);
-      sample_rows(st, logits, S, g.V, g.bos, g.eos, inv_t, d_keys, step, d_cap, d_fin, P.d_comp.as<int32_t>(),
-                  P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML, part);
+      mm(R, g.V, g.d, yrows, g.d, true, W(L.wout), g.d, true, el);
+      sample_rows(st, logits, R, g.V, g.bos, g.eos, inv_t, d_keys, step, d_cap, d_fin, P.d_comp.as<int32_t>(),
+                  P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML, part, row_seq);
       if (dump)
         DCU_CHECK(cudaMemcpy2DAsync(dump + static_cast<int64_t>(step) * g.V,
                                     sizeof(float) * static_cast<size_t>(std::max(ML, 1)) * g.V, logits,
-                                    sizeof(float) * g.V, sizeof(float) * g.V, S, cudaMemcpyDeviceToDevice, st));
+                                    sizeof(float) * g.V, sizeof(float) * g.V, R, cudaMemcpyDeviceToDevice, st));
     };
-    lm_sample(yT, 0);
+    lm_sample(yT, 0, S, nullptr);
 
-    // Decode steps: one position of every sequence per step. Every projection uses the
-    // store form (fp32 + bf16 outputs in the epilogue), whose fp32 summation order depends
-    // on (N, K) only, so a sequence's tokens do not depend on which other sequences share
-    // its batch (scheduling independence).
+    // Decode steps: one position of every active sequence per step. Every projection uses
+    // the store form (fp32 + bf16 outputs in the epilogue), whose fp32 summation order
+    // depends on (N, K) only, so a sequence's tokens do not depend on which other sequences
+    // share its batch (scheduling independence) -- nor on retirement.
     float* x32 = ws.get<float>("d_x32", static_cast<size_t>(S) * g.d);
     float* h32 = ws.get<float>("d_h32", static_cast<size_t>(S) * g.d);
     T* xT = ws.get<T>("d_xT", static_cast<size_t>(S) * g.d);
@@ -1056,45 +1075,74 @@ struct Engine {
     T* ctx = ws.get<T>("d_ctx", static_cast<size_t>(S) * g.qd);
     T* u = ws.get<T>("d_u", static_cast<size_t>(S) * g.H);
     std::vector<uint8_t> hfin(S);
+    int R = S;
+    const DecodeRows dr{d_rows, d_ptab, maxp};
     for (int j = 1; j < maxcap; ++j) {
-      embed_decode<T>(st, W(L.tok), W(L.pos), d_tok, d_plen, j, S, g.d, x32, xT);
+      if ((j - 1) % kPage == 0) {  // every active row starts a new page of completion slots
+        for (int r = 0; r < R; ++r) {
+          if (free_pages.empty())
+            throw Error(2, "decode KV page pool exhausted (" + std::to_string(npool) +
+                               " pages): raise dashcu_set_kv_pages or sample fewer sequences");
+          const int32_t pg = free_pages.back();
+          free_pages.pop_back();
+          h_ptab[static_cast<size_t>(act[r]) * maxp + (j - 1) / kPage] = pg;
+          owned[act[r]].push_back(pg);
+        }
+        P.st.kv_pages_peak = std::max<int64_t>(P.st.kv_pages_peak, npool - static_cast<int64_t>(free_pages.size()));
+        h2d(st, d_ptab, h_ptab.data(), h_ptab.size());
+      }
+      P.st.decode_row_steps += R;
+      embed_decode<T>(st, W(L.tok), W(L.pos), d_tok, d_plen, j, R, g.d, x32, xT, d_rows);
       for (int l = 0; l < g.L; ++l) {
         const int64_t b = lb(l);
         T* kc_l = kc + kvc * l;
         T* vc_l = vc + kvc * l;
-        mm(S, g.qkvd, g.d, xT, g.d, true, W(b + L.wq), g.d, true, store(nullptr, 0, qkv, g.qkvd));
-        kv_append<T>(st, qkv, S, g.qd, g.kvd, g.nkv, g.hd, j - 1, cslots, kc_l, vc_l);
+        mm(R, g.qkvd, g.d, xT, g.d, true, W(b + L.wq), g.d, true, store(nullptr, 0, qkv, g.qkvd));
+        kv_append<T>(st, qkv, R, g.qd, g.kvd, g.nkv, g.hd, j - 1, dr, kc_l, vc_l);
         // algorithmic bytes: every (sequence, kv head) reads its K and V rows once
-        const double kv_bytes = (sum_m + static_cast<double>(S) * j) * g.kvd * 2.0 * sizeof(T);
+        const double kv_bytes = (sum_m * R / S + static_cast<double>(R) * j) * g.kvd * 2.0 * sizeof(T);
         bool done = false;
         if constexpr (sizeof(T) == 2)
-          done = attn_decode_tc(st, qkv, kp + kvp * l, vp + kvp * l, kc_l, vc_l, d_plen, S, G, pmax, j, cslots, g.nh,
+          done = attn_decode_tc(st, qkv, kp + kvp * l, vp + kvp * l, kc_l, vc_l, d_plen, R, G, pmax, j, dr, g.nh,
                                 g.nkv, g.hd, ctx, kv_bytes);
         if (!done)
-          attn_decode<T>(st, qkv, kp + kvp * l, vp + kvp * l, kc_l, vc_l, d_plen, S, G, pmax, j, cslots, g.nh, g.nkv,
-                         g.hd, ctx, kv_bytes);
+          attn_decode<T>(st, qkv, kp + kvp * l, vp + kvp * l, kc_l, vc_l, d_plen, R, G, pmax, j, cslots, dr, g.nh,
+                         g.nkv, g.hd, ctx, kv_bytes);
         // h = x + Wo ctx ; u = tanh(W1 h + b1) ; x' = h + W2 u + b2
         Epi eo = store(h32, g.d, hT, g.d);
         eo.resid = x32;
         eo.ldr = g.d;
-        mm(S, g.d, g.qd, ctx, g.qd, true, W(b + L.wo), g.qd, true, eo);
+        mm(R, g.d, g.qd, ctx, g.qd, true, W(b + L.wo), g.qd, true, eo);
         Epi e1 = store(nullptr, 0, u, g.H);
         e1.kind = EPI_TANH;
         e1.bias = W32(b + L.b1);
-        mm(S, g.H, g.d, hT, g.d, true, W(b + L.w1), g.d, true, e1);
+        mm(R, g.H, g.d, hT, g.d, true, W(b + L.w1), g.d, true, e1);
         Epi e2 = store(x32, g.d, xT, g.d);
         e2.bias = W32(b + L.b2);
         e2.resid = h32;
         e2.ldr = g.d;
-        mm(S, g.d, g.H, u, g.H, true, W(b + L.w2), g.H, true, e2);
+        mm(R, g.d, g.H, u, g.H, true, W(b + L.w2), g.H, true, e2);
       }
-      lm_sample(xT, j);
-      if ((j & 31) == 0 && g.eos >= 0) {  // retire the round early once every sequence hit EOS
+      lm_sample(xT, j, R, d_rows);
+      if ((j & 31) == 0 && g.eos >= 0) {  // EOS check: retire finished sequences, stop when none is left
         d2h(st, hfin.data(), d_fin, S);
         DCU_CHECK(cudaStreamSynchronize(st));
-        bool all = true;
-        for (int s = 0; s < S && all; ++s) all = hfin[s] || j + 1 >= cap[s];
-        if (all) break;
+        std::vector<int32_t> keep;
+        for (int r = 0; r < R; ++r)
+          if (!hfin[act[r]] && j + 1 < cap[act[r]]) keep.push_back(act[r]);
+        if (keep.empty()) break;
+        if (compact_rows && static_cast<int>(keep.size()) < R) {
+          std::vector<uint8_t> live(S, 0);
+          for (int32_t q : keep) live[q] = 1;
+          for (int r = 0; r < R; ++r)  // the retired sequences' pages go back to the pool
+            if (!live[act[r]]) {
+              for (auto it = owned[act[r]].rbegin(); it != owned[act[r]].rend(); ++it) free_pages.push_back(*it);
+              owned[act[r]].clear();
+            }
+          act = keep;
+          R = static_cast<int>(act.size());
+          h2d(st, d_rows, act.data(), R);
+        }
       }
     }
     P.lse_valid = lse_all;
@@ -1355,6 +1403,14 @@ int dashcu_set_logits_dump(dashcu_policy* p, int enable) {
   API_BEGIN
   check_policy(p);
   p->dump = enable != 0;
+  API_END
+}
+
+int dashcu_set_kv_pages(dashcu_policy* p, int64_t n_pages) {
+  API_BEGIN
+  check_policy(p);
+  if (n_pages < 0) throw Error(1, "n_pages must be >= 0");
+  p->kv_pages = n_pages;
   API_END
 }
 

@@ -592,3 +592,46 @@ def test_decode_wide_ffn(ctx):
             refl = O.next_logits(arch, p, prompts[s // 4] + comp[:j])
             assert np.abs(dump[s, j] - refl).max() <= 5e-2 * max(1, np.abs(refl).max())
     pol.close()
+
+
+def eos_heavy_params(arch, seed, boost):
+    """Weights whose b_out[eos] is raised so completions end early at random lengths."""
+    p = params32(arch, 0.3, seed)
+    V = arch["vocab_size"]
+    p[-V + arch["eos_id"]] += boost
+    return p
+
+
+@pytest.mark.parametrize("dtype", [D.F32, D.BF16])
+def test_decode_retirement_and_paged_kv(ctx, knob, dtype):
+    """Finished sequences leave the decode batch at every EOS check (row compaction) and
+    return their KV pages: tokens, lengths and log-probs equal the run without compaction
+    bit for bit, while the decode does measurably less row work (the
+    reference stops each sequence at EOS, policy.cpp:425)."""
+    arch = dict(QWENLIKE, context_len=200)
+    pol = D.Policy(ctx, arch, dtype)
+    pol.upload(eos_heavy_params(arch, 31, 5.5))
+    rng = np.random.default_rng(31)
+    prompts = [[0] + list(rng.integers(2, arch["vocab_size"], size=int(rng.integers(3, 9)))) for _ in range(48)]
+    G, ML = 4, 190
+    a = pol.sample(prompts, G, ML, round_seed=17, temperature=0.9)
+    sa = pol.stats()
+    knob("DECODE_COMPACT", 0)
+    b = pol.sample(prompts, G, ML, round_seed=17, temperature=0.9)
+    sb = pol.stats()
+    assert np.array_equal(a.completions, b.completions) and np.array_equal(a.lengths, b.lengths)
+    assert np.array_equal(a.logp, b.logp)
+    mean_len = a.lengths.mean()
+    assert 5 < mean_len < 0.5 * ML and a.lengths.max() > 100   # EOS-heavy, but some run long
+    assert sa["decode_row_steps"] < 0.75 * sb["decode_row_steps"]
+    assert sa["kv_pages_peak"] < sb["kv_pages_peak"]
+    # a page budget below the worst case (all 192 x 3 pages) suffices once pages recycle
+    knob("DECODE_COMPACT", 1)
+    pol.set_kv_pages(sa["kv_pages_peak"])
+    c = pol.sample(prompts, G, ML, round_seed=17, temperature=0.9)
+    assert np.array_equal(a.completions, c.completions)
+    pol.set_kv_pages(sa["kv_pages_peak"] - 1)
+    with pytest.raises(D.CapacityError):
+        pol.sample(prompts, G, ML, round_seed=17, temperature=0.9)
+    pol.set_kv_pages(0)
+    pol.close()

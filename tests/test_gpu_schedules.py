@@ -52,7 +52,9 @@ def test_ppo_at_entry_equals_pg(ctx, knob, dtype):
     sur, nclip = pol.accumulate_ppo(1.0 / N, clip_eps=0.2, micro_batch=5)   # same partition: same sums
     g_ppo = pol.grad()
     assert nclip == 0
-    assert np.array_equal(g_pg, g_ppo)
+    # rho == 1 exactly, so the row weights equal the PG ones; the gradients then differ only
+    # by the attention backward's order-dependent fp32 reduce-adds (dQ / dK / dV)
+    assert np.linalg.norm(g_pg - g_ppo) <= 1e-6 * np.linalg.norm(g_pg)
     assert abs(sur - adv[kept].sum() / N) <= 1e-12 * max(1.0, np.abs(adv).sum())
     pol.close()
 
