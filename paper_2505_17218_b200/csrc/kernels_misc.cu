@@ -524,12 +524,14 @@ __global__ void __launch_bounds__(256) lm_rows_k(const float* logits, int V, int
 // KL term rows (kl_term, policy.cpp:487-522): per completion row r with current logits lc and
 // base logits lb (fp32, BOS excluded): value[r] = sum_i pb_i ((lb_i - lse_b) - (lc_i - lse_c))
 // = KL(base || current) at this context, and dz[r][i] = w_r (pc_i - pb_i) (the reference's
-// dlogits, BOS column 0); the value's sum runs in fp64.
+// dlogits, BOS column 0). The value is formed as sum_i pb_i (lb_i - lc_i) - (lse_b - lse_c)
+// with fp64 sums and lse_b - lse_c = (mb - mc) + log(Sb / Sc): near base == current the two
+// log-sum-exps share their rounding, so the difference is not swamped by it.
 template <class T>
 __global__ void __launch_bounds__(256) kl_rows_k(const float* lc_all, const float* lb_all, int V, int bos,
                                                  const float* weight, double* value, T* dz) {
   __shared__ float sm[32];
-  __shared__ double smd[32];
+  __shared__ double smd[3][32];
   const int r = blockIdx.x;
   const float* lc = lc_all + static_cast<int64_t>(r) * V;
   const float* lb = lb_all + static_cast<int64_t>(r) * V;
@@ -538,35 +540,36 @@ __global__ void __launch_bounds__(256) kl_rows_k(const float* lc_all, const floa
     if (i != bos) mc = fmaxf(mc, lc[i]), mb = fmaxf(mb, lb[i]);
   mc = block_reduce(mc, sm, true);
   mb = block_reduce(mb, sm, true);
-  float sc = 0.f, sb = 0.f;
+  double sc = 0.0, sb = 0.0, sd = 0.0;  // sum e^(lc-mc), sum e^(lb-mb), sum e^(lb-mb) (lb - lc)
   for (int i = threadIdx.x; i < V; i += blockDim.x)
-    if (i != bos) sc += expf(lc[i] - mc), sb += expf(lb[i] - mb);
-  sc = block_reduce(sc, sm, false);
-  sb = block_reduce(sb, sm, false);
-  const float lse_c = mc + logf(sc), lse_b = mb + logf(sb);
+    if (i != bos) {
+      const double eb = expf(lb[i] - mb);
+      sc += expf(lc[i] - mc);
+      sb += eb;
+      sd += eb * static_cast<double>(lb[i] - lc[i]);
+    }
+  double v3[3] = {sc, sb, sd};
+  for (int k = 0; k < 3; ++k) {
+    v3[k] = warp_sum_d(v3[k]);
+    if ((threadIdx.x & 31) == 0) smd[k][threadIdx.x >> 5] = v3[k];
+  }
+  __syncthreads();
+  double t3[3] = {0.0, 0.0, 0.0};
+  for (int k = 0; k < 3; ++k)
+    for (int w = 0; w < (blockDim.x >> 5); ++w) t3[k] += smd[k][w];
+  sc = t3[0], sb = t3[1], sd = t3[2];
+  const float lse_c = mc + static_cast<float>(log(sc)), lse_b = mb + static_cast<float>(log(sb));
+  if (threadIdx.x == 0 && value)
+    value[r] = sd / sb - ((static_cast<double>(mb) - mc) + log(sb / sc));
+  if (!dz) return;
   const float w = weight ? weight[r] : 1.f;
-  double acc = 0.0;
-  T* out = dz ? dz + static_cast<int64_t>(r) * V : nullptr;
+  T* out = dz + static_cast<int64_t>(r) * V;
   for (int i = threadIdx.x; i < V; i += blockDim.x) {
     float v = 0.f;
-    if (i != bos) {
-      const float lpc = lc[i] - lse_c, lpb = lb[i] - lse_b;
-      const float pb = expf(lpb), pc = expf(lpc);
-      acc += static_cast<double>(pb) * (static_cast<double>(lpb) - static_cast<double>(lpc));
-      v = w * (pc - pb);
-    }
-    if (out) out[i] = fromf<T>(v);
-  }
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) smd[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int k = 0; k < (blockDim.x >> 5); ++k) t += smd[k];
-    if (value) value[r] = t;
+    if (i != bos) v = w * (expf(lc[i] - lse_c) - expf(lb[i] - lse_b));
+    out[i] = fromf<T>(v);
   }
 }
-
 
 // ------------------------------------------------------------------- KV plumbing
 

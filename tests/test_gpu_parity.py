@@ -610,7 +610,7 @@ def test_decode_retirement_and_paged_kv(ctx, knob, dtype):
     reference stops each sequence at EOS, policy.cpp:425)."""
     arch = dict(QWENLIKE, context_len=200)
     pol = D.Policy(ctx, arch, dtype)
-    pol.upload(eos_heavy_params(arch, 31, 5.5))
+    pol.upload(eos_heavy_params(arch, 31, 1.8))   # P(EOS) ~ 2 % per step
     rng = np.random.default_rng(31)
     prompts = [[0] + list(rng.integers(2, arch["vocab_size"], size=int(rng.integers(3, 9)))) for _ in range(48)]
     G, ML = 4, 190
