@@ -242,6 +242,19 @@ typedef struct {
 DASHCU_API int dashcu_run_schedule(dashcu_policy* pol, const dashcu_schedule* sched, const dashcu_opt* opt,
                                    dashcu_policy* base, dashcu_step_log* logs, int32_t max_logs, int32_t* n_logs);
 
+/* ---- post-filter rebalancing across ranks ----
+ * After dashcu_rollout_advantage each rank holds a different number of kept sequences
+ * (advantage.cpp:135-140). dashcu_rebalance moves kept sequences (prompt, completion,
+ * advantage and the sampler's log-sum-exp rows) between ranks over NCCL so every rank's
+ * accumulate covers about the same number of tokens; the next dashcu_accumulate then runs
+ * over this rank's new kept set with the same global weight_scale, so the all-reduced
+ * gradient is unchanged up to summation order. Collective (every rank calls it); no-op at
+ * world 1. n_out / n_in: sequences sent / received. dashcu_rebalance_plan is the pure
+ * planner every rank runs on the all-gathered costs: n_items[world], costs (concatenated
+ * per rank, e.g. prompt + completion tokens) -> dest (the rank that accumulates each item). */
+DASHCU_API int dashcu_rebalance(dashcu_policy* pol, int32_t* n_out, int32_t* n_in);
+DASHCU_API int dashcu_rebalance_plan(int32_t world, const int32_t* n_items, const int64_t* costs, int32_t* dest);
+
 DASHCU_API int dashcu_grad_download(dashcu_policy* pol, double* grad, int64_t n);
 /* Replace the device gradient (fp64 views() order), e.g. a GradientVector computed elsewhere. */
 DASHCU_API int dashcu_grad_upload(dashcu_policy* pol, const double* grad, int64_t n);

@@ -159,6 +159,8 @@ def lib():
             "dashcu_shard_span": [C.c_int64, C.c_int32, C.c_int32, i64p, i64p],
             "dashcu_get_stats": [vp, C.POINTER(Stats)],
             "dashcu_rollout_snapshot": [vp],
+            "dashcu_rebalance": [vp, i32p, i32p],
+            "dashcu_rebalance_plan": [C.c_int32, i32p, i64p, i32p],
             "dashcu_policy_save": [vp, C.c_char_p, C.c_int32],
             "dashcu_policy_load": [vp, C.c_char_p, C.c_int32],
             "dashcu_checkpoint_arch": [C.c_char_p, C.POINTER(Arch)],
@@ -305,6 +307,22 @@ def task_rewards(kind: int, difficulty: int, seeds, group_size: int, completions
                                      sd.shape[0], group_size, _p(comp, i32p), comp.shape[1], _p(lens, i32p),
                                      _p(out, f64p)))
     return out[:lens.shape[0]]
+
+
+def rebalance_plan(costs_per_rank):
+    """Post-filter work plan (dashcu_rebalance_plan, no device work): for every rank's list of
+    item costs, the rank that accumulates each item."""
+    n = np.ascontiguousarray([len(c) for c in costs_per_rank], dtype=np.int32)
+    flat = np.ascontiguousarray(np.concatenate([np.asarray(c, dtype=np.int64) for c in costs_per_rank] +
+                                               [np.zeros(0, dtype=np.int64)]), dtype=np.int64)
+    dest = np.zeros(max(flat.shape[0], 1), dtype=np.int32)
+    _check(lib().dashcu_rebalance_plan(len(costs_per_rank), _p(n, i32p), _p(flat if flat.size else
+                                       np.zeros(1, np.int64), i64p), _p(dest, i32p)))
+    out, off = [], 0
+    for c in costs_per_rank:
+        out.append(dest[off:off + len(c)].copy())
+        off += len(c)
+    return out
 
 
 def checkpoint_arch(path: str) -> dict:
@@ -513,6 +531,12 @@ class Policy:
     def accumulate_weighted(self, weights, micro_batch: int = 32):
         w = np.ascontiguousarray(weights, dtype=np.float64)
         _check(lib().dashcu_accumulate_weighted(self.h, _p(w, f64p), w.shape[0], micro_batch))
+
+    def rebalance(self):
+        """Move kept sequences between ranks to even out the accumulate work (collective)."""
+        o, i = C.c_int32(0), C.c_int32(0)
+        _check(lib().dashcu_rebalance(self.h, C.byref(o), C.byref(i)))
+        return o.value, i.value
 
     # ---- PPO / KL / schedules (SPEC.md:293-328)
     def snapshot(self):

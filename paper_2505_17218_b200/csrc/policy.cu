@@ -305,6 +305,9 @@ struct dashcu_policy {
   std::vector<double> h_rewards, h_adv;
   std::vector<int32_t> h_kidx;
   bool adv_valid = false;
+  // sequences imported by dashcu_rebalance: sequence n_seq + k has prompt ext_prompt[k]
+  // (an entry appended to h_prompt_off); they exist for the accumulate only
+  std::vector<int32_t> ext_prompt;
   // PPO snapshot (theta_old) of the current rollout: per-sequence summed teacher-forced log-probs
   std::vector<double> h_oldlp;
   bool snap_valid = false;
@@ -721,7 +724,7 @@ struct Engine {
     B.start.push_back(0);
     for (size_t k = 0; k < seqs.size(); ++k) {
       const int s = seqs[k];
-      const int p = s / P.G;
+      const int p = s < P.n_seq ? s / P.G : P.ext_prompt[s - P.n_seq];  // imported: own prompt
       const int64_t po = P.h_prompt_off[p];
       const int m = static_cast<int>(P.h_prompt_off[p + 1] - po);
       const int len = P.h_len[s];
@@ -1475,6 +1478,7 @@ static int sample_impl(dashcu_policy* p, const dashcu_plan* plan, const int32_t*
   p->ro_valid = false;
   p->adv_valid = false;
   p->snap_valid = false;
+  p->ext_prompt.clear();
   const float inv_t = static_cast<float>(1.0 / plan->temperature);
   Timer tm(p->ctx->stream);
   dispatch(p, [&](auto& e) { e.sample(*plan, cap, keys, inv_t); });
@@ -1537,6 +1541,7 @@ int dashcu_rollout_load(dashcu_policy* p, const int32_t* prompt_tokens, const in
   p->lse_valid = false;  // external trajectories: the backward runs its own LSE pass
   p->adv_valid = false;
   p->snap_valid = false;
+  p->ext_prompt.clear();
   p->st.n_seq = S;
   API_END
 }
@@ -1684,6 +1689,202 @@ int dashcu_accumulate_weighted(dashcu_policy* p, const double* weights, int32_t 
       w.push_back(weights[s]);
     }
   accumulate_impl(p, seqs, w, micro);
+  API_END
+}
+
+// ------------------------------------------------------------ post-filter rebalancing
+// Filtering leaves every rank a different kept set (advantage.cpp:135-140), so the ranks'
+// accumulate work differs; one slow rank holds up the gradient allreduce. Every rank computes
+// the same plan from the all-gathered per-item costs (prompt + completion tokens: the
+// forward / backward work is linear in them at these lengths): donors above the mean give
+// their last items to the least-loaded rank while that lowers the larger of the two loads.
+// The global 1/N weights make the summed gradient independent of where an item is
+// accumulated (up to fp32 summation order).
+namespace dashcu {
+std::vector<std::vector<int>> rebalance_plan(const std::vector<std::vector<int64_t>>& cost) {
+  const int W = static_cast<int>(cost.size());
+  std::vector<double> load(W, 0.0);
+  double total = 0.0;
+  std::vector<std::vector<int>> dest(W);
+  for (int r = 0; r < W; ++r) {
+    dest[r].assign(cost[r].size(), r);
+    for (int64_t c : cost[r]) load[r] += static_cast<double>(c);
+    total += load[r];
+  }
+  const double target = total / std::max(W, 1);
+  for (int r = 0; r < W; ++r) {
+    for (int i = static_cast<int>(cost[r].size()) - 1; i >= 0 && load[r] > target; --i) {
+      int q = 0;
+      for (int k = 1; k < W; ++k)
+        if (load[k] < load[q]) q = k;
+      if (q == r) break;
+      const double c = static_cast<double>(cost[r][i]);
+      if (load[q] + c >= load[r]) continue;  // would not lower the larger load: try a smaller item
+      dest[r][i] = q;
+      load[r] -= c;
+      load[q] += c;
+    }
+  }
+  return dest;
+}
+}  // namespace dashcu
+
+int dashcu_rebalance_plan(int32_t world, const int32_t* n_items, const int64_t* costs, int32_t* dest) {
+  API_BEGIN
+  if (world < 1 || !n_items || (!costs && world > 0) || !dest) throw Error(1, "null argument");
+  std::vector<std::vector<int64_t>> c(world);
+  int64_t off = 0;
+  for (int r = 0; r < world; ++r) {
+    if (n_items[r] < 0) throw Error(1, "negative item count");
+    c[r].assign(costs + off, costs + off + n_items[r]);
+    off += n_items[r];
+  }
+  const auto d = rebalance_plan(c);
+  off = 0;
+  for (int r = 0; r < world; ++r)
+    for (int v : d[r]) dest[off++] = v;
+  API_END
+}
+
+int dashcu_rebalance(dashcu_policy* p, int32_t* n_out, int32_t* n_in) {
+  API_BEGIN
+  check_policy(p);
+  if (!p->adv_valid) throw Error(1, "call dashcu_rollout_advantage first");
+  if (!p->ext_prompt.empty()) throw Error(1, "this round is already rebalanced");
+  dashcu_ctx* c = p->ctx;
+  int32_t sent = 0, recvd = 0;
+  if (c->world > 1) {
+    NcclApi& nc = NcclApi::get();
+    if (!c->comm) throw Error(4, "communicator not initialised (dashcu_ctx_init_comm)");
+    if (!nc.AllGather || !nc.Send || !nc.Recv || !nc.GroupStart || !nc.GroupEnd)
+      throw Error(4, "libnccl lacks ncclAllGather / ncclSend / ncclRecv");
+    cudaStream_t s = c->stream;
+    const int W = c->world, me = c->rank;
+    const int stride = std::max(p->max_len, 1);
+    auto prompt_of = [&](int q) { return q < p->n_seq ? q / p->G : p->ext_prompt[q - p->n_seq]; };
+    auto prompt_len = [&](int q) {
+      const int pr = prompt_of(q);
+      return static_cast<int>(p->h_prompt_off[pr + 1] - p->h_prompt_off[pr]);
+    };
+    // 1. item counts and costs of every rank
+    const std::vector<int32_t>& K = p->h_kidx;
+    int64_t* dcnt = c->ws.get<int64_t>("rb_cnt", 2 * W);
+    int64_t mine = static_cast<int64_t>(K.size());
+    h2d(s, dcnt + W, &mine, 1);
+    NCCL_CHECK(nc.AllGather(dcnt + W, dcnt, 1, ncclInt64, c->comm, s));
+    std::vector<int64_t> cnt(W);
+    d2h(s, cnt.data(), dcnt, W);
+    nccl_wait(c->comm, s);
+    const int64_t maxc = std::max<int64_t>(1, *std::max_element(cnt.begin(), cnt.end()));
+    std::vector<int64_t> my_cost(maxc, 0), all_cost(maxc * W);
+    for (size_t i = 0; i < K.size(); ++i) my_cost[i] = prompt_len(K[i]) + p->h_len[K[i]];
+    int64_t* dcost = c->ws.get<int64_t>("rb_cost", maxc * (W + 1));
+    h2d(s, dcost + maxc * W, my_cost.data(), maxc);
+    NCCL_CHECK(nc.AllGather(dcost + maxc * W, dcost, maxc, ncclInt64, c->comm, s));
+    d2h(s, all_cost.data(), dcost, maxc * W);
+    nccl_wait(c->comm, s);
+    std::vector<std::vector<int64_t>> cost(W);
+    for (int r = 0; r < W; ++r) cost[r].assign(all_cost.begin() + r * maxc, all_cost.begin() + r * maxc + cnt[r]);
+    const auto dest = rebalance_plan(cost);
+    // 2. records {m, len, adv, prompt[m], completion[len], lse[len]} per destination
+    std::vector<float> lse_h;
+    if (p->lse_valid) {
+      lse_h.resize(static_cast<size_t>(p->n_seq + p->ext_prompt.size()) * stride);
+      d2h(s, lse_h.data(), p->d_lse.as<float>(), lse_h.size());
+      DCU_CHECK(cudaStreamSynchronize(s));
+    }
+    std::vector<std::vector<uint8_t>> out(W);
+    auto put = [](std::vector<uint8_t>& b, const void* v, size_t n) {
+      const uint8_t* q = static_cast<const uint8_t*>(v);
+      b.insert(b.end(), q, q + n);
+    };
+    std::vector<int32_t> keep;
+    for (size_t i = 0; i < K.size(); ++i) {
+      const int q = K[i], d = dest[me][i];
+      if (d == me) {
+        keep.push_back(q);
+        continue;
+      }
+      const int32_t m = prompt_len(q), len = p->h_len[q];
+      const int64_t po = p->h_prompt_off[prompt_of(q)];
+      put(out[d], &m, 4);
+      put(out[d], &len, 4);
+      put(out[d], &p->h_adv[q], 8);
+      put(out[d], p->h_prompt_tok.data() + po, 4 * m);
+      put(out[d], p->h_comp.data() + static_cast<size_t>(q) * stride, 4 * len);
+      if (p->lse_valid) put(out[d], lse_h.data() + static_cast<size_t>(q) * stride, 4 * len);
+      else out[d].resize(out[d].size() + 4 * len, 0);
+      ++sent;
+    }
+    // 3. byte counts: every rank's row of the W x W matrix
+    std::vector<int64_t> my_row(W), mat(W * W);
+    for (int r = 0; r < W; ++r) my_row[r] = static_cast<int64_t>(out[r].size());
+    int64_t* dmat = c->ws.get<int64_t>("rb_mat", W * (W + 1));
+    h2d(s, dmat + W * W, my_row.data(), W);
+    NCCL_CHECK(nc.AllGather(dmat + W * W, dmat, W, ncclInt64, c->comm, s));
+    d2h(s, mat.data(), dmat, W * W);
+    nccl_wait(c->comm, s);
+    // 4. point-to-point exchange (device staging buffers)
+    int64_t tot_out = 0, tot_in = 0;
+    for (int r = 0; r < W; ++r) tot_out += my_row[r], tot_in += mat[r * W + me];
+    uint8_t* dout = c->ws.get<uint8_t>("rb_out", std::max<int64_t>(tot_out, 1));
+    uint8_t* din = c->ws.get<uint8_t>("rb_in", std::max<int64_t>(tot_in, 1));
+    {
+      int64_t o = 0;
+      for (int r = 0; r < W; ++r) {
+        h2d(s, dout + o, out[r].data(), out[r].size());
+        o += static_cast<int64_t>(out[r].size());
+      }
+    }
+    NCCL_CHECK(nc.GroupStart());
+    for (int64_t r = 0, oo = 0, oi = 0; r < W; ++r) {
+      if (r != me && my_row[r]) NCCL_CHECK(nc.Send(dout + oo, my_row[r], ncclUint8, static_cast<int>(r), c->comm, s));
+      if (r != me && mat[r * W + me])
+        NCCL_CHECK(nc.Recv(din + oi, mat[r * W + me], ncclUint8, static_cast<int>(r), c->comm, s));
+      oo += my_row[r];
+      oi += mat[r * W + me];
+    }
+    NCCL_CHECK(nc.GroupEnd());
+    std::vector<uint8_t> in(tot_in);
+    d2h(s, in.data(), din, tot_in);
+    nccl_wait(c->comm, s);
+    // 5. append the imported sequences to the rollout (own prompt entries) and the kept list
+    size_t at = 0;
+    std::vector<float> lse_new;
+    while (at < in.size()) {
+      int32_t m, len;
+      double adv;
+      std::memcpy(&m, in.data() + at, 4);
+      std::memcpy(&len, in.data() + at + 4, 4);
+      std::memcpy(&adv, in.data() + at + 8, 8);
+      at += 16;
+      const int q = p->n_seq + static_cast<int>(p->ext_prompt.size());
+      p->ext_prompt.push_back(static_cast<int32_t>(p->h_prompt_off.size() - 1));
+      const int32_t* pt = reinterpret_cast<const int32_t*>(in.data() + at);
+      p->h_prompt_tok.insert(p->h_prompt_tok.end(), pt, pt + m);
+      p->h_prompt_off.push_back(p->h_prompt_off.back() + m);
+      at += 4 * m;
+      p->h_comp.resize(static_cast<size_t>(q + 1) * stride, -1);
+      std::memcpy(p->h_comp.data() + static_cast<size_t>(q) * stride, in.data() + at, 4 * len);
+      at += 4 * len;
+      p->h_len.push_back(len);
+      p->h_adv.push_back(adv);
+      lse_new.resize(static_cast<size_t>(q + 1 - p->n_seq) * stride, 0.f);
+      std::memcpy(lse_new.data() + static_cast<size_t>(q - p->n_seq) * stride, in.data() + at, 4 * len);
+      at += 4 * len;
+      keep.push_back(q);
+      ++recvd;
+    }
+    if (p->lse_valid && recvd) {  // the imported rows' sampler LSE, after the local ones
+      lse_h.insert(lse_h.end(), lse_new.begin(), lse_new.end());
+      p->d_lse.ensure(sizeof(float) * lse_h.size());
+      h2d(s, p->d_lse.as<float>(), lse_h.data(), lse_h.size());
+    }
+    p->h_kidx = keep;
+    DCU_CHECK(cudaStreamSynchronize(s));
+  }
+  if (n_out) *n_out = sent;
+  if (n_in) *n_in = recvd;
   API_END
 }
 

@@ -78,3 +78,59 @@ def test_world2_allreduce_and_sharded_step(dtype):
         assert np.linalg.norm(g - g1) <= 1e-5 * np.linalg.norm(g1)
         assert np.max(np.abs(p - p1)) <= 1e-6
     assert np.array_equal(res[0][1], res[1][1])   # all-gathered masters identical on every rank
+
+
+def run_rank_rebalance(rank, world, uid, q):
+    prompts, comps, w = batch()
+    rewards = np.zeros(M * G)
+    rewards[:G * (M // 2)] = np.tile([1.0, 0.0, 0.0, 1.0], M // 2)   # rank 0's groups mixed, rank 1's uniform
+    ctx = D.Context(rank)
+    ctx.init_comm(world, rank, uid)
+    pol = D.Policy(ctx, ARCH, D.F32)
+    pol.init_normal(0.05, 3)
+    per = M // world
+    lo, hi = rank * per, (rank + 1) * per
+    pol.load_rollout(prompts[lo:hi], G, comps[lo * G:hi * G])
+    pol.set_rewards(rewards[lo * G:hi * G])
+    pol.advantage(tau=0.1)
+    before = pol.stats()["n_kept"]
+    n_out, n_in = pol.rebalance()
+    pol.grad_zero()
+    pol.accumulate(1.0 / (M * G), micro_batch=4)
+    pol.allreduce_grads()
+    q.put((rank, before, n_out, n_in, pol.grad()))
+    pol.close()
+    ctx.close()
+
+
+def test_world2_rebalance():
+    """dashcu_rebalance moves kept sequences from the loaded rank to the idle one; the
+    all-reduced gradient equals the single-GPU one."""
+    prompts, comps, _ = batch()
+    rewards = np.zeros(M * G)
+    rewards[:G * (M // 2)] = np.tile([1.0, 0.0, 0.0, 1.0], M // 2)
+    ctx = D.Context(0)
+    pol = D.Policy(ctx, ARCH, D.F32)
+    pol.init_normal(0.05, 3)
+    pol.load_rollout(prompts, G, comps)
+    pol.set_rewards(rewards)
+    pol.advantage(tau=0.1)
+    pol.grad_zero()
+    pol.accumulate(1.0 / (M * G), micro_batch=4)
+    g1 = pol.grad()
+    pol.close()
+    ctx.close()
+    uid = D.comm_unique_id()
+    mpc = mp.get_context("spawn")
+    q = mpc.Queue()
+    procs = [mpc.Process(target=run_rank_rebalance, args=(r, 2, uid, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r[0], r[1:]) for r in (q.get(timeout=300) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][0] == 8 and res[1][0] == 0          # kept before: all on rank 0
+    assert res[0][1] == res[1][2] > 0                  # what rank 0 sent, rank 1 received
+    for r in range(2):
+        assert np.linalg.norm(res[r][3] - g1) <= 1e-5 * np.linalg.norm(g1)

@@ -117,3 +117,87 @@ def test_sharded_step_equals_single_process():
         assert np.linalg.norm(res[r][1] - g_all) <= 1e-12 * max(1.0, np.linalg.norm(g_all))
     assert np.array_equal(res[0][2], res[1][2])            # replicated optimizer state stays in sync
     assert res[0][4] == 2.0 and res[0][5] == 3.0            # max / sum over ranks
+
+
+def rebalance_worker(rank, world, port, q):
+    """Post-filter rebalancing (dashcu_rebalance's plan) as every rank runs it:
+    kept-item costs all-gathered, the library's planner on each rank, items accumulated where
+    the plan sends them; the all-reduced gradient must not change."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2505_17218_b200 as D
+    params = O.init_params(ARCH, 0.4, 2)
+    per = M // world
+
+    def items(r):   # (cost, prompt, completion, weight) of rank r's kept sequences, in index order
+        lo, hi = r * per, (r + 1) * per
+        prompts = W.synthetic_prompts(3, lo, hi, 4, ARCH["vocab_size"], 0, 1)
+        r_ = W.synthetic_rewards(5, lo, hi, G)
+        adv, kept, idx = O.advantage_filter(r_, G, 1, False, 0.0, 0.1)
+        out = []
+        for s in idx:
+            m = lo + s // G
+            c, _ = O.sample(ARCH, params, list(prompts[s // G]), ML, 1.0, O.derive_seed(SEED, "sample", m, s % G))
+            out.append((4 + len(c), list(prompts[s // G]), list(c), adv[s] / (M * G)))
+        return out
+    mine = items(rank)
+    costs = [None] * world
+    dist.all_gather_object(costs, [it[0] for it in mine])
+    plan = D.rebalance_plan(costs)
+    before = [sum(c) for c in costs]
+    after = [0] * world
+    for r in range(world):
+        for i, d in enumerate(plan[r]):
+            after[d] += costs[r][i]
+    # every rank accumulates what the plan sends it (its own kept items or imported ones)
+    g = np.zeros_like(params)
+    for r in range(world):
+        src = mine if r == rank else items(r)
+        for i, d in enumerate(plan[r]):
+            if d == rank:
+                _, pr, c, w = src[i]
+                O.grad_log_prob(ARCH, params, pr, c, w, g)
+    t = torch.from_numpy(g)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    q.put((rank, [list(p) for p in plan], before, after, t.numpy().copy()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_rebalance_plan_world2():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=rebalance_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+    assert res[0][1] == res[1][1]                              # the same plan on every rank
+    before, after = res[0][2], res[0][3]
+    assert sum(before) == sum(after) and max(after) <= max(before)
+    params = O.init_params(ARCH, 0.4, 2)
+    g_all, _ = rank_gradient(params, 0, M)
+    for r in range(world):
+        assert np.linalg.norm(res[r][4] - g_all) <= 1e-12 * max(1.0, np.linalg.norm(g_all))
+
+
+def test_rebalance_plan_properties():
+    import paper_2505_17218_b200 as D
+    rng = np.random.default_rng(0)
+    for world in (2, 4, 8):
+        for _ in range(20):
+            costs = [list(rng.integers(10, 1200, size=int(rng.integers(0, 60)))) for _ in range(world)]
+            plan = D.rebalance_plan(costs)
+            load = [0] * world
+            for r in range(world):
+                assert len(plan[r]) == len(costs[r])
+                for i, d in enumerate(plan[r]):
+                    load[d] += costs[r][i]
+            before = [sum(c) for c in costs]
+            assert sum(load) == sum(before) and max(load) <= max(before)
+            if sum(before):
+                assert max(load) - sum(load) / world <= max(max(c) if c else 0 for c in costs) + 1e-9
+    assert [list(x) for x in D.rebalance_plan([[100, 200, 300, 400], [50], [10, 10]])] == [[0, 0, 1, 2], [1], [0, 0]]
