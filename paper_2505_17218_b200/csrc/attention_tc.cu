@@ -50,9 +50,13 @@ __global__ void __launch_bounds__(DecCfg<HD>::NW * 32)
   const int sq = dr_seq(dr, s);
   const int grp = nh / nkv, qd = nh * HD, kvd = nkv * HD, qkvd = qd + 2 * kvd;
   const int m = prompt_len[sq];
-  const int nk = m + n_comp;
   const bf16* kpb = kp + (static_cast<int64_t>(sq / G) * nkv + kvh) * pmax * HD;
   const bf16* vpb = vp + (static_cast<int64_t>(sq / G) * nkv + kvh) * pmax * HD;
+  // the sequence's page-table row, one entry per lane (completion <= 32 pages = 2048 slots);
+  // longer rows read the table directly
+  const bool shfl_pages = dr.max_pages <= 32;
+  const int32_t lane_page =
+      shfl_pages && lane < dr.max_pages ? __ldg(dr.ptab + static_cast<int64_t>(sq) * dr.max_pages + lane) : 0;
   uint8_t* wsm = smem + warp * Cf::WARP_BYTES;
   const uint32_t wsm_a = smem_addr(wsm);
 
@@ -74,21 +78,37 @@ __global__ void __launch_bounds__(DecCfg<HD>::NW * 32)
     }
   }
 
+  // chunks: cpm over the prompt keys [0, m), then chunks over the completion slots
+  // [0, n_comp) aligned to slot 0, so a completion chunk (KC | kPage) lies in one page
+  const int cpm = (m + KC - 1) / KC;
+  auto chunk_keys = [&](int c, int* first) {  // first key / slot of chunk c and its bound
+    *first = (c < cpm ? c : c - cpm) * KC;
+    return c < cpm ? m : n_comp;
+  };
   auto load_chunk = [&](int c, int stage) {
     const uint32_t kbase = wsm_a + stage * 2 * Cf::CHUNK_BYTES, vbase = kbase + Cf::CHUNK_BYTES;
+    int first;
+    const int lim = chunk_keys(c, &first);
+    const bf16 *kb, *vb;
+    if (c < cpm) {
+      kb = kpb + static_cast<int64_t>(first) * HD;
+      vb = vpb + static_cast<int64_t>(first) * HD;
+    } else {
+      const int page = shfl_pages ? __shfl_sync(0xffffffffu, lane_page, (first / kPage) & 31)
+                                  : __ldg(dr.ptab + static_cast<int64_t>(sq) * dr.max_pages + first / kPage);
+      const int64_t po = ((static_cast<int64_t>(page) * nkv + kvh) * kPage + first % kPage) * HD;
+      kb = kc + po;
+      vb = vc + po;
+    }
 #pragma unroll
     for (int i = 0; i < KC * UNITS / 32; ++i) {
       const int idx = lane + i * 32;
       const int r = idx / UNITS, u = idx % UNITS;
-      const int j = c * KC + r;
-      const bool ok = j < nk;
-      const int jj = ok ? j : 0;
-      const int64_t po = jj < m ? static_cast<int64_t>(jj) * HD : kv_slot_off(dr, sq, kvh, nkv, jj - m, HD);
-      const bf16* ks = (jj < m ? kpb : kc) + po;
-      const bf16* vs = (jj < m ? vpb : vc) + po;
+      const bool ok = first + r < lim;
+      const int64_t ro = ok ? static_cast<int64_t>(r) * HD + u * 8 : 0;
       const int off = swz(r, u, UNITS);
-      cp_async16(kbase + off, ks + u * 8, ok ? 16 : 0);
-      cp_async16(vbase + off, vs + u * 8, ok ? 16 : 0);
+      cp_async16(kbase + off, kb + ro, ok ? 16 : 0);
+      cp_async16(vbase + off, vb + ro, ok ? 16 : 0);
     }
   };
 
@@ -97,7 +117,7 @@ __global__ void __launch_bounds__(DecCfg<HD>::NW * 32)
   for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float mrow[2] = {-FLT_MAX, -FLT_MAX}, lrow[2] = {0.f, 0.f};
 
-  const int nch = (nk + KC - 1) / KC;
+  const int nch = cpm + (n_comp + KC - 1) / KC;
 #pragma unroll
   for (int c = 0; c < ST - 1; ++c) {
     if (c < nch) load_chunk(c, c);
@@ -128,12 +148,14 @@ __global__ void __launch_bounds__(DecCfg<HD>::NW * 32)
     }
     // scale into the log2 domain, mask keys past the end, online softmax
     float cmax[2] = {-FLT_MAX, -FLT_MAX};
+    int cfirst;
+    const int clim = chunk_keys(c, &cfirst);
 #pragma unroll
     for (int nt = 0; nt < KC / 8; ++nt) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int key = c * KC + nt * 8 + t * 2 + (e & 1);
-        const float v = key < nk ? sc[nt][e] * scale_log2 : -FLT_MAX;
+        const int key = cfirst + nt * 8 + t * 2 + (e & 1);
+        const float v = key < clim ? sc[nt][e] * scale_log2 : -FLT_MAX;
         sc[nt][e] = v;
         cmax[e >> 1] = fmaxf(cmax[e >> 1], v);
       }

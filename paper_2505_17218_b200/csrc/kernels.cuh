@@ -44,10 +44,12 @@ template <class T>
 void embed_decode(cudaStream_t s, const T* tok_emb, const T* pos_emb, const int32_t* tok,
                   const int32_t* prompt_len, int step, int rows, int d, float* x32, T* xT,
                   const int32_t* row_seq = nullptr);
-// deterministic (stable sort by id + in-order run sums); tmp: embed_bwd_tmp_bytes(rows)
+// deterministic (stable sort by id + in-order run sums); tmp: embed_bwd_tmp_bytes(rows),
+// part: embed_bwd_part_floats(rows, d) floats of window partials
 size_t embed_bwd_tmp_bytes(int rows);
+size_t embed_bwd_part_floats(int rows, int d);
 void embed_bwd(cudaStream_t s, const float* dx, const int32_t* tok, const int32_t* pos, int rows, int d, int n_tok,
-               int n_pos, float* g_tok, float* g_pos, void* tmp);
+               int n_pos, float* g_tok, float* g_pos, void* tmp, float* part);
 // out[n] += sum_m X[m][n]  (bias gradients: db_out, db1, db2); deterministic two-pass,
 // tmp holds colsum_tmp_floats<T>(M, N) floats of row-segment partials
 template <class T>

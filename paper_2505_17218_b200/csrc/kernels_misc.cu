@@ -122,31 +122,59 @@ __global__ void embed_seg_mark_k(const int32_t* ids, int rows, int32_t* keys, in
   if (r < rows) keys[r] = ids[r], vals[r] = r;
 }
 
-__global__ void embed_seg_sum_k(const float* __restrict__ dx, const int32_t* __restrict__ skey,
-                                const int32_t* __restrict__ srow, int rows, int d, float* __restrict__ g) {
+// Pass 1: window w holds sorted positions [w kEmbWin, (w+1) kEmbWin); every run of equal
+// ids inside it is summed in row order into part[position of the run's first row in the
+// window]. Pass 2: the block owning the head of an id's run adds that run's window partials
+// in window order to the id's gradient row. Long runs (a token repeated thousands of times
+// in a micro-batch) spread over many blocks in pass 1 instead of one serial loop.
+constexpr int kEmbWin = 64;
+__global__ void embed_win_k(const float* __restrict__ dx, const int32_t* __restrict__ skey,
+                            const int32_t* __restrict__ srow, int rows, int d, float* __restrict__ part) {
+  const int w0 = blockIdx.x * kEmbWin, w1 = min(rows, w0 + kEmbWin);
+  const int c = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
+  if (c >= d) return;
+  const bool v4 = (d & 3) == 0;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int start = w0;
+  for (int i = w0; i < w1; ++i) {
+    const float* src = dx + static_cast<int64_t>(srow[i]) * d + c;
+    if (v4) {
+      const float4 v = *reinterpret_cast<const float4*>(src);
+      acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
+    } else {
+      acc.x += src[0];
+      if (c + 1 < d) acc.y += src[1];
+      if (c + 2 < d) acc.z += src[2];
+      if (c + 3 < d) acc.w += src[3];
+    }
+    if (i + 1 == w1 || skey[i + 1] != skey[i]) {
+      float* dst = part + static_cast<int64_t>(start) * d + c;
+      if (v4) {
+        *reinterpret_cast<float4*>(dst) = acc;
+      } else {
+        dst[0] = acc.x;
+        if (c + 1 < d) dst[1] = acc.y;
+        if (c + 2 < d) dst[2] = acc.z;
+        if (c + 3 < d) dst[3] = acc.w;
+      }
+      acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      start = i + 1;
+    }
+  }
+}
+
+__global__ void embed_run_k(const float* __restrict__ part, const int32_t* __restrict__ skey, int rows, int d,
+                            float* __restrict__ g) {
   const int i = blockIdx.x;
   const int key = skey[i];
   if (i > 0 && skey[i - 1] == key) return;  // not the head of its run
-  int end = i + 1;
-  while (end < rows && skey[end] == key) ++end;
   float* gr = g + static_cast<int64_t>(key) * d;
-  for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
-    if (c + 4 <= d && (d & 3) == 0) {
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int j = i; j < end; ++j) {
-        const float4 v = *reinterpret_cast<const float4*>(dx + static_cast<int64_t>(srow[j]) * d + c);
-        acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
-      }
-      float4 o = *reinterpret_cast<float4*>(gr + c);
-      o.x += acc.x, o.y += acc.y, o.z += acc.z, o.w += acc.w;
-      *reinterpret_cast<float4*>(gr + c) = o;
-    } else {
-      for (int cc = c; cc < min(d, c + 4); ++cc) {
-        float acc = 0.f;
-        for (int j = i; j < end; ++j) acc += dx[static_cast<int64_t>(srow[j]) * d + cc];
-        gr[cc] += acc;
-      }
-    }
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float acc = part[static_cast<int64_t>(i) * d + c];
+    // the run's later windows start at multiples of kEmbWin while the id is unchanged
+    for (int p = (i / kEmbWin + 1) * kEmbWin; p < rows && skey[p] == key; p += kEmbWin)
+      acc += part[static_cast<int64_t>(p) * d + c];
+    gr[c] += acc;
   }
 }
 
@@ -780,9 +808,10 @@ size_t embed_bwd_tmp_bytes(int rows) {
                                   static_cast<int32_t*>(nullptr), rows);
   return 4 * sizeof(int32_t) * static_cast<size_t>(rows) + (cub_bytes + 255) / 256 * 256 + 256;
 }
+size_t embed_bwd_part_floats(int rows, int d) { return static_cast<size_t>(rows) * d; }
 
 void embed_bwd(cudaStream_t s, const float* dx, const int32_t* tok, const int32_t* pos, int rows, int d, int n_tok,
-               int n_pos, float* gt, float* gp, void* tmp) {
+               int n_pos, float* gt, float* gp, void* tmp, float* part) {
   if (rows <= 0) return;
   int32_t* keys = static_cast<int32_t*>(tmp);
   int32_t* vals = keys + rows;
@@ -801,7 +830,9 @@ void embed_bwd(cudaStream_t s, const float* dx, const int32_t* tok, const int32_
     cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, keys, skeys, vals, svals, rows, 0, bits_needed[w], s);
     DCU_CHECK(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, keys, skeys, vals, svals, rows, 0, bits_needed[w],
                                               s));
-    embed_seg_sum_k<<<rows, bs, 0, s>>>(dx, skeys, svals, rows, d, grads[w]);
+    embed_win_k<<<dim3(cdiv(rows, kEmbWin), cdiv(d, 4 * 128)), 128, 0, s>>>(dx, skeys, svals, rows, d, part);
+    DCU_LAUNCHED();
+    embed_run_k<<<rows, bs, 0, s>>>(part, skeys, rows, d, grads[w]);
     DCU_LAUNCHED();
   }
 }

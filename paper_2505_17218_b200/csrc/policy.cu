@@ -697,7 +697,8 @@ struct Engine {
       std::swap(dy32, dx32);  // dy for the layer below; dx32 is scratch again
     }
     embed_bwd(st, dy32, tok, pos, Tn, g.d, g.V, g.ctx, G32(L.tok), G32(L.pos),
-              ws.get<uint8_t>("b_embtmp", embed_bwd_tmp_bytes(Tn)));
+              ws.get<uint8_t>("b_embtmp", embed_bwd_tmp_bytes(Tn)),
+              ws.get<float>("b_embpart", embed_bwd_part_floats(Tn, g.d)));
   }
 
   void cast_to_T(const float* in, T* out, size_t n) {
