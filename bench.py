@@ -62,9 +62,13 @@ CONFIGS = {
                workload="BASELINE configs[0]: SPEC tiny policy (2 layers, d=128, byte vocab), 64 prompts x G=8"),
 }
 C1_ARCH = dict(vocab_size=256, embed_dim=128, context_len=64, ffn_hidden=512, n_layers=2, bos_id=0, eos_id=1)
-# bounded CPU sample of the same workload for the reference arm / cpu_baseline
 PROF_PERIOD = 17
-REF_SAMPLE = dict(prompts=1, G=8, prompt_len=4, max_len=4)
+# bounded CPU samples of the same workload: the reference arm's per-step
+# sample (short, so K steps end within minutes) and the cpu_baseline sub-batch of our arm
+# (8 sequences per 8 host cores x 16 generated tokens); prompt 4 tokens because the
+# reference re-runs the prompt for every sample (policy.cpp:396) at ~0.5 s per token-core
+REF_SAMPLE = dict(G=8, prompt_len=4, max_len=4)
+CPU_BASELINE_SAMPLE = dict(G=8, prompt_len=4, max_len=16)
 
 
 def prompts_of(cfg, arch, m_lo, m_hi, reference=False):
@@ -213,16 +217,17 @@ def pinned(shape, dtype):
 
 # --------------------------------------------------------------- reference arm
 
-def ref_step_runner(cfg, threads):
-    """The reference's own CPU DASH step (oracle/_ref ref_dash_step) on a bounded sample."""
+def ref_step_runner(cfg, threads, sample_cfg=None):
+    """The reference's own CPU DASH step (oracle/_ref ref_dash_step) on a bounded sample;
+    run(step) -> RefStepStats (per-phase seconds, tokens)."""
     import ctypes as C
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_ffi as O
     arch = arch_of(cfg)
     for k in ("n_heads", "n_kv_heads", "head_dim"):   # the reference is single-head (policy.cpp:93-129)
         arch.pop(k, None)
-    rs = REF_SAMPLE if cfg["size"] else dict(prompts=cfg["prompts"], G=cfg["G"], prompt_len=cfg["prompt_len"],
-                                               max_len=cfg["max_len"])
+    rs = dict(sample_cfg or REF_SAMPLE, prompts=max(1, threads // 8)) if cfg["size"] else \
+        dict(prompts=cfg["prompts"], G=cfg["G"], prompt_len=cfg["prompt_len"], max_len=cfg["max_len"])
     arch["context_len"] = max(arch["context_len"], rs["prompt_len"] + rs["max_len"])
     n = O.num_params(arch)
     params = (np.random.default_rng(1).standard_normal(n, dtype=np.float32) * 0.02).astype(np.float64)
@@ -245,7 +250,7 @@ def ref_step_runner(cfg, threads):
                              1e-6, O.ptr(m, O.f64p), O.ptr(v, O.f64p), C.byref(t), threads, C.byref(st))
         if rc != 0:
             raise RuntimeError("reference step failed")
-        return st.tokens_sampled, st.total_s
+        return st
     return run, sample
 
 
@@ -258,9 +263,9 @@ def run_reference(args, cfg, world, rank):
         run(i)
     toks, secs = 0, 0.0
     for i in range(args.steps):
-        a, b = run(100 + i)
-        toks += a
-        secs += b
+        st = run(100 + i)
+        toks += st.tokens_sampled
+        secs += st.total_s
     val = toks / secs
     line = {"metric": "dash_step_sampled_tokens_per_s", "value": val, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": 1000 * secs / args.steps,
@@ -297,10 +302,20 @@ def run_ours(args, cfg, world, rank, local):
     outs = (pinned((S, max(ML, 1)), np.int32), pinned(S, np.int32), pinned((S, max(ML, 1)), np.float32))
     N_global = M * G * world
 
-    def step(i):
+    phase_prof = {"sample": {}, "accumulate": {}}
+
+    def add_prof(ph):  # kernel-class totals of the phase that just ran (profiling on)
+        for k, v in D.profile_read(reset=True).items():
+            a = phase_prof[ph].setdefault(k, dict(ms=0.0, flops=0.0, bytes=0.0, launches=0))
+            for f in a:
+                a[f] += v[f]
+
+    def step(i, prof=False):
         t0 = time.perf_counter()
         ro = pol.sample(None, G, ML, 1.0, round_seed=i, prompt_index_base=base, prompt_tokens=ptok,
                         prompt_offsets=poff, outputs=outs)
+        if prof:
+            add_prof("sample")
         r = W.synthetic_rewards(2 + i, base, base + M, G)
         pol.set_rewards(r)
         adv, kept, nk = pol.advantage(tau=cfg["tau"])
@@ -311,6 +326,8 @@ def run_ours(args, cfg, world, rank, local):
         else:
             pol.allreduce_grads()
             pol.optimizer_step(D.OPT_ADAM, lr=1e-6)
+        if prof:
+            add_prof("accumulate")
         st = pol.stats()
         wall = time.perf_counter() - t0
         dev = st["sample_ms"] + st["advantage_ms"] + st["accumulate_ms"] + st["allreduce_ms"] + st["optimizer_ms"]
@@ -328,17 +345,25 @@ def run_ours(args, cfg, world, rank, local):
     D.profile_enable()
     D.profile_read(reset=True)
     l0 = D.kernel_launches()
-    toks, dev_ms, wall_ms, last = 0, 0.0, 0.0, None
+    toks, dev_ms, wall_ms, last, phase_ms = 0, 0.0, 0.0, None, {"sample": 0.0, "accumulate": 0.0}
     for i in range(args.steps):
-        a, b, c, last = step(args.warmup + i)
+        a, b, c, last = step(args.warmup + i, prof=True)
         toks += a
         dev_ms += b
         wall_ms += c
+        phase_ms["sample"] += last["sample_ms"]
+        phase_ms["accumulate"] += last["accumulate_ms"] + last["allreduce_ms"] + last["optimizer_ms"]
     ctx.sync()
     barrier()
     launches = D.kernel_launches() - l0
-    prof = D.profile_read(reset=True)
+    add_prof("accumulate")
     D.profile_enable(())
+    prof = {}
+    for ph in phase_prof.values():
+        for k, v in ph.items():
+            a = prof.setdefault(k, dict(ms=0.0, flops=0.0, bytes=0.0, launches=0))
+            for f in a:
+                a[f] += v[f]
     clk = clocks.stop()
     tot_toks = allreduce([toks], "sum")[0]
     dev_ms, wall_ms = allreduce([dev_ms, wall_ms], "max")
@@ -357,10 +382,15 @@ def run_ours(args, cfg, world, rank, local):
     else:
         achieved = pr["flops"] / (pr["ms"] / 1e3) / 1e12
         peak, unit = pk["tc_sus"], "TFLOP/s"
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    traffic, traffic_note = None, None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic_c2.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(name)
+        t = json.load(open(tp)).get(name)
+        if t:
+            traffic = t["dram_bytes"]
+            traffic_note = (f"ncu --set full, {t['shape']}: DRAM {t['dram_bytes'] / 1e6:.1f} MB per launch vs "
+                            f"{t['alg_bytes'] / 1e6:.1f} MB algorithmic (x{t['dram_bytes'] / t['alg_bytes']:.2f})")
+    phase_roofline = phase_rooflines(phase_prof, phase_ms, pk, args.steps)
 
     S_all = S
     h2d = ptok.nbytes + poff.nbytes + S_all * 8       # prompts + rewards
@@ -379,6 +409,7 @@ def run_ours(args, cfg, world, rank, local):
         "gpu_launches": launches,
         "roofline": {"bound": "hbm" if hbm_bound else "tensor", "kernel": name, "achieved": achieved,
                      "peak": peak, "unit": unit, "frac": achieved / peak, "traffic": traffic,
+                     "traffic_note": traffic_note,
                      "per_launch_ms": per_launch_ms, "event_sampling": f"1 in {PROF_PERIOD} launches per class",
                      "peak_source": pk["src"] + (" burst" if False else
                                                                                 " sustained" if not hbm_bound else "")},
@@ -386,14 +417,12 @@ def run_ours(args, cfg, world, rank, local):
                                            "optimizer_ms")},
         "kernel_classes": {k: {"ms_per_step": v["ms"] / args.steps, "launches": v["launches"]}
                            for k, v in prof.items() if v["launches"]},
+        "phase_rooflines": phase_roofline,
         "kept": last["n_kept"], "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            run, sample = ref_step_runner(cfg, os.cpu_count() or 1)
-            a, b = run(0)
-            line["cpu_baseline"] = {"value": a / b, "unit": "tokens/s", "cores": os.cpu_count() or 1,
-                                    "kind": "reference", "sample": sample}
+            line["cpu_baseline"] = cpu_baseline(cfg, arch, S, tot_toks / args.steps, last)
         except Exception as e:  # reference not built on this box
             line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
@@ -401,6 +430,64 @@ def run_ours(args, cfg, world, rank, local):
         print(json.dumps(line), flush=True)
     pol.close()
     ctx.close()
+
+
+def phase_rooflines(pp, phase_ms, pk, steps):
+    """Per-phase roofline fractions (north_star targets) from the phase-split kernel classes:
+    decode attention (HBM-bound; K/V bytes with the group's prompt KV counted once), the
+    decode projections + sampling GEMM (tensor), the decode phase against its serial floor
+    (attention bytes / HBM + GEMM flops / tensor peak), and the accumulate phase (every
+    tensor-core flop of the PG step over the phase time, optimizer + allreduce included)."""
+    s, a = pp["sample"], pp["accumulate"]
+    out = {}
+    ad = s.get("attn_decode")
+    if ad and ad["ms"]:
+        gbs = ad["bytes"] / (ad["ms"] / 1e3) / 1e9
+        out["decode_attention"] = {"achieved": gbs, "unit": "GB/s", "peak": pk["hbm"], "frac": gbs / pk["hbm"],
+                                   "ms_per_step": ad["ms"] / steps}
+    gf = sum(s[k]["flops"] for k in ("gemm_tc", "sample", "attn_fwd") if k in s)
+    gm = sum(s[k]["ms"] for k in ("gemm_tc", "sample", "attn_fwd") if k in s)
+    if gm:
+        tf = gf / (gm / 1e3) / 1e12
+        out["decode_gemm"] = {"achieved": tf, "unit": "TFLOP/s", "peak": pk["tc_sus"], "frac": tf / pk["tc_sus"],
+                              "ms_per_step": gm / steps, "note": "prefill + decode projections + LM-head sampling"}
+    if phase_ms["sample"] and ad:
+        floor = ad["bytes"] / (pk["hbm"] * 1e9) * 1e3 + gf / (pk["tc_sus"] * 1e12) * 1e3
+        out["decode_phase"] = {"floor_ms_per_step": floor / steps, "ms_per_step": phase_ms["sample"] / steps,
+                               "frac": floor / phase_ms["sample"],
+                               "note": "attention HBM floor + GEMM tensor floor, serial, over the sampling phase"}
+    af = sum(a[k]["flops"] for k in ("gemm_tc", "attn_fwd", "attn_bwd", "lm_rows") if k in a)
+    if phase_ms["accumulate"]:
+        tf = af / (phase_ms["accumulate"] / 1e3) / 1e12
+        out["accumulate_phase"] = {"achieved": tf, "unit": "TFLOP/s", "peak": pk["tc_sus"], "frac": tf / pk["tc_sus"],
+                                   "ms_per_step": phase_ms["accumulate"] / steps,
+                                   "kernel_ms_per_step": {k: v["ms"] / steps for k, v in a.items() if v["launches"]}}
+    return out
+
+
+def cpu_baseline(cfg, arch, S, toks_per_step, last):
+    """The reference's own CPU DASH step (oracle/_ref, all host cores) on the BASELINE.md §3
+    sub-batch, per phase, with a labelled extrapolation to this workload's step."""
+    threads = os.cpu_count() or 1
+    run, sample = ref_step_runner(cfg, threads, CPU_BASELINE_SAMPLE)
+    st = run(0)
+    grad_tokens = st.kept * (CPU_BASELINE_SAMPLE["prompt_len"] + st.tokens_sampled / max(st.n_seq, 1))
+    out = {"value": st.tokens_sampled / st.total_s, "unit": "tokens/s", "cores": threads, "kind": "reference",
+           "sample": sample, "sample_s": st.sample_s, "grad_s": st.grad_s, "adam_s": st.update_s,
+           "sample_tok_s_per_core": st.tokens_sampled / st.sample_s / threads}
+    if st.grad_s > 0 and grad_tokens:
+        out["grad_tok_s_per_core"] = grad_tokens / st.grad_s / threads
+    if cfg["size"] and out.get("grad_tok_s_per_core"):
+        # this step's tokens on the reference (it re-runs each prompt per sample, policy.cpp:396)
+        samp_tok = S * cfg["prompt_len"] + toks_per_step
+        kept_tok = last["loss_tokens"] + last["n_kept"] * cfg["prompt_len"]
+        box = threads
+        est = samp_tok / (out["sample_tok_s_per_core"] * box) + kept_tok / (out["grad_tok_s_per_core"] * box)
+        est += st.update_s
+        out["extrapolated_step_s"] = est
+        out["extrapolation"] = ("EXTRAPOLATION, not measured: this workload's sampled + prompt tokens at the "
+                                "measured sample rate, kept tokens at the measured grad rate, plus one Adam step")
+    return out
 
 
 def main():
