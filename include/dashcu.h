@@ -108,6 +108,7 @@ typedef struct {
   int64_t kernel_launches;  /* kernels this policy launched since creation */
   int64_t decode_row_steps; /* sum over the last rollout's decode steps of the active rows */
   int64_t kv_pages_peak;    /* most completion-KV pages (per layer) in use at once */
+  int64_t slice_recompute_mismatches; /* logits dump on: recomputed slice logits != the dump (0) */
 } dashcu_stats;
 
 DASHCU_API const char* dashcu_last_error(void);

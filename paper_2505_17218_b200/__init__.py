@@ -100,7 +100,8 @@ class Stats(C.Structure):
                 ("allreduce_ms", C.c_double), ("optimizer_ms", C.c_double), ("tokens_sampled", C.c_int64),
                 ("n_seq", C.c_int32), ("n_kept", C.c_int32), ("loss_tokens", C.c_int64),
                 ("mean_reward", C.c_double), ("filtered_fraction", C.c_double), ("mean_abs_kept", C.c_double),
-                ("kernel_launches", C.c_int64), ("decode_row_steps", C.c_int64), ("kv_pages_peak", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("decode_row_steps", C.c_int64), ("kv_pages_peak", C.c_int64),
+                ("slice_recompute_mismatches", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

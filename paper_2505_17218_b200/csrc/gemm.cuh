@@ -11,6 +11,7 @@
 // in place into the fp32 gradient (the reference's add_scaled, tensors.cpp:109).
 #pragma once
 #include "common.cuh"
+#include "kernels.cuh"
 
 namespace dashcu {
 
@@ -75,6 +76,7 @@ struct SampleArgs {
   const float* weight = nullptr;   // DZ: per-row weight w_r = A_n / N
   bf16* dz = nullptr;              // DZ: [rows][ld_dz]
   int64_t ld_dz = 0;
+  const SliceSel* sel = nullptr;   // SLICE: per-row chosen slice (sample_scan phase 1)
 };
 int gemm_tc_lse(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa);
 bool gemm_tc_dz(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa);
@@ -89,6 +91,10 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g, const Epi& e);
 // Fused LM head + sampling partials; returns the number of N tiles (0 if not TMA-legal).
 int gemm_tc_sample(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa);
 int gemm_tc_sample_tiles(int N);
+// The chosen 32-id slice of every row recomputed on the sampling GEMM's instruction sequence:
+// sa.logits[row * 32 + i] = logit of id 32 sel[row].sb + i (bias added), bit-identical to the
+// sampling epilogue's value; g = the sampling GEMM's shape (A = the rows, B = W_out).
+bool gemm_tc_slice(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa);
 
 template <class T>
 __device__ __forceinline__ void epi_apply(const Epi& e, int m, int n, float acc) {

@@ -491,9 +491,11 @@ __device__ __forceinline__ void epilogue_sample(const GemmShape& g, const Epi& e
     const bool full = nb + 32 <= g.N;
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = __fadd_rn(v[i], b[i]);
-    stage_acquire(lane);  // fp32 logits (the scan reads the chosen slice; the parity dump)
-    stage_f32(stg, lane, v);
-    stage_release(lane, &om.f32, stg, nb, r0, false);
+    if (sa.logits) {  // fp32 logits only for the parity dump (the scan recomputes its slice)
+      stage_acquire(lane);
+      stage_f32(stg, lane, v);
+      stage_release(lane, &om.f32, stg, nb, r0, false);
+    }
     if (!live) continue;
     float m, m1, Z, Z1;
     if (full && (sa.bos < nb || sa.bos >= nb + 32)) {
@@ -631,7 +633,33 @@ __device__ __forceinline__ void epilogue_dz(const GemmShape& g, const Epi& e, co
   }
 }
 
-// MODE: 0 generic store epilogue, 1 fused sampling, 2 LSE partials, 3 dz
+// Chosen-slice recompute (MODE 4, gemm_tc_slice): tile (row block mb, nt) multiplies the 128
+// rows of the block with the W_out rows of the slices chosen by its rows 8 nt .. 8 nt + 7
+// (B staged as eight 32-row boxes); row 8 nt + j keeps columns [32 j, 32 j + 32): its own
+// slice. Same instruction sequence as the MODE 1 sampling GEMM (128 x 256 tiles, BK 64, the
+// same K order), so the 32 logits equal the ones the sampling epilogue saw, bit for bit.
+__device__ __forceinline__ void epilogue_slice(const GemmShape& g, const Epi& e, const SampleArgs& sa,
+                                               uint32_t taddr, int row, int nt, int q, int c_lo, int c_hi,
+                                               int lane) {
+  float v[32];
+  const int base = nt * 8 - q * 32;  // lane of the tile's first useful row within this quarter
+  const bool mine = lane >= base && lane < base + 8 && row < g.M;
+  const int j = lane - base;
+  const int sb = mine ? sa.sel[row].sb : -1;
+#pragma unroll 1
+  for (int c = c_lo; c < c_hi; c += 32) {
+    tmem_ld32(taddr + c, v);  // warp-collective
+    if (!mine || c != 32 * j || sb < 0) continue;
+    float* out = sa.logits + static_cast<int64_t>(row) * kSlice;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int id = sb * kSlice + i;
+      out[i] = id < g.N ? __fadd_rn(v[i], __ldg(e.bias + id)) : 0.f;
+    }
+  }
+}
+
+// MODE: 0 generic store epilogue, 1 fused sampling, 2 LSE partials, 3 dz, 4 chosen-slice recompute
 template <int BN, int STAGES, bool AK, bool BKM, int EPW, int MODE>
 __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
@@ -648,7 +676,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkb = (g.K + BK - 1) / BK;
-  const int tiles_m = (g.M + BM - 1) / BM, tiles_n = (g.N + BN - 1) / BN;
+  const int tiles_m = (g.M + BM - 1) / BM, tiles_n = MODE == 4 ? BM / 8 : (g.N + BN - 1) / BN;
   const int ntile = tiles_m * tiles_n;
   // split-K (EPI_ACCUM only): work item w = (tile w / S, K slice w % S), slices of kps k-blocks
   const int S = MODE == 0 ? e.splits : 1;
@@ -685,7 +713,16 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
       int kb_all = 0;
       for (int w = blockIdx.x; w < nitem; w += gridDim.x) {
         const int t = w / S, sp = w % S;
-        const int m0 = tile_m(g, t, tiles_m, tiles_n) * BM, n0 = tile_n(g, t, tiles_m, tiles_n) * BN;
+        const int m0 = (MODE == 4 ? t / tiles_n : tile_m(g, t, tiles_m, tiles_n)) * BM,
+                  n0 = MODE == 4 ? t % tiles_n : tile_n(g, t, tiles_m, tiles_n) * BN;
+        int slice_row[8];  // MODE 4: W_out row of each 32-row B box
+        if constexpr (MODE == 4) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int r = m0 + n0 * 8 + j;
+            slice_row[j] = r < g.M ? max(sa.sel[r].sb, 0) * kSlice : 0;
+          }
+        }
         const int kb_lo = sp * kps, kb_hi = min(nkb, kb_lo + kps);
         for (int kb = kb_lo; kb < kb_hi; ++kb, ++kb_all) {
           const int s = kb_all % STAGES;
@@ -701,7 +738,10 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
             tma_load_2d(sa_, &mapA, &full[s], m0, k0);
             tma_load_2d(sa_ + 64 * BK * 2, &mapA, &full[s], m0 + 64, k0);
           }
-          if (BKM) {
+          if constexpr (MODE == 4) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) tma_load_2d(sb_ + j * kSlice * BK * 2, &mapB, &full[s], k0, slice_row[j]);
+          } else if (BKM) {
             tma_load_2d(sb_, &mapB, &full[s], k0, n0);
           } else {
 #pragma unroll
@@ -756,7 +796,8 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
     int i = 0;
     for (int w = blockIdx.x; w < nitem; w += gridDim.x, ++i) {
       const int t = w / S, sp = w % S;
-      const int m0 = tile_m(g, t, tiles_m, tiles_n) * BM, n0 = tile_n(g, t, tiles_m, tiles_n) * BN;
+      const int m0 = (MODE == 4 ? t / tiles_n : tile_m(g, t, tiles_m, tiles_n)) * BM,
+                n0 = MODE == 4 ? t % tiles_n : tile_n(g, t, tiles_m, tiles_n) * BN;
       const int acc = i & 1;
       const uint32_t aph = (i >> 1) & 1;
       mbar_wait_sleep(&tfull[acc], aph);
@@ -771,6 +812,8 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
         epilogue_lse(g, e, sa, taddr, row, n0, c_lo, c_hi, tile_n(g, t, tiles_m, tiles_n) * NSL + slice);
       else if constexpr (MODE == 3)
         epilogue_dz(g, e, sa, om, taddr, row, r0, n0, c_lo, c_hi, stg, lane);
+      else if constexpr (MODE == 4)
+        epilogue_slice(g, e, sa, taddr, row, n0, q, c_lo, c_hi, lane);
       else if (e.tma)
         epilogue_store_tma(g, e, om, taddr, row, r0, n0, c_lo, c_hi, stg, lane, &ebar[ew], ephase,
                            sp > 0 ? nullptr : e.bias);
@@ -857,11 +900,12 @@ void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const 
     DCU_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
-  const int nitem = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) * (MODE == 0 ? e.splits : 1);
+  const int nitem = ((g.M + BM - 1) / BM) * (MODE == 4 ? BM / 8 : (g.N + BN - 1) / BN) * (MODE == 0 ? e.splits : 1);
   const int cap = num_sms();
   const int grid = nitem < cap ? nitem : cap;  // persistent: all CTAs co-resident
-  ProfScope ps(MODE == 1 ? PROF_SAMPLE : MODE >= 2 ? PROF_LM_ROWS : PROF_GEMM_TC, s,
-               2.0 * g.M * g.N * static_cast<double>(g.K), 0);
+  ProfScope ps(MODE == 1 || MODE == 4 ? PROF_SAMPLE : MODE >= 2 ? PROF_LM_ROWS : PROF_GEMM_TC, s,
+               MODE == 4 ? 2.0 * g.M * kSlice * static_cast<double>(g.K) : 2.0 * g.M * g.N * static_cast<double>(g.K),
+               0);
   if (ps.keyed())
     snprintf(ps.key, sizeof(ps.key), "mode%d 128x%d M%d N%d K%d %c%c epi%d split%d", MODE, BN, g.M, g.N, g.K,
              AK ? 'k' : 'm', BKM ? 'k' : 'm', e.kind, MODE == 0 ? e.splits : 1);
@@ -1320,13 +1364,25 @@ int gemm_tc_sample(cudaStream_t s, const GemmShape& g, const float* bias, const 
   if (!make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) || !make_map(&mb, g.B, g.N, g.K, g.ldb, BK, kSampleBN)) return 0;
   OutMaps om;
   memset(&om, 0, sizeof(om));
-  if (!make_out_map(&om.f32, sa.logits, g.M, g.N, sa.logits_ld, true)) return 0;
+  if (sa.logits && !make_out_map(&om.f32, sa.logits, g.M, g.N, sa.logits_ld, true)) return 0;
   Epi e;
   e.bias = bias;
   SampleArgs a = sa;
   a.ntiles = gemm_tc_sample_tiles(g.N);
   launch<kSampleBN, 4, true, true, kSampleEPW, 1>(s, ma, mb, om, g, e, a);
   return a.ntiles;
+}
+
+bool gemm_tc_slice(cudaStream_t s, const GemmShape& g, const float* bias, const SampleArgs& sa) {
+  if (!legal(g) || !g.a_kmajor || !g.b_kmajor) return false;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) || !make_map(&mb, g.B, g.N, g.K, g.ldb, BK, kSlice)) return false;
+  OutMaps om;
+  memset(&om, 0, sizeof(om));
+  Epi e;
+  e.bias = bias;
+  launch<kSampleBN, 4, true, true, kSampleEPW, 4>(s, ma, mb, om, g, e, sa);
+  return true;
 }
 
 int gemm_tc_lse_tiles(int N) { return ((N + 255) / 256) * 2; }  // two column slices per tile (8 epilogue warps)

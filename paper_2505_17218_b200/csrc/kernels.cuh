@@ -115,14 +115,29 @@ void sample_rows(cudaStream_t s, const float* logits, int rows, int V, int bos, 
                  float* logp, int32_t* len, int32_t* tok_next, int max_len, float* part,
                  const int32_t* row_seq = nullptr);
 
+// The walk's state at the chosen 32-id slice (sample_scan phase 1 -> phase 2).
+struct SliceSel {
+  int sb;          // chosen slice (-1: the row's sequence is not active)
+  float target;    // u * total
+  float sbase;     // running sum before the slice
+  float ms;        // the slice's max at 1/T
+  float scale;     // sexp2((m_s - M) log2e)
+  float lse1;      // T = 1 log-sum-exp of the row
+};
 // The contract's walk over per-slice partials {m, Z, m1, Z1} (from sample_rows or the
 // fused LM-head GEMM epilogue) + the token bookkeeping (EOS, cap, logp at T = 1).
+// phase 0: one pass over stored fp32 logits; phase 1: down to the slice (-> sel);
+// phase 2: the id walk over the slice's logits recomputed by gemm_tc_slice (logits =
+// [rows x 32]); with dump != null phase 2 also counts recomputed logits that differ from
+// the dumped GEMM logits (dump + row * dump_ld) into *mismatches.
 void sample_scan(cudaStream_t s, const float* part, int nslices, const float* logits, int64_t logits_ld, int rows,
                  int V, int bos, int eos, float inv_t, const uint64_t* keys, int step, const int32_t* cap,
                  uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len,
                  bool compact = false,    // compact: {m, Z} records (fused epilogue at T = 1)
                  float* lse_out = nullptr,   // optional [seqs x max_len]: the row's T = 1 log-sum-exp
-                 const int32_t* row_seq = nullptr);  // row -> sequence (null = identity)
+                 const int32_t* row_seq = nullptr,   // row -> sequence (null = identity)
+                 int phase = 0, SliceSel* sel = nullptr, const float* dump = nullptr, int64_t dump_ld = 0,
+                 int* mismatches = nullptr);
 // dst[i] = src[idx[i]] (fp32 gather)
 void gather_f32(cudaStream_t s, const float* src, const int32_t* idx, int n, float* dst);
 

@@ -329,7 +329,34 @@ __global__ void sample_partials_k(const float* __restrict__ logits, int rows, in
   }
 }
 
-constexpr int kScanMaxB = 192;  // slices per lane block staged in shared memory (V <= 196608)
+constexpr int kScanMaxB = 192;
+
+// id search inside the chosen slice sb (the contract's last level) + the token bookkeeping
+// of policy.cpp:423-426 (EOS stops, cap, logp at T = 1); l = the slice's 32 fp32 logits
+__device__ __forceinline__ void scan_finish(const SliceSel& q, const float* l, int sq, int V, int bos, int eos,
+                                            float inv_t, int step, uint8_t* finished, int32_t* comp, float* logp,
+                                            int32_t* len, int32_t* tok_next, int max_len, float* lse_out) {
+  int tk = -1, last_i = -1;
+  float r = q.sbase;
+  for (int i = 0; i < kSlice; ++i) {
+    const int id = q.sb * kSlice + i;
+    if (id >= V || id == bos) continue;
+    const float e = sexp2(__fmul_rn(__fsub_rn(__fmul_rn(l[i], inv_t), q.ms), kLog2e));
+    r = __fmaf_rn(e, q.scale, r);
+    last_i = id;
+    if (q.target < r) {
+      tk = id;
+      break;
+    }
+  }
+  if (tk < 0) tk = last_i;
+  comp[static_cast<int64_t>(sq) * max_len + step] = tk;
+  logp[static_cast<int64_t>(sq) * max_len + step] = l[tk - q.sb * kSlice] - q.lse1;
+  if (lse_out) lse_out[static_cast<int64_t>(sq) * max_len + step] = q.lse1;
+  len[sq] = step + 1;
+  if (tk == eos) finished[sq] = 1;
+  tok_next[sq] = tk;
+}  // slices per lane block staged in shared memory (V <= 196608)
 
 // The inverse-CDF walk of the sampling contract (rule.cuh), one warp per row: lane j
 // owns a block of consecutive slices; block, slice and id sums are accumulated in the
@@ -340,14 +367,34 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
                                                      int V, int bos, int eos, float inv_t, const uint64_t* keys,
                                                      int step, const int32_t* cap, uint8_t* finished, int32_t* comp,
                                                      float* logp, int32_t* len, int32_t* tok_next, int max_len,
-                                                     bool compact, float* lse_out, const int32_t* row_seq) {
+                                                     bool compact, float* lse_out, const int32_t* row_seq, int phase,
+                                                     SliceSel* sel, const float* dump, int64_t dump_ld,
+                                                     int* mismatches) {
   pdl_wait();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= rows) return;
   const int sq = row_seq ? row_seq[row] : row;  // per-sequence state below, per-row records above
+  if (phase == 2) {  // finish: the chosen slice's logits, recomputed by gemm_tc_slice (row-major [rows x 32])
+    if (lane != 0) return;
+    const SliceSel q = sel[row];
+    if (q.sb < 0) return;
+    const float* l = logits + static_cast<int64_t>(row) * kSlice;
+    if (dump && mismatches) {  // parity runs: the recomputed slice must equal the GEMM's logits bit for bit
+      const float* ref = dump + static_cast<int64_t>(row) * dump_ld + q.sb * kSlice;
+      int bad = 0;
+      for (int i = 0; i < kSlice && q.sb * kSlice + i < V; ++i)
+        bad += __float_as_uint(ref[i]) != __float_as_uint(l[i]);
+      if (bad) atomicAdd(mismatches, bad);
+    }
+    scan_finish(q, l, sq, V, bos, eos, inv_t, step, finished, comp, logp, len, tok_next, max_len, lse_out);
+    return;
+  }
   const bool active = !finished[sq] && step < cap[sq];
   if (!active) {
-    if (lane == 0) tok_next[sq] = eos;
+    if (lane == 0) {
+      tok_next[sq] = eos;
+      if (phase == 1) sel[row].sb = -1;
+    }
     return;
   }
   // records {m, Z, m1, Z1}; at T = 1 the fused epilogue stores only {m, Z} (m1 = m, Z1 = Z)
@@ -453,31 +500,20 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
     sb = last_s;
     sbase = last_sbase;
   }
-  // id search inside slice sb
+  SliceSel q;
   const float4 p = rec(sb);
-  const float scale = sexp2(__fmul_rn(__fsub_rn(p.x, M), kLog2e));
-  const float* l = logits + static_cast<int64_t>(row) * logits_ld + sb * kSlice;
-  int tk = -1, last_i = -1;
-  r = sbase;
-  for (int i = 0; i < kSlice; ++i) {
-    const int id = sb * kSlice + i;
-    if (id >= V || id == bos) continue;
-    const float e = sexp2(__fmul_rn(__fsub_rn(__fmul_rn(l[i], inv_t), p.x), kLog2e));
-    r = __fmaf_rn(e, scale, r);
-    last_i = id;
-    if (target < r) {
-      tk = id;
-      break;
-    }
+  q.sb = sb;
+  q.target = target;
+  q.sbase = sbase;
+  q.ms = p.x;
+  q.scale = sexp2(__fmul_rn(__fsub_rn(p.x, M), kLog2e));
+  q.lse1 = M1 + logf(L1);  // T = 1 log-sum-exp over non-BOS ids (policy.cpp:424)
+  if (phase == 1) {  // select: the slice is recomputed by gemm_tc_slice, the walk finishes in phase 2
+    sel[row] = q;
+    return;
   }
-  if (tk < 0) tk = last_i;
-  comp[static_cast<int64_t>(sq) * max_len + step] = tk;
-  const float lse1 = M1 + logf(L1);  // T = 1 log-sum-exp over non-BOS ids (policy.cpp:424)
-  logp[static_cast<int64_t>(sq) * max_len + step] = l[tk - sb * kSlice] - lse1;
-  if (lse_out) lse_out[static_cast<int64_t>(sq) * max_len + step] = lse1;
-  len[sq] = step + 1;
-  if (tk == eos) finished[sq] = 1;
-  tok_next[sq] = tk;
+  scan_finish(q, logits + static_cast<int64_t>(row) * logits_ld + sb * kSlice, sq, V, bos, eos, inv_t, step, finished,
+              comp, logp, len, tok_next, max_len, lse_out);
 }
 
 // Row LSE from the LSE-mode GEMM partials; optionally logp = logit[y] - lse with the
@@ -897,9 +933,11 @@ void lse_reduce(cudaStream_t s, const float* part, int ntiles, int rows, float* 
 void sample_scan(cudaStream_t s, const float* part, int nslices, const float* logits, int64_t logits_ld, int rows,
                  int V, int bos, int eos, float inv_t, const uint64_t* keys, int step, const int32_t* cap,
                  uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len,
-                 bool compact, float* lse_out, const int32_t* row_seq) {
+                 bool compact, float* lse_out, const int32_t* row_seq, int phase, SliceSel* sel, const float* dump,
+                 int64_t dump_ld, int* mismatches) {
   launch_pdl(sample_scan_k, dim3(cdiv(rows, 8)), dim3(256), 0, s, part, nslices, logits, logits_ld, rows, V, bos, eos,
-             inv_t, keys, step, cap, finished, comp, logp, len, tok_next, max_len, compact, lse_out, row_seq);
+             inv_t, keys, step, cap, finished, comp, logp, len, tok_next, max_len, compact, lse_out, row_seq, phase, sel,
+             dump, dump_ld, mismatches);
   DCU_LAUNCHED();
 }
 

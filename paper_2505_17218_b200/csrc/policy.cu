@@ -1031,11 +1031,17 @@ struct Engine {
     // LM head + sampling step: fused tcgen05 epilogue (bf16) or GEMM + row kernel (fp32 parity path)
     const int nslices = (g.V + 31) / 32;
     float* part = ws.get<float>("d_part", static_cast<size_t>(S) * nslices * 4);
-    float* logits = ws.get<float>("d_logits", static_cast<size_t>(S) * g.V);
+    // fp32 logits rows exist only on the fp32 parity path; the bf16 sampler never stores them
+    float* logits = sizeof(T) == 4 ? ws.get<float>("d_logits", static_cast<size_t>(S) * g.V) : nullptr;
+    SliceSel* sel = ws.get<SliceSel>("d_sel", S);
+    float* slice_logits = ws.get<float>("d_slice_logits", static_cast<size_t>(S) * kSlice);
+    int* d_mism = ws.get<int>("d_mism", 1);
+    DCU_CHECK(cudaMemsetAsync(d_mism, 0, sizeof(int), st));
     auto lm_sample = [&](const T* yrows, int step, int R, const int32_t* row_seq) {
       if constexpr (sizeof(T) == 2) {
-        // the epilogue writes the logits straight into the parity dump when one is requested
-        float* lg = dump ? dump + static_cast<int64_t>(step) * g.V : logits;
+        // the sampling epilogue writes only the per-slice records (+ the logits into the
+        // parity dump when one is requested); the chosen slice of each row is recomputed
+        float* lg = dump ? dump + static_cast<int64_t>(step) * g.V : nullptr;
         const int64_t ld = dump ? static_cast<int64_t>(std::max(ML, 1)) * g.V : g.V;
         SampleArgs sa;
         sa.keys = d_keys;
@@ -1048,11 +1054,21 @@ struct Engine {
         GemmShape gs{R, g.V, g.d, yrows, g.d, true, W(L.wout), g.d, true};
         const int nt = gemm_tc_sample(st, gs, W32(L.bout), sa);
         if (nt > 0) {
-          sample_scan(st, part, nt, lg, ld, R, g.V, g.bos, g.eos, inv_t, d_keys, step, d_cap, d_fin,
+          sample_scan(st, part, nt, nullptr, 0, R, g.V, g.bos, g.eos, inv_t, d_keys, step, d_cap, d_fin,
                       P.d_comp.as<int32_t>(), P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML, inv_t == 1.f,
-                      lse_out, row_seq);
+                      lse_out, row_seq, 1, sel);
+          SampleArgs s2;
+          s2.sel = sel;
+          s2.logits = slice_logits;
+          if (!gemm_tc_slice(st, gs, W32(L.bout), s2)) throw Error(4, "slice recompute GEMM unavailable");
+          sample_scan(st, part, nt, slice_logits, kSlice, R, g.V, g.bos, g.eos, inv_t, d_keys, step, d_cap, d_fin,
+                      P.d_comp.as<int32_t>(), P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML, inv_t == 1.f,
+                      lse_out, row_seq, 2, sel, lg, ld, lg ? d_mism : nullptr);
           return;
         }
+        // not TMA-legal (e.g. a parity dump whose row pitch is not 16-byte aligned): the
+        // unfused GEMM + row kernels below
+        if (!logits) logits = ws.get<float>("d_logits", static_cast<size_t>(S) * g.V);
       }
       lse_all = false;
       Epi el = store(logits, g.V, nullptr, 0);
@@ -1104,7 +1120,7 @@ struct Engine {
         mm(R, g.qkvd, g.d, xT, g.d, true, W(b + L.wq), g.d, true, store(nullptr, 0, qkv, g.qkvd));
         kv_append<T>(st, qkv, R, g.qd, g.kvd, g.nkv, g.hd, j - 1, dr, kc_l, vc_l);
         // algorithmic bytes: every (sequence, kv head) reads its K and V rows once
-        const double kv_bytes = (sum_m * R / S + static_cast<double>(R) * j) * g.kvd * 2.0 * sizeof(T);
+        const double kv_bytes = (sum_m / G * R / S + static_cast<double>(R) * j) * g.kvd * 2.0 * sizeof(T);
         bool done = false;
         if constexpr (sizeof(T) == 2)
           done = attn_decode_tc(st, qkv, kp + kvp * l, vp + kvp * l, kc_l, vc_l, d_plen, R, G, pmax, j, dr, g.nh,
@@ -1150,6 +1166,12 @@ struct Engine {
       }
     }
     P.lse_valid = lse_all;
+    if (dump) {
+      int mism = 0;
+      d2h(st, &mism, d_mism, 1);
+      DCU_CHECK(cudaStreamSynchronize(st));
+      P.st.slice_recompute_mismatches = mism;
+    }
   }
 };
 

@@ -167,6 +167,8 @@ def test_sampled_tokens_bit_exact_under_logits_dump(ctx, arch, dtype):
         for j in range(L):
             tok = O.sample_rule(dump[s, j], arch["bos_id"], inv_t, key, j)
             assert tok == ro.completions[s, j], (s, j)
+    # the bf16 sampler walks a slice recomputed by a second GEMM; it must equal the dump
+    assert pol.stats()["slice_recompute_mismatches"] == 0
     pol.close()
 
 

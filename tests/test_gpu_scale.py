@@ -140,6 +140,7 @@ def test_sampler_full_length_qwen_vocab(ctx, arch):
     ro = pol.sample(prompts, G, ML, temperature=T, round_seed=13)
     _, checked = check_tokens(pol, ro, prompts, G, ML, 13, 1.0, arch["bos_id"])
     assert checked >= 2 * G * 900
+    assert pol.stats()["slice_recompute_mismatches"] == 0   # recomputed slices == the GEMM's logits
     pol.set_logits_dump(False)
     # decode-path log-probs vs the teacher-forced forward on the same sequences
     ro = pol.sample(prompts, G, ML, temperature=T, round_seed=13)
@@ -197,6 +198,7 @@ def test_true_c2_width(ctx):
     pol.set_logits_dump(True)
     ro = pol.sample(prompts, G, ML, temperature=T, round_seed=3)
     check_tokens(pol, ro, prompts, G, ML, 3, float(np.float32(1.0 / T)), arch["bos_id"])
+    assert pol.stats()["slice_recompute_mismatches"] == 0
     pol.set_logits_dump(False)
     ro = pol.sample(prompts, G, ML, temperature=1.0, round_seed=3)
     comps = [list(ro.completion(s)) for s in range(len(prompts) * G)]
