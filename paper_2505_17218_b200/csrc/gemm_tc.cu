@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 
 #include "gemm.cuh"
 #include "rule.cuh"
@@ -1268,10 +1269,33 @@ bool raster_n_fast(const GemmShape& g) {
   return a > 2.0 * b && a > 48e6;
 }
 
+// Skinny GEMMs (at most one 128-row tile: small-batch decode, e.g. the GRPO-style arm's 32
+// sequences) stream their weight matrix through every SM only with narrow N tiles: one
+// 128 x 64 (N >= 4096) or 128 x 32 tile per CTA, the whole K per tile, so the per-element
+// accumulation order stays that of every other tile shape (scheduling independence).
+bool gemm_tc_skinny(cudaStream_t s, const GemmShape& g, const Epi& e) {
+  const int BN = g.N >= 64 * 64 ? 64 : 32;
+  CUtensorMap ma, mb;
+  bool ok = g.a_kmajor ? make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) : make_map(&ma, g.A, g.K, g.M, g.lda, 64, BK);
+  ok = ok && (g.b_kmajor ? make_map(&mb, g.B, g.N, g.K, g.ldb, BK, BN) : make_map(&mb, g.B, g.K, g.N, g.ldb, 64, BK));
+  if (!ok) return false;
+  OutMaps om;
+  memset(&om, 0, sizeof(om));
+  Epi et = e;
+  et.tma = out_maps_for(g, e, &om);
+  et.splits = 1;
+  if (BN == 64) dispatch_majors<64, 8>(s, ma, mb, om, g, et);  // 8 x 24 KB stages
+  else dispatch_majors<32, 8>(s, ma, mb, om, g, et);           // 8 x 20 KB stages
+  return true;
+}
+
 bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
   if (!legal(g_in)) return false;
   GemmShape g = g_in;
   g.n_fast = raster_n_fast(g);
+  if (g.M <= BM && g.b_kmajor && e.kind != EPI_ACCUM && knob(KNOB_GEMM_PAIR) == 0 && g.N <= 16384 &&
+      gemm_tc_skinny(s, g, e))
+    return true;
   // Tile shape by the persistent schedule: time ~ rounds x per-tile cost, rounds =
   // ceil(tiles / concurrent CTAs). Measured per-SM efficiencies: 128x128 tiles 0.76
   // (shared-memory bound), 128x256 1.0, CTA-pair 256x256 1.12 (B staged half per SM).
@@ -1429,8 +1453,38 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 }  // namespace
 
+namespace {
+// Encoded maps by (base, shape, box, type): the decode re-launches the same ~8 GEMM shapes on
+// the same buffers every step, and cuTensorMapEncodeTiled costs more host time than the
+// launch itself at small batch. Per thread, bounded (cleared when it fills up).
+struct MapKey {
+  const void* base;
+  int64_t rows, cols, ld;
+  int box_cols, box_rows, flags;
+  bool operator==(const MapKey& o) const {
+    return base == o.base && rows == o.rows && cols == o.cols && ld == o.ld && box_cols == o.box_cols &&
+           box_rows == o.box_rows && flags == o.flags;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    uint64_t h = reinterpret_cast<uint64_t>(k.base) * 0x9E3779B97F4A7C15ull;
+    for (int64_t v : {k.rows, k.cols, k.ld, static_cast<int64_t>(k.box_cols) << 20 | k.box_rows << 4 | k.flags})
+      h = (h ^ static_cast<uint64_t>(v)) * 0xBF58476D1CE4E5B9ull;
+    return static_cast<size_t>(h ^ (h >> 31));
+  }
+};
+thread_local std::unordered_map<MapKey, CUtensorMap, MapKeyHash> t_maps;
+}  // namespace
+
 bool tma_map_2d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_cols, int box_rows,
                 bool f32, int swizzle_bytes, bool l2_promote) {
+  const MapKey key{base, rows, cols, ld, box_cols, box_rows, (f32 ? 1 : 0) | (l2_promote ? 2 : 0) | (swizzle_bytes << 2)};
+  auto it = t_maps.find(key);
+  if (it != t_maps.end()) {
+    *m = it->second;
+    return true;
+  }
   auto fn = encode_fn();
   const int esz = f32 ? 4 : 2;
   if (!fn || !base || ((reinterpret_cast<uintptr_t>(base) | static_cast<uintptr_t>(ld * esz)) & 15)) return false;
@@ -1446,7 +1500,10 @@ bool tma_map_2d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, in
                   const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                   l2_promote ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  if (r != CUDA_SUCCESS) return false;
+  if (t_maps.size() >= 4096) t_maps.clear();
+  t_maps.emplace(key, *m);
+  return true;
 }
 
 
