@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(32) attn_decode_k(const T* __restrict__ qkv, c
   const int qd = nh * hd, kvd = nkv * hd, qkvd = qd + 2 * kvd;
   const int kvh = h / (nh / nkv);
   const int sq = dr_seq(dr, s);
+  if (dr.step) n_comp = *dr.step;
   const int p = sq / G, m = prompt_len[sq];
   const int nk = m + n_comp;
   float* sc = sm;

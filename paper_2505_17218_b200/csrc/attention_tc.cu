@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(DecCfg<HD>::NW * 32)
   using Cf = DecCfg<HD>;
   constexpr int KC = Cf::KC, ST = Cf::ST, UNITS = Cf::UNITS;
   pdl_wait();
+  if (dr.step) n_comp = *dr.step;
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * Cf::NW + warp;

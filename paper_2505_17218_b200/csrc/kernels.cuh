@@ -31,6 +31,7 @@ struct DecodeRows {
   const int32_t* row_seq = nullptr;
   const int32_t* ptab = nullptr;
   int max_pages = 0;
+  const int* step = nullptr;  // CUDA-graph replay: the decode step read from device memory
 };
 __device__ __forceinline__ int dr_seq(const DecodeRows& dr, int row) { return dr.row_seq ? dr.row_seq[row] : row; }
 // element offset of completion slot `slot` of (seq, kv head) in a layer's page pool
@@ -43,7 +44,7 @@ __device__ __forceinline__ int64_t kv_slot_off(const DecodeRows& dr, int seq, in
 template <class T>
 void embed_decode(cudaStream_t s, const T* tok_emb, const T* pos_emb, const int32_t* tok,
                   const int32_t* prompt_len, int step, int rows, int d, float* x32, T* xT,
-                  const int32_t* row_seq = nullptr);
+                  const int32_t* row_seq = nullptr, const int* step_dev = nullptr);
 // deterministic (stable sort by id + in-order run sums); tmp: embed_bwd_tmp_bytes(rows),
 // part: embed_bwd_part_floats(rows, d) floats of window partials
 size_t embed_bwd_tmp_bytes(int rows);
@@ -137,7 +138,9 @@ void sample_scan(cudaStream_t s, const float* part, int nslices, const float* lo
                  float* lse_out = nullptr,   // optional [seqs x max_len]: the row's T = 1 log-sum-exp
                  const int32_t* row_seq = nullptr,   // row -> sequence (null = identity)
                  int phase = 0, SliceSel* sel = nullptr, const float* dump = nullptr, int64_t dump_ld = 0,
-                 int* mismatches = nullptr);
+                 int* mismatches = nullptr, const int* step_dev = nullptr);
+// step_dev += 1 (the last node of a captured decode step)
+void step_advance(cudaStream_t s, int* step_dev);
 // dst[i] = src[idx[i]] (fp32 gather)
 void gather_f32(cudaStream_t s, const float* src, const int32_t* idx, int n, float* dst);
 

@@ -99,8 +99,9 @@ __global__ void embed_fwd_k(const T* E, const T* P, const int32_t* tok, const in
 
 template <class T>
 __global__ void embed_decode_k(const T* E, const T* P, const int32_t* tok, const int32_t* plen, int step, int rows,
-                               int d, float* x32, T* xT, const int32_t* row_seq) {
+                               int d, float* x32, T* xT, const int32_t* row_seq, const int* step_dev) {
   pdl_wait();
+  if (step_dev) step = *step_dev;
   const int64_t n = static_cast<int64_t>(rows) * d;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int r = static_cast<int>(i / d), c = static_cast<int>(i % d);
@@ -369,8 +370,9 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
                                                      float* logp, int32_t* len, int32_t* tok_next, int max_len,
                                                      bool compact, float* lse_out, const int32_t* row_seq, int phase,
                                                      SliceSel* sel, const float* dump, int64_t dump_ld,
-                                                     int* mismatches) {
+                                                     int* mismatches, const int* step_dev) {
   pdl_wait();
+  if (step_dev) step = *step_dev;
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= rows) return;
   const int sq = row_seq ? row_seq[row] : row;  // per-sequence state below, per-row records above
@@ -658,6 +660,7 @@ template <class T>
 __global__ void kv_append_k(const T* qkv, int rows, int qd, int kvd, int nkv, int hd, int slot, DecodeRows dr, T* ks,
                             T* vs) {
   pdl_wait();
+  if (dr.step) slot = *dr.step - 1;
   const int qkvd = qd + 2 * kvd;
   const int64_t n = static_cast<int64_t>(rows) * kvd;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -832,9 +835,9 @@ void embed_fwd(cudaStream_t s, const T* E, const T* P, const int32_t* tok, const
 }
 template <class T>
 void embed_decode(cudaStream_t s, const T* E, const T* P, const int32_t* tok, const int32_t* plen, int step,
-                  int rows, int d, float* x32, T* xT, const int32_t* row_seq) {
+                  int rows, int d, float* x32, T* xT, const int32_t* row_seq, const int* step_dev) {
   launch_pdl(embed_decode_k<T>, dim3(grid1d(static_cast<int64_t>(rows) * d)), dim3(256), 0, s, E, P, tok, plen, step,
-             rows, d, x32, xT, row_seq);
+             rows, d, x32, xT, row_seq, step_dev);
   DCU_LAUNCHED();
 }
 size_t embed_bwd_tmp_bytes(int rows) {
@@ -934,10 +937,19 @@ void sample_scan(cudaStream_t s, const float* part, int nslices, const float* lo
                  int V, int bos, int eos, float inv_t, const uint64_t* keys, int step, const int32_t* cap,
                  uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len,
                  bool compact, float* lse_out, const int32_t* row_seq, int phase, SliceSel* sel, const float* dump,
-                 int64_t dump_ld, int* mismatches) {
+                 int64_t dump_ld, int* mismatches, const int* step_dev) {
   launch_pdl(sample_scan_k, dim3(cdiv(rows, 8)), dim3(256), 0, s, part, nslices, logits, logits_ld, rows, V, bos, eos,
              inv_t, keys, step, cap, finished, comp, logp, len, tok_next, max_len, compact, lse_out, row_seq, phase, sel,
-             dump, dump_ld, mismatches);
+             dump, dump_ld, mismatches, step_dev);
+}
+
+__global__ void step_advance_k(int* step) {
+  pdl_wait();
+  *step += 1;
+}
+void step_advance(cudaStream_t s, int* step_dev) {
+  launch_pdl(step_advance_k, dim3(1), dim3(1), 0, s, step_dev);
+  DCU_LAUNCHED();
   DCU_LAUNCHED();
 }
 
@@ -1060,7 +1072,7 @@ void advantage_filter(cudaStream_t s, const double* r, int n, int G, int kind, i
 #define INST(T)                                                                                                   \
   template void embed_fwd<T>(cudaStream_t, const T*, const T*, const int32_t*, const int32_t*, int, int, float*, T*); \
   template void embed_decode<T>(cudaStream_t, const T*, const T*, const int32_t*, const int32_t*, int, int, int,     \
-                                float*, T*, const int32_t*);                                                      \
+                                float*, T*, const int32_t*, const int*);                                          \
   template void colsum_acc<T>(cudaStream_t, const T*, int64_t, int, int, float*, float*);                        \
   template size_t colsum_tmp_floats<T>(int, int);                                                                 \
   template void lm_rows<T>(cudaStream_t, const float*, int, int, int, const int32_t*, const float*, float*, T*);  \

@@ -1037,7 +1037,7 @@ struct Engine {
     float* slice_logits = ws.get<float>("d_slice_logits", static_cast<size_t>(S) * kSlice);
     int* d_mism = ws.get<int>("d_mism", 1);
     DCU_CHECK(cudaMemsetAsync(d_mism, 0, sizeof(int), st));
-    auto lm_sample = [&](const T* yrows, int step, int R, const int32_t* row_seq) {
+    auto lm_sample = [&](const T* yrows, int step, int R, const int32_t* row_seq, const int* sdev) {
       if constexpr (sizeof(T) == 2) {
         // the sampling epilogue writes only the per-slice records (+ the logits into the
         // parity dump when one is requested); the chosen slice of each row is recomputed
@@ -1056,14 +1056,14 @@ struct Engine {
         if (nt > 0) {
           sample_scan(st, part, nt, nullptr, 0, R, g.V, g.bos, g.eos, inv_t, d_keys, step, d_cap, d_fin,
                       P.d_comp.as<int32_t>(), P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML, inv_t == 1.f,
-                      lse_out, row_seq, 1, sel);
+                      lse_out, row_seq, 1, sel, nullptr, 0, nullptr, sdev);
           SampleArgs s2;
           s2.sel = sel;
           s2.logits = slice_logits;
           if (!gemm_tc_slice(st, gs, W32(L.bout), s2)) throw Error(4, "slice recompute GEMM unavailable");
           sample_scan(st, part, nt, slice_logits, kSlice, R, g.V, g.bos, g.eos, inv_t, d_keys, step, d_cap, d_fin,
                       P.d_comp.as<int32_t>(), P.d_logp.as<float>(), P.d_len.as<int32_t>(), d_tok, ML, inv_t == 1.f,
-                      lse_out, row_seq, 2, sel, lg, ld, lg ? d_mism : nullptr);
+                      lse_out, row_seq, 2, sel, lg, ld, lg ? d_mism : nullptr, sdev);
           return;
         }
         // not TMA-legal (e.g. a parity dump whose row pitch is not 16-byte aligned): the
@@ -1081,7 +1081,7 @@ struct Engine {
                                     sizeof(float) * static_cast<size_t>(std::max(ML, 1)) * g.V, logits,
                                     sizeof(float) * g.V, sizeof(float) * g.V, R, cudaMemcpyDeviceToDevice, st));
     };
-    lm_sample(yT, 0, S, nullptr);
+    lm_sample(yT, 0, S, nullptr, nullptr);
 
     // Decode steps: one position of every active sequence per step. Every projection uses
     // the store form (fp32 + bf16 outputs in the epilogue), whose fp32 summation order
@@ -1096,30 +1096,26 @@ struct Engine {
     T* u = ws.get<T>("d_u", static_cast<size_t>(S) * g.H);
     std::vector<uint8_t> hfin(S);
     int R = S;
-    const DecodeRows dr{d_rows, d_ptab, maxp};
-    for (int j = 1; j < maxcap; ++j) {
-      if ((j - 1) % kPage == 0) {  // every active row starts a new page of completion slots
-        for (int r = 0; r < R; ++r) {
-          if (free_pages.empty())
-            throw Error(2, "decode KV page pool exhausted (" + std::to_string(npool) +
-                               " pages): raise dashcu_set_kv_pages or sample fewer sequences");
-          const int32_t pg = free_pages.back();
-          free_pages.pop_back();
-          h_ptab[static_cast<size_t>(act[r]) * maxp + (j - 1) / kPage] = pg;
-          owned[act[r]].push_back(pg);
-        }
-        P.st.kv_pages_peak = std::max<int64_t>(P.st.kv_pages_peak, npool - static_cast<int64_t>(free_pages.size()));
-        h2d(st, d_ptab, h_ptab.data(), h_ptab.size());
-      }
-      P.st.decode_row_steps += R;
-      embed_decode<T>(st, W(L.tok), W(L.pos), d_tok, d_plen, j, R, g.d, x32, xT, d_rows);
+    // CUDA-graph replay of the decode step (bf16, no profiler events, no parity dump): the
+    // step index lives in device memory (d_step, advanced by the graph's last node), so one
+    // captured step replays until the active row count changes at an EOS check; the page
+    // table uploads stay outside the graph, stream-ordered before the replays that use them
+    const bool use_graph = sizeof(T) == 2 && !dump && g_prof_mask == 0 && knob(KNOB_DECODE_GRAPH) != 0;
+    int* d_step = ws.get<int>("d_step", 1);
+    cudaGraphExec_t gexec = nullptr;
+    int graph_rows = -1;
+    bool step_set = false;
+    auto decode_step = [&](int j, const int* sdev) {
+      const DecodeRows dr{d_rows, d_ptab, maxp, sdev};
+      embed_decode<T>(st, W(L.tok), W(L.pos), d_tok, d_plen, j, R, g.d, x32, xT, d_rows, sdev);
       for (int l = 0; l < g.L; ++l) {
         const int64_t b = lb(l);
         T* kc_l = kc + kvc * l;
         T* vc_l = vc + kvc * l;
         mm(R, g.qkvd, g.d, xT, g.d, true, W(b + L.wq), g.d, true, store(nullptr, 0, qkv, g.qkvd));
         kv_append<T>(st, qkv, R, g.qd, g.kvd, g.nkv, g.hd, j - 1, dr, kc_l, vc_l);
-        // algorithmic bytes: every (sequence, kv head) reads its K and V rows once
+        // algorithmic bytes: every (sequence, kv head) reads its K and V rows once (a group's
+        // prompt KV once per group)
         const double kv_bytes = (sum_m / G * R / S + static_cast<double>(R) * j) * g.kvd * 2.0 * sizeof(T);
         bool done = false;
         if constexpr (sizeof(T) == 2)
@@ -1143,7 +1139,43 @@ struct Engine {
         e2.ldr = g.d;
         mm(R, g.d, g.H, u, g.H, true, W(b + L.w2), g.H, true, e2);
       }
-      lm_sample(xT, j, R, d_rows);
+      lm_sample(xT, j, R, d_rows, sdev);
+    };
+    for (int j = 1; j < maxcap; ++j) {
+      if ((j - 1) % kPage == 0) {  // every active row starts a new page of completion slots
+        for (int r = 0; r < R; ++r) {
+          if (free_pages.empty())
+            throw Error(2, "decode KV page pool exhausted (" + std::to_string(npool) +
+                               " pages): raise dashcu_set_kv_pages or sample fewer sequences");
+          const int32_t pg = free_pages.back();
+          free_pages.pop_back();
+          h_ptab[static_cast<size_t>(act[r]) * maxp + (j - 1) / kPage] = pg;
+          owned[act[r]].push_back(pg);
+        }
+        P.st.kv_pages_peak = std::max<int64_t>(P.st.kv_pages_peak, npool - static_cast<int64_t>(free_pages.size()));
+        h2d(st, d_ptab, h_ptab.data(), h_ptab.size());
+      }
+      P.st.decode_row_steps += R;
+      if (use_graph && j > 1) {  // step 1 runs eagerly (attributes, tensor maps, buffers set up)
+        if (!step_set) {
+          h2d(st, d_step, &j, 1);
+          step_set = true;
+        }
+        if (graph_rows != R) {  // (re)capture one step for this many rows
+          if (gexec) DCU_CHECK(cudaGraphExecDestroy(gexec));
+          cudaGraph_t graph;
+          DCU_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+          decode_step(j, d_step);
+          step_advance(st, d_step);
+          DCU_CHECK(cudaStreamEndCapture(st, &graph));
+          DCU_CHECK(cudaGraphInstantiate(&gexec, graph, 0));
+          DCU_CHECK(cudaGraphDestroy(graph));
+          graph_rows = R;
+        }
+        DCU_CHECK(cudaGraphLaunch(gexec, st));
+      } else {
+        decode_step(j, nullptr);
+      }
       if ((j & 31) == 0 && g.eos >= 0) {  // EOS check: retire finished sequences, stop when none is left
         d2h(st, hfin.data(), d_fin, S);
         DCU_CHECK(cudaStreamSynchronize(st));
@@ -1164,6 +1196,10 @@ struct Engine {
           h2d(st, d_rows, act.data(), R);
         }
       }
+    }
+    if (gexec) {
+      DCU_CHECK(cudaStreamSynchronize(st));
+      DCU_CHECK(cudaGraphExecDestroy(gexec));
     }
     P.lse_valid = lse_all;
     if (dump) {
