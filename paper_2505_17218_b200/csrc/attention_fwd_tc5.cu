@@ -90,7 +90,8 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 template <int HD>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_tc5_k(const __grid_constant__ CUtensorMap mQKV, const int32_t* __restrict__ seq_start, int nh, int nkv,
-                   int nqt_max, bf16* __restrict__ ctx, float* __restrict__ lse, float scale_log2) {
+                   int nqt_max, bf16* __restrict__ ctx, float* __restrict__ lse, float scale_log2,
+                   bf16* __restrict__ ctx_lo) {
   using FLay = dashcu::FLay<HD>;
   constexpr int kHD = HD, kTile = FLay::kTile, kST = FLay::kST, kQS = FLay::kQS;
   constexpr uint32_t kTS0 = FLay::TS0, kTS1 = FLay::TS1, kTO0 = FLay::TO0, kTO1 = FLay::TO1;
@@ -291,8 +292,10 @@ __global__ void __launch_bounds__(384, 1)
           const float p0 = ex2(a0);
           // a fraction of the exponentials on the FMA pipe (the exp loop is MUFU-bound)
           const float p1 = (kSplitExp && ((c >> 1) % kSplitEvery == 0)) ? ex2_poly(a1) : ex2(a1);
-          rs2[(c >> 1) & 1] = f2_add(rs2[(c >> 1) & 1], f2_pack(p0, p1));
           pk[c >> 1] = pack2(p0, p1);
+          // the row sum adds the bf16-rounded values the PV product consumes (O / l consistent)
+          rs2[(c >> 1) & 1] = f2_add(rs2[(c >> 1) & 1], f2_pack(__uint_as_float(pk[c >> 1] << 16),
+                                                                __uint_as_float(pk[c >> 1] & 0xffff0000u)));
         }
         float r0, r1, r2, r3;
         f2_unpack(rs2[0], r0, r1);
@@ -334,6 +337,15 @@ __global__ void __launch_bounds__(384, 1)
           v.z = pack2(acc[i + 4] * inv, acc[i + 5] * inv);
           v.w = pack2(acc[i + 6] * inv, acc[i + 7] * inv);
           *reinterpret_cast<uint4*>(out + i) = v;
+          if (ctx_lo) {  // O - bf16(O), for the backward's D
+            const uint32_t hv[4] = {v.x, v.y, v.z, v.w};
+            uint32_t lv[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              lv[k] = pack2(acc[i + 2 * k] * inv - __uint_as_float(hv[k] << 16),
+                            acc[i + 2 * k + 1] * inv - __uint_as_float(hv[k] & 0xffff0000u));
+            *reinterpret_cast<uint4*>(ctx_lo + (out - ctx) + i) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+          }
         }
         if (hf == 0) lse[static_cast<int64_t>(s0 + q) * nh + h] = (m + __log2f(lt)) * 0.6931471805599453f;
       }
@@ -349,7 +361,7 @@ __global__ void __launch_bounds__(384, 1)
 namespace {
 template <int HD>
 void launch_fwd_tc5(cudaStream_t s, const CUtensorMap& mq, const int32_t* seq_start, int n_seq, int nqt, int nh,
-                    int nkv, bf16* ctx, float* lse) {
+                    int nkv, bf16* ctx, float* lse, bf16* ctx_lo) {
   static bool attr = false;
   if (!attr) {
     DCU_CHECK(cudaFuncSetAttribute(attn_fwd_tc5_k<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, FLay<HD>::BYTES));
@@ -357,13 +369,13 @@ void launch_fwd_tc5(cudaStream_t s, const CUtensorMap& mq, const int32_t* seq_st
   }
   dim3 grid(n_seq * nkv, 2 * nqt);
   attn_fwd_tc5_k<HD><<<grid, 384, FLay<HD>::BYTES, s>>>(mq, seq_start, nh, nkv, nqt, ctx, lse,
-                                                        1.4426950408889634f / sqrtf(static_cast<float>(HD)));
+                                                        1.4426950408889634f / sqrtf(static_cast<float>(HD)), ctx_lo);
   DCU_LAUNCHED();
 }
 }  // namespace
 
 bool attn_fwd_tc5(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int n_seq, int max_len, int rows, int nh,
-                  int nkv, int hd, bf16* ctx, float* lse) {
+                  int nkv, int hd, bf16* ctx, float* lse, bf16* ctx_lo) {
   if ((hd != 64 && hd != 128) || nh % nkv) return false;
   const int force = knob(KNOB_ATTN_FWD);
   if (force == 1) return false;
@@ -375,9 +387,9 @@ bool attn_fwd_tc5(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int
   if (!tma_map_2d(&mq, qkv, rows, qkvd, qkvd, 64, 128, false, 128, true)) return false;  // one swizzle atom per box
   const int nqt = (max_len + kQ - 1) / kQ;
   if (hd == 64)
-    launch_fwd_tc5<64>(s, mq, seq_start, n_seq, nqt, nh, nkv, ctx, lse);
+    launch_fwd_tc5<64>(s, mq, seq_start, n_seq, nqt, nh, nkv, ctx, lse, ctx_lo);
   else
-    launch_fwd_tc5<128>(s, mq, seq_start, n_seq, nqt, nh, nkv, ctx, lse);
+    launch_fwd_tc5<128>(s, mq, seq_start, n_seq, nqt, nh, nkv, ctx, lse, ctx_lo);
   return true;
 }
 

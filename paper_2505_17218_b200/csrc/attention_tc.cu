@@ -258,7 +258,7 @@ struct FwdCfg {
 template <int HD>
 __global__ void __launch_bounds__(128) attn_fwd_tc_k(const bf16* __restrict__ qkv, const int32_t* __restrict__ seq_start,
                                                      int nh, int nkv, bf16* __restrict__ ctx, float* __restrict__ lse,
-                                                     float scale_log2) {
+                                                     float scale_log2, bf16* __restrict__ ctx_lo) {
   using Cf = FwdCfg<HD>;
   constexpr int UNITS = Cf::UNITS;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -356,7 +356,8 @@ __global__ void __launch_bounds__(128) attn_fwd_tc_k(const bf16* __restrict__ qk
     for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float p = sc[nt][e] == -FLT_MAX ? 0.f : exp2f(sc[nt][e] - mrow[e >> 1]);
+        // rounded to bf16 here, as the PV product consumes it, so the normaliser matches O
+        const float p = sc[nt][e] == -FLT_MAX ? 0.f : __bfloat162float(__float2bfloat16_rn(exp2f(sc[nt][e] - mrow[e >> 1])));
         sc[nt][e] = p;
         lrow[e >> 1] += p;
       }
@@ -391,22 +392,31 @@ __global__ void __launch_bounds__(128) attn_fwd_tc_k(const bf16* __restrict__ qk
     const float inv = 1.f / lrow[hh];
     bf16* out = ctx + static_cast<int64_t>(s0 + qr) * qd + h * HD;
 #pragma unroll
-    for (int nt2 = 0; nt2 < HD / 8; ++nt2)
-      *reinterpret_cast<uint32_t*>(out + nt2 * 8 + t * 2) = pack_bf16(o[nt2][2 * hh] * inv, o[nt2][2 * hh + 1] * inv);
+    for (int nt2 = 0; nt2 < HD / 8; ++nt2) {
+      const float v0 = o[nt2][2 * hh] * inv, v1 = o[nt2][2 * hh + 1] * inv;
+      const uint32_t hi = pack_bf16(v0, v1);
+      *reinterpret_cast<uint32_t*>(out + nt2 * 8 + t * 2) = hi;
+      if (ctx_lo) {
+        const __nv_bfloat162 h2 = *reinterpret_cast<const __nv_bfloat162*>(&hi);
+        *reinterpret_cast<uint32_t*>(ctx_lo + (out - ctx) + nt2 * 8 + t * 2) =
+            pack_bf16(v0 - __low2float(h2), v1 - __high2float(h2));
+      }
+    }
     if (t == 0) lse[static_cast<int64_t>(s0 + qr) * nh + h] = (mrow[hh] + log2f(lrow[hh])) * 0.6931471805599453f;
   }
 }
 
 // D[row][h] = sum_i dO[row][h][i] * O[row][h][i]   (the reference's wsum, policy.cpp:298-304)
-__global__ void attn_bwd_dot_k(const bf16* __restrict__ dctx, const bf16* __restrict__ ctx, int rows, int nh, int hd,
-                               float* __restrict__ D) {
+__global__ void attn_bwd_dot_k(const bf16* __restrict__ dctx, const bf16* __restrict__ ctx,
+                               const bf16* __restrict__ ctx_lo, int rows, int nh, int hd, float* __restrict__ D) {
   const int64_t n = static_cast<int64_t>(rows) * nh;
   const int lane = threadIdx.x & 31;
   for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < n; w += (gridDim.x * (int64_t)blockDim.x) >> 5) {
     const bf16* a = dctx + w * hd;
     const bf16* b = ctx + w * hd;
     float s = 0.f;
-    for (int i = lane; i < hd; i += 32) s += __bfloat162float(a[i]) * __bfloat162float(b[i]);
+    for (int i = lane; i < hd; i += 32)
+      s += __bfloat162float(a[i]) * (__bfloat162float(b[i]) + (ctx_lo ? __bfloat162float(ctx_lo[w * hd + i]) : 0.f));
     s = warp_sum(s);
     if (lane == 0) D[w] = s;
   }
@@ -626,19 +636,19 @@ void smem_attr(K k, int bytes) {
 }  // namespace
 
 bool attn_fwd_tc(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int n_seq, int max_len, int rows, int nh,
-                 int nkv, int hd, bf16* ctx, float* lse, double alg_flops) {
+                 int nkv, int hd, bf16* ctx, float* lse, double alg_flops, bf16* ctx_lo) {
   if (hd != 64 && hd != 128) return false;
   if (n_seq <= 0) return true;
   ProfScope ps(PROF_ATTN_FWD, s, alg_flops, 0);
-  if (attn_fwd_tc5(s, qkv, seq_start, n_seq, max_len, rows, nh, nkv, hd, ctx, lse)) return true;
+  if (attn_fwd_tc5(s, qkv, seq_start, n_seq, max_len, rows, nh, nkv, hd, ctx, lse, ctx_lo)) return true;
   const float sl2 = kLog2e / sqrtf(static_cast<float>(hd));
   dim3 grid((max_len + 63) / 64, n_seq, nh);
   if (hd == 64) {
     smem_attr(attn_fwd_tc_k<64>, FwdCfg<64>::SMEM);
-    attn_fwd_tc_k<64><<<grid, 128, FwdCfg<64>::SMEM, s>>>(qkv, seq_start, nh, nkv, ctx, lse, sl2);
+    attn_fwd_tc_k<64><<<grid, 128, FwdCfg<64>::SMEM, s>>>(qkv, seq_start, nh, nkv, ctx, lse, sl2, ctx_lo);
   } else {
     smem_attr(attn_fwd_tc_k<128>, FwdCfg<128>::SMEM);
-    attn_fwd_tc_k<128><<<grid, 128, FwdCfg<128>::SMEM, s>>>(qkv, seq_start, nh, nkv, ctx, lse, sl2);
+    attn_fwd_tc_k<128><<<grid, 128, FwdCfg<128>::SMEM, s>>>(qkv, seq_start, nh, nkv, ctx, lse, sl2, ctx_lo);
   }
   DCU_LAUNCHED();
   return true;
@@ -646,11 +656,11 @@ bool attn_fwd_tc(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int 
 
 bool attn_bwd_tc(cudaStream_t s, const bf16* qkv, const bf16* ctx, const bf16* dctx, const float* lse,
                  const int32_t* seq_start, int n_seq, int max_len, int rows, int nh, int nkv, int hd, float* Dbuf,
-                 float* dq32, float* dkv32, double alg_flops) {
+                 float* dq32, float* dkv32, double alg_flops, const bf16* ctx_lo) {
   if (hd != 64 && hd != 128) return false;
   if (n_seq <= 0) return true;
   ProfScope ps(PROF_ATTN_BWD, s, alg_flops, 0);
-  attn_bwd_dot_k<<<kNumSMs * 8, 256, 0, s>>>(dctx, ctx, rows, nh, hd, Dbuf);
+  attn_bwd_dot_k<<<kNumSMs * 8, 256, 0, s>>>(dctx, ctx, ctx_lo, rows, nh, hd, Dbuf);
   DCU_LAUNCHED();
   DCU_CHECK(cudaMemsetAsync(dq32, 0, sizeof(float) * static_cast<size_t>(rows) * nh * hd, s));
   if (attn_bwd_tc5(s, qkv, dctx, lse, Dbuf, seq_start, n_seq, max_len, rows, nh, nkv, hd, dq32, dkv32)) return true;

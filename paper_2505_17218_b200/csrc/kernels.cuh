@@ -69,15 +69,21 @@ void attn_bwd_varlen(cudaStream_t s, const T* qkv, const T* dctx, const float* l
                      int n_seq, int max_len, int nh, int nkv, int hd, float* dq32, float* dkv32, double alg_flops = 0);
 // Tensor-core (mma.sync) flash attention for the bf16 path; head_dim 64/128.
 // Return false when the geometry is not covered (caller uses the CUDA-core kernels).
+//
+// Backward-consistent forward (bf16): the softmax normaliser is the sum of the bf16-ROUNDED
+// probabilities the PV product consumed, and ctx_lo (optional) receives the bf16 residual
+// O - bf16(O). The backward's D = dO . (ctx + ctx_lo) then equals sum_j P_ij dP_ij up to fp32
+// rounding with the row's common value component cancelled exactly (in deep random-init
+// policies dP_ij - D_i is a small difference, and bf16-rounded O / P would swamp it).
 bool attn_fwd_tc(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int n_seq, int max_len, int rows, int nh,
-                 int nkv, int hd, bf16* ctx, float* lse, double alg_flops);
+                 int nkv, int hd, bf16* ctx, float* lse, double alg_flops, bf16* ctx_lo = nullptr);
 // dq32 is overwritten (zeroed then accumulated), dkv32 rows are written.
 bool attn_bwd_tc(cudaStream_t s, const bf16* qkv, const bf16* ctx, const bf16* dctx, const float* lse,
                  const int32_t* seq_start, int n_seq, int max_len, int rows, int nh, int nkv, int hd, float* Dbuf,
-                 float* dq32, float* dkv32, double alg_flops);
+                 float* dq32, float* dkv32, double alg_flops, const bf16* ctx_lo = nullptr);
 // tcgen05 forward (head_dim 64); false if not covered (DASHCU_ATTN_FWD=mma forces mma.sync)
 bool attn_fwd_tc5(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int n_seq, int max_len, int rows, int nh,
-                  int nkv, int hd, bf16* ctx, float* lse);
+                  int nkv, int hd, bf16* ctx, float* lse, bf16* ctx_lo);
 // tcgen05 backward (head_dim 64): dq32 must be zero, D (Dbuf) computed; false if not covered
 // (DASHCU_ATTN_BWD=mma forces the mma.sync kernel).
 bool attn_bwd_tc5(cudaStream_t s, const bf16* qkv, const bf16* dctx, const float* lse, const float* Dbuf,

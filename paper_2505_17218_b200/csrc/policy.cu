@@ -378,16 +378,18 @@ struct Engine {
   struct Acts {
     int T_ = 0;
     T *xT, *qkv, *ctx, *hT, *u, *yT;
+    T* ctx_lo = nullptr;  // bf16 path, training only: O - bf16(O) for the backward's D
     float *lse, *x32, *h32;
   };
 
-  Acts alloc_acts(Workspace& ws, int Tn, const std::string& tag) {
+  Acts alloc_acts(Workspace& ws, int Tn, const std::string& tag, bool for_backward = false) {
     Acts a;
     a.T_ = Tn;
     const size_t t = static_cast<size_t>(Tn);
     a.xT = ws.get<T>(tag + "xT", t * g.d * g.L);
     a.qkv = ws.get<T>(tag + "qkv", t * g.qkvd * g.L);
     a.ctx = ws.get<T>(tag + "ctx", t * g.qd * g.L);
+    if (sizeof(T) == 2 && for_backward) a.ctx_lo = ws.get<T>(tag + "ctx_lo", t * g.qd * g.L);
     a.hT = ws.get<T>(tag + "hT", t * g.d * g.L);
     a.u = ws.get<T>(tag + "u", t * g.H * g.L);
     a.yT = ws.get<T>(tag + "yT", t * g.d);
@@ -414,7 +416,8 @@ struct Engine {
       mm(Tn, g.qkvd, g.d, xl, g.d, true, W(b + L.wq), g.d, true, store(nullptr, 0, qkv, g.qkvd));
       bool done = false;
       if constexpr (sizeof(T) == 2)
-        done = attn_fwd_tc(st, qkv, start, nseq, maxlen, Tn, g.nh, g.nkv, g.hd, ctx, lse, 4.0 * g.nh * g.hd * pairs);
+        done = attn_fwd_tc(st, qkv, start, nseq, maxlen, Tn, g.nh, g.nkv, g.hd, ctx, lse, 4.0 * g.nh * g.hd * pairs,
+                           A.ctx_lo ? reinterpret_cast<bf16*>(A.ctx_lo) + t * g.qd * l : nullptr);
       if (!done)
         attn_fwd_varlen<T>(st, qkv, start, nseq, maxlen, g.nh, g.nkv, g.hd, ctx, lse, 4.0 * g.nh * g.hd * pairs);
       Epi eo = store(A.h32, g.d, hT, g.d);
@@ -603,7 +606,7 @@ struct Engine {
       DevBatch D = upload(B);
       const int Tn = static_cast<int>(B.tok.size());
       const int R = static_cast<int>(B.rows.size());
-      Acts A = alloc_acts(P.ws, Tn, "a_");
+      Acts A = alloc_acts(P.ws, Tn, "a_", true);
       pairs = B.pairs;
       forward(A, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen);
       Acts Ab = alloc_acts(P.ws, Tn, "kb_");
@@ -681,7 +684,8 @@ struct Engine {
       bool done = false;
       if constexpr (sizeof(T) == 2)
         done = attn_bwd_tc(st, qkv, ctx, dctx, lse, start, nseq, maxlen, Tn, g.nh, g.nkv, g.hd,
-                           ws.get<float>("b_D", t * g.nh), dq32, dkv32, 10.0 * g.nh * g.hd * pairs);
+                           ws.get<float>("b_D", t * g.nh), dq32, dkv32, 10.0 * g.nh * g.hd * pairs,
+                           A.ctx_lo ? reinterpret_cast<const bf16*>(A.ctx_lo) + t * g.qd * l : nullptr);
       if (!done)
         attn_bwd_varlen<T>(st, qkv, dctx, lse, start, nseq, maxlen, g.nh, g.nkv, g.hd, dq32, dkv32,
                            10.0 * g.nh * g.hd * pairs);
@@ -872,7 +876,7 @@ struct Engine {
       const Batch& B = batches[bi];
       const DevBatch& D = dev[bi];
       const int Tn = static_cast<int>(B.tok.size());
-      Acts A = alloc_acts(P.ws, Tn, "a_");
+      Acts A = alloc_acts(P.ws, Tn, "a_", true);
       pairs = B.pairs;
       forward(A, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen);
       float* dy32 = P.ws.get<float>("b_dy32", static_cast<size_t>(Tn) * g.d);

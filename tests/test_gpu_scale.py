@@ -41,10 +41,6 @@ WIDE = dict(vocab_size=V_QWEN, embed_dim=896, context_len=1152, ffn_hidden=4864,
             n_heads=14, n_kv_heads=2, head_dim=64)
 
 
-# bf16 attention q / k projection gradients at 24-28 layers (see assert_grad_close_deep)
-QK_TOL_DEEP = 0.25
-
-
 @pytest.fixture(scope="module")
 def ctx():
     return D.Context(0)
@@ -71,24 +67,6 @@ def check_tokens(pol, ro, prompts, G, ML, seed, inv_t, bos):
             assert O.sample_rule(dump[s, j], bos, inv_t, key, j) == ro.completions[s, j], (s, j)
             checked += 1
     return dump, checked
-
-
-def assert_grad_close_deep(arch, got, ref, tol, qk_tol):
-    """Per-tensor relative error <= tol, except the attention query / key projections of a
-    deep policy, bounded by qk_tol: their gradients are 1e-6 of the total at random init
-    (near-uniform attention) and come out of the softmax-backward difference dP_j - D_i,
-    whose cancellation amplifies the bf16 rounding of O / P (tools/deep_grad_probe.py:
-    f32 path 3e-5, bf16 5e-2 median / 0.16 worst at 24 layers, identical with and without
-    the sampler-LSE reuse)."""
-    worst, worst_qk = [], []
-    for name, sl in tensor_slices(arch):
-        nr = np.linalg.norm(ref[sl])
-        e = np.linalg.norm(got[sl] - ref[sl]) / max(nr, 1e-300)
-        (worst_qk if name.endswith((".wq", ".wk")) else worst).append((e, name))
-    worst.sort(reverse=True)
-    worst_qk.sort(reverse=True)
-    assert worst[0][0] <= tol, worst[:3]
-    assert worst_qk[0][0] <= qk_tol, worst_qk[:3]
 
 
 def oracle_grad(arch, p, prompts, comps, w, G):
@@ -179,7 +157,11 @@ def test_lse_reuse_backward_vs_oracle_deep(ctx, arch):
     pol.accumulate_weighted(w, micro_batch=4)
     got = pol.grad()
     ref = oracle_grad(arch, p, prompts, comps, w, G)
-    assert_grad_close_deep(arch, got, ref, 2e-2, QK_TOL_DEEP)
+    # every tensor within 2e-2, the attention q / k projections of the top layers included:
+    # at random init their gradient is ~1e-6 of the total and comes out of dP_ij - D_i, a
+    # small difference; the forward's normaliser over the bf16-rounded P and the O residual
+    # kept for D make that difference exact up to fp32 (attn_fwd_tc; 16 % -> 1.4 % at 24 layers)
+    assert_grad_close(arch, got, ref, 2e-2)
     # and the teacher-forced log-probs vs the oracle
     lp = pol.rollout_log_prob(int(ro.lengths.sum()))
     ref_lp = np.concatenate([O.log_prob(arch, p, prompts[s // G], comps[s])[1] for s in range(len(comps))])
