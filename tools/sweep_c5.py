@@ -9,6 +9,12 @@ one warm-up step then one timed step, device-timed by the library's phase timers
 "GRPO-style" is the small sampling batch (4 prompts x G = 8 = 32 sequences, one
 micro-batch) without the filter (every sequence, including the zero-advantage ones of
 uniform groups, goes through the backward). Prints one JSON line per point and a table.
+
+--interleaved M1,M2,..: the SPEC's GRPO baseline round (interleaved_sample):
+the same M prompts x G served as M/4 interleaved calls of one 32-sequence micro-batch each
+(sample -> rewards -> advantage, no filter -> accumulate with the round's global 1/N), then
+one optimizer step -- the token multiset equals the preemptive call's (scheduling
+independence), so the two round times compare like for like.
 """
 import argparse
 import json
@@ -48,6 +54,43 @@ def run_point(ctx, arch, M, G, P, ML, tau, micro, seed0):
     return out
 
 
+def run_interleaved(ctx, arch, M, G, P, ML, micro_prompts, seed0):
+    import numpy as np
+    pol = D.Policy(ctx, arch, D.BF16)
+    pol.init_normal(0.02, 1)
+    prompts = W.synthetic_prompts(1, 0, M, P, arch["vocab_size"], 0, 1)
+    N = M * G
+    out = None
+    for it in range(2):   # warm-up round, timed round
+        samp = acc = 0.0
+        toks = trained = kept = 0
+        pol.grad_zero()
+        for c in range(0, M, micro_prompts):
+            tok = prompts[c:c + micro_prompts].reshape(-1).copy()
+            off = (np.arange(micro_prompts + 1) * P).astype(np.int64)
+            ro = pol.sample(None, G, ML, 1.0, round_seed=seed0 + it, prompt_index_base=c, prompt_tokens=tok,
+                            prompt_offsets=off)
+            pol.set_rewards(W.synthetic_rewards(2 + seed0 + it, c, c + micro_prompts, G))
+            pol.advantage(tau=None)
+            pol.accumulate(1.0 / N, micro_prompts * G)
+            st = pol.stats()
+            samp += st["sample_ms"]
+            acc += st["accumulate_ms"] + st["advantage_ms"]
+            toks += int(ro.lengths.sum())
+            trained += st["loss_tokens"]
+            kept += st["n_kept"]
+        pol.allreduce_grads()
+        pol.optimizer_step(D.OPT_ADAM, lr=1e-6)
+        st = pol.stats()
+        step = samp + acc + st["optimizer_ms"] + st["allreduce_ms"]
+        out = dict(mode="interleaved", prompts=M, seqs=N, calls=M // micro_prompts, tau="off", step_ms=step,
+                   sample_ms=samp, accumulate_ms=acc, kept=kept, sampled_tokens=toks, trained_tokens=trained)
+    pol.close()
+    out["sampled_tokens_per_s"] = out["sampled_tokens"] / (out["step_ms"] / 1e3)
+    out["ms_per_sequence"] = out["step_ms"] / out["seqs"]
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--max-len", type=int, default=1024)
@@ -55,21 +98,27 @@ def main():
     ap.add_argument("--prompts", default="4,64,256,512")
     ap.add_argument("--taus", default="off,0,0.1,0.3")
     ap.add_argument("--micro", type=int, default=32)
+    ap.add_argument("--interleaved", default="", help="round sizes (prompts) for the interleaved GRPO baseline")
     args = ap.parse_args()
     G, P, ML = 8, args.prompt_len, args.max_len
     arch = W.qwen_arch("0.5b", P + ML)
     ctx = D.Context(0)
     rows = []
-    for M in [int(x) for x in args.prompts.split(",")]:
+    for M in [int(x) for x in args.interleaved.split(",") if x]:
+        r = run_interleaved(ctx, arch, M, G, P, ML, 4, 100)
+        print(json.dumps(r), flush=True)
+        rows.append(r)
+    for M in [int(x) for x in args.prompts.split(",") if x]:
         for t in args.taus.split(","):
             tau = None if t == "off" else float(t)
             r = run_point(ctx, arch, M, G, P, ML, tau, args.micro, 100)
             print(json.dumps(r), flush=True)
             rows.append(r)
-    print("\n| prompts x G | tau | kept / seqs | step s | sample s | accumulate s | sampled tok/s | ms / sequence |")
-    print("|---|---|---|---|---|---|---|---|")
+    print("\n| mode | prompts x G | tau | kept / seqs | step s | sample s | accumulate s | sampled tok/s | ms / sequence |")
+    print("|---|---|---|---|---|---|---|---|---|")
     for r in rows:
-        print(f"| {r['prompts']} x {G} | {r['tau']} | {r['kept']} / {r['seqs']} | {r['step_ms'] / 1e3:.2f} | "
+        mode = f"interleaved ({r['calls']} calls)" if r.get("mode") else "preemptive"
+        print(f"| {mode} | {r['prompts']} x {G} | {r['tau']} | {r['kept']} / {r['seqs']} | {r['step_ms'] / 1e3:.2f} | "
               f"{r['sample_ms'] / 1e3:.2f} | {r['accumulate_ms'] / 1e3:.2f} | {r['sampled_tokens_per_s']:.0f} | "
               f"{r['ms_per_sequence']:.2f} |")
 
