@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "dash/advantage.hpp"
@@ -27,6 +28,8 @@ LogProbResult log_prob(const PolicyParams& params, const Trajectory& traj);     
 Trajectory sample(const PolicyParams& params, const std::vector<int>& prompt,     // policy.cpp:379-429
                   int max_len, double temperature, std::uint64_t seed);
 GradientVector grad_log_prob(const PolicyParams& params, const Trajectory& traj);  // policy.cpp:463-485
+KlResult kl_term(const PolicyParams& params, const PolicyParams& base,            // policy.cpp:487-522
+                 const Trajectory& traj);
 
 // ---- advantage.hpp:36-50 ----
 AdvantageBatch single_path_advantage(const std::vector<double>& rewards);
@@ -56,5 +59,9 @@ struct OptState {
 };
 // optimizer_step: ascent on the device master weights, written back.
 void optimizer_step(PolicyParams& params, const GradientVector& grad, OptState& st, double lr);
+// Checkpoint container (dashcu_policy_save / _load: named f64 tensors in the
+// views() order with the reference's content_hash).
+void save_checkpoint(const PolicyParams& params, const std::string& path);
+PolicyParams load_checkpoint(const ArchConfig& arch, const std::string& path);
 
 }  // namespace dash::b200

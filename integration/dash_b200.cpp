@@ -25,6 +25,8 @@ struct State {
   int dtype = DASHCU_BF16;
   dashcu_ctx* ctx = nullptr;
   dashcu_policy* pol = nullptr;
+  dashcu_policy* base = nullptr;  // kl_term's base policy
+  std::uint64_t base_hash = 0;
   ArchConfig arch{};
   bool have_arch = false;
   std::uint64_t hash = 0;
@@ -155,8 +157,10 @@ void configure(int device, bool fp32_parity_mode) {
   s.device = device;
   s.dtype = fp32_parity_mode ? DASHCU_F32 : DASHCU_BF16;
   if (s.pol) dashcu_policy_destroy(s.pol);
+  if (s.base) dashcu_policy_destroy(s.base);
   if (s.ctx) dashcu_ctx_destroy(s.ctx);
   s.pol = nullptr;
+  s.base = nullptr;
   s.ctx = nullptr;
   s.have_arch = s.have_params = false;
 }
@@ -204,6 +208,29 @@ GradientVector grad_log_prob(const PolicyParams& params, const Trajectory& traj)
   const double w = 1.0;
   check(dashcu_accumulate_weighted(pol, &w, 1, 0));
   return download_grad(pol, params.arch);
+}
+
+KlResult kl_term(const PolicyParams& params, const PolicyParams& base, const Trajectory& traj) {
+  if (!(params.arch == base.arch)) throw InputError("kl_term: parameter sets have different architectures");
+  State& s = S();
+  std::lock_guard<std::mutex> lk(s.mu);
+  dashcu_policy* pol = bind(params);
+  const std::uint64_t bh = base.content_hash();
+  if (!s.base || bh != s.base_hash) {
+    if (s.base) dashcu_policy_destroy(s.base);
+    s.base = nullptr;
+    const dashcu_arch a = to_c(base.arch);
+    check(dashcu_policy_create(s.ctx, &a, s.dtype, &s.base));
+    const auto flat = flatten(base);
+    check(dashcu_policy_upload(s.base, flat.data(), static_cast<std::int64_t>(flat.size())));
+    s.base_hash = bh;
+  }
+  load(pol, {&traj});
+  check(dashcu_grad_zero(pol));
+  KlResult r;
+  check(dashcu_accumulate_kl(pol, s.base, 1.0, 0, nullptr, 0, &r.value));
+  r.grad = download_grad(pol, params.arch);
+  return r;
 }
 
 AdvantageBatch single_path_advantage(const std::vector<double>& rewards) {
@@ -310,6 +337,25 @@ void optimizer_step(PolicyParams& params, const GradientVector& grad, OptState& 
   check(dashcu_policy_download(pol, flat.data(), static_cast<std::int64_t>(flat.size())));
   unflatten(flat, params);
   s.hash = params.content_hash();  // device already holds exactly these (fp32-rounded) weights
+}
+
+void save_checkpoint(const PolicyParams& params, const std::string& path) {
+  State& s = S();
+  std::lock_guard<std::mutex> lk(s.mu);
+  check(dashcu_policy_save(bind(params), path.c_str(), 0));
+}
+
+PolicyParams load_checkpoint(const ArchConfig& arch, const std::string& path) {
+  State& s = S();
+  std::lock_guard<std::mutex> lk(s.mu);
+  PolicyParams p = PolicyParams::zeros(arch);
+  dashcu_policy* pol = bind(p);
+  check(dashcu_policy_load(pol, path.c_str(), 0));
+  std::vector<double> flat(p.num_params());
+  check(dashcu_policy_download(pol, flat.data(), static_cast<std::int64_t>(flat.size())));
+  unflatten(flat, p);
+  s.hash = p.content_hash();
+  return p;
 }
 
 }  // namespace dash::b200

@@ -133,6 +133,24 @@ int main() {
       threw = true;
     }
     expect(threw, tag + "BOS in completion -> InputError");
+    // kl_term against the reference's (value and gradient), and kl(p, p) = 0
+    PolicyParams base = p;
+    {
+      Rng br(5);
+      for (auto& v : base.views())
+        for (size_t i = 0; i < v.size; ++i) v.data[i] = static_cast<double>(static_cast<float>(v.data[i] + 0.01 * br.normal()));
+    }
+    const KlResult kr = kl_term(p, base, t), kb = b200::kl_term(p, base, t);
+    expect(std::fabs(kb.value - kr.value) <= (f32 ? 1e-3 : 2e-2) * std::fabs(kr.value), tag + "kl_term value vs reference",
+           std::fabs(kb.value - kr.value) / std::fabs(kr.value));
+    expect(rel(kb.grad, kr.grad) <= tol, tag + "kl_term gradient vs reference", rel(kb.grad, kr.grad));
+    const KlResult k0 = b200::kl_term(p, p, t);
+    expect(std::fabs(k0.value) <= 1e-6 && k0.grad.max_abs() <= 1e-6, tag + "kl_term(p, p) = 0", std::fabs(k0.value));
+    // checkpoint round trip through the container (bitwise)
+    const std::string ck = "/tmp/dropin_ckpt_" + std::to_string(mode) + ".bin";
+    b200::save_checkpoint(p, ck);
+    const PolicyParams pl = b200::load_checkpoint(p.arch, ck);
+    expect(pl.content_hash() == p.content_hash(), tag + "checkpoint save/load bitwise (content_hash)");
   }
   std::printf("%s (%d failures)\n", failures ? "DROPIN FAIL" : "DROPIN OK", failures);
   return failures ? 1 : 0;
