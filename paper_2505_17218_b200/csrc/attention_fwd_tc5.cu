@@ -60,18 +60,10 @@ template <int HD>
 struct FLay {
   static constexpr int kTile = 128 * HD * 2;  // 16 / 32 KB: HD / 64 atoms
   static constexpr int kQS = HD == 64 ? 2 : 1;  // Q stages
-  // head_dim 64: P double-buffered (the softmax writes P_t while the MMA still reads P_{t-1})
-  // within 227 KB by a 3-deep K/V ring; head_dim 128: one P buffer, 2-deep ring
-#ifndef DASHCU_FWD_SINGLE_P
-  static constexpr int kST = HD == 64 ? 3 : 2;  // K/V pipeline depth (loads run kST - 1 key tiles ahead)
-  static constexpr int kPB = HD == 64 ? 2 : 1;  // P buffers
-#else  // A/B builds only: the single-P layout (4-deep ring at head_dim 64)
-  static constexpr int kST = HD == 64 ? 4 : 2;
-  static constexpr int kPB = 1;
-#endif
+  static constexpr int kST = HD == 64 ? 4 : 2;  // K/V pipeline depth (loads run kST - 1 key tiles ahead)
   static constexpr int Q = 0, K = kQS * kTile, V = K + kST * kTile;
-  static constexpr int P = V + kST * kTile;  // P [128 q x 128 keys] bf16: two 64-key swizzle atoms each
-  static constexpr int XMAX = P + kPB * 2 * kAtom;  // row-max exchange [2][2][128] + row sums [2][128]
+  static constexpr int P = V + kST * kTile;  // P [128 q x 128 keys] bf16: two 64-key swizzle atoms
+  static constexpr int XMAX = P + 2 * kAtom;  // row-max exchange [2][2][128] + row sums [2][128]
   static constexpr int BAR = XMAX + 4096;
   static constexpr int BYTES = BAR + 256 + 1024;
   static_assert(BYTES <= 232448, "exceeds the 227 KB of opt-in shared memory per CTA");
@@ -101,7 +93,7 @@ __global__ void __launch_bounds__(384, 1)
                    int nqt_max, bf16* __restrict__ ctx, float* __restrict__ lse, float scale_log2,
                    bf16* __restrict__ ctx_lo) {
   using FLay = dashcu::FLay<HD>;
-  constexpr int kHD = HD, kTile = FLay::kTile, kST = FLay::kST, kQS = FLay::kQS, kPB = FLay::kPB;
+  constexpr int kHD = HD, kTile = FLay::kTile, kST = FLay::kST, kQS = FLay::kQS;
   constexpr uint32_t kTS0 = FLay::TS0, kTS1 = FLay::TS1, kTO0 = FLay::TO0, kTO1 = FLay::TO1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -127,9 +119,9 @@ __global__ void __launch_bounds__(384, 1)
 
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FLay::BAR);
   uint64_t *qfull = bar /*[2]*/, *qempty = bar + 2 /*[2]*/, *sfull = bar + 4 /*[2]*/, *sfree = bar + 6 /*[2]*/,
-           *pready = bar + 8 /*[2]*/, *ofull = bar + 10 /*[2]*/, *ofree = bar + 12 /*[2]*/, *kvfull = bar + 14 /*[kST]*/,
-           *kvempty = bar + 14 + kST /*[kST]*/;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14 + 2 * kST);
+           *pready = bar + 8, *ofull = bar + 9 /*[2]*/, *ofree = bar + 11 /*[2]*/, *kvfull = bar + 13 /*[kST]*/,
+           *kvempty = bar + 13 + kST /*[kST]*/;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13 + 2 * kST);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kST; ++i) {
@@ -144,8 +136,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&ofull[i], 1);
       mbar_init(&ofree[i], 256);
     }
-    mbar_init(&pready[0], 256);
-    mbar_init(&pready[1], 256);
+    mbar_init(pready, 256);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mQKV)) : "memory");
   }
@@ -208,15 +199,14 @@ __global__ void __launch_bounds__(384, 1)
         const int sb = t & 1, st = t % kST;
         if (t + 1 < ntiles) issue_s(t + 1);
         TRF(t, 0);
-        mbar_wait_sleep(&pready[t % kPB], (t / kPB) & 1);
+        mbar_wait_sleep(pready, t & 1);
         TRF(t, 1);
         if (t >= 2) mbar_wait_sleep(&ofree[sb], ((t >> 1) - 1) & 1);  // O_{t-2} read out
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t v = sV + st * kTile;
 #pragma unroll
         for (int kk = 0; kk < kKeys / 16; ++kk)
-          umma_bf16(tmem + (sb ? kTO1 : kTO0),
-                    smem_desc(sP + (t % kPB) * 2 * kAtom + (kk >> 2) * kAtom + (kk & 3) * 32, 16, 1024),
+          umma_bf16(tmem + (sb ? kTO1 : kTO0), smem_desc(sP + (kk >> 2) * kAtom + (kk & 3) * 32, 16, 1024),
                     smem_desc(v + kk * 2048, kAtom, 1024), I_O, kk > 0);  // V atoms kAtom apart along hd
         umma_commit(&kvempty[st]);
         umma_commit(&ofull[sb]);
@@ -311,18 +301,18 @@ __global__ void __launch_bounds__(384, 1)
         f2_unpack(rs2[0], r0, r1);
         f2_unpack(rs2[1], r2, r3);
         l = l * ex2(m - m_new) + ((r0 + r1) + (r2 + r3));  // this half's share of the row sum
-        // P_t overwrites P_{t-kPB}: the MMA of O_{t-kPB} must be complete
+        // P_t overwrites P_{t-1}: the MMA of O_{t-1} must be complete
         if (warp == 4) TRF(t, 8);
-        if (t >= kPB) mbar_wait_sleep(&ofull[(t - kPB) & 1], ((t - kPB) >> 1) & 1);
+        if (t > 0) mbar_wait_sleep(&ofull[(t - 1) & 1], ((t - 1) >> 1) & 1);
         if (warp == 4) TRF(t, 9);
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch)  // keys [64 hf, 64 hf + 64) = swizzle atom hf of P
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sP + (t % kPB) * 2 * kAtom + hf * kAtom + r * 128 +
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sP + hf * kAtom + r * 128 +
                                                                          ((ch ^ (r & 7)) << 4)),
                        "r"(pk[ch * 4]), "r"(pk[ch * 4 + 1]), "r"(pk[ch * 4 + 2]), "r"(pk[ch * 4 + 3])
                        : "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&pready[t % kPB]);
+        mbar_arrive(pready);
         if (warp == 4) TRF(t, 10);
         if (j > 0) take_o(t - 1, m_prev, m);
         if (warp == 4) TRF(t, 11);
