@@ -270,6 +270,15 @@ DASHCU_API int dashcu_optimizer_step(dashcu_policy* pol, const dashcu_opt* opt);
  * for its whole life (InputError otherwise). After it the gradient buffer is valid only
  * on this rank's slice. */
 DASHCU_API int dashcu_sharded_step(dashcu_policy* pol, const dashcu_opt* opt);
+/* The same update as ONE kernel per rank over NVLink peer memory (the
+ * optimizer fused into the collective): the ranks' gradient / fp32 master / bf16 buffers
+ * are shared once through CUDA IPC (handles all-gathered over the communicator); the kernel
+ * sums this rank's slice of every rank's gradient (rank order), updates it with the
+ * slice-sized moments, and writes the new master + bf16 values into every rank's buffers,
+ * between an entry and an exit barrier of system-scope flags (status 4 on a timeout).
+ * Shares the moment layout of dashcu_sharded_step (the two may be mixed); world 1 runs
+ * the same kernel on the local buffers. At most 8 ranks. */
+DASHCU_API int dashcu_fused_step(dashcu_policy* pol, const dashcu_opt* opt);
 /* The slice of a `total`-element flat vector rank `rank` of `world` owns in the sharded
  * step (no device work). */
 DASHCU_API int dashcu_shard_span(int64_t total, int32_t world, int32_t rank, int64_t* off, int64_t* len);
@@ -349,6 +358,14 @@ DASHCU_API int dashcu_rollout_task_rewards(dashcu_policy* pol, int32_t kind, int
 DASHCU_API int dashcu_set_knob(const char* name, int value);
 
 /* ---- diagnostics (used by the kernel tests) ----
+ * dashcu_selftest_fused_step: `world` virtual ranks on this GPU, each a full replica
+ * (gradient g_all[r * n ..], master w0, bf16 copy, flags, slice moments) running the fused
+ * kernel on its own stream concurrently, `steps` times (Adam bias corrections per step);
+ * w_out / wT_out receive every replica's master and bf16 weights [world x n]. */
+DASHCU_API int dashcu_selftest_fused_step(dashcu_ctx* ctx, int32_t world, int64_t n, int32_t kind, double lr,
+                                          int32_t steps, const float* g_all, const float* w0, float* w_out,
+                                          uint16_t* wT_out);
+/* dashcu_selftest_gemm:
  * C[M x N] (fp32, ldc = N) = A(m,k) . B(n,k) on bf16 operands given as raw
  * bit patterns, through the production GEMM dispatcher (tcgen05 when the
  * operands are TMA-legal) or, with force_simt, the CUDA-core kernel.

@@ -157,6 +157,9 @@ def lib():
             "dashcu_allreduce_grads": [vp],
             "dashcu_optimizer_step": [vp, C.POINTER(Opt)],
             "dashcu_sharded_step": [vp, C.POINTER(Opt)],
+            "dashcu_fused_step": [vp, C.POINTER(Opt)],
+            "dashcu_selftest_fused_step": [vp, C.c_int32, C.c_int64, C.c_int32, C.c_double, C.c_int32, f32p, f32p,
+                                           f32p, C.POINTER(C.c_uint16)],
             "dashcu_shard_span": [C.c_int64, C.c_int32, C.c_int32, i64p, i64p],
             "dashcu_get_stats": [vp, C.POINTER(Stats)],
             "dashcu_rollout_snapshot": [vp],
@@ -385,6 +388,17 @@ class Context:
                                           None if b is None else _p(b, f32p), epi, int(force_simt), _p(out, f32p)))
         return out
 
+    def selftest_fused_step(self, g_all, w0, kind=OPT_ADAM, lr=1e-3, steps=1):
+        """Virtual ranks (rows of g_all) running the fused step concurrently; (w [world x n], wT bits)."""
+        g = np.ascontiguousarray(g_all, dtype=np.float32)
+        w = np.ascontiguousarray(w0, dtype=np.float32)
+        world, n = g.shape
+        wo = np.zeros((world, n), dtype=np.float32)
+        to = np.zeros((world, n), dtype=np.uint16)
+        _check(lib().dashcu_selftest_fused_step(self.h, world, n, kind, lr, steps, _p(g, f32p), _p(w, f32p),
+                                                _p(wo, f32p), to.ctypes.data_as(C.POINTER(C.c_uint16))))
+        return wo, to
+
     def close(self):
         if self.h:
             lib().dashcu_ctx_destroy(self.h)
@@ -598,6 +612,11 @@ class Policy:
         """reduce-scatter + update of this rank's slice + all-gather (dashcu_sharded_step)."""
         o = Opt(kind, lr, beta1, beta2, eps)
         _check(lib().dashcu_sharded_step(self.h, C.byref(o)))
+
+    def fused_step(self, kind=OPT_ADAM, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8):
+        """reduce-scatter + update + all-gather as one kernel over peer memory (dashcu_fused_step)."""
+        o = Opt(kind, lr, beta1, beta2, eps)
+        _check(lib().dashcu_fused_step(self.h, C.byref(o)))
 
     def stats(self) -> dict:
         s = Stats()

@@ -11,6 +11,43 @@ void f64_to_f32(cudaStream_t s, const double* in, float* out, int64_t n);
 void f32_to_f64(cudaStream_t s, const float* in, double* out, int64_t n);
 void cast_f32_bf16(cudaStream_t s, const float* in, bf16* out, int64_t n);
 void fill_f32(cudaStream_t s, float* p, float v, int64_t n);
+// One parameter's ascent update: SGD w + lr g, or Adam with bias
+// corrections c1 = 1 - b1^t, c2 = 1 - b2^t (m, v updated in place). Shared by the replicated
+// update and the fused reduce-scatter / update / all-gather kernel so both round alike.
+__device__ __forceinline__ float opt_update(int kind, float wi, float gi, float* m, float* v, float lr, float b1,
+                                            float b2, float eps, float c1, float c2) {
+  if (kind == 0) return wi + lr * gi;
+  const float mi = b1 * *m + (1.f - b1) * gi;
+  const float vi = b2 * *v + (1.f - b2) * gi * gi;
+  *m = mi;
+  *v = vi;
+  return wi + lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+}
+
+// Fused reduce-scatter + update + all-gather over peer memory (dashcu_fused_step): rank
+// `rank` of `world` sums its slice [off, off + len) of every rank's gradient (rank order),
+// updates its master slice with its slice-sized moments and writes the new fp32 + bf16
+// weights into every rank's buffers; an entry barrier (all gradients final) and an exit
+// barrier (all slices written, all peer reads of this rank's gradient done) use flag words
+// in every rank's memory (system-scope release / acquire, epoch-valued). Spins time out
+// after ~4 s (err = 1) instead of hanging.
+constexpr int kMaxFusedRanks = 8;
+struct FusedStepArgs {
+  int world = 1, rank = 0, kind = 1;
+  int64_t off = 0, len = 0;
+  float* g[kMaxFusedRanks] = {};
+  float* w[kMaxFusedRanks] = {};
+  bf16* wT[kMaxFusedRanks] = {};
+  uint32_t* flags[kMaxFusedRanks] = {};  // rank p's flag words: [0, world) entry, [world, 2 world) exit
+  float* m = nullptr;                    // this rank's slice moments
+  float* v = nullptr;
+  uint32_t* done = nullptr;              // this rank's block-completion counter (zero between calls)
+  int* err = nullptr;
+  uint32_t epoch = 0;
+  float lr = 0, b1 = 0, b2 = 0, eps = 0, c1 = 1, c2 = 1;
+};
+void fused_step(cudaStream_t s, const FusedStepArgs& a, int grid);
+
 // SPEC.md:329-337 (ascent). kind 0 SGD, 1 Adam. Writes the bf16 working copy if wT != null.
 void optimizer_update(cudaStream_t s, int kind, float* w, const float* g, float* m, float* v, bf16* wT,
                       int64_t n, float lr, float b1, float b2, float eps, float c1, float c2);

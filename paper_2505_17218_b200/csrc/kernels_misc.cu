@@ -67,17 +67,7 @@ __global__ void optimizer_k(int kind, float* __restrict__ w, const float* __rest
                             float* __restrict__ v, bf16* __restrict__ wT, int64_t n, float lr, float b1, float b2,
                             float eps, float c1, float c2) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const float gi = g[i];
-    float wi = w[i];
-    if (kind == 0) {
-      wi += lr * gi;
-    } else {
-      const float mi = b1 * m[i] + (1.f - b1) * gi;
-      const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
-      m[i] = mi;
-      v[i] = vi;
-      wi += lr * (mi / c1) / (sqrtf(vi / c2) + eps);
-    }
+    const float wi = opt_update(kind, w[i], g[i], m + i, v + i, lr, b1, b2, eps, c1, c2);
     w[i] = wi;
     if (wT) wT[i] = __float2bfloat16_rn(wi);
   }

@@ -315,6 +315,17 @@ struct dashcu_policy {
   dashcu::DevMem d_dump;
   int64_t dump_n = 0;
   dashcu_stats st{};
+  // dashcu_fused_step: every rank's gradient / master / bf16 / flag buffers (CUDA IPC)
+  struct FusedPeers {
+    bool ready = false;
+    float* g[dashcu::kMaxFusedRanks] = {};
+    float* w[dashcu::kMaxFusedRanks] = {};
+    dashcu::bf16* wT[dashcu::kMaxFusedRanks] = {};
+    uint32_t* flags[dashcu::kMaxFusedRanks] = {};
+    std::vector<void*> opened;
+    dashcu::DevMem flags_local, done, err;
+    uint32_t epoch = 0;
+  } fused;
   int64_t launches0 = 0;
   int64_t kv_pages = 0;  // decode KV page pool per layer (0: the worst case of the round)
   dashcu::Workspace ws;
@@ -1419,6 +1430,7 @@ int dashcu_policy_destroy(dashcu_policy* p) {
   dashcu_ctx* c = p->ctx;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  for (void* q : p->fused.opened) cudaIpcCloseMemHandle(q);
   delete p;
   if (--c->refs == 0 && c->closed) ctx_free(c);
   API_END
@@ -2462,6 +2474,176 @@ int dashcu_policy_load(dashcu_policy* p, const char* path, int32_t with_optimize
   }
   DCU_CHECK(cudaStreamSynchronize(s));
   ++p->version;
+  API_END
+}
+
+// ---------------------------------------------- fused reduce-scatter / update / all-gather
+namespace dashcu {
+namespace {
+int num_sms_host() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = kNumSMs;
+  return n;
+}
+// Peer buffers for the fused step: each rank's IPC handles of its gradient, fp32 master,
+// bf16 working copy and flag words, all-gathered over the communicator, opened once.
+void fused_setup(dashcu_policy* p) {
+  dashcu_ctx* c = p->ctx;
+  auto& F = p->fused;
+  const int W = c->world;
+  if (W > kMaxFusedRanks) throw Error(1, "dashcu_fused_step supports at most 8 ranks");
+  F.flags_local.ensure(sizeof(uint32_t) * 2 * W);
+  F.done.ensure(sizeof(uint32_t));
+  F.err.ensure(sizeof(int));
+  DCU_CHECK(cudaMemsetAsync(F.flags_local.p, 0, sizeof(uint32_t) * 2 * W, c->stream));
+  DCU_CHECK(cudaMemsetAsync(F.done.p, 0, sizeof(uint32_t), c->stream));
+  DCU_CHECK(cudaMemsetAsync(F.err.p, 0, sizeof(int), c->stream));
+  F.g[c->rank] = p->g32.as<float>();
+  F.w[c->rank] = p->w32.as<float>();
+  F.wT[c->rank] = p->dtype == DASHCU_BF16 ? p->wT.as<bf16>() : nullptr;
+  F.flags[c->rank] = F.flags_local.as<uint32_t>();
+  if (W > 1) {
+    NcclApi& nc = NcclApi::get();
+    if (!c->comm) throw Error(4, "communicator not initialised (dashcu_ctx_init_comm)");
+    constexpr int kH = static_cast<int>(sizeof(cudaIpcMemHandle_t));
+    std::vector<uint8_t> mine(4 * kH, 0), all(static_cast<size_t>(4 * kH) * W);
+    void* bufs[4] = {p->g32.p, p->w32.p, p->dtype == DASHCU_BF16 ? p->wT.p : nullptr, F.flags_local.p};
+    for (int k = 0; k < 4; ++k)
+      if (bufs[k]) DCU_CHECK(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data() + k * kH), bufs[k]));
+    uint8_t* d = c->ws.get<uint8_t>("fused_h", static_cast<size_t>(4 * kH) * (W + 1));
+    h2d(c->stream, d + static_cast<size_t>(4 * kH) * W, mine.data(), 4 * kH);
+    NCCL_CHECK(nc.AllGather(d + static_cast<size_t>(4 * kH) * W, d, 4 * kH, ncclUint8, c->comm, c->stream));
+    d2h(c->stream, all.data(), d, all.size());
+    nccl_wait(c->comm, c->stream);
+    for (int r = 0; r < W; ++r) {
+      if (r == c->rank) continue;
+      void* q[4] = {};
+      for (int k = 0; k < 4; ++k) {
+        if (k == 2 && p->dtype != DASHCU_BF16) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, all.data() + static_cast<size_t>(4 * kH) * r + k * kH, kH);
+        DCU_CHECK(cudaIpcOpenMemHandle(&q[k], h, cudaIpcMemLazyEnablePeerAccess));
+        F.opened.push_back(q[k]);
+      }
+      F.g[r] = static_cast<float*>(q[0]);
+      F.w[r] = static_cast<float*>(q[1]);
+      F.wT[r] = static_cast<bf16*>(q[2]);
+      F.flags[r] = static_cast<uint32_t*>(q[3]);
+    }
+    // every rank's flags are zeroed before any rank's first kernel signals into them
+    DCU_CHECK(cudaStreamSynchronize(c->stream));
+    int32_t* bar = c->ws.get<int32_t>("fused_bar", 2);
+    NCCL_CHECK(nc.AllReduce(bar, bar + 1, 1, ncclInt32, ncclSum, c->comm, c->stream));
+    nccl_wait(c->comm, c->stream);
+  }
+  F.ready = true;
+}
+}  // namespace
+}  // namespace dashcu
+
+int dashcu_fused_step(dashcu_policy* p, const dashcu_opt* o) {
+  API_BEGIN
+  check_policy(p);
+  if (!o) throw Error(1, "null optimizer config");
+  if (o->kind != DASHCU_OPT_SGD && o->kind != DASHCU_OPT_ADAM) throw Error(1, "unknown optimizer");
+  dashcu_ctx* c = p->ctx;
+  if (c->world != p->shard_world) throw Error(1, "communicator changed after the policy was created");
+  if (p->opt_state == 0) throw Error(1, "optimizer state is replicated: use dashcu_optimizer_step");
+  int64_t off, len, slice;
+  shard_span(p->lay.total, c->world, c->rank, &off, &len, &slice);
+  ensure_moments(p, slice, 1);
+  if (!p->fused.ready) fused_setup(p);
+  auto& F = p->fused;
+  Timer tm(c->stream);
+  FusedStepArgs a;
+  a.world = c->world;
+  a.rank = c->rank;
+  a.kind = o->kind;
+  a.off = off;
+  a.len = len;
+  for (int r = 0; r < c->world; ++r) a.g[r] = F.g[r], a.w[r] = F.w[r], a.wT[r] = F.wT[r], a.flags[r] = F.flags[r];
+  a.m = p->am.as<float>();
+  a.v = p->av.as<float>();
+  a.done = F.done.as<uint32_t>();
+  a.err = F.err.as<int>();
+  a.epoch = ++F.epoch;
+  float c1, c2;
+  bias_corrections(p, o, &c1, &c2);
+  a.lr = static_cast<float>(o->lr);
+  a.b1 = static_cast<float>(o->beta1);
+  a.b2 = static_cast<float>(o->beta2);
+  a.eps = static_cast<float>(o->eps);
+  a.c1 = c1;
+  a.c2 = c2;
+  fused_step(c->stream, a, num_sms_host());
+  int err = 0;
+  d2h(c->stream, &err, F.err.as<int>(), 1);
+  p->st.optimizer_ms = tm.stop_ms();
+  p->st.allreduce_ms = 0.0;
+  if (err) throw Error(4, "fused step: a peer did not reach the barrier (timeout)");
+  ++p->version;
+  API_END
+}
+
+// Virtual ranks on one GPU (tests): `world` replicas of (gradient, master, bf16, flags,
+// slice moments) and one fused kernel per replica on its own stream, all concurrent, exactly
+// as `world` GPUs would run them; outputs every replica's master and bf16 weights.
+int dashcu_selftest_fused_step(dashcu_ctx* c, int32_t world, int64_t n, int32_t kind, double lr, int32_t steps,
+                               const float* g_all, const float* w0, float* w_out, uint16_t* wT_out) {
+  API_BEGIN
+  if (!c || world < 1 || world > kMaxFusedRanks || n < 1 || steps < 1) throw Error(1, "bad arguments");
+  DCU_CHECK(cudaSetDevice(c->device));
+  int64_t off[kMaxFusedRanks], len[kMaxFusedRanks], slice = 0;
+  for (int r = 0; r < world; ++r) shard_span(n, world, r, &off[r], &len[r], &slice);
+  const size_t padded = static_cast<size_t>(slice) * world;
+  std::vector<DevMem> g(world), w(world), wT(world), fl(world), m(world), v(world), done(world), err(world);
+  std::vector<cudaStream_t> ss(world);
+  for (int r = 0; r < world; ++r) {
+    g[r].ensure(padded * 4), w[r].ensure(padded * 4), wT[r].ensure(padded * 2), fl[r].ensure(2 * world * 4);
+    m[r].ensure(slice * 4), v[r].ensure(slice * 4), done[r].ensure(4), err[r].ensure(4);
+    DCU_CHECK(cudaMemset(g[r].p, 0, padded * 4));
+    DCU_CHECK(cudaMemset(w[r].p, 0, padded * 4));
+    DCU_CHECK(cudaMemcpy(g[r].p, g_all + static_cast<size_t>(r) * n, n * 4, cudaMemcpyHostToDevice));
+    DCU_CHECK(cudaMemcpy(w[r].p, w0, n * 4, cudaMemcpyHostToDevice));
+    for (DevMem* q : {&fl[r], &m[r], &v[r], &done[r], &err[r]}) DCU_CHECK(cudaMemset(q->p, 0, q->n));
+    DCU_CHECK(cudaStreamCreateWithFlags(&ss[r], cudaStreamNonBlocking));
+  }
+  DCU_CHECK(cudaDeviceSynchronize());
+  const int grid = std::max(1, 2 * num_sms_host() / world);
+  for (int t = 1; t <= steps; ++t)
+    for (int r = 0; r < world; ++r) {
+      FusedStepArgs a;
+      a.world = world;
+      a.rank = r;
+      a.kind = kind;
+      a.off = off[r];
+      a.len = len[r];
+      for (int q = 0; q < world; ++q)
+        a.g[q] = g[q].as<float>(), a.w[q] = w[q].as<float>(), a.wT[q] = wT[q].as<bf16>(), a.flags[q] = fl[q].as<uint32_t>();
+      a.m = m[r].as<float>();
+      a.v = v[r].as<float>();
+      a.done = done[r].as<uint32_t>();
+      a.err = err[r].as<int>();
+      a.epoch = static_cast<uint32_t>(t);
+      a.lr = static_cast<float>(lr);
+      a.b1 = 0.9f, a.b2 = 0.999f, a.eps = 1e-8f;
+      a.c1 = static_cast<float>(1.0 - std::pow(0.9, t));
+      a.c2 = static_cast<float>(1.0 - std::pow(0.999, t));
+      if (kind == DASHCU_OPT_SGD) a.c1 = a.c2 = 1.f;
+      fused_step(ss[r], a, grid);
+    }
+  DCU_CHECK(cudaDeviceSynchronize());
+  int bad = 0;
+  for (int r = 0; r < world; ++r) {
+    int e = 0;
+    DCU_CHECK(cudaMemcpy(&e, err[r].p, 4, cudaMemcpyDeviceToHost));
+    bad |= e;
+    DCU_CHECK(cudaMemcpy(w_out + static_cast<size_t>(r) * n, w[r].p, n * 4, cudaMemcpyDeviceToHost));
+    DCU_CHECK(cudaMemcpy(wT_out + static_cast<size_t>(r) * n, wT[r].p, n * 2, cudaMemcpyDeviceToHost));
+    cudaStreamDestroy(ss[r]);
+  }
+  if (bad) throw Error(4, "fused step selftest: barrier timeout");
   API_END
 }
 

@@ -43,6 +43,13 @@ def run_rank(rank, world, uid, q, dtype):
     g = pol.grad()
     pol.sharded_step(D.OPT_ADAM, lr=1e-3)    # reduce-scatters the (already summed) gradient again:
     p_sh = pol.download()                     # the update uses world x grad, as below
+    # the fused kernel over NVLink peer memory: same update from the same starting point
+    pol2 = D.Policy(ctx, ARCH, dtype)
+    pol2.init_normal(0.05, 3)
+    pol2.grad_upload(g)
+    pol2.fused_step(D.OPT_ADAM, lr=1e-3)
+    assert np.abs(pol2.download() - p_sh).max() <= 1e-6
+    pol2.close()
     q.put((rank, g, p_sh))
     pol.close()
     ctx.close()

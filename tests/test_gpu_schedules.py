@@ -280,3 +280,62 @@ def test_checkpoint_round_trip(ctx, tmp_path, arch):
         c.load(path)
     for p in (a, b, c):
         p.close()
+
+
+# ------------------------------------------------ fused reduce-scatter / update / all-gather
+
+def adam_fp32(w, g, m, v, t, lr, b1=0.9, b2=0.999, eps=1e-8):
+    f = np.float32
+    m = f(b1) * m + f(1 - b1) * g
+    v = f(b2) * v + f(1 - b2) * g * g
+    c1, c2 = f(1 - b1 ** t), f(1 - b2 ** t)
+    return w + f(lr) * (m / c1) / (np.sqrt(v / c2) + f(eps)), m, v
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_fused_step_virtual_ranks(ctx, world):
+    """dashcu_fused_step's kernel as `world` concurrent virtual ranks on one GPU (their own
+    gradient / master / bf16 / flag buffers, the same peer-pointer arrays NVLink ranks get):
+    every replica ends with the same master weights = Adam over the rank-order gradient sum
+    (three steps, slice-sized moments, the entry / exit barriers each step), and the bf16
+    copies are their rounding."""
+    n = 100003   # slices of ceil(n / world) rounded up to 64, the last one short
+    rng = np.random.default_rng(world)
+    g = rng.standard_normal((world, n)).astype(np.float32)
+    w0 = rng.standard_normal(n).astype(np.float32)
+    wo, wt = ctx.selftest_fused_step(g, w0, D.OPT_ADAM, 1e-3, steps=3)
+    for r in range(1, world):
+        assert np.array_equal(wo[r].view(np.uint32), wo[0].view(np.uint32))
+    gs = g[0].copy()
+    for r in range(1, world):
+        gs = gs + g[r]
+    w, m, v = w0.copy(), np.zeros(n, np.float32), np.zeros(n, np.float32)
+    for t in (1, 2, 3):   # the same gradient each step
+        w, m, v = adam_fp32(w, gs, m, v, t, 1e-3)
+    assert np.max(np.abs(wo[0] - w)) <= 1e-6
+    from test_gpu_gemm import bf16_bits
+    assert np.array_equal(wt[0], bf16_bits(wo[0]))
+    wo, _ = ctx.selftest_fused_step(g, w0, D.OPT_SGD, 1e-2, steps=1)
+    assert np.max(np.abs(wo[world - 1] - (w0 + np.float32(1e-2) * gs))) <= 1e-6
+
+
+@pytest.mark.parametrize("dtype", [D.F32, D.BF16])
+def test_fused_step_world1_equals_sharded(ctx, dtype):
+    """At world 1 dashcu_fused_step runs its kernel on the local buffers: bit-identical to
+    dashcu_sharded_step over several Adam steps (same slice moments), rollouts included."""
+    arch = GQA
+    p = params32(arch, 0.3, 10)
+    g = np.random.default_rng(3).standard_normal(len(p)).astype(np.float32).astype(np.float64)
+    a, b = D.Policy(ctx, arch, dtype), D.Policy(ctx, arch, dtype)
+    for pol in (a, b):
+        pol.upload(p)
+    for step in range(3):
+        for pol in (a, b):
+            pol.grad_upload(g * (step + 1))
+        a.sharded_step(D.OPT_ADAM, lr=1e-2)
+        b.fused_step(D.OPT_ADAM, lr=1e-2)
+        assert np.array_equal(a.download(), b.download())
+    ra, rb = a.sample([[0, 5, 6]], 4, 9, round_seed=5), b.sample([[0, 5, 6]], 4, 9, round_seed=5)
+    assert np.array_equal(ra.completions, rb.completions)
+    a.close()
+    b.close()
