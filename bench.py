@@ -321,7 +321,9 @@ def run_ours(args, cfg, world, rank, local):
         adv, kept, nk = pol.advantage(tau=cfg["tau"])
         pol.grad_zero()
         pol.accumulate(1.0 / N_global, cfg["micro"])
-        if args.sharded:   # ZeRO-1 form: reduce-scatter, update own slice, all-gather
+        if args.fused:     # ZeRO-1 form as one kernel over NVLink peer memory
+            pol.fused_step(D.OPT_ADAM, lr=1e-6)
+        elif args.sharded:   # ZeRO-1 form: reduce-scatter, update own slice, all-gather
             pol.sharded_step(D.OPT_ADAM, lr=1e-6)
         else:
             pol.allreduce_grads()
@@ -406,7 +408,8 @@ def run_ours(args, cfg, world, rank, local):
         "config": {"workload": cfg["workload"], "model": f"Qwen2.5-{cfg['size'] or 'tiny'}-shaped (reference math,"
                    f" GQA {arch.get('n_heads', 1)}/{arch.get('n_kv_heads', 1)})", "prompts_per_gpu": M, "G": G,
                    "prompt_len": cfg["prompt_len"], "gen_len": ML, "micro_batch": cfg["micro"], "tau": cfg["tau"] if cfg["tau"] is not None else "off",
-                   "optimizer": "adam (sharded, ZeRO-1)" if args.sharded else "adam", "global_batch": M * G * world, "seq_len": cfg["prompt_len"] + ML,
+                   "optimizer": ("adam (ZeRO-1, fused peer-memory kernel)" if args.fused else
+                                 "adam (sharded, ZeRO-1)" if args.sharded else "adam"), "global_batch": M * G * world, "seq_len": cfg["prompt_len"] + ML,
                    "parallelism": f"dp{world}", "init_std": cfg.get("init", 0.02),
                    "mean_completion_len": tot_toks / (args.steps * M * G * world), "l2": "inputs > L2 (KV cache + weights stream every step)"},
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -506,6 +509,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tau", default=None, help="filter threshold override; 'off' = no filter (GRPO-style)")
     ap.add_argument("--sharded", action="store_true", help="ZeRO-1 style sharded optimizer step")
+    ap.add_argument("--fused", action="store_true",
+                    help="ZeRO-1 update fused into one peer-memory kernel (dashcu_fused_step)")
     ap.add_argument("--no-profile", action="store_true",
                     help="no kernel-class events in the timed region (decode steps replay as CUDA graphs; "
                          "no roofline / kernel_classes)")

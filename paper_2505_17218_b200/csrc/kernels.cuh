@@ -16,12 +16,13 @@ void fill_f32(cudaStream_t s, float* p, float v, int64_t n);
 // update and the fused reduce-scatter / update / all-gather kernel so both round alike.
 __device__ __forceinline__ float opt_update(int kind, float wi, float gi, float* m, float* v, float lr, float b1,
                                             float b2, float eps, float c1, float c2) {
-  if (kind == 0) return wi + lr * gi;
-  const float mi = b1 * *m + (1.f - b1) * gi;
-  const float vi = b2 * *v + (1.f - b2) * gi * gi;
+  // explicit roundings: the same bits whichever kernel inlines it
+  if (kind == 0) return __fmaf_rn(lr, gi, wi);
+  const float mi = __fmaf_rn(b1, *m, __fmul_rn(1.f - b1, gi));
+  const float vi = __fmaf_rn(b2, *v, __fmul_rn(__fmul_rn(1.f - b2, gi), gi));
   *m = mi;
   *v = vi;
-  return wi + lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+  return __fmaf_rn(lr, __fdiv_rn(__fdiv_rn(mi, c1), __fadd_rn(__fsqrt_rn(__fdiv_rn(vi, c2)), eps)), wi);
 }
 
 // Fused reduce-scatter + update + all-gather over peer memory (dashcu_fused_step): rank
