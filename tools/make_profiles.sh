@@ -6,7 +6,7 @@ TAG=${1:-r1}
 O=gpurun_out
 P=profiles
 mkdir -p $P
-python tools/traffic_summary.py $O/launches_mini_$TAG.csv $P/ncu_traffic.json > $P/${TAG}_launch_list.md
+python tools/traffic_summary.py $O/launches_mini_$TAG.csv $P/${TAG}_traffic_mini.json > $P/${TAG}_launch_list.md
 for k in sample train_gemm attn_bwd attn_fwd attn_decode; do
   [ -f $O/prof_${k}_$TAG.ncu-rep ] && python tools/ncu_summary.py $O/prof_${k}_$TAG.ncu-rep > $P/${TAG}_ncu_${k}.md
 done
