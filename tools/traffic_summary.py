@@ -16,11 +16,11 @@ def klass(name):
     m = re.search(r"gemm_tc_kernel<(\d+), (\d+), (\w+), (\w+), (\d+), (\d+)>", n)
     if m:
         mode = int(m.group(6))
-        return {0: "gemm_tc", 1: "sample", 2: "lm_rows", 3: "lm_rows"}[mode]
+        return {0: "gemm_tc", 1: "sample", 2: "lm_rows", 3: "lm_rows", 4: "sample"}[mode]
     if "gemm_tc2_kernel" in n:
         return "gemm_tc"
     for key, cls in (("attn_decode", "attn_decode"), ("attn_fwd", "attn_fwd"), ("attn_bwd", "attn_bwd"),
-                     ("sample_scan", "sample"), ("lse_reduce", "lm_rows"), ("optimizer_k", "optimizer"),
+                     ("sample_scan", "sample"), ("embed_", "embed"), ("DeviceRadixSort", "embed"), ("lse_reduce", "lm_rows"), ("optimizer_k", "optimizer"),
                      ("gemm_simt", "gemm_simt"), ("colsum", "colsum"), ("kv_append", "kv_append")):
         if key in n:
             return cls
