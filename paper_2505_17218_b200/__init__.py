@@ -215,7 +215,7 @@ KNOB_DEFAULT = -(2 ** 31)
 
 def set_knob(name: str, value) -> int:
     """Kernel-variant knob (dashcu_set_knob); value None restores the default. Returns the old value."""
-    v = KNOB_DEFAULT if value is None else int({"mma": 1, "tc5": 2, "tc5head": 3}.get(value, value))
+    v = KNOB_DEFAULT if value is None else int({"mma": 1, "tc5": 2}.get(value, value))
     old = lib().dashcu_set_knob(name.encode(), v)
     if old == KNOB_DEFAULT:
         raise InputError(f"unknown knob {name}")

@@ -356,272 +356,6 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
-
-// ---------------------------------------------------------------------------------------
-// Head-pair ping-pong forward (head_dim 64, the C2 geometry). A CTA owns 128 queries of one
-// sequence and runs the KV group's query heads two at a time: heads A and B share every
-// K / V tile (one load, two S = Q K^T products), and each has its own softmax warpgroup
-// (warps 4-7: A, 8-11: B) with ONE query row per thread (no cross-warp max exchange). While
-// one warpgroup is in its exponentials (MUFU-bound) the other loads S, takes the row max,
-// stores P and folds O back into registers, so the MUFU unit stays busy; the MMA warp
-// alternates S_A, S_B, PV_A, PV_B. TMEM: S_A 0, S_B 128, O_A 256, O_B 320 (fp32 columns).
-// Same arithmetic per row as attn_fwd_tc5_k (online softmax in the log2 domain, a quarter
-// of the exponentials on the FMA polynomial, the normaliser over the bf16-rounded P, the
-// O residual for the backward's D).
-struct PPLay {
-  static constexpr int kTile = 128 * 64 * 2;  // one 64-column swizzle atom x 128 rows
-  static constexpr int kST = 4;               // K/V ring depth
-  static constexpr int QA = 0, QB = kTile, K = 2 * kTile, V = K + kST * kTile;
-  static constexpr int PA = V + kST * kTile;  // P per head: [128 q x 128 keys] as two atoms
-  static constexpr int PB = PA + 2 * kTile;
-  static constexpr int BAR = PB + 2 * kTile;
-  static constexpr int BYTES = BAR + 512 + 1024;
-  static_assert(BYTES <= 232448, "exceeds the 227 KB of opt-in shared memory per CTA");
-};
-
-__global__ void __launch_bounds__(384, 1)
-    attn_fwd_pp_k(const __grid_constant__ CUtensorMap mQKV, const int32_t* __restrict__ seq_start, int nh, int nkv,
-                  int nqt_max, bf16* __restrict__ ctx, float* __restrict__ lse, float scale_log2,
-                  bf16* __restrict__ ctx_lo) {
-  constexpr int kHD = 64, kST = PPLay::kST;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int sq = blockIdx.x / nkv, kvh = blockIdx.x % nkv;
-  const int qt = nqt_max - 1 - static_cast<int>(blockIdx.y >> 1), part = blockIdx.y & 1;
-  const int s0 = seq_start[sq], n = seq_start[sq + 1] - s0;
-  const int q0 = qt * kQ;
-  if (q0 >= n) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp0 = nh / nkv, qd = nh * kHD, kvd = nkv * kHD;
-  const int nkt = qt + 1;
-  const bool split = grp0 > 1 && nkt >= 3;  // the longer query tiles split the group over two CTAs
-  if (!split && part) return;
-  const int h_lo = split && part ? (grp0 + 1) / 2 : 0, h_hi = split && !part ? (grp0 + 1) / 2 : grp0;
-  const int nheads = h_hi - h_lo, npairs = (nheads + 1) / 2;
-
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + PPLay::BAR);
-  // [2] each (index = head slot A / B): qfull, qempty, sfull, sfree, pready, ofull, ofree
-  uint64_t *qfull = bar, *qempty = bar + 2, *sfull = bar + 4, *sfree = bar + 6, *pready = bar + 8, *ofull = bar + 10,
-           *ofree = bar + 12, *kvfull = bar + 14, *kvempty = bar + 14 + kST;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14 + 2 * kST);
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kST; ++i) {
-      mbar_init(&kvfull[i], 1);
-      mbar_init(&kvempty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&qfull[i], 1);
-      mbar_init(&qempty[i], 1);
-      mbar_init(&sfull[i], 1);
-      mbar_init(&sfree[i], 128);
-      mbar_init(&pready[i], 128);
-      mbar_init(&ofull[i], 1);
-      mbar_init(&ofree[i], 128);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mQKV)) : "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t sK = smem_u32(smem + PPLay::K), sV = smem_u32(smem + PPLay::V);
-
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------------------------------------------------------- TMA
-      for (int pi = 0, t = 0; pi < npairs; ++pi) {
-        for (int x = 0; x < 2; ++x) {
-          const int hh = 2 * pi + x;
-          if (hh >= nheads) break;
-          mbar_wait_sleep(&qempty[x], (pi & 1) ^ 1);
-          mbar_expect_tx(&qfull[x], PPLay::kTile);
-          tma_load_2d(smem + (x ? PPLay::QB : PPLay::QA), &mQKV, &qfull[x], (kvh * grp0 + h_lo + hh) * kHD, s0 + q0);
-        }
-        for (int j = 0; j < nkt; ++j, ++t) {
-          const int st = t % kST;
-          mbar_wait_sleep(&kvempty[st], ((t / kST) & 1) ^ 1);
-          mbar_expect_tx(&kvfull[st], 2 * PPLay::kTile);
-          tma_load_2d(smem + PPLay::K + st * PPLay::kTile, &mQKV, &kvfull[st], qd + kvh * kHD, s0 + j * kKeys);
-          tma_load_2d(smem + PPLay::V + st * PPLay::kTile, &mQKV, &kvfull[st], qd + kvd + kvh * kHD, s0 + j * kKeys);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------------------------------------------------------- MMA
-      constexpr uint32_t I_S = idesc(128, false, false), I_O = idesc(kHD, false, true);
-      // per head slot x: tile counter tx (its S / P / O phases)
-      auto issue_s = [&](int x, int t, int pi, int j) {
-        if (t >= 1) mbar_wait_sleep(&sfree[x], (t - 1) & 1);  // the warpgroup holds S_{t-1} in registers
-        if (j == 0) mbar_wait_sleep(&qfull[x], pi & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t k = sK + ((pi * nkt + j) % kST) * PPLay::kTile, qa = smem_u32(smem + (x ? PPLay::QB : PPLay::QA));
-#pragma unroll
-        for (int kk = 0; kk < kHD / 16; ++kk)
-          umma_bf16(tmem + static_cast<uint32_t>(x) * 128u, smem_desc(qa + kk * 32, 16, 1024), smem_desc(k + kk * 32, 16, 1024), I_S, kk > 0);
-        umma_commit(&sfull[x]);
-        if (j == nkt - 1) umma_commit(&qempty[x]);
-      };
-      auto issue_pv = [&](int x, int t, int st) {
-        mbar_wait_sleep(&pready[x], t & 1);
-        if (t >= 1) mbar_wait_sleep(&ofree[x], (t - 1) & 1);  // O_{t-1} read out
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t v = sV + st * PPLay::kTile, p = smem_u32(smem + (x ? PPLay::PB : PPLay::PA));
-#pragma unroll
-        for (int kk = 0; kk < kKeys / 16; ++kk)
-          umma_bf16(tmem + 256u + static_cast<uint32_t>(x) * 64u, smem_desc(p + (kk >> 2) * PPLay::kTile + (kk & 3) * 32, 16, 1024),
-                    smem_desc(v + kk * 2048, PPLay::kTile, 1024), I_O, kk > 0);
-        umma_commit(&ofull[x]);
-      };
-      int ta = 0, tb = 0;  // per-slot tile counters
-      for (int pi = 0, t = 0; pi < npairs; ++pi) {
-        const bool hb = 2 * pi + 1 < nheads;
-        mbar_wait_sleep(&kvfull[t % kST], (t / kST) & 1);
-        issue_s(0, ta, pi, 0);
-        if (hb) issue_s(1, tb, pi, 0);
-        for (int j = 0; j < nkt; ++j, ++t) {
-          const int st = t % kST;
-          issue_pv(0, ta, st);
-          ++ta;
-          if (j + 1 < nkt) {
-            mbar_wait_sleep(&kvfull[(t + 1) % kST], ((t + 1) / kST) & 1);
-            issue_s(0, ta, pi, j + 1);
-          }
-          if (hb) {
-            issue_pv(1, tb, st);
-            ++tb;
-          }
-          umma_commit(&kvempty[st]);  // both PV products of this K / V tile are queued before it
-          if (hb && j + 1 < nkt) issue_s(1, tb, pi, j + 1);
-        }
-      }
-    }
-  } else if (warp >= 4) {  // ------------------------------------------------------- softmax
-    const int x = (warp - 4) >> 2, qq = warp & 3, r = qq * 32 + lane, q = q0 + r;
-    const uint32_t lanes = static_cast<uint32_t>(qq * 32) << 16;
-    const uint32_t sP = smem_u32(smem + (x ? PPLay::PB : PPLay::PA));
-    float acc[kHD];
-    int t = 0;  // this slot's tile counter
-    for (int pi = 0; pi < npairs; ++pi) {
-      const int hh = 2 * pi + x;
-      if (hh >= nheads) break;
-      const int h = kvh * grp0 + h_lo + hh;
-#pragma unroll
-      for (int i = 0; i < kHD; ++i) acc[i] = 0.f;
-      float m = -FLT_MAX, m_prev = -FLT_MAX, l = 0.f;
-      // O_{t-1} into the registers: acc = acc * 2^(m_old - m_new) + O
-      auto take_o = [&](int tt, float m_old, float m_new) {
-        mbar_wait_sleep(&ofull[x], tt & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const float c = ex2(m_old - m_new);
-        const uint64_t c2 = f2_pack(c, c);
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {  // 32 head dims at a time (register pressure)
-          uint32_t o[32];
-          tmem_ld32_async(tmem + lanes + 256u + static_cast<uint32_t>(x) * 64u + h2 * 32, o);
-          tmem_wait_ld();
-          if (h2 == 1) {
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            mbar_arrive(&ofree[x]);
-          }
-#pragma unroll
-          for (int i = 0; i < 32; i += 2)
-            f2_unpack(f2_fma(f2_pack(acc[h2 * 32 + i], acc[h2 * 32 + i + 1]), c2,
-                             f2_pack(__uint_as_float(o[i]), __uint_as_float(o[i + 1]))),
-                      acc[h2 * 32 + i], acc[h2 * 32 + i + 1]);
-        }
-      };
-      for (int j = 0; j < nkt; ++j, ++t) {
-        mbar_wait_sleep(&sfull[x], t & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        // pass 1: the row max over 128 keys (32-column chunks; the causal diagonal masked)
-        float mx = -FLT_MAX;
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t sr[32];
-          tmem_ld32_async(tmem + lanes + static_cast<uint32_t>(x) * 128u + ch * 32, sr);
-          tmem_wait_ld();
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const float v = __uint_as_float(sr[c]);
-            mx = (j < qt || j * kKeys + ch * 32 + c <= q) ? fmaxf(mx, v) : mx;
-          }
-        }
-        const float m_new = fmaxf(m, mx * scale_log2);
-        // O_{t-1} out of TMEM (its PV also frees the P buffer) before P_t is written
-        if (j > 0) take_o(t - 1, m_prev, m);
-        // pass 2: exponentials, P (bf16, UMMA swizzle layout) and the row sum of the rounded P
-        uint64_t rs2[2] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
-        const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nm2 = f2_pack(-m_new, -m_new);
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t sr[32], pk[16];
-          tmem_ld32_async(tmem + lanes + static_cast<uint32_t>(x) * 128u + ch * 32, sr);
-          tmem_wait_ld();
-          if (ch == 3) {
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            mbar_arrive(&sfree[x]);
-          }
-#pragma unroll
-          for (int c = 0; c < 32; c += 2) {
-            float a0, a1;
-            f2_unpack(f2_fma(f2_pack(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sc2, nm2), a0, a1);
-            const bool diag = j == qt;
-            const int key = j * kKeys + ch * 32 + c;
-            const float p0 = (diag && key > q) ? 0.f : ex2(a0);
-            const float p1 = (diag && key + 1 > q) ? 0.f : (((c >> 1) & 1) == 0 ? ex2_poly(a1) : ex2(a1));
-            pk[c >> 1] = pack2(p0, p1);
-            rs2[(c >> 1) & 1] = f2_add(rs2[(c >> 1) & 1], f2_pack(__uint_as_float(pk[c >> 1] << 16),
-                                                                  __uint_as_float(pk[c >> 1] & 0xffff0000u)));
-          }
-          // keys [32 ch, 32 ch + 32): atom ch / 2, 16-byte chunks 4 (ch % 2) .. + 3
-#pragma unroll
-          for (int k4 = 0; k4 < 4; ++k4) {
-            const int chunk = (ch & 1) * 4 + k4;
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sP + (ch >> 1) * PPLay::kTile + r * 128 +
-                                                                           ((chunk ^ (r & 7)) << 4)),
-                         "r"(pk[k4 * 4]), "r"(pk[k4 * 4 + 1]), "r"(pk[k4 * 4 + 2]), "r"(pk[k4 * 4 + 3])
-                         : "memory");
-          }
-        }
-        float r0, r1, r2, r3;
-        f2_unpack(rs2[0], r0, r1);
-        f2_unpack(rs2[1], r2, r3);
-        l = l * ex2(m - m_new) + ((r0 + r1) + (r2 + r3));
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&pready[x]);
-        m_prev = m;
-        m = m_new;
-      }
-      take_o(t - 1, m_prev, m);
-      if (q < n) {
-        const float inv = 1.f / l;
-        bf16* out = ctx + static_cast<int64_t>(s0 + q) * qd + h * kHD;
-#pragma unroll
-        for (int i = 0; i < kHD; i += 8) {
-          uint32_t hv[4], lv[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            hv[k] = pack2(acc[i + 2 * k] * inv, acc[i + 2 * k + 1] * inv);
-            lv[k] = pack2(acc[i + 2 * k] * inv - __uint_as_float(hv[k] << 16),
-                          acc[i + 2 * k + 1] * inv - __uint_as_float(hv[k] & 0xffff0000u));
-          }
-          *reinterpret_cast<uint4*>(out + i) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
-          if (ctx_lo) *reinterpret_cast<uint4*>(ctx_lo + (out - ctx) + i) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
-        }
-        lse[static_cast<int64_t>(s0 + q) * nh + h] = (m + __log2f(l)) * 0.6931471805599453f;
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
-}
-
 }  // namespace
 
 namespace {
@@ -647,21 +381,12 @@ bool attn_fwd_tc5(cudaStream_t s, const bf16* qkv, const int32_t* seq_start, int
   if (force == 1) return false;
   // one-tile sequences (the prompt prefill) amortise the per-CTA TMEM / barrier / first-load
   // latency poorly; the mma.sync kernel (several CTAs per SM) is faster there
-  if (max_len <= 2 * kQ && force < 2) return false;
+  if (max_len <= 2 * kQ && force != 2) return false;
   const int qkvd = nh * hd + 2 * nkv * hd;
   CUtensorMap mq;
   if (!tma_map_2d(&mq, qkv, rows, qkvd, qkvd, 64, 128, false, 128, true)) return false;  // one swizzle atom per box
   const int nqt = (max_len + kQ - 1) / kQ;
-  if (hd == 64 && force != 3) {  // KNOB_ATTN_FWD = 3: the one-head-at-a-time kernel
-    static bool attr = false;
-    if (!attr) {
-      DCU_CHECK(cudaFuncSetAttribute(attn_fwd_pp_k, cudaFuncAttributeMaxDynamicSharedMemorySize, PPLay::BYTES));
-      attr = true;
-    }
-    attn_fwd_pp_k<<<dim3(n_seq * nkv, 2 * nqt), 384, PPLay::BYTES, s>>>(
-        mq, seq_start, nh, nkv, nqt, ctx, lse, 1.4426950408889634f / sqrtf(64.f), ctx_lo);
-    DCU_LAUNCHED();
-  } else if (hd == 64)
+  if (hd == 64)
     launch_fwd_tc5<64>(s, mq, seq_start, n_seq, nqt, nh, nkv, ctx, lse, ctx_lo);
   else
     launch_fwd_tc5<128>(s, mq, seq_start, n_seq, nqt, nh, nkv, ctx, lse, ctx_lo);

@@ -60,8 +60,7 @@ enum Knob : int {
   KNOB_NO_TMA_STORE,     // 1: per-thread epilogue stores instead of bulk tensor stores
   KNOB_GEMM_RESID_DB,    // 0: no double-buffered residual prefetch in the pair epilogue
   KNOB_GEMM_RESID_DEEP,  // -1 model (K >= 2048), 0 / 1 force the 5-stage / 4-epilogue-warp ring
-  KNOB_ATTN_FWD,         // 0 auto, 1 mma.sync kernel, 2 tcgen05 even for one-tile sequences, 3 = 2 with the
-                         // one-head-at-a-time tcgen05 kernel instead of the head-pair one (head_dim 64)
+  KNOB_ATTN_FWD,         // 0 auto, 1 mma.sync kernel, 2 tcgen05 kernel even for one-tile sequences
   KNOB_ATTN_BWD,         // 0 auto, 1 mma.sync kernel
   KNOB_ATTN_BWD_CHUNK,   // sequences per CTA chunk in the tcgen05 backward (0: 2-D grid order)
   KNOB_LSE_RECOMPUTE,    // 1: the backward recomputes the LM-head LSE instead of reusing the sampler's

@@ -42,7 +42,6 @@ int knob_value(int i, const char* v) {
   if (i == KNOB_ATTN_FWD || i == KNOB_ATTN_BWD) {
     if (!strcmp(v, "mma")) return 1;
     if (!strcmp(v, "tc5")) return 2;
-    if (!strcmp(v, "tc5head")) return 3;
   }
   return atoi(v);
 }

@@ -289,12 +289,12 @@ def test_pg_gradient_parity(ctx, arch, dtype):
     pol.close()
 
 
-@pytest.mark.parametrize("kernel", ["tc5", "mma", "tc5:0", "tc5:3", "tc5head"])
+@pytest.mark.parametrize("kernel", ["tc5", "mma", "tc5:0", "tc5:3"])
 def test_pg_gradient_parity_long_sequences(ctx, knob, kernel):
     """Ragged sequences up to 300 tokens: several key and query tiles, the causal
     diagonal tiles and ragged tile ends, through the tcgen05 and the mma.sync attention
     kernels (forward and backward); tc5:<chunk> is the backward's chunked CTA order
-    (0: 2-D grid order); tc5 runs the head-pair forward, tc5head the one-head-at-a-time one."""
+    (0: 2-D grid order)."""
     if kernel == "mma":
         knob("ATTN_BWD", "mma")
     if kernel.startswith("tc5:"):
