@@ -289,24 +289,9 @@ __global__ void __launch_bounds__(384, 1)
         for (int c = 0; c < 64; c += 2) {  // exponent arguments and row sums on the fp32x2 pipe
           float a0, a1;
           f2_unpack(f2_fma(f2_pack(sv[c], sv[c + 1]), sc2, nm2), a0, a1);
-#ifdef DASHCU_FWD_EXP_F16
-          // two exponentials per MUFU op: 2^a on packed f16 (11-bit arguments and results:
-          // relative error ~ |a| 2^-12, below the bf16 rounding P gets anyway; results under
-          // 2^-24 of the row max flush to 0, masked keys included), then bf16 for the PV operand
-          float p0, p1;
-          {
-            uint32_t h, e;
-            asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(fmaxf(a1, -32.f)), "f"(fmaxf(a0, -32.f)));
-            asm("ex2.approx.f16x2 %0, %1;" : "=r"(e) : "r"(h));
-            asm("{\n\t.reg .f16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\tcvt.f32.f16 %0, lo;\n\tcvt.f32.f16 %1, hi;\n\t}"
-                : "=f"(p0), "=f"(p1)
-                : "r"(e));
-          }
-#else
           const float p0 = ex2(a0);
           // a fraction of the exponentials on the FMA pipe (the exp loop is MUFU-bound)
           const float p1 = (kSplitExp && ((c >> 1) % kSplitEvery == 0)) ? ex2_poly(a1) : ex2(a1);
-#endif
           pk[c >> 1] = pack2(p0, p1);
           // the row sum adds the bf16-rounded values the PV product consumes (O / l consistent)
           rs2[(c >> 1) & 1] = f2_add(rs2[(c >> 1) & 1], f2_pack(__uint_as_float(pk[c >> 1] << 16),
