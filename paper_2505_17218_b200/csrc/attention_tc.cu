@@ -33,6 +33,14 @@ struct DecCfg {
   static constexpr int SMEM = NW * WARP_BYTES;
 };
 
+// The completion KV stream (GBs per decode step) is loaded with an L2 evict-first policy so
+// it does not evict the next GEMMs' weights and activations (-DDASHCU_DECODE_KV_NORMAL: A/B).
+#ifndef DASHCU_DECODE_KV_NORMAL
+constexpr bool kStreamKV = true;
+#else
+constexpr bool kStreamKV = false;
+#endif
+
 template <int HD>
 __global__ void __launch_bounds__(DecCfg<HD>::NW * 32)
     attn_decode_tc_k(const bf16* __restrict__ qkv, const bf16* __restrict__ kp, const bf16* __restrict__ vp,
@@ -56,6 +64,7 @@ __global__ void __launch_bounds__(DecCfg<HD>::NW * 32)
   // the sequence's page-table row, one entry per lane (completion <= 32 pages = 2048 slots);
   // longer rows read the table directly
   const bool shfl_pages = dr.max_pages <= 32;
+  const uint64_t stream_pol = l2_policy_evict_first();
   const int32_t lane_page =
       shfl_pages && lane < dr.max_pages ? __ldg(dr.ptab + static_cast<int64_t>(sq) * dr.max_pages + lane) : 0;
   uint8_t* wsm = smem + warp * Cf::WARP_BYTES;
@@ -108,8 +117,13 @@ __global__ void __launch_bounds__(DecCfg<HD>::NW * 32)
       const bool ok = first + r < lim;
       const int64_t ro = ok ? static_cast<int64_t>(r) * HD + u * 8 : 0;
       const int off = swz(r, u, UNITS);
-      cp_async16(kbase + off, kb + ro, ok ? 16 : 0);
-      cp_async16(vbase + off, vb + ro, ok ? 16 : 0);
+      if (c < cpm || !kStreamKV) {  // the group's prompt KV: read by its G sequences, keep in L2
+        cp_async16(kbase + off, kb + ro, ok ? 16 : 0);
+        cp_async16(vbase + off, vb + ro, ok ? 16 : 0);
+      } else {  // this sequence's completion KV: read once per step, evict first
+        cp_async16_hint(kbase + off, kb + ro, ok ? 16 : 0, stream_pol);
+        cp_async16_hint(vbase + off, vb + ro, ok ? 16 : 0, stream_pol);
+      }
     }
   };
 
