@@ -67,6 +67,7 @@ enum Knob : int {
   KNOB_PDL,              // 1: programmatic dependent launch
   KNOB_DECODE_GRAPH,     // 0: no CUDA-graph replay of decode steps
   KNOB_DECODE_COMPACT,   // 0: finished sequences keep their decode rows until the round ends
+  KNOB_GEMM_SKINNY_AR,   // 0: skinny GEMMs (M <= 128) stage full 128-row A boxes
   KNOB_NUM
 };
 extern int g_knob[KNOB_NUM];
@@ -172,5 +173,16 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 inline int cdiv(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 
 constexpr int kNumSMs = 148;
+
+// SM count of the current device (host side, cached after the first query)
+inline int num_sms_host() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = kNumSMs;
+  }
+  return n;
+}
 
 }  // namespace dashcu

@@ -162,17 +162,24 @@ struct OutMaps {
   CUtensorMap ax;   // input: bf16 tanh activations of EPI_DTANH (bit 3)
 };
 
-template <int BN, int STAGES, bool AK, bool BKM, int EPW>
+// AR: rows of the A box a stage holds (BM, or 32 / 64 for the skinny decode GEMMs: the MMA
+// still reads 128 rows, the rows past AR are stale shared memory whose accumulator rows
+// (>= M) are never stored, and the TMA no longer writes 96 zero-filled rows per k-block).
+// KSUB: k-blocks per ring stage (one full-barrier wait + fence + commit per stage: that
+// sequence costs the MMA issuer ~190 cycles, which is 2.4 x the four MMAs of a k-block
+// at N <= 64, tools/mma_probe.cu; the MMA order over K is the same for every KSUB).
+template <int BN, int STAGES, bool AK, bool BKM, int EPW, int AR = BM, int KSUB = 1>
 struct Cfg {
-  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int A_BYTES = AR * BK * 2;
   static constexpr int BNS = BN;
   static constexpr int B_BYTES = BNS * BK * 2;
-  static constexpr int B_LOAD = BN * BK * 2;  // bytes the B loads of a stage deliver
+  static constexpr int B_LOAD = BN * BK * 2;  // bytes the B loads of a k-block deliver
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int KB_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGE_BYTES = KSUB * KB_BYTES;
   static constexpr int STG_OFF = STAGES * STAGE_BYTES;  // EPW x 4 KB epilogue staging
   static constexpr int BAR_OFF = STG_OFF + EPW * kStageBytes;
-  static constexpr int SMEM = BAR_OFF + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = BAR_OFF + 1024 /*align*/ + (2 * STAGES + 4 + EPW) * 8 + 16 /*barriers, TMEM slot*/;
   static constexpr int THREADS = 128 + EPW * 32;
   // kind::f16 instruction descriptor: D f32, A/B bf16, majors, N>>3, M>>4
   static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((AK ? 0u : 1u) << 15) |
@@ -660,12 +667,24 @@ __device__ __forceinline__ void epilogue_slice(const GemmShape& g, const Epi& e,
   }
 }
 
+#ifdef DASHCU_GEMM_TRACE
+// experiment builds: CTA 0's per-k-block clocks (producer issue, MMA data-ready) of the
+// last launch, read with dashcu_debug_gemm_trace
+__device__ long long g_trace[3][512];
+#define GEMM_TRACE(i, k) \
+  if (blockIdx.x == 0 && (k) < 512) g_trace[i][k] = clock64()
+#else
+#define GEMM_TRACE(i, k)
+#endif
+
 // MODE: 0 generic store epilogue, 1 fused sampling, 2 LSE partials, 3 dz, 4 chosen-slice recompute
-template <int BN, int STAGES, bool AK, bool BKM, int EPW, int MODE>
-__global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
+template <int BN, int STAGES, bool AK, bool BKM, int EPW, int MODE, int AR = BM, int KSUB = 1>
+__global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ OutMaps om, GemmShape g, Epi e, SampleArgs sa) {
-  using C = Cfg<BN, STAGES, AK, BKM, EPW>;
+  static_assert(AR == BM || AK, "partial A boxes are K-major only");
+  static_assert(KSUB == 1 || MODE == 0, "multi-k-block stages: generic GEMMs only");
+  using C = Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
@@ -711,7 +730,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      int kb_all = 0;
+      int st_all = 0;
       for (int w = blockIdx.x; w < nitem; w += gridDim.x) {
         const int t = w / S, sp = w % S;
         const int m0 = (MODE == 4 ? t / tiles_n : tile_m(g, t, tiles_m, tiles_n)) * BM,
@@ -725,13 +744,17 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
           }
         }
         const int kb_lo = sp * kps, kb_hi = min(nkb, kb_lo + kps);
-        for (int kb = kb_lo; kb < kb_hi; ++kb, ++kb_all) {
-          const int s = kb_all % STAGES;
-          const uint32_t ph = (kb_all / STAGES) & 1;
+        for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += KSUB, ++st_all) {
+          const int s = st_all % STAGES;
+          const uint32_t ph = (st_all / STAGES) & 1;
           mbar_wait_pipe(&empty[s], ph ^ 1);
-          uint8_t* sa_ = smem + s * C::STAGE_BYTES;
+          GEMM_TRACE(0, st_all);
+          const int cnt = min(KSUB, kb_hi - kb0);
+          mbar_expect_tx(&full[s], cnt * (C::A_BYTES + C::B_LOAD));
+          for (int j = 0; j < cnt; ++j) {
+          const int kb = kb0 + j;
+          uint8_t* sa_ = smem + s * C::STAGE_BYTES + j * C::KB_BYTES;
           uint8_t* sb_ = sa_ + C::A_BYTES;
-          mbar_expect_tx(&full[s], C::A_BYTES + C::B_LOAD);
           const int k0 = kb * BK;
           if (AK) {
             tma_load_2d(sa_, &mapA, &full[s], k0, m0);
@@ -748,12 +771,13 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
 #pragma unroll
             for (int j = 0; j < C::BNS / 64; ++j) tma_load_2d(sb_ + j * 64 * BK * 2, &mapB, &full[s], n0 + 64 * j, k0);
           }
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      int kb_all = 0, i = 0;
+      int st_all = 0, i = 0;
       for (int w = blockIdx.x; w < nitem; w += gridDim.x, ++i) {
         const int kb_lo = (w % S) * kps, kb_hi = min(nkb, kb_lo + kps);
         const int acc = i & 1;
@@ -761,12 +785,18 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
         mbar_wait_pipe(&tempty[acc], aph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * BN;
-        for (int kb = kb_lo; kb < kb_hi; ++kb, ++kb_all) {
-          const int s = kb_all % STAGES;
-          const uint32_t ph = (kb_all / STAGES) & 1;
+        for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += KSUB, ++st_all) {
+          const int s = st_all % STAGES;
+          const uint32_t ph = (st_all / STAGES) & 1;
+          GEMM_TRACE(1, st_all);
           mbar_wait_pipe(&full[s], ph);
+          GEMM_TRACE(2, st_all);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t sa_ = smem_u32(smem + s * C::STAGE_BYTES);
+          const int cnt = min(KSUB, kb_hi - kb0);
+#pragma unroll 1
+          for (int j = 0; j < cnt; ++j) {
+          const int kb = kb0 + j;
+          const uint32_t sa_ = smem_u32(smem + s * C::STAGE_BYTES + j * C::KB_BYTES);
           const uint32_t sb_ = sa_ + C::A_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
@@ -774,6 +804,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW>::THREADS, 1)
             const uint64_t da = AK ? smem_desc(sa_ + k * 32, 16, 1024) : smem_desc(sa_ + k * 2048, 64 * BK * 2, 1024);
             const uint64_t db = BKM ? smem_desc(sb_ + k * 32, 16, 1024) : smem_desc(sb_ + k * 2048, 64 * BK * 2, 1024);
             umma_bf16(d, da, db, C::IDESC, (kb > kb_lo || k > 0) ? 1u : 0u);
+          }
           }
           umma_commit(&empty[s]);
         }
@@ -891,11 +922,12 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, bool AK, bool BKM, int EPW, int MODE>
+template <int BN, int STAGES, bool AK, bool BKM, int EPW, int MODE, int AR = BM, int KSUB = 1>
 void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& om, const GemmShape& g,
             const Epi& e, const SampleArgs& sa) {
-  using C = Cfg<BN, STAGES, AK, BKM, EPW>;
-  auto k = gemm_tc_kernel<BN, STAGES, AK, BKM, EPW, MODE>;
+  using C = Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB>;
+  static_assert(C::SMEM <= 232448, "shared memory");
+  auto k = gemm_tc_kernel<BN, STAGES, AK, BKM, EPW, MODE, AR, KSUB>;
   static bool attr = false;
   if (!attr) {
     DCU_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -908,8 +940,8 @@ void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const 
                MODE == 4 ? 2.0 * g.M * kSlice * static_cast<double>(g.K) : 2.0 * g.M * g.N * static_cast<double>(g.K),
                0);
   if (ps.keyed())
-    snprintf(ps.key, sizeof(ps.key), "mode%d 128x%d M%d N%d K%d %c%c epi%d split%d", MODE, BN, g.M, g.N, g.K,
-             AK ? 'k' : 'm', BKM ? 'k' : 'm', e.kind, MODE == 0 ? e.splits : 1);
+    snprintf(ps.key, sizeof(ps.key), "mode%d %dx%d/%d M%d N%d K%d %c%c epi%d split%d", MODE, AR, BN, KSUB, g.M, g.N,
+             g.K, AK ? 'k' : 'm', BKM ? 'k' : 'm', e.kind, MODE == 0 ? e.splits : 1);
   launch_pdl(k, dim3(grid), dim3(C::THREADS), C::SMEM, s, ma, mb, om, g, e, sa);
   DCU_LAUNCHED();
 }
@@ -924,6 +956,17 @@ void dispatch_majors(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& m
   else if (g.b_kmajor) launch<BN, STAGES, false, true, 8, 0>(s, ma, mb, om, g, e, none);
   else launch<BN, STAGES, false, false, 8, 0>(s, ma, mb, om, g, e, none);
 }
+
+}  // namespace
+extern "C" __attribute__((visibility("default"))) int dashcu_debug_gemm_trace(long long* out) {
+#ifdef DASHCU_GEMM_TRACE
+  return cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace)) == cudaSuccess ? 0 : 4;
+#else
+  (void)out;
+  return 1;
+#endif
+}
+namespace {
 
 bool legal(const GemmShape& g) {
   if (g.K <= 0 || g.M <= 0 || g.N <= 0) return false;
@@ -1275,8 +1318,10 @@ bool raster_n_fast(const GemmShape& g) {
 // accumulation order stays that of every other tile shape (scheduling independence).
 bool gemm_tc_skinny(cudaStream_t s, const GemmShape& g, const Epi& e) {
   const int BN = g.N >= 64 * 64 ? 64 : 32;
+  // A box rows: the batch rounded up to 32 / 64 / 128 (both operands K-major: the decode)
+  const int AR = !(g.a_kmajor && g.b_kmajor) || knob(KNOB_GEMM_SKINNY_AR) == 0 ? BM : g.M <= 32 ? 32 : g.M <= 64 ? 64 : BM;
   CUtensorMap ma, mb;
-  bool ok = g.a_kmajor ? make_map(&ma, g.A, g.M, g.K, g.lda, BK, BM) : make_map(&ma, g.A, g.K, g.M, g.lda, 64, BK);
+  bool ok = g.a_kmajor ? make_map(&ma, g.A, g.M, g.K, g.lda, BK, AR) : make_map(&ma, g.A, g.K, g.M, g.lda, 64, BK);
   ok = ok && (g.b_kmajor ? make_map(&mb, g.B, g.N, g.K, g.ldb, BK, BN) : make_map(&mb, g.B, g.K, g.N, g.ldb, 64, BK));
   if (!ok) return false;
   OutMaps om;
@@ -1284,8 +1329,22 @@ bool gemm_tc_skinny(cudaStream_t s, const GemmShape& g, const Epi& e) {
   Epi et = e;
   et.tma = out_maps_for(g, e, &om);
   et.splits = 1;
-  if (BN == 64) dispatch_majors<64, 8>(s, ma, mb, om, g, et);  // 8 x 24 KB stages
-  else dispatch_majors<32, 8>(s, ma, mb, om, g, et);           // 8 x 20 KB stages
+  const SampleArgs none;
+  // four k-blocks per ring stage (one barrier round trip per 16 MMAs), ~192 KB of ring
+  if (AR == 32) {
+    if (BN == 64) launch<64, 4, true, true, 8, 0, 32, 4>(s, ma, mb, om, g, et, none);  // 4 x 48 KB
+    else launch<32, 6, true, true, 8, 0, 32, 4>(s, ma, mb, om, g, et, none);           // 6 x 32 KB
+  } else if (AR == 64) {
+    if (BN == 64) launch<64, 3, true, true, 8, 0, 64, 4>(s, ma, mb, om, g, et, none);  // 3 x 64 KB
+    else launch<32, 4, true, true, 8, 0, 64, 4>(s, ma, mb, om, g, et, none);           // 4 x 48 KB
+  } else if (g.a_kmajor && g.b_kmajor && knob(KNOB_GEMM_SKINNY_AR) != 0) {
+    if (BN == 64) launch<64, 4, true, true, 8, 0, BM, 2>(s, ma, mb, om, g, et, none);  // 4 x 48 KB
+    else launch<32, 4, true, true, 8, 0, BM, 2>(s, ma, mb, om, g, et, none);           // 4 x 40 KB
+  } else if (BN == 64) {
+    dispatch_majors<64, 8>(s, ma, mb, om, g, et);  // 8 x 24 KB stages
+  } else {
+    dispatch_majors<32, 8>(s, ma, mb, om, g, et);  // 8 x 20 KB stages
+  }
   return true;
 }
 

@@ -353,6 +353,10 @@ __device__ __forceinline__ void scan_finish(const SliceSel& q, const float* l, i
 // owns a block of consecutive slices; block, slice and id sums are accumulated in the
 // contract's order, so the chosen id is a pure function of the fp32 logits, 1/T and the
 // row key. Then the token bookkeeping of policy.cpp:423-426 (EOS stops, cap, logp at T=1).
+// The row's slice records (38 KB at V = 151,936, T = 1) are first copied into the warp's
+// shared-memory window with coalesced, independent vector loads: the lane-blocked walk
+// reads lane-strided records, which straight from global memory was a chain of ~300
+// dependent-latency loads per lane (33 us per decode step at any batch size).
 __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ part, int nslices,
                                                      const float* __restrict__ logits, int64_t logits_ld, int rows,
                                                      int V, int bos, int eos, float inv_t, const uint64_t* keys,
@@ -390,8 +394,20 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
     return;
   }
   // records {m, Z, m1, Z1}; at T = 1 the fused epilogue stores only {m, Z} (m1 = m, Z1 = Z)
-  const float4* P4 = reinterpret_cast<const float4*>(part) + static_cast<int64_t>(row) * nslices;
-  const float2* P2 = reinterpret_cast<const float2*>(part) + static_cast<int64_t>(row) * nslices;
+  extern __shared__ float4 s_rec[];  // [warps per block][nslices records]
+  const int recf = compact ? 2 : 4;  // floats per record
+  float* srow = reinterpret_cast<float*>(s_rec) + static_cast<int64_t>(threadIdx.x >> 5) * nslices * recf;
+  {
+    const float* grow = part + static_cast<int64_t>(row) * nslices * recf;
+    const int n2 = nslices * recf / 2;  // float2 units (rows are 8-byte aligned)
+    const float2* g2 = reinterpret_cast<const float2*>(grow);
+    float2* s2 = reinterpret_cast<float2*>(srow);
+#pragma unroll 8
+    for (int i = lane; i < n2; i += 32) s2[i] = __ldg(g2 + i);
+    __syncwarp();
+  }
+  const float4* P4 = reinterpret_cast<const float4*>(srow);
+  const float2* P2 = reinterpret_cast<const float2*>(srow);
   auto rec = [&](int s) -> float4 {
     if (compact) {
       const float2 q = P2[s];
@@ -928,9 +944,22 @@ void sample_scan(cudaStream_t s, const float* part, int nslices, const float* lo
                  uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len,
                  bool compact, float* lse_out, const int32_t* row_seq, int phase, SliceSel* sel, const float* dump,
                  int64_t dump_ld, int* mismatches, const int* step_dev) {
-  launch_pdl(sample_scan_k, dim3(cdiv(rows, 8)), dim3(256), 0, s, part, nslices, logits, logits_ld, rows, V, bos, eos,
-             inv_t, keys, step, cap, finished, comp, logp, len, tok_next, max_len, compact, lse_out, row_seq, phase, sel,
-             dump, dump_ld, mismatches, step_dev);
+  // phases 0 / 1 stage each row's records in shared memory: warps per block by the row size
+  // (one warp per CTA for small batches, so the copies spread over many SMs)
+  const size_t row_bytes = static_cast<size_t>(nslices) * (compact ? 8 : 16);
+  if (phase != 2 && row_bytes > 200 * 1024) throw Error(1, "sample_scan: vocabulary too large for the staged walk");
+  int wpb = 8;
+  if (phase != 2) wpb = rows <= 2 * num_sms_host() ? 1 : std::max(1, std::min(8, static_cast<int>(200 * 1024 / row_bytes)));
+  const size_t smem = phase == 2 ? 0 : row_bytes * wpb;
+  static size_t smem_set = 0;
+  if (smem > 48 * 1024 && smem > smem_set) {
+    DCU_CHECK(cudaFuncSetAttribute(sample_scan_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 16));
+    smem_set = 200 * 1024 + 16;
+  }
+  launch_pdl(sample_scan_k, dim3(cdiv(rows, wpb)), dim3(32 * wpb), smem, s, part, nslices, logits, logits_ld, rows, V,
+             bos, eos, inv_t, keys, step, cap, finished, comp, logp, len, tok_next, max_len, compact, lse_out, row_seq,
+             phase, sel, dump, dump_ld, mismatches, step_dev);
+  DCU_LAUNCHED();
 }
 
 __global__ void step_advance_k(int* step) {
@@ -939,7 +968,6 @@ __global__ void step_advance_k(int* step) {
 }
 void step_advance(cudaStream_t s, int* step_dev) {
   launch_pdl(step_advance_k, dim3(1), dim3(1), 0, s, step_dev);
-  DCU_LAUNCHED();
   DCU_LAUNCHED();
 }
 

@@ -2480,12 +2480,6 @@ int dashcu_policy_load(dashcu_policy* p, const char* path, int32_t with_optimize
 // ---------------------------------------------- fused reduce-scatter / update / all-gather
 namespace dashcu {
 namespace {
-int num_sms_host() {
-  int dev = 0, n = 0;
-  cudaGetDevice(&dev);
-  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = kNumSMs;
-  return n;
-}
 // Peer buffers for the fused step: each rank's IPC handles of its gradient, fp32 master,
 // bf16 working copy and flag words, all-gathered over the communicator, opened once.
 void fused_setup(dashcu_policy* p) {

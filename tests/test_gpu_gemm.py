@@ -164,3 +164,27 @@ def test_pair_residual_prefetch_epilogue(ctx, knob, shape, deep, pair):
     ref = ctx.selftest_gemm(A, True, B, True, M, N, K, bias=bias, epi=4, C_init=c0)
     assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
     assert np.array_equal(mid.view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("M", [1, 8, 32, 33, 64, 100])
+@pytest.mark.parametrize("NK", [(896, 4864), (1152, 896), (4864, 896)])
+def test_skinny_rows_equal_big_batch_rows(ctx, knob, M, NK):
+    """A decode step at a few rows (the skinny path: 32- / 64-row A boxes, deep rings)
+    computes every row bit-identically to the same row inside a 4096-row batch (other
+    tile shapes, CTA pairs) and to the full 128-row-box path: a sequence's tokens do not
+    depend on how many sequences share its decode batch."""
+    N, K = NK
+    rng = np.random.default_rng(M + N + K)
+    A = bf16_bits(rng.standard_normal((4096, K)).astype(np.float32) * 0.1)
+    B = bf16_bits(rng.standard_normal((N, K)).astype(np.float32) * 0.1)
+    bias = rng.standard_normal(N).astype(np.float32)
+    c0 = rng.standard_normal((4096, N)).astype(np.float32)
+    for epi in (1, 4):   # tanh (W1) and the residual-stream store (Wo / W2)
+        kw = dict(bias=bias, epi=epi)
+        big = ctx.selftest_gemm(A, True, B, True, 4096, N, K, C_init=c0 if epi == 4 else None, **kw)
+        small = ctx.selftest_gemm(A[:M], True, B, True, M, N, K, C_init=c0[:M] if epi == 4 else None, **kw)
+        assert np.array_equal(small.view(np.uint32), big[:M].view(np.uint32)), epi
+        knob("GEMM_SKINNY_AR", "0")
+        full = ctx.selftest_gemm(A[:M], True, B, True, M, N, K, C_init=c0[:M] if epi == 4 else None, **kw)
+        knob("GEMM_SKINNY_AR", None)
+        assert np.array_equal(small.view(np.uint32), full.view(np.uint32)), epi

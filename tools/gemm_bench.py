@@ -24,6 +24,11 @@ SHAPES = {
     # tanh epilogue (W1 forward, decode and training)
     "dec_w1_tanh": (4096, 4864, 896, 1, 1, 1), "fwd_w1_tanh": (36864, 4864, 896, 1, 1, 1),
     "wgrad_wo": (896, 896, 36864, 0, 0, 3), "wgrad_qkv": (1152, 896, 36864, 0, 0, 3),
+    # small-batch decode (the GRPO-arm micro-batch of 32 sequences, and 64)
+    "s32_qkv": (32, 1152, 896, 1, 1, 0), "s32_wo_res": (32, 896, 896, 1, 1, 4),
+    "s32_w1_tanh": (32, 4864, 896, 1, 1, 1), "s32_w2_res": (32, 896, 4864, 1, 1, 4),
+    "s64_qkv": (64, 1152, 896, 1, 1, 0), "s64_w2_res": (64, 896, 4864, 1, 1, 4),
+    "s128_w2_res": (128, 896, 4864, 1, 1, 4),
 }
 
 

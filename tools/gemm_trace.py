@@ -1,0 +1,27 @@
+"""Per-k-block clocks of CTA 0 in one GEMM launch (experiment build with
+-DDASHCU_GEMM_TRACE, loaded through DASHCU_LIB_PATH): producer issue, MMA wait start,
+MMA data ready, relative to the first producer issue."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2505_17218_b200 as D  # noqa: E402
+from gemm_bench import SHAPES  # noqa: E402
+
+L = D.lib()
+L.dashcu_selftest_gemm_timed.argtypes = [C.c_void_p] + [C.c_int] * 7 + [C.POINTER(C.c_double)]
+ctx = D.Context(0)
+for n in sys.argv[1:]:
+    M, N, K, ak, bk, epi = SHAPES[n]
+    ms = C.c_double(0)
+    assert L.dashcu_selftest_gemm_timed(ctx.h, M, N, K, ak, bk, epi, 3, C.byref(ms)) == 0
+    tr = np.zeros((3, 512), dtype=np.int64)
+    assert L.dashcu_debug_gemm_trace(tr.ctypes.data_as(C.c_void_p)) == 0
+    nkb = (K + 63) // 64
+    t = tr[:, :nkb] - tr[0, 0]
+    print(n, f"{ms.value * 1e3:.2f} us/launch; k-block: producer issue / mma wait / data ready (cycles)")
+    for k in list(range(0, min(nkb, 40))) + list(range(max(40, nkb - 5), nkb)):
+        print(f"  {k:3d} {t[0, k]:7d} {t[1, k]:7d} {t[2, k]:7d}")
