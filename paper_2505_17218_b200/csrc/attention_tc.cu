@@ -41,12 +41,14 @@ constexpr bool kStreamKV = true;
 constexpr bool kStreamKV = false;
 #endif
 
+// append: the warp first stores its (row, kv head)'s new K / V row (qkv columns qd.. and
+// qd + kvd..) into completion slot n_comp - 1, the separate kv_append kernel's work.
 template <int HD>
 __global__ void __launch_bounds__(DecCfg<HD>::NW * 32)
     attn_decode_tc_k(const bf16* __restrict__ qkv, const bf16* __restrict__ kp, const bf16* __restrict__ vp,
-                     const bf16* __restrict__ kc, const bf16* __restrict__ vc, const int32_t* __restrict__ prompt_len,
-                     int S, int G, int pmax, int n_comp, DecodeRows dr, int nh, int nkv, bf16* __restrict__ ctx,
-                     float scale_log2) {
+                     bf16* kc, bf16* vc, const int32_t* __restrict__ prompt_len, int S, int G, int pmax,
+                     int n_comp, DecodeRows dr, int nh, int nkv, bf16* __restrict__ ctx, float scale_log2,
+                     bool append) {
   using Cf = DecCfg<HD>;
   constexpr int KC = Cf::KC, ST = Cf::ST, UNITS = Cf::UNITS;
   pdl_wait();
@@ -69,6 +71,21 @@ __global__ void __launch_bounds__(DecCfg<HD>::NW * 32)
       shfl_pages && lane < dr.max_pages ? __ldg(dr.ptab + static_cast<int64_t>(sq) * dr.max_pages + lane) : 0;
   uint8_t* wsm = smem + warp * Cf::WARP_BYTES;
   const uint32_t wsm_a = smem_addr(wsm);
+  if (append) {  // HD / 2 words of K and of V, one or two per lane
+    const int slot = n_comp - 1;
+    const int page = shfl_pages ? __shfl_sync(0xffffffffu, lane_page, (slot / kPage) & 31)
+                                : __ldg(dr.ptab + static_cast<int64_t>(sq) * dr.max_pages + slot / kPage);
+    const int64_t dst = ((static_cast<int64_t>(page) * nkv + kvh) * kPage + slot % kPage) * HD;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(qkv + static_cast<int64_t>(s) * qkvd + qd +
+                                                            static_cast<int64_t>(kvh) * HD);
+#pragma unroll
+    for (int w = lane; w < HD / 2; w += 32) {
+      reinterpret_cast<uint32_t*>(kc + dst)[w] = src[w];
+      reinterpret_cast<uint32_t*>(vc + dst)[w] = src[w + kvd / 2];
+    }
+    __threadfence_block();  // the slot is read back below through cp.async by other lanes
+    __syncwarp();
+  }
 
   // Query tile: rows r < grp are the heads kvh*grp + r.
   const int g = lane >> 2, t = lane & 3;
@@ -242,9 +259,9 @@ __global__ void __launch_bounds__(DecCfg<HD>::NW * 32)
 }
 
 template <int HD>
-void launch_decode(cudaStream_t s, const bf16* qkv, const bf16* kp, const bf16* vp, const bf16* kc, const bf16* vc,
+void launch_decode(cudaStream_t s, const bf16* qkv, const bf16* kp, const bf16* vp, bf16* kc, bf16* vc,
                    const int32_t* plen, int rows, int G, int pmax, int n_comp, const DecodeRows& dr, int nh, int nkv,
-                   bf16* ctx) {
+                   bf16* ctx, bool append) {
   using Cf = DecCfg<HD>;
   static bool attr = false;
   if (!attr) {
@@ -253,8 +270,8 @@ void launch_decode(cudaStream_t s, const bf16* qkv, const bf16* kp, const bf16* 
   }
   const int items = rows * nkv;
   const float scale_log2 = kLog2e / sqrtf(static_cast<float>(HD));
-  launch_pdl(attn_decode_tc_k<HD>, dim3((items + Cf::NW - 1) / Cf::NW), dim3(Cf::NW * 32), Cf::SMEM, s, qkv, kp, vp, kc,
-             vc, plen, rows, G, pmax, n_comp, dr, nh, nkv, ctx, scale_log2);
+  launch_pdl(attn_decode_tc_k<HD>, dim3((items + Cf::NW - 1) / Cf::NW), dim3(Cf::NW * 32), Cf::SMEM, s, qkv, kp,
+             vp, kc, vc, plen, rows, G, pmax, n_comp, dr, nh, nkv, ctx, scale_log2, append);
   DCU_LAUNCHED();
 }
 
@@ -694,13 +711,15 @@ bool attn_bwd_tc(cudaStream_t s, const bf16* qkv, const bf16* ctx, const bf16* d
   return true;
 }
 
-bool attn_decode_tc(cudaStream_t s, const bf16* qkv, const bf16* kp, const bf16* vp, const bf16* kc, const bf16* vc,
+bool attn_decode_tc_supported(int nh, int nkv, int hd) { return nh / nkv <= 16 && (hd == 64 || hd == 128); }
+
+bool attn_decode_tc(cudaStream_t s, const bf16* qkv, const bf16* kp, const bf16* vp, bf16* kc, bf16* vc,
                     const int32_t* plen, int rows, int G, int pmax, int n_comp, const DecodeRows& dr, int nh, int nkv,
-                    int hd, bf16* ctx, double alg_bytes) {
-  if (nh / nkv > 16 || (hd != 64 && hd != 128)) return false;
+                    int hd, bf16* ctx, double alg_bytes, bool append) {
+  if (!attn_decode_tc_supported(nh, nkv, hd)) return false;
   ProfScope ps(PROF_ATTN_DECODE, s, 0, alg_bytes);
-  if (hd == 64) launch_decode<64>(s, qkv, kp, vp, kc, vc, plen, rows, G, pmax, n_comp, dr, nh, nkv, ctx);
-  else launch_decode<128>(s, qkv, kp, vp, kc, vc, plen, rows, G, pmax, n_comp, dr, nh, nkv, ctx);
+  if (hd == 64) launch_decode<64>(s, qkv, kp, vp, kc, vc, plen, rows, G, pmax, n_comp, dr, nh, nkv, ctx, append);
+  else launch_decode<128>(s, qkv, kp, vp, kc, vc, plen, rows, G, pmax, n_comp, dr, nh, nkv, ctx, append);
   return true;
 }
 

@@ -36,6 +36,11 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle row of bf16
+// k-blocks per ring stage of the large-tile kernels (A/B builds; the skinny kernels use 4)
+#ifndef DASHCU_KSUB_BIG
+#define DASHCU_KSUB_BIG 1
+#endif
+constexpr int kKsubBig = DASHCU_KSUB_BIG;
 
 // Producer / MMA-issuer waits on the operand ring. Default: tight try_wait loop; with
 // -DDASHCU_GEMM_SLEEP_WAITS the suspend-hint form (frees issue slots for the epilogue
@@ -673,7 +678,11 @@ __device__ __forceinline__ void epilogue_slice(const GemmShape& g, const Epi& e,
 __device__ long long g_trace[3][512];
 #define GEMM_TRACE(i, k) \
   if (blockIdx.x == 0 && (k) < 512) g_trace[i][k] = clock64()
+// phase marks of CTA 0 (thread-0 / warp-leader clocks) in g_trace[2][500 + ...]
+#define GEMM_MARK(k) \
+  if (blockIdx.x == 0) g_trace[2][500 + (k)] = clock64()
 #else
+#define GEMM_MARK(k)
 #define GEMM_TRACE(i, k)
 #endif
 
@@ -695,6 +704,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB>::THREA
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + EPW);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) GEMM_MARK(0);
   const int nkb = (g.K + BK - 1) / BK;
   const int tiles_m = (g.M + BM - 1) / BM, tiles_n = MODE == 4 ? BM / 8 : (g.N + BN - 1) / BN;
   const int ntile = tiles_m * tiles_n;
@@ -726,7 +736,9 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB>::THREA
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) GEMM_MARK(1);
   pdl_wait();  // set-up above overlapped the previous kernel; its outputs are visible now
+  if (threadIdx.x == 0) GEMM_MARK(2);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -810,6 +822,10 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB>::THREA
         }
         umma_commit(&tfull[acc]);
       }
+      // every MMA is issued: the next kernel may launch now (its CTAs land on the SMs this
+      // grid leaves idle and set up while our epilogues drain; its pdl_wait() still waits
+      // for this whole grid)
+      pdl_trigger();
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
@@ -833,6 +849,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB>::THREA
       const int acc = i & 1;
       const uint32_t aph = (i >> 1) & 1;
       mbar_wait_sleep(&tfull[acc], aph);
+      if (threadIdx.x == 128 && i == 0) GEMM_MARK(3);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       uint32_t* flag = S > 1 ? e.split_flags + t * EPW + ew : nullptr;
       if (flag && sp > 0) split_wait(flag, sp, lane);  // K slices reduce into C in slice order
@@ -855,7 +872,9 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB>::THREA
       mbar_arrive(&tempty[acc]);
       if (flag) split_signal(flag, lane);
     }
+    if (threadIdx.x == 128) GEMM_MARK(4);
     stage_drain(lane);  // bulk stores complete before the CTA's shared memory goes away
+    if (threadIdx.x == 128) GEMM_MARK(5);
   }
   pdl_trigger();  // this CTA's work is done: the next kernel may be scheduled
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -946,15 +965,16 @@ void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const 
   DCU_LAUNCHED();
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES_KB, int KSUB = 1>
 void dispatch_majors(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& om,
                      const GemmShape& g, const Epi& e) {
   const SampleArgs none;
+  constexpr int STAGES = STAGES_KB / KSUB < 2 ? 2 : STAGES_KB / KSUB;
   // 8 epilogue warps (two per SM sub-partition, each owning half of the tile's columns)
-  if (g.a_kmajor && g.b_kmajor) launch<BN, STAGES, true, true, 8, 0>(s, ma, mb, om, g, e, none);
-  else if (g.a_kmajor) launch<BN, STAGES, true, false, 8, 0>(s, ma, mb, om, g, e, none);
-  else if (g.b_kmajor) launch<BN, STAGES, false, true, 8, 0>(s, ma, mb, om, g, e, none);
-  else launch<BN, STAGES, false, false, 8, 0>(s, ma, mb, om, g, e, none);
+  if (g.a_kmajor && g.b_kmajor) launch<BN, STAGES, true, true, 8, 0, BM, KSUB>(s, ma, mb, om, g, e, none);
+  else if (g.a_kmajor) launch<BN, STAGES, true, false, 8, 0, BM, KSUB>(s, ma, mb, om, g, e, none);
+  else if (g.b_kmajor) launch<BN, STAGES, false, true, 8, 0, BM, KSUB>(s, ma, mb, om, g, e, none);
+  else launch<BN, STAGES, false, false, 8, 0, BM, KSUB>(s, ma, mb, om, g, e, none);
 }
 
 }  // namespace
@@ -1033,7 +1053,7 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
-template <int BN, int STAGES, bool AK, bool BKM, int EPW, bool DB = false>
+template <int BN, int STAGES, bool AK, bool BKM, int EPW, bool DB = false, int KSUB = kKsubBig>
 struct Cfg2 {
   static constexpr int BNH = BN / 2;  // B rows staged per CTA
   // BN = 224 (N = 896 = 4 x 224 without the half-empty fourth 256 tile): the B stage keeps
@@ -1043,8 +1063,9 @@ struct Cfg2 {
   static constexpr int TMEM_COLS = BN == 224 ? 512 : 2 * BN;  // alloc: power of two
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = BNS * BK * 2;
-  static constexpr int B_LOAD = (BKM ? BNH : BNS) * BK * 2;  // bytes the B loads of a stage deliver
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int B_LOAD = (BKM ? BNH : BNS) * BK * 2;  // bytes the B loads of a k-block deliver
+  static constexpr int KB_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGE_BYTES = KSUB * KB_BYTES;
   static constexpr int STG_OFF = STAGES * STAGE_BYTES;
   static constexpr int STG_WARP = DB ? 10240 : kStageBytes;  // DB: 2 residual/fp32 + 1 bf16 buffer
   static constexpr int BAR_OFF = STG_OFF + EPW * STG_WARP;
@@ -1060,6 +1081,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                     const __grid_constant__ OutMaps om, GemmShape g, Epi e) {
   using C = Cfg2<BN, STAGES, AK, BKM, EPW, DB>;
+  constexpr int KSUB = kKsubBig;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
@@ -1070,6 +1092,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 2 * EPW);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) GEMM_MARK(0);
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
@@ -1105,7 +1128,9 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
   cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive / TMA
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) GEMM_MARK(1);
   pdl_wait();  // set-up above overlapped the previous kernel; its outputs are visible now
+  if (threadIdx.x == 0) GEMM_MARK(2);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1114,14 +1139,18 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
         const int t = w / S, kb_lo = (w % S) * kps, kb_hi = min(nkb, kb_lo + kps);
         const int m0 = tile_m(g, t, tiles_m, tiles_n) * 256 + static_cast<int>(rank) * 128;
         const int n0 = tile_n(g, t, tiles_m, tiles_n) * BN + static_cast<int>(rank) * C::BNH;
-        for (int kb = kb_lo; kb < kb_hi; ++kb, ++kb_all) {
+        for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += KSUB, ++kb_all) {
           const int s = kb_all % STAGES;
           const uint32_t ph = (kb_all / STAGES) & 1;
           mbar_wait_pipe(&empty[s], ph ^ 1);
-          uint8_t* sa_ = smem + s * C::STAGE_BYTES;
-          uint8_t* sb_ = sa_ + C::A_BYTES;
+          GEMM_TRACE(0, kb_all);
+          const int cnt = min(KSUB, kb_hi - kb0);
           const uint32_t lb = leader_addr(&full[s]);
-          if (leader) mbar_expect_tx(&full[s], 2 * (C::A_BYTES + C::B_LOAD));
+          if (leader) mbar_expect_tx(&full[s], 2 * cnt * (C::A_BYTES + C::B_LOAD));
+          for (int j = 0; j < cnt; ++j) {
+          const int kb = kb0 + j;
+          uint8_t* sa_ = smem + s * C::STAGE_BYTES + j * C::KB_BYTES;
+          uint8_t* sb_ = sa_ + C::A_BYTES;
           const int k0 = kb * BK;
           if (AK) {
             tma_load_2d_pair(sa_, &mapA, lb, k0, m0);
@@ -1134,6 +1163,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
           } else {
 #pragma unroll
             for (int j = 0; j < C::BNS / 64; ++j) tma_load_2d_pair(sb_ + j * 64 * BK * 2, &mapB, lb, n0 + 64 * j, k0);
+          }
           }
         }
       }
@@ -1148,18 +1178,25 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
         mbar_wait_cluster(&tempty[acc], aph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * BN;
-        for (int kb = kb_lo; kb < kb_hi; ++kb, ++kb_all) {
+        for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += KSUB, ++kb_all) {
           const int s = kb_all % STAGES;
           const uint32_t ph = (kb_all / STAGES) & 1;
+          GEMM_TRACE(1, kb_all);
           mbar_wait_pipe(&full[s], ph);
+          GEMM_TRACE(2, kb_all);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t sa_ = smem_u32(smem + s * C::STAGE_BYTES);
+          const int cnt = min(KSUB, kb_hi - kb0);
+#pragma unroll 1
+          for (int j = 0; j < cnt; ++j) {
+          const int kb = kb0 + j;
+          const uint32_t sa_ = smem_u32(smem + s * C::STAGE_BYTES + j * C::KB_BYTES);
           const uint32_t sb_ = sa_ + C::A_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t da = AK ? smem_desc(sa_ + k * 32, 16, 1024) : smem_desc(sa_ + k * 2048, 64 * BK * 2, 1024);
             const uint64_t db = BKM ? smem_desc(sb_ + k * 32, 16, 1024) : smem_desc(sb_ + k * 2048, 64 * BK * 2, 1024);
             umma_bf16_pair(d, da, db, C::IDESC, (kb > kb_lo || k > 0) ? 1u : 0u);
+          }
           }
           umma_commit_pair(&empty[s]);
         }
@@ -1189,6 +1226,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
       const int acc = i & 1;
       const uint32_t aph = (i >> 1) & 1;
       mbar_wait_sleep(&tfull[acc], aph);
+      if (threadIdx.x == 128 && i == 0) GEMM_MARK(3);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       uint32_t* flag = S > 1 ? e.split_flags + (t * 2 + static_cast<int>(rank)) * EPW + ew : nullptr;
       if (flag && sp > 0) split_wait(flag, sp, lane);  // K slices reduce into C in slice order
@@ -1206,7 +1244,9 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
                    : "memory");
       if (flag) split_signal(flag, lane);
     }
+    if (threadIdx.x == 128) GEMM_MARK(4);
     stage_drain(lane);
+    if (threadIdx.x == 128) GEMM_MARK(5);
   }
   pdl_trigger();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1219,8 +1259,11 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
 template <int BN, int STAGES, bool AK, bool BKM, bool DB = false, int EPW = 8>
 void launch2(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& om, const GemmShape& g,
              const Epi& e) {
-  using C = Cfg2<BN, STAGES, AK, BKM, EPW, DB>;
-  auto k = gemm_tc2_kernel<BN, STAGES, AK, BKM, EPW, DB>;
+  // STAGES counts k-blocks; the ring holds STAGES / KSUB stages of KSUB k-blocks
+  constexpr int NST = STAGES / kKsubBig < 2 ? 2 : STAGES / kKsubBig;
+  using C = Cfg2<BN, NST, AK, BKM, EPW, DB>;
+  static_assert(C::SMEM <= 232448, "shared memory");
+  auto k = gemm_tc2_kernel<BN, NST, AK, BKM, EPW, DB>;
   static bool attr = false;
   if (!attr) {
     DCU_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -1434,8 +1477,8 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
     et.split_flags = split_flag_buffer(tiles * 8);
     DCU_CHECK(cudaMemsetAsync(et.split_flags, 0, sizeof(uint32_t) * tiles * 8, s));
   }
-  if (BN == 256) dispatch_majors<256, 4>(s, ma, mb, om, g, et);  // 4 x 48 KB stages
-  else dispatch_majors<128, 6>(s, ma, mb, om, g, et);             // 6 x 32 KB stages
+  if (BN == 256) dispatch_majors<256, 4, kKsubBig>(s, ma, mb, om, g, et);  // 4 x 48 KB stages
+  else dispatch_majors<128, 6, kKsubBig>(s, ma, mb, om, g, et);             // 6 x 32 KB stages
   return true;
 }
 

@@ -149,9 +149,12 @@ void attn_decode(cudaStream_t s, const T* qkv, const T* kp, const T* vp, const T
                  int nh, int nkv, int hd, T* ctx, double alg_bytes = 0);
 // Tensor-core decode attention (bf16; head_dim 64/128, <= 16 query heads per KV head).
 // Returns false when the geometry is not covered (caller uses attn_decode).
-bool attn_decode_tc(cudaStream_t s, const bf16* qkv, const bf16* kp, const bf16* vp, const bf16* kc, const bf16* vc,
+// append: the kernel also stores each row's new K / V (qkv) into completion slot
+// n_comp - 1 (what kv_append does), so the decode step needs no separate append launch
+bool attn_decode_tc_supported(int nh, int nkv, int hd);
+bool attn_decode_tc(cudaStream_t s, const bf16* qkv, const bf16* kp, const bf16* vp, bf16* kc, bf16* vc,
                     const int32_t* prompt_len, int rows, int G, int pmax, int n_comp, const DecodeRows& dr, int nh,
-                    int nkv, int hd, bf16* ctx, double alg_bytes);
+                    int nkv, int hd, bf16* ctx, double alg_bytes, bool append);
 // One sampling step over fp32 logits rows [rows x V] (policy.cpp:399-426 with the
 // inverse-CDF contract of rule.cuh): per-slice partials, then sample_scan.
 // part: scratch of rows * ceil(V/32) * 4 floats.

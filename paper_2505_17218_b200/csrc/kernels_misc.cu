@@ -5,6 +5,7 @@
 #include <cfloat>
 
 #include "kernels.cuh"
+#include "tc5.cuh"
 #include "rule.cuh"
 
 namespace dashcu {
@@ -395,16 +396,34 @@ __global__ void __launch_bounds__(256) sample_scan_k(const float* __restrict__ p
   }
   // records {m, Z, m1, Z1}; at T = 1 the fused epilogue stores only {m, Z} (m1 = m, Z1 = Z)
   extern __shared__ float4 s_rec[];  // [warps per block][nslices records]
+  __shared__ uint64_t s_bar[8];
   const int recf = compact ? 2 : 4;  // floats per record
   float* srow = reinterpret_cast<float*>(s_rec) + static_cast<int64_t>(threadIdx.x >> 5) * nslices * recf;
   {
     const float* grow = part + static_cast<int64_t>(row) * nslices * recf;
-    const int n2 = nslices * recf / 2;  // float2 units (rows are 8-byte aligned)
-    const float2* g2 = reinterpret_cast<const float2*>(grow);
-    float2* s2 = reinterpret_cast<float2*>(srow);
+    const uint32_t bytes = static_cast<uint32_t>(nslices) * recf * 4;
+    if (((reinterpret_cast<uintptr_t>(grow) | bytes) & 15) == 0) {  // one bulk (TMA) copy per row
+      uint64_t* bar = &s_bar[threadIdx.x >> 5];
+      if (lane == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(bar, bytes);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(srow)),
+            "l"(grow), "r"(bytes), "r"(smem_u32(bar))
+            : "memory");
+      }
+      __syncwarp();
+      mbar_wait(bar, 0);
+    } else {
+      const int n2 = nslices * recf / 2;  // float2 units (rows are 8-byte aligned)
+      const float2* g2 = reinterpret_cast<const float2*>(grow);
+      float2* s2 = reinterpret_cast<float2*>(srow);
 #pragma unroll 8
-    for (int i = lane; i < n2; i += 32) s2[i] = __ldg(g2 + i);
-    __syncwarp();
+      for (int i = lane; i < n2; i += 32) s2[i] = __ldg(g2 + i);
+      __syncwarp();
+    }
   }
   const float4* P4 = reinterpret_cast<const float4*>(srow);
   const float2* P2 = reinterpret_cast<const float2*>(srow);
@@ -944,13 +963,12 @@ void sample_scan(cudaStream_t s, const float* part, int nslices, const float* lo
                  uint8_t* finished, int32_t* comp, float* logp, int32_t* len, int32_t* tok_next, int max_len,
                  bool compact, float* lse_out, const int32_t* row_seq, int phase, SliceSel* sel, const float* dump,
                  int64_t dump_ld, int* mismatches, const int* step_dev) {
-  // phases 0 / 1 stage each row's records in shared memory: warps per block by the row size
-  // (one warp per CTA for small batches, so the copies spread over many SMs)
+  // phases 0 / 1 stage each row's records in shared memory (one bulk copy per row): one
+  // warp per CTA, as many CTAs per SM as the row windows fit (5 at V = 151,936, T = 1)
   const size_t row_bytes = static_cast<size_t>(nslices) * (compact ? 8 : 16);
   if (phase != 2 && row_bytes > 200 * 1024) throw Error(1, "sample_scan: vocabulary too large for the staged walk");
-  int wpb = 8;
-  if (phase != 2) wpb = rows <= 2 * num_sms_host() ? 1 : std::max(1, std::min(8, static_cast<int>(200 * 1024 / row_bytes)));
-  const size_t smem = phase == 2 ? 0 : row_bytes * wpb;
+  const int wpb = phase == 2 ? 8 : 1;
+  const size_t smem = phase == 2 ? 0 : row_bytes;
   static size_t smem_set = 0;
   if (smem > 48 * 1024 && smem > smem_set) {
     DCU_CHECK(cudaFuncSetAttribute(sample_scan_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 16));

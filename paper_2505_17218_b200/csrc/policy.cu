@@ -1120,6 +1120,7 @@ struct Engine {
     cudaGraphExec_t gexec = nullptr;
     int graph_rows = -1;
     bool step_set = false;
+    const bool fused_append = sizeof(T) == 2 && attn_decode_tc_supported(g.nh, g.nkv, g.hd);
     auto decode_step = [&](int j, const int* sdev) {
       const DecodeRows dr{d_rows, d_ptab, maxp, sdev};
       embed_decode<T>(st, W(L.tok), W(L.pos), d_tok, d_plen, j, R, g.d, x32, xT, d_rows, sdev);
@@ -1128,14 +1129,15 @@ struct Engine {
         T* kc_l = kc + kvc * l;
         T* vc_l = vc + kvc * l;
         mm(R, g.qkvd, g.d, xT, g.d, true, W(b + L.wq), g.d, true, store(nullptr, 0, qkv, g.qkvd));
-        kv_append<T>(st, qkv, R, g.qd, g.kvd, g.nkv, g.hd, j - 1, dr, kc_l, vc_l);
+        // the bf16 tensor-core decode attention appends the new K / V itself
+        if (!fused_append) kv_append<T>(st, qkv, R, g.qd, g.kvd, g.nkv, g.hd, j - 1, dr, kc_l, vc_l);
         // algorithmic bytes: every (sequence, kv head) reads its K and V rows once (a group's
         // prompt KV once per group)
         const double kv_bytes = (sum_m / G * R / S + static_cast<double>(R) * j) * g.kvd * 2.0 * sizeof(T);
         bool done = false;
         if constexpr (sizeof(T) == 2)
           done = attn_decode_tc(st, qkv, kp + kvp * l, vp + kvp * l, kc_l, vc_l, d_plen, R, G, pmax, j, dr, g.nh,
-                                g.nkv, g.hd, ctx, kv_bytes);
+                                g.nkv, g.hd, ctx, kv_bytes, fused_append);
         if (!done)
           attn_decode<T>(st, qkv, kp + kvp * l, vp + kvp * l, kc_l, vc_l, d_plen, R, G, pmax, j, cslots, dr, g.nh,
                          g.nkv, g.hd, ctx, kv_bytes);

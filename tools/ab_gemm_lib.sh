@@ -1,0 +1,9 @@
+S="dec_qkv dec_w1_tanh dec_w2_res dec_wo_res fwd_w1_tanh fwd_w2_res fwd_wo_res dgrad_w1_res dgrad_qkv_res wgrad_w1 wgrad_lm dgrad_lm wgrad_wo dec_lm"
+P='import json,sys
+for l in sys.stdin:
+    d=json.loads(l); print(sys.argv[1], d["shape"], round(d["ms"]*1e3,1), round(d["tflops"]))'
+for i in 1 2; do
+python tools/gemm_bench.py $S | python3 -c "$P" NEW
+DASHCU_LIB_PATH=$PWD/paper_2505_17218_b200/lib/libdashcu_alt.so python tools/gemm_bench.py $S | python3 -c "$P" ALT
+done
+DASHCU_LIB_PATH=$PWD/paper_2505_17218_b200/lib/libdashcu_alt.so python -m pytest tests/test_gpu_gemm.py -q -x 2>&1 | tail -2

@@ -20,8 +20,13 @@ for n in sys.argv[1:]:
     assert L.dashcu_selftest_gemm_timed(ctx.h, M, N, K, ak, bk, epi, 3, C.byref(ms)) == 0
     tr = np.zeros((3, 512), dtype=np.int64)
     assert L.dashcu_debug_gemm_trace(tr.ctypes.data_as(C.c_void_p)) == 0
-    nkb = (K + 63) // 64
+    nkb = ((K + 63) // 64 + 3) // 4 if M <= 64 else (K + 63) // 64  # ring stages (4 k-blocks at M <= 64)
+    nkb = min(nkb, 500)
     t = tr[:, :nkb] - tr[0, 0]
     print(n, f"{ms.value * 1e3:.2f} us/launch; k-block: producer issue / mma wait / data ready (cycles)")
-    for k in list(range(0, min(nkb, 40))) + list(range(max(40, nkb - 5), nkb)):
+    for k in list(range(0, min(nkb, 12))) + list(range(max(12, nkb - 3), nkb)):
         print(f"  {k:3d} {t[0, k]:7d} {t[1, k]:7d} {t[2, k]:7d}")
+    marks = tr[2, 500:506] - tr[2, 500]
+    print("  marks (cycles from kernel entry): setup done %d, pdl_wait done %d, first accumulator %d, "
+          "epilogue done %d, stores drained %d; first producer issue %d"
+          % (marks[1], marks[2], marks[3], marks[4], marks[5], tr[0, 0] - tr[2, 500]))
