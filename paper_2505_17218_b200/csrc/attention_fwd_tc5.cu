@@ -4,11 +4,16 @@
 // One CTA owns 128 queries of one sequence for every query head of a KV group (heads run
 // back to back through one pipeline) and walks the causal key tiles (128 keys each) with an
 // online softmax:
-//   S_j = Q K_j^T          M128 N128 K=hd   A = Q (K-major)   B = K_j (K-major)   -> TMEM S[j&1]
-//   softmax warps: m_j = max(m_{j-1}, rowmax(S_j)/sqrt(d)), P_j = exp(S_j/sqrt(d) - m_j) (bf16, smem)
-//   O_j = P_j V_j          M128 N=hd K128   A = P_j (K-major) B = V_j (MN-major)  -> TMEM O[j&1]
-//   registers: acc = acc * 2^(m_{j-1} - m_j) + O_j,  l likewise; out = acc / l, LSE = m + log l.
-// S and O are double-buffered in TMEM so the MMA of S_{j+1} and of O_j overlap the softmax.
+//   S_j = Q K_j^T          M128 N128 K=hd   A = Q (K-major, smem)  B = K_j (K-major)   -> TMEM S[j&1]
+//   softmax warps: m = running row max of S/sqrt(d) (log2 domain), P_j = exp2(S_j/sqrt(d) - m)
+//                  (bf16, written into TMEM with tcgen05.st)
+//   O += P_j V_j           M128 N=hd K128   A = P_j (TMEM)          B = V_j (MN-major)  -> TMEM O
+//   out = O / l, LSE = m + log l (l = sum of the bf16-rounded P the MMA consumed).
+// Lazy rescaling: the max the exponentials use only moves when a row's true running max
+// exceeds it by more than kRescale (log2 units); then that row's O (TMEM) and l are scaled
+// by 2^(m_old - m_new) before the next PV. Otherwise P <= 2^kRescale, exact in the
+// normalised result. No per-tile O round trip through registers, and P never touches
+// shared memory. S is double-buffered in TMEM so the MMA of S_{j+1} overlaps the softmax.
 // Tiles of hd 128 are two 64-column swizzle atoms side by side (two TMA boxes); with 32 KB
 // tiles the shared-memory budget allows one Q stage and a 2-deep K/V ring.
 // Warp roles: 0 TMA producer (Q once, K/V kST-stage ring), 1 MMA issuer, 2 TMEM allocator,
@@ -62,14 +67,36 @@ struct FLay {
   static constexpr int kQS = HD == 64 ? 2 : 1;  // Q stages
   static constexpr int kST = HD == 64 ? 4 : 2;  // K/V pipeline depth (loads run kST - 1 key tiles ahead)
   static constexpr int Q = 0, K = kQS * kTile, V = K + kST * kTile;
-  static constexpr int P = V + kST * kTile;  // P [128 q x 128 keys] bf16: two 64-key swizzle atoms
-  static constexpr int XMAX = P + 2 * kAtom;  // row-max exchange [2][2][128] + row sums [2][128]
+  static constexpr int XMAX = V + kST * kTile;  // row-max exchange [2][2][128] + row sums [2][128]
   static constexpr int BAR = XMAX + 4096;
   static constexpr int BYTES = BAR + 256 + 1024;
   static_assert(BYTES <= 232448, "exceeds the 227 KB of opt-in shared memory per CTA");
-  // TMEM columns: S double buffer, then the O double buffer (HD columns each)
-  static constexpr uint32_t TS0 = 0, TS1 = 128, TO0 = 256, TO1 = 256 + HD;
+  // TMEM columns: S double buffer, O (HD columns), P (128 bf16 keys = 64 columns)
+  static constexpr uint32_t TS0 = 0, TS1 = 128, TO = 256, TP = 256 + HD;
 };
+
+constexpr float kRescale = 8.f;  // lazy-rescale threshold (log2 units): P <= 256
+
+// O += P V with A = P from TMEM (a_tmem: lane 0, first column of this K step)
+__device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t a_tmem, uint64_t db, uint32_t idesc,
+                                             uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(a_tmem), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 constexpr uint32_t idesc(int n, bool a_mn, bool b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
@@ -94,7 +121,7 @@ __global__ void __launch_bounds__(384, 1)
                    bf16* __restrict__ ctx_lo) {
   using FLay = dashcu::FLay<HD>;
   constexpr int kHD = HD, kTile = FLay::kTile, kST = FLay::kST, kQS = FLay::kQS;
-  constexpr uint32_t kTS0 = FLay::TS0, kTS1 = FLay::TS1, kTO0 = FLay::TO0, kTO1 = FLay::TO1;
+  constexpr uint32_t kTS0 = FLay::TS0, kTS1 = FLay::TS1, kTO = FLay::TO, kTP = FLay::TP;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // grid (sequence x KV head, query tile), the longest (last) query tiles launched first; the
@@ -119,7 +146,7 @@ __global__ void __launch_bounds__(384, 1)
 
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FLay::BAR);
   uint64_t *qfull = bar /*[2]*/, *qempty = bar + 2 /*[2]*/, *sfull = bar + 4 /*[2]*/, *sfree = bar + 6 /*[2]*/,
-           *pready = bar + 8, *ofull = bar + 9 /*[2]*/, *ofree = bar + 11 /*[2]*/, *kvfull = bar + 13 /*[kST]*/,
+           *pready = bar + 8, *ofull = bar + 9 /*[1]*/, *kvfull = bar + 13 /*[kST]*/,
            *kvempty = bar + 13 + kST /*[kST]*/;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13 + 2 * kST);
 
@@ -134,7 +161,6 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&sfull[i], 1);
       mbar_init(&sfree[i], 256);
       mbar_init(&ofull[i], 1);
-      mbar_init(&ofree[i], 256);
     }
     mbar_init(pready, 256);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -149,8 +175,7 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  const uint32_t sQ = smem_u32(smem + FLay::Q), sK = smem_u32(smem + FLay::K), sV = smem_u32(smem + FLay::V),
-                 sP = smem_u32(smem + FLay::P);
+  const uint32_t sQ = smem_u32(smem + FLay::Q), sK = smem_u32(smem + FLay::K), sV = smem_u32(smem + FLay::V);
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------------------------------------------------------- TMA
@@ -196,61 +221,37 @@ __global__ void __launch_bounds__(384, 1)
       };
       issue_s(0);
       for (int t = 0; t < ntiles; ++t) {
-        const int sb = t & 1, st = t % kST;
+        const int st = t % kST, j = t % nkt;
         if (t + 1 < ntiles) issue_s(t + 1);
         TRF(t, 0);
+        // P_t is in TMEM and every row of O is rescaled; the softmax waited for PV(t-1) (and
+        // at a head's first tile it has read the previous head's O) before arriving
         mbar_wait_sleep(pready, t & 1);
         TRF(t, 1);
-        if (t >= 2) mbar_wait_sleep(&ofree[sb], ((t >> 1) - 1) & 1);  // O_{t-2} read out
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t v = sV + st * kTile;
 #pragma unroll
-        for (int kk = 0; kk < kKeys / 16; ++kk)
-          umma_bf16(tmem + (sb ? kTO1 : kTO0), smem_desc(sP + (kk >> 2) * kAtom + (kk & 3) * 32, 16, 1024),
-                    smem_desc(v + kk * 2048, kAtom, 1024), I_O, kk > 0);  // V atoms kAtom apart along hd
+        for (int kk = 0; kk < kKeys / 16; ++kk)  // 16 keys = 8 TMEM columns of P per K step
+          umma_bf16_ts(tmem + kTO, tmem + kTP + kk * 8, smem_desc(v + kk * 2048, kAtom, 1024), I_O,
+                       (j > 0 || kk > 0) ? 1u : 0u);  // V atoms kAtom apart along hd
         umma_commit(&kvempty[st]);
-        umma_commit(&ofull[sb]);
+        umma_commit(&ofull[0]);
         TRF(t, 2);
       }
     }
   } else if (warp >= 4) {  // ---------------------------------------------------------- softmax
     // 8 warps: TMEM lane quarter qq = warp % 4 (query rows 32 qq ..), column half hf: keys
-    // [64 hf, 64 hf + 64) of S and head dims [hd/2 hf, hd/2 hf + hd/2) of O. The two warps of a
-    // quarter exchange their row maxima through shared memory once per tile (named barrier
-    // 1 + qq, 64 threads); their row sums stay separate until the end.
+    // [64 hf, 64 hf + 64) of S and P, head dims [hd/2 hf, hd/2 hf + hd/2) of O. The two warps
+    // of a quarter exchange their row maxima through shared memory once per tile (named
+    // barrier 1 + qq, 64 threads); they take the same rescale decisions from the same maxima.
     const int qq = warp & 3, hf = (warp - 4) >> 2, r = qq * 32 + lane, q = q0 + r;
     const uint32_t lanes = static_cast<uint32_t>(qq * 32) << 16;
+    const uint32_t o_cols = tmem + lanes + kTO + hf * (kHD / 2);
     float* xmax = reinterpret_cast<float*>(smem + FLay::XMAX);  // [2 parity][2 halves][128 rows]
-    float acc[kHD / 2];
-    float m, m_prev, l;
-    // O_t (TMEM, this warp's 32 head dims) into the registers: acc = acc * 2^(m_old - m_new) + O_t
-    auto take_o = [&](int t, float m_old, float m_new) {
-      const int sb = t & 1;
-      mbar_wait_sleep(&ofull[sb], (t >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const float c = ex2(m_old - m_new);
-      const uint64_t c2 = f2_pack(c, c);
-#pragma unroll
-      for (int ch = 0; ch < kHD / 64; ++ch) {  // 32-column chunks (registers at hd 128)
-        uint32_t o[32];
-        tmem_ld32_async(tmem + lanes + (sb ? kTO1 : kTO0) + hf * (kHD / 2) + ch * 32, o);
-        tmem_wait_ld();
-        if (ch == kHD / 64 - 1) {
-          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-          mbar_arrive(&ofree[sb]);
-        }
-#pragma unroll
-        for (int i = 0; i < 32; i += 2)  // packed fp32x2 FMAs
-          f2_unpack(f2_fma(f2_pack(acc[ch * 32 + i], acc[ch * 32 + i + 1]), c2,
-                           f2_pack(__uint_as_float(o[i]), __uint_as_float(o[i + 1]))),
-                    acc[ch * 32 + i], acc[ch * 32 + i + 1]);
-      }
-    };
-    for (int hh = 0, t = 0; hh < grp; ++hh) {
+    int t = 0;
+    for (int hh = 0; hh < grp; ++hh) {
       const int h = kvh * grp0 + h_lo + hh;
-#pragma unroll
-      for (int i = 0; i < kHD / 2; ++i) acc[i] = 0.f;
-      m = -FLT_MAX, m_prev = -FLT_MAX, l = 0.f;
+      float m = -FLT_MAX, l = 0.f;  // the max the exponentials use (log2 domain), this half's sum
       for (int j = 0; j < nkt; ++j, ++t) {
         const int sb = t & 1;
         if (warp == 4) TRF(t, 4);
@@ -281,7 +282,9 @@ __global__ void __launch_bounds__(384, 1)
         if (warp == 4) TRF(t, 6);
         asm volatile("bar.sync %0, 64;" ::"r"(1 + qq) : "memory");
         if (warp == 4) TRF(t, 7);
-        const float m_new = fmaxf(m, fmaxf(tm[0], xm[(hf ^ 1) * 128 + r]) * scale_log2);
+        const float m_true = fmaxf(m, fmaxf(tm[0], xm[(hf ^ 1) * 128 + r]) * scale_log2);
+        const bool move = m_true > m + kRescale;  // first tile: m = -FLT_MAX
+        const float m_new = move ? m_true : m;
         uint64_t rs2[2] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
         uint32_t pk[32];
         const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nm2 = f2_pack(-m_new, -m_new);
@@ -300,26 +303,44 @@ __global__ void __launch_bounds__(384, 1)
         float r0, r1, r2, r3;
         f2_unpack(rs2[0], r0, r1);
         f2_unpack(rs2[1], r2, r3);
-        l = l * ex2(m - m_new) + ((r0 + r1) + (r2 + r3));  // this half's share of the row sum
-        // P_t overwrites P_{t-1}: the MMA of O_{t-1} must be complete
+        const float corr = move ? ex2(m - m_new) : 1.f;  // 0 on the first tile (l = 0)
+        l = l * corr + ((r0 + r1) + (r2 + r3));  // this half's share of the row sum
+        m = m_new;
+        // PV(t-1) complete: P is free, O is final for tile t-1
         if (warp == 4) TRF(t, 8);
-        if (t > 0) mbar_wait_sleep(&ofull[(t - 1) & 1], ((t - 1) >> 1) & 1);
+        if (t > 0) mbar_wait_sleep(&ofull[0], (t - 1) & 1);
         if (warp == 4) TRF(t, 9);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (j > 0 && __any_sync(0xffffffffu, move)) {  // rescale this half of the rows' O
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch)  // keys [64 hf, 64 hf + 64) = swizzle atom hf of P
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sP + hf * kAtom + r * 128 +
-                                                                         ((ch ^ (r & 7)) << 4)),
-                       "r"(pk[ch * 4]), "r"(pk[ch * 4 + 1]), "r"(pk[ch * 4 + 2]), "r"(pk[ch * 4 + 3])
-                       : "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          for (int ch = 0; ch < kHD / 64; ++ch) {
+            uint32_t o[32];
+            tmem_ld32_async(o_cols + ch * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
+            tmem_st32(o_cols + ch * 32, o);
+          }
+        }
+        tmem_st32(tmem + lanes + kTP + hf * 32, pk);  // keys [64 hf, 64 hf + 64): 32 columns
+        tmem_wait_st();
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         mbar_arrive(pready);
         if (warp == 4) TRF(t, 10);
-        if (j > 0) take_o(t - 1, m_prev, m);
-        if (warp == 4) TRF(t, 11);
-        m_prev = m;
-        m = m_new;
       }
-      take_o(t - 1, m_prev, m);
+      // the head's O: wait for its last PV, read this half's head dims
+      mbar_wait_sleep(&ofull[0], (t - 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float acc[kHD / 2];
+#pragma unroll
+      for (int ch = 0; ch < kHD / 64; ++ch) {
+        uint32_t o[32];
+        tmem_ld32_async(o_cols + ch * 32, o);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[ch * 32 + i] = __uint_as_float(o[i]);
+      }
+      // (the next head's first PV overwrites O only after this thread's next pready arrive)
       // full row sum = both halves' shares (same running max in both)
       float* xl = xmax + 512;
       xl[hf * 128 + r] = l;
