@@ -13,11 +13,12 @@
 // exceeds it by more than kRescale (log2 units); then that row's O (TMEM) and l are scaled
 // by 2^(m_old - m_new) before the next PV. Otherwise P <= 2^kRescale, exact in the
 // normalised result. No per-tile O round trip through registers, and P never touches
-// shared memory. S is double-buffered in TMEM so the MMA of S_{j+1} overlaps the softmax.
-// Tiles of hd 128 are two 64-column swizzle atoms side by side (two TMA boxes); with 32 KB
-// tiles the shared-memory budget allows one Q stage and a 2-deep K/V ring.
-// Warp roles: 0 TMA producer (Q once, K/V kST-stage ring), 1 MMA issuer, 2 TMEM allocator,
-// 4..11 softmax (TMEM lane quarter = warp % 4; two warps per quarter split the columns).
+// shared memory. The MMA of S_{j+1} is issued as soon as the softmax warps hold S_j in
+// registers, so it overlaps the softmax. Tiles of hd 128 are two 64-column swizzle atoms side
+// by side (two TMA boxes).
+// Warp roles: 0 TMA producer (Q once per head, K/V kST-stage ring), 1 TMEM allocator and
+// MMA issuer, 2..9 softmax (TMEM lane quarter = warp % 4; two warps per quarter split the
+// columns).
 #include <cfloat>
 #include <cstdlib>
 #include <string>
@@ -61,19 +62,28 @@ constexpr bool kSplitExp = false;
 constexpr int kSplitEvery = DASHCU_SPLIT_EVERY;  // one pair in kSplitEvery uses ex2_poly for its odd element
 constexpr int kAtom = 128 * 64 * 2;  // 16 KB: 128 rows x one 64-column (128-byte) swizzle atom
 
+// hd 64: two CTAs per SM (~85 KB of shared memory and 256 TMEM columns each: one S buffer,
+// O, P), so one CTA's exponentials run while the other's softmax warps load S, reduce the
+// row max and store P (the exponential loop is MUFU-bound and the rest of a tile is not).
+// hd 128: one CTA per SM with a double-buffered S.
 template <int HD>
 struct FLay {
+  static constexpr int kCTAs = HD == 64 ? 2 : 1;  // CTAs per SM
   static constexpr int kTile = 128 * HD * 2;  // 16 / 32 KB: HD / 64 atoms
-  static constexpr int kQS = HD == 64 ? 2 : 1;  // Q stages
-  static constexpr int kST = HD == 64 ? 4 : 2;  // K/V pipeline depth (loads run kST - 1 key tiles ahead)
+  static constexpr int kQS = 1;               // Q stages
+  static constexpr int kST = 2;               // K/V pipeline depth (loads run kST - 1 key tiles ahead)
+  static constexpr int kNSB = HD == 64 ? 1 : 2;  // S buffers in TMEM
   static constexpr int Q = 0, K = kQS * kTile, V = K + kST * kTile;
   static constexpr int XMAX = V + kST * kTile;  // row-max exchange [2][2][128] + row sums [2][128]
   static constexpr int BAR = XMAX + 4096;
   static constexpr int BYTES = BAR + 256 + 1024;
-  static_assert(BYTES <= 232448, "exceeds the 227 KB of opt-in shared memory per CTA");
-  // TMEM columns: S double buffer, O (HD columns), P (128 bf16 keys = 64 columns)
-  static constexpr uint32_t TS0 = 0, TS1 = 128, TO = 256, TP = 256 + HD;
+  static_assert(BYTES * kCTAs <= 232448, "exceeds the 227 KB of shared memory per SM");
+  // TMEM columns: S buffer(s), O (HD columns), P (128 bf16 keys = 64 columns)
+  static constexpr uint32_t TS1 = 128, TO = 128 * kNSB, TP = TO + HD;
+  static constexpr uint32_t ALLOC = TP + 64 <= 256 ? 256 : 512;
+  static_assert(ALLOC * kCTAs <= 512, "TMEM columns");
 };
+constexpr int kThreads = 320;  // warp 0 TMA, 1 TMEM allocation + MMA, 2..9 softmax
 
 constexpr float kRescale = 8.f;  // lazy-rescale threshold (log2 units): P <= 256
 
@@ -96,6 +106,14 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
       "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 constexpr uint32_t idesc(int n, bool a_mn, bool b_mn) {
@@ -115,13 +133,13 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 }
 
 template <int HD>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(kThreads, FLay<HD>::kCTAs)
     attn_fwd_tc5_k(const __grid_constant__ CUtensorMap mQKV, const int32_t* __restrict__ seq_start, int nh, int nkv,
                    int nqt_max, bf16* __restrict__ ctx, float* __restrict__ lse, float scale_log2,
                    bf16* __restrict__ ctx_lo) {
   using FLay = dashcu::FLay<HD>;
-  constexpr int kHD = HD, kTile = FLay::kTile, kST = FLay::kST, kQS = FLay::kQS;
-  constexpr uint32_t kTS0 = FLay::TS0, kTS1 = FLay::TS1, kTO = FLay::TO, kTP = FLay::TP;
+  constexpr int kHD = HD, kTile = FLay::kTile, kST = FLay::kST, kQS = FLay::kQS, kNSB = FLay::kNSB;
+  constexpr uint32_t kTS1 = FLay::TS1, kTO = FLay::TO, kTP = FLay::TP;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // grid (sequence x KV head, query tile), the longest (last) query tiles launched first; the
@@ -159,16 +177,16 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&qfull[i], 1);
       mbar_init(&qempty[i], 1);
       mbar_init(&sfull[i], 1);
-      mbar_init(&sfree[i], 256);
+      mbar_init(&sfree[i], 256);  // the 8 softmax warps
       mbar_init(&ofull[i], 1);
     }
     mbar_init(pready, 256);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mQKV)) : "memory");
   }
-  if (warp == 2) {
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(512));
+                 "r"(FLay::ALLOC));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -205,8 +223,8 @@ __global__ void __launch_bounds__(384, 1)
     if (lane == 0) {  // ---------------------------------------------------------------- MMA
       constexpr uint32_t I_S = idesc(128, false, false), I_O = idesc(kHD, false, true);
       auto issue_s = [&](int t) {
-        const int sb = t & 1, st = t % kST, hh = t / nkt, j = t % nkt, qs = hh % kQS;
-        if (t >= 2) mbar_wait_sleep(&sfree[sb], ((t >> 1) - 1) & 1);  // softmax holds S_{t-2} in registers
+        const int sb = t % kNSB, st = t % kST, hh = t / nkt, j = t % nkt, qs = hh % kQS;
+        if (t >= kNSB) mbar_wait_sleep(&sfree[sb], ((t / kNSB) - 1) & 1);  // softmax holds S_{t-kNSB} in registers
         if (j == 0) mbar_wait_sleep(&qfull[qs], (hh / kQS) & 1);
         mbar_wait_sleep(&kvfull[st], (t / kST) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -214,7 +232,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int kk = 0; kk < kHD / 16; ++kk) {  // 16-dim K step kk: atom kk / 4, 32-byte chunk kk % 4
           const uint32_t o = (kk >> 2) * kAtom + (kk & 3) * 32;
-          umma_bf16(tmem + (sb ? kTS1 : kTS0), smem_desc(qa + o, 16, 1024), smem_desc(k + o, 16, 1024), I_S, kk > 0);
+          umma_bf16(tmem + (sb ? kTS1 : 0u), smem_desc(qa + o, 16, 1024), smem_desc(k + o, 16, 1024), I_S, kk > 0);
         }
         umma_commit(&sfull[sb]);
         if (j == nkt - 1) umma_commit(&qempty[qs]);  // the head's last S: its Q tile is free
@@ -239,12 +257,12 @@ __global__ void __launch_bounds__(384, 1)
         TRF(t, 2);
       }
     }
-  } else if (warp >= 4) {  // ---------------------------------------------------------- softmax
+  } else if (warp >= 2) {  // ---------------------------------------------------------- softmax
     // 8 warps: TMEM lane quarter qq = warp % 4 (query rows 32 qq ..), column half hf: keys
     // [64 hf, 64 hf + 64) of S and P, head dims [hd/2 hf, hd/2 hf + hd/2) of O. The two warps
     // of a quarter exchange their row maxima through shared memory once per tile (named
     // barrier 1 + qq, 64 threads); they take the same rescale decisions from the same maxima.
-    const int qq = warp & 3, hf = (warp - 4) >> 2, r = qq * 32 + lane, q = q0 + r;
+    const int qq = warp & 3, hf = (warp - 2) >> 2, r = qq * 32 + lane, q = q0 + r;
     const uint32_t lanes = static_cast<uint32_t>(qq * 32) << 16;
     const uint32_t o_cols = tmem + lanes + kTO + hf * (kHD / 2);
     float* xmax = reinterpret_cast<float*>(smem + FLay::XMAX);  // [2 parity][2 halves][128 rows]
@@ -253,25 +271,29 @@ __global__ void __launch_bounds__(384, 1)
       const int h = kvh * grp0 + h_lo + hh;
       float m = -FLT_MAX, l = 0.f;  // the max the exponentials use (log2 domain), this half's sum
       for (int j = 0; j < nkt; ++j, ++t) {
-        const int sb = t & 1;
+        const int sb = t % kNSB;
         if (warp == 4) TRF(t, 4);
-        mbar_wait_sleep(&sfull[sb], (t >> 1) & 1);
+        mbar_wait_sleep(&sfull[sb], (t / kNSB) & 1);
         if (warp == 4) TRF(t, 5);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        uint32_t sr[64];
-        tmem_ld32_async(tmem + lanes + (sb ? kTS1 : kTS0) + hf * 64, sr);
-        tmem_ld32_async(tmem + lanes + (sb ? kTS1 : kTS0) + hf * 64 + 32, sr + 32);
-        tmem_wait_ld();
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        mbar_arrive(&sfree[sb]);
-        float* sv = reinterpret_cast<float*>(sr);  // raw scores; 1/sqrt(d) * log2(e) goes into the exponent
-        if (j == qt) {  // causal diagonal: key j*128 + 64 hf + c > q is masked
-#pragma unroll
-          for (int c = 0; c < 64; ++c) sv[c] = (j * kKeys + hf * 64 + c <= q) ? sv[c] : -FLT_MAX;
-        }
+        // S stays in TMEM until the exponentials are done: read once for the row max, then
+        // again 32 keys at a time for the exponentials (64 live scores instead of 96+)
+        const uint32_t s_cols = tmem + lanes + (sb ? kTS1 : 0u) + hf * 64;
+        const bool diag = j == qt;  // causal diagonal: key j*128 + 64 hf + c > q is masked
         float tm[16];
+        {
+          uint32_t sr[64];
+          tmem_ld32_async(s_cols, sr);
+          tmem_ld32_async(s_cols + 32, sr + 32);
+          tmem_wait_ld();
+          float* sv = reinterpret_cast<float*>(sr);  // raw scores; 1/sqrt(d) * log2(e) goes into the exponent
+          if (diag) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) tm[i] = fmaxf(fmaxf(sv[i], sv[i + 16]), fmaxf(sv[i + 32], sv[i + 48]));
+            for (int c = 0; c < 64; ++c) sv[c] = (j * kKeys + hf * 64 + c <= q) ? sv[c] : -FLT_MAX;
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) tm[i] = fmaxf(fmaxf(sv[i], sv[i + 16]), fmaxf(sv[i + 32], sv[i + 48]));
+        }
 #pragma unroll
         for (int w = 8; w >= 1; w >>= 1)
 #pragma unroll
@@ -285,28 +307,9 @@ __global__ void __launch_bounds__(384, 1)
         const float m_true = fmaxf(m, fmaxf(tm[0], xm[(hf ^ 1) * 128 + r]) * scale_log2);
         const bool move = m_true > m + kRescale;  // first tile: m = -FLT_MAX
         const float m_new = move ? m_true : m;
-        uint64_t rs2[2] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
-        uint32_t pk[32];
-        const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nm2 = f2_pack(-m_new, -m_new);
-#pragma unroll
-        for (int c = 0; c < 64; c += 2) {  // exponent arguments and row sums on the fp32x2 pipe
-          float a0, a1;
-          f2_unpack(f2_fma(f2_pack(sv[c], sv[c + 1]), sc2, nm2), a0, a1);
-          const float p0 = ex2(a0);
-          // a fraction of the exponentials on the FMA pipe (the exp loop is MUFU-bound)
-          const float p1 = (kSplitExp && ((c >> 1) % kSplitEvery == 0)) ? ex2_poly(a1) : ex2(a1);
-          pk[c >> 1] = pack2(p0, p1);
-          // the row sum adds the bf16-rounded values the PV product consumes (O / l consistent)
-          rs2[(c >> 1) & 1] = f2_add(rs2[(c >> 1) & 1], f2_pack(__uint_as_float(pk[c >> 1] << 16),
-                                                                __uint_as_float(pk[c >> 1] & 0xffff0000u)));
-        }
-        float r0, r1, r2, r3;
-        f2_unpack(rs2[0], r0, r1);
-        f2_unpack(rs2[1], r2, r3);
         const float corr = move ? ex2(m - m_new) : 1.f;  // 0 on the first tile (l = 0)
-        l = l * corr + ((r0 + r1) + (r2 + r3));  // this half's share of the row sum
-        m = m_new;
-        // PV(t-1) complete: P is free, O is final for tile t-1
+        // PV(t-1) complete: P is free and O final for tile t-1 (normally long done: PV(t-1)
+        // was issued when tile t-1's P arrived, before this tile's S load and row max)
         if (warp == 4) TRF(t, 8);
         if (t > 0) mbar_wait_sleep(&ofull[0], (t - 1) & 1);
         if (warp == 4) TRF(t, 9);
@@ -322,9 +325,41 @@ __global__ void __launch_bounds__(384, 1)
             tmem_st32(o_cols + ch * 32, o);
           }
         }
-        tmem_st32(tmem + lanes + kTP + hf * 32, pk);  // keys [64 hf, 64 hf + 64): 32 columns
+        uint64_t rs2[2] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
+        const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nm2 = f2_pack(-m_new, -m_new);
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {  // 32 keys at a time: 16 TMEM columns of P per store
+          uint32_t sr[32], pk[16];
+          tmem_ld32_async(s_cols + 32 * h2, sr);
+          tmem_wait_ld();
+          float* sv = reinterpret_cast<float*>(sr) - 32 * h2;  // sv[c] for c in [32 h2, 32 h2 + 32)
+          if (diag) {
+#pragma unroll
+            for (int c = 32 * h2; c < 32 * h2 + 32; ++c) sv[c] = (j * kKeys + hf * 64 + c <= q) ? sv[c] : -FLT_MAX;
+          }
+#pragma unroll
+          for (int c = 32 * h2; c < 32 * h2 + 32; c += 2) {  // exponent arguments and row sums on the fp32x2 pipe
+            float a0, a1;
+            f2_unpack(f2_fma(f2_pack(sv[c], sv[c + 1]), sc2, nm2), a0, a1);
+            const float p0 = ex2(a0);
+            // a fraction of the exponentials on the FMA pipe (the exp loop is MUFU-bound)
+            const float p1 = (kSplitExp && ((c >> 1) % kSplitEvery == 0)) ? ex2_poly(a1) : ex2(a1);
+            const uint32_t pp = pack2(p0, p1);
+            pk[(c >> 1) & 15] = pp;
+            // the row sum adds the bf16-rounded values the PV product consumes (O / l consistent)
+            rs2[(c >> 1) & 1] =
+                f2_add(rs2[(c >> 1) & 1], f2_pack(__uint_as_float(pp << 16), __uint_as_float(pp & 0xffff0000u)));
+          }
+          tmem_st16(tmem + lanes + kTP + hf * 32 + h2 * 16, pk);  // keys [64 hf + 32 h2, +32)
+        }
+        float r0, r1, r2, r3;
+        f2_unpack(rs2[0], r0, r1);
+        f2_unpack(rs2[1], r2, r3);
+        l = l * corr + ((r0 + r1) + (r2 + r3));  // this half's share of the row sum
+        m = m_new;
         tmem_wait_st();
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(&sfree[sb]);  // S read for the last time: the next S may overwrite it
         mbar_arrive(pready);
         if (warp == 4) TRF(t, 10);
       }
@@ -374,7 +409,7 @@ __global__ void __launch_bounds__(384, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(FLay::ALLOC));
 }
 
 }  // namespace
@@ -389,7 +424,7 @@ void launch_fwd_tc5(cudaStream_t s, const CUtensorMap& mq, const int32_t* seq_st
     attr = true;
   }
   dim3 grid(n_seq * nkv, 2 * nqt);
-  attn_fwd_tc5_k<HD><<<grid, 384, FLay<HD>::BYTES, s>>>(mq, seq_start, nh, nkv, nqt, ctx, lse,
+  attn_fwd_tc5_k<HD><<<grid, kThreads, FLay<HD>::BYTES, s>>>(mq, seq_start, nh, nkv, nqt, ctx, lse,
                                                         1.4426950408889634f / sqrtf(static_cast<float>(HD)), ctx_lo);
   DCU_LAUNCHED();
 }
