@@ -21,7 +21,7 @@ for n in sys.argv[1:]:
     tr = np.zeros((3, 512), dtype=np.int64)
     assert L.dashcu_debug_gemm_trace(tr.ctypes.data_as(C.c_void_p)) == 0
     nkb = ((K + 63) // 64 + 3) // 4 if M <= 64 else (K + 63) // 64  # ring stages (4 k-blocks at M <= 64)
-    nkb = min(nkb, 500)
+    nkb = min(nkb, 290)
     t = tr[:, :nkb] - tr[0, 0]
     print(n, f"{ms.value * 1e3:.2f} us/launch; k-block: producer issue / mma wait / data ready (cycles)")
     for k in list(range(0, min(nkb, 12))) + list(range(max(12, nkb - 3), nkb)):
@@ -30,3 +30,9 @@ for n in sys.argv[1:]:
     print("  marks (cycles from kernel entry): setup done %d, pdl_wait done %d, first accumulator %d, "
           "epilogue done %d, stores drained %d; first producer issue %d"
           % (marks[1], marks[2], marks[3], marks[4], marks[5], tr[0, 0] - tr[2, 500]))
+    ep = tr[2, 300:480].reshape(-1, 2) - tr[2, 500]
+    ep = ep[(ep[:, 0] > 0) & (ep[:, 0] < 1e9)]
+    if len(ep):
+        print("  epilogue per tile (start, end, length):", [(int(a), int(b), int(b - a)) for a, b in ep[:12]])
+    kbt = t[1, :nkb]
+    print("  mma wait times every 14 k-blocks:", [int(x) for x in kbt[::14][:12]])
