@@ -96,6 +96,10 @@ size_t colsum_tmp_floats(int M, int N);
 template <class T>
 void colsum_acc(cudaStream_t s, const T* X, int64_t ld, int M, int N, float* out, float* tmp);
 void colsum_acc_f32(cudaStream_t s, const float* X, int64_t ld, int M, int N, float* out, float* tmp);
+// micro-batch packing on the device (policy.cu upload_all): one CTA per listed sequence
+void pack_batch_rows(cudaStream_t s, int nseq, const int32_t* info, const float* wq, const int32_t* ptok,
+                     const int32_t* comp, int max_len, int32_t* tok, int32_t* pos, int32_t* rows, int32_t* tgt,
+                     int32_t* lsei, float* w);
 
 // ---- attention (policy.cpp:105-129 forward, :292-322 backward) -------------------
 // Packed variable-length causal self-attention over qkv rows [T x (qd + 2 kvd)].

@@ -980,6 +980,40 @@ void sample_scan(cudaStream_t s, const float* part, int nslices, const float* lo
   DCU_LAUNCHED();
 }
 
+// Micro-batch packing on the device (forward_for_loss, policy.cpp:350-358): CTA k writes
+// sequence k's packed tokens (prompt, then completion[:-1]) and positions, and its loss
+// rows (packed row of the token predicting completion j, the target id, the sampler-LSE cell
+// s * max_len + j, the row weight). info[8k..]: s, m, len, token offset in the round / in
+// its micro-batch, loss-row offset, prompt offset lo / hi (31 bits each).
+__global__ void pack_batch_rows_k(const int32_t* __restrict__ info, const float* __restrict__ wq,
+                                  const int32_t* __restrict__ ptok, const int32_t* __restrict__ comp, int max_len,
+                                  int32_t* __restrict__ tok, int32_t* __restrict__ pos, int32_t* __restrict__ rows,
+                                  int32_t* __restrict__ tgt, int32_t* __restrict__ lsei, float* __restrict__ w) {
+  const int32_t* f = info + 8 * static_cast<int64_t>(blockIdx.x);
+  const int s = f[0], m = f[1], len = f[2], tg = f[3], tl = f[4], rg = f[5];
+  const int64_t po = static_cast<int64_t>(f[6]) | (static_cast<int64_t>(f[7]) << 31);
+  const int32_t* cs = comp + static_cast<int64_t>(s) * max_len;
+  const int n = m + len - 1;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    tok[tg + t] = t < m ? ptok[po + t] : cs[t - m];
+    pos[tg + t] = t;
+  }
+  const float wk = wq[blockIdx.x];
+  for (int j = threadIdx.x; j < len; j += blockDim.x) {
+    rows[rg + j] = tl + m - 1 + j;
+    tgt[rg + j] = cs[j];
+    lsei[rg + j] = static_cast<int32_t>(static_cast<int64_t>(s) * max_len + j);
+    w[rg + j] = wk;
+  }
+}
+void pack_batch_rows(cudaStream_t s, int nseq, const int32_t* info, const float* wq, const int32_t* ptok,
+                     const int32_t* comp, int max_len, int32_t* tok, int32_t* pos, int32_t* rows, int32_t* tgt,
+                     int32_t* lsei, float* w) {
+  if (nseq <= 0) return;
+  pack_batch_rows_k<<<nseq, 256, 0, s>>>(info, wq, ptok, comp, max_len, tok, pos, rows, tgt, lsei, w);
+  DCU_LAUNCHED();
+}
+
 __global__ void step_advance_k(int* step) {
   pdl_wait();
   *step += 1;

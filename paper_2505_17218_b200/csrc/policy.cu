@@ -298,6 +298,10 @@ struct dashcu_policy {
   std::vector<int64_t> h_prompt_off;
   std::vector<int32_t> h_comp, h_len;
   dashcu::DevMem d_comp, d_len, d_logp;
+  // device copy of h_prompt_tok for the micro-batch packing kernel; d_comp is device-resident
+  // for sampled and loaded rollouts, re-uploaded after a rebalance appended sequences
+  dashcu::DevMem d_prompt_tok;
+  bool prompt_dev_ok = false, comp_dev_ok = true;
   // T = 1 log-sum-exp of every sampled position [n_seq x max_len], written by the fused
   // sampling epilogue (bf16 path); reused by the teacher-forced LM-head backward
   dashcu::DevMem d_lse;
@@ -615,8 +619,8 @@ struct Engine {
       Batch B = pack(ss, {});
       if (B.seqs.empty()) continue;
       DevBatch D = upload(B);
-      const int Tn = static_cast<int>(B.tok.size());
-      const int R = static_cast<int>(B.rows.size());
+      const int Tn = B.ntok;
+      const int R = B.nrows;
       Acts A = alloc_acts(P.ws, Tn, "a_", true);
       pairs = B.pairs;
       forward(A, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen);
@@ -725,11 +729,16 @@ struct Engine {
   }
 
   // ------------------------------------------------------------ micro-batch
+  // A micro-batch as the host sees it: per-sequence geometry only (O(sequences)); the
+  // packed token / position / loss-row arrays are built on the device (pack_batch_rows).
   struct Batch {
-    std::vector<int32_t> tok, pos, start, rows, tgt, seqs, lsei;  // lsei: row -> d_lse cell
-    std::vector<int32_t> rstart{0};  // loss rows of sequence k: [rstart[k], rstart[k+1])
-    std::vector<double> sw;          // per-sequence weight (PPO: A_n * scale)
-    std::vector<float> w;
+    std::vector<int32_t> start;       // packed token offset of each sequence (+ total)
+    std::vector<int32_t> rstart{0};   // loss rows of sequence k: [rstart[k], rstart[k+1])
+    std::vector<int32_t> seqs;        // rollout sequence ids
+    std::vector<int64_t> po;          // prompt offset in h_prompt_tok
+    std::vector<int32_t> m;           // prompt length
+    std::vector<double> sw;           // per-sequence weight (PPO: A_n * scale)
+    int ntok = 0, nrows = 0;
     int maxlen = 0;
     double pairs = 0;  // sum over sequences of n(n+1)/2 causal (query, key) pairs
   };
@@ -745,29 +754,18 @@ struct Engine {
       const int m = static_cast<int>(P.h_prompt_off[p + 1] - po);
       const int len = P.h_len[s];
       if (len == 0) continue;
-      const int s0 = B.start.back();
-      for (int i = 0; i < m; ++i) {
-        B.tok.push_back(P.h_prompt_tok[po + i]);
-        B.pos.push_back(i);
-      }
-      for (int j = 0; j + 1 < len; ++j) {
-        B.tok.push_back(P.h_comp[static_cast<int64_t>(s) * P.max_len + j]);
-        B.pos.push_back(m + j);
-      }
       const int n = m + len - 1;
-      for (int j = 0; j < len; ++j) {
-        B.rows.push_back(s0 + m - 1 + j);
-        B.tgt.push_back(P.h_comp[static_cast<int64_t>(s) * P.max_len + j]);
-        B.lsei.push_back(static_cast<int32_t>(static_cast<int64_t>(s) * P.max_len + j));
-        B.w.push_back(static_cast<float>(weight.empty() ? 1.0 : weight[k]));
-      }
-      B.start.push_back(s0 + n);
-      B.rstart.push_back(static_cast<int32_t>(B.rows.size()));
+      B.start.push_back(B.start.back() + n);
+      B.nrows += len;
+      B.rstart.push_back(B.nrows);
       B.sw.push_back(weight.empty() ? 1.0 : weight[k]);
       B.seqs.push_back(s);
+      B.po.push_back(po);
+      B.m.push_back(m);
       B.maxlen = std::max(B.maxlen, n);
       B.pairs += 0.5 * n * (n + 1.0);
     }
+    B.ntok = B.start.back();
     return B;
   }
 
@@ -779,46 +777,49 @@ struct Engine {
     double* sw = nullptr;
     double* old_lp = nullptr;
   };
-  DevBatch upload(const Batch& B) {
-    DevBatch d;
-    d.tok = P.ws.get<int32_t>("mb_tok", B.tok.size());
-    d.pos = P.ws.get<int32_t>("mb_pos", B.pos.size());
-    d.start = P.ws.get<int32_t>("mb_start", B.start.size());
-    d.rows = P.ws.get<int32_t>("mb_rows", B.rows.size());
-    d.tgt = P.ws.get<int32_t>("mb_tgt", B.tgt.size());
-    d.w = P.ws.get<float>("mb_w", B.w.size());
-    h2d(st, d.tok, B.tok.data(), B.tok.size());
-    h2d(st, d.pos, B.pos.data(), B.pos.size());
-    h2d(st, d.start, B.start.data(), B.start.size());
-    h2d(st, d.rows, B.rows.data(), B.rows.size());
-    h2d(st, d.tgt, B.tgt.data(), B.tgt.size());
-    h2d(st, d.w, B.w.data(), B.w.size());
-    d.lsei = nullptr;
-    return d;
+  DevBatch upload(const Batch& B) { return upload_all(std::vector<Batch>{B})[0]; }
+
+  // The device inputs of the packing kernel: prompt tokens and completions.
+  void sync_rollout_device() {
+    if (!P.prompt_dev_ok) {
+      P.d_prompt_tok.ensure(sizeof(int32_t) * std::max<size_t>(P.h_prompt_tok.size(), 1));
+      h2d(st, P.d_prompt_tok.as<int32_t>(), P.h_prompt_tok.data(), P.h_prompt_tok.size());
+      P.prompt_dev_ok = true;
+    }
+    if (!P.comp_dev_ok) {
+      P.d_comp.ensure(sizeof(int32_t) * std::max<size_t>(P.h_comp.size(), 1));
+      h2d(st, P.d_comp.as<int32_t>(), P.h_comp.data(), P.h_comp.size());
+      P.comp_dev_ok = true;
+    }
   }
 
-  // All micro-batches of a round packed on the host up front and uploaded with one
-  // copy per array, so the GPU never waits for host packing between micro-batches.
+  // All micro-batches of a round: the host uploads each sequence's geometry (a few words
+  // per sequence) and one kernel writes every micro-batch's packed tokens, positions, loss
+  // rows, targets, LSE cells and row weights from the device-resident prompts and
+  // completions (no per-token host work, no token-sized host-to-device copies).
   std::vector<DevBatch> upload_all(const std::vector<Batch>& bs, const std::vector<double>* old_lp = nullptr) {
-    size_t nt = 0, ns = 0, nr = 0;
-    for (const Batch& b : bs) nt += b.tok.size(), ns += b.start.size(), nr += b.rows.size();
-    std::vector<int32_t> tok, pos, start, rows, tgt, lsei, rstart;
+    sync_rollout_device();
+    size_t nt = 0, ns = 0, nr = 0, nq = 0;
+    for (const Batch& b : bs) nt += b.ntok, ns += b.start.size(), nr += b.nrows, nq += b.seqs.size();
+    // info: per sequence {s, m, len, packed token offset in the round / in its micro-batch,
+    // loss-row offset in the round, prompt offset lo / hi}
+    std::vector<int32_t> start, rstart, info;
     std::vector<double> sw, olp;
-    std::vector<float> w;
-    tok.reserve(nt), pos.reserve(nt), start.reserve(ns), rows.reserve(nr), tgt.reserve(nr), w.reserve(nr);
-    lsei.reserve(nr);
+    std::vector<float> wq;
+    start.reserve(ns), rstart.reserve(ns), info.reserve(8 * nq), sw.reserve(nq), wq.reserve(nq);
+    size_t ot = 0, orr = 0;
     for (const Batch& b : bs) {
-      tok.insert(tok.end(), b.tok.begin(), b.tok.end());
-      pos.insert(pos.end(), b.pos.begin(), b.pos.end());
       start.insert(start.end(), b.start.begin(), b.start.end());
-      rows.insert(rows.end(), b.rows.begin(), b.rows.end());
-      tgt.insert(tgt.end(), b.tgt.begin(), b.tgt.end());
-      w.insert(w.end(), b.w.begin(), b.w.end());
-      lsei.insert(lsei.end(), b.lsei.begin(), b.lsei.end());
       rstart.insert(rstart.end(), b.rstart.begin(), b.rstart.end());
       sw.insert(sw.end(), b.sw.begin(), b.sw.end());
-      if (old_lp)
-        for (int sq : b.seqs) olp.push_back((*old_lp)[sq]);
+      for (size_t k = 0; k < b.seqs.size(); ++k) {
+        info.insert(info.end(), {b.seqs[k], b.m[k], P.h_len[b.seqs[k]], static_cast<int32_t>(ot + b.start[k]),
+                                 b.start[k], static_cast<int32_t>(orr + b.rstart[k]),
+                                 static_cast<int32_t>(b.po[k] & 0x7fffffff), static_cast<int32_t>(b.po[k] >> 31)});
+        wq.push_back(static_cast<float>(b.sw[k]));
+        if (old_lp) olp.push_back((*old_lp)[b.seqs[k]]);
+      }
+      ot += b.ntok, orr += b.nrows;
     }
     int32_t* dtok = P.ws.get<int32_t>("mb_tok", nt);
     int32_t* dpos = P.ws.get<int32_t>("mb_pos", nt);
@@ -827,13 +828,13 @@ struct Engine {
     int32_t* dtgt = P.ws.get<int32_t>("mb_tgt", nr);
     float* dw = P.ws.get<float>("mb_w", nr);
     int32_t* dlsei = P.ws.get<int32_t>("mb_lsei", nr);
-    h2d(st, dlsei, lsei.data(), nr);
-    h2d(st, dtok, tok.data(), nt);
-    h2d(st, dpos, pos.data(), nt);
+    int32_t* dinfo = P.ws.get<int32_t>("mb_info", info.size());
+    float* dwq = P.ws.get<float>("mb_wq", wq.size());
     h2d(st, dstart, start.data(), ns);
-    h2d(st, drows, rows.data(), nr);
-    h2d(st, dtgt, tgt.data(), nr);
-    h2d(st, dw, w.data(), nr);
+    h2d(st, dinfo, info.data(), info.size());
+    h2d(st, dwq, wq.data(), wq.size());
+    pack_batch_rows(st, static_cast<int>(nq), dinfo, dwq, P.d_prompt_tok.as<int32_t>(), P.d_comp.as<int32_t>(),
+                    P.max_len, dtok, dpos, drows, dtgt, dlsei, dw);
     int32_t* drst = P.ws.get<int32_t>("mb_rstart", rstart.size());
     double* dsw = P.ws.get<double>("mb_sw", sw.size());
     double* dolp = old_lp ? P.ws.get<double>("mb_oldlp", olp.size()) : nullptr;
@@ -841,14 +842,15 @@ struct Engine {
     h2d(st, dsw, sw.data(), sw.size());
     if (old_lp) h2d(st, dolp, olp.data(), olp.size());
     std::vector<DevBatch> out;
-    size_t ot = 0, os = 0, orr = 0, oq = 0;
+    size_t os = 0, oq = 0;
+    ot = 0, orr = 0;
     for (const Batch& b : bs) {
       DevBatch d{dtok + ot, dpos + ot, dstart + os, drows + orr, dtgt + orr, dw + orr, dlsei + orr};
       d.rstart = drst + os;  // rstart has one entry per start entry (n_seq + 1 per batch)
       d.sw = dsw + oq;
       d.old_lp = dolp ? dolp + oq : nullptr;
       out.push_back(d);
-      ot += b.tok.size(), os += b.start.size(), orr += b.rows.size(), oq += b.seqs.size();
+      ot += b.ntok, os += b.start.size(), orr += b.nrows, oq += b.seqs.size();
     }
     return out;
   }
@@ -886,18 +888,18 @@ struct Engine {
     for (size_t bi = 0; bi < batches.size(); ++bi) {
       const Batch& B = batches[bi];
       const DevBatch& D = dev[bi];
-      const int Tn = static_cast<int>(B.tok.size());
+      const int Tn = B.ntok;
       Acts A = alloc_acts(P.ws, Tn, "a_", true);
       pairs = B.pairs;
       forward(A, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen);
       float* dy32 = P.ws.get<float>("b_dy32", static_cast<size_t>(Tn) * g.d);
       PpoRows pr{D.rstart, static_cast<int>(B.seqs.size()), D.old_lp, D.sw, clip_eps,
                  dstats ? dstats + 3 * seq_off : nullptr};
-      lm_head(A, static_cast<int>(B.rows.size()), D.rows, D.tgt, D.w, nullptr, true, dy32, reuse_lse ? D.lsei : nullptr,
+      lm_head(A, B.nrows, D.rows, D.tgt, D.w, nullptr, true, dy32, reuse_lse ? D.lsei : nullptr,
               ppo_old ? &pr : nullptr);
       seq_off += B.seqs.size();
       backward(A, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen, dy32);
-      loss_tokens += static_cast<int64_t>(B.rows.size());
+      loss_tokens += static_cast<int64_t>(B.nrows);
     }
     if (dstats) {  // back to the caller's order; empty completions: rho = 1, unclipped
       std::vector<double> packed(3 * std::max<size_t>(seq_off, 1));
@@ -929,16 +931,16 @@ struct Engine {
       Batch B = pack(ss, {});
       if (B.seqs.empty()) continue;
       DevBatch D = upload(B);
-      const int Tn = static_cast<int>(B.tok.size());
+      const int Tn = B.ntok;
       Acts A = alloc_acts(P.ws, Tn, "a_");
       pairs = B.pairs;
       forward(A, D.tok, D.pos, D.start, static_cast<int>(B.seqs.size()), B.maxlen);
-      float* lp = P.ws.get<float>("lp_out", B.rows.size());
-      lm_head(A, static_cast<int>(B.rows.size()), D.rows, D.tgt, nullptr, lp, false, nullptr);
-      if (off + static_cast<int64_t>(B.rows.size()) > n_tokens) throw Error(1, "log_prob: output buffer too small");
-      d2h(st, host_out + off, lp, B.rows.size());
+      float* lp = P.ws.get<float>("lp_out", B.nrows);
+      lm_head(A, B.nrows, D.rows, D.tgt, nullptr, lp, false, nullptr);
+      if (off + static_cast<int64_t>(B.nrows) > n_tokens) throw Error(1, "log_prob: output buffer too small");
+      d2h(st, host_out + off, lp, B.nrows);
       DCU_CHECK(cudaStreamSynchronize(st));
-      off += static_cast<int64_t>(B.rows.size());
+      off += static_cast<int64_t>(B.nrows);
     }
   }
 
@@ -1286,6 +1288,7 @@ void set_prompts(Pol* p, const int32_t* tok, const int64_t* off, int NP) {
   validate_tokens(p->g, tok, off[NP], false);
   p->h_prompt_tok.assign(tok, tok + off[NP]);
   p->h_prompt_off.assign(off, off + NP + 1);
+  p->prompt_dev_ok = false;
 }
 
 }  // namespace dashcu
@@ -1574,6 +1577,7 @@ static int sample_impl(dashcu_policy* p, const dashcu_plan* plan, const int32_t*
   p->st.n_seq = S;
   p->ro_version = p->version;
   p->ro_valid = true;
+  p->comp_dev_ok = true;  // d_comp holds this rollout (sampled on the device or uploaded)
   API_END
 }
 
@@ -1615,6 +1619,7 @@ int dashcu_rollout_load(dashcu_policy* p, const int32_t* prompt_tokens, const in
   DCU_CHECK(cudaStreamSynchronize(p->ctx->stream));
   p->ro_version = p->version;
   p->ro_valid = true;
+  p->comp_dev_ok = true;  // d_comp holds this rollout (sampled on the device or uploaded)
   p->lse_valid = false;  // external trajectories: the backward runs its own LSE pass
   p->adv_valid = false;
   p->snap_valid = false;
@@ -1939,6 +1944,8 @@ int dashcu_rebalance(dashcu_policy* p, int32_t* n_out, int32_t* n_in) {
       p->ext_prompt.push_back(static_cast<int32_t>(p->h_prompt_off.size() - 1));
       const int32_t* pt = reinterpret_cast<const int32_t*>(in.data() + at);
       p->h_prompt_tok.insert(p->h_prompt_tok.end(), pt, pt + m);
+      p->prompt_dev_ok = false;
+      p->comp_dev_ok = false;
       p->h_prompt_off.push_back(p->h_prompt_off.back() + m);
       at += 4 * m;
       p->h_comp.resize(static_cast<size_t>(q + 1) * stride, -1);
