@@ -173,7 +173,9 @@ struct OutMaps {
 // KSUB: k-blocks per ring stage (one full-barrier wait + fence + commit per stage: that
 // sequence costs the MMA issuer ~190 cycles, which is 2.4 x the four MMAs of a k-block
 // at N <= 64, tools/mma_probe.cu; the MMA order over K is the same for every KSUB).
-template <int BN, int STAGES, bool AK, bool BKM, int EPW, int AR = BM, int KSUB = 1>
+// MM: MMA M (128, or 64 for skinny tiles of <= 64 rows: half the A operand read per MMA;
+// the accumulator then sits in TMEM lanes 0-15 of each 32-lane quarter, row 16 q + lane).
+template <int BN, int STAGES, bool AK, bool BKM, int EPW, int AR = BM, int KSUB = 1, int MM = BM>
 struct Cfg {
   static constexpr int A_BYTES = AR * BK * 2;
   static constexpr int BNS = BN;
@@ -189,7 +191,7 @@ struct Cfg {
   // kind::f16 instruction descriptor: D f32, A/B bf16, majors, N>>3, M>>4
   static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((AK ? 0u : 1u) << 15) |
                                     ((BKM ? 0u : 1u) << 16) | (static_cast<uint32_t>(BN >> 3) << 17) |
-                                    (static_cast<uint32_t>(BM >> 4) << 24);
+                                    (static_cast<uint32_t>(MM >> 4) << 24);
 };
 
 // 32 bias values of columns [nb, nb + 32) (0 past N); issued before the TMEM load so
@@ -687,13 +689,15 @@ __device__ long long g_trace[3][512];
 #endif
 
 // MODE: 0 generic store epilogue, 1 fused sampling, 2 LSE partials, 3 dz, 4 chosen-slice recompute
-template <int BN, int STAGES, bool AK, bool BKM, int EPW, int MODE, int AR = BM, int KSUB = 1>
-__global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB>::THREADS, 1)
+template <int BN, int STAGES, bool AK, bool BKM, int EPW, int MODE, int AR = BM, int KSUB = 1, int MM = BM>
+__global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB, MM>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ OutMaps om, GemmShape g, Epi e, SampleArgs sa) {
   static_assert(AR == BM || AK, "partial A boxes are K-major only");
   static_assert(KSUB == 1 || MODE == 0, "multi-k-block stages: generic GEMMs only");
-  using C = Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB>;
+  static_assert(MM == BM || (MODE == 0 && AR <= MM), "M = 64 MMAs: generic GEMMs with <= 64-row A boxes");
+  using C = Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB, MM>;
+  constexpr int TM = MODE == 0 ? MM : BM;  // rows per tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
@@ -706,7 +710,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB>::THREA
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) GEMM_MARK(0);
   const int nkb = (g.K + BK - 1) / BK;
-  const int tiles_m = (g.M + BM - 1) / BM, tiles_n = MODE == 4 ? BM / 8 : (g.N + BN - 1) / BN;
+  const int tiles_m = (g.M + TM - 1) / TM, tiles_n = MODE == 4 ? BM / 8 : (g.N + BN - 1) / BN;
   const int ntile = tiles_m * tiles_n;
   // split-K (EPI_ACCUM only): work item w = (tile w / S, K slice w % S), slices of kps k-blocks
   const int S = MODE == 0 ? e.splits : 1;
@@ -745,7 +749,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB>::THREA
       int st_all = 0;
       for (int w = blockIdx.x; w < nitem; w += gridDim.x) {
         const int t = w / S, sp = w % S;
-        const int m0 = (MODE == 4 ? t / tiles_n : tile_m(g, t, tiles_m, tiles_n)) * BM,
+        const int m0 = (MODE == 4 ? t / tiles_n : tile_m(g, t, tiles_m, tiles_n)) * TM,
                   n0 = MODE == 4 ? t % tiles_n : tile_n(g, t, tiles_m, tiles_n) * BN;
         int slice_row[8];  // MODE 4: W_out row of each 32-row B box
         if constexpr (MODE == 4) {
@@ -844,7 +848,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB>::THREA
     int i = 0;
     for (int w = blockIdx.x; w < nitem; w += gridDim.x, ++i) {
       const int t = w / S, sp = w % S;
-      const int m0 = (MODE == 4 ? t / tiles_n : tile_m(g, t, tiles_m, tiles_n)) * BM,
+      const int m0 = (MODE == 4 ? t / tiles_n : tile_m(g, t, tiles_m, tiles_n)) * TM,
                 n0 = MODE == 4 ? t % tiles_n : tile_n(g, t, tiles_m, tiles_n) * BN;
       const int acc = i & 1;
       const uint32_t aph = (i >> 1) & 1;
@@ -854,8 +858,12 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB>::THREA
       uint32_t* flag = S > 1 ? e.split_flags + t * EPW + ew : nullptr;
       if (flag && sp > 0) split_wait(flag, sp, lane);  // K slices reduce into C in slice order
       const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      const int r0 = m0 + q * 32, row = r0 + lane;
-      if constexpr (MODE == 1)
+      const int r0 = m0 + q * 32;
+      // M = 64: rows 16 q .. 16 q + 15 in lanes 0-15 of the quarter (lanes 16-31 hold none)
+      const int row = MM == 64 ? (lane < 16 ? m0 + q * 16 + lane : g.M) : r0 + lane;
+      if constexpr (MM == 64)
+        epilogue_store(g, e, taddr, row, n0, c_lo, c_hi, vec);
+      else if constexpr (MODE == 1)
         epilogue_sample(g, e, sa, om, taddr, row, r0, n0, c_lo, c_hi, stg, lane);
       else if constexpr (MODE == 2)
         epilogue_lse(g, e, sa, taddr, row, n0, c_lo, c_hi, tile_n(g, t, tiles_m, tiles_n) * NSL + slice);
@@ -941,18 +949,19 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, bool AK, bool BKM, int EPW, int MODE, int AR = BM, int KSUB = 1>
+template <int BN, int STAGES, bool AK, bool BKM, int EPW, int MODE, int AR = BM, int KSUB = 1, int MM = BM>
 void launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& om, const GemmShape& g,
             const Epi& e, const SampleArgs& sa) {
-  using C = Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB>;
+  using C = Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB, MM>;
   static_assert(C::SMEM <= 232448, "shared memory");
-  auto k = gemm_tc_kernel<BN, STAGES, AK, BKM, EPW, MODE, AR, KSUB>;
+  auto k = gemm_tc_kernel<BN, STAGES, AK, BKM, EPW, MODE, AR, KSUB, MM>;
   static bool attr = false;
   if (!attr) {
     DCU_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
-  const int nitem = ((g.M + BM - 1) / BM) * (MODE == 4 ? BM / 8 : (g.N + BN - 1) / BN) * (MODE == 0 ? e.splits : 1);
+  constexpr int TM = MODE == 0 ? MM : BM;
+  const int nitem = ((g.M + TM - 1) / TM) * (MODE == 4 ? BM / 8 : (g.N + BN - 1) / BN) * (MODE == 0 ? e.splits : 1);
   const int cap = num_sms();
   const int grid = nitem < cap ? nitem : cap;  // persistent: all CTAs co-resident
   ProfScope ps(MODE == 1 || MODE == 4 ? PROF_SAMPLE : MODE >= 2 ? PROF_LM_ROWS : PROF_GEMM_TC, s,
@@ -1373,8 +1382,18 @@ bool gemm_tc_skinny(cudaStream_t s, const GemmShape& g, const Epi& e) {
   et.tma = out_maps_for(g, e, &om);
   et.splits = 1;
   const SampleArgs none;
-  // four k-blocks per ring stage (one barrier round trip per 16 MMAs), ~192 KB of ring
-  if (AR == 32) {
+  // four k-blocks per ring stage (one barrier round trip per 16 MMAs), ~192 KB of ring;
+  // KNOB_GEMM_SKINNY_M64: M = 64 MMAs for <= 64 rows (direct-store epilogue)
+  if (AR <= 64 && knob(KNOB_GEMM_SKINNY_M64) == 1) {
+    et.tma = 0;
+    if (AR == 32) {
+      if (BN == 64) launch<64, 4, true, true, 8, 0, 32, 4, 64>(s, ma, mb, om, g, et, none);
+      else launch<32, 6, true, true, 8, 0, 32, 4, 64>(s, ma, mb, om, g, et, none);
+    } else {
+      if (BN == 64) launch<64, 3, true, true, 8, 0, 64, 4, 64>(s, ma, mb, om, g, et, none);
+      else launch<32, 4, true, true, 8, 0, 64, 4, 64>(s, ma, mb, om, g, et, none);
+    }
+  } else if (AR == 32) {
     if (BN == 64) launch<64, 4, true, true, 8, 0, 32, 4>(s, ma, mb, om, g, et, none);  // 4 x 48 KB
     else launch<32, 6, true, true, 8, 0, 32, 4>(s, ma, mb, om, g, et, none);           // 6 x 32 KB
   } else if (AR == 64) {

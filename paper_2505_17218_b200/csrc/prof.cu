@@ -28,7 +28,7 @@ const KnobDef kKnobs[KNOB_NUM] = {
     {"GEMM_PAIR", 0},       {"GEMM_RASTER", -1},    {"NO_SPLITK", 0},  {"NO_TMA_STORE", 0},
     {"GEMM_RESID_DB", 1},   {"GEMM_RESID_DEEP", -1}, {"ATTN_FWD", 0},  {"ATTN_BWD", 0},
     {"ATTN_BWD_CHUNK", 4},  {"LSE_RECOMPUTE", 0},   {"PDL", 1},        {"DECODE_GRAPH", 1},
-    {"DECODE_COMPACT", 1},  {"GEMM_SKINNY_AR", 1},
+    {"DECODE_COMPACT", 1},  {"GEMM_SKINNY_AR", 1},  {"GEMM_SKINNY_M64", 1},
 };
 int knob_index(const char* name) {
   if (!name) return -1;

@@ -188,3 +188,23 @@ def test_skinny_rows_equal_big_batch_rows(ctx, knob, M, NK):
         full = ctx.selftest_gemm(A[:M], True, B, True, M, N, K, C_init=c0[:M] if epi == 4 else None, **kw)
         knob("GEMM_SKINNY_AR", None)
         assert np.array_equal(small.view(np.uint32), full.view(np.uint32)), epi
+
+
+@pytest.mark.parametrize("M", [1, 16, 32, 33, 64])
+@pytest.mark.parametrize("NK", [(896, 4864), (1152, 896), (4864, 896)])
+def test_skinny_m64_mma_rows_equal_big_batch_rows(ctx, knob, M, NK):
+    """The M = 64 MMA form of the skinny path (KNOB_GEMM_SKINNY_M64: accumulator rows in
+    TMEM lanes 0-15 of each quarter) gives the same bits as the same rows in a 4096-row batch."""
+    N, K = NK
+    rng = np.random.default_rng(M * 3 + N + K)
+    A = bf16_bits(rng.standard_normal((4096, K)).astype(np.float32) * 0.1)
+    B = bf16_bits(rng.standard_normal((N, K)).astype(np.float32) * 0.1)
+    bias = rng.standard_normal(N).astype(np.float32)
+    c0 = rng.standard_normal((4096, N)).astype(np.float32)
+    for epi in (1, 4):
+        kw = dict(bias=bias, epi=epi)
+        big = ctx.selftest_gemm(A, True, B, True, 4096, N, K, C_init=c0 if epi == 4 else None, **kw)
+        knob("GEMM_SKINNY_M64", "1")
+        small = ctx.selftest_gemm(A[:M], True, B, True, M, N, K, C_init=c0[:M] if epi == 4 else None, **kw)
+        knob("GEMM_SKINNY_M64", None)
+        assert np.array_equal(small.view(np.uint32), big[:M].view(np.uint32)), (epi, np.abs(small - big[:M]).max())

@@ -29,7 +29,7 @@ REPS=1 timeout 600 $NCU -k regex:attn_fwd_tc5 -s 2 -c 1 -o $O/prof_attn_fwd_$TAG
 timeout 600 $NCU -k regex:attn_decode -s 60 -c 1 -o $O/prof_attn_decode_$TAG python tools/sample_bench.py 4 \
   > $O/ncu_attn_decode_$TAG.log 2>&1
 # the sampling GEMM's DRAM traffic (no logits store) and the chosen-slice recompute, C2 decode
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-  -k regex:"gemm_tc_kernel<256, 4, 1, 1, 8, (1|4)>" -s 4 -c 4 --csv --log-file $O/sample_traffic_$TAG.csv \
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --kernel-name-base demangled \
+  -k regex:"gemm_tc_kernel<\\(int\\)256, \\(int\\)4," -s 4 -c 4 --csv --log-file $O/sample_traffic_$TAG.csv \
   python tools/sample_bench.py 4 > $O/ncu_sample_traffic_$TAG.log 2>&1
 echo done

@@ -13,7 +13,7 @@ import sys
 
 def klass(name):
     n = name.replace("(int)", "").replace("(bool)", "")
-    m = re.search(r"gemm_tc_kernel<(\d+), (\d+), (\w+), (\w+), (\d+), (\d+)>", n)
+    m = re.search(r"gemm_tc_kernel<(\d+), (\d+), (\w+), (\w+), (\d+), (\d+)[,>]", n)
     if m:
         mode = int(m.group(6))
         return {0: "gemm_tc", 1: "sample", 2: "lm_rows", 3: "lm_rows", 4: "sample"}[mode]
@@ -21,7 +21,8 @@ def klass(name):
         return "gemm_tc"
     for key, cls in (("attn_decode", "attn_decode"), ("attn_fwd", "attn_fwd"), ("attn_bwd", "attn_bwd"),
                      ("sample_scan", "sample"), ("embed_", "embed"), ("DeviceRadixSort", "embed"), ("lse_reduce", "lm_rows"), ("optimizer_k", "optimizer"),
-                     ("gemm_simt", "gemm_simt"), ("colsum", "colsum"), ("kv_append", "kv_append")):
+                     ("gemm_simt", "gemm_simt"), ("colsum", "colsum"), ("kv_append", "kv_append"),
+                     ("attn_bwd_dot", "attn_bwd"), ("pack_dqkv", "attn_bwd"), ("pack_batch_rows", "pack")):
         if key in n:
             return cls
     return "other"
