@@ -69,6 +69,7 @@ enum Knob : int {
   KNOB_DECODE_COMPACT,   // 0: finished sequences keep their decode rows until the round ends
   KNOB_GEMM_SKINNY_AR,   // 0: skinny GEMMs (M <= 128) stage full 128-row A boxes
   KNOB_GEMM_SKINNY_M64,  // 0: skinny GEMMs with <= 64 rows issue M = 128 MMAs (default: M = 64)
+  KNOB_SPLITK_MAX,       // largest ordered split-K slice count the tile model may pick
   KNOB_NUM
 };
 extern int g_knob[KNOB_NUM];

@@ -1446,20 +1446,22 @@ bool gemm_tc(cudaStream_t s, const GemmShape& g_in, const Epi& e) {
   double cpair_s = rpair * pscale;
   if (e.kind == EPI_ACCUM && e.c32 && !knob(KNOB_NO_SPLITK)) {
     const int tp = tm2 * ((g.N + pbn - 1) / pbn), nkb_ = (g.K + BK - 1) / BK;
-    for (int S = 2; S <= 8 && nkb_ / S >= 16; ++S) {
+    for (int S = 2; S <= knob(KNOB_SPLITK_MAX) && nkb_ / S >= 16; ++S) {
       const double c = std::ceil(tp * S / std::floor(sms / 2)) / S * (pbn / 256.0) * (1.0 + 0.03 * (S - 1));
       if (c < cpair_s * 0.97) cpair_s = c, splitp = S;
     }
   }
   // Split-K for accumulating GEMMs with few output tiles (weight gradients over a long
   // token axis): S K slices per tile fill the machine; each extra slice costs one more
-  // ordered fp32 reduce of the tile (~3%). Slices keep >= 16 k-blocks.
+  // ordered fp32 reduce of the tile (~3%). Slices keep >= 16 k-blocks. S <= 4
+  // (KNOB_SPLITK_MAX): the slices of a tile run in the same round and reduce one after the
+  // other, so more slices serialise more epilogues (wgrad_qkv 93.6 -> 78.2 us at <= 4)
   int split128 = 1, split256 = 1;
   const int nkb = (g.K + BK - 1) / BK;
   if (e.kind == EPI_ACCUM && e.c32 && !knob(KNOB_NO_SPLITK)) {
     auto best = [&](int tiles, double unit, double* cost) {
       int sb = 1;
-      for (int S = 2; S <= 8 && nkb / S >= 16; ++S) {
+      for (int S = 2; S <= knob(KNOB_SPLITK_MAX) && nkb / S >= 16; ++S) {
         const double c = std::ceil(tiles * S / sms) / S * unit * (1.0 + 0.03 * (S - 1));
         if (c < *cost * 0.97) *cost = c, sb = S;
       }
