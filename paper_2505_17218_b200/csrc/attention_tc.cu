@@ -442,6 +442,30 @@ __global__ void attn_bwd_dot_k(const bf16* __restrict__ dctx, const bf16* __rest
                                const bf16* __restrict__ ctx_lo, int rows, int nh, int hd, float* __restrict__ D) {
   const int64_t n = static_cast<int64_t>(rows) * nh;
   const int lane = threadIdx.x & 31;
+  if (hd % 8 == 0 && hd <= 256 && 32 % (hd / 8) == 0) {
+    // 16-byte loads: hd / 8 lanes per (row, head), 32 / (hd / 8) pairs per warp iteration
+    const int lpp = hd / 8, ppw = 32 / lpp, sub = lane / lpp, li = lane % lpp;
+    for (int64_t w0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * ppw; w0 < n;
+         w0 += ((gridDim.x * (int64_t)blockDim.x) >> 5) * ppw) {
+      const int64_t w = w0 + sub;
+      float s = 0.f;
+      if (w < n) {
+        const int64_t o = w * hd + li * 8;
+        const uint4 ua = *reinterpret_cast<const uint4*>(dctx + o);
+        const uint4 ub = *reinterpret_cast<const uint4*>(ctx + o);
+        const uint4 uc = ctx_lo ? *reinterpret_cast<const uint4*>(ctx_lo + o) : make_uint4(0, 0, 0, 0);
+        const bf16* a = reinterpret_cast<const bf16*>(&ua);
+        const bf16* b = reinterpret_cast<const bf16*>(&ub);
+        const bf16* c = reinterpret_cast<const bf16*>(&uc);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          s += __bfloat162float(a[i]) * (__bfloat162float(b[i]) + __bfloat162float(c[i]));
+      }
+      for (int off = lpp / 2; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (li == 0 && w < n) D[w] = s;
+    }
+    return;
+  }
   for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < n; w += (gridDim.x * (int64_t)blockDim.x) >> 5) {
     const bf16* a = dctx + w * hd;
     const bf16* b = ctx + w * hd;
