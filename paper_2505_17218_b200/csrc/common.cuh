@@ -70,6 +70,7 @@ enum Knob : int {
   KNOB_GEMM_SKINNY_AR,   // 0: skinny GEMMs (M <= 128) stage full 128-row A boxes
   KNOB_GEMM_SKINNY_M64,  // 0: skinny GEMMs with <= 64 rows issue M = 128 MMAs (default: M = 64)
   KNOB_SPLITK_MAX,       // largest ordered split-K slice count the tile model may pick
+  KNOB_COMM_WORLD1,      // 1: dashcu_ctx_init_comm creates a 1-rank NCCL communicator at world 1 (tests)
   KNOB_NUM
 };
 extern int g_knob[KNOB_NUM];

@@ -1373,7 +1373,9 @@ int dashcu_ctx_init_comm(dashcu_ctx* c, int world, int rank, const uint8_t id[12
   if (world < 1 || rank < 0 || rank >= world) throw Error(1, "bad world/rank");
   c->world = world;
   c->rank = rank;
-  if (world == 1) return 0;
+  // world 1 needs no communicator (every collective is the identity); KNOB_COMM_WORLD1
+  // creates a 1-rank NCCL communicator anyway, so one-GPU tests run the NCCL calls
+  if (world == 1 && knob(KNOB_COMM_WORLD1) != 1) return 0;
   NcclApi& n = NcclApi::get();
   if (!n.ok) throw Error(4, "libnccl.so.2 not found");
   ncclUniqueId uid;
@@ -2181,7 +2183,7 @@ int dashcu_allreduce_grads(dashcu_policy* p) {
   check_policy(p);
   dashcu_ctx* c = p->ctx;
   Timer tm(c->stream);
-  if (c->world > 1) {
+  if (c->world > 1 || c->comm) {
     if (!c->comm) throw Error(4, "communicator not initialised (dashcu_ctx_init_comm)");
     NCCL_CHECK(NcclApi::get().AllReduce(p->g32.p, p->g32.p, static_cast<size_t>(p->lay.total), ncclFloat32, ncclSum,
                                         c->comm, c->stream));
@@ -2237,14 +2239,15 @@ int dashcu_sharded_step(dashcu_policy* p, const dashcu_opt* o) {
   shard_span(p->lay.total, c->world, c->rank, &off, &len, &slice);
   ensure_moments(p, slice, 1);
   NcclApi& nc = NcclApi::get();
-  if (c->world > 1) {
+  const bool coll = c->world > 1 || c->comm;  // NCCL (also a forced 1-rank communicator)
+  if (coll) {
     if (!c->comm) throw Error(4, "communicator not initialised (dashcu_ctx_init_comm)");
     if (!nc.ReduceScatter || !nc.AllGather) throw Error(4, "libnccl lacks ncclReduceScatter / ncclAllGather");
   }
   Timer tc(c->stream);
   float* g = p->g32.as<float>();
   float* w = p->w32.as<float>();
-  if (c->world > 1)  // in place: rank r's slice of the sum lands at g + r * slice
+  if (coll)  // in place: rank r's slice of the sum lands at g + r * slice
   {
     NCCL_CHECK(nc.ReduceScatter(g, g + off, static_cast<size_t>(slice), ncclFloat32, ncclSum, c->comm, c->stream));
     nccl_wait(c->comm, c->stream);
@@ -2259,7 +2262,7 @@ int dashcu_sharded_step(dashcu_policy* p, const dashcu_opt* o) {
                      static_cast<float>(o->eps), c1, c2);
   const double up_ms = to.stop_ms();
   Timer tg(c->stream);
-  if (c->world > 1)
+  if (coll)
   {
     NCCL_CHECK(nc.AllGather(w + off, w, static_cast<size_t>(slice), ncclFloat32, c->comm, c->stream));
     nccl_wait(c->comm, c->stream);

@@ -29,7 +29,7 @@ const KnobDef kKnobs[KNOB_NUM] = {
     {"GEMM_RESID_DB", 1},   {"GEMM_RESID_DEEP", -1}, {"ATTN_FWD", 0},  {"ATTN_BWD", 0},
     {"ATTN_BWD_CHUNK", 4},  {"LSE_RECOMPUTE", 0},   {"PDL", 1},        {"DECODE_GRAPH", 1},
     {"DECODE_COMPACT", 1},  {"GEMM_SKINNY_AR", 1},  {"GEMM_SKINNY_M64", 1},
-    {"SPLITK_MAX", 4},
+    {"SPLITK_MAX", 4},      {"COMM_WORLD1", 0},
 };
 int knob_index(const char* name) {
   if (!name) return -1;
