@@ -29,6 +29,9 @@ SHAPES = {
     "s32_w1_tanh": (32, 4864, 896, 1, 1, 1), "s32_w2_res": (32, 896, 4864, 1, 1, 4),
     "s64_qkv": (64, 1152, 896, 1, 1, 0), "s64_w2_res": (64, 896, 4864, 1, 1, 4),
     "s128_w2_res": (128, 896, 4864, 1, 1, 4),
+    # C4 decode (Qwen2.5-3B, 64 prompts x 8 = 512 rows) and C3 decode (1.5B, 2048 rows)
+    "c4_qkv": (512, 2560, 2048, 1, 1, 0), "c4_wo_res": (512, 2048, 2048, 1, 1, 4),
+    "c4_w1_tanh": (512, 11008, 2048, 1, 1, 1), "c4_w2_res": (512, 2048, 11008, 1, 1, 4),
 }
 
 
