@@ -1,4 +1,4 @@
-S="dec_qkv dec_w1_tanh dec_w2_res dec_wo_res fwd_w1_tanh fwd_w2_res fwd_wo_res dgrad_w1_res dgrad_qkv_res s32_wo_res s32_w2_res"
+S="dec_w1_tanh fwd_w1_tanh dec_qkv fwd_qkv dgrad_w1_res wgrad_lm dgrad_lm"
 P='import json,sys
 for l in sys.stdin:
     d=json.loads(l); print(sys.argv[1], d["shape"], round(d["ms"]*1e3,1), round(d["tflops"]))'
