@@ -485,6 +485,55 @@ __device__ __forceinline__ void epilogue_resid_db(const GemmShape& g, const Epi&
   }
 }
 
+#ifndef DASHCU_NO_AUX_DB  // A/B builds: -DDASHCU_NO_AUX_DB keeps the single-buffered dtanh epilogue
+constexpr bool kAuxDb = true;
+#else
+constexpr bool kAuxDb = false;
+#endif
+// dtanh epilogue (EPI_DTANH, bf16 output only) with the next chunk's tanh-activation box
+// prefetched (CTA-pair kernel): the warp's 4 KB buffer holds two 2 KB bf16 boxes used
+// alternately. Chunk k reads aux(k) from buf[k & 1], writes its bf16 result into the same
+// buffer and bulk-stores it; aux(k+1) is already loading into buf[(k+1) & 1] (whose
+// previous store, chunk k-1's, must have been read first).
+__device__ __forceinline__ void epilogue_aux_db(const GemmShape& g, const Epi& e, const OutMaps& om, uint32_t taddr,
+                                                int r0, int n0, int c_lo, int c_hi, uint32_t stg, int lane,
+                                                uint64_t* ebar2, uint32_t* eph2) {
+  float v[32], a[32];
+  const uint32_t buf[2] = {stg, stg + 2048};
+  auto load = [&](int k) {  // tanh activations of chunk k into buf[k & 1]
+    if (lane == 0) {
+      mbar_expect_tx(&ebar2[k & 1], 2048u);
+      tma_load_2d(reinterpret_cast<uint8_t*>(__cvta_shared_to_generic(buf[k & 1])), &om.ax, &ebar2[k & 1],
+                  n0 + c_lo + 32 * k, r0);
+    }
+  };
+  const int nk = min((c_hi - c_lo) / 32, (g.N - n0 - c_lo + 31) / 32);
+  if (nk <= 0) return;
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // previous tile's stores
+  __syncwarp();
+  load(0);
+#pragma unroll 1
+  for (int k = 0; k < nk; ++k) {
+    const int nb = n0 + c_lo + 32 * k;
+    if (k + 1 < nk) {  // buf[(k+1)&1] held chunk k-1's output: read by its store before reuse
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
+      load(k + 1);
+    }
+    tmem_ld32(taddr + c_lo + 32 * k, v);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(v[i], e.alpha);
+    mbar_wait(&ebar2[k & 1], eph2[k & 1]);
+    eph2[k & 1] ^= 1u;
+    unstage_b16(buf[k & 1], lane, a);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= (1.f - a[i] * a[i]);
+    __syncwarp();  // every lane has read its activations before the buffer is overwritten
+    stage_b16(buf[k & 1], lane, v);
+    stage_release(lane, &om.b16, buf[k & 1], nb, r0, false);
+  }
+}
+
 // LM-head sampling epilogue (inverse-CDF contract, rule.cuh): per 32-id slice the
 // epilogue stores the fp32 logits (the scan needs the chosen slice's ids) and one
 // 4-float record {m_s, Z_s, m1_s, Z1_s}: the contract's max / sexp2-sum at 1/T and
@@ -683,7 +732,11 @@ __device__ long long g_trace[3][512];
 // phase marks of CTA 0 (thread-0 / warp-leader clocks) in g_trace[2][500 + ...]
 #define GEMM_MARK(k) \
   if (blockIdx.x == 0) g_trace[2][500 + (k)] = clock64()
+// per-tile epilogue start / end of CTA 0's first epilogue warp: g_trace[2][300 + 2 i + k]
+#define GEMM_TILE(i, k) \
+  if (blockIdx.x == 0 && threadIdx.x == 128 && (i) < 90) g_trace[2][300 + 2 * (i) + (k)] = clock64()
 #else
+#define GEMM_TILE(i, k)
 #define GEMM_MARK(k)
 #define GEMM_TRACE(i, k)
 #endif
@@ -1235,6 +1288,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
       const int acc = i & 1;
       const uint32_t aph = (i >> 1) & 1;
       mbar_wait_sleep(&tfull[acc], aph);
+      GEMM_TILE(i, 0);
       if (threadIdx.x == 128 && i == 0) GEMM_MARK(3);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       uint32_t* flag = S > 1 ? e.split_flags + (t * 2 + static_cast<int>(rank)) * EPW + ew : nullptr;
@@ -1242,6 +1296,8 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
       const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       if (DB && (e.tma & 4))
         epilogue_resid_db(g, e, om, taddr, m0 + q * 32, n0, c_lo, c_hi, stg, lane, &ebar[2 * ew], eph2);
+      else if (kAuxDb && e.kind == EPI_DTANH && e.tma == (2 | 8) && !e.bias)
+        epilogue_aux_db(g, e, om, taddr, m0 + q * 32, n0, c_lo, c_hi, stg, lane, &ebar[2 * ew], eph2);
       else if (e.tma)
         epilogue_store_tma(g, e, om, taddr, m0 + q * 32 + lane, m0 + q * 32, n0, c_lo, c_hi, stg, lane,
                            &ebar[2 * ew], ephase, sp > 0 ? nullptr : e.bias);
@@ -1252,6 +1308,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
                                                                                             : tempty_leader0)
                    : "memory");
       if (flag) split_signal(flag, lane);
+      GEMM_TILE(i, 1);
     }
     if (threadIdx.x == 128) GEMM_MARK(4);
     stage_drain(lane);

@@ -2769,7 +2769,14 @@ int dashcu_selftest_gemm_timed(dashcu_ctx* c, int M, int N, int K, int a_kmajor,
   GemmShape g{M, N, K, dA, a_kmajor ? K : M, a_kmajor != 0, dB, b_kmajor ? K : N, b_kmajor != 0};
   Epi e;
   // epi 1: the W1 shape (bias + tanh, bf16 out)
-  e.kind = epi == EPI_ACCUM ? EPI_ACCUM : epi == EPI_TANH ? EPI_TANH : EPI_STORE;
+  // epi 2: the W2-backward shape (bf16 out = acc * (1 - aux^2), aux = the bf16 tanh activations)
+  e.kind = epi == EPI_ACCUM ? EPI_ACCUM : epi == EPI_TANH ? EPI_TANH : epi == EPI_DTANH ? EPI_DTANH : EPI_STORE;
+  if (epi == EPI_DTANH) {
+    bf16* aux = c->ws.get<bf16>("tt_aux", static_cast<size_t>(M) * N);
+    DCU_CHECK(cudaMemsetAsync(aux, 0, sizeof(bf16) * static_cast<size_t>(M) * N, s));
+    e.aux = aux;
+    e.ld_aux = N;
+  }
   if (epi == EPI_TANH) {
     float* bias = c->ws.get<float>("tt_bias", N);
     DCU_CHECK(cudaMemsetAsync(bias, 0, sizeof(float) * N, s));

@@ -1,4 +1,4 @@
-S="dec_w1_tanh fwd_w1_tanh dec_qkv fwd_qkv dgrad_w1_res wgrad_lm dgrad_lm"
+S="dgrad_w2_dtanh fwd_w1_tanh"
 P='import json,sys
 for l in sys.stdin:
     d=json.loads(l); print(sys.argv[1], d["shape"], round(d["ms"]*1e3,1), round(d["tflops"]))'

@@ -16,6 +16,8 @@ SHAPES = {
     "dgrad_w1": (36864, 896, 4864, 1, 0, 0), "wgrad_w1": (4864, 896, 36864, 0, 0, 3),
     "wgrad_lm": (151936, 896, 16384, 0, 0, 3), "dgrad_lm": (16384, 896, 151936, 1, 0, 0),
     "big_sq": (8192, 8192, 8192, 1, 1, 0), "fwd_qkv": (36864, 1152, 896, 1, 1, 0),
+    # W2 backward into u with the dtanh epilogue (du = (dy W2) * (1 - tanh^2))
+    "dgrad_w2_dtanh": (36864, 4864, 896, 1, 0, 2),
     # residual-stream epilogue (fp32 resid in, fp32 + bf16 out)
     "dec_wo_res": (4096, 896, 896, 1, 1, 4), "dec_w2_res": (4096, 896, 4864, 1, 1, 4),
     "fwd_wo_res": (36864, 896, 896, 1, 1, 4), "dgrad_qkv_res": (36864, 896, 1152, 1, 0, 4),
