@@ -820,26 +820,26 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB, MM>::T
           GEMM_TRACE(0, st_all);
           const int cnt = min(KSUB, kb_hi - kb0);
           mbar_expect_tx(&full[s], cnt * (C::A_BYTES + C::B_LOAD));
-          for (int j = 0; j < cnt; ++j) {
-          const int kb = kb0 + j;
-          uint8_t* sa_ = smem + s * C::STAGE_BYTES + j * C::KB_BYTES;
-          uint8_t* sb_ = sa_ + C::A_BYTES;
-          const int k0 = kb * BK;
-          if (AK) {
-            tma_load_2d(sa_, &mapA, &full[s], k0, m0);
-          } else {
-            tma_load_2d(sa_, &mapA, &full[s], m0, k0);
-            tma_load_2d(sa_ + 64 * BK * 2, &mapA, &full[s], m0 + 64, k0);
-          }
-          if constexpr (MODE == 4) {
+          for (int sub = 0; sub < cnt; ++sub) {
+            const int kb = kb0 + sub;
+            uint8_t* sa_ = smem + s * C::STAGE_BYTES + sub * C::KB_BYTES;
+            uint8_t* sb_ = sa_ + C::A_BYTES;
+            const int k0 = kb * BK;
+            if (AK) {
+              tma_load_2d(sa_, &mapA, &full[s], k0, m0);
+            } else {
+              tma_load_2d(sa_, &mapA, &full[s], m0, k0);
+              tma_load_2d(sa_ + 64 * BK * 2, &mapA, &full[s], m0 + 64, k0);
+            }
+            if constexpr (MODE == 4) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) tma_load_2d(sb_ + j * kSlice * BK * 2, &mapB, &full[s], k0, slice_row[j]);
-          } else if (BKM) {
-            tma_load_2d(sb_, &mapB, &full[s], k0, n0);
-          } else {
+              for (int j = 0; j < 8; ++j) tma_load_2d(sb_ + j * kSlice * BK * 2, &mapB, &full[s], k0, slice_row[j]);
+            } else if (BKM) {
+              tma_load_2d(sb_, &mapB, &full[s], k0, n0);
+            } else {
 #pragma unroll
-            for (int j = 0; j < C::BNS / 64; ++j) tma_load_2d(sb_ + j * 64 * BK * 2, &mapB, &full[s], n0 + 64 * j, k0);
-          }
+              for (int j = 0; j < C::BNS / 64; ++j) tma_load_2d(sb_ + j * 64 * BK * 2, &mapB, &full[s], n0 + 64 * j, k0);
+            }
           }
         }
       }
@@ -863,17 +863,17 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB, MM>::T
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const int cnt = min(KSUB, kb_hi - kb0);
 #pragma unroll 1
-          for (int j = 0; j < cnt; ++j) {
-          const int kb = kb0 + j;
-          const uint32_t sa_ = smem_u32(smem + s * C::STAGE_BYTES + j * C::KB_BYTES);
-          const uint32_t sb_ = sa_ + C::A_BYTES;
+          for (int sub = 0; sub < cnt; ++sub) {
+            const int kb = kb0 + sub;
+            const uint32_t sa_ = smem_u32(smem + s * C::STAGE_BYTES + sub * C::KB_BYTES);
+            const uint32_t sb_ = sa_ + C::A_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // K-major: advance 32 B inside the swizzle row; MN-major: advance 16 k-rows (2 x 1024 B)
-            const uint64_t da = AK ? smem_desc(sa_ + k * 32, 16, 1024) : smem_desc(sa_ + k * 2048, 64 * BK * 2, 1024);
-            const uint64_t db = BKM ? smem_desc(sb_ + k * 32, 16, 1024) : smem_desc(sb_ + k * 2048, 64 * BK * 2, 1024);
-            umma_bf16(d, da, db, C::IDESC, (kb > kb_lo || k > 0) ? 1u : 0u);
-          }
+            for (int k = 0; k < BK / 16; ++k) {
+              // K-major: advance 32 B inside the swizzle row; MN-major: advance 16 k-rows (2 x 1024 B)
+              const uint64_t da = AK ? smem_desc(sa_ + k * 32, 16, 1024) : smem_desc(sa_ + k * 2048, 64 * BK * 2, 1024);
+              const uint64_t db = BKM ? smem_desc(sb_ + k * 32, 16, 1024) : smem_desc(sb_ + k * 2048, 64 * BK * 2, 1024);
+              umma_bf16(d, da, db, C::IDESC, (kb > kb_lo || k > 0) ? 1u : 0u);
+            }
           }
           umma_commit(&empty[s]);
         }
@@ -1209,23 +1209,23 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
           const int cnt = min(KSUB, kb_hi - kb0);
           const uint32_t lb = leader_addr(&full[s]);
           if (leader) mbar_expect_tx(&full[s], 2 * cnt * (C::A_BYTES + C::B_LOAD));
-          for (int j = 0; j < cnt; ++j) {
-          const int kb = kb0 + j;
-          uint8_t* sa_ = smem + s * C::STAGE_BYTES + j * C::KB_BYTES;
-          uint8_t* sb_ = sa_ + C::A_BYTES;
-          const int k0 = kb * BK;
-          if (AK) {
-            tma_load_2d_pair(sa_, &mapA, lb, k0, m0);
-          } else {
-            tma_load_2d_pair(sa_, &mapA, lb, m0, k0);
-            tma_load_2d_pair(sa_ + 64 * BK * 2, &mapA, lb, m0 + 64, k0);
-          }
-          if (BKM) {
-            tma_load_2d_pair(sb_, &mapB, lb, k0, n0);
-          } else {
+          for (int sub = 0; sub < cnt; ++sub) {
+            const int kb = kb0 + sub;
+            uint8_t* sa_ = smem + s * C::STAGE_BYTES + sub * C::KB_BYTES;
+            uint8_t* sb_ = sa_ + C::A_BYTES;
+            const int k0 = kb * BK;
+            if (AK) {
+              tma_load_2d_pair(sa_, &mapA, lb, k0, m0);
+            } else {
+              tma_load_2d_pair(sa_, &mapA, lb, m0, k0);
+              tma_load_2d_pair(sa_ + 64 * BK * 2, &mapA, lb, m0 + 64, k0);
+            }
+            if (BKM) {
+              tma_load_2d_pair(sb_, &mapB, lb, k0, n0);
+            } else {
 #pragma unroll
-            for (int j = 0; j < C::BNS / 64; ++j) tma_load_2d_pair(sb_ + j * 64 * BK * 2, &mapB, lb, n0 + 64 * j, k0);
-          }
+              for (int j = 0; j < C::BNS / 64; ++j) tma_load_2d_pair(sb_ + j * 64 * BK * 2, &mapB, lb, n0 + 64 * j, k0);
+            }
           }
         }
       }
@@ -1249,16 +1249,16 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const int cnt = min(KSUB, kb_hi - kb0);
 #pragma unroll 1
-          for (int j = 0; j < cnt; ++j) {
-          const int kb = kb0 + j;
-          const uint32_t sa_ = smem_u32(smem + s * C::STAGE_BYTES + j * C::KB_BYTES);
-          const uint32_t sb_ = sa_ + C::A_BYTES;
+          for (int sub = 0; sub < cnt; ++sub) {
+            const int kb = kb0 + sub;
+            const uint32_t sa_ = smem_u32(smem + s * C::STAGE_BYTES + sub * C::KB_BYTES);
+            const uint32_t sb_ = sa_ + C::A_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t da = AK ? smem_desc(sa_ + k * 32, 16, 1024) : smem_desc(sa_ + k * 2048, 64 * BK * 2, 1024);
-            const uint64_t db = BKM ? smem_desc(sb_ + k * 32, 16, 1024) : smem_desc(sb_ + k * 2048, 64 * BK * 2, 1024);
-            umma_bf16_pair(d, da, db, C::IDESC, (kb > kb_lo || k > 0) ? 1u : 0u);
-          }
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t da = AK ? smem_desc(sa_ + k * 32, 16, 1024) : smem_desc(sa_ + k * 2048, 64 * BK * 2, 1024);
+              const uint64_t db = BKM ? smem_desc(sb_ + k * 32, 16, 1024) : smem_desc(sb_ + k * 2048, 64 * BK * 2, 1024);
+              umma_bf16_pair(d, da, db, C::IDESC, (kb > kb_lo || k > 0) ? 1u : 0u);
+            }
           }
           umma_commit_pair(&empty[s]);
         }
