@@ -765,7 +765,9 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB, MM>::T
   const int nkb = (g.K + BK - 1) / BK;
   const int tiles_m = (g.M + TM - 1) / TM, tiles_n = MODE == 4 ? BM / 8 : (g.N + BN - 1) / BN;
   const int ntile = tiles_m * tiles_n;
-  // split-K (EPI_ACCUM only): work item w = (tile w / S, K slice w % S), slices of kps k-blocks
+  // split-K (EPI_ACCUM only): work item w = (tile w % ntile, K slice w / ntile), slices of kps
+  // k-blocks. Slice-major: a tile's slices run about a round apart, so each slice's ordered
+  // reduce finds its predecessor done instead of all of them finishing together and queueing
   const int S = MODE == 0 ? e.splits : 1;
   const int kps = (nkb + S - 1) / S;
   const int nitem = ntile * S;
@@ -801,7 +803,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB, MM>::T
     if (lane == 0) {
       int st_all = 0;
       for (int w = blockIdx.x; w < nitem; w += gridDim.x) {
-        const int t = w / S, sp = w % S;
+        const int t = w % ntile, sp = w / ntile;
         const int m0 = (MODE == 4 ? t / tiles_n : tile_m(g, t, tiles_m, tiles_n)) * TM,
                   n0 = MODE == 4 ? t % tiles_n : tile_n(g, t, tiles_m, tiles_n) * BN;
         int slice_row[8];  // MODE 4: W_out row of each 32-row B box
@@ -848,7 +850,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB, MM>::T
     if (lane == 0) {
       int st_all = 0, i = 0;
       for (int w = blockIdx.x; w < nitem; w += gridDim.x, ++i) {
-        const int kb_lo = (w % S) * kps, kb_hi = min(nkb, kb_lo + kps);
+        const int kb_lo = (w / ntile) * kps, kb_hi = min(nkb, kb_lo + kps);
         const int acc = i & 1;
         const uint32_t aph = (i >> 1) & 1;
         mbar_wait_pipe(&tempty[acc], aph ^ 1);
@@ -900,7 +902,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, AK, BKM, EPW, AR, KSUB, MM>::T
     uint32_t ephase = 0;
     int i = 0;
     for (int w = blockIdx.x; w < nitem; w += gridDim.x, ++i) {
-      const int t = w / S, sp = w % S;
+      const int t = w % ntile, sp = w / ntile;
       const int m0 = (MODE == 4 ? t / tiles_n : tile_m(g, t, tiles_m, tiles_n)) * TM,
                 n0 = MODE == 4 ? t % tiles_n : tile_n(g, t, tiles_m, tiles_n) * BN;
       const int acc = i & 1;
@@ -1161,8 +1163,8 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
   const int nkb = (g.K + BK - 1) / BK;
   const int tiles_m = (g.M + 255) / 256, tiles_n = (g.N + BN - 1) / BN;
   const int ntile = tiles_m * tiles_n;
-  // split-K (EPI_ACCUM only), as in the single-CTA kernel: item w = (tile w / S, K slice
-  // w % S); each CTA's epilogue warps reduce their 128-row half in slice order
+  // split-K (EPI_ACCUM only), as in the single-CTA kernel: item w = (tile w % ntile, K slice
+  // w / ntile); each CTA's epilogue warps reduce their 128-row half in slice order
   const int S = e.splits > 1 ? e.splits : 1;
   const int kps = (nkb + S - 1) / S;
   const int nitem = ntile * S;
@@ -1198,7 +1200,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
     if (lane == 0) {
       int kb_all = 0;
       for (int w = pair; w < nitem; w += npairs) {
-        const int t = w / S, kb_lo = (w % S) * kps, kb_hi = min(nkb, kb_lo + kps);
+        const int t = w % ntile, kb_lo = (w / ntile) * kps, kb_hi = min(nkb, kb_lo + kps);
         const int m0 = tile_m(g, t, tiles_m, tiles_n) * 256 + static_cast<int>(rank) * 128;
         const int n0 = tile_n(g, t, tiles_m, tiles_n) * BN + static_cast<int>(rank) * C::BNH;
         for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += KSUB, ++kb_all) {
@@ -1234,7 +1236,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
     if (leader && lane == 0) {
       int kb_all = 0, i = 0;
       for (int w = pair; w < nitem; w += npairs, ++i) {
-        const int kb_lo = (w % S) * kps, kb_hi = min(nkb, kb_lo + kps);
+        const int kb_lo = (w / ntile) * kps, kb_hi = min(nkb, kb_lo + kps);
         const int acc = i & 1;
         const uint32_t aph = (i >> 1) & 1;
         mbar_wait_cluster(&tempty[acc], aph ^ 1);
@@ -1282,7 +1284,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES, AK, BKM, EPW, DB>::THREADS, 1
     uint32_t ephase = 0, eph2[2] = {0, 0};
     int i = 0;
     for (int w = pair; w < nitem; w += npairs, ++i) {
-      const int t = w / S, sp = w % S;
+      const int t = w % ntile, sp = w / ntile;
       const int m0 = tile_m(g, t, tiles_m, tiles_n) * 256 + static_cast<int>(rank) * 128,
                 n0 = tile_n(g, t, tiles_m, tiles_n) * BN;
       const int acc = i & 1;

@@ -1,4 +1,4 @@
-S="dgrad_w2_dtanh fwd_w1_tanh"
+S="wgrad_w1 wgrad_qkv wgrad_wo wgrad_lm"
 P='import json,sys
 for l in sys.stdin:
     d=json.loads(l); print(sys.argv[1], d["shape"], round(d["ms"]*1e3,1), round(d["tflops"]))'
