@@ -239,6 +239,9 @@ __global__ void __launch_bounds__(DecCfg<HD>::NW * 32)
     }
   }
   cp_async_wait<0>();
+  // every key is in: the next kernel (the W_o GEMM) may launch and set up on idle SMs; its
+  // pdl_wait() still waits for this grid's ctx stores
+  pdl_trigger();
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 1);
