@@ -17,16 +17,16 @@ namespace {
 constexpr float kLog2e = 1.4426950408889634f;
 
 #ifndef DASHCU_DEC_ST
-#define DASHCU_DEC_ST 2  // 3 CTAs x 4 warps per SM; measured 3.6 % faster than 3 stages at 384 steps
+#define DASHCU_DEC_ST 2  // measured 3.6 % faster than 3 stages at 384 steps (r1)
 #endif
-#ifndef DASHCU_DEC_NW
-#define DASHCU_DEC_NW 4
-#endif
+// head_dim 64: 64-key chunks, 2 warps per CTA (3 CTAs x 2 warps per SM, the same bytes in
+// flight as 32-key chunks x 4 warps, half the per-warp iterations: C2 decode attention
+// -3.7 %); head_dim 128: 32-key chunks, 2 warps per CTA
 template <int HD>
 struct DecCfg {
-  static constexpr int KC = 32;             // keys per chunk
-  static constexpr int ST = DASHCU_DEC_ST;  // pipeline stages (per warp)
-  static constexpr int NW = HD == 64 ? DASHCU_DEC_NW : 2;  // warps per CTA
+  static constexpr int KC = HD == 64 ? 64 : 32;  // keys per chunk (divides kPage)
+  static constexpr int ST = DASHCU_DEC_ST;       // pipeline stages (per warp)
+  static constexpr int NW = 2;                    // warps per CTA
   static constexpr int UNITS = HD / 8;      // 16-byte units per key row
   static constexpr int CHUNK_BYTES = KC * HD * 2;
   static constexpr int WARP_BYTES = ST * 2 * CHUNK_BYTES;  // K and V
