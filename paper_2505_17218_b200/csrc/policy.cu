@@ -2676,7 +2676,14 @@ int dashcu_selftest_gemm(dashcu_ctx* c, int M, int N, int K, const uint16_t* A, 
   const size_t na = static_cast<size_t>(a_kmajor ? M : K) * lda, nb = static_cast<size_t>(b_kmajor ? N : K) * ldb;
   uint16_t* dA = c->ws.get<uint16_t>("t_A", na);
   uint16_t* dB = c->ws.get<uint16_t>("t_B", nb);
-  float* dC = c->ws.get<float>("t_C", static_cast<size_t>(M) * N);
+  // guard bands around C (16 KB before, 256 rows after, filled with 0xA5 bytes) catch
+  // out-of-bounds epilogue stores of ragged tiles: checked after the GEMM (compute-sanitizer
+  // is not available on the GPU pool)
+  const size_t head = 4096, tail = static_cast<size_t>(256) * N, nc = static_cast<size_t>(M) * N;
+  float* dCg = c->ws.get<float>("t_C", head + nc + tail);
+  float* dC = dCg + head;
+  DCU_CHECK(cudaMemsetAsync(dCg, 0xA5, sizeof(float) * head, s));
+  DCU_CHECK(cudaMemsetAsync(dC + nc, 0xA5, sizeof(float) * tail, s));
   float* dbias = c->ws.get<float>("t_bias", N);
   h2d(s, dA, A, na);
   h2d(s, dB, B, nb);
@@ -2694,8 +2701,16 @@ int dashcu_selftest_gemm(dashcu_ctx* c, int M, int N, int K, const uint16_t* A, 
   e.bias = bias ? dbias : nullptr;
   if (force_simt) gemm_simt<bf16>(s, g, e);
   else gemm(s, 1, g, e);
-  d2h(s, Cout, dC, static_cast<size_t>(M) * N);
+  d2h(s, Cout, dC, nc);
+  std::vector<uint32_t> guard(head + tail);
+  d2h(s, guard.data(), reinterpret_cast<uint32_t*>(dCg), head);
+  d2h(s, guard.data() + head, reinterpret_cast<uint32_t*>(dC + nc), tail);
   DCU_CHECK(cudaStreamSynchronize(s));
+  for (size_t i = 0; i < guard.size(); ++i)
+    if (guard[i] != 0xA5A5A5A5u)
+      throw Error(4, "GEMM wrote outside its output (guard word " + std::to_string(i < head ? -static_cast<int64_t>(head - i)
+                                                                                           : static_cast<int64_t>(i - head)) +
+                         (i < head ? " before C)" : " past the end of C)"));
   API_END
 }
 

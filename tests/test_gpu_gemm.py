@@ -208,3 +208,36 @@ def test_skinny_m64_mma_rows_equal_big_batch_rows(ctx, knob, M, NK):
         small = ctx.selftest_gemm(A[:M], True, B, True, M, N, K, C_init=c0[:M] if epi == 4 else None, **kw)
         knob("GEMM_SKINNY_M64", None)
         assert np.array_equal(small.view(np.uint32), big[:M].view(np.uint32)), (epi, np.abs(small - big[:M]).max())
+
+
+@pytest.mark.parametrize("pair", ["0", "-1", "1", "2", "3"])
+@pytest.mark.parametrize("shape", [(1, 8, 16), (33, 72, 40), (65, 904, 200), (129, 264, 64), (257, 1160, 72),
+                                   (300, 4872, 64), (511, 896, 1096)])
+@pytest.mark.parametrize("epi", [0, 1, 3, 4])
+def test_ragged_tiles_stay_inside_the_output(ctx, knob, pair, shape, epi):
+    """Every kernel family (skinny M = 64 / 128-row, single-CTA 128 / 256 wide, CTA pairs
+    256 / 128 / 224 wide, split-K accumulate) on ragged M / N / K: selftest_gemm surrounds C
+    with 0xA5 guard bands (16 KB before, 256 rows after) and fails if any epilogue store
+    lands outside C (our stand-in for compute-sanitizer memcheck, closed on the GPU pool);
+    the values match the fp64 reference."""
+    knob("GEMM_PAIR", pair)
+    M, N, K = shape
+    rng = np.random.default_rng(M * 31 + N + K + epi)
+    A = bf16_bits(rng.standard_normal((M, K)).astype(np.float32) * 0.1)
+    B = bf16_bits(rng.standard_normal((N, K)).astype(np.float32) * 0.1)
+    bias = rng.standard_normal(N).astype(np.float32)
+    c0 = rng.standard_normal((M, N)).astype(np.float32)
+    ref = bits_to_f32(A).astype(np.float64) @ bits_to_f32(B).astype(np.float64).T
+    if epi == 3:   # accumulate (weight-gradient form, MN-major operands)
+        def pad(x):   # 16-byte row pitch for the TMA maps (the padding columns lie outside M / N)
+            p = (-x.shape[1]) % 8
+            return np.pad(x, ((0, 0), (0, p))) if p else x
+        got = ctx.selftest_gemm(pad(np.ascontiguousarray(A.T)), False, pad(np.ascontiguousarray(B.T)), False, M, N, K,
+                                epi=3, C_init=c0)
+        want, tol = c0 + ref, 1e-4
+    else:
+        got = ctx.selftest_gemm(A, True, B, True, M, N, K, bias=bias if epi else None, epi=epi,
+                                C_init=c0 if epi == 4 else None)
+        want = {0: ref, 1: np.tanh(ref + bias), 4: c0 + ref + bias}[epi]
+        tol = 1e-3 if epi == 1 else 1e-4
+    assert np.abs(got - want).max() < tol
