@@ -19,12 +19,14 @@ constexpr float kLog2e = 1.4426950408889634f;
 #ifndef DASHCU_DEC_ST
 #define DASHCU_DEC_ST 2  // measured 3.6 % faster than 3 stages at 384 steps (r1)
 #endif
-// head_dim 64: 64-key chunks, 2 warps per CTA (3 CTAs x 2 warps per SM, the same bytes in
-// flight as 32-key chunks x 4 warps, half the per-warp iterations: C2 decode attention
-// -3.7 %); head_dim 128: 32-key chunks, 2 warps per CTA
+
+// 32-key chunks, 2 warps per CTA (32 KB of ring at head_dim 64: 12 warps per SM). Same-box
+// A/B at C2 (1024 decode steps, tools/ab_dec.sh): decode attention 4780 ms with 64-key
+// chunks (6 warps per SM), 4637 ms with 32-key chunks, 4875 ms with 16-key chunks; two
+// 64-key warps per item (split walk) or 3 stages lose 22 % (fewer warps per SM).
 template <int HD>
 struct DecCfg {
-  static constexpr int KC = HD == 64 ? 64 : 32;  // keys per chunk (divides kPage)
+  static constexpr int KC = 32;                   // keys per chunk (divides kPage)
   static constexpr int ST = DASHCU_DEC_ST;       // pipeline stages (per warp)
   static constexpr int NW = 2;                    // warps per CTA
   static constexpr int UNITS = HD / 8;      // 16-byte units per key row
