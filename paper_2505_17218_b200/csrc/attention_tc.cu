@@ -23,7 +23,9 @@ constexpr float kLog2e = 1.4426950408889634f;
 // 32-key chunks, 2 warps per CTA (32 KB of ring at head_dim 64: 12 warps per SM). Same-box
 // A/B at C2 (1024 decode steps, tools/ab_dec.sh): decode attention 4780 ms with 64-key
 // chunks (6 warps per SM), 4637 ms with 32-key chunks, 4875 ms with 16-key chunks; two
-// 64-key warps per item (split walk) or 3 stages lose 22 % (fewer warps per SM).
+// 64-key warps per item (split walk) or 3 stages lose 22 % (fewer warps per SM). Head_dim
+// 128 with 16-key chunks (12 instead of 6 warps per SM, 168 registers): C3 decode attention
+// 5357 -> 6092 ms, slower.
 template <int HD>
 struct DecCfg {
   static constexpr int KC = 32;                   // keys per chunk (divides kPage)
