@@ -34,6 +34,9 @@ SHAPES = {
     # C4 decode (Qwen2.5-3B, 64 prompts x 8 = 512 rows) and C3 decode (1.5B, 2048 rows)
     "c4_qkv": (512, 2560, 2048, 1, 1, 0), "c4_wo_res": (512, 2048, 2048, 1, 1, 4),
     "c4_w1_tanh": (512, 11008, 2048, 1, 1, 1), "c4_w2_res": (512, 2048, 11008, 1, 1, 4),
+    "c3_w2_res": (2048, 1536, 8960, 1, 1, 4),
+    # the same long-K decode W2 shapes as fp32 accumulates (split-K candidates)
+    "c4_w2_acc": (512, 2048, 11008, 1, 1, 3), "c3_w2_acc": (2048, 1536, 8960, 1, 1, 3),
 }
 
 
